@@ -1,0 +1,250 @@
+/*
+ * rt_b200.h -- C ABI of the B200-native stereo Whitted ray tracer (arXiv 1702.01530 hot path).
+ *
+ * The paper (§3, lines 54-56, Fig. 2) synthesises a stereo pair by ray tracing
+ * the scene twice, once per eye camera ("parallel level 1": left/right channels;
+ * "parallel level 2": the pixels of one channel on the multiprocessor cores), and
+ * attributes ~40% of its time to CPU<->GPU transfer.  This library
+ * exposes exactly the calls the north star names -- rt_scene_upload, rt_set_stereo_camera,
+ * rt_render_stereo, rt_download -- plus the context, event, shard and peer helpers the
+ * bench and the multi-GPU path need.
+ *
+ * Conventions (every entry point):
+ *   - returns rt_status; RT_OK == 0.  No C++ exception ever crosses this boundary.
+ *   - on failure the thread-local message is available from rt_last_error().
+ *   - device work is ASYNCHRONOUS on the context's stream; calls return after enqueue,
+ *     except rt_scene_upload, which returns once the scene's host arrays were copied
+ *     (host buffers may be freed on return).
+ *   - a context is bound to one device and one stream and is NOT thread-safe; use one
+ *     context per (device, host thread).
+ *   - "device pointer" arguments must be CUDA device allocations on the context's device
+ *     (e.g. torch tensors' data_ptr()); "host pointer" arguments are ordinary host memory
+ *     unless stated "pinned".
+ *   - coordinates are world units; colours are linear radiance; IDs are int32.
+ *
+ * Global primitive ID (tie-break order, SPEC.md:183 generalised; reading 9):
+ *   spheres [0, S), planes [S, S+P), triangles [S+P, S+P+T), each in upload order.
+ */
+#ifndef RT_B200_H
+#define RT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RT_ABI_VERSION 1
+#define RT_MAX_DEPTH 16          /* max_depth limit (stack sizing)                 */
+#define RT_TILE 16               /* shard tile edge in pixels (16x16 tiles)        */
+#define RT_NUM_COUNTERS 12       /* see rt_counter                                  */
+
+typedef enum rt_status {
+    RT_OK = 0,
+    RT_ERR_INVALID_ARG = 1,      /* bad pointer/size/value (SPEC.md:76 ValidationError analogue) */
+    RT_ERR_CUDA = 2,             /* a CUDA runtime call failed (message has cudaGetErrorString)  */
+    RT_ERR_OOM = 3,              /* device or pinned allocation failed                           */
+    RT_ERR_NO_SCENE = 4,         /* render before a successful rt_scene_upload                   */
+    RT_ERR_NO_CAMERA = 5,        /* render before a successful rt_set_stereo_camera              */
+    RT_ERR_SIZE = 6,             /* width*height == 0, too large, pitch too small, depth > 16    */
+    RT_ERR_NOT_READY = 7,        /* rt_query: work still in flight (not an error)                */
+    RT_ERR_PEER = 8              /* CUDA IPC / peer mapping failed                               */
+} rt_status;
+
+typedef struct rt_context rt_context;
+typedef struct rt_event rt_event;
+
+/* Scene primitives, HOST pointers, caller-owned, copied during rt_scene_upload.
+ * Every array may be NULL when its count is 0. */
+typedef struct rt_primitives {
+    const float* spheres;        /* [4*n_spheres]  (cx, cy, cz, r), r > 0                        */
+    const uint32_t* sphere_mat;  /* [n_spheres]    material index                               */
+    uint32_t n_spheres;
+    const float* planes;         /* [4*n_planes]   (nx, ny, nz, k): plane n.x = k, |n| > 0      */
+    const uint32_t* plane_mat;   /* [n_planes]                                                  */
+    uint32_t n_planes;
+    const float* vertices;       /* [3*n_vertices] (x, y, z)                                    */
+    uint32_t n_vertices;
+    const uint32_t* tri_indices; /* [3*n_triangles] vertex indices, CCW seen from outside       */
+    const uint32_t* tri_mat;     /* [n_triangles]                                               */
+    uint32_t n_triangles;
+} rt_primitives;
+
+/* SPEC.md:40-44 Material, extended by the north star with refraction (kt, ior). */
+typedef struct rt_material {
+    float kd[3];                 /* diffuse colour, >= 0                      */
+    float ks[3];                 /* specular colour, >= 0                     */
+    float shininess;             /* Phong exponent, >= 1         */
+    float kr;                    /* mirror reflectivity in [0,1]              */
+    float kt;                    /* transmissivity in [0,1], kr + kt <= 1     */
+    float ior;                   /* index of refraction (> 0), outside = 1    */
+} rt_material;
+
+typedef struct rt_light { float pos[3]; float intensity[3]; } rt_light;   /* SPEC.md:53 PointLight */
+typedef struct rt_env { float ambient[3]; float background[3]; } rt_env;  /* SPEC.md:65 Scene      */
+
+typedef enum rt_format { RT_FORMAT_RGBA8 = 0, RT_FORMAT_RGBA16F = 1 } rt_format;
+
+/* A caller-owned DEVICE framebuffer: row-major, top row first.
+ * RGBA8: byte = floor(255*clamp(c,0,1) + 0.5), A = 255.
+ * RGBA16F: binary16 round-to-nearest-even of clamp(c,0,1), A = 1.0.
+ * pitch_bytes >= width * (4 or 8).  dev_ptr NULL = do not write this eye. */
+typedef struct rt_fb {
+    void* dev_ptr;
+    uint32_t format;             /* rt_format */
+    uint64_t pitch_bytes;
+} rt_fb;
+
+/* Counter slots of rt_outputs.counters (uint64, accumulated, never reset by the library). */
+typedef enum rt_counter {
+    RT_CNT_PRIMARY = 0, RT_CNT_REFLECTION = 1, RT_CNT_REFRACTION = 2, RT_CNT_SHADOW = 3,
+    RT_CNT_NODE_VISITS = 4,      /* BVH2 internal nodes visited (2 box tests each)    */
+    RT_CNT_TRI_TESTS = 5, RT_CNT_SPHERE_TESTS = 6, RT_CNT_PLANE_TESTS = 7,
+    RT_CNT_SHADE_HITS = 8,       /* nearest-hit shading points                        */
+    RT_CNT_LIGHT_EVALS = 9,      /* (hit, light) pairs evaluated                      */
+    RT_CNT_MISSES = 10,          /* tree rays that hit nothing                        */
+    RT_CNT_PIXELS = 11
+} rt_counter;
+
+/* rt_render_params.flags */
+#define RT_RENDER_COUNT 1u       /* run the instrumented kernel variant (fills counters; slower) */
+#define RT_RENDER_BRUTE_FORCE 2u /* debug: test every primitive, no BVH (same FP32 intersectors) */
+
+typedef struct rt_render_params {
+    uint32_t width, height;      /* per eye; 1 <= w,h <= 16384                              */
+    uint32_t max_depth;          /* bounces still allowed, 0 = local shading only  */
+    uint32_t shard_rank;         /* render only this rank's tiles ...                        */
+    uint32_t shard_world;        /* ... of shard_world ranks (1 = every tile), see rt_shard_* */
+    uint32_t flags;              /* RT_RENDER_* */
+} rt_render_params;
+
+/* Optional outputs of rt_render_stereo_ex; every DEVICE pointer may be NULL. */
+typedef struct rt_outputs {
+    rt_fb left, right;           /* row-major framebuffers                                   */
+    int32_t* prim_id;            /* [2*H*W] primary nearest-hit global ID, -1 = miss; eye-major */
+    float* radiance;             /* [2*H*W*4] unclamped linear RGB + 0 pad; eye-major        */
+    void* shard;                 /* packed tile-major shard (rt_shard_bytes) for the gather  */
+    uint32_t shard_format;       /* rt_format of `shard`                                     */
+    unsigned long long* counters;/* [RT_NUM_COUNTERS], accumulated when RT_RENDER_COUNT set  */
+} rt_outputs;
+
+/* ------------------------------------------------------------------ context */
+/* Bind a new context to CUDA `device` and `cuda_stream` (a cudaStream_t; NULL -> the
+ * library creates and owns a non-blocking stream).  *out is library-owned. */
+rt_status rt_create(int device, void* cuda_stream, rt_context** out);
+/* Synchronise and free every library-owned resource of ctx (scene, BVH, events). */
+rt_status rt_destroy(rt_context* ctx);
+/* Block until all work enqueued by ctx (render and copy streams) has completed. */
+rt_status rt_synchronize(rt_context* ctx);
+/* Thread-local message of the last failed call on this thread ("" if none). */
+const char* rt_last_error(void);
+int rt_version(void);
+
+/* ------------------------------------------------------------------ scene */
+/* PAPER.md:64-66,82 (§4: scene of objects + light sources, copied to the GPU) and
+ * SURVEY §8(a) rows a1-a2.  Validates (indices < n_vertices, finite values, r > 0, |n| > 0,
+ * triangle area > 1e-12 * bbox_diag^2, 0 <= kr, kt, kr + kt <= 1,
+ * shininess >= 1, ior > 0, kd, ks, intensities >= 0, material index <
+ * n_mats), copies the arrays to the device as SoA records, and builds the Morton-code
+ * LBVH over spheres + triangles on the device (planes stay outside the BVH).
+ * Replaces any previous scene.  An empty scene (no primitives) is valid.
+ * Errors: RT_ERR_INVALID_ARG (validation; message names the entity), RT_ERR_OOM, RT_ERR_CUDA. */
+rt_status rt_scene_upload(rt_context* ctx, const rt_primitives* prims,
+                          const rt_material* mats, uint32_t n_mats,
+                          const rt_light* lights, uint32_t n_lights, const rt_env* env);
+
+/* PAPER.md:33 (§2: "two projections ... from two cameras, corresponding to eyes of the
+ * observer") with SPEC.md:422-430 derive_eyes: `eye` is the cyclopean midpoint, the eyes
+ * sit at eye -/+ (interocular/2) * r^, r^ = normalize(f^ x up).  vfov is vertical, in
+ * degrees, in (0,180).  interocular >= 0 (0 -> identical eyes).  convergence = distance of
+ * the zero-parallax plane (off-axis window shift sigma = +-s/(2C)); convergence <= 0 or
+ * +inf selects the parallel rig.  The basis is derived in double on the host.
+ * Errors: RT_ERR_INVALID_ARG for eye == look_at, up parallel to the view direction,
+ * vfov outside (0,180), negative interocular, any non-finite input (except C = inf). */
+rt_status rt_set_stereo_camera(rt_context* ctx, const float eye[3], const float look_at[3],
+                               const float up[3], float vfov_deg, float interocular,
+                               float convergence);
+
+/* ------------------------------------------------------------------ render */
+/* PAPER.md:54-56 (§3 Fig. 2): render both channels of the stereo pair.  For every pixel of
+ * each eye: primary ray -> nearest hit over spheres, planes, triangles -> Phong shading with
+ * hard shadow rays per light -> reflection/refraction up to max_depth bounces -> clamp and
+ * pack into out_left / out_right (caller-owned device framebuffers, which must stay alive
+ * until the work completes).  Asynchronous on the context stream.
+ * Errors: RT_ERR_NO_SCENE, RT_ERR_NO_CAMERA, RT_ERR_SIZE, RT_ERR_INVALID_ARG, RT_ERR_CUDA. */
+rt_status rt_render_stereo(rt_context* ctx, uint32_t width, uint32_t height, uint32_t max_depth,
+                           rt_fb out_left, rt_fb out_right);
+
+/* Superset for tests, bench and sharding: optional ID / radiance / shard / counter outputs,
+ * instrumented and brute-force variants, and a tile subset (rank shard_rank of
+ * shard_world, "dividing the picture to N identical parts").  Pixels outside
+ * the shard are not written. */
+rt_status rt_render_stereo_ex(rt_context* ctx, const rt_render_params* params, const rt_outputs* out);
+
+/* ------------------------------------------------------------------ download */
+/* PAPER.md:15,107 (the CPU<->GPU transfer stage).  Asynchronous device->host copy of
+ * `bytes` from DEVICE `dev_src` into PINNED host `host_dst` (rt_host_alloc or
+ * cudaHostRegister'ed), on the context's copy stream, ordered after all work enqueued on
+ * the render stream so far; rendering of later frames overlaps it.  *done (library-owned)
+ * completes when the bytes are on the host; release it with rt_wait.  done may be NULL.
+ * Errors: RT_ERR_INVALID_ARG (NULL, zero size, host_dst not pinned), RT_ERR_CUDA. */
+rt_status rt_download(rt_context* ctx, const void* dev_src, void* host_dst, size_t bytes,
+                      rt_event** done);
+/* Block until ev completes, then free it. */
+rt_status rt_wait(rt_event* ev);
+/* RT_OK if ev has completed (ev stays valid), RT_ERR_NOT_READY otherwise. */
+rt_status rt_query(rt_event* ev);
+/* Page-locked host allocation / release for rt_download targets. */
+rt_status rt_host_alloc(size_t bytes, void** out);
+rt_status rt_host_free(void* ptr);
+/* Async host->device copy on the render stream (camera-independent inputs for e2e runs);
+ * host_src must be pinned. */
+rt_status rt_upload(rt_context* ctx, const void* host_src, void* dev_dst, size_t bytes);
+
+/* ------------------------------------------------------------------ sharding (host logic) */
+/* Tile shard map: the image of each eye is cut into RT_TILE x RT_TILE tiles,
+ * tiles_per_eye = ceil(W/16)*ceil(H/16), global tile g = eye*tiles_per_eye + tile.
+ * world == 1: every tile.  world even: ranks [0, world/2) render the left eye and
+ * [world/2, world) the right eye (world 2 = the paper's level-1 eye split), tile t of that
+ * eye going to rank (t mod world/2) within the group.  world odd: g mod world.
+ * rt_shard_tiles writes rank's global tile ids (ascending) into tile_ids (may be NULL to
+ * query the count) and their number into *n_tiles.  Pure host functions, no context. */
+rt_status rt_shard_tiles(uint32_t width, uint32_t height, uint32_t rank, uint32_t world,
+                         uint32_t* n_tiles, uint32_t* tile_ids);
+/* Bytes of one rank's packed shard, padded to the largest rank (equal gather counts):
+ * max_rank(n_tiles) * 256 * bytes_per_pixel(format). */
+rt_status rt_shard_bytes(uint32_t width, uint32_t height, uint32_t world, uint32_t format,
+                         uint64_t* bytes);
+/* Scatter `world` concatenated shards (rank-major, each rt_shard_bytes long) into two
+ * row-major framebuffers.  _host: HOST buffers (pure host logic);
+ * rt_unpack_shards: DEVICE buffers, asynchronous on the context stream. */
+rt_status rt_unpack_shards_host(const void* gathered, uint32_t width, uint32_t height, uint32_t world,
+                                uint32_t format, void* left, void* right, uint64_t pitch_bytes);
+rt_status rt_unpack_shards(rt_context* ctx, const void* gathered, uint32_t width, uint32_t height,
+                           uint32_t world, uint32_t format, rt_fb left, rt_fb right);
+
+/* ------------------------------------------------------------------ peer memory (fused gather) */
+/* CUDA IPC: export a DEVICE allocation of this process as a 64-byte handle, open a peer's
+ * handle to get a device pointer that kernels of this context may store to (NVLink P2P,
+ * or the same device), and close it.  Used by the fused render->gather path in which each
+ * rank's pack epilogue writes its tiles straight into rank 0's framebuffers. */
+rt_status rt_ipc_get_handle(const void* dev_ptr, void* handle64);
+rt_status rt_ipc_open(rt_context* ctx, const void* handle64, void** dev_ptr);
+rt_status rt_ipc_close(rt_context* ctx, void* dev_ptr);
+
+/* ------------------------------------------------------------------ introspection */
+/* Scene statistics after upload: [0] n_spheres [1] n_planes [2] n_triangles [3] bvh prims
+ * [4] bvh internal nodes [5] bvh max depth [6] device bytes of scene+BVH [7] build time us. */
+rt_status rt_scene_info(rt_context* ctx, uint64_t info[8]);
+/* Copy the device BVH (nodes: 16 floats each) and the leaf-order primitive global IDs to
+ * HOST arrays for structural tests; pass NULL to query sizes via *n_nodes / *n_prims. */
+rt_status rt_bvh_export(rt_context* ctx, float* nodes, uint32_t* n_nodes, int32_t* prim_gid, uint32_t* n_prims);
+/* FFMA throughput microbenchmark (roofline denominator): runs `iters` FMA chains on every
+ * SM and returns achieved FP32 TFLOP/s and the kernel time in ms. */
+rt_status rt_bench_ffma(rt_context* ctx, uint32_t iters, double* tflops, double* ms);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RT_B200_H */

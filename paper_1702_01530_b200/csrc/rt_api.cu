@@ -1,0 +1,799 @@
+// rt_api.cu -- host runtime behind the C ABI of include/rt_b200.h.
+//
+// Owns the per-context CUDA streams (render + copy), the device scene (SoA records + LBVH),
+// the camera block, the work counter of the persistent kernel, and the events of the pinned
+// download path.  No exception crosses the ABI: every entry point catches and maps to rt_status.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/rt_b200.h"
+#include "rt_internal.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+rt_status fail(rt_status s, const char* fmt, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return s;
+}
+
+#define CUDA_TRY(call)                                                                           \
+    do {                                                                                         \
+        cudaError_t e_ = (call);                                                                 \
+        if (e_ != cudaSuccess) {                                                                 \
+            if (e_ == cudaErrorMemoryAllocation)                                                 \
+                return fail(RT_ERR_OOM, "%s: %s", #call, cudaGetErrorString(e_));                \
+            return fail(RT_ERR_CUDA, "%s: %s", #call, cudaGetErrorString(e_));                   \
+        }                                                                                        \
+    } while (0)
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+};
+
+}  // namespace
+
+struct rt_event {
+    cudaEvent_t ev = nullptr;
+};
+
+struct rt_context {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t order_ev = nullptr;
+    int num_sms = 148;
+    int* work_counter = nullptr;
+    unsigned long long* scratch_counters = nullptr;
+    float* ffma_out = nullptr;
+    // scene
+    bool has_scene = false;
+    std::vector<DevBuf> scene_bufs;
+    rtb::DevScene sc{};
+    uint64_t info[8] = {0};
+    // camera
+    bool has_camera = false;
+    double cam_eye[2][3], cam_f[3], cam_r[3], cam_u[3], cam_th, cam_sigma_unit;
+    float vfov = 0;
+};
+
+namespace {
+
+template <typename T>
+rt_status dalloc(rt_context* c, size_t count, T** out) {
+    *out = nullptr;
+    if (count == 0) return RT_OK;
+    DevBuf b;
+    b.bytes = count * sizeof(T);
+    cudaError_t e = cudaMalloc(&b.p, b.bytes);
+    if (e != cudaSuccess) return fail(RT_ERR_OOM, "cudaMalloc(%zu bytes): %s", b.bytes, cudaGetErrorString(e));
+    c->scene_bufs.push_back(b);
+    *out = static_cast<T*>(b.p);
+    return RT_OK;
+}
+
+void free_scene(rt_context* c) {
+    for (auto& b : c->scene_bufs) b.release();
+    c->scene_bufs.clear();
+    c->has_scene = false;
+    c->sc = rtb::DevScene{};
+}
+
+bool finite3(const float* p) { return std::isfinite(p[0]) && std::isfinite(p[1]) && std::isfinite(p[2]); }
+
+}  // namespace
+
+extern "C" {
+
+int rt_version(void) { return RT_ABI_VERSION; }
+
+const char* rt_last_error(void) { return g_err.c_str(); }
+
+rt_status rt_create(int device, void* cuda_stream, rt_context** out) {
+    if (!out) return fail(RT_ERR_INVALID_ARG, "rt_create: out is NULL");
+    *out = nullptr;
+    int ndev = 0;
+    CUDA_TRY(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return fail(RT_ERR_INVALID_ARG, "rt_create: device %d of %d", device, ndev);
+    rt_context* c = new (std::nothrow) rt_context();
+    if (!c) return fail(RT_ERR_OOM, "rt_create: host allocation");
+    c->device = device;
+    cudaError_t e = cudaSetDevice(device);
+    if (e == cudaSuccess && cuda_stream) {
+        c->stream = static_cast<cudaStream_t>(cuda_stream);
+    } else if (e == cudaSuccess) {
+        e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+        c->own_stream = true;
+    }
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->order_ev, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaMalloc(&c->work_counter, 64 * sizeof(int));
+    if (e == cudaSuccess) e = cudaMalloc(&c->scratch_counters, RT_NUM_COUNTERS * sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMalloc(&c->ffma_out, 64);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+    if (e != cudaSuccess) {
+        rt_destroy(c);
+        return fail(RT_ERR_CUDA, "rt_create: %s", cudaGetErrorString(e));
+    }
+    *out = c;
+    return RT_OK;
+}
+
+rt_status rt_destroy(rt_context* c) {
+    if (!c) return RT_OK;
+    cudaSetDevice(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
+    free_scene(c);
+    if (c->work_counter) cudaFree(c->work_counter);
+    if (c->scratch_counters) cudaFree(c->scratch_counters);
+    if (c->ffma_out) cudaFree(c->ffma_out);
+    if (c->order_ev) cudaEventDestroy(c->order_ev);
+    if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+    if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+    return RT_OK;
+}
+
+rt_status rt_synchronize(rt_context* c) {
+    if (!c) return fail(RT_ERR_INVALID_ARG, "rt_synchronize: NULL context");
+    CUDA_TRY(cudaSetDevice(c->device));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->copy_stream));
+    return RT_OK;
+}
+
+// ------------------------------------------------------------------------------ scene upload
+rt_status rt_scene_upload(rt_context* c, const rt_primitives* P, const rt_material* mats, uint32_t n_mats,
+                          const rt_light* lights, uint32_t n_lights, const rt_env* env) {
+    if (!c || !P || !env) return fail(RT_ERR_INVALID_ARG, "rt_scene_upload: NULL context/primitives/env");
+    if ((n_mats && !mats) || (n_lights && !lights))
+        return fail(RT_ERR_INVALID_ARG, "rt_scene_upload: NULL materials/lights with nonzero count");
+    const uint32_t S = P->n_spheres, PL = P->n_planes, T = P->n_triangles, V = P->n_vertices;
+    if ((S && (!P->spheres || !P->sphere_mat)) || (PL && (!P->planes || !P->plane_mat)) ||
+        (T && (!P->tri_indices || !P->tri_mat || !P->vertices)))
+        return fail(RT_ERR_INVALID_ARG, "rt_scene_upload: NULL primitive array with nonzero count");
+    if ((uint64_t)S + T >= (1ull << rtb::LEAF_SHIFT) || (uint64_t)S + PL + T >= (1ull << 31))
+        return fail(RT_ERR_INVALID_ARG, "rt_scene_upload: too many primitives (%u spheres + %u triangles)", S, T);
+    // ---- validation (SPEC.md:76 ValidationError analogue; SPEC.md:111 degenerate faces)
+    for (uint32_t i = 0; i < n_mats; ++i) {
+        const rt_material& m = mats[i];
+        if (!finite3(m.kd) || !finite3(m.ks) || !std::isfinite(m.shininess) || !std::isfinite(m.kr) ||
+            !std::isfinite(m.kt) || !std::isfinite(m.ior))
+            return fail(RT_ERR_INVALID_ARG, "material %u: non-finite value", i);
+        for (int k = 0; k < 3; ++k)
+            if (m.kd[k] < 0 || m.ks[k] < 0) return fail(RT_ERR_INVALID_ARG, "material %u: negative kd/ks", i);
+        if (m.shininess < 1.0f) return fail(RT_ERR_INVALID_ARG, "material %u: shininess < 1", i);
+        if (m.kr < 0 || m.kr > 1 || m.kt < 0 || m.kt > 1 || m.kr + m.kt > 1.0f)
+            return fail(RT_ERR_INVALID_ARG, "material %u: kr/kt outside [0,1] or kr+kt > 1", i);
+        if (!(m.ior > 0)) return fail(RT_ERR_INVALID_ARG, "material %u: ior <= 0", i);
+    }
+    for (uint32_t i = 0; i < n_lights; ++i) {
+        if (!finite3(lights[i].pos) || !finite3(lights[i].intensity))
+            return fail(RT_ERR_INVALID_ARG, "light %u: non-finite value", i);
+        for (int k = 0; k < 3; ++k)
+            if (lights[i].intensity[k] < 0) return fail(RT_ERR_INVALID_ARG, "light %u: negative intensity", i);
+    }
+    if (!finite3(env->ambient) || !finite3(env->background))
+        return fail(RT_ERR_INVALID_ARG, "env: non-finite ambient/background");
+    double bound = 0.0;
+    for (uint32_t i = 0; i < S; ++i) {
+        const float* s = P->spheres + 4 * i;
+        if (!finite3(s) || !std::isfinite(s[3])) return fail(RT_ERR_INVALID_ARG, "sphere %u: non-finite value", i);
+        if (!(s[3] > 0)) return fail(RT_ERR_INVALID_ARG, "sphere %u: radius <= 0", i);
+        if (P->sphere_mat[i] >= n_mats) return fail(RT_ERR_INVALID_ARG, "sphere %u: material %u >= %u", i, P->sphere_mat[i], n_mats);
+        bound = std::max(bound, std::fabs((double)s[0]) + std::fabs((double)s[1]) + std::fabs((double)s[2]) + 3.0 * s[3]);
+    }
+    std::vector<float> planes(4 * (size_t)PL);
+    for (uint32_t i = 0; i < PL; ++i) {
+        const float* p = P->planes + 4 * i;
+        if (!finite3(p) || !std::isfinite(p[3])) return fail(RT_ERR_INVALID_ARG, "plane %u: non-finite value", i);
+        const double n = std::sqrt((double)p[0] * p[0] + (double)p[1] * p[1] + (double)p[2] * p[2]);
+        if (!(n > 0)) return fail(RT_ERR_INVALID_ARG, "plane %u: zero normal", i);
+        if (P->plane_mat[i] >= n_mats) return fail(RT_ERR_INVALID_ARG, "plane %u: material %u >= %u", i, P->plane_mat[i], n_mats);
+        for (int k = 0; k < 4; ++k) planes[4 * i + k] = (float)(p[k] / n);
+    }
+    if (T) {
+        for (uint32_t i = 0; i < V; ++i) {
+            const float* v = P->vertices + 3 * i;
+            if (!finite3(v)) return fail(RT_ERR_INVALID_ARG, "vertex %u: non-finite value", i);
+        }
+        for (uint32_t j = 0; j < T; ++j) {
+            const uint32_t* t = P->tri_indices + 3 * j;
+            if (t[0] >= V || t[1] >= V || t[2] >= V)
+                return fail(RT_ERR_INVALID_ARG, "triangle %u: vertex index >= %u", j, V);
+            if (P->tri_mat[j] >= n_mats) return fail(RT_ERR_INVALID_ARG, "triangle %u: material %u >= %u", j, P->tri_mat[j], n_mats);
+            double lo[3], hi[3], e1[3], e2[3];
+            for (int k = 0; k < 3; ++k) {
+                const double a = P->vertices[3 * t[0] + k], b = P->vertices[3 * t[1] + k], cc = P->vertices[3 * t[2] + k];
+                lo[k] = std::min(a, std::min(b, cc));
+                hi[k] = std::max(a, std::max(b, cc));
+                e1[k] = b - a;
+                e2[k] = cc - a;
+                bound = std::max(bound, 0.0);
+            }
+            const double cx = e1[1] * e2[2] - e1[2] * e2[1], cy = e1[2] * e2[0] - e1[0] * e2[2],
+                         cz = e1[0] * e2[1] - e1[1] * e2[0];
+            const double area = 0.5 * std::sqrt(cx * cx + cy * cy + cz * cz);
+            const double diag2 = (hi[0] - lo[0]) * (hi[0] - lo[0]) + (hi[1] - lo[1]) * (hi[1] - lo[1]) +
+                                 (hi[2] - lo[2]) * (hi[2] - lo[2]);
+            if (!(area > 1e-12 * diag2)) return fail(RT_ERR_INVALID_ARG, "triangle %u: degenerate (area %g)", j, area);
+        }
+        for (uint32_t i = 0; i < V; ++i) {
+            const float* v = P->vertices + 3 * i;
+            bound = std::max(bound, std::fabs((double)v[0]) + std::fabs((double)v[1]) + std::fabs((double)v[2]));
+        }
+    }
+
+    CUDA_TRY(cudaSetDevice(c->device));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    free_scene(c);
+    const auto t0 = std::chrono::steady_clock::now();
+    rt_status st;
+    const int N = (int)(S + T);
+    // ---- device copies of the raw arrays
+    float4* d_spheres = nullptr;
+    float* d_vertices = nullptr;
+    uint32_t *d_tri = nullptr, *d_trimat = nullptr, *d_smat = nullptr;
+    float4* d_planes = nullptr;
+    int* d_pmat = nullptr;
+    float4 *d_mats = nullptr, *d_lights = nullptr;
+    if ((st = dalloc(c, S, &d_spheres)) || (st = dalloc(c, 3 * (size_t)V * (T ? 1 : 0), &d_vertices)) ||
+        (st = dalloc(c, 3 * (size_t)T, &d_tri)) || (st = dalloc(c, T, &d_trimat)) || (st = dalloc(c, S, &d_smat)) ||
+        (st = dalloc(c, PL, &d_planes)) || (st = dalloc(c, PL, &d_pmat)) || (st = dalloc(c, 3 * (size_t)n_mats, &d_mats)) ||
+        (st = dalloc(c, 2 * (size_t)n_lights, &d_lights))) {
+        free_scene(c);
+        return st;
+    }
+    if (S) {
+        CUDA_TRY(cudaMemcpy(d_spheres, P->spheres, 16 * (size_t)S, cudaMemcpyHostToDevice));
+        CUDA_TRY(cudaMemcpy(d_smat, P->sphere_mat, 4 * (size_t)S, cudaMemcpyHostToDevice));
+    }
+    if (T) {
+        CUDA_TRY(cudaMemcpy(d_vertices, P->vertices, 12 * (size_t)V, cudaMemcpyHostToDevice));
+        CUDA_TRY(cudaMemcpy(d_tri, P->tri_indices, 12 * (size_t)T, cudaMemcpyHostToDevice));
+        CUDA_TRY(cudaMemcpy(d_trimat, P->tri_mat, 4 * (size_t)T, cudaMemcpyHostToDevice));
+    }
+    if (PL) {
+        std::vector<int> pm(PL);
+        for (uint32_t i = 0; i < PL; ++i) pm[i] = (int)P->plane_mat[i];
+        CUDA_TRY(cudaMemcpy(d_planes, planes.data(), 16 * (size_t)PL, cudaMemcpyHostToDevice));
+        CUDA_TRY(cudaMemcpy(d_pmat, pm.data(), 4 * (size_t)PL, cudaMemcpyHostToDevice));
+    }
+    if (n_mats) {
+        std::vector<float4> m(3 * (size_t)n_mats);
+        for (uint32_t i = 0; i < n_mats; ++i) {
+            const rt_material& x = mats[i];
+            m[3 * i] = make_float4(x.kd[0], x.kd[1], x.kd[2], x.shininess);
+            m[3 * i + 1] = make_float4(x.ks[0], x.ks[1], x.ks[2], x.kr);
+            m[3 * i + 2] = make_float4(x.kt, x.ior, 0.f, 0.f);
+        }
+        CUDA_TRY(cudaMemcpy(d_mats, m.data(), m.size() * sizeof(float4), cudaMemcpyHostToDevice));
+    }
+    if (n_lights) {
+        std::vector<float4> l(2 * (size_t)n_lights);
+        for (uint32_t i = 0; i < n_lights; ++i) {
+            l[2 * i] = make_float4(lights[i].pos[0], lights[i].pos[1], lights[i].pos[2], 0.f);
+            l[2 * i + 1] = make_float4(lights[i].intensity[0], lights[i].intensity[1], lights[i].intensity[2], 0.f);
+        }
+        CUDA_TRY(cudaMemcpy(d_lights, l.data(), l.size() * sizeof(float4), cudaMemcpyHostToDevice));
+    }
+    // ---- LBVH build buffers
+    BuildBuffers B{};
+    B.spheres = d_spheres;
+    B.vertices = d_vertices;
+    B.tri_idx = d_tri;
+    B.tri_mat = d_trimat;
+    B.sphere_mat = d_smat;
+    B.n_spheres = (int)S;
+    B.n_planes = (int)PL;
+    B.n_tris = (int)T;
+    std::vector<void*> scratch;
+    auto salloc = [&](size_t bytes, void** p) -> rt_status {
+        *p = nullptr;
+        if (!bytes) return RT_OK;
+        cudaError_t e = cudaMalloc(p, bytes);
+        if (e != cudaSuccess) return fail(RT_ERR_OOM, "BVH scratch cudaMalloc(%zu): %s", bytes, cudaGetErrorString(e));
+        scratch.push_back(*p);
+        return RT_OK;
+    };
+    auto free_scratch = [&]() {
+        for (void* p : scratch) cudaFree(p);
+        scratch.clear();
+    };
+    float4* d_prims = nullptr;
+    float4* d_nodes = nullptr;
+    int* d_maxdepth = nullptr;
+    const size_t Nn = N > 1 ? N - 1 : 0;
+    if ((st = dalloc(c, 3 * (size_t)N, &d_prims)) || (st = dalloc(c, 4 * Nn, &d_nodes)) || (st = dalloc(c, 1, &d_maxdepth))) {
+        free_scene(c);
+        return st;
+    }
+    B.prims = d_prims;
+    B.nodes = d_nodes;
+    B.max_depth = d_maxdepth;
+    if (N > 0) {
+        if ((st = salloc(48 * (size_t)N, (void**)&B.prims_unsorted)) || (st = salloc(16 * (size_t)N, (void**)&B.aabb_lo)) ||
+            (st = salloc(16 * (size_t)N, (void**)&B.aabb_hi)) || (st = salloc(16 * (size_t)N, (void**)&B.centroid)) ||
+            (st = salloc(16 * (size_t)N, (void**)&B.leaf_lo)) || (st = salloc(16 * (size_t)N, (void**)&B.leaf_hi)) ||
+            (st = salloc(64, (void**)&B.bounds)) || (st = salloc(4 * (size_t)N, (void**)&B.keys[0])) ||
+            (st = salloc(4 * (size_t)N, (void**)&B.keys[1])) || (st = salloc(4 * (size_t)N, (void**)&B.vals[0])) ||
+            (st = salloc(4 * (size_t)N, (void**)&B.vals[1])) ||
+            (st = salloc(4 * rtb_sort_hist_entries(N), (void**)&B.hist)) || (st = salloc(4 * Nn, (void**)&B.left)) ||
+            (st = salloc(4 * Nn, (void**)&B.right)) || (st = salloc(4 * Nn, (void**)&B.parent_int)) ||
+            (st = salloc(4 * (size_t)N, (void**)&B.parent_leaf)) || (st = salloc(4 * Nn, (void**)&B.flags)) ||
+            (st = salloc(16 * Nn, (void**)&B.node_lo)) || (st = salloc(16 * Nn, (void**)&B.node_hi))) {
+            free_scratch();
+            free_scene(c);
+            return st;
+        }
+        cudaError_t e = rtb_build_bvh(B, c->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+        free_scratch();
+        if (e != cudaSuccess) {
+            free_scene(c);
+            return fail(RT_ERR_CUDA, "LBVH build: %s", cudaGetErrorString(e));
+        }
+    }
+    int maxd = 0;
+    if (N > 0) CUDA_TRY(cudaMemcpy(&maxd, d_maxdepth, sizeof(int), cudaMemcpyDeviceToHost));
+    const auto t1 = std::chrono::steady_clock::now();
+
+    rtb::DevScene& D = c->sc;
+    D.nodes = d_nodes;
+    D.prims = d_prims;
+    D.planes = d_planes;
+    D.plane_mat = d_pmat;
+    D.mats = d_mats;
+    D.lights = d_lights;
+    D.n_bvh = N;
+    D.root = N >= 2 ? 0 : ~0;
+    D.n_spheres = (int)S;
+    D.n_planes = (int)PL;
+    D.n_lights = (int)n_lights;
+    D.bound = (float)(bound * (1.0 + 1e-6));
+    D.ambient = make_float3(env->ambient[0], env->ambient[1], env->ambient[2]);
+    D.background = make_float3(env->background[0], env->background[1], env->background[2]);
+    size_t bytes = 0;
+    for (auto& b : c->scene_bufs) bytes += b.bytes;
+    c->info[0] = S;
+    c->info[1] = PL;
+    c->info[2] = T;
+    c->info[3] = N;
+    c->info[4] = Nn;
+    c->info[5] = (uint64_t)maxd;
+    c->info[6] = bytes;
+    c->info[7] = (uint64_t)std::chrono::duration_cast<std::chrono::microseconds>(t1 - t0).count();
+    c->has_scene = true;
+    return RT_OK;
+}
+
+// ------------------------------------------------------------------------------ camera
+rt_status rt_set_stereo_camera(rt_context* c, const float eye[3], const float look_at[3], const float up[3],
+                               float vfov_deg, float interocular, float convergence) {
+    if (!c || !eye || !look_at || !up) return fail(RT_ERR_INVALID_ARG, "rt_set_stereo_camera: NULL argument");
+    if (!finite3(eye) || !finite3(look_at) || !finite3(up) || !std::isfinite(vfov_deg) || !std::isfinite(interocular) ||
+        std::isnan(convergence) || convergence == -INFINITY)
+        return fail(RT_ERR_INVALID_ARG, "rt_set_stereo_camera: non-finite input");
+    if (!(vfov_deg > 0.0f && vfov_deg < 180.0f)) return fail(RT_ERR_INVALID_ARG, "vfov %g outside (0,180)", vfov_deg);
+    if (interocular < 0.0f) return fail(RT_ERR_INVALID_ARG, "negative interocular distance");
+    // SPEC.md:425 (derive_eyes), in double
+    double f[3] = {(double)look_at[0] - eye[0], (double)look_at[1] - eye[1], (double)look_at[2] - eye[2]};
+    const double fl = std::sqrt(f[0] * f[0] + f[1] * f[1] + f[2] * f[2]);
+    if (!(fl > 0)) return fail(RT_ERR_INVALID_ARG, "eye == look_at");
+    for (double& x : f) x /= fl;
+    double r[3] = {f[1] * up[2] - f[2] * up[1], f[2] * up[0] - f[0] * up[2], f[0] * up[1] - f[1] * up[0]};
+    const double rl = std::sqrt(r[0] * r[0] + r[1] * r[1] + r[2] * r[2]);
+    if (!(rl > 0)) return fail(RT_ERR_INVALID_ARG, "up is parallel to the view direction");
+    for (double& x : r) x /= rl;
+    const double u[3] = {r[1] * f[2] - r[2] * f[1], r[2] * f[0] - r[0] * f[2], r[0] * f[1] - r[1] * f[0]};
+    const double s = interocular;
+    for (int k = 0; k < 3; ++k) {
+        c->cam_eye[0][k] = eye[k] - 0.5 * s * r[k];
+        c->cam_eye[1][k] = eye[k] + 0.5 * s * r[k];
+        c->cam_f[k] = f[k];
+        c->cam_r[k] = r[k];
+        c->cam_u[k] = u[k];
+    }
+    c->cam_th = std::tan(0.5 * (double)vfov_deg * M_PI / 180.0);
+    c->cam_sigma_unit = (convergence > 0.0f && std::isfinite(convergence)) ? s / (2.0 * convergence) : 0.0;
+    c->has_camera = true;
+    return RT_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+rt_status fill_camera(rt_context* c, uint32_t W, uint32_t H, rtb::DevCamera& cam) {
+    for (int e = 0; e < 2; ++e)
+        cam.eye[e] = make_float3((float)c->cam_eye[e][0], (float)c->cam_eye[e][1], (float)c->cam_eye[e][2]);
+    cam.f = make_float3((float)c->cam_f[0], (float)c->cam_f[1], (float)c->cam_f[2]);
+    cam.r = make_float3((float)c->cam_r[0], (float)c->cam_r[1], (float)c->cam_r[2]);
+    cam.u = make_float3((float)c->cam_u[0], (float)c->cam_u[1], (float)c->cam_u[2]);
+    cam.th = (float)c->cam_th;
+    cam.tha = (float)(c->cam_th * (double)W / (double)H);
+    cam.sigma[0] = (float)(+c->cam_sigma_unit);
+    cam.sigma[1] = (float)(-c->cam_sigma_unit);
+    return RT_OK;
+}
+
+struct ShardGeom {
+    int tiles_x, tiles_y, tiles_per_eye, mode, half;
+};
+
+ShardGeom shard_geom(uint32_t W, uint32_t H, uint32_t world) {
+    ShardGeom g;
+    g.tiles_x = (int)((W + RT_TILE - 1) / RT_TILE);
+    g.tiles_y = (int)((H + RT_TILE - 1) / RT_TILE);
+    g.tiles_per_eye = g.tiles_x * g.tiles_y;
+    g.mode = world == 1 ? 0 : (world % 2 == 0 ? 1 : 2);
+    g.half = world % 2 == 0 ? (int)world / 2 : 1;
+    return g;
+}
+
+uint32_t shard_count(const ShardGeom& g, uint32_t rank, uint32_t world) {
+    if (g.mode == 0) return 2u * g.tiles_per_eye;
+    if (g.mode == 1) {
+        const int j = (int)rank % g.half;
+        return j < g.tiles_per_eye ? (uint32_t)((g.tiles_per_eye - j + g.half - 1) / g.half) : 0u;
+    }
+    const int total = 2 * g.tiles_per_eye;
+    return (int)rank < total ? (uint32_t)((total - (int)rank + (int)world - 1) / (int)world) : 0u;
+}
+
+uint32_t shard_tile(const ShardGeom& g, uint32_t rank, uint32_t world, uint32_t lt) {
+    if (g.mode == 0) return lt;
+    if (g.mode == 1) {
+        const int grp = (int)rank / g.half, j = (int)rank % g.half;
+        return (uint32_t)(grp * g.tiles_per_eye + j + (int)lt * g.half);
+    }
+    return rank + lt * world;
+}
+
+rt_status check_fb(const rt_fb& fb, uint32_t W, const char* name) {
+    if (!fb.dev_ptr) return RT_OK;
+    if (fb.format != RT_FORMAT_RGBA8 && fb.format != RT_FORMAT_RGBA16F)
+        return fail(RT_ERR_INVALID_ARG, "%s: unknown format %u", name, fb.format);
+    const uint64_t need = (uint64_t)W * (fb.format == RT_FORMAT_RGBA8 ? 4 : 8);
+    if (fb.pitch_bytes < need) return fail(RT_ERR_SIZE, "%s: pitch %llu < %llu", name, (unsigned long long)fb.pitch_bytes, (unsigned long long)need);
+    if (fb.pitch_bytes % (fb.format == RT_FORMAT_RGBA8 ? 4 : 8))
+        return fail(RT_ERR_INVALID_ARG, "%s: pitch not a multiple of the pixel size", name);
+    return RT_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+rt_status rt_render_stereo_ex(rt_context* c, const rt_render_params* p, const rt_outputs* out) {
+    if (!c || !p || !out) return fail(RT_ERR_INVALID_ARG, "rt_render_stereo_ex: NULL argument");
+    if (!c->has_scene) return fail(RT_ERR_NO_SCENE, "render before rt_scene_upload");
+    if (!c->has_camera) return fail(RT_ERR_NO_CAMERA, "render before rt_set_stereo_camera");
+    const uint32_t W = p->width, H = p->height;
+    if (W == 0 || H == 0 || W > 16384 || H > 16384) return fail(RT_ERR_SIZE, "image size %ux%u", W, H);
+    if (p->max_depth > RT_MAX_DEPTH) return fail(RT_ERR_SIZE, "max_depth %u > %d", p->max_depth, RT_MAX_DEPTH);
+    if (p->shard_world == 0 || p->shard_rank >= p->shard_world || p->shard_world > 4096)
+        return fail(RT_ERR_INVALID_ARG, "shard %u of %u", p->shard_rank, p->shard_world);
+    if (p->flags & ~(RT_RENDER_COUNT | RT_RENDER_BRUTE_FORCE)) return fail(RT_ERR_INVALID_ARG, "unknown flags 0x%x", p->flags);
+    if ((p->flags & RT_RENDER_COUNT) && !out->counters) return fail(RT_ERR_INVALID_ARG, "RT_RENDER_COUNT needs counters");
+    rt_status st;
+    if ((st = check_fb(out->left, W, "out_left")) || (st = check_fb(out->right, W, "out_right"))) return st;
+    if (out->shard && out->shard_format != RT_FORMAT_RGBA8 && out->shard_format != RT_FORMAT_RGBA16F)
+        return fail(RT_ERR_INVALID_ARG, "shard: unknown format");
+    TraceParams P{};
+    P.sc = c->sc;
+    fill_camera(c, W, H, P.cam);
+    P.W = (int)W;
+    P.H = (int)H;
+    P.max_depth = (int)p->max_depth;
+    P.work_counter = c->work_counter;
+    const ShardGeom g = shard_geom(W, H, p->shard_world);
+    const uint64_t n_tiles = shard_count(g, p->shard_rank, p->shard_world);
+    if (n_tiles * 256ull >= (1ull << 31)) return fail(RT_ERR_SIZE, "too many pixels in one shard");
+    P.n_work = (int)(n_tiles * 256);
+    P.tiles_x = g.tiles_x;
+    P.tiles_per_eye = g.tiles_per_eye;
+    P.shard_mode = g.mode;
+    P.shard_rank = (int)p->shard_rank;
+    P.shard_world = (int)p->shard_world;
+    P.shard_half = g.half;
+    P.fb[0] = out->left.dev_ptr;
+    P.fb[1] = out->right.dev_ptr;
+    P.fb_fmt[0] = (int)out->left.format;
+    P.fb_fmt[1] = (int)out->right.format;
+    P.fb_pitch[0] = (long long)out->left.pitch_bytes;
+    P.fb_pitch[1] = (long long)out->right.pitch_bytes;
+    P.prim_id = out->prim_id;
+    P.radiance = reinterpret_cast<float4*>(out->radiance);
+    P.shard = out->shard;
+    P.shard_fmt = (int)out->shard_format;
+    P.counters = out->counters ? out->counters : c->scratch_counters;
+    if (P.n_work == 0) return RT_OK;
+    CUDA_TRY(cudaSetDevice(c->device));
+    int occ = 0;
+    CUDA_TRY(rtb_trace_occupancy(p->flags, &occ));
+    if (occ < 1) occ = 1;
+    const long long max_blocks = ((long long)P.n_work + 255) / 256;
+    const int grid = (int)std::min<long long>((long long)c->num_sms * occ, std::max<long long>(1, max_blocks));
+    CUDA_TRY(cudaMemsetAsync(c->work_counter, 0, sizeof(int), c->stream));
+    CUDA_TRY(rtb_launch_trace(P, p->flags, grid, c->stream));
+    return RT_OK;
+}
+
+rt_status rt_render_stereo(rt_context* c, uint32_t width, uint32_t height, uint32_t max_depth, rt_fb out_left,
+                           rt_fb out_right) {
+    rt_render_params p{};
+    p.width = width;
+    p.height = height;
+    p.max_depth = max_depth;
+    p.shard_rank = 0;
+    p.shard_world = 1;
+    rt_outputs o{};
+    o.left = out_left;
+    o.right = out_right;
+    return rt_render_stereo_ex(c, &p, &o);
+}
+
+// ------------------------------------------------------------------------------ download
+rt_status rt_host_alloc(size_t bytes, void** out) {
+    if (!out || !bytes) return fail(RT_ERR_INVALID_ARG, "rt_host_alloc: NULL out or zero size");
+    cudaError_t e = cudaHostAlloc(out, bytes, cudaHostAllocPortable);
+    if (e != cudaSuccess) {
+        *out = nullptr;
+        return fail(RT_ERR_OOM, "cudaHostAlloc(%zu): %s", bytes, cudaGetErrorString(e));
+    }
+    return RT_OK;
+}
+
+rt_status rt_host_free(void* p) {
+    if (!p) return RT_OK;
+    CUDA_TRY(cudaFreeHost(p));
+    return RT_OK;
+}
+
+static bool is_pinned(const void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+rt_status rt_download(rt_context* c, const void* dev_src, void* host_dst, size_t bytes, rt_event** done) {
+    if (done) *done = nullptr;
+    if (!c || !dev_src || !host_dst || !bytes) return fail(RT_ERR_INVALID_ARG, "rt_download: NULL pointer or zero size");
+    CUDA_TRY(cudaSetDevice(c->device));
+    if (!is_pinned(host_dst)) return fail(RT_ERR_INVALID_ARG, "rt_download: host_dst is not pinned host memory");
+    CUDA_TRY(cudaEventRecord(c->order_ev, c->stream));
+    CUDA_TRY(cudaStreamWaitEvent(c->copy_stream, c->order_ev, 0));
+    CUDA_TRY(cudaMemcpyAsync(host_dst, dev_src, bytes, cudaMemcpyDeviceToHost, c->copy_stream));
+    if (done) {
+        rt_event* ev = new (std::nothrow) rt_event();
+        if (!ev) return fail(RT_ERR_OOM, "rt_download: event allocation");
+        cudaError_t e = cudaEventCreateWithFlags(&ev->ev, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventRecord(ev->ev, c->copy_stream);
+        if (e != cudaSuccess) {
+            if (ev->ev) cudaEventDestroy(ev->ev);
+            delete ev;
+            return fail(RT_ERR_CUDA, "rt_download: %s", cudaGetErrorString(e));
+        }
+        *done = ev;
+    }
+    return RT_OK;
+}
+
+rt_status rt_upload(rt_context* c, const void* host_src, void* dev_dst, size_t bytes) {
+    if (!c || !host_src || !dev_dst || !bytes) return fail(RT_ERR_INVALID_ARG, "rt_upload: NULL pointer or zero size");
+    CUDA_TRY(cudaSetDevice(c->device));
+    if (!is_pinned(host_src)) return fail(RT_ERR_INVALID_ARG, "rt_upload: host_src is not pinned host memory");
+    CUDA_TRY(cudaMemcpyAsync(dev_dst, host_src, bytes, cudaMemcpyHostToDevice, c->stream));
+    return RT_OK;
+}
+
+rt_status rt_wait(rt_event* ev) {
+    if (!ev) return fail(RT_ERR_INVALID_ARG, "rt_wait: NULL event");
+    cudaError_t e = cudaEventSynchronize(ev->ev);
+    cudaEventDestroy(ev->ev);
+    delete ev;
+    if (e != cudaSuccess) return fail(RT_ERR_CUDA, "rt_wait: %s", cudaGetErrorString(e));
+    return RT_OK;
+}
+
+rt_status rt_query(rt_event* ev) {
+    if (!ev) return fail(RT_ERR_INVALID_ARG, "rt_query: NULL event");
+    cudaError_t e = cudaEventQuery(ev->ev);
+    if (e == cudaSuccess) return RT_OK;
+    if (e == cudaErrorNotReady) {
+        cudaGetLastError();
+        return RT_ERR_NOT_READY;
+    }
+    return fail(RT_ERR_CUDA, "rt_query: %s", cudaGetErrorString(e));
+}
+
+// ------------------------------------------------------------------------------ shards
+rt_status rt_shard_tiles(uint32_t W, uint32_t H, uint32_t rank, uint32_t world, uint32_t* n_tiles, uint32_t* ids) {
+    if (!n_tiles || W == 0 || H == 0 || world == 0 || rank >= world || W > 16384 || H > 16384)
+        return fail(RT_ERR_INVALID_ARG, "rt_shard_tiles: bad arguments");
+    const ShardGeom g = shard_geom(W, H, world);
+    const uint32_t n = shard_count(g, rank, world);
+    if (ids)
+        for (uint32_t lt = 0; lt < n; ++lt) ids[lt] = shard_tile(g, rank, world, lt);
+    *n_tiles = n;
+    return RT_OK;
+}
+
+rt_status rt_shard_bytes(uint32_t W, uint32_t H, uint32_t world, uint32_t format, uint64_t* bytes) {
+    if (!bytes || W == 0 || H == 0 || world == 0 || (format != RT_FORMAT_RGBA8 && format != RT_FORMAT_RGBA16F))
+        return fail(RT_ERR_INVALID_ARG, "rt_shard_bytes: bad arguments");
+    const ShardGeom g = shard_geom(W, H, world);
+    uint32_t mx = 0;
+    for (uint32_t r = 0; r < world; ++r) mx = std::max(mx, shard_count(g, r, world));
+    *bytes = (uint64_t)mx * 256u * (format == RT_FORMAT_RGBA8 ? 4u : 8u);
+    return RT_OK;
+}
+
+rt_status rt_unpack_shards_host(const void* gathered, uint32_t W, uint32_t H, uint32_t world, uint32_t format,
+                                void* left, void* right, uint64_t pitch) {
+    uint64_t per = 0;
+    rt_status st = rt_shard_bytes(W, H, world, format, &per);
+    if (st) return st;
+    if (!gathered) return fail(RT_ERR_INVALID_ARG, "rt_unpack_shards_host: NULL gathered");
+    const uint32_t bpp = format == RT_FORMAT_RGBA8 ? 4 : 8;
+    if (pitch < (uint64_t)W * bpp) return fail(RT_ERR_SIZE, "rt_unpack_shards_host: pitch too small");
+    const ShardGeom g = shard_geom(W, H, world);
+    const char* src = static_cast<const char*>(gathered);
+    for (uint32_t r = 0; r < world; ++r) {
+        const uint32_t n = shard_count(g, r, world);
+        for (uint32_t lt = 0; lt < n; ++lt) {
+            const uint32_t gt = shard_tile(g, r, world, lt);
+            const int eye = (int)gt / g.tiles_per_eye;
+            const int t = (int)gt - eye * g.tiles_per_eye;
+            char* dst = static_cast<char*>(eye ? right : left);
+            if (!dst) continue;
+            for (int w = 0; w < 256; ++w) {
+                const int px = (t % g.tiles_x) * RT_TILE + w % RT_TILE;
+                const int py = (t / g.tiles_x) * RT_TILE + w / RT_TILE;
+                if (px >= (int)W || py >= (int)H) continue;
+                memcpy(dst + (uint64_t)py * pitch + (uint64_t)px * bpp,
+                       src + r * per + ((uint64_t)lt * 256 + w) * bpp, bpp);
+            }
+        }
+    }
+    return RT_OK;
+}
+
+rt_status rt_unpack_shards(rt_context* c, const void* gathered, uint32_t W, uint32_t H, uint32_t world, uint32_t format,
+                           rt_fb left, rt_fb right) {
+    if (!c || !gathered) return fail(RT_ERR_INVALID_ARG, "rt_unpack_shards: NULL argument");
+    uint64_t per = 0;
+    rt_status st = rt_shard_bytes(W, H, world, format, &per);
+    if (st) return st;
+    if ((left.dev_ptr && left.format != format) || (right.dev_ptr && right.format != format))
+        return fail(RT_ERR_INVALID_ARG, "rt_unpack_shards: framebuffer format differs from the shard format");
+    if (left.dev_ptr && right.dev_ptr && left.pitch_bytes != right.pitch_bytes)
+        return fail(RT_ERR_INVALID_ARG, "rt_unpack_shards: left/right pitch differ");
+    if ((st = check_fb(left, W, "left")) || (st = check_fb(right, W, "right"))) return st;
+    const ShardGeom g = shard_geom(W, H, world);
+    UnpackParams U{};
+    U.left = left.dev_ptr;
+    U.right = right.dev_ptr;
+    U.pitch = (long long)(left.dev_ptr ? left.pitch_bytes : right.pitch_bytes);
+    U.fmt = (int)format;
+    U.W = (int)W;
+    U.H = (int)H;
+    U.tiles_x = g.tiles_x;
+    U.tiles_per_eye = g.tiles_per_eye;
+    U.tiles_per_rank = (int)(per / (256u * (format == RT_FORMAT_RGBA8 ? 4u : 8u)));
+    U.world = (int)world;
+    U.shard_mode = g.mode;
+    U.shard_half = g.half;
+    CUDA_TRY(cudaSetDevice(c->device));
+    CUDA_TRY(rtb_launch_unpack(gathered, U, c->stream));
+    return RT_OK;
+}
+
+// ------------------------------------------------------------------------------ peer memory
+rt_status rt_ipc_get_handle(const void* dev_ptr, void* handle64) {
+    if (!dev_ptr || !handle64) return fail(RT_ERR_INVALID_ARG, "rt_ipc_get_handle: NULL argument");
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+    cudaIpcMemHandle_t h;
+    cudaError_t e = cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr));
+    if (e != cudaSuccess) return fail(RT_ERR_PEER, "cudaIpcGetMemHandle: %s", cudaGetErrorString(e));
+    memcpy(handle64, &h, 64);
+    return RT_OK;
+}
+
+rt_status rt_ipc_open(rt_context* c, const void* handle64, void** dev_ptr) {
+    if (!c || !handle64 || !dev_ptr) return fail(RT_ERR_INVALID_ARG, "rt_ipc_open: NULL argument");
+    CUDA_TRY(cudaSetDevice(c->device));
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle64, 64);
+    cudaError_t e = cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return fail(RT_ERR_PEER, "cudaIpcOpenMemHandle: %s", cudaGetErrorString(e));
+    return RT_OK;
+}
+
+rt_status rt_ipc_close(rt_context* c, void* dev_ptr) {
+    if (!c || !dev_ptr) return fail(RT_ERR_INVALID_ARG, "rt_ipc_close: NULL argument");
+    CUDA_TRY(cudaSetDevice(c->device));
+    cudaError_t e = cudaIpcCloseMemHandle(dev_ptr);
+    if (e != cudaSuccess) return fail(RT_ERR_PEER, "cudaIpcCloseMemHandle: %s", cudaGetErrorString(e));
+    return RT_OK;
+}
+
+// ------------------------------------------------------------------------------ introspection
+rt_status rt_scene_info(rt_context* c, uint64_t info[8]) {
+    if (!c || !info) return fail(RT_ERR_INVALID_ARG, "rt_scene_info: NULL argument");
+    if (!c->has_scene) return fail(RT_ERR_NO_SCENE, "rt_scene_info: no scene");
+    memcpy(info, c->info, sizeof c->info);
+    return RT_OK;
+}
+
+rt_status rt_bvh_export(rt_context* c, float* nodes, uint32_t* n_nodes, int32_t* prim_gid, uint32_t* n_prims) {
+    if (!c || !n_nodes || !n_prims) return fail(RT_ERR_INVALID_ARG, "rt_bvh_export: NULL argument");
+    if (!c->has_scene) return fail(RT_ERR_NO_SCENE, "rt_bvh_export: no scene");
+    const uint32_t nn = c->sc.n_bvh > 1 ? (uint32_t)c->sc.n_bvh - 1 : 0, np = (uint32_t)c->sc.n_bvh;
+    CUDA_TRY(cudaSetDevice(c->device));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    if (nodes && nn) CUDA_TRY(cudaMemcpy(nodes, c->sc.nodes, (size_t)nn * 64, cudaMemcpyDeviceToHost));
+    if (prim_gid && np) {
+        std::vector<float4> p(3 * (size_t)np);
+        CUDA_TRY(cudaMemcpy(p.data(), c->sc.prims, p.size() * sizeof(float4), cudaMemcpyDeviceToHost));
+        for (uint32_t k = 0; k < np; ++k) {
+            int32_t g;
+            memcpy(&g, &p[3 * k].w, 4);
+            prim_gid[k] = g;
+        }
+    }
+    *n_nodes = nn;
+    *n_prims = np;
+    return RT_OK;
+}
+
+rt_status rt_bench_ffma(rt_context* c, uint32_t iters, double* tflops, double* ms) {
+    if (!c || !tflops || !ms || !iters) return fail(RT_ERR_INVALID_ARG, "rt_bench_ffma: bad argument");
+    CUDA_TRY(cudaSetDevice(c->device));
+    const int grid = c->num_sms * 8;
+    cudaEvent_t a, b;
+    CUDA_TRY(cudaEventCreate(&a));
+    CUDA_TRY(cudaEventCreate(&b));
+    CUDA_TRY(rtb_launch_ffma(c->ffma_out, (int)iters, grid, c->stream));   // warm-up
+    CUDA_TRY(cudaEventRecord(a, c->stream));
+    CUDA_TRY(rtb_launch_ffma(c->ffma_out, (int)iters, grid, c->stream));
+    CUDA_TRY(cudaEventRecord(b, c->stream));
+    CUDA_TRY(cudaEventSynchronize(b));
+    float t = 0;
+    CUDA_TRY(cudaEventElapsedTime(&t, a, b));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    const double flops = 2.0 * 8 * 16 * (double)iters * grid * 256;
+    *ms = t;
+    *tflops = flops / (t * 1e-3) / 1e12;
+    return RT_OK;
+}
+
+}  // extern "C"

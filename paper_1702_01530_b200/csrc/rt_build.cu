@@ -1,0 +1,356 @@
+// rt_build.cu -- device-side scene packing and Morton-code LBVH construction.
+//
+// SURVEY.md §8(a) rows a1-a2; PAPER.md:44 (Table 1: BVH "high speed and adaptability of
+// construction", "good for the GPU").  Steps, all on the device:
+//   k_prim_setup     triangles -> (v0, e1, e2) records, spheres -> (c, r, r^2) records, AABBs, centroids
+//   k_bounds         centroid bounds (order-independent min/max -> deterministic)
+//   k_morton         30-bit Morton code (10 bits per axis) of the normalised centroid
+//   radix sort       hand-written stable LSD sort, 4 passes of 8/8/8/6 bits, ties keep the
+//                    original primitive order -> the 64-bit key (morton << 32 | position) is unique
+//   k_karras         Karras 2012 hierarchy: each internal node finds its key range and split
+//                    from common-prefix lengths (__clzll)
+//   k_refit          bottom-up AABB union with atomic arrival counters
+//   k_layout         box-pair node layout for traversal (rt_device.cuh), leaves = ~prim slot
+//   k_gather_prims   primitive records in leaf order
+// The result is a deterministic function of the input arrays.
+#include <cfloat>
+
+#include "rt_device.cuh"
+#include "rt_internal.h"
+
+namespace rtb {
+
+constexpr int SORT_THREADS = 256;
+constexpr int SORT_ITEMS = 8;
+constexpr int SORT_TILE = SORT_THREADS * SORT_ITEMS;
+
+__device__ __forceinline__ unsigned int f2ord(float f) {
+    const unsigned int u = __float_as_uint(f);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float ord2f(unsigned int u) {
+    return __uint_as_float((u & 0x80000000u) ? (u & 0x7fffffffu) : ~u);
+}
+
+__global__ void k_prim_setup(BuildBuffers B) {
+    const int N = B.n_spheres + B.n_tris;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
+        float4 r0, r1, r2, lo, hi, ce;
+        if (i < B.n_spheres) {
+            const float4 s = B.spheres[i];
+            r0 = make_float4(s.x, s.y, s.z, __int_as_float(i));
+            r1 = make_float4(s.w, s.w * s.w, 0.0f, __int_as_float((int)B.sphere_mat[i]));
+            r2 = make_float4(0.f, 0.f, 0.f, 0.f);
+            // round outward so the box contains the sphere
+            lo = make_float4(__fsub_rd(s.x, s.w), __fsub_rd(s.y, s.w), __fsub_rd(s.z, s.w), 0.f);
+            hi = make_float4(__fadd_ru(s.x, s.w), __fadd_ru(s.y, s.w), __fadd_ru(s.z, s.w), 0.f);
+            ce = make_float4(s.x, s.y, s.z, 0.f);
+        } else {
+            const int j = i - B.n_spheres;
+            const uint32_t a = B.tri_idx[3 * j], b = B.tri_idx[3 * j + 1], c = B.tri_idx[3 * j + 2];
+            const float3 v0 = f3(B.vertices[3 * a], B.vertices[3 * a + 1], B.vertices[3 * a + 2]);
+            const float3 v1 = f3(B.vertices[3 * b], B.vertices[3 * b + 1], B.vertices[3 * b + 2]);
+            const float3 v2 = f3(B.vertices[3 * c], B.vertices[3 * c + 1], B.vertices[3 * c + 2]);
+            const int gid = B.n_spheres + B.n_planes + j;
+            r0 = make_float4(v0.x, v0.y, v0.z, __int_as_float(gid));
+            r1 = make_float4(v1.x - v0.x, v1.y - v0.y, v1.z - v0.z, __int_as_float((int)B.tri_mat[j]));
+            r2 = make_float4(v2.x - v0.x, v2.y - v0.y, v2.z - v0.z, 0.f);
+            lo = make_float4(fminf(v0.x, fminf(v1.x, v2.x)), fminf(v0.y, fminf(v1.y, v2.y)),
+                             fminf(v0.z, fminf(v1.z, v2.z)), 0.f);
+            hi = make_float4(fmaxf(v0.x, fmaxf(v1.x, v2.x)), fmaxf(v0.y, fmaxf(v1.y, v2.y)),
+                             fmaxf(v0.z, fmaxf(v1.z, v2.z)), 0.f);
+            ce = make_float4((v0.x + v1.x + v2.x) * (1.0f / 3.0f), (v0.y + v1.y + v2.y) * (1.0f / 3.0f),
+                             (v0.z + v1.z + v2.z) * (1.0f / 3.0f), 0.f);
+        }
+        B.prims_unsorted[3 * i] = r0;
+        B.prims_unsorted[3 * i + 1] = r1;
+        B.prims_unsorted[3 * i + 2] = r2;
+        B.aabb_lo[i] = lo;
+        B.aabb_hi[i] = hi;
+        B.centroid[i] = ce;
+    }
+}
+
+__global__ void k_bounds_init(unsigned int* b) {
+    if (threadIdx.x < 3) b[threadIdx.x] = f2ord(FLT_MAX);
+    else if (threadIdx.x < 6) b[threadIdx.x] = f2ord(-FLT_MAX);
+}
+
+__global__ void k_bounds(const float4* __restrict__ ce, int n, unsigned int* b) {
+    float mn[3] = {FLT_MAX, FLT_MAX, FLT_MAX}, mx[3] = {-FLT_MAX, -FLT_MAX, -FLT_MAX};
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const float4 c = ce[i];
+        mn[0] = fminf(mn[0], c.x); mn[1] = fminf(mn[1], c.y); mn[2] = fminf(mn[2], c.z);
+        mx[0] = fmaxf(mx[0], c.x); mx[1] = fmaxf(mx[1], c.y); mx[2] = fmaxf(mx[2], c.z);
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            mn[k] = fminf(mn[k], __shfl_xor_sync(0xffffffffu, mn[k], off));
+            mx[k] = fmaxf(mx[k], __shfl_xor_sync(0xffffffffu, mx[k], off));
+        }
+    }
+    if ((threadIdx.x & 31) == 0) {
+        for (int k = 0; k < 3; ++k) {
+            atomicMin(&b[k], f2ord(mn[k]));
+            atomicMax(&b[3 + k], f2ord(mx[k]));
+        }
+    }
+}
+
+__device__ __forceinline__ uint32_t expand_bits10(uint32_t v) {
+    v = (v * 0x00010001u) & 0xFF0000FFu;
+    v = (v * 0x00000101u) & 0x0F00F00Fu;
+    v = (v * 0x00000011u) & 0xC30C30C3u;
+    v = (v * 0x00000005u) & 0x49249249u;
+    return v;
+}
+
+__global__ void k_morton(const float4* __restrict__ ce, int n, const unsigned int* b, uint32_t* keys, uint32_t* vals) {
+    const float lo[3] = {ord2f(b[0]), ord2f(b[1]), ord2f(b[2])};
+    const float hi[3] = {ord2f(b[3]), ord2f(b[4]), ord2f(b[5])};
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const float4 c = ce[i];
+        const float v[3] = {c.x, c.y, c.z};
+        uint32_t q[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const float ext = hi[k] - lo[k];
+            const float u = ext > 0.0f ? (v[k] - lo[k]) / ext : 0.5f;
+            q[k] = (uint32_t)fminf(fmaxf(u * 1024.0f, 0.0f), 1023.0f);
+        }
+        keys[i] = (expand_bits10(q[0]) << 2) | (expand_bits10(q[1]) << 1) | expand_bits10(q[2]);
+        vals[i] = (uint32_t)i;
+    }
+}
+
+// ---------------------------------------------------------------- stable LSD radix sort
+__global__ void __launch_bounds__(SORT_THREADS) k_radix_hist(const uint32_t* __restrict__ keys, int n, int shift,
+                                                           uint32_t* hist, int nblocks) {
+    __shared__ uint32_t h[256];
+    h[threadIdx.x] = 0;
+    __syncthreads();
+    const int base = blockIdx.x * SORT_TILE;
+#pragma unroll
+    for (int i = 0; i < SORT_ITEMS; ++i) {
+        const int idx = base + i * SORT_THREADS + threadIdx.x;
+        if (idx < n) atomicAdd(&h[(keys[idx] >> shift) & 255u], 1u);
+    }
+    __syncthreads();
+    hist[threadIdx.x * nblocks + blockIdx.x] = h[threadIdx.x];
+}
+
+// Exclusive scan of `n` entries with one block of 1024 threads (n is ~256 * N/2048).
+__global__ void __launch_bounds__(1024) k_scan_single(uint32_t* a, int n) {
+    __shared__ uint32_t warp_sums[32];
+    __shared__ uint32_t carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int base = 0; base < n; base += 1024) {
+        const int i = base + threadIdx.x;
+        const uint32_t v = i < n ? a[i] : 0u;
+        uint32_t x = v;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, off);
+            if (lane >= off) x += y;
+        }
+        if (lane == 31) warp_sums[wid] = x;
+        __syncthreads();
+        if (wid == 0) {
+            uint32_t s = warp_sums[lane];
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, s, off);
+                if (lane >= off) s += y;
+            }
+            warp_sums[lane] = s;
+        }
+        __syncthreads();
+        const uint32_t excl = x - v + (wid ? warp_sums[wid - 1] : 0u) + carry;
+        if (i < n) a[i] = excl;
+        __syncthreads();
+        if (threadIdx.x == 1023) carry = excl + v;
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(SORT_THREADS) k_radix_scatter(const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
+                                                              uint32_t* kout, uint32_t* vout, int n, int shift,
+                                                              const uint32_t* __restrict__ hist, int nblocks) {
+    constexpr int NW = SORT_THREADS / 32;
+    __shared__ uint32_t goff[256];
+    __shared__ uint32_t wcnt[NW][256];
+    __shared__ uint32_t woff[NW][256];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    goff[threadIdx.x] = hist[threadIdx.x * nblocks + blockIdx.x];
+    const int base = blockIdx.x * SORT_TILE;
+    const uint32_t lt_mask = (1u << lane) - 1u;
+    for (int it = 0; it < SORT_ITEMS; ++it) {
+#pragma unroll
+        for (int w = 0; w < NW; ++w) wcnt[w][threadIdx.x] = 0;
+        __syncthreads();
+        const int idx = base + it * SORT_THREADS + threadIdx.x;
+        const bool valid = idx < n;
+        uint32_t key = 0, val = 0, dig = 0xFFFFFFFFu;
+        if (valid) { key = kin[idx]; val = vin[idx]; dig = (key >> shift) & 255u; }
+        const uint32_t peers = __match_any_sync(0xffffffffu, dig);
+        const uint32_t rank = __popc(peers & lt_mask);
+        if (valid && rank == 0) wcnt[wid][dig] = __popc(peers);
+        __syncthreads();
+        {
+            const int d = threadIdx.x;
+            uint32_t run = goff[d];
+#pragma unroll
+            for (int w = 0; w < NW; ++w) { woff[w][d] = run; run += wcnt[w][d]; }
+            goff[d] = run;
+        }
+        __syncthreads();
+        if (valid) {
+            const uint32_t pos = woff[wid][dig] + rank;
+            kout[pos] = key;
+            vout[pos] = val;
+        }
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------- Karras hierarchy
+__device__ __forceinline__ int delta(const uint32_t* __restrict__ keys, int n, int i, int j) {
+    if (j < 0 || j >= n) return -1;
+    const unsigned long long a = ((unsigned long long)keys[i] << 32) | (unsigned)i;
+    const unsigned long long b = ((unsigned long long)keys[j] << 32) | (unsigned)j;
+    return __clzll(a ^ b);
+}
+
+__global__ void k_karras(const uint32_t* __restrict__ keys, int n, int* left, int* right, int* parent_int, int* parent_leaf) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n - 1; i += gridDim.x * blockDim.x) {
+        const int d = (delta(keys, n, i, i + 1) - delta(keys, n, i, i - 1)) >= 0 ? 1 : -1;
+        const int dmin = delta(keys, n, i, i - d);
+        int lmax = 2;
+        while (delta(keys, n, i, i + lmax * d) > dmin) lmax <<= 1;
+        int l = 0;
+        for (int t = lmax >> 1; t >= 1; t >>= 1)
+            if (delta(keys, n, i, i + (l + t) * d) > dmin) l += t;
+        const int j = i + l * d;
+        const int first = min(i, j), last = max(i, j);
+        const int dnode = delta(keys, n, first, last);
+        int split = first, step = last - first;
+        do {
+            step = (step + 1) >> 1;
+            const int ns = split + step;
+            if (ns < last && delta(keys, n, first, ns) > dnode) split = ns;
+        } while (step > 1);
+        int lc, rc;
+        if (split == first) { lc = ~split; parent_leaf[split] = i; }          // leaf: ~slot (count 1)
+        else { lc = split; parent_int[split] = i; }
+        if (split + 1 == last) { rc = ~(split + 1); parent_leaf[split + 1] = i; }
+        else { rc = split + 1; parent_int[split + 1] = i; }
+        left[i] = lc;
+        right[i] = rc;
+        if (i == 0) parent_int[0] = -1;
+    }
+}
+
+__device__ __forceinline__ void child_box(int c, const float4* lo_leaf, const float4* hi_leaf, const float4* lo_int,
+                                          const float4* hi_int, float4& lo, float4& hi) {
+    if (c < 0) { lo = lo_leaf[~c]; hi = hi_leaf[~c]; }
+    else { lo = __ldcg(&lo_int[c]); hi = __ldcg(&hi_int[c]); }
+}
+
+__global__ void k_refit(BuildBuffers B, int n, const float4* __restrict__ slo, const float4* __restrict__ shi) {
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+        int p = B.parent_leaf[k];
+        while (p >= 0) {
+            __threadfence();
+            if (atomicAdd(&B.flags[p], 1) == 0) break;    // first arrival: the sibling finishes p
+            __threadfence();
+            float4 a0, a1, b0, b1;
+            child_box(B.left[p], slo, shi, B.node_lo, B.node_hi, a0, a1);
+            child_box(B.right[p], slo, shi, B.node_lo, B.node_hi, b0, b1);
+            __stcg(&B.node_lo[p], make_float4(fminf(a0.x, b0.x), fminf(a0.y, b0.y), fminf(a0.z, b0.z), 0.f));
+            __stcg(&B.node_hi[p], make_float4(fmaxf(a1.x, b1.x), fmaxf(a1.y, b1.y), fmaxf(a1.z, b1.z), 0.f));
+            p = B.parent_int[p];
+        }
+    }
+}
+
+__global__ void k_layout(BuildBuffers B, int n, const float4* __restrict__ slo, const float4* __restrict__ shi) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n - 1; i += gridDim.x * blockDim.x) {
+        const int l = B.left[i], r = B.right[i];
+        float4 a0, a1, b0, b1;
+        child_box(l, slo, shi, B.node_lo, B.node_hi, a0, a1);
+        child_box(r, slo, shi, B.node_lo, B.node_hi, b0, b1);
+        B.nodes[4 * i + 0] = make_float4(a0.x, a1.x, a0.y, a1.y);
+        B.nodes[4 * i + 1] = make_float4(b0.x, b1.x, b0.y, b1.y);
+        B.nodes[4 * i + 2] = make_float4(a0.z, a1.z, b0.z, b1.z);
+        B.nodes[4 * i + 3] = make_float4(__int_as_float(l), __int_as_float(r), 0.f, 0.f);
+    }
+}
+
+// leaf-order records and leaf AABBs (slot k = sorted position k)
+__global__ void k_gather_prims(BuildBuffers B, int n, const uint32_t* __restrict__ order, float4* slo, float4* shi) {
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+        const uint32_t s = order[k];
+        B.prims[3 * k] = B.prims_unsorted[3 * s];
+        B.prims[3 * k + 1] = B.prims_unsorted[3 * s + 1];
+        B.prims[3 * k + 2] = B.prims_unsorted[3 * s + 2];
+        slo[k] = B.aabb_lo[s];
+        shi[k] = B.aabb_hi[s];
+    }
+}
+
+__global__ void k_depth(const int* __restrict__ parent_leaf, const int* __restrict__ parent_int, int n, int* maxd) {
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+        int d = 0, p = parent_leaf[k];
+        while (p >= 0) { ++d; p = parent_int[p]; }
+        atomicMax(maxd, d);
+    }
+}
+
+}  // namespace rtb
+
+using namespace rtb;
+
+size_t rtb_sort_hist_entries(int n) { return 256u * (size_t)((n + SORT_TILE - 1) / SORT_TILE); }
+
+static int grid_for(int n, int block = 256) {
+    const int g = (n + block - 1) / block;
+    return g < 1 ? 1 : (g > 148 * 16 ? 148 * 16 : g);
+}
+
+cudaError_t rtb_build_bvh(const BuildBuffers& Bc, cudaStream_t st) {
+    BuildBuffers B = Bc;
+    const int n = B.n_spheres + B.n_tris;
+    if (n == 0) return cudaSuccess;
+    k_prim_setup<<<grid_for(n), 256, 0, st>>>(B);
+    if (n == 1) {
+        cudaMemcpyAsync(B.prims, B.prims_unsorted, 3 * sizeof(float4), cudaMemcpyDeviceToDevice, st);
+        cudaMemsetAsync(B.max_depth, 0, sizeof(int), st);
+        return cudaGetLastError();
+    }
+    k_bounds_init<<<1, 32, 0, st>>>(B.bounds);
+    k_bounds<<<grid_for(n), 256, 0, st>>>(B.centroid, n, B.bounds);
+    k_morton<<<grid_for(n), 256, 0, st>>>(B.centroid, n, B.bounds, B.keys[0], B.vals[0]);
+    const int nb = (n + SORT_TILE - 1) / SORT_TILE;
+    int cur = 0;
+    for (int shift = 0; shift < 30; shift += 8) {
+        k_radix_hist<<<nb, SORT_THREADS, 0, st>>>(B.keys[cur], n, shift, B.hist, nb);
+        k_scan_single<<<1, 1024, 0, st>>>(B.hist, 256 * nb);
+        k_radix_scatter<<<nb, SORT_THREADS, 0, st>>>(B.keys[cur], B.vals[cur], B.keys[cur ^ 1], B.vals[cur ^ 1], n,
+                                                     shift, B.hist, nb);
+        cur ^= 1;
+    }
+    float4* slo = B.leaf_lo;
+    float4* shi = B.leaf_hi;
+    k_gather_prims<<<grid_for(n), 256, 0, st>>>(B, n, B.vals[cur], slo, shi);
+    k_karras<<<grid_for(n - 1), 256, 0, st>>>(B.keys[cur], n, B.left, B.right, B.parent_int, B.parent_leaf);
+    cudaMemsetAsync(B.flags, 0, sizeof(int) * (n - 1), st);
+    k_refit<<<grid_for(n), 256, 0, st>>>(B, n, slo, shi);
+    k_layout<<<grid_for(n - 1), 256, 0, st>>>(B, n, slo, shi);
+    cudaMemsetAsync(B.max_depth, 0, sizeof(int), st);
+    k_depth<<<grid_for(n), 256, 0, st>>>(B.parent_leaf, B.parent_int, n, B.max_depth);
+    return cudaGetLastError();
+}

@@ -1,0 +1,153 @@
+// rt_device.cuh -- device-side data layout and FP32 intersectors of the B200 stereo ray tracer.
+//
+// Layout in HBM:
+//   nodes  : BVH2 internal nodes, 4 x float4 = 64 B each (box pair, Aila-Laine order)
+//              n0 = (c0.lo.x, c0.hi.x, c0.lo.y, c0.hi.y)
+//              n1 = (c1.lo.x, c1.hi.x, c1.lo.y, c1.hi.y)
+//              n2 = (c0.lo.z, c0.hi.z, c1.lo.z, c1.hi.z)
+//              n3 = (child0, child1, -, -) as int; child >= 0 internal node, child < 0 leaf
+//                   ~child = (count-1) << 24 | first_prim
+//   prims  : 3 x float4 = 48 B per BVH primitive, in leaf (Morton) order
+//              triangle: (v0.xyz, gid) (e1.xyz, mat) (e2.xyz, 0)        -- SPEC:170 Moller-Trumbore
+//              sphere  : (c.xyz,  gid) (r, r^2, 0, mat) (0)
+//            gid < n_spheres <=> sphere (global IDs: spheres, planes, triangles).
+//   planes : (n^.xyz, k) float4 + mat int, tested linearly (infinite, not in the BVH)
+//   mats   : 3 x float4: (kd.xyz, shininess) (ks.xyz, kr) (kt, ior, 0, 0)
+//   lights : 2 x float4: (pos.xyz, 0) (I.xyz, 0)
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_fp16.h>
+#include <stdint.h>
+
+namespace rtb {
+
+constexpr float T_MIN = 1e-4f;     // SPEC.md:156 t_min
+constexpr float BIAS = 1e-4f;      // SPEC.md:156 shadow_bias (also reflection/refraction origins)
+constexpr int MAX_DEPTH = 16;
+constexpr int BVH_STACK = 64;      // LBVH depth <= 30 Morton bits + 32 index bits
+constexpr int LEAF_SHIFT = 24;     // leaf encoding: ~((count-1) << 24 | first)
+constexpr int TILE = 16;
+
+struct DevScene {
+    const float4* __restrict__ nodes;
+    const float4* __restrict__ prims;
+    const float4* __restrict__ planes;
+    const int* __restrict__ plane_mat;
+    const float4* __restrict__ mats;
+    const float4* __restrict__ lights;
+    int n_bvh;          // primitives in the BVH
+    int root;           // >= 0 internal node, < 0 leaf encoding, meaningless if n_bvh == 0
+    int n_spheres;
+    int n_planes;
+    int n_lights;
+    float bound;        // max |x|+|y|+|z| over the BVH bounds (box-test margin scale)
+    float3 ambient;
+    float3 background;
+};
+
+struct DevCamera {
+    float3 eye[2];
+    float3 f, r, u;
+    float tha, th;      // tan(vfov/2) * aspect, tan(vfov/2)
+    float sigma[2];     // off-axis shift per eye
+};
+
+// ------------------------------------------------------------------ float3 helpers
+__device__ __forceinline__ float3 f3(float x, float y, float z) { return make_float3(x, y, z); }
+__device__ __forceinline__ float3 xyz(float4 a) { return make_float3(a.x, a.y, a.z); }
+__device__ __forceinline__ float3 operator+(float3 a, float3 b) { return f3(a.x + b.x, a.y + b.y, a.z + b.z); }
+__device__ __forceinline__ float3 operator-(float3 a, float3 b) { return f3(a.x - b.x, a.y - b.y, a.z - b.z); }
+__device__ __forceinline__ float3 operator*(float3 a, float s) { return f3(a.x * s, a.y * s, a.z * s); }
+__device__ __forceinline__ float3 operator*(float3 a, float3 b) { return f3(a.x * b.x, a.y * b.y, a.z * b.z); }
+__device__ __forceinline__ float dot(float3 a, float3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+__device__ __forceinline__ float3 cross(float3 a, float3 b) {
+    return f3(a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x);
+}
+__device__ __forceinline__ float3 normalize(float3 a) { return a * rsqrtf(dot(a, a)); }
+__device__ __forceinline__ float3 fma3(float3 a, float s, float3 b) {
+    return f3(fmaf(a.x, s, b.x), fmaf(a.y, s, b.y), fmaf(a.z, s, b.z));
+}
+
+// ------------------------------------------------------------------ intersectors (FP32)
+// Moller-Trumbore with stored v0, e1, e2: inclusive edges, det == 0 -> miss.
+// Returns the raw t (caller applies t_min / t_best).
+__device__ __forceinline__ bool tri_intersect(float3 o, float3 d, float4 a, float4 b, float4 c, float& t) {
+    const float3 e1 = xyz(b), e2 = xyz(c);
+    const float3 p = cross(d, e2);
+    const float det = dot(e1, p);
+    if (det == 0.0f) return false;
+    const float inv = __frcp_rn(det);
+    const float3 s = o - xyz(a);
+    const float u = dot(s, p) * inv;
+    if (u < 0.0f || u > 1.0f) return false;
+    const float3 q = cross(s, e1);
+    const float v = dot(d, q) * inv;
+    if (v < 0.0f || u + v > 1.0f) return false;
+    t = dot(e2, q) * inv;
+    return true;
+}
+
+// Sphere |o + t d - c| = r, |d| = 1, numerically stable form (reading 21):
+// disc = r^2 - |oc - (oc.d) d|^2, roots -b -/+ sqrt(disc); returns the smallest root > tmin.
+__device__ __forceinline__ bool sphere_intersect(float3 o, float3 d, float4 a, float4 b, float tmin, float& t) {
+    const float3 oc = o - xyz(a);
+    const float bb = dot(oc, d);
+    const float3 f = oc - d * bb;
+    const float disc = b.y - dot(f, f);
+    if (disc < 0.0f) return false;
+    const float q = sqrtf(disc);
+    const float cc = dot(oc, oc) - b.y;
+    const float h = bb > 0.0f ? -(bb + q) : (q - bb);     // larger-magnitude root
+    float t0, t1;
+    if (h != 0.0f) { t0 = cc / h; t1 = h; } else { t0 = 0.0f; t1 = 0.0f; }
+    if (t0 > t1) { const float x = t0; t0 = t1; t1 = x; }
+    if (t0 > tmin) { t = t0; return true; }
+    if (t1 > tmin) { t = t1; return true; }
+    return false;
+}
+
+// Plane n^.x = k: t = (k - n^.o) / (n^.d); n^.d == 0 -> miss.
+__device__ __forceinline__ bool plane_intersect(float3 o, float3 d, float4 p, float& t) {
+    const float3 n = xyz(p);
+    const float den = dot(n, d);
+    if (den == 0.0f) return false;
+    t = (p.w - dot(n, o)) / den;
+    return true;
+}
+
+// Conservative slab-test setup.  Box planes are tested as fma(plane, 1/d, -(o -/+ m)/d),
+// i.e. against the box inflated by m = 1e-6 (|o|_1 + B) world units, which exceeds the
+// FP32 error of every primitive test by >10x, so the BVH never culls a primitive the
+// brute-force loop would accept (GPU LBVH == GPU brute force, bit-exact).
+struct RayBox {
+    float3 idir;
+    float3 nlo;   // -(o + m) * idir
+    float3 nhi;   // -(o - m) * idir
+};
+
+__device__ __forceinline__ float safe_inv(float x) {
+    const float ax = fabsf(x);
+    return 1.0f / (ax < 1e-30f ? copysignf(1e-30f, x) : x);
+}
+
+__device__ __forceinline__ RayBox make_raybox(float3 o, float3 d, float bound) {
+    RayBox rb;
+    const float m = 1e-6f * (fabsf(o.x) + fabsf(o.y) + fabsf(o.z) + bound);
+    rb.idir = f3(safe_inv(d.x), safe_inv(d.y), safe_inv(d.z));
+    rb.nlo = f3(-(o.x + m) * rb.idir.x, -(o.y + m) * rb.idir.y, -(o.z + m) * rb.idir.z);
+    rb.nhi = f3(-(o.x - m) * rb.idir.x, -(o.y - m) * rb.idir.y, -(o.z - m) * rb.idir.z);
+    return rb;
+}
+
+// Returns the entry distance, or +inf when the (inflated) box is missed within [0, tmax].
+__device__ __forceinline__ float box_enter(const RayBox& rb, float lox, float hix, float loy, float hiy,
+                                           float loz, float hiz, float tmax) {
+    const float ax = fmaf(lox, rb.idir.x, rb.nlo.x), bx = fmaf(hix, rb.idir.x, rb.nhi.x);
+    const float ay = fmaf(loy, rb.idir.y, rb.nlo.y), by = fmaf(hiy, rb.idir.y, rb.nhi.y);
+    const float az = fmaf(loz, rb.idir.z, rb.nlo.z), bz = fmaf(hiz, rb.idir.z, rb.nhi.z);
+    const float tn = fmaxf(fmaxf(fminf(ax, bx), fminf(ay, by)), fmaxf(fminf(az, bz), 0.0f));
+    const float tf = fminf(fminf(fmaxf(ax, bx), fmaxf(ay, by)), fminf(fmaxf(az, bz), tmax));
+    return tn <= tf ? tn : __int_as_float(0x7f800000);
+}
+
+}  // namespace rtb

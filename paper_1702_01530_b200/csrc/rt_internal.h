@@ -1,0 +1,90 @@
+// rt_internal.h -- shared between the host runtime (rt_api.cu) and the kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/rt_b200.h"
+#include "rt_device.cuh"
+
+enum {
+    CNT_PRIMARY = RT_CNT_PRIMARY,
+    CNT_REFLECTION = RT_CNT_REFLECTION,
+    CNT_REFRACTION = RT_CNT_REFRACTION,
+    CNT_SHADOW = RT_CNT_SHADOW,
+    CNT_NODE_VISITS = RT_CNT_NODE_VISITS,
+    CNT_TRI_TESTS = RT_CNT_TRI_TESTS,
+    CNT_SPHERE_TESTS = RT_CNT_SPHERE_TESTS,
+    CNT_PLANE_TESTS = RT_CNT_PLANE_TESTS,
+    CNT_SHADE_HITS = RT_CNT_SHADE_HITS,
+    CNT_LIGHT_EVALS = RT_CNT_LIGHT_EVALS,
+    CNT_MISSES = RT_CNT_MISSES,
+    CNT_PIXELS = RT_CNT_PIXELS,
+};
+#define RT_NUM_COUNTERS_INTERNAL RT_NUM_COUNTERS
+
+struct TraceParams {
+    rtb::DevScene sc;
+    rtb::DevCamera cam;
+    int W, H, max_depth;
+    int* work_counter;
+    int n_work;             // work items (pixels incl. tile padding) of this shard
+    int tiles_x, tiles_per_eye;
+    int shard_mode;         // 0 all tiles, 1 eye-split groups (even world), 2 interleaved (odd world)
+    int shard_rank, shard_world, shard_half;
+    void* fb[2];
+    int fb_fmt[2];
+    long long fb_pitch[2];
+    int* prim_id;
+    float4* radiance;
+    void* shard;
+    int shard_fmt;
+    unsigned long long* counters;
+};
+
+struct UnpackParams {
+    void* left;
+    void* right;
+    long long pitch;
+    int fmt;
+    int W, H, tiles_x, tiles_per_eye, tiles_per_rank;
+    int world, shard_mode, shard_half;
+};
+
+// BVH build scratch (device pointers), owned by the context.
+struct BuildBuffers {
+    const float4* spheres;      // [S] (c, r)
+    const float* vertices;      // [3V]
+    const uint32_t* tri_idx;    // [3T]
+    const uint32_t* tri_mat;    // [T]
+    const uint32_t* sphere_mat; // [S]
+    int n_spheres, n_planes, n_tris;
+    float4* prims_unsorted;     // [3N]
+    float4* prims;              // [3N] leaf order
+    float4* aabb_lo;            // [N]
+    float4* aabb_hi;            // [N]
+    float4* centroid;           // [N]
+    float4* leaf_lo;            // [N] leaf-order AABBs
+    float4* leaf_hi;            // [N]
+    unsigned int* bounds;       // [6] ordered-int centroid bounds
+    uint32_t* keys[2];          // [N]
+    uint32_t* vals[2];          // [N]
+    uint32_t* hist;             // [256 * nblocks]
+    int* left;                  // [N-1] child encodings
+    int* right;                 // [N-1]
+    int* parent_int;            // [N-1]
+    int* parent_leaf;           // [N]
+    int* flags;                 // [N-1]
+    float4* node_lo;            // [N-1]
+    float4* node_hi;            // [N-1]
+    float4* nodes;              // [4(N-1)] final layout
+    int* max_depth;             // [1]
+};
+
+// launchers (rt_trace.cu)
+cudaError_t rtb_launch_trace(const TraceParams& P, unsigned flags, int grid, cudaStream_t st);
+cudaError_t rtb_trace_occupancy(unsigned flags, int* blocks_per_sm);
+cudaError_t rtb_launch_unpack(const void* gathered, const UnpackParams& U, cudaStream_t st);
+cudaError_t rtb_launch_ffma(float* out, int iters, int grid, cudaStream_t st);
+// launchers (rt_build.cu)
+size_t rtb_sort_hist_entries(int n);
+cudaError_t rtb_build_bvh(const BuildBuffers& B, cudaStream_t st);

@@ -1,0 +1,446 @@
+// rt_trace.cu -- the hot path: one persistent-thread megakernel that, for every pixel of both
+// eyes (§3 Fig. 2 "level 1" channels x "level 2" pixels), generates the primary
+// ray, finds nearest hits through the LBVH (+ linear planes), shades with Phong + shadow rays
+// per light, follows reflection/refraction with an iterative per-thread ray stack up to
+// max_depth bounces, and packs the clamped radiance straight into the RGBA8/FP16 framebuffers
+// (and, optionally, prim-ID / radiance debug planes, a tile-packed shard, or a peer rank's
+// framebuffer over NVLink).  SURVEY.md §8(a) rows a3-a6; DESIGN.md §5.
+#include "rt_device.cuh"
+#include "rt_internal.h"
+
+namespace rtb {
+
+struct Cnt {
+    unsigned long long v[RT_NUM_COUNTERS_INTERNAL];
+};
+
+template <bool COUNT>
+struct Counters {
+    uint32_t c[RT_NUM_COUNTERS_INTERNAL];
+    __device__ void zero() {
+#pragma unroll
+        for (int i = 0; i < RT_NUM_COUNTERS_INTERNAL; ++i) c[i] = 0;
+    }
+    __device__ __forceinline__ void add(int i, uint32_t n = 1) { if (COUNT) c[i] += n; }
+};
+
+struct Hit {
+    float t;
+    int gid;    // global primitive ID, -1 = miss
+    int slot;   // BVH prim slot (>= 0) or ~plane index (< 0)
+};
+
+// Nearest hit over the BVH (or every BVH primitive when BRUTE) and the planes.
+// Acceptance: t > t_min and (t, gid) lexicographically smallest (reading 9).
+template <bool COUNT, bool BRUTE>
+__device__ __forceinline__ Hit closest_hit(const DevScene& S, float3 o, float3 d, Counters<COUNT>& cnt) {
+    Hit h;
+    h.t = __int_as_float(0x7f800000);
+    h.gid = -1;
+    h.slot = 0;
+    for (int i = 0; i < S.n_planes; ++i) {
+        cnt.add(CNT_PLANE_TESTS);
+        float t;
+        if (plane_intersect(o, d, S.planes[i], t) && t > T_MIN) {
+            const int gid = S.n_spheres + i;
+            if (t < h.t || (t == h.t && gid < h.gid)) { h.t = t; h.gid = gid; h.slot = ~i; }
+        }
+    }
+    if (S.n_bvh == 0) return h;
+
+    auto test_prim = [&](int k) {
+        const float4 a = __ldg(&S.prims[3 * k]);
+        const int gid = __float_as_int(a.w);
+        float t;
+        bool ok;
+        if (gid < S.n_spheres) {
+            cnt.add(CNT_SPHERE_TESTS);
+            ok = sphere_intersect(o, d, a, __ldg(&S.prims[3 * k + 1]), T_MIN, t);
+        } else {
+            cnt.add(CNT_TRI_TESTS);
+            ok = tri_intersect(o, d, a, __ldg(&S.prims[3 * k + 1]), __ldg(&S.prims[3 * k + 2]), t) && t > T_MIN;
+        }
+        if (ok && (t < h.t || (t == h.t && gid < h.gid))) { h.t = t; h.gid = gid; h.slot = k; }
+    };
+
+    if (BRUTE) {
+        for (int k = 0; k < S.n_bvh; ++k) test_prim(k);
+        return h;
+    }
+
+    const RayBox rb = make_raybox(o, d, S.bound);
+    int stack[BVH_STACK];
+    int sp = 0;
+    int node = S.root;
+    while (true) {
+        while (node >= 0) {
+            cnt.add(CNT_NODE_VISITS);
+            const float4 n0 = __ldg(&S.nodes[4 * node + 0]);
+            const float4 n1 = __ldg(&S.nodes[4 * node + 1]);
+            const float4 n2 = __ldg(&S.nodes[4 * node + 2]);
+            const int4 n3 = __ldg(reinterpret_cast<const int4*>(&S.nodes[4 * node + 3]));
+            const float t0 = box_enter(rb, n0.x, n0.y, n0.z, n0.w, n2.x, n2.y, h.t);
+            const float t1 = box_enter(rb, n1.x, n1.y, n1.z, n1.w, n2.z, n2.w, h.t);
+            const bool h0 = t0 <= h.t, h1 = t1 <= h.t;
+            if (h0 && h1) {
+                const bool swap = t1 < t0;
+                node = swap ? n3.y : n3.x;
+                stack[sp++] = swap ? n3.x : n3.y;
+            } else if (h0) {
+                node = n3.x;
+            } else if (h1) {
+                node = n3.y;
+            } else {
+                if (sp == 0) return h;
+                node = stack[--sp];
+            }
+        }
+        // leaf
+        const int enc = ~node;
+        const int first = enc & ((1 << LEAF_SHIFT) - 1);
+        const int count = (enc >> LEAF_SHIFT) + 1;
+        for (int k = first; k < first + count; ++k) test_prim(k);
+        if (sp == 0) return h;
+        node = stack[--sp];
+    }
+}
+
+// Any hit with t_min < t < dist (binary visibility, reading 4).
+template <bool COUNT, bool BRUTE>
+__device__ __forceinline__ bool occluded(const DevScene& S, float3 o, float3 d, float dist, Counters<COUNT>& cnt) {
+    for (int i = 0; i < S.n_planes; ++i) {
+        cnt.add(CNT_PLANE_TESTS);
+        float t;
+        if (plane_intersect(o, d, S.planes[i], t) && t > T_MIN && t < dist) return true;
+    }
+    if (S.n_bvh == 0) return false;
+
+    auto test_prim = [&](int k) -> bool {
+        const float4 a = __ldg(&S.prims[3 * k]);
+        const int gid = __float_as_int(a.w);
+        float t;
+        if (gid < S.n_spheres) {
+            cnt.add(CNT_SPHERE_TESTS);
+            return sphere_intersect(o, d, a, __ldg(&S.prims[3 * k + 1]), T_MIN, t) && t < dist;
+        }
+        cnt.add(CNT_TRI_TESTS);
+        return tri_intersect(o, d, a, __ldg(&S.prims[3 * k + 1]), __ldg(&S.prims[3 * k + 2]), t) &&
+               t > T_MIN && t < dist;
+    };
+
+    if (BRUTE) {
+        for (int k = 0; k < S.n_bvh; ++k)
+            if (test_prim(k)) return true;
+        return false;
+    }
+
+    const RayBox rb = make_raybox(o, d, S.bound);
+    int stack[BVH_STACK];
+    int sp = 0;
+    int node = S.root;
+    while (true) {
+        while (node >= 0) {
+            cnt.add(CNT_NODE_VISITS);
+            const float4 n0 = __ldg(&S.nodes[4 * node + 0]);
+            const float4 n1 = __ldg(&S.nodes[4 * node + 1]);
+            const float4 n2 = __ldg(&S.nodes[4 * node + 2]);
+            const int4 n3 = __ldg(reinterpret_cast<const int4*>(&S.nodes[4 * node + 3]));
+            const float t0 = box_enter(rb, n0.x, n0.y, n0.z, n0.w, n2.x, n2.y, dist);
+            const float t1 = box_enter(rb, n1.x, n1.y, n1.z, n1.w, n2.z, n2.w, dist);
+            const bool h0 = t0 <= dist, h1 = t1 <= dist;
+            if (h0 && h1) {
+                node = n3.x;
+                stack[sp++] = n3.y;
+            } else if (h0) {
+                node = n3.x;
+            } else if (h1) {
+                node = n3.y;
+            } else {
+                if (sp == 0) return false;
+                node = stack[--sp];
+            }
+        }
+        const int enc = ~node;
+        const int first = enc & ((1 << LEAF_SHIFT) - 1);
+        const int count = (enc >> LEAF_SHIFT) + 1;
+        for (int k = first; k < first + count; ++k)
+            if (test_prim(k)) return true;
+        if (sp == 0) return false;
+        node = stack[--sp];
+    }
+}
+
+// Work item -> (eye, px, py).  16x16 tiles, each tile = 8 warps of 8x4 pixels so a warp's
+// primary rays are spatially coherent.  Tiles are drawn from this rank's shard.
+__device__ __forceinline__ bool map_work(const TraceParams& P, int k, int& eye, int& px, int& py, int& gtile) {
+    const int lt = k >> 8;
+    const int within = k & 255;
+    int g;
+    if (P.shard_mode == 0) {
+        g = lt;
+    } else if (P.shard_mode == 1) {
+        const int grp = P.shard_rank / P.shard_half;
+        const int j = P.shard_rank % P.shard_half;
+        g = grp * P.tiles_per_eye + j + lt * P.shard_half;
+    } else {
+        g = P.shard_rank + lt * P.shard_world;
+    }
+    gtile = g;
+    eye = g / P.tiles_per_eye;
+    const int t = g - eye * P.tiles_per_eye;
+    const int tx = t % P.tiles_x, ty = t / P.tiles_x;
+    const int w = within >> 5, lane = within & 31;
+    px = tx * TILE + (w & 1) * 8 + (lane & 7);
+    py = ty * TILE + (w >> 1) * 4 + (lane >> 3);
+    return px < P.W && py < P.H;
+}
+
+__device__ __forceinline__ uint32_t pack_rgba8(float3 c) {
+    const float r = __saturatef(c.x), g = __saturatef(c.y), b = __saturatef(c.z);
+    const uint32_t R = __float2uint_rd(fmaf(r, 255.0f, 0.5f));
+    const uint32_t G = __float2uint_rd(fmaf(g, 255.0f, 0.5f));
+    const uint32_t B = __float2uint_rd(fmaf(b, 255.0f, 0.5f));
+    return R | (G << 8) | (B << 16) | (0xFFu << 24);
+}
+
+__device__ __forceinline__ uint2 pack_rgba16f(float3 c) {
+    const __half r = __float2half_rn(__saturatef(c.x)), g = __float2half_rn(__saturatef(c.y));
+    const __half b = __float2half_rn(__saturatef(c.z)), a = __float2half_rn(1.0f);
+    return make_uint2((uint32_t)__half_as_ushort(r) | ((uint32_t)__half_as_ushort(g) << 16),
+                      (uint32_t)__half_as_ushort(b) | ((uint32_t)__half_as_ushort(a) << 16));
+}
+
+__device__ __forceinline__ void store_px(void* base, int fmt, long long pitch, int x, int y, float3 c) {
+    char* row = static_cast<char*>(base) + (long long)y * pitch;
+    if (fmt == RT_FORMAT_RGBA8) reinterpret_cast<uint32_t*>(row)[x] = pack_rgba8(c);
+    else reinterpret_cast<uint2*>(row)[x] = pack_rgba16f(c);
+}
+
+// Trace the whole ray tree of one pixel.  Iterative: the reflection child continues in
+// registers, the refraction child is pushed on a per-thread stack (<= max_depth entries).
+// Radiance accumulates as sum over tree nodes of path_weight * local_term, which equals the
+// recursive definition c = local + kt*T(refr) + kr_eff*T(refl) (reading 17).
+template <bool COUNT, bool BRUTE>
+__device__ float3 trace_pixel(const TraceParams& P, float3 o, float3 d, int& prim_id, Counters<COUNT>& cnt) {
+    const DevScene& S = P.sc;
+    float4 st_a[MAX_DEPTH], st_b[MAX_DEPTH];   // (o, w) (d, depth)
+    int sp = 0;
+    float w = 1.0f;
+    int depth = P.max_depth;
+    bool primary = true;
+    float3 col = f3(0.f, 0.f, 0.f);
+    cnt.add(CNT_PRIMARY);
+    while (true) {
+        const Hit h = closest_hit<COUNT, BRUTE>(S, o, d, cnt);
+        if (primary) { prim_id = h.gid; primary = false; }
+        bool cont = false;
+        if (h.gid < 0) {
+            cnt.add(CNT_MISSES);
+            col = fma3(S.background, w, col);                       // S:203 miss -> background
+        } else {
+            cnt.add(CNT_SHADE_HITS);
+            const float3 p = fma3(d, h.t, o);
+            float3 ng;
+            int mat;
+            if (h.slot < 0) {
+                const int i = ~h.slot;
+                ng = xyz(S.planes[i]);
+                mat = S.plane_mat[i];
+            } else {
+                const float4 a = __ldg(&S.prims[3 * h.slot]);
+                const float4 b = __ldg(&S.prims[3 * h.slot + 1]);
+                mat = __float_as_int(b.w);
+                if (h.gid < S.n_spheres) {
+                    ng = (p - xyz(a)) * (1.0f / b.x);
+                } else {
+                    const float4 c = __ldg(&S.prims[3 * h.slot + 2]);
+                    ng = normalize(cross(xyz(b), xyz(c)));
+                }
+            }
+            const bool front = dot(d, ng) < 0.0f;
+            const float3 nf = front ? ng : ng * -1.0f;               // S:150 faces the ray
+            const float4 m0 = __ldg(&S.mats[3 * mat]), m1 = __ldg(&S.mats[3 * mat + 1]);
+            const float4 m2 = __ldg(&S.mats[3 * mat + 2]);
+            const float3 kd = xyz(m0), ks = xyz(m1);
+            float3 c = S.ambient * kd;                               // S:193 ambient * kd
+            for (int j = 0; j < S.n_lights; ++j) {
+                cnt.add(CNT_LIGHT_EVALS);
+                const float3 Lp = xyz(__ldg(&S.lights[2 * j]));
+                const float3 l = normalize(Lp - p);
+                const float ndl = dot(nf, l);
+                if (ndl <= 0.0f) continue;                           // reading 2 gate
+                const float3 os = fma3(nf, BIAS, p);
+                const float3 sv = Lp - os;
+                const float dist = sqrtf(dot(sv, sv));
+                const float3 sd = sv * (1.0f / dist);
+                cnt.add(CNT_SHADOW);
+                if (occluded<COUNT, BRUTE>(S, os, sd, dist, cnt)) continue;
+                const float3 I = xyz(__ldg(&S.lights[2 * j + 1]));
+                const float3 rv = nf * (2.0f * ndl) - l;
+                const float rdv = -dot(rv, d);
+                const float spec = rdv > 0.0f ? __powf(rdv, m0.w) : 0.0f;
+                c = c + (kd * I) * ndl + (ks * I) * spec;            // no falloff, reading 3
+            }
+            col = fma3(c, w, col);
+            if (depth > 0) {
+                float kr_eff = m1.w;
+                const float kt = m2.x;
+                if (kt > 0.0f) {
+                    const float eta = front ? 1.0f / m2.y : m2.y;
+                    const float cosi = -dot(d, nf);
+                    const float k = 1.0f - eta * eta * (1.0f - cosi * cosi);
+                    if (k < 0.0f) {
+                        kr_eff += kt;                                // reading 5 TIR
+                    } else {
+                        cnt.add(CNT_REFRACTION);
+                        const float3 td = normalize(d * eta + nf * (eta * cosi - sqrtf(k)));
+                        const float3 to = fma3(nf, -BIAS, p);
+                        st_a[sp] = make_float4(to.x, to.y, to.z, w * kt);
+                        st_b[sp] = make_float4(td.x, td.y, td.z, __int_as_float(depth - 1));
+                        ++sp;
+                    }
+                }
+                if (kr_eff > 0.0f) {
+                    cnt.add(CNT_REFLECTION);
+                    d = normalize(d - nf * (2.0f * dot(d, nf)));
+                    o = fma3(nf, BIAS, p);
+                    w *= kr_eff;
+                    depth -= 1;
+                    cont = true;
+                }
+            }
+        }
+        if (cont) continue;
+        if (sp == 0) break;
+        --sp;
+        const float4 a = st_a[sp], b = st_b[sp];
+        o = xyz(a);
+        w = a.w;
+        d = xyz(b);
+        depth = __float_as_int(b.w);
+    }
+    return col;
+}
+
+template <bool COUNT, bool BRUTE>
+__global__ void __launch_bounds__(256) k_trace_stereo(const TraceParams P) {
+    Counters<COUNT> cnt;
+    cnt.zero();
+    const int lane = threadIdx.x & 31;
+    while (true) {
+        int base = 0;
+        if (lane == 0) base = atomicAdd(P.work_counter, 32);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (base >= P.n_work) break;
+        const int k = base + lane;
+        int eye, px, py, gtile;
+        const bool in_img = map_work(P, k, eye, px, py, gtile);
+        if (in_img) {
+            cnt.add(CNT_PIXELS);
+            const float sx = fmaf(2.0f * (px + 0.5f), 1.0f / P.W, -1.0f) * P.cam.tha;
+            const float sy = fmaf(-2.0f * (py + 0.5f), 1.0f / P.H, 1.0f) * P.cam.th;
+            const float3 o = P.cam.eye[eye];
+            const float3 d = normalize(P.cam.f + P.cam.r * (sx + P.cam.sigma[eye]) + P.cam.u * sy);
+            int pid = -1;
+            const float3 c = trace_pixel<COUNT, BRUTE>(P, o, d, pid, cnt);
+            const long long pix = ((long long)eye * P.H + py) * P.W + px;
+            if (P.fb[eye]) store_px(P.fb[eye], P.fb_fmt[eye], P.fb_pitch[eye], px, py, c);
+            if (P.prim_id) P.prim_id[pix] = pid;
+            if (P.radiance) P.radiance[pix] = make_float4(c.x, c.y, c.z, 0.0f);
+            if (P.shard) {
+                const long long s = (long long)(k >> 8) * 256 + ((py % TILE) * TILE + (px % TILE));
+                if (P.shard_fmt == RT_FORMAT_RGBA8) reinterpret_cast<uint32_t*>(P.shard)[s] = pack_rgba8(c);
+                else reinterpret_cast<uint2*>(P.shard)[s] = pack_rgba16f(c);
+            }
+        }
+    }
+    if (COUNT) {
+#pragma unroll
+        for (int i = 0; i < RT_NUM_COUNTERS_INTERNAL; ++i) {
+            uint32_t v = cnt.c[i];
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+            if (lane == 0 && v) atomicAdd(&P.counters[i], (unsigned long long)v);
+        }
+    }
+}
+
+// Root-side tile unpack for the NCCL gather path: shards (rank-major) -> row-major FBs.
+__global__ void k_unpack_shards(const void* __restrict__ gathered, UnpackParams U) {
+    const long long n = (long long)U.world * U.tiles_per_rank * 256;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const int rank = (int)(i / ((long long)U.tiles_per_rank * 256));
+        const long long r = i - (long long)rank * U.tiles_per_rank * 256;
+        const int lt = (int)(r >> 8);
+        const int within = (int)(r & 255);
+        int g;
+        if (U.shard_mode == 0) {
+            g = lt;
+        } else if (U.shard_mode == 1) {
+            const int grp = rank / U.shard_half, j = rank % U.shard_half;
+            if (j + lt * U.shard_half >= U.tiles_per_eye) continue;
+            g = grp * U.tiles_per_eye + j + lt * U.shard_half;
+        } else {
+            g = rank + lt * U.world;
+            if (g >= 2 * U.tiles_per_eye) continue;
+        }
+        if (U.shard_mode == 0 && g >= 2 * U.tiles_per_eye) continue;
+        const int eye = g / U.tiles_per_eye;
+        const int t = g - eye * U.tiles_per_eye;
+        const int px = (t % U.tiles_x) * TILE + (within % TILE);
+        const int py = (t / U.tiles_x) * TILE + (within / TILE);
+        if (px >= U.W || py >= U.H) continue;
+        char* dst = static_cast<char*>(eye ? U.right : U.left);
+        if (!dst) continue;
+        dst += (long long)py * U.pitch;
+        if (U.fmt == RT_FORMAT_RGBA8)
+            reinterpret_cast<uint32_t*>(dst)[px] = reinterpret_cast<const uint32_t*>(gathered)[i];
+        else
+            reinterpret_cast<uint2*>(dst)[px] = reinterpret_cast<const uint2*>(gathered)[i];
+    }
+}
+
+// FFMA peak microbenchmark: 8 independent FMA chains per thread.
+__global__ void __launch_bounds__(256) k_ffma_peak(float* out, int iters, float a, float b) {
+    float x0 = threadIdx.x, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3, x4 = x0 + 4, x5 = x0 + 5, x6 = x0 + 6, x7 = x0 + 7;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            x0 = fmaf(x0, a, b); x1 = fmaf(x1, a, b); x2 = fmaf(x2, a, b); x3 = fmaf(x3, a, b);
+            x4 = fmaf(x4, a, b); x5 = fmaf(x5, a, b); x6 = fmaf(x6, a, b); x7 = fmaf(x7, a, b);
+        }
+    }
+    const float s = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+    if (s == 1234.5f) out[0] = s;
+}
+
+}  // namespace rtb
+
+// ------------------------------------------------------------------ launchers
+using namespace rtb;
+
+cudaError_t rtb_launch_trace(const TraceParams& P, unsigned flags, int grid, cudaStream_t st) {
+    const bool count = flags & RT_RENDER_COUNT, brute = flags & RT_RENDER_BRUTE_FORCE;
+    if (count && brute) k_trace_stereo<true, true><<<grid, 256, 0, st>>>(P);
+    else if (count) k_trace_stereo<true, false><<<grid, 256, 0, st>>>(P);
+    else if (brute) k_trace_stereo<false, true><<<grid, 256, 0, st>>>(P);
+    else k_trace_stereo<false, false><<<grid, 256, 0, st>>>(P);
+    return cudaGetLastError();
+}
+
+cudaError_t rtb_trace_occupancy(unsigned flags, int* blocks_per_sm) {
+    const bool count = flags & RT_RENDER_COUNT, brute = flags & RT_RENDER_BRUTE_FORCE;
+    const void* f = count ? (brute ? (const void*)k_trace_stereo<true, true> : (const void*)k_trace_stereo<true, false>)
+                          : (brute ? (const void*)k_trace_stereo<false, true> : (const void*)k_trace_stereo<false, false>);
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, f, 256, 0);
+}
+
+cudaError_t rtb_launch_unpack(const void* gathered, const UnpackParams& U, cudaStream_t st) {
+    k_unpack_shards<<<148 * 8, 256, 0, st>>>(gathered, U);
+    return cudaGetLastError();
+}
+
+cudaError_t rtb_launch_ffma(float* out, int iters, int grid, cudaStream_t st) {
+    k_ffma_peak<<<grid, 256, 0, st>>>(out, iters, 1.0000001f, 1e-7f);
+    return cudaGetLastError();
+}

@@ -1,0 +1,111 @@
+"""CPU-side checks of the C-ABI library: it loads, exports every symbol include/rt_b200.h
+declares, and its pure host logic (shard map, host unpack) is correct.  No GPU needed."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+from paper_1702_01530_b200 import rt
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_symbols():
+    src = open(os.path.join(ROOT, "include", "rt_b200.h")).read()
+    return sorted(set(re.findall(r"^\s*(?:rt_status|int|const char\*)\s+(rt_\w+)\s*\(", src, re.M)))
+
+
+def test_library_exports_every_declared_symbol():
+    syms = header_symbols()
+    assert len(syms) >= 20
+    assert sorted(rt.EXPORTED) == syms
+    L = rt.lib()
+    for name in syms:
+        assert getattr(L, name) is not None
+    assert rt.rt_version() == 1
+
+
+def test_library_is_sm100a_only():
+    """The fatbin carries sm_100a SASS only (no PTX / other-arch fallback)."""
+    import subprocess
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", rt.LIB_PATH], capture_output=True, text=True)
+    assert out.returncode == 0, out.stderr
+    arches = set(re.findall(r"sm_(\d+a?)", out.stdout))
+    assert arches == {"100a"}, out.stdout
+    ptx = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-ptx", rt.LIB_PATH], capture_output=True, text=True)
+    assert ".ptx" not in ptx.stdout
+
+
+def test_create_without_device_fails_cleanly():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("has a device")
+    with pytest.raises(rt.RtError):
+        rt.rt_create(0)
+    assert rt.rt_last_error() != ""
+
+
+@pytest.mark.parametrize("W,H", [(64, 48), (67, 45), (1920, 1080), (17, 1), (1, 1), (33, 200)])
+@pytest.mark.parametrize("world", [1, 2, 3, 4, 5, 8])
+def test_shard_map_exact_cover(W, H, world):
+    """PAPER.md:48 'dividing the picture to N identical parts': every tile of both eyes is
+    owned by exactly one rank; world 2 is the level-1 eye split."""
+    tx, ty = -(-W // 16), -(-H // 16)
+    T = tx * ty
+    owners = np.full(2 * T, -1)
+    counts = []
+    for r in range(world):
+        ids = rt.rt_shard_tiles(W, H, r, world)
+        assert np.all(np.diff(ids.astype(np.int64)) > 0)
+        assert np.all(owners[ids] == -1)
+        owners[ids] = r
+        counts.append(len(ids))
+    assert np.all(owners >= 0)
+    assert max(counts) - min(counts) <= 1 or T < world
+    if world == 2:
+        assert np.all(owners[:T] == 0) and np.all(owners[T:] == 1)
+    per = rt.rt_shard_bytes(W, H, world)
+    assert per == max(counts) * 256 * 4
+    assert rt.rt_shard_bytes(W, H, world, rt.RT_FORMAT_RGBA16F) == 2 * per
+
+
+def synth_shards(W, H, world):
+    """Each rank fills its packed shard with a code of (eye, px, py) using only the shard map."""
+    per = rt.rt_shard_bytes(W, H, world) // 4
+    tx = -(-W // 16)
+    T = tx * -(-H // 16)
+    buf = np.zeros((world, per), np.uint32)
+    for r in range(world):
+        for lt, g in enumerate(rt.rt_shard_tiles(W, H, r, world)):
+            eye, t = divmod(int(g), T)
+            w = np.arange(256)
+            px = (t % tx) * 16 + w % 16
+            py = (t // tx) * 16 + w // 16
+            buf[r, lt * 256:(lt + 1) * 256] = (eye << 30) | (py << 15) | px
+    return buf
+
+
+def expected_image(W, H):
+    py, px = np.mgrid[0:H, 0:W]
+    return np.stack([(e << 30) | (py << 15) | px for e in (0, 1)]).astype(np.uint32)
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 4, 8])
+def test_host_unpack_roundtrip(world):
+    W, H = 93, 61
+    g = synth_shards(W, H, world)
+    L, R = rt.rt_unpack_shards_host(g.view(np.uint8).reshape(-1), W, H, world)
+    got = np.stack([L, R]).view(np.uint32)[..., 0]
+    np.testing.assert_array_equal(got, expected_image(W, H))
+
+
+def test_product_package_never_touches_the_oracle():
+    """The product path must not import/link/execute oracle/ (it is test infrastructure)."""
+    pkg = os.path.join(ROOT, "paper_1702_01530_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")) or f == "Makefile":
+                txt = open(os.path.join(dirpath, f)).read()
+                assert not re.search(r"(import\s+oracle|from\s+oracle|liboracle|whitted_oracle|oracle\.py)", txt), \
+                    os.path.join(dirpath, f)

@@ -1,0 +1,294 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle on the same seeded scenes.
+
+Sizes: full frames the oracle finishes in seconds spanning several 16x16 tiles plus a ragged
+tail, and sampled pixels of the full BASELINE.json configurations C4/C5 rendered in the exact
+launch configuration bench.py times.  Criteria in tests/parity.py (north star).
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle.oracle import Oracle  # noqa: E402
+from paper_1702_01530_b200 import rt, scenes  # noqa: E402
+from paper_1702_01530_b200.scenes import Rig  # noqa: E402
+from tests.parity import assert_parity, compare  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def R():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    r = rt.StereoRenderer(0)
+    yield r
+    r.close()
+
+
+def gpu_render(R, s, **kw):
+    R.upload(s)
+    R.set_camera(s.rig)
+    out = R.render(s.width, s.height, s.max_depth, want_id=True, want_radiance=True, **kw)
+    torch.cuda.synchronize()
+    return {k: (v.cpu().numpy() if hasattr(v, "cpu") else v) for k, v in out.items()}
+
+
+def full_parity(R, s, label):
+    g = gpu_render(R, s)
+    ref = Oracle(s).render()
+    st = compare(ref, g["id"], g["fb"], g["radiance"], label)
+    print(st)
+    assert_parity(st)
+    return g, ref
+
+
+def test_c1_full(R):
+    full_parity(R, scenes.scene_c1(), "C1 64x48 d1")
+
+
+def test_c1_ragged(R):
+    full_parity(R, scenes.scene_c1().with_view(width=67, height=45, max_depth=3), "C1 67x45 d3")
+
+
+def test_c2_small(R):
+    full_parity(R, scenes.scene_c2().with_view(width=100, height=75), "C2 100x75 d5")
+
+
+def test_c3_small(R):
+    full_parity(R, scenes.scene_c3().with_view(width=96, height=54), "C3 96x54 d4")
+
+
+def test_paper_scene6(R):
+    full_parity(R, scenes.paper_scene(6).with_view(width=70, height=50), "paper6 70x50 d3")
+
+
+def test_depth_extremes(R):
+    s = scenes.scene_c2().with_view(width=50, height=37, max_depth=0)
+    full_parity(R, s, "C2 d0")
+    full_parity(R, s.with_view(max_depth=16), "C2 d16")
+
+
+def test_degenerate_scenes(R):
+    """Empty scene (background only), planes only, a lone sphere (1-prim BVH), a lone triangle."""
+    base = scenes.scene_c1().with_view(width=33, height=17)
+    e = base.with_view()
+    e.spheres, e.sphere_mat = np.zeros((0, 4)), np.zeros(0, np.uint32)
+    e.planes, e.plane_mat = np.zeros((0, 4)), np.zeros(0, np.uint32)
+    full_parity(R, e.finalize(), "empty")
+    p = base.with_view()
+    p.spheres, p.sphere_mat = np.zeros((0, 4)), np.zeros(0, np.uint32)
+    full_parity(R, p.finalize(), "plane only")
+    one = base.with_view()
+    one.spheres, one.sphere_mat = base.spheres[:1], base.sphere_mat[:1]
+    full_parity(R, one.finalize(), "one sphere + plane")
+    t = base.with_view()
+    t.spheres, t.sphere_mat = np.zeros((0, 4)), np.zeros(0, np.uint32)
+    t.vertices = np.array([[-2.0, 0.5, 0], [2.0, 0.5, 0], [0.0, 2.5, -1]])
+    t.tris = np.array([[0, 1, 2]], np.uint32)
+    t.tri_mat = np.array([1], np.uint32)
+    full_parity(R, t.finalize(), "one triangle + plane")
+
+
+def sampled_parity(R, s, n_per_eye, seed, label):
+    """Full-size frame in bench's launch configuration; the oracle evaluates sampled pixels."""
+    g = gpu_render(R, s)
+    pix = scenes.sample_pixels(s.width, s.height, n_per_eye, seed)
+    ref = Oracle(s).render(pixels=pix)
+    e, x, y = pix[:, 0], pix[:, 1], pix[:, 2]
+    st = compare(ref, g["id"][e, y, x], g["fb"][e, y, x], g["radiance"][e, y, x], label)
+    print(st)
+    assert_parity(st)
+
+
+def test_c3_full_sampled(R):
+    sampled_parity(R, scenes.scene_c3(), 400, 11, "C3 1080p sampled")
+
+
+@pytest.mark.slow
+def test_c4_full_sampled(R):
+    sampled_parity(R, scenes.scene_c4(), 48, 12, "C4 1080p sampled")
+
+
+@pytest.mark.slow
+def test_c5_frames_sampled(R):
+    for f in (0, 30):
+        sampled_parity(R, scenes.scene_c5(frame=f), 16, 13 + f, f"C5 4K frame {f} sampled")
+
+
+def test_bvh_equals_bruteforce(R):
+    """GPU LBVH traversal == GPU brute force (same FP32 intersectors), bit-exact
+    (SPEC.md:303 oracle equivalence moved to the GPU)."""
+    for s in (scenes.scene_c3().with_view(width=160, height=90), scenes.paper_scene(6).with_view(width=64, height=64),
+              scenes.scene_c2().with_view(width=80, height=60)):
+        a = gpu_render(R, s)
+        b = gpu_render(R, s, brute=True)
+        np.testing.assert_array_equal(a["id"], b["id"])
+        np.testing.assert_array_equal(a["radiance"].view(np.uint32), b["radiance"].view(np.uint32))
+        np.testing.assert_array_equal(a["fb"], b["fb"])
+
+
+def test_determinism_and_counters(R):
+    """S:225 determinism; ray counters by type agree with the oracle's counts."""
+    s = scenes.scene_c2().with_view(width=64, height=48)
+    a = gpu_render(R, s, count=True)
+    b = gpu_render(R, s)
+    np.testing.assert_array_equal(a["fb"], b["fb"])
+    np.testing.assert_array_equal(a["radiance"].view(np.uint32), b["radiance"].view(np.uint32))
+    c = R.counters_dict(torch.from_numpy(a["counters"]))
+    ref = Oracle(s).render(flags=False)
+    oc = dict(zip(["primary", "reflection", "refraction", "shadow"], ref["counts"]))
+    assert c["primary"] == oc["primary"] == 2 * 64 * 48
+    assert c["pixels"] == 2 * 64 * 48
+    for k in ("reflection", "refraction", "shadow"):
+        assert abs(c[k] - oc[k]) <= max(3, 0.002 * oc[k]), (k, c[k], oc[k])
+
+
+def test_rgba16f_pack(R):
+    """RGBA16F = binary16 RNE of the clamped radiance (numpy float16 of the GPU's own FP32)."""
+    s = scenes.scene_c1().with_view(width=40, height=30)
+    g = gpu_render(R, s, fmt=rt.RT_FORMAT_RGBA16F)
+    exp = np.clip(g["radiance"][..., :3], 0, 1).astype(np.float16)
+    np.testing.assert_array_equal(g["fb"][..., :3].view(np.uint16), exp.view(np.uint16))
+    assert np.all(g["fb"][..., 3] == 1.0)
+    ref = Oracle(s).render()
+    d = np.abs(g["fb"][..., :3].astype(np.float64) - ref["rgba16"][..., :3].view(np.float16).astype(np.float64))
+    assert d[ref["tflags"] == 0].max() <= 1e-3 + 2 ** -11
+
+
+def test_rgba8_pack_formula(R):
+    """S:494 quantisation of the GPU's own radiance."""
+    s = scenes.scene_c2().with_view(width=48, height=32)
+    g = gpu_render(R, s)
+    exp = np.floor(np.clip(g["radiance"][..., :3].astype(np.float64), 0, 1) * 255 + 0.5)
+    assert np.abs(g["fb"][..., :3] - exp).max() <= 1      # fp32 fma rounding at .5 boundaries
+    assert (g["fb"][..., :3] == exp).mean() > 0.999
+    assert np.all(g["fb"][..., 3] == 255)
+
+
+@pytest.mark.parametrize("world", [2, 3, 4, 8])
+def test_virtual_shards_bit_exact(R, world):
+    """Gathered R-shard image == 1-GPU image, bit-exact: each rank's tile set is
+    rendered on this GPU into its packed shard, then unpacked on the device."""
+    s = scenes.scene_c2().with_view(width=93, height=61, max_depth=3)
+    full = gpu_render(R, s)["fb"]
+    per = rt.rt_shard_bytes(s.width, s.height, world)
+    gathered = torch.zeros(world * per, dtype=torch.uint8, device="cuda")
+    for r in range(world):
+        R.render(s.width, s.height, s.max_depth, fb=False, shard=(r, world), shard_buf=gathered[r * per:(r + 1) * per])
+    fb = torch.zeros((2, s.height, s.width, 4), dtype=torch.uint8, device="cuda")
+    pitch = s.width * 4
+    rt.rt_unpack_shards(R.ctx, gathered.data_ptr(), s.width, s.height, world, rt.RT_FORMAT_RGBA8,
+                        rt.rt_fb(fb[0].data_ptr(), 0, pitch), rt.rt_fb(fb[1].data_ptr(), 0, pitch))
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(fb.cpu().numpy(), full)
+    # host-side unpack agrees with the device unpack
+    L, Rr = rt.rt_unpack_shards_host(gathered.cpu().numpy(), s.width, s.height, world)
+    np.testing.assert_array_equal(np.stack([L, Rr]), full)
+
+
+def test_shard_writes_only_its_tiles(R):
+    """S:483 channel independence: the right channel rendered alone (eye-split shard 1 of 2)
+    equals the right channel of the stereo render, bit-exact; the left FB is untouched."""
+    s = scenes.scene_c1().with_view(width=50, height=40)
+    full = gpu_render(R, s)["fb"]
+    fb = torch.zeros((2, s.height, s.width, 4), dtype=torch.uint8, device="cuda")
+    R.render(s.width, s.height, s.max_depth, fb=fb, shard=(1, 2))           # right eye only
+    torch.cuda.synchronize()
+    f = fb.cpu().numpy()
+    assert np.all(f[0] == 0)
+    np.testing.assert_array_equal(f[1], full[1])
+
+
+def test_download_pinned(R):
+    """rt_download (PAPER.md:15 transfer stage): async D2H into pinned memory == device FB."""
+    s = scenes.scene_c1()
+    R.upload(s)
+    R.set_camera(s.rig)
+    out = R.render(s.width, s.height, s.max_depth)
+    nbytes = out["fb"].numel()
+    host = rt.rt_host_alloc(nbytes)
+    try:
+        ev = rt.rt_download(R.ctx, out["fb"].data_ptr(), host, nbytes)
+        rt.rt_wait(ev)
+        import ctypes
+        got = np.frombuffer((ctypes.c_uint8 * nbytes).from_address(host), np.uint8).copy()
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(got, out["fb"].cpu().numpy().reshape(-1))
+        # unpinned destination is rejected
+        buf = np.zeros(nbytes, np.uint8)
+        with pytest.raises(rt.RtError):
+            rt.rt_download(R.ctx, out["fb"].data_ptr(), buf.ctypes.data, nbytes)
+    finally:
+        rt.rt_host_free(host)
+
+
+def test_validation_errors(R):
+    s = scenes.scene_c1()
+    bad = s.with_view()
+    bad.spheres = s.spheres.copy()
+    bad.spheres[0, 3] = -1.0
+    with pytest.raises(rt.RtError) as e:
+        R.upload(bad)
+    assert e.value.status == rt.RT_ERR_INVALID_ARG
+    t = scenes.paper_scene(1)
+    t.tris = t.tris.copy()
+    t.tris[0, 0] = 10_000
+    with pytest.raises(rt.RtError):
+        R.upload(t)
+    t = scenes.paper_scene(1)
+    t.materials = t.materials.copy()
+    t.materials[0, 7] = 0.9
+    t.materials[0, 8] = 0.5           # kr + kt > 1
+    with pytest.raises(rt.RtError):
+        R.upload(t)
+    R.upload(s)
+    with pytest.raises(rt.RtError):
+        rt.rt_set_stereo_camera(R.ctx, [0, 0, 0], [0, 0, 0], [0, 1, 0], 40, 0.06, 5)
+    with pytest.raises(rt.RtError):
+        rt.rt_set_stereo_camera(R.ctx, [0, 0, 0], [0, 1, 0], [0, 1, 0], 40, 0.06, 5)
+    with pytest.raises(rt.RtError):
+        rt.rt_set_stereo_camera(R.ctx, [0, 0, 5], [0, 0, 0], [0, 1, 0], 180, 0.06, 5)
+    R.set_camera(s.rig)
+    with pytest.raises(rt.RtError) as e:
+        R.render(0, 10, 1)
+    assert e.value.status == rt.RT_ERR_SIZE
+    with pytest.raises(rt.RtError):
+        R.render(10, 10, 17)
+    ctx = rt.rt_create(0)
+    try:
+        with pytest.raises(rt.RtError) as e:
+            rt.rt_render_stereo(ctx, 8, 8, 1, rt.rt_fb(), rt.rt_fb())
+        assert e.value.status == rt.RT_ERR_NO_SCENE
+    finally:
+        rt.rt_destroy(ctx)
+
+
+def test_bvh_structure(R):
+    """SPEC.md:259-262 / :305: every primitive in exactly one leaf, parents contain children,
+    depth bounded."""
+    s = scenes.scene_c3()
+    info = R.upload(s)
+    nodes, gids = rt.rt_bvh_export(R.ctx)
+    n = s.n_spheres + s.n_tris
+    assert info["bvh_prims"] == n and info["bvh_nodes"] == n - 1
+    assert sorted(gids.tolist()) == list(range(s.n_spheres)) + list(range(s.n_spheres + s.n_planes, s.n_spheres + s.n_planes + s.n_tris))
+    assert info["bvh_depth"] <= 64
+    child = nodes[:, 12:14].view(np.int32)
+    seen_leaf = np.zeros(n, int)
+    seen_int = np.zeros(n - 1, int)
+    for c in child.reshape(-1):
+        if c < 0:
+            seen_leaf[(~c) & 0xFFFFFF] += 1
+        else:
+            seen_int[c] += 1
+    assert np.all(seen_leaf == 1) and seen_int[0] == 0 and np.all(seen_int[1:] == 1)
+    # each child box stored in a node contains the union of that child's own two boxes
+    LO = ([0, 2, 8], [4, 6, 10])
+    HI = ([1, 3, 9], [5, 7, 11])
+    for i in range(n - 1):
+        for side in (0, 1):
+            c = child[i, side]
+            if c >= 0:
+                sub_lo = np.minimum(nodes[c, LO[0]], nodes[c, LO[1]])
+                sub_hi = np.maximum(nodes[c, HI[0]], nodes[c, HI[1]])
+                assert np.all(nodes[i, LO[side]] <= sub_lo) and np.all(nodes[i, HI[side]] >= sub_hi)
