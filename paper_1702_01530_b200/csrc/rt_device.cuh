@@ -139,7 +139,7 @@ __device__ __forceinline__ RayBox make_raybox(float3 o, float3 d, float bound) {
     return rb;
 }
 
-// Returns the entry distance, or +inf when the (inflated) box is missed within [0, tmax].
+// Returns the entry distance (>= 0), or -1 when the (inflated) box is missed within [0, tmax].
 __device__ __forceinline__ float box_enter(const RayBox& rb, float lox, float hix, float loy, float hiy,
                                            float loz, float hiz, float tmax) {
     const float ax = fmaf(lox, rb.idir.x, rb.nlo.x), bx = fmaf(hix, rb.idir.x, rb.nhi.x);
@@ -147,7 +147,7 @@ __device__ __forceinline__ float box_enter(const RayBox& rb, float lox, float hi
     const float az = fmaf(loz, rb.idir.z, rb.nlo.z), bz = fmaf(hiz, rb.idir.z, rb.nhi.z);
     const float tn = fmaxf(fmaxf(fminf(ax, bx), fminf(ay, by)), fmaxf(fminf(az, bz), 0.0f));
     const float tf = fminf(fminf(fmaxf(ax, bx), fmaxf(ay, by)), fminf(fmaxf(az, bz), tmax));
-    return tn <= tf ? tn : __int_as_float(0x7f800000);
+    return tn <= tf ? tn : -1.0f;
 }
 
 }  // namespace rtb

@@ -81,7 +81,7 @@ __device__ __forceinline__ Hit closest_hit(const DevScene& S, float3 o, float3 d
             const int4 n3 = __ldg(reinterpret_cast<const int4*>(&S.nodes[4 * node + 3]));
             const float t0 = box_enter(rb, n0.x, n0.y, n0.z, n0.w, n2.x, n2.y, h.t);
             const float t1 = box_enter(rb, n1.x, n1.y, n1.z, n1.w, n2.z, n2.w, h.t);
-            const bool h0 = t0 <= h.t, h1 = t1 <= h.t;
+            const bool h0 = t0 >= 0.0f, h1 = t1 >= 0.0f;
             if (h0 && h1) {
                 const bool swap = t1 < t0;
                 node = swap ? n3.y : n3.x;
@@ -147,7 +147,7 @@ __device__ __forceinline__ bool occluded(const DevScene& S, float3 o, float3 d, 
             const int4 n3 = __ldg(reinterpret_cast<const int4*>(&S.nodes[4 * node + 3]));
             const float t0 = box_enter(rb, n0.x, n0.y, n0.z, n0.w, n2.x, n2.y, dist);
             const float t1 = box_enter(rb, n1.x, n1.y, n1.z, n1.w, n2.z, n2.w, dist);
-            const bool h0 = t0 <= dist, h1 = t1 <= dist;
+            const bool h0 = t0 >= 0.0f, h1 = t1 >= 0.0f;
             if (h0 && h1) {
                 node = n3.x;
                 stack[sp++] = n3.y;

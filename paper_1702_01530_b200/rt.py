@@ -316,7 +316,9 @@ class StereoRenderer:
         if stream is None:
             stream = torch.cuda.current_stream(self.device)
         self.stream = stream
-        self.ctx = rt_create(device, stream.cuda_stream)
+        # torch's default stream has handle 0; pass cudaStreamLegacy (0x1) so the library
+        # enqueues on that same stream instead of creating its own (NULL) one.
+        self.ctx = rt_create(device, stream.cuda_stream or 1)
         self._counters = torch.zeros(RT_NUM_COUNTERS, dtype=torch.int64, device=self.device)
         self.scene = None
 
