@@ -55,6 +55,13 @@ def workload_desc(s):
             f"{s.n_planes} planes via LBVH, {len(s.lights)} point lights, depth {s.max_depth}")
 
 
+def gather_to_root(dist, shard_buf, gathered, world, rank, per):
+    """a7: every rank's packed tile shard -> rank 0's `gathered` buffer (rank-major), one
+    collective (NCCL ncclSend/Recv over NVLink on GPUs; gloo in the CPU tests)."""
+    glist = [gathered[r * per:(r + 1) * per] for r in range(world)] if rank == 0 else None
+    dist.gather(shard_buf, glist, dst=0)
+
+
 # ------------------------------------------------------------------------------ clocks
 class ClockSampler:
     """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed region."""
@@ -216,8 +223,7 @@ def run_ours(args, scene):
             R.render(W, H, D, fb=fb)
         else:
             R.render(W, H, D, fb=False, shard=shard, shard_buf=shard_buf)
-            glist = [gathered[r * per:(r + 1) * per] for r in range(world)] if rank == 0 else None
-            dist.gather(shard_buf, glist, dst=0)
+            gather_to_root(dist, shard_buf, gathered, world, rank, per)
             if rank == 0:
                 rt.rt_unpack_shards(R.ctx, gathered.data_ptr(), W, H, world, rt.RT_FORMAT_RGBA8,
                                     rt.rt_fb(fb[0].data_ptr(), 0, pitch), rt.rt_fb(fb[1].data_ptr(), 0, pitch))
@@ -243,8 +249,7 @@ def run_ours(args, scene):
         else:
             R.render(W, H, D, fb=False, shard=shard, shard_buf=shard_buf)
             ev_k[k].record()
-            glist = [gathered[r * per:(r + 1) * per] for r in range(world)] if rank == 0 else None
-            dist.gather(shard_buf, glist, dst=0)
+            gather_to_root(dist, shard_buf, gathered, world, rank, per)
             if rank == 0:
                 rt.rt_unpack_shards(R.ctx, gathered.data_ptr(), W, H, world, rt.RT_FORMAT_RGBA8,
                                     rt.rt_fb(fb[0].data_ptr(), 0, pitch), rt.rt_fb(fb[1].data_ptr(), 0, pitch))
@@ -343,8 +348,7 @@ def run_e2e(args, R, scene, rank, world, shard, per, dev, rays_total):
             rt.rt_render_stereo(R.ctx, W, H, D, rt.rt_fb(fb[0].data_ptr(), 0, pitch), rt.rt_fb(fb[1].data_ptr(), 0, pitch))
         else:
             R.render(W, H, D, fb=False, shard=shard, shard_buf=shard_buf)
-            glist = [gathered[r * per:(r + 1) * per] for r in range(world)] if rank == 0 else None
-            dist.gather(shard_buf, glist, dst=0)
+            gather_to_root(dist, shard_buf, gathered, world, rank, per)
             if rank == 0:
                 rt.rt_unpack_shards(R.ctx, gathered.data_ptr(), W, H, world, rt.RT_FORMAT_RGBA8,
                                     rt.rt_fb(fb[0].data_ptr(), 0, pitch), rt.rt_fb(fb[1].data_ptr(), 0, pitch))

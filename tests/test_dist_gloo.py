@@ -1,0 +1,79 @@
+"""World-size-2 CPU tests (gloo) of the multi-GPU host logic: shard map -> per-rank packed
+shards -> bench.gather_to_root -> root unpack == the full image; max-over-ranks timing;
+and the reference arm under a 2-process launch (rank 1 exits without work)."""
+import os
+import socket
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, W, H, q):
+    sys.path.insert(0, ROOT)
+    import bench
+    from paper_1702_01530_b200 import rt
+    from tests.test_abi import expected_image, synth_shards
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    per = rt.rt_shard_bytes(W, H, world)
+    mine = synth_shards(W, H, world)[rank].view(np.uint8)
+    shard = torch.from_numpy(mine.copy())
+    gathered = torch.zeros(world * per, dtype=torch.uint8) if rank == 0 else None
+    bench.gather_to_root(dist, shard, gathered, world, rank, per)
+    t = torch.tensor([1.0 + rank], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ok = float(t[0]) == float(world)
+    if rank == 0:
+        L, R = rt.rt_unpack_shards_host(gathered.numpy(), W, H, world)
+        got = np.stack([L, R]).view(np.uint32)[..., 0]
+        ok = ok and np.array_equal(got, expected_image(W, H))
+        q.put(ok)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("W,H", [(93, 61), (64, 48)])
+def test_gloo_world2_gather_unpack(W, H):
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, W, H, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    assert q.get(timeout=10) is True
+
+
+def test_reference_arm_under_torchrun():
+    """`bench.py --impl reference` launched like the driver's N=2 run: rank 0 prints one JSON
+    line with impl=reference, rank 1 exits 0 without work."""
+    port = _free_port()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
+           "--impl", "reference", "--gpus", "2", "--steps", "1", "--warmup", "0", "--config", "C1"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    import json
+    lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1
+    ln = lines[0]
+    assert ln["impl"] == "reference" and ln["n_gpus"] == 2 and ln["value"] > 0
+    assert ln["e2e"]["h2d_bytes_per_step"] == 0 and ln["cpu_baseline"]["kind"] == "oracle"
