@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -77,6 +78,7 @@ struct rt_context {
     bool has_camera = false;
     double cam_eye[2][3], cam_f[3], cam_r[3], cam_u[3], cam_th, cam_sigma_unit;
     float vfov = 0;
+    int refill = 8;          // traversal-loop refill threshold (env RT_REFILL, tuning knob)
 };
 
 namespace {
@@ -120,6 +122,7 @@ rt_status rt_create(int device, void* cuda_stream, rt_context** out) {
     rt_context* c = new (std::nothrow) rt_context();
     if (!c) return fail(RT_ERR_OOM, "rt_create: host allocation");
     c->device = device;
+    if (const char* r = getenv("RT_REFILL")) c->refill = std::max(1, std::min(32, atoi(r)));
     cudaError_t e = cudaSetDevice(device);
     if (e == cudaSuccess && cuda_stream) {
         c->stream = static_cast<cudaStream_t>(cuda_stream);
@@ -531,10 +534,12 @@ rt_status rt_render_stereo_ex(rt_context* c, const rt_render_params* p, const rt
     P.shard = out->shard;
     P.shard_fmt = (int)out->shard_format;
     P.counters = out->counters ? out->counters : c->scratch_counters;
+    P.stack_entries = std::max(1, (int)c->info[5] + 1);
+    P.refill = c->refill;
     if (P.n_work == 0) return RT_OK;
     CUDA_TRY(cudaSetDevice(c->device));
     int occ = 0;
-    CUDA_TRY(rtb_trace_occupancy(p->flags, &occ));
+    CUDA_TRY(rtb_trace_occupancy(p->flags, P.stack_entries, &occ));
     if (occ < 1) occ = 1;
     const long long max_blocks = ((long long)P.n_work + 255) / 256;
     const int grid = (int)std::min<long long>((long long)c->num_sms * occ, std::max<long long>(1, max_blocks));

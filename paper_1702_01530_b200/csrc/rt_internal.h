@@ -39,6 +39,8 @@ struct TraceParams {
     void* shard;
     int shard_fmt;
     unsigned long long* counters;
+    int stack_entries;      // BVH traversal stack depth (shared memory, [entry][thread])
+    int refill;             // leave the traversal loop when this many lanes of a warp are idle
 };
 
 struct UnpackParams {
@@ -82,7 +84,8 @@ struct BuildBuffers {
 
 // launchers (rt_trace.cu)
 cudaError_t rtb_launch_trace(const TraceParams& P, unsigned flags, int grid, cudaStream_t st);
-cudaError_t rtb_trace_occupancy(unsigned flags, int* blocks_per_sm);
+cudaError_t rtb_trace_occupancy(unsigned flags, int stack_entries, int* blocks_per_sm);
+size_t rtb_trace_smem(int stack_entries);
 cudaError_t rtb_launch_unpack(const void* gathered, const UnpackParams& U, cudaStream_t st);
 cudaError_t rtb_launch_ffma(float* out, int iters, int grid, cudaStream_t st);
 // launchers (rt_build.cu)

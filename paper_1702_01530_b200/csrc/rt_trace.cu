@@ -3,16 +3,20 @@
 // ray, finds nearest hits through the LBVH (+ linear planes), shades with Phong + shadow rays
 // per light, follows reflection/refraction with an iterative per-thread ray stack up to
 // max_depth bounces, and packs the clamped radiance straight into the RGBA8/FP16 framebuffers
-// (and, optionally, prim-ID / radiance debug planes, a tile-packed shard, or a peer rank's
-// framebuffer over NVLink).  SURVEY.md §8(a) rows a3-a6; DESIGN.md §5.
+// (and, optionally, prim-ID / radiance debug planes or a tile-packed shard).
+// SURVEY.md §8(a) rows a3-a6; DESIGN.md §5.
+//
+// Execution model (v1): every lane runs a small state machine over ITS OWN pixel's ray tree
+// (tree ray -> one shadow ray per lit light -> reflection / refraction children), and all ray
+// kinds share ONE traversal loop.  When a lane's ray finishes it advances its state machine
+// (producing the next ray of its tree, or finishing the pixel and taking a new one from the
+// work queue with a warp-aggregated atomic), so the warp keeps ~all lanes traversing instead
+// of waiting for the longest ray tree (the v0 kernel averaged 8 of 32 active lanes).  The
+// BVH traversal stack lives in shared memory, [entry][thread], conflict-free.
 #include "rt_device.cuh"
 #include "rt_internal.h"
 
 namespace rtb {
-
-struct Cnt {
-    unsigned long long v[RT_NUM_COUNTERS_INTERNAL];
-};
 
 template <bool COUNT>
 struct Counters {
@@ -24,155 +28,9 @@ struct Counters {
     __device__ __forceinline__ void add(int i, uint32_t n = 1) { if (COUNT) c[i] += n; }
 };
 
-struct Hit {
-    float t;
-    int gid;    // global primitive ID, -1 = miss
-    int slot;   // BVH prim slot (>= 0) or ~plane index (< 0)
-};
-
-// Nearest hit over the BVH (or every BVH primitive when BRUTE) and the planes.
-// Acceptance: t > t_min and (t, gid) lexicographically smallest (reading 9).
-template <bool COUNT, bool BRUTE>
-__device__ __forceinline__ Hit closest_hit(const DevScene& S, float3 o, float3 d, Counters<COUNT>& cnt) {
-    Hit h;
-    h.t = __int_as_float(0x7f800000);
-    h.gid = -1;
-    h.slot = 0;
-    for (int i = 0; i < S.n_planes; ++i) {
-        cnt.add(CNT_PLANE_TESTS);
-        float t;
-        if (plane_intersect(o, d, S.planes[i], t) && t > T_MIN) {
-            const int gid = S.n_spheres + i;
-            if (t < h.t || (t == h.t && gid < h.gid)) { h.t = t; h.gid = gid; h.slot = ~i; }
-        }
-    }
-    if (S.n_bvh == 0) return h;
-
-    auto test_prim = [&](int k) {
-        const float4 a = __ldg(&S.prims[3 * k]);
-        const int gid = __float_as_int(a.w);
-        float t;
-        bool ok;
-        if (gid < S.n_spheres) {
-            cnt.add(CNT_SPHERE_TESTS);
-            ok = sphere_intersect(o, d, a, __ldg(&S.prims[3 * k + 1]), T_MIN, t);
-        } else {
-            cnt.add(CNT_TRI_TESTS);
-            ok = tri_intersect(o, d, a, __ldg(&S.prims[3 * k + 1]), __ldg(&S.prims[3 * k + 2]), t) && t > T_MIN;
-        }
-        if (ok && (t < h.t || (t == h.t && gid < h.gid))) { h.t = t; h.gid = gid; h.slot = k; }
-    };
-
-    if (BRUTE) {
-        for (int k = 0; k < S.n_bvh; ++k) test_prim(k);
-        return h;
-    }
-
-    const RayBox rb = make_raybox(o, d, S.bound);
-    int stack[BVH_STACK];
-    int sp = 0;
-    int node = S.root;
-    while (true) {
-        while (node >= 0) {
-            cnt.add(CNT_NODE_VISITS);
-            const float4 n0 = __ldg(&S.nodes[4 * node + 0]);
-            const float4 n1 = __ldg(&S.nodes[4 * node + 1]);
-            const float4 n2 = __ldg(&S.nodes[4 * node + 2]);
-            const int4 n3 = __ldg(reinterpret_cast<const int4*>(&S.nodes[4 * node + 3]));
-            const float t0 = box_enter(rb, n0.x, n0.y, n0.z, n0.w, n2.x, n2.y, h.t);
-            const float t1 = box_enter(rb, n1.x, n1.y, n1.z, n1.w, n2.z, n2.w, h.t);
-            const bool h0 = t0 >= 0.0f, h1 = t1 >= 0.0f;
-            if (h0 && h1) {
-                const bool swap = t1 < t0;
-                node = swap ? n3.y : n3.x;
-                stack[sp++] = swap ? n3.x : n3.y;
-            } else if (h0) {
-                node = n3.x;
-            } else if (h1) {
-                node = n3.y;
-            } else {
-                if (sp == 0) return h;
-                node = stack[--sp];
-            }
-        }
-        // leaf
-        const int enc = ~node;
-        const int first = enc & ((1 << LEAF_SHIFT) - 1);
-        const int count = (enc >> LEAF_SHIFT) + 1;
-        for (int k = first; k < first + count; ++k) test_prim(k);
-        if (sp == 0) return h;
-        node = stack[--sp];
-    }
-}
-
-// Any hit with t_min < t < dist (binary visibility, reading 4).
-template <bool COUNT, bool BRUTE>
-__device__ __forceinline__ bool occluded(const DevScene& S, float3 o, float3 d, float dist, Counters<COUNT>& cnt) {
-    for (int i = 0; i < S.n_planes; ++i) {
-        cnt.add(CNT_PLANE_TESTS);
-        float t;
-        if (plane_intersect(o, d, S.planes[i], t) && t > T_MIN && t < dist) return true;
-    }
-    if (S.n_bvh == 0) return false;
-
-    auto test_prim = [&](int k) -> bool {
-        const float4 a = __ldg(&S.prims[3 * k]);
-        const int gid = __float_as_int(a.w);
-        float t;
-        if (gid < S.n_spheres) {
-            cnt.add(CNT_SPHERE_TESTS);
-            return sphere_intersect(o, d, a, __ldg(&S.prims[3 * k + 1]), T_MIN, t) && t < dist;
-        }
-        cnt.add(CNT_TRI_TESTS);
-        return tri_intersect(o, d, a, __ldg(&S.prims[3 * k + 1]), __ldg(&S.prims[3 * k + 2]), t) &&
-               t > T_MIN && t < dist;
-    };
-
-    if (BRUTE) {
-        for (int k = 0; k < S.n_bvh; ++k)
-            if (test_prim(k)) return true;
-        return false;
-    }
-
-    const RayBox rb = make_raybox(o, d, S.bound);
-    int stack[BVH_STACK];
-    int sp = 0;
-    int node = S.root;
-    while (true) {
-        while (node >= 0) {
-            cnt.add(CNT_NODE_VISITS);
-            const float4 n0 = __ldg(&S.nodes[4 * node + 0]);
-            const float4 n1 = __ldg(&S.nodes[4 * node + 1]);
-            const float4 n2 = __ldg(&S.nodes[4 * node + 2]);
-            const int4 n3 = __ldg(reinterpret_cast<const int4*>(&S.nodes[4 * node + 3]));
-            const float t0 = box_enter(rb, n0.x, n0.y, n0.z, n0.w, n2.x, n2.y, dist);
-            const float t1 = box_enter(rb, n1.x, n1.y, n1.z, n1.w, n2.z, n2.w, dist);
-            const bool h0 = t0 >= 0.0f, h1 = t1 >= 0.0f;
-            if (h0 && h1) {
-                node = n3.x;
-                stack[sp++] = n3.y;
-            } else if (h0) {
-                node = n3.x;
-            } else if (h1) {
-                node = n3.y;
-            } else {
-                if (sp == 0) return false;
-                node = stack[--sp];
-            }
-        }
-        const int enc = ~node;
-        const int first = enc & ((1 << LEAF_SHIFT) - 1);
-        const int count = (enc >> LEAF_SHIFT) + 1;
-        for (int k = first; k < first + count; ++k)
-            if (test_prim(k)) return true;
-        if (sp == 0) return false;
-        node = stack[--sp];
-    }
-}
-
-// Work item -> (eye, px, py).  16x16 tiles, each tile = 8 warps of 8x4 pixels so a warp's
-// primary rays are spatially coherent.  Tiles are drawn from this rank's shard.
-__device__ __forceinline__ bool map_work(const TraceParams& P, int k, int& eye, int& px, int& py, int& gtile) {
+// Work item -> (eye, px, py).  16x16 tiles, each tile = 8 warps of 8x4 pixels so consecutive
+// work items are spatially coherent.  Tiles are drawn from this rank's shard.
+__device__ __forceinline__ bool map_work(const TraceParams& P, int k, int& eye, int& px, int& py) {
     const int lt = k >> 8;
     const int within = k & 255;
     int g;
@@ -185,7 +43,6 @@ __device__ __forceinline__ bool map_work(const TraceParams& P, int k, int& eye, 
     } else {
         g = P.shard_rank + lt * P.shard_world;
     }
-    gtile = g;
     eye = g / P.tiles_per_eye;
     const int t = g - eye * P.tiles_per_eye;
     const int tx = t % P.tiles_x, ty = t / P.tiles_x;
@@ -216,156 +73,340 @@ __device__ __forceinline__ void store_px(void* base, int fmt, long long pitch, i
     else reinterpret_cast<uint2*>(row)[x] = pack_rgba16f(c);
 }
 
-// Trace the whole ray tree of one pixel.  Iterative: the reflection child continues in
-// registers, the refraction child is pushed on a per-thread stack (<= max_depth entries).
-// Radiance accumulates as sum over tree nodes of path_weight * local_term, which equals the
-// recursive definition c = local + kt*T(refr) + kr_eff*T(refl) (reading 17).
-template <bool COUNT, bool BRUTE>
-__device__ float3 trace_pixel(const TraceParams& P, float3 o, float3 d, int& prim_id, Counters<COUNT>& cnt) {
-    const DevScene& S = P.sc;
-    float4 st_a[MAX_DEPTH], st_b[MAX_DEPTH];   // (o, w) (d, depth)
-    int sp = 0;
-    float w = 1.0f;
-    int depth = P.max_depth;
-    bool primary = true;
-    float3 col = f3(0.f, 0.f, 0.f);
-    cnt.add(CNT_PRIMARY);
-    while (true) {
-        const Hit h = closest_hit<COUNT, BRUTE>(S, o, d, cnt);
-        if (primary) { prim_id = h.gid; primary = false; }
-        bool cont = false;
-        if (h.gid < 0) {
-            cnt.add(CNT_MISSES);
-            col = fma3(S.background, w, col);                       // S:203 miss -> background
-        } else {
-            cnt.add(CNT_SHADE_HITS);
-            const float3 p = fma3(d, h.t, o);
-            float3 ng;
-            int mat;
-            if (h.slot < 0) {
-                const int i = ~h.slot;
-                ng = xyz(S.planes[i]);
-                mat = S.plane_mat[i];
-            } else {
-                const float4 a = __ldg(&S.prims[3 * h.slot]);
-                const float4 b = __ldg(&S.prims[3 * h.slot + 1]);
-                mat = __float_as_int(b.w);
-                if (h.gid < S.n_spheres) {
-                    ng = (p - xyz(a)) * (1.0f / b.x);
-                } else {
-                    const float4 c = __ldg(&S.prims[3 * h.slot + 2]);
-                    ng = normalize(cross(xyz(b), xyz(c)));
-                }
-            }
-            const bool front = dot(d, ng) < 0.0f;
-            const float3 nf = front ? ng : ng * -1.0f;               // S:150 faces the ray
-            const float4 m0 = __ldg(&S.mats[3 * mat]), m1 = __ldg(&S.mats[3 * mat + 1]);
-            const float4 m2 = __ldg(&S.mats[3 * mat + 2]);
-            const float3 kd = xyz(m0), ks = xyz(m1);
-            float3 c = S.ambient * kd;                               // S:193 ambient * kd
-            for (int j = 0; j < S.n_lights; ++j) {
-                cnt.add(CNT_LIGHT_EVALS);
-                const float3 Lp = xyz(__ldg(&S.lights[2 * j]));
-                const float3 l = normalize(Lp - p);
-                const float ndl = dot(nf, l);
-                if (ndl <= 0.0f) continue;                           // reading 2 gate
-                const float3 os = fma3(nf, BIAS, p);
-                const float3 sv = Lp - os;
-                const float dist = sqrtf(dot(sv, sv));
-                const float3 sd = sv * (1.0f / dist);
-                cnt.add(CNT_SHADOW);
-                if (occluded<COUNT, BRUTE>(S, os, sd, dist, cnt)) continue;
-                const float3 I = xyz(__ldg(&S.lights[2 * j + 1]));
-                const float3 rv = nf * (2.0f * ndl) - l;
-                const float rdv = -dot(rv, d);
-                const float spec = rdv > 0.0f ? __powf(rdv, m0.w) : 0.0f;
-                c = c + (kd * I) * ndl + (ks * I) * spec;            // no falloff, reading 3
-            }
-            col = fma3(c, w, col);
-            if (depth > 0) {
-                float kr_eff = m1.w;
-                const float kt = m2.x;
-                if (kt > 0.0f) {
-                    const float eta = front ? 1.0f / m2.y : m2.y;
-                    const float cosi = -dot(d, nf);
-                    const float k = 1.0f - eta * eta * (1.0f - cosi * cosi);
-                    if (k < 0.0f) {
-                        kr_eff += kt;                                // reading 5 TIR
-                    } else {
-                        cnt.add(CNT_REFRACTION);
-                        const float3 td = normalize(d * eta + nf * (eta * cosi - sqrtf(k)));
-                        const float3 to = fma3(nf, -BIAS, p);
-                        st_a[sp] = make_float4(to.x, to.y, to.z, w * kt);
-                        st_b[sp] = make_float4(td.x, td.y, td.z, __int_as_float(depth - 1));
-                        ++sp;
-                    }
-                }
-                if (kr_eff > 0.0f) {
-                    cnt.add(CNT_REFLECTION);
-                    d = normalize(d - nf * (2.0f * dot(d, nf)));
-                    o = fma3(nf, BIAS, p);
-                    w *= kr_eff;
-                    depth -= 1;
-                    cont = true;
-                }
-            }
-        }
-        if (cont) continue;
-        if (sp == 0) break;
-        --sp;
-        const float4 a = st_a[sp], b = st_b[sp];
-        o = xyz(a);
-        w = a.w;
-        d = xyz(b);
-        depth = __float_as_int(b.w);
+// Primitive test shared by the BVH leaves and the brute-force path (bit-identical results).
+// Returns true when prim k is hit with T_MIN < t and (closest) (t, gid) < (tmax, hit_gid) or
+// (shadow) t < tmax.
+template <bool COUNT>
+__device__ __forceinline__ bool test_prim(const DevScene& S, int k, float3 o, float3 d, bool shadow, float tmax,
+                                          int hit_gid, float& t_out, int& gid_out, Counters<COUNT>& cnt) {
+    const float4 a = __ldg(&S.prims[3 * k]);
+    const int gid = __float_as_int(a.w);
+    float t;
+    bool ok;
+    if (gid < S.n_spheres) {
+        cnt.add(CNT_SPHERE_TESTS);
+        ok = sphere_intersect(o, d, a, __ldg(&S.prims[3 * k + 1]), T_MIN, t);
+    } else {
+        cnt.add(CNT_TRI_TESTS);
+        ok = tri_intersect(o, d, a, __ldg(&S.prims[3 * k + 1]), __ldg(&S.prims[3 * k + 2]), t) && t > T_MIN;
     }
-    return col;
+    if (!ok) return false;
+    if (shadow ? !(t < tmax) : !(t < tmax || (t == tmax && gid < hit_gid))) return false;
+    t_out = t;
+    gid_out = gid;
+    return true;
 }
 
+enum Stage : int { ST_TREE = 0, ST_SHADOW = 1 };
+
 template <bool COUNT, bool BRUTE>
-__global__ void __launch_bounds__(256) k_trace_stereo(const TraceParams P) {
+__global__ void __launch_bounds__(256, 3) k_trace_stereo(const TraceParams P) {
+    extern __shared__ int s_stack[];                 // [stack_entries][256]
+    const DevScene& S = P.sc;
     Counters<COUNT> cnt;
     cnt.zero();
+    const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
-    while (true) {
-        int base = 0;
-        if (lane == 0) base = atomicAdd(P.work_counter, 32);
-        base = __shfl_sync(0xffffffffu, base, 0);
-        if (base >= P.n_work) break;
-        const int k = base + lane;
-        int eye, px, py, gtile;
-        const bool in_img = map_work(P, k, eye, px, py, gtile);
-        if (in_img) {
-            cnt.add(CNT_PIXELS);
-            const float sx = fmaf(2.0f * (px + 0.5f), 1.0f / P.W, -1.0f) * P.cam.tha;
-            const float sy = fmaf(-2.0f * (py + 0.5f), 1.0f / P.H, 1.0f) * P.cam.th;
-            const float3 o = P.cam.eye[eye];
-            const float3 d = normalize(P.cam.f + P.cam.r * (sx + P.cam.sigma[eye]) + P.cam.u * sy);
-            int pid = -1;
-            const float3 c = trace_pixel<COUNT, BRUTE>(P, o, d, pid, cnt);
-            const long long pix = ((long long)eye * P.H + py) * P.W + px;
-            if (P.fb[eye]) store_px(P.fb[eye], P.fb_fmt[eye], P.fb_pitch[eye], px, py, c);
-            if (P.prim_id) P.prim_id[pix] = pid;
-            if (P.radiance) P.radiance[pix] = make_float4(c.x, c.y, c.z, 0.0f);
-            if (P.shard) {
-                const long long s = (long long)(k >> 8) * 256 + ((py % TILE) * TILE + (px % TILE));
-                if (P.shard_fmt == RT_FORMAT_RGBA8) reinterpret_cast<uint32_t*>(P.shard)[s] = pack_rgba8(c);
-                else reinterpret_cast<uint2*>(P.shard)[s] = pack_rgba16f(c);
+    int* const stk = s_stack + threadIdx.x;          // entry i at stk[i * 256]
+
+    // ---- ray in flight
+    float3 ro = f3(0.f, 0.f, 0.f), rd = f3(0.f, 0.f, 1.f);
+    RayBox rb{};
+    float tmax = 0.f;          // closest: best t so far; shadow: segment length
+    int hit_gid = -1, hit_slot = 0;
+    int node = 0, sp = 0;
+    bool tracing = false, shadow = false, occl = false;
+    int stage = ST_TREE;
+
+    // ---- pixel / ray-tree state
+    int k = 0;
+    bool need_pixel = true, exhausted = false, primary = false;
+    float3 col = f3(0.f, 0.f, 0.f);
+    int prim_id = -1;
+    float w = 1.f;
+    int depth = 0;
+    float3 hp = f3(0.f, 0.f, 0.f), hn = f3(0.f, 0.f, 0.f), hd = f3(0.f, 0.f, 0.f), hc = f3(0.f, 0.f, 0.f);
+    int hmat = 0, light_j = 0;
+    bool hfront = true;
+    float4 st_a[MAX_DEPTH], st_b[MAX_DEPTH];         // refraction children: (o, w) (d, depth)
+    int sst = 0;
+
+    // Start a ray: planes are tested linearly here; the BVH part runs in the traversal loop.
+    auto emit = [&](float3 o, float3 d, bool is_shadow, float t_limit) {
+        ro = o;
+        rd = d;
+        shadow = is_shadow;
+        occl = false;
+        tmax = t_limit;
+        hit_gid = -1;
+        hit_slot = 0;
+        for (int i = 0; i < S.n_planes; ++i) {
+            cnt.add(CNT_PLANE_TESTS);
+            float t;
+            if (plane_intersect(o, d, __ldg(&S.planes[i]), t) && t > T_MIN) {
+                const int gid = S.n_spheres + i;
+                if (is_shadow) {
+                    if (t < tmax) occl = true;
+                } else if (t < tmax || (t == tmax && gid < hit_gid)) {
+                    tmax = t;
+                    hit_gid = gid;
+                    hit_slot = ~i;
+                }
             }
         }
+        tracing = S.n_bvh > 0 && !occl;
+        if (tracing) {
+            rb = make_raybox(o, d, S.bound);
+            node = S.root;
+            sp = 0;
+        }
+    };
+
+    while (true) {
+        // ================================================================ refill
+        // Lanes without a ray in flight advance their ray tree until they emit the next ray
+        // or finish their pixel.
+        while (!tracing && !need_pixel && !exhausted) {
+            if (stage == ST_SHADOW) {
+                if (!occl) {
+                    const float3 Lp = xyz(__ldg(&S.lights[2 * light_j]));
+                    const float3 l = normalize(Lp - hp);
+                    const float ndl = dot(hn, l);
+                    const float3 I = xyz(__ldg(&S.lights[2 * light_j + 1]));
+                    const float4 m0 = __ldg(&S.mats[3 * hmat]);
+                    const float3 ks = xyz(__ldg(&S.mats[3 * hmat + 1]));
+                    const float3 rv = hn * (2.0f * ndl) - l;
+                    const float rdv = -dot(rv, hd);
+                    const float spec = rdv > 0.0f ? __powf(rdv, m0.w) : 0.0f;
+                    hc = hc + (xyz(m0) * I) * ndl + (ks * I) * spec;           // no falloff, reading 3
+                }
+                ++light_j;
+            } else {                                                          // ST_TREE finished
+                if (primary) { prim_id = hit_gid; primary = false; }
+                if (hit_gid < 0) {
+                    cnt.add(CNT_MISSES);
+                    col = fma3(S.background, w, col);                         // S:203 miss
+                    light_j = -1;                                             // nothing to shade
+                } else {
+                    cnt.add(CNT_SHADE_HITS);
+                    hp = fma3(rd, tmax, ro);
+                    float3 ng;
+                    if (hit_slot < 0) {
+                        const int i = ~hit_slot;
+                        ng = xyz(__ldg(&S.planes[i]));
+                        hmat = __ldg(&S.plane_mat[i]);
+                    } else {
+                        const float4 a = __ldg(&S.prims[3 * hit_slot]);
+                        const float4 b = __ldg(&S.prims[3 * hit_slot + 1]);
+                        hmat = __float_as_int(b.w);
+                        if (hit_gid < S.n_spheres) ng = (hp - xyz(a)) * (1.0f / b.x);
+                        else ng = normalize(cross(xyz(b), xyz(__ldg(&S.prims[3 * hit_slot + 2]))));
+                    }
+                    hfront = dot(rd, ng) < 0.0f;
+                    hn = hfront ? ng : ng * -1.0f;                            // S:150 faces the ray
+                    hd = rd;
+                    hc = S.ambient * xyz(__ldg(&S.mats[3 * hmat]));           // S:193 ambient * kd
+                    light_j = 0;
+                }
+            }
+            // ---- next shadow ray of this shading point (reading 2: gate on n.l > 0)
+            if (light_j >= 0) {
+                bool emitted = false;
+                for (; light_j < S.n_lights; ++light_j) {
+                    cnt.add(CNT_LIGHT_EVALS);
+                    const float3 Lp = xyz(__ldg(&S.lights[2 * light_j]));
+                    const float3 l = normalize(Lp - hp);
+                    if (dot(hn, l) <= 0.0f) continue;
+                    const float3 os = fma3(hn, BIAS, hp);                     // S:193 p + bias*n
+                    const float3 sv = Lp - os;
+                    const float dist = sqrtf(dot(sv, sv));
+                    cnt.add(CNT_SHADOW);
+                    stage = ST_SHADOW;
+                    emit(os, sv * (1.0f / dist), true, dist);
+                    emitted = true;
+                    break;
+                }
+                if (emitted) continue;
+                // all lights done: accumulate the local term and spawn the children
+                col = fma3(hc, w, col);
+                light_j = -1;
+                if (depth > 0) {
+                    const float4 m1 = __ldg(&S.mats[3 * hmat + 1]);
+                    const float4 m2 = __ldg(&S.mats[3 * hmat + 2]);
+                    float kr_eff = m1.w;
+                    const float kt = m2.x;
+                    if (kt > 0.0f) {
+                        const float eta = hfront ? 1.0f / m2.y : m2.y;
+                        const float cosi = -dot(hd, hn);
+                        const float kk = 1.0f - eta * eta * (1.0f - cosi * cosi);
+                        if (kk < 0.0f) {
+                            kr_eff += kt;                                      // reading 5 TIR
+                        } else {
+                            cnt.add(CNT_REFRACTION);
+                            const float3 td = normalize(hd * eta + hn * (eta * cosi - sqrtf(kk)));
+                            const float3 to = fma3(hn, -BIAS, hp);
+                            st_a[sst] = make_float4(to.x, to.y, to.z, w * kt);
+                            st_b[sst] = make_float4(td.x, td.y, td.z, __int_as_float(depth - 1));
+                            ++sst;
+                        }
+                    }
+                    if (kr_eff > 0.0f) {
+                        cnt.add(CNT_REFLECTION);
+                        const float3 rdir = normalize(hd - hn * (2.0f * dot(hd, hn)));
+                        w *= kr_eff;
+                        depth -= 1;
+                        stage = ST_TREE;
+                        emit(fma3(hn, BIAS, hp), rdir, false, __int_as_float(0x7f800000));
+                        continue;
+                    }
+                }
+            }
+            // ---- next pending tree ray, or the pixel is complete
+            if (sst > 0) {
+                --sst;
+                const float4 a = st_a[sst], b = st_b[sst];
+                w = a.w;
+                depth = __float_as_int(b.w);
+                stage = ST_TREE;
+                emit(xyz(a), xyz(b), false, __int_as_float(0x7f800000));
+                continue;
+            }
+            int eye, px, py;
+            map_work(P, k, eye, px, py);
+            const long long pix = ((long long)eye * P.H + py) * P.W + px;
+            if (P.fb[eye]) store_px(P.fb[eye], P.fb_fmt[eye], P.fb_pitch[eye], px, py, col);
+            if (P.prim_id) P.prim_id[pix] = prim_id;
+            if (P.radiance) P.radiance[pix] = make_float4(col.x, col.y, col.z, 0.0f);
+            if (P.shard) {
+                const long long s = (long long)(k >> 8) * 256 + ((py % TILE) * TILE + (px % TILE));
+                if (P.shard_fmt == RT_FORMAT_RGBA8) reinterpret_cast<uint32_t*>(P.shard)[s] = pack_rgba8(col);
+                else reinterpret_cast<uint2*>(P.shard)[s] = pack_rgba16f(col);
+            }
+            need_pixel = true;
+        }
+
+        // ================================================================ new pixels
+        // warp-aggregated fetch from the work queue; consecutive items = one 8x4 pixel block
+        const unsigned want = __ballot_sync(FULL, need_pixel && !exhausted);
+        if (want) {
+            int base = 0;
+            const int leader = __ffs(want) - 1;
+            if (lane == leader) base = atomicAdd(P.work_counter, __popc(want));
+            base = __shfl_sync(FULL, base, leader);
+            if (need_pixel && !exhausted) {
+                k = base + __popc(want & ((1u << lane) - 1u));
+                need_pixel = false;
+                int eye, px, py;
+                if (k >= P.n_work) {
+                    exhausted = true;
+                } else if (!map_work(P, k, eye, px, py)) {
+                    need_pixel = true;                                         // ragged tile padding
+                } else {
+                    cnt.add(CNT_PIXELS);
+                    cnt.add(CNT_PRIMARY);
+                    const float sx = fmaf(2.0f * (px + 0.5f), 1.0f / P.W, -1.0f) * P.cam.tha;
+                    const float sy = fmaf(-2.0f * (py + 0.5f), 1.0f / P.H, 1.0f) * P.cam.th;
+                    const float3 d = normalize(P.cam.f + P.cam.r * (sx + P.cam.sigma[eye]) + P.cam.u * sy);
+                    col = f3(0.f, 0.f, 0.f);
+                    prim_id = -1;
+                    primary = true;
+                    w = 1.0f;
+                    depth = P.max_depth;
+                    sst = 0;
+                    stage = ST_TREE;
+                    emit(P.cam.eye[eye], d, false, __int_as_float(0x7f800000));
+                }
+            }
+            if (__any_sync(FULL, need_pixel && !exhausted)) continue;         // ragged / empty-scene lanes
+        }
+        if (__all_sync(FULL, exhausted)) break;
+        if (!__any_sync(FULL, tracing)) continue;                              // finished rays need shading
+
+        // ================================================================ traversal
+        // Every lane with a ray in flight walks the BVH; the warp leaves the loop when enough
+        // lanes have finished to be worth a refill, or when none is left.
+        while (true) {
+            if (tracing) {
+                if (BRUTE) {
+                    for (int kk = 0; kk < S.n_bvh; ++kk) {
+                        float t;
+                        int g;
+                        if (test_prim<COUNT>(S, kk, ro, rd, shadow, tmax, hit_gid, t, g, cnt)) {
+                            if (shadow) { occl = true; break; }
+                            tmax = t;
+                            hit_gid = g;
+                            hit_slot = kk;
+                        }
+                    }
+                    tracing = false;
+                } else {
+                    // internal nodes until this lane reaches a leaf (or runs out of nodes)
+                    while (node >= 0) {
+                        cnt.add(CNT_NODE_VISITS);
+                        const float4 n0 = __ldg(&S.nodes[4 * node + 0]);
+                        const float4 n1 = __ldg(&S.nodes[4 * node + 1]);
+                        const float4 n2 = __ldg(&S.nodes[4 * node + 2]);
+                        const int4 n3 = __ldg(reinterpret_cast<const int4*>(&S.nodes[4 * node + 3]));
+                        const float t0 = box_enter(rb, n0.x, n0.y, n0.z, n0.w, n2.x, n2.y, tmax);
+                        const float t1 = box_enter(rb, n1.x, n1.y, n1.z, n1.w, n2.z, n2.w, tmax);
+                        const bool h0 = t0 >= 0.0f, h1 = t1 >= 0.0f;
+                        if (h0 && h1) {
+                            const bool swap = t1 < t0;
+                            node = swap ? n3.y : n3.x;
+                            stk[sp * 256] = swap ? n3.x : n3.y;
+                            ++sp;
+                        } else if (h0 | h1) {
+                            node = h0 ? n3.x : n3.y;
+                        } else if (sp > 0) {
+                            --sp;
+                            node = stk[sp * 256];
+                        } else {
+                            tracing = false;
+                            break;
+                        }
+                    }
+                    if (tracing) {                                             // leaf
+                        const int enc = ~node;
+                        const int first = enc & ((1 << LEAF_SHIFT) - 1);
+                        const int last = first + (enc >> LEAF_SHIFT);
+                        for (int kk = first; kk <= last; ++kk) {
+                            float t;
+                            int g;
+                            if (test_prim<COUNT>(S, kk, ro, rd, shadow, tmax, hit_gid, t, g, cnt)) {
+                                if (shadow) { occl = true; break; }
+                                tmax = t;
+                                hit_gid = g;
+                                hit_slot = kk;
+                            }
+                        }
+                        if (occl || sp == 0) {
+                            tracing = false;
+                        } else {
+                            --sp;
+                            node = stk[sp * 256];
+                        }
+                    }
+                }
+            }
+            const unsigned busy = __ballot_sync(FULL, tracing);
+            if (busy == 0) break;
+            const unsigned idle = __ballot_sync(FULL, !tracing && !exhausted);
+            if (__popc(idle) >= P.refill) break;
+        }
     }
+
     if (COUNT) {
 #pragma unroll
         for (int i = 0; i < RT_NUM_COUNTERS_INTERNAL; ++i) {
             uint32_t v = cnt.c[i];
 #pragma unroll
-            for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+            for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(FULL, v, off);
             if (lane == 0 && v) atomicAdd(&P.counters[i], (unsigned long long)v);
         }
     }
 }
 
-// Root-side tile unpack for the NCCL gather path: shards (rank-major) -> row-major FBs.
+// Root-side tile unpack for the gather path: shards (rank-major) -> row-major FBs.
 __global__ void k_unpack_shards(const void* __restrict__ gathered, UnpackParams U) {
     const long long n = (long long)U.world * U.tiles_per_rank * 256;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
@@ -376,6 +417,7 @@ __global__ void k_unpack_shards(const void* __restrict__ gathered, UnpackParams 
         int g;
         if (U.shard_mode == 0) {
             g = lt;
+            if (g >= 2 * U.tiles_per_eye) continue;
         } else if (U.shard_mode == 1) {
             const int grp = rank / U.shard_half, j = rank % U.shard_half;
             if (j + lt * U.shard_half >= U.tiles_per_eye) continue;
@@ -384,7 +426,6 @@ __global__ void k_unpack_shards(const void* __restrict__ gathered, UnpackParams 
             g = rank + lt * U.world;
             if (g >= 2 * U.tiles_per_eye) continue;
         }
-        if (U.shard_mode == 0 && g >= 2 * U.tiles_per_eye) continue;
         const int eye = g / U.tiles_per_eye;
         const int t = g - eye * U.tiles_per_eye;
         const int px = (t % U.tiles_x) * TILE + (within % TILE);
@@ -419,20 +460,29 @@ __global__ void __launch_bounds__(256) k_ffma_peak(float* out, int iters, float 
 // ------------------------------------------------------------------ launchers
 using namespace rtb;
 
-cudaError_t rtb_launch_trace(const TraceParams& P, unsigned flags, int grid, cudaStream_t st) {
+static const void* trace_fn(unsigned flags) {
     const bool count = flags & RT_RENDER_COUNT, brute = flags & RT_RENDER_BRUTE_FORCE;
-    if (count && brute) k_trace_stereo<true, true><<<grid, 256, 0, st>>>(P);
-    else if (count) k_trace_stereo<true, false><<<grid, 256, 0, st>>>(P);
-    else if (brute) k_trace_stereo<false, true><<<grid, 256, 0, st>>>(P);
-    else k_trace_stereo<false, false><<<grid, 256, 0, st>>>(P);
-    return cudaGetLastError();
+    return count ? (brute ? (const void*)k_trace_stereo<true, true> : (const void*)k_trace_stereo<true, false>)
+                 : (brute ? (const void*)k_trace_stereo<false, true> : (const void*)k_trace_stereo<false, false>);
 }
 
-cudaError_t rtb_trace_occupancy(unsigned flags, int* blocks_per_sm) {
-    const bool count = flags & RT_RENDER_COUNT, brute = flags & RT_RENDER_BRUTE_FORCE;
-    const void* f = count ? (brute ? (const void*)k_trace_stereo<true, true> : (const void*)k_trace_stereo<true, false>)
-                          : (brute ? (const void*)k_trace_stereo<false, true> : (const void*)k_trace_stereo<false, false>);
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, f, 256, 0);
+size_t rtb_trace_smem(int stack_entries) { return (size_t)stack_entries * 256 * sizeof(int); }
+
+cudaError_t rtb_launch_trace(const TraceParams& P, unsigned flags, int grid, cudaStream_t st) {
+    const size_t smem = rtb_trace_smem(P.stack_entries);
+    const void* f = trace_fn(flags);
+    cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    void* args[] = {const_cast<TraceParams*>(&P)};
+    return cudaLaunchKernel(f, dim3(grid), dim3(256), args, smem, st);
+}
+
+cudaError_t rtb_trace_occupancy(unsigned flags, int stack_entries, int* blocks_per_sm) {
+    const void* f = trace_fn(flags);
+    const size_t smem = rtb_trace_smem(stack_entries);
+    cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, f, 256, smem);
 }
 
 cudaError_t rtb_launch_unpack(const void* gathered, const UnpackParams& U, cudaStream_t st) {
