@@ -78,7 +78,8 @@ struct rt_context {
     bool has_camera = false;
     double cam_eye[2][3], cam_f[3], cam_r[3], cam_u[3], cam_th, cam_sigma_unit;
     float vfov = 0;
-    int refill = 8;          // traversal-loop refill threshold (env RT_REFILL, tuning knob)
+    float4* rq_overflow = nullptr;   // per-CTA spill slices of the tree-ray stack
+    size_t rq_overflow_bytes = 0;
 };
 
 namespace {
@@ -122,7 +123,6 @@ rt_status rt_create(int device, void* cuda_stream, rt_context** out) {
     rt_context* c = new (std::nothrow) rt_context();
     if (!c) return fail(RT_ERR_OOM, "rt_create: host allocation");
     c->device = device;
-    if (const char* r = getenv("RT_REFILL")) c->refill = std::max(1, std::min(32, atoi(r)));
     cudaError_t e = cudaSetDevice(device);
     if (e == cudaSuccess && cuda_stream) {
         c->stream = static_cast<cudaStream_t>(cuda_stream);
@@ -153,6 +153,7 @@ rt_status rt_destroy(rt_context* c) {
     if (c->work_counter) cudaFree(c->work_counter);
     if (c->scratch_counters) cudaFree(c->scratch_counters);
     if (c->ffma_out) cudaFree(c->ffma_out);
+    if (c->rq_overflow) cudaFree(c->rq_overflow);
     if (c->order_ev) cudaEventDestroy(c->order_ev);
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
@@ -201,6 +202,9 @@ rt_status rt_scene_upload(rt_context* c, const rt_primitives* P, const rt_materi
     }
     if (!finite3(env->ambient) || !finite3(env->background))
         return fail(RT_ERR_INVALID_ARG, "env: non-finite ambient/background");
+    for (int k = 0; k < 3; ++k)
+        if (env->ambient[k] < 0 || env->background[k] < 0)
+            return fail(RT_ERR_INVALID_ARG, "env: negative ambient/background (SPEC.md:35 colours are >= 0)");
     double bound = 0.0;
     for (uint32_t i = 0; i < S; ++i) {
         const float* s = P->spheres + 4 * i;
@@ -535,7 +539,7 @@ rt_status rt_render_stereo_ex(rt_context* c, const rt_render_params* p, const rt
     P.shard_fmt = (int)out->shard_format;
     P.counters = out->counters ? out->counters : c->scratch_counters;
     P.stack_entries = std::max(1, (int)c->info[5] + 1);
-    P.refill = c->refill;
+    P.n_tiles = (int)n_tiles;
     if (P.n_work == 0) return RT_OK;
     CUDA_TRY(cudaSetDevice(c->device));
     int occ = 0;
@@ -543,6 +547,19 @@ rt_status rt_render_stereo_ex(rt_context* c, const rt_render_params* p, const rt
     if (occ < 1) occ = 1;
     const long long max_blocks = ((long long)P.n_work + 255) / 256;
     const int grid = (int)std::min<long long>((long long)c->num_sms * occ, std::max<long long>(1, max_blocks));
+    P.rq_overflow_entries = rtb_rq_overflow_entries((int)p->max_depth);
+    const size_t need = (size_t)grid * P.rq_overflow_entries * 2 * sizeof(float4);
+    if (need > c->rq_overflow_bytes) {
+        if (c->rq_overflow) {
+            CUDA_TRY(cudaStreamSynchronize(c->stream));
+            cudaFree(c->rq_overflow);
+            c->rq_overflow = nullptr;
+            c->rq_overflow_bytes = 0;
+        }
+        CUDA_TRY(cudaMalloc(&c->rq_overflow, need));
+        c->rq_overflow_bytes = need;
+    }
+    P.rq_overflow = c->rq_overflow;
     CUDA_TRY(cudaMemsetAsync(c->work_counter, 0, sizeof(int), c->stream));
     CUDA_TRY(rtb_launch_trace(P, p->flags, grid, c->stream));
     return RT_OK;

@@ -40,7 +40,9 @@ struct TraceParams {
     int shard_fmt;
     unsigned long long* counters;
     int stack_entries;      // BVH traversal stack depth (shared memory, [entry][thread])
-    int refill;             // leave the traversal loop when this many lanes of a warp are idle
+    int n_tiles;            // 16x16 tiles in this shard (= n_work / 256)
+    float4* rq_overflow;    // per-CTA global spill of the tree-ray stack (2 float4 per entry)
+    int rq_overflow_entries;
 };
 
 struct UnpackParams {
@@ -86,6 +88,7 @@ struct BuildBuffers {
 cudaError_t rtb_launch_trace(const TraceParams& P, unsigned flags, int grid, cudaStream_t st);
 cudaError_t rtb_trace_occupancy(unsigned flags, int stack_entries, int* blocks_per_sm);
 size_t rtb_trace_smem(int stack_entries);
+int rtb_rq_overflow_entries(int max_depth);
 cudaError_t rtb_launch_unpack(const void* gathered, const UnpackParams& U, cudaStream_t st);
 cudaError_t rtb_launch_ffma(float* out, int iters, int grid, cudaStream_t st);
 // launchers (rt_build.cu)

@@ -1,22 +1,32 @@
 // rt_trace.cu -- the hot path: one persistent-thread megakernel that, for every pixel of both
 // eyes (§3 Fig. 2 "level 1" channels x "level 2" pixels), generates the primary
 // ray, finds nearest hits through the LBVH (+ linear planes), shades with Phong + shadow rays
-// per light, follows reflection/refraction with an iterative per-thread ray stack up to
-// max_depth bounces, and packs the clamped radiance straight into the RGBA8/FP16 framebuffers
-// (and, optionally, prim-ID / radiance debug planes or a tile-packed shard).
-// SURVEY.md §8(a) rows a3-a6; DESIGN.md §5.
+// per light, follows reflection/refraction up to max_depth bounces, and packs the clamped
+// radiance straight into the RGBA8/FP16 framebuffers (and, optionally, prim-ID / radiance
+// debug planes or a tile-packed shard).  SURVEY.md §8(a) rows a3-a6; DESIGN.md §5.
 //
-// Execution model (v1): every lane runs a small state machine over ITS OWN pixel's ray tree
-// (tree ray -> one shadow ray per lit light -> reflection / refraction children), and all ray
-// kinds share ONE traversal loop.  When a lane's ray finishes it advances its state machine
-// (producing the next ray of its tree, or finishing the pixel and taking a new one from the
-// work queue with a warp-aggregated atomic), so the warp keeps ~all lanes traversing instead
-// of waiting for the longest ray tree (the v0 kernel averaged 8 of 32 active lanes).  The
-// BVH traversal stack lives in shared memory, [entry][thread], conflict-free.
+// Execution model (v2, "CTA wavefront"): a persistent CTA of 256 threads owns one 16x16 pixel
+// tile at a time.  The tile's pending tree rays live in a CTA-shared ray stack in shared memory
+// (overflowing to a per-CTA global slice only for glass-heavy trees).  Each round the CTA pops
+// up to 256 rays -- one per thread, so a round's rays are always packed into full warps -- and
+// every thread traces its ray (nearest hit), shades it with one shadow ray per lit light
+// (lights in index order, so the warp's shadow rays head to the same light together), adds
+// w * local term to its pixel's accumulator and pushes the reflection / refraction children.
+// v0 (one thread per pixel tree) averaged 8 of 32 active lanes because lanes idled while their
+// neighbours finished deeper trees; compaction per round removes that idling.
+// Accumulators are 64-bit fixed point (2^-40) so the result does not depend on the order in
+// which rays of one pixel finish (bit-exact determinism).  The BVH traversal stack is
+// in shared memory, [entry][thread], conflict-free.
 #include "rt_device.cuh"
 #include "rt_internal.h"
 
 namespace rtb {
+
+#ifndef RT_MINB
+#define RT_MINB 3
+#endif
+constexpr int RQ_SMEM = 512;                 // tree-ray stack entries held in shared memory
+constexpr double ACC_SCALE = 1099511627776.0; // 2^40
 
 template <bool COUNT>
 struct Counters {
@@ -28,8 +38,14 @@ struct Counters {
     __device__ __forceinline__ void add(int i, uint32_t n = 1) { if (COUNT) c[i] += n; }
 };
 
-// Work item -> (eye, px, py).  16x16 tiles, each tile = 8 warps of 8x4 pixels so consecutive
-// work items are spatially coherent.  Tiles are drawn from this rank's shard.
+struct Hit {
+    float t;
+    int gid;    // global primitive ID, -1 = miss
+    int slot;   // BVH prim slot (>= 0) or ~plane index (< 0)
+};
+
+// Work item -> (eye, px, py).  16x16 tiles, each tile = 8 warps of 8x4 pixels so a warp's
+// primary rays are spatially coherent.  Tiles are drawn from this rank's shard.
 __device__ __forceinline__ bool map_work(const TraceParams& P, int k, int& eye, int& px, int& py) {
     const int lt = k >> 8;
     const int within = k & 255;
@@ -74,333 +90,313 @@ __device__ __forceinline__ void store_px(void* base, int fmt, long long pitch, i
 }
 
 // Primitive test shared by the BVH leaves and the brute-force path (bit-identical results).
-// Returns true when prim k is hit with T_MIN < t and (closest) (t, gid) < (tmax, hit_gid) or
-// (shadow) t < tmax.
 template <bool COUNT>
-__device__ __forceinline__ bool test_prim(const DevScene& S, int k, float3 o, float3 d, bool shadow, float tmax,
-                                          int hit_gid, float& t_out, int& gid_out, Counters<COUNT>& cnt) {
+__device__ __forceinline__ bool prim_t(const DevScene& S, int k, float3 o, float3 d, float& t, int& gid,
+                                       Counters<COUNT>& cnt) {
     const float4 a = __ldg(&S.prims[3 * k]);
-    const int gid = __float_as_int(a.w);
-    float t;
-    bool ok;
+    gid = __float_as_int(a.w);
     if (gid < S.n_spheres) {
         cnt.add(CNT_SPHERE_TESTS);
-        ok = sphere_intersect(o, d, a, __ldg(&S.prims[3 * k + 1]), T_MIN, t);
-    } else {
-        cnt.add(CNT_TRI_TESTS);
-        ok = tri_intersect(o, d, a, __ldg(&S.prims[3 * k + 1]), __ldg(&S.prims[3 * k + 2]), t) && t > T_MIN;
+        return sphere_intersect(o, d, a, __ldg(&S.prims[3 * k + 1]), T_MIN, t);
     }
-    if (!ok) return false;
-    if (shadow ? !(t < tmax) : !(t < tmax || (t == tmax && gid < hit_gid))) return false;
-    t_out = t;
-    gid_out = gid;
-    return true;
+    cnt.add(CNT_TRI_TESTS);
+    return tri_intersect(o, d, a, __ldg(&S.prims[3 * k + 1]), __ldg(&S.prims[3 * k + 2]), t) && t > T_MIN;
 }
 
-enum Stage : int { ST_TREE = 0, ST_SHADOW = 1 };
+// Nearest hit over the BVH (or every BVH primitive when BRUTE) and the planes.
+// Acceptance: t > t_min and (t, gid) lexicographically smallest (reading 9).
+template <bool COUNT, bool BRUTE>
+__device__ __forceinline__ Hit closest_hit(const DevScene& S, float3 o, float3 d, int* stk, Counters<COUNT>& cnt) {
+    Hit h;
+    h.t = __int_as_float(0x7f800000);
+    h.gid = -1;
+    h.slot = 0;
+    for (int i = 0; i < S.n_planes; ++i) {
+        cnt.add(CNT_PLANE_TESTS);
+        float t;
+        if (plane_intersect(o, d, __ldg(&S.planes[i]), t) && t > T_MIN) {
+            const int gid = S.n_spheres + i;
+            if (t < h.t || (t == h.t && gid < h.gid)) { h.t = t; h.gid = gid; h.slot = ~i; }
+        }
+    }
+    if (S.n_bvh == 0) return h;
+    auto leaf = [&](int first, int last) {
+        for (int k = first; k <= last; ++k) {
+            float t;
+            int gid;
+            if (prim_t<COUNT>(S, k, o, d, t, gid, cnt) && (t < h.t || (t == h.t && gid < h.gid))) {
+                h.t = t; h.gid = gid; h.slot = k;
+            }
+        }
+    };
+    if (BRUTE) {
+        leaf(0, S.n_bvh - 1);
+        return h;
+    }
+    const RayBox rb = make_raybox(o, d, S.bound);
+    int sp = 0;
+    int node = S.root;
+    while (true) {
+        while (node >= 0) {
+            cnt.add(CNT_NODE_VISITS);
+            const float4 n0 = __ldg(&S.nodes[4 * node + 0]);
+            const float4 n1 = __ldg(&S.nodes[4 * node + 1]);
+            const float4 n2 = __ldg(&S.nodes[4 * node + 2]);
+            const int4 n3 = __ldg(reinterpret_cast<const int4*>(&S.nodes[4 * node + 3]));
+            const float t0 = box_enter(rb, n0.x, n0.y, n0.z, n0.w, n2.x, n2.y, h.t);
+            const float t1 = box_enter(rb, n1.x, n1.y, n1.z, n1.w, n2.z, n2.w, h.t);
+            const bool h0 = t0 >= 0.0f, h1 = t1 >= 0.0f;
+            if (h0 && h1) {
+                const bool swap = t1 < t0;
+                node = swap ? n3.y : n3.x;
+                stk[sp * 256] = swap ? n3.x : n3.y;
+                ++sp;
+            } else if (h0 | h1) {
+                node = h0 ? n3.x : n3.y;
+            } else {
+                if (sp == 0) return h;
+                --sp;
+                node = stk[sp * 256];
+            }
+        }
+        const int enc = ~node;
+        const int first = enc & ((1 << LEAF_SHIFT) - 1);
+        leaf(first, first + (enc >> LEAF_SHIFT));
+        if (sp == 0) return h;
+        --sp;
+        node = stk[sp * 256];
+    }
+}
+
+// Any hit with t_min < t < dist (binary visibility, reading 4).
+template <bool COUNT, bool BRUTE>
+__device__ __forceinline__ bool occluded(const DevScene& S, float3 o, float3 d, float dist, int* stk, Counters<COUNT>& cnt) {
+    for (int i = 0; i < S.n_planes; ++i) {
+        cnt.add(CNT_PLANE_TESTS);
+        float t;
+        if (plane_intersect(o, d, __ldg(&S.planes[i]), t) && t > T_MIN && t < dist) return true;
+    }
+    if (S.n_bvh == 0) return false;
+    auto leaf = [&](int first, int last) -> bool {
+        for (int k = first; k <= last; ++k) {
+            float t;
+            int gid;
+            if (prim_t<COUNT>(S, k, o, d, t, gid, cnt) && t < dist) return true;
+        }
+        return false;
+    };
+    if (BRUTE) return leaf(0, S.n_bvh - 1);
+    const RayBox rb = make_raybox(o, d, S.bound);
+    int sp = 0;
+    int node = S.root;
+    while (true) {
+        while (node >= 0) {
+            cnt.add(CNT_NODE_VISITS);
+            const float4 n0 = __ldg(&S.nodes[4 * node + 0]);
+            const float4 n1 = __ldg(&S.nodes[4 * node + 1]);
+            const float4 n2 = __ldg(&S.nodes[4 * node + 2]);
+            const int4 n3 = __ldg(reinterpret_cast<const int4*>(&S.nodes[4 * node + 3]));
+            const float t0 = box_enter(rb, n0.x, n0.y, n0.z, n0.w, n2.x, n2.y, dist);
+            const float t1 = box_enter(rb, n1.x, n1.y, n1.z, n1.w, n2.z, n2.w, dist);
+            const bool h0 = t0 >= 0.0f, h1 = t1 >= 0.0f;
+            if (h0 && h1) {
+                node = n3.x;
+                stk[sp * 256] = n3.y;
+                ++sp;
+            } else if (h0 | h1) {
+                node = h0 ? n3.x : n3.y;
+            } else {
+                if (sp == 0) return false;
+                --sp;
+                node = stk[sp * 256];
+            }
+        }
+        const int enc = ~node;
+        const int first = enc & ((1 << LEAF_SHIFT) - 1);
+        if (leaf(first, first + (enc >> LEAF_SHIFT))) return true;
+        if (sp == 0) return false;
+        --sp;
+        node = stk[sp * 256];
+    }
+}
+
+__device__ __forceinline__ void acc_add(unsigned long long* acc, float3 c) {
+    // non-negative terms (validated inputs), 2^-40 fixed point: order-independent sums
+    atomicAdd(&acc[0], __double2ull_rn((double)c.x * ACC_SCALE));
+    atomicAdd(&acc[1], __double2ull_rn((double)c.y * ACC_SCALE));
+    atomicAdd(&acc[2], __double2ull_rn((double)c.z * ACC_SCALE));
+}
+
+// Tree-ray stack entry: (o.xyz, w) (d.xyz, meta); meta = pixel (8 bits) | depth << 8 | primary << 16
+__device__ __forceinline__ float4* rq_slot(float4* s_rq, float4* g_rq, int i) {
+    return i < RQ_SMEM ? s_rq + 2 * i : g_rq + 2 * (i - RQ_SMEM);
+}
 
 template <bool COUNT, bool BRUTE>
-__global__ void __launch_bounds__(256, 3) k_trace_stereo(const TraceParams P) {
-    extern __shared__ int s_stack[];                 // [stack_entries][256]
+__global__ void __launch_bounds__(256, RT_MINB) k_trace_stereo(const TraceParams P) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    float4* const s_rq = reinterpret_cast<float4*>(smem);                                   // [RQ_SMEM][2]
+    unsigned long long* const s_acc = reinterpret_cast<unsigned long long*>(smem + RQ_SMEM * 32);  // [256][3]
+    int* const s_id = reinterpret_cast<int*>(smem + RQ_SMEM * 32 + 256 * 24);             // [256]
+    int* const s_stack = s_id + 256;                                                       // [entries][256]
+    __shared__ int s_tile, s_count;
     const DevScene& S = P.sc;
     Counters<COUNT> cnt;
     cnt.zero();
-    const unsigned FULL = 0xffffffffu;
-    const int lane = threadIdx.x & 31;
-    int* const stk = s_stack + threadIdx.x;          // entry i at stk[i * 256]
-
-    // ---- ray in flight
-    float3 ro = f3(0.f, 0.f, 0.f), rd = f3(0.f, 0.f, 1.f);
-    RayBox rb{};
-    float tmax = 0.f;          // closest: best t so far; shadow: segment length
-    int hit_gid = -1, hit_slot = 0;
-    int node = 0, sp = 0;
-    bool tracing = false, shadow = false, occl = false;
-    int stage = ST_TREE;
-
-    // ---- pixel / ray-tree state
-    int k = 0;
-    bool need_pixel = true, exhausted = false, primary = false;
-    float3 col = f3(0.f, 0.f, 0.f);
-    int prim_id = -1;
-    float w = 1.f;
-    int depth = 0;
-    float3 hp = f3(0.f, 0.f, 0.f), hn = f3(0.f, 0.f, 0.f), hd = f3(0.f, 0.f, 0.f), hc = f3(0.f, 0.f, 0.f);
-    int hmat = 0, light_j = 0;
-    bool hfront = true;
-    float4 st_a[MAX_DEPTH], st_b[MAX_DEPTH];         // refraction children: (o, w) (d, depth)
-    int sst = 0;
-
-    // Start a ray: planes are tested linearly here; the BVH part runs in the traversal loop.
-    auto emit = [&](float3 o, float3 d, bool is_shadow, float t_limit) {
-        ro = o;
-        rd = d;
-        shadow = is_shadow;
-        occl = false;
-        tmax = t_limit;
-        hit_gid = -1;
-        hit_slot = 0;
-        for (int i = 0; i < S.n_planes; ++i) {
-            cnt.add(CNT_PLANE_TESTS);
-            float t;
-            if (plane_intersect(o, d, __ldg(&S.planes[i]), t) && t > T_MIN) {
-                const int gid = S.n_spheres + i;
-                if (is_shadow) {
-                    if (t < tmax) occl = true;
-                } else if (t < tmax || (t == tmax && gid < hit_gid)) {
-                    tmax = t;
-                    hit_gid = gid;
-                    hit_slot = ~i;
-                }
-            }
-        }
-        tracing = S.n_bvh > 0 && !occl;
-        if (tracing) {
-            rb = make_raybox(o, d, S.bound);
-            node = S.root;
-            sp = 0;
-        }
-    };
+    const int tid = threadIdx.x;
+    int* const stk = s_stack + tid;
+    float4* const g_rq = P.rq_overflow + (long long)blockIdx.x * 2 * P.rq_overflow_entries;
 
     while (true) {
-        // ================================================================ refill
-        // Lanes without a ray in flight advance their ray tree until they emit the next ray
-        // or finish their pixel.
-        while (!tracing && !need_pixel && !exhausted) {
-            if (stage == ST_SHADOW) {
-                if (!occl) {
-                    const float3 Lp = xyz(__ldg(&S.lights[2 * light_j]));
-                    const float3 l = normalize(Lp - hp);
-                    const float ndl = dot(hn, l);
-                    const float3 I = xyz(__ldg(&S.lights[2 * light_j + 1]));
-                    const float4 m0 = __ldg(&S.mats[3 * hmat]);
-                    const float3 ks = xyz(__ldg(&S.mats[3 * hmat + 1]));
-                    const float3 rv = hn * (2.0f * ndl) - l;
-                    const float rdv = -dot(rv, hd);
-                    const float spec = rdv > 0.0f ? __powf(rdv, m0.w) : 0.0f;
-                    hc = hc + (xyz(m0) * I) * ndl + (ks * I) * spec;           // no falloff, reading 3
-                }
-                ++light_j;
-            } else {                                                          // ST_TREE finished
-                if (primary) { prim_id = hit_gid; primary = false; }
-                if (hit_gid < 0) {
+        if (tid == 0) s_tile = atomicAdd(P.work_counter, 1);
+        __syncthreads();
+        const int tile = s_tile;
+        if (tile >= P.n_tiles) break;
+        const int k = tile * 256 + tid;
+        int eye, px, py;
+        const bool valid = map_work(P, k, eye, px, py);
+        s_acc[3 * tid] = 0ull;
+        s_acc[3 * tid + 1] = 0ull;
+        s_acc[3 * tid + 2] = 0ull;
+        s_id[tid] = -1;
+        if (valid) {
+            cnt.add(CNT_PIXELS);
+            cnt.add(CNT_PRIMARY);
+            const float sx = fmaf(2.0f * (px + 0.5f), 1.0f / P.W, -1.0f) * P.cam.tha;
+            const float sy = fmaf(-2.0f * (py + 0.5f), 1.0f / P.H, 1.0f) * P.cam.th;
+            const float3 d = normalize(P.cam.f + P.cam.r * (sx + P.cam.sigma[eye]) + P.cam.u * sy);
+            const float3 o = P.cam.eye[eye];
+            s_rq[2 * tid] = make_float4(o.x, o.y, o.z, 1.0f);
+            s_rq[2 * tid + 1] = make_float4(d.x, d.y, d.z, __int_as_float(tid | (P.max_depth << 8) | (1 << 16)));
+        } else {
+            s_rq[2 * tid] = make_float4(0.f, 0.f, 0.f, 0.0f);
+            s_rq[2 * tid + 1] = make_float4(0.f, 0.f, 1.f, __int_as_float(-1));
+        }
+        if (tid == 0) s_count = 256;
+        __syncthreads();
+
+        // ---- rounds: pop up to 256 tree rays (one per thread), trace, shade, push children
+        while (true) {
+            const int count = s_count;
+            if (count == 0) break;
+            const int nb = min(256, count), base = count - nb;
+            float4 ra = make_float4(0.f, 0.f, 0.f, 0.f), rbv = make_float4(0.f, 0.f, 0.f, __int_as_float(-1));
+            if (tid < nb) {
+                const float4* e = rq_slot(s_rq, g_rq, base + tid);
+                ra = e[0];
+                rbv = e[1];
+            }
+            __syncthreads();                          // every thread holds its ray; slots are free
+            if (tid == 0) s_count = base;
+            __syncthreads();
+            const int meta = __float_as_int(rbv.w);
+            if (meta >= 0) {
+                const int pl = meta & 255, depth = (meta >> 8) & 255;
+                const bool primary = (meta >> 16) & 1;
+                const float3 o = xyz(ra), d = xyz(rbv);
+                const float w = ra.w;
+                const Hit h = closest_hit<COUNT, BRUTE>(S, o, d, stk, cnt);
+                if (primary) s_id[pl] = h.gid;
+                if (h.gid < 0) {
                     cnt.add(CNT_MISSES);
-                    col = fma3(S.background, w, col);                         // S:203 miss
-                    light_j = -1;                                             // nothing to shade
+                    acc_add(&s_acc[3 * pl], S.background * w);                  // S:203 miss
                 } else {
                     cnt.add(CNT_SHADE_HITS);
-                    hp = fma3(rd, tmax, ro);
+                    const float3 p = fma3(d, h.t, o);
                     float3 ng;
-                    if (hit_slot < 0) {
-                        const int i = ~hit_slot;
+                    int mat;
+                    if (h.slot < 0) {
+                        const int i = ~h.slot;
                         ng = xyz(__ldg(&S.planes[i]));
-                        hmat = __ldg(&S.plane_mat[i]);
+                        mat = __ldg(&S.plane_mat[i]);
                     } else {
-                        const float4 a = __ldg(&S.prims[3 * hit_slot]);
-                        const float4 b = __ldg(&S.prims[3 * hit_slot + 1]);
-                        hmat = __float_as_int(b.w);
-                        if (hit_gid < S.n_spheres) ng = (hp - xyz(a)) * (1.0f / b.x);
-                        else ng = normalize(cross(xyz(b), xyz(__ldg(&S.prims[3 * hit_slot + 2]))));
+                        const float4 a = __ldg(&S.prims[3 * h.slot]);
+                        const float4 b = __ldg(&S.prims[3 * h.slot + 1]);
+                        mat = __float_as_int(b.w);
+                        if (h.gid < S.n_spheres) ng = (p - xyz(a)) * (1.0f / b.x);
+                        else ng = normalize(cross(xyz(b), xyz(__ldg(&S.prims[3 * h.slot + 2]))));
                     }
-                    hfront = dot(rd, ng) < 0.0f;
-                    hn = hfront ? ng : ng * -1.0f;                            // S:150 faces the ray
-                    hd = rd;
-                    hc = S.ambient * xyz(__ldg(&S.mats[3 * hmat]));           // S:193 ambient * kd
-                    light_j = 0;
-                }
-            }
-            // ---- next shadow ray of this shading point (reading 2: gate on n.l > 0)
-            if (light_j >= 0) {
-                bool emitted = false;
-                for (; light_j < S.n_lights; ++light_j) {
-                    cnt.add(CNT_LIGHT_EVALS);
-                    const float3 Lp = xyz(__ldg(&S.lights[2 * light_j]));
-                    const float3 l = normalize(Lp - hp);
-                    if (dot(hn, l) <= 0.0f) continue;
-                    const float3 os = fma3(hn, BIAS, hp);                     // S:193 p + bias*n
-                    const float3 sv = Lp - os;
-                    const float dist = sqrtf(dot(sv, sv));
-                    cnt.add(CNT_SHADOW);
-                    stage = ST_SHADOW;
-                    emit(os, sv * (1.0f / dist), true, dist);
-                    emitted = true;
-                    break;
-                }
-                if (emitted) continue;
-                // all lights done: accumulate the local term and spawn the children
-                col = fma3(hc, w, col);
-                light_j = -1;
-                if (depth > 0) {
-                    const float4 m1 = __ldg(&S.mats[3 * hmat + 1]);
-                    const float4 m2 = __ldg(&S.mats[3 * hmat + 2]);
-                    float kr_eff = m1.w;
-                    const float kt = m2.x;
-                    if (kt > 0.0f) {
-                        const float eta = hfront ? 1.0f / m2.y : m2.y;
-                        const float cosi = -dot(hd, hn);
-                        const float kk = 1.0f - eta * eta * (1.0f - cosi * cosi);
-                        if (kk < 0.0f) {
-                            kr_eff += kt;                                      // reading 5 TIR
-                        } else {
-                            cnt.add(CNT_REFRACTION);
-                            const float3 td = normalize(hd * eta + hn * (eta * cosi - sqrtf(kk)));
-                            const float3 to = fma3(hn, -BIAS, hp);
-                            st_a[sst] = make_float4(to.x, to.y, to.z, w * kt);
-                            st_b[sst] = make_float4(td.x, td.y, td.z, __int_as_float(depth - 1));
-                            ++sst;
+                    const bool front = dot(d, ng) < 0.0f;
+                    const float3 nf = front ? ng : ng * -1.0f;
+                    const float4 m0 = __ldg(&S.mats[3 * mat]), m1 = __ldg(&S.mats[3 * mat + 1]);
+                    const float3 kd = xyz(m0), ks = xyz(m1);
+                    float3 c = S.ambient * kd;
+                    for (int j = 0; j < S.n_lights; ++j) {
+                        cnt.add(CNT_LIGHT_EVALS);
+                        const float3 Lp = xyz(__ldg(&S.lights[2 * j]));
+                        const float3 l = normalize(Lp - p);
+                        const float ndl = dot(nf, l);
+                        if (ndl <= 0.0f) continue;                                   // reading 2
+                        const float3 os = fma3(nf, BIAS, p);
+                        const float3 sv = Lp - os;
+                        const float dist = sqrtf(dot(sv, sv));
+                        cnt.add(CNT_SHADOW);
+                        if (occluded<COUNT, BRUTE>(S, os, sv * (1.0f / dist), dist, stk, cnt)) continue;
+                        const float3 I = xyz(__ldg(&S.lights[2 * j + 1]));
+                        const float3 rv = nf * (2.0f * ndl) - l;
+                        const float rdv = -dot(rv, d);
+                        const float spec = rdv > 0.0f ? __powf(rdv, m0.w) : 0.0f;
+                        c = c + (kd * I) * ndl + (ks * I) * spec;                   // reading 3
+                    }
+                    acc_add(&s_acc[3 * pl], c * w);
+                    if (depth > 0) {
+                        const float4 m2 = __ldg(&S.mats[3 * mat + 2]);
+                        float kr_eff = m1.w;
+                        const float kt = m2.x;
+                        if (kt > 0.0f) {
+                            const float eta = front ? 1.0f / m2.y : m2.y;
+                            const float cosi = -dot(d, nf);
+                            const float kk = 1.0f - eta * eta * (1.0f - cosi * cosi);
+                            if (kk < 0.0f) {
+                                kr_eff += kt;                                        // reading 5
+                            } else {
+                                cnt.add(CNT_REFRACTION);
+                                const float3 td = normalize(d * eta + nf * (eta * cosi - sqrtf(kk)));
+                                const float3 to = fma3(nf, -BIAS, p);
+                                float4* e = rq_slot(s_rq, g_rq, atomicAdd(&s_count, 1));
+                                e[0] = make_float4(to.x, to.y, to.z, w * kt);
+                                e[1] = make_float4(td.x, td.y, td.z, __int_as_float(pl | ((depth - 1) << 8)));
+                            }
+                        }
+                        if (kr_eff > 0.0f) {
+                            cnt.add(CNT_REFLECTION);
+                            const float3 rd = normalize(d - nf * (2.0f * dot(d, nf)));
+                            const float3 ro = fma3(nf, BIAS, p);
+                            float4* e = rq_slot(s_rq, g_rq, atomicAdd(&s_count, 1));
+                            e[0] = make_float4(ro.x, ro.y, ro.z, w * kr_eff);
+                            e[1] = make_float4(rd.x, rd.y, rd.z, __int_as_float(pl | ((depth - 1) << 8)));
                         }
                     }
-                    if (kr_eff > 0.0f) {
-                        cnt.add(CNT_REFLECTION);
-                        const float3 rdir = normalize(hd - hn * (2.0f * dot(hd, hn)));
-                        w *= kr_eff;
-                        depth -= 1;
-                        stage = ST_TREE;
-                        emit(fma3(hn, BIAS, hp), rdir, false, __int_as_float(0x7f800000));
-                        continue;
-                    }
                 }
             }
-            // ---- next pending tree ray, or the pixel is complete
-            if (sst > 0) {
-                --sst;
-                const float4 a = st_a[sst], b = st_b[sst];
-                w = a.w;
-                depth = __float_as_int(b.w);
-                stage = ST_TREE;
-                emit(xyz(a), xyz(b), false, __int_as_float(0x7f800000));
-                continue;
-            }
-            int eye, px, py;
-            map_work(P, k, eye, px, py);
+            __syncthreads();
+        }
+
+        // ---- pack epilogue: one thread per pixel of the tile
+        if (valid) {
+            const float3 col = f3((float)((double)s_acc[3 * tid] * (1.0 / ACC_SCALE)),
+                                  (float)((double)s_acc[3 * tid + 1] * (1.0 / ACC_SCALE)),
+                                  (float)((double)s_acc[3 * tid + 2] * (1.0 / ACC_SCALE)));
             const long long pix = ((long long)eye * P.H + py) * P.W + px;
             if (P.fb[eye]) store_px(P.fb[eye], P.fb_fmt[eye], P.fb_pitch[eye], px, py, col);
-            if (P.prim_id) P.prim_id[pix] = prim_id;
+            if (P.prim_id) P.prim_id[pix] = s_id[tid];
             if (P.radiance) P.radiance[pix] = make_float4(col.x, col.y, col.z, 0.0f);
             if (P.shard) {
-                const long long s = (long long)(k >> 8) * 256 + ((py % TILE) * TILE + (px % TILE));
+                const long long s = (long long)tile * 256 + ((py % TILE) * TILE + (px % TILE));
                 if (P.shard_fmt == RT_FORMAT_RGBA8) reinterpret_cast<uint32_t*>(P.shard)[s] = pack_rgba8(col);
                 else reinterpret_cast<uint2*>(P.shard)[s] = pack_rgba16f(col);
             }
-            need_pixel = true;
         }
-
-        // ================================================================ new pixels
-        // warp-aggregated fetch from the work queue; consecutive items = one 8x4 pixel block
-        const unsigned want = __ballot_sync(FULL, need_pixel && !exhausted);
-        if (want) {
-            int base = 0;
-            const int leader = __ffs(want) - 1;
-            if (lane == leader) base = atomicAdd(P.work_counter, __popc(want));
-            base = __shfl_sync(FULL, base, leader);
-            if (need_pixel && !exhausted) {
-                k = base + __popc(want & ((1u << lane) - 1u));
-                need_pixel = false;
-                int eye, px, py;
-                if (k >= P.n_work) {
-                    exhausted = true;
-                } else if (!map_work(P, k, eye, px, py)) {
-                    need_pixel = true;                                         // ragged tile padding
-                } else {
-                    cnt.add(CNT_PIXELS);
-                    cnt.add(CNT_PRIMARY);
-                    const float sx = fmaf(2.0f * (px + 0.5f), 1.0f / P.W, -1.0f) * P.cam.tha;
-                    const float sy = fmaf(-2.0f * (py + 0.5f), 1.0f / P.H, 1.0f) * P.cam.th;
-                    const float3 d = normalize(P.cam.f + P.cam.r * (sx + P.cam.sigma[eye]) + P.cam.u * sy);
-                    col = f3(0.f, 0.f, 0.f);
-                    prim_id = -1;
-                    primary = true;
-                    w = 1.0f;
-                    depth = P.max_depth;
-                    sst = 0;
-                    stage = ST_TREE;
-                    emit(P.cam.eye[eye], d, false, __int_as_float(0x7f800000));
-                }
-            }
-            if (__any_sync(FULL, need_pixel && !exhausted)) continue;         // ragged / empty-scene lanes
-        }
-        if (__all_sync(FULL, exhausted)) break;
-        if (!__any_sync(FULL, tracing)) continue;                              // finished rays need shading
-
-        // ================================================================ traversal
-        // Every lane with a ray in flight walks the BVH; the warp leaves the loop when enough
-        // lanes have finished to be worth a refill, or when none is left.
-        while (true) {
-            if (tracing) {
-                if (BRUTE) {
-                    for (int kk = 0; kk < S.n_bvh; ++kk) {
-                        float t;
-                        int g;
-                        if (test_prim<COUNT>(S, kk, ro, rd, shadow, tmax, hit_gid, t, g, cnt)) {
-                            if (shadow) { occl = true; break; }
-                            tmax = t;
-                            hit_gid = g;
-                            hit_slot = kk;
-                        }
-                    }
-                    tracing = false;
-                } else {
-                    // internal nodes until this lane reaches a leaf (or runs out of nodes)
-                    while (node >= 0) {
-                        cnt.add(CNT_NODE_VISITS);
-                        const float4 n0 = __ldg(&S.nodes[4 * node + 0]);
-                        const float4 n1 = __ldg(&S.nodes[4 * node + 1]);
-                        const float4 n2 = __ldg(&S.nodes[4 * node + 2]);
-                        const int4 n3 = __ldg(reinterpret_cast<const int4*>(&S.nodes[4 * node + 3]));
-                        const float t0 = box_enter(rb, n0.x, n0.y, n0.z, n0.w, n2.x, n2.y, tmax);
-                        const float t1 = box_enter(rb, n1.x, n1.y, n1.z, n1.w, n2.z, n2.w, tmax);
-                        const bool h0 = t0 >= 0.0f, h1 = t1 >= 0.0f;
-                        if (h0 && h1) {
-                            const bool swap = t1 < t0;
-                            node = swap ? n3.y : n3.x;
-                            stk[sp * 256] = swap ? n3.x : n3.y;
-                            ++sp;
-                        } else if (h0 | h1) {
-                            node = h0 ? n3.x : n3.y;
-                        } else if (sp > 0) {
-                            --sp;
-                            node = stk[sp * 256];
-                        } else {
-                            tracing = false;
-                            break;
-                        }
-                    }
-                    if (tracing) {                                             // leaf
-                        const int enc = ~node;
-                        const int first = enc & ((1 << LEAF_SHIFT) - 1);
-                        const int last = first + (enc >> LEAF_SHIFT);
-                        for (int kk = first; kk <= last; ++kk) {
-                            float t;
-                            int g;
-                            if (test_prim<COUNT>(S, kk, ro, rd, shadow, tmax, hit_gid, t, g, cnt)) {
-                                if (shadow) { occl = true; break; }
-                                tmax = t;
-                                hit_gid = g;
-                                hit_slot = kk;
-                            }
-                        }
-                        if (occl || sp == 0) {
-                            tracing = false;
-                        } else {
-                            --sp;
-                            node = stk[sp * 256];
-                        }
-                    }
-                }
-            }
-            const unsigned busy = __ballot_sync(FULL, tracing);
-            if (busy == 0) break;
-            const unsigned idle = __ballot_sync(FULL, !tracing && !exhausted);
-            if (__popc(idle) >= P.refill) break;
-        }
+        __syncthreads();
     }
 
     if (COUNT) {
+        const int lane = tid & 31;
 #pragma unroll
         for (int i = 0; i < RT_NUM_COUNTERS_INTERNAL; ++i) {
             uint32_t v = cnt.c[i];
 #pragma unroll
-            for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(FULL, v, off);
+            for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
             if (lane == 0 && v) atomicAdd(&P.counters[i], (unsigned long long)v);
         }
     }
@@ -466,7 +462,11 @@ static const void* trace_fn(unsigned flags) {
                  : (brute ? (const void*)k_trace_stereo<false, true> : (const void*)k_trace_stereo<false, false>);
 }
 
-size_t rtb_trace_smem(int stack_entries) { return (size_t)stack_entries * 256 * sizeof(int); }
+size_t rtb_trace_smem(int stack_entries) {
+    return (size_t)RQ_SMEM * 32 + 256 * 24 + 256 * 4 + (size_t)stack_entries * 256 * sizeof(int);
+}
+
+int rtb_rq_overflow_entries(int max_depth) { return 256 * (max_depth + 2); }
 
 cudaError_t rtb_launch_trace(const TraceParams& P, unsigned flags, int grid, cudaStream_t st) {
     const size_t smem = rtb_trace_smem(P.stack_entries);

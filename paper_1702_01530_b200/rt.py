@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "librt_b200.so")
+LIB_PATH = os.environ.get("RT_LIB_PATH") or os.path.join(_HERE, "lib", "librt_b200.so")   # override: experiments only
 
 RT_OK, RT_ERR_INVALID_ARG, RT_ERR_CUDA, RT_ERR_OOM, RT_ERR_NO_SCENE, RT_ERR_NO_CAMERA, RT_ERR_SIZE, \
     RT_ERR_NOT_READY, RT_ERR_PEER = range(9)
