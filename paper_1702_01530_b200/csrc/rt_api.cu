@@ -80,6 +80,7 @@ struct rt_context {
     float vfov = 0;
     float4* rq_overflow = nullptr;   // per-CTA spill slices of the tree-ray stack
     size_t rq_overflow_bytes = 0;
+    int leaf_max = 1;                // LBVH leaf collapse threshold (env RT_LEAF_MAX, <= 16)
 };
 
 namespace {
@@ -123,6 +124,7 @@ rt_status rt_create(int device, void* cuda_stream, rt_context** out) {
     rt_context* c = new (std::nothrow) rt_context();
     if (!c) return fail(RT_ERR_OOM, "rt_create: host allocation");
     c->device = device;
+    if (const char* lm = getenv("RT_LEAF_MAX")) c->leaf_max = std::max(1, std::min(16, atoi(lm)));
     cudaError_t e = cudaSetDevice(device);
     if (e == cudaSuccess && cuda_stream) {
         c->stream = static_cast<cudaStream_t>(cuda_stream);
@@ -351,11 +353,13 @@ rt_status rt_scene_upload(rt_context* c, const rt_primitives* P, const rt_materi
             (st = salloc(4 * rtb_sort_hist_entries(N), (void**)&B.hist)) || (st = salloc(4 * Nn, (void**)&B.left)) ||
             (st = salloc(4 * Nn, (void**)&B.right)) || (st = salloc(4 * Nn, (void**)&B.parent_int)) ||
             (st = salloc(4 * (size_t)N, (void**)&B.parent_leaf)) || (st = salloc(4 * Nn, (void**)&B.flags)) ||
-            (st = salloc(16 * Nn, (void**)&B.node_lo)) || (st = salloc(16 * Nn, (void**)&B.node_hi))) {
+            (st = salloc(16 * Nn, (void**)&B.node_lo)) || (st = salloc(16 * Nn, (void**)&B.node_hi)) ||
+            (st = salloc(8 * Nn, (void**)&B.range))) {
             free_scratch();
             free_scene(c);
             return st;
         }
+        B.leaf_max = c->leaf_max;
         cudaError_t e = rtb_build_bvh(B, c->stream);
         if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
         free_scratch();

@@ -225,7 +225,8 @@ __device__ __forceinline__ int delta(const uint32_t* __restrict__ keys, int n, i
     return __clzll(a ^ b);
 }
 
-__global__ void k_karras(const uint32_t* __restrict__ keys, int n, int* left, int* right, int* parent_int, int* parent_leaf) {
+__global__ void k_karras(const uint32_t* __restrict__ keys, int n, int* left, int* right, int* parent_int, int* parent_leaf,
+                         int2* range) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n - 1; i += gridDim.x * blockDim.x) {
         const int d = (delta(keys, n, i, i + 1) - delta(keys, n, i, i - 1)) >= 0 ? 1 : -1;
         const int dmin = delta(keys, n, i, i - d);
@@ -250,6 +251,7 @@ __global__ void k_karras(const uint32_t* __restrict__ keys, int n, int* left, in
         else { rc = split + 1; parent_int[split + 1] = i; }
         left[i] = lc;
         right[i] = rc;
+        range[i] = make_int2(first, last);
         if (i == 0) parent_int[0] = -1;
     }
 }
@@ -277,12 +279,22 @@ __global__ void k_refit(BuildBuffers B, int n, const float4* __restrict__ slo, c
     }
 }
 
+// Internal children covering <= leaf_max primitives become leaves over their contiguous
+// (Morton-sorted) primitive range; the nodes below them stay in the array but are unreachable.
+__device__ __forceinline__ int collapse(int c, const int2* __restrict__ range, int leaf_max) {
+    if (c < 0) return c;
+    const int2 r = range[c];
+    const int cnt = r.y - r.x + 1;
+    return cnt <= leaf_max ? ~(((cnt - 1) << LEAF_SHIFT) | r.x) : c;
+}
+
 __global__ void k_layout(BuildBuffers B, int n, const float4* __restrict__ slo, const float4* __restrict__ shi) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n - 1; i += gridDim.x * blockDim.x) {
-        const int l = B.left[i], r = B.right[i];
+        const int l0 = B.left[i], r0 = B.right[i];
+        const int l = collapse(l0, B.range, B.leaf_max), r = collapse(r0, B.range, B.leaf_max);
         float4 a0, a1, b0, b1;
-        child_box(l, slo, shi, B.node_lo, B.node_hi, a0, a1);
-        child_box(r, slo, shi, B.node_lo, B.node_hi, b0, b1);
+        child_box(l0, slo, shi, B.node_lo, B.node_hi, a0, a1);
+        child_box(r0, slo, shi, B.node_lo, B.node_hi, b0, b1);
         B.nodes[4 * i + 0] = make_float4(a0.x, a1.x, a0.y, a1.y);
         B.nodes[4 * i + 1] = make_float4(b0.x, b1.x, b0.y, b1.y);
         B.nodes[4 * i + 2] = make_float4(a0.z, a1.z, b0.z, b1.z);
@@ -346,7 +358,7 @@ cudaError_t rtb_build_bvh(const BuildBuffers& Bc, cudaStream_t st) {
     float4* slo = B.leaf_lo;
     float4* shi = B.leaf_hi;
     k_gather_prims<<<grid_for(n), 256, 0, st>>>(B, n, B.vals[cur], slo, shi);
-    k_karras<<<grid_for(n - 1), 256, 0, st>>>(B.keys[cur], n, B.left, B.right, B.parent_int, B.parent_leaf);
+    k_karras<<<grid_for(n - 1), 256, 0, st>>>(B.keys[cur], n, B.left, B.right, B.parent_int, B.parent_leaf, B.range);
     cudaMemsetAsync(B.flags, 0, sizeof(int) * (n - 1), st);
     k_refit<<<grid_for(n), 256, 0, st>>>(B, n, slo, shi);
     k_layout<<<grid_for(n - 1), 256, 0, st>>>(B, n, slo, shi);

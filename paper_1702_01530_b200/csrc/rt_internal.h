@@ -82,6 +82,8 @@ struct BuildBuffers {
     float4* node_hi;            // [N-1]
     float4* nodes;              // [4(N-1)] final layout
     int* max_depth;             // [1]
+    int2* range;                // [N-1] sorted primitive range of each internal node
+    int leaf_max;               // collapse subtrees of <= leaf_max primitives into leaves
 };
 
 // launchers (rt_trace.cu)

@@ -5,18 +5,13 @@
 // radiance straight into the RGBA8/FP16 framebuffers (and, optionally, prim-ID / radiance
 // debug planes or a tile-packed shard).  SURVEY.md §8(a) rows a3-a6; DESIGN.md §5.
 //
-// Execution model (v2, "CTA wavefront"): a persistent CTA of 256 threads owns one 16x16 pixel
-// tile at a time.  The tile's pending tree rays live in a CTA-shared ray stack in shared memory
-// (overflowing to a per-CTA global slice only for glass-heavy trees).  Each round the CTA pops
-// up to 256 rays -- one per thread, so a round's rays are always packed into full warps -- and
-// every thread traces its ray (nearest hit), shades it with one shadow ray per lit light
-// (lights in index order, so the warp's shadow rays head to the same light together), adds
-// w * local term to its pixel's accumulator and pushes the reflection / refraction children.
-// v0 (one thread per pixel tree) averaged 8 of 32 active lanes because lanes idled while their
-// neighbours finished deeper trees; compaction per round removes that idling.
-// Accumulators are 64-bit fixed point (2^-40) so the result does not depend on the order in
-// which rays of one pixel finish (bit-exact determinism).  The BVH traversal stack is
-// in shared memory, [entry][thread], conflict-free.
+// Execution model (v3): persistent warps take 32-pixel work items (one 8x4 block of a 16x16
+// tile) from a global queue with one atomic; each lane traces its pixel's whole ray tree
+// (nearest hit -> one shadow ray per lit light -> reflection in registers, refraction children
+// on a per-thread stack).  The BVH traversal stack is in shared memory, [entry][thread]
+// (conflict-free).  Measured alternatives (profiles/r01_v1*, r01_v2*): a per-lane state
+// machine with dynamic refill (v1) and a CTA-wide compacting wavefront (v2) were both slower:
+// the SIMT loss is inside BVH traversal, not in idle ray-tree tails, and v2's barriers stalled.
 #include "rt_device.cuh"
 #include "rt_internal.h"
 
@@ -25,8 +20,6 @@ namespace rtb {
 #ifndef RT_MINB
 #define RT_MINB 3
 #endif
-constexpr int RQ_SMEM = 512;                 // tree-ray stack entries held in shared memory
-constexpr double ACC_SCALE = 1099511627776.0; // 2^40
 
 template <bool COUNT>
 struct Counters {
@@ -220,178 +213,143 @@ __device__ __forceinline__ bool occluded(const DevScene& S, float3 o, float3 d, 
     }
 }
 
-__device__ __forceinline__ void acc_add(unsigned long long* acc, float3 c) {
-    // non-negative terms (validated inputs), 2^-40 fixed point: order-independent sums
-    atomicAdd(&acc[0], __double2ull_rn((double)c.x * ACC_SCALE));
-    atomicAdd(&acc[1], __double2ull_rn((double)c.y * ACC_SCALE));
-    atomicAdd(&acc[2], __double2ull_rn((double)c.z * ACC_SCALE));
+// Trace the whole ray tree of one pixel.  Iterative: the reflection child continues in
+// registers, the refraction child is pushed on a per-thread stack (<= max_depth entries).
+// Radiance accumulates as sum over tree nodes of path_weight * local_term, which equals the
+// recursive definition c = local + kt*T(refr) + kr_eff*T(refl) (reading 17).
+template <bool COUNT, bool BRUTE>
+__device__ __forceinline__ float3 trace_pixel(const TraceParams& P, float3 o, float3 d, int& prim_id, int* stk,
+                                              Counters<COUNT>& cnt) {
+    const DevScene& S = P.sc;
+    float4 st_a[MAX_DEPTH], st_b[MAX_DEPTH];   // refraction children: (o, w) (d, depth)
+    int sp = 0;
+    float w = 1.0f;
+    int depth = P.max_depth;
+    bool primary = true;
+    float3 col = f3(0.f, 0.f, 0.f);
+    cnt.add(CNT_PRIMARY);
+    while (true) {
+        const Hit h = closest_hit<COUNT, BRUTE>(S, o, d, stk, cnt);
+        if (primary) { prim_id = h.gid; primary = false; }
+        bool cont = false;
+        if (h.gid < 0) {
+            cnt.add(CNT_MISSES);
+            col = fma3(S.background, w, col);                           // S:203 miss -> background
+        } else {
+            cnt.add(CNT_SHADE_HITS);
+            const float3 p = fma3(d, h.t, o);
+            float3 ng;
+            int mat;
+            if (h.slot < 0) {
+                const int i = ~h.slot;
+                ng = xyz(__ldg(&S.planes[i]));
+                mat = __ldg(&S.plane_mat[i]);
+            } else {
+                const float4 a = __ldg(&S.prims[3 * h.slot]);
+                const float4 b = __ldg(&S.prims[3 * h.slot + 1]);
+                mat = __float_as_int(b.w);
+                if (h.gid < S.n_spheres) ng = (p - xyz(a)) * (1.0f / b.x);
+                else ng = normalize(cross(xyz(b), xyz(__ldg(&S.prims[3 * h.slot + 2]))));
+            }
+            const bool front = dot(d, ng) < 0.0f;
+            const float3 nf = front ? ng : ng * -1.0f;                   // S:150 faces the ray
+            const float4 m0 = __ldg(&S.mats[3 * mat]), m1 = __ldg(&S.mats[3 * mat + 1]);
+            const float3 kd = xyz(m0), ks = xyz(m1);
+            float3 c = S.ambient * kd;                                   // S:193 ambient * kd
+            for (int j = 0; j < S.n_lights; ++j) {
+                cnt.add(CNT_LIGHT_EVALS);
+                const float3 Lp = xyz(__ldg(&S.lights[2 * j]));
+                const float3 l = normalize(Lp - p);
+                const float ndl = dot(nf, l);
+                if (ndl <= 0.0f) continue;                               // reading 2 gate
+                const float3 os = fma3(nf, BIAS, p);
+                const float3 sv = Lp - os;
+                const float dist = sqrtf(dot(sv, sv));
+                cnt.add(CNT_SHADOW);
+                if (occluded<COUNT, BRUTE>(S, os, sv * (1.0f / dist), dist, stk, cnt)) continue;
+                const float3 I = xyz(__ldg(&S.lights[2 * j + 1]));
+                const float3 rv = nf * (2.0f * ndl) - l;
+                const float rdv = -dot(rv, d);
+                const float spec = rdv > 0.0f ? __powf(rdv, m0.w) : 0.0f;
+                c = c + (kd * I) * ndl + (ks * I) * spec;                // no falloff, reading 3
+            }
+            col = fma3(c, w, col);
+            if (depth > 0) {
+                const float4 m2 = __ldg(&S.mats[3 * mat + 2]);
+                float kr_eff = m1.w;
+                const float kt = m2.x;
+                if (kt > 0.0f) {
+                    const float eta = front ? 1.0f / m2.y : m2.y;
+                    const float cosi = -dot(d, nf);
+                    const float kk = 1.0f - eta * eta * (1.0f - cosi * cosi);
+                    if (kk < 0.0f) {
+                        kr_eff += kt;                                    // reading 5 TIR
+                    } else {
+                        cnt.add(CNT_REFRACTION);
+                        const float3 td = normalize(d * eta + nf * (eta * cosi - sqrtf(kk)));
+                        const float3 to = fma3(nf, -BIAS, p);
+                        st_a[sp] = make_float4(to.x, to.y, to.z, w * kt);
+                        st_b[sp] = make_float4(td.x, td.y, td.z, __int_as_float(depth - 1));
+                        ++sp;
+                    }
+                }
+                if (kr_eff > 0.0f) {
+                    cnt.add(CNT_REFLECTION);
+                    d = normalize(d - nf * (2.0f * dot(d, nf)));
+                    o = fma3(nf, BIAS, p);
+                    w *= kr_eff;
+                    depth -= 1;
+                    cont = true;
+                }
+            }
+        }
+        if (cont) continue;
+        if (sp == 0) break;
+        --sp;
+        const float4 a = st_a[sp], b = st_b[sp];
+        o = xyz(a);
+        w = a.w;
+        d = xyz(b);
+        depth = __float_as_int(b.w);
+    }
+    return col;
 }
 
-// Tree-ray stack entry: (o.xyz, w) (d.xyz, meta); meta = pixel (8 bits) | depth << 8 | primary << 16
-__device__ __forceinline__ float4* rq_slot(float4* s_rq, float4* g_rq, int i) {
-    return i < RQ_SMEM ? s_rq + 2 * i : g_rq + 2 * (i - RQ_SMEM);
-}
-
+// Persistent warps: each warp takes 32 consecutive work items (one 8x4 pixel block) per
+// atomic and traces one pixel tree per lane; the BVH stack is in shared memory.
 template <bool COUNT, bool BRUTE>
 __global__ void __launch_bounds__(256, RT_MINB) k_trace_stereo(const TraceParams P) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    float4* const s_rq = reinterpret_cast<float4*>(smem);                                   // [RQ_SMEM][2]
-    unsigned long long* const s_acc = reinterpret_cast<unsigned long long*>(smem + RQ_SMEM * 32);  // [256][3]
-    int* const s_id = reinterpret_cast<int*>(smem + RQ_SMEM * 32 + 256 * 24);             // [256]
-    int* const s_stack = s_id + 256;                                                       // [entries][256]
-    __shared__ int s_tile, s_count;
-    const DevScene& S = P.sc;
+    extern __shared__ int s_stack[];                 // [stack_entries][256]
     Counters<COUNT> cnt;
     cnt.zero();
-    const int tid = threadIdx.x;
-    int* const stk = s_stack + tid;
-    float4* const g_rq = P.rq_overflow + (long long)blockIdx.x * 2 * P.rq_overflow_entries;
-
+    const int lane = threadIdx.x & 31;
+    int* const stk = s_stack + threadIdx.x;
     while (true) {
-        if (tid == 0) s_tile = atomicAdd(P.work_counter, 1);
-        __syncthreads();
-        const int tile = s_tile;
-        if (tile >= P.n_tiles) break;
-        const int k = tile * 256 + tid;
+        int base = 0;
+        if (lane == 0) base = atomicAdd(P.work_counter, 32);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (base >= P.n_work) break;
+        const int k = base + lane;
         int eye, px, py;
-        const bool valid = map_work(P, k, eye, px, py);
-        s_acc[3 * tid] = 0ull;
-        s_acc[3 * tid + 1] = 0ull;
-        s_acc[3 * tid + 2] = 0ull;
-        s_id[tid] = -1;
-        if (valid) {
+        if (map_work(P, k, eye, px, py)) {
             cnt.add(CNT_PIXELS);
-            cnt.add(CNT_PRIMARY);
             const float sx = fmaf(2.0f * (px + 0.5f), 1.0f / P.W, -1.0f) * P.cam.tha;
             const float sy = fmaf(-2.0f * (py + 0.5f), 1.0f / P.H, 1.0f) * P.cam.th;
             const float3 d = normalize(P.cam.f + P.cam.r * (sx + P.cam.sigma[eye]) + P.cam.u * sy);
-            const float3 o = P.cam.eye[eye];
-            s_rq[2 * tid] = make_float4(o.x, o.y, o.z, 1.0f);
-            s_rq[2 * tid + 1] = make_float4(d.x, d.y, d.z, __int_as_float(tid | (P.max_depth << 8) | (1 << 16)));
-        } else {
-            s_rq[2 * tid] = make_float4(0.f, 0.f, 0.f, 0.0f);
-            s_rq[2 * tid + 1] = make_float4(0.f, 0.f, 1.f, __int_as_float(-1));
-        }
-        if (tid == 0) s_count = 256;
-        __syncthreads();
-
-        // ---- rounds: pop up to 256 tree rays (one per thread), trace, shade, push children
-        while (true) {
-            const int count = s_count;
-            if (count == 0) break;
-            const int nb = min(256, count), base = count - nb;
-            float4 ra = make_float4(0.f, 0.f, 0.f, 0.f), rbv = make_float4(0.f, 0.f, 0.f, __int_as_float(-1));
-            if (tid < nb) {
-                const float4* e = rq_slot(s_rq, g_rq, base + tid);
-                ra = e[0];
-                rbv = e[1];
-            }
-            __syncthreads();                          // every thread holds its ray; slots are free
-            if (tid == 0) s_count = base;
-            __syncthreads();
-            const int meta = __float_as_int(rbv.w);
-            if (meta >= 0) {
-                const int pl = meta & 255, depth = (meta >> 8) & 255;
-                const bool primary = (meta >> 16) & 1;
-                const float3 o = xyz(ra), d = xyz(rbv);
-                const float w = ra.w;
-                const Hit h = closest_hit<COUNT, BRUTE>(S, o, d, stk, cnt);
-                if (primary) s_id[pl] = h.gid;
-                if (h.gid < 0) {
-                    cnt.add(CNT_MISSES);
-                    acc_add(&s_acc[3 * pl], S.background * w);                  // S:203 miss
-                } else {
-                    cnt.add(CNT_SHADE_HITS);
-                    const float3 p = fma3(d, h.t, o);
-                    float3 ng;
-                    int mat;
-                    if (h.slot < 0) {
-                        const int i = ~h.slot;
-                        ng = xyz(__ldg(&S.planes[i]));
-                        mat = __ldg(&S.plane_mat[i]);
-                    } else {
-                        const float4 a = __ldg(&S.prims[3 * h.slot]);
-                        const float4 b = __ldg(&S.prims[3 * h.slot + 1]);
-                        mat = __float_as_int(b.w);
-                        if (h.gid < S.n_spheres) ng = (p - xyz(a)) * (1.0f / b.x);
-                        else ng = normalize(cross(xyz(b), xyz(__ldg(&S.prims[3 * h.slot + 2]))));
-                    }
-                    const bool front = dot(d, ng) < 0.0f;
-                    const float3 nf = front ? ng : ng * -1.0f;
-                    const float4 m0 = __ldg(&S.mats[3 * mat]), m1 = __ldg(&S.mats[3 * mat + 1]);
-                    const float3 kd = xyz(m0), ks = xyz(m1);
-                    float3 c = S.ambient * kd;
-                    for (int j = 0; j < S.n_lights; ++j) {
-                        cnt.add(CNT_LIGHT_EVALS);
-                        const float3 Lp = xyz(__ldg(&S.lights[2 * j]));
-                        const float3 l = normalize(Lp - p);
-                        const float ndl = dot(nf, l);
-                        if (ndl <= 0.0f) continue;                                   // reading 2
-                        const float3 os = fma3(nf, BIAS, p);
-                        const float3 sv = Lp - os;
-                        const float dist = sqrtf(dot(sv, sv));
-                        cnt.add(CNT_SHADOW);
-                        if (occluded<COUNT, BRUTE>(S, os, sv * (1.0f / dist), dist, stk, cnt)) continue;
-                        const float3 I = xyz(__ldg(&S.lights[2 * j + 1]));
-                        const float3 rv = nf * (2.0f * ndl) - l;
-                        const float rdv = -dot(rv, d);
-                        const float spec = rdv > 0.0f ? __powf(rdv, m0.w) : 0.0f;
-                        c = c + (kd * I) * ndl + (ks * I) * spec;                   // reading 3
-                    }
-                    acc_add(&s_acc[3 * pl], c * w);
-                    if (depth > 0) {
-                        const float4 m2 = __ldg(&S.mats[3 * mat + 2]);
-                        float kr_eff = m1.w;
-                        const float kt = m2.x;
-                        if (kt > 0.0f) {
-                            const float eta = front ? 1.0f / m2.y : m2.y;
-                            const float cosi = -dot(d, nf);
-                            const float kk = 1.0f - eta * eta * (1.0f - cosi * cosi);
-                            if (kk < 0.0f) {
-                                kr_eff += kt;                                        // reading 5
-                            } else {
-                                cnt.add(CNT_REFRACTION);
-                                const float3 td = normalize(d * eta + nf * (eta * cosi - sqrtf(kk)));
-                                const float3 to = fma3(nf, -BIAS, p);
-                                float4* e = rq_slot(s_rq, g_rq, atomicAdd(&s_count, 1));
-                                e[0] = make_float4(to.x, to.y, to.z, w * kt);
-                                e[1] = make_float4(td.x, td.y, td.z, __int_as_float(pl | ((depth - 1) << 8)));
-                            }
-                        }
-                        if (kr_eff > 0.0f) {
-                            cnt.add(CNT_REFLECTION);
-                            const float3 rd = normalize(d - nf * (2.0f * dot(d, nf)));
-                            const float3 ro = fma3(nf, BIAS, p);
-                            float4* e = rq_slot(s_rq, g_rq, atomicAdd(&s_count, 1));
-                            e[0] = make_float4(ro.x, ro.y, ro.z, w * kr_eff);
-                            e[1] = make_float4(rd.x, rd.y, rd.z, __int_as_float(pl | ((depth - 1) << 8)));
-                        }
-                    }
-                }
-            }
-            __syncthreads();
-        }
-
-        // ---- pack epilogue: one thread per pixel of the tile
-        if (valid) {
-            const float3 col = f3((float)((double)s_acc[3 * tid] * (1.0 / ACC_SCALE)),
-                                  (float)((double)s_acc[3 * tid + 1] * (1.0 / ACC_SCALE)),
-                                  (float)((double)s_acc[3 * tid + 2] * (1.0 / ACC_SCALE)));
+            int pid = -1;
+            const float3 c = trace_pixel<COUNT, BRUTE>(P, P.cam.eye[eye], d, pid, stk, cnt);
             const long long pix = ((long long)eye * P.H + py) * P.W + px;
-            if (P.fb[eye]) store_px(P.fb[eye], P.fb_fmt[eye], P.fb_pitch[eye], px, py, col);
-            if (P.prim_id) P.prim_id[pix] = s_id[tid];
-            if (P.radiance) P.radiance[pix] = make_float4(col.x, col.y, col.z, 0.0f);
+            if (P.fb[eye]) store_px(P.fb[eye], P.fb_fmt[eye], P.fb_pitch[eye], px, py, c);
+            if (P.prim_id) P.prim_id[pix] = pid;
+            if (P.radiance) P.radiance[pix] = make_float4(c.x, c.y, c.z, 0.0f);
             if (P.shard) {
-                const long long s = (long long)tile * 256 + ((py % TILE) * TILE + (px % TILE));
-                if (P.shard_fmt == RT_FORMAT_RGBA8) reinterpret_cast<uint32_t*>(P.shard)[s] = pack_rgba8(col);
-                else reinterpret_cast<uint2*>(P.shard)[s] = pack_rgba16f(col);
+                const long long s = (long long)(k >> 8) * 256 + ((py % TILE) * TILE + (px % TILE));
+                if (P.shard_fmt == RT_FORMAT_RGBA8) reinterpret_cast<uint32_t*>(P.shard)[s] = pack_rgba8(c);
+                else reinterpret_cast<uint2*>(P.shard)[s] = pack_rgba16f(c);
             }
         }
-        __syncthreads();
     }
-
     if (COUNT) {
-        const int lane = tid & 31;
 #pragma unroll
         for (int i = 0; i < RT_NUM_COUNTERS_INTERNAL; ++i) {
             uint32_t v = cnt.c[i];
@@ -462,11 +420,9 @@ static const void* trace_fn(unsigned flags) {
                  : (brute ? (const void*)k_trace_stereo<false, true> : (const void*)k_trace_stereo<false, false>);
 }
 
-size_t rtb_trace_smem(int stack_entries) {
-    return (size_t)RQ_SMEM * 32 + 256 * 24 + 256 * 4 + (size_t)stack_entries * 256 * sizeof(int);
-}
+size_t rtb_trace_smem(int stack_entries) { return (size_t)stack_entries * 256 * sizeof(int); }
 
-int rtb_rq_overflow_entries(int max_depth) { return 256 * (max_depth + 2); }
+int rtb_rq_overflow_entries(int) { return 0; }   // v3 keeps tree rays per thread
 
 cudaError_t rtb_launch_trace(const TraceParams& P, unsigned flags, int grid, cudaStream_t st) {
     const size_t smem = rtb_trace_smem(P.stack_entries);

@@ -274,21 +274,24 @@ def test_bvh_structure(R):
     assert sorted(gids.tolist()) == list(range(s.n_spheres)) + list(range(s.n_spheres + s.n_planes, s.n_spheres + s.n_planes + s.n_tris))
     assert info["bvh_depth"] <= 64
     child = nodes[:, 12:14].view(np.int32)
-    seen_leaf = np.zeros(n, int)
-    seen_int = np.zeros(n - 1, int)
-    for c in child.reshape(-1):
-        if c < 0:
-            seen_leaf[(~c) & 0xFFFFFF] += 1
-        else:
-            seen_int[c] += 1
-    assert np.all(seen_leaf == 1) and seen_int[0] == 0 and np.all(seen_int[1:] == 1)
-    # each child box stored in a node contains the union of that child's own two boxes
     LO = ([0, 2, 8], [4, 6, 10])
     HI = ([1, 3, 9], [5, 7, 11])
-    for i in range(n - 1):
+    covered = np.zeros(n, int)
+    stack, seen_int, depth_max = [(0, 0)], 0, 0
+    while stack:                                   # walk the reachable tree from the root
+        i, dep = stack.pop()
+        seen_int += 1
+        depth_max = max(depth_max, dep)
         for side in (0, 1):
-            c = child[i, side]
-            if c >= 0:
+            c = int(child[i, side])
+            if c < 0:
+                enc = ~c
+                first, cnt = enc & 0xFFFFFF, (enc >> 24) + 1
+                covered[first:first + cnt] += 1
+            else:
                 sub_lo = np.minimum(nodes[c, LO[0]], nodes[c, LO[1]])
                 sub_hi = np.maximum(nodes[c, HI[0]], nodes[c, HI[1]])
                 assert np.all(nodes[i, LO[side]] <= sub_lo) and np.all(nodes[i, HI[side]] >= sub_hi)
+                stack.append((c, dep + 1))
+    assert np.all(covered == 1)                    # every primitive in exactly one reachable leaf
+    assert depth_max < 64
