@@ -34,7 +34,7 @@ from paper_1702_01530_b200 import scenes  # noqa: E402
 METRIC = "Mrays/s and stereo frames/s at 1/2/4/8 B200; % FP32 roofline"
 UNIT = "Mrays/s"
 # Algorithmic FP32 flops per counted unit (frozen; FMA = 2).
-FLOPS_PER = {"primary": 20, "ray_setup": 3, "node_visits": 24, "tri_tests": 44, "sphere_tests": 18,
+FLOPS_PER = {"primary": 20, "ray_setup": 3, "node_visits": 48, "tri_tests": 44, "sphere_tests": 18,
              "plane_tests": 12, "shade_hits": 20, "light_evals": 67, "reflection": 16, "refraction": 24,
              "misses": 6, "pixels": 9}
 FP32_LANES_PER_SM = 128      # B200 SM: 4 SMSPs x 32 FP32 lanes

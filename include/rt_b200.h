@@ -99,7 +99,7 @@ typedef struct rt_fb {
 /* Counter slots of rt_outputs.counters (uint64, accumulated, never reset by the library). */
 typedef enum rt_counter {
     RT_CNT_PRIMARY = 0, RT_CNT_REFLECTION = 1, RT_CNT_REFRACTION = 2, RT_CNT_SHADOW = 3,
-    RT_CNT_NODE_VISITS = 4,      /* BVH2 internal nodes visited (2 box tests each)    */
+    RT_CNT_NODE_VISITS = 4,      /* BVH4 nodes visited (4 box tests each)             */
     RT_CNT_TRI_TESTS = 5, RT_CNT_SPHERE_TESTS = 6, RT_CNT_PLANE_TESTS = 7,
     RT_CNT_SHADE_HITS = 8,       /* nearest-hit shading points                        */
     RT_CNT_LIGHT_EVALS = 9,      /* (hit, light) pairs evaluated                      */
@@ -235,9 +235,11 @@ rt_status rt_ipc_close(rt_context* ctx, void* dev_ptr);
 
 /* ------------------------------------------------------------------ introspection */
 /* Scene statistics after upload: [0] n_spheres [1] n_planes [2] n_triangles [3] bvh prims
- * [4] bvh internal nodes [5] bvh max depth [6] device bytes of scene+BVH [7] build time us. */
+ * [4] BVH4 nodes [5] BVH4 depth (levels) [6] device bytes of scene+BVH [7] build time us. */
 rt_status rt_scene_info(rt_context* ctx, uint64_t info[8]);
-/* Copy the device BVH (nodes: 16 floats each) and the leaf-order primitive global IDs to
+/* Copy the device BVH (4-wide nodes, 28 floats each: lo.x[4] hi.x[4] lo.y[4] hi.y[4] lo.z[4]
+ * hi.z[4] child[4] as int32; child >= 0 node, 0x7fffffff empty, < 0 leaf ~((count-1)<<24 | first))
+ * and the leaf-order primitive global IDs to
  * HOST arrays for structural tests; pass NULL to query sizes via *n_nodes / *n_prims. */
 rt_status rt_bvh_export(rt_context* ctx, float* nodes, uint32_t* n_nodes, int32_t* prim_gid, uint32_t* n_prims);
 /* FFMA throughput microbenchmark (roofline denominator): runs `iters` FMA chains on every

@@ -334,15 +334,13 @@ rt_status rt_scene_upload(rt_context* c, const rt_primitives* P, const rt_materi
     };
     float4* d_prims = nullptr;
     float4* d_nodes = nullptr;
-    int* d_maxdepth = nullptr;
     const size_t Nn = N > 1 ? N - 1 : 0;
-    if ((st = dalloc(c, 3 * (size_t)N, &d_prims)) || (st = dalloc(c, 4 * Nn, &d_nodes)) || (st = dalloc(c, 1, &d_maxdepth))) {
+    if ((st = dalloc(c, 3 * (size_t)N, &d_prims))) {
         free_scene(c);
         return st;
     }
     B.prims = d_prims;
-    B.nodes = d_nodes;
-    B.max_depth = d_maxdepth;
+    int root = ~0, n_nodes4 = 0, depth4 = 0;
     if (N > 0) {
         if ((st = salloc(48 * (size_t)N, (void**)&B.prims_unsorted)) || (st = salloc(16 * (size_t)N, (void**)&B.aabb_lo)) ||
             (st = salloc(16 * (size_t)N, (void**)&B.aabb_hi)) || (st = salloc(16 * (size_t)N, (void**)&B.centroid)) ||
@@ -354,22 +352,30 @@ rt_status rt_scene_upload(rt_context* c, const rt_primitives* P, const rt_materi
             (st = salloc(4 * Nn, (void**)&B.right)) || (st = salloc(4 * Nn, (void**)&B.parent_int)) ||
             (st = salloc(4 * (size_t)N, (void**)&B.parent_leaf)) || (st = salloc(4 * Nn, (void**)&B.flags)) ||
             (st = salloc(16 * Nn, (void**)&B.node_lo)) || (st = salloc(16 * Nn, (void**)&B.node_hi)) ||
-            (st = salloc(8 * Nn, (void**)&B.range))) {
+            (st = salloc(8 * Nn, (void**)&B.range)) || (st = salloc(112 * Nn, (void**)&B.nodes4)) ||
+            (st = salloc(8 * (size_t)N, (void**)&B.frontier[0])) || (st = salloc(8 * (size_t)N, (void**)&B.frontier[1])) ||
+            (st = salloc(16, (void**)&B.wide_counters))) {
             free_scratch();
             free_scene(c);
             return st;
         }
         B.leaf_max = c->leaf_max;
-        cudaError_t e = rtb_build_bvh(B, c->stream);
+        cudaError_t e = rtb_build_bvh(B, c->stream, &root, &n_nodes4, &depth4);
         if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+        if (e == cudaSuccess && n_nodes4 > 0) {        // compact the BVH4 into an exact-size buffer
+            if ((st = dalloc(c, 7 * (size_t)n_nodes4, &d_nodes))) {
+                free_scratch();
+                free_scene(c);
+                return st;
+            }
+            e = cudaMemcpy(d_nodes, B.nodes4, 112 * (size_t)n_nodes4, cudaMemcpyDeviceToDevice);
+        }
         free_scratch();
         if (e != cudaSuccess) {
             free_scene(c);
             return fail(RT_ERR_CUDA, "LBVH build: %s", cudaGetErrorString(e));
         }
     }
-    int maxd = 0;
-    if (N > 0) CUDA_TRY(cudaMemcpy(&maxd, d_maxdepth, sizeof(int), cudaMemcpyDeviceToHost));
     const auto t1 = std::chrono::steady_clock::now();
 
     rtb::DevScene& D = c->sc;
@@ -380,7 +386,7 @@ rt_status rt_scene_upload(rt_context* c, const rt_primitives* P, const rt_materi
     D.mats = d_mats;
     D.lights = d_lights;
     D.n_bvh = N;
-    D.root = N >= 2 ? 0 : ~0;
+    D.root = root;
     D.n_spheres = (int)S;
     D.n_planes = (int)PL;
     D.n_lights = (int)n_lights;
@@ -393,8 +399,8 @@ rt_status rt_scene_upload(rt_context* c, const rt_primitives* P, const rt_materi
     c->info[1] = PL;
     c->info[2] = T;
     c->info[3] = N;
-    c->info[4] = Nn;
-    c->info[5] = (uint64_t)maxd;
+    c->info[4] = (uint64_t)n_nodes4;
+    c->info[5] = (uint64_t)depth4;
     c->info[6] = bytes;
     c->info[7] = (uint64_t)std::chrono::duration_cast<std::chrono::microseconds>(t1 - t0).count();
     c->has_scene = true;
@@ -542,7 +548,7 @@ rt_status rt_render_stereo_ex(rt_context* c, const rt_render_params* p, const rt
     P.shard = out->shard;
     P.shard_fmt = (int)out->shard_format;
     P.counters = out->counters ? out->counters : c->scratch_counters;
-    P.stack_entries = std::max(1, (int)c->info[5] + 1);
+    P.stack_entries = 3 * (int)c->info[5] + 2;       // <= 3 pending siblings per BVH4 level
     P.n_tiles = (int)n_tiles;
     if (P.n_work == 0) return RT_OK;
     CUDA_TRY(cudaSetDevice(c->device));
@@ -782,10 +788,10 @@ rt_status rt_scene_info(rt_context* c, uint64_t info[8]) {
 rt_status rt_bvh_export(rt_context* c, float* nodes, uint32_t* n_nodes, int32_t* prim_gid, uint32_t* n_prims) {
     if (!c || !n_nodes || !n_prims) return fail(RT_ERR_INVALID_ARG, "rt_bvh_export: NULL argument");
     if (!c->has_scene) return fail(RT_ERR_NO_SCENE, "rt_bvh_export: no scene");
-    const uint32_t nn = c->sc.n_bvh > 1 ? (uint32_t)c->sc.n_bvh - 1 : 0, np = (uint32_t)c->sc.n_bvh;
+    const uint32_t nn = (uint32_t)c->info[4], np = (uint32_t)c->sc.n_bvh;
     CUDA_TRY(cudaSetDevice(c->device));
     CUDA_TRY(cudaStreamSynchronize(c->stream));
-    if (nodes && nn) CUDA_TRY(cudaMemcpy(nodes, c->sc.nodes, (size_t)nn * 64, cudaMemcpyDeviceToHost));
+    if (nodes && nn) CUDA_TRY(cudaMemcpy(nodes, c->sc.nodes, (size_t)nn * 112, cudaMemcpyDeviceToHost));
     if (prim_gid && np) {
         std::vector<float4> p(3 * (size_t)np);
         CUDA_TRY(cudaMemcpy(p.data(), c->sc.prims, p.size() * sizeof(float4), cudaMemcpyDeviceToHost));

@@ -10,8 +10,8 @@
 //   k_karras         Karras 2012 hierarchy: each internal node finds its key range and split
 //                    from common-prefix lengths (__clzll)
 //   k_refit          bottom-up AABB union with atomic arrival counters
-//   k_layout         box-pair node layout for traversal (rt_device.cuh), leaves = ~prim slot
 //   k_gather_prims   primitive records in leaf order
+//   k_wide           BVH2 -> 4-wide BVH collapse (level by level), small subtrees -> leaves
 // The result is a deterministic function of the input arrays.
 #include <cfloat>
 
@@ -279,26 +279,88 @@ __global__ void k_refit(BuildBuffers B, int n, const float4* __restrict__ slo, c
     }
 }
 
-// Internal children covering <= leaf_max primitives become leaves over their contiguous
-// (Morton-sorted) primitive range; the nodes below them stay in the array but are unreachable.
-__device__ __forceinline__ int collapse(int c, const int2* __restrict__ range, int leaf_max) {
-    if (c < 0) return c;
-    const int2 r = range[c];
-    const int cnt = r.y - r.x + 1;
-    return cnt <= leaf_max ? ~(((cnt - 1) << LEAF_SHIFT) | r.x) : c;
+// ---------------------------------------------------------------- BVH2 -> BVH4 collapse
+// Node layout (rt_device.cuh): 7 float4 = lo.x[4] hi.x[4] lo.y[4] hi.y[4] lo.z[4] hi.z[4] child[4].
+// A BVH2 internal child covering <= leaf_max primitives becomes a leaf over its contiguous
+// (Morton-sorted) range.  Each BVH4 node starts from the two children of one BVH2 node and
+// greedily opens the internal child with the largest surface area until it has 4 children.
+struct WChild {
+    int code;      // BVH2: >= 0 internal node, < 0 ~leaf-slot; after finalize: BVH4 code
+    float4 lo, hi;
+};
+
+__device__ __forceinline__ float half_area(float4 lo, float4 hi) {
+    const float x = hi.x - lo.x, y = hi.y - lo.y, z = hi.z - lo.z;
+    return x * y + y * z + z * x;
 }
 
-__global__ void k_layout(BuildBuffers B, int n, const float4* __restrict__ slo, const float4* __restrict__ shi) {
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n - 1; i += gridDim.x * blockDim.x) {
-        const int l0 = B.left[i], r0 = B.right[i];
-        const int l = collapse(l0, B.range, B.leaf_max), r = collapse(r0, B.range, B.leaf_max);
-        float4 a0, a1, b0, b1;
-        child_box(l0, slo, shi, B.node_lo, B.node_hi, a0, a1);
-        child_box(r0, slo, shi, B.node_lo, B.node_hi, b0, b1);
-        B.nodes[4 * i + 0] = make_float4(a0.x, a1.x, a0.y, a1.y);
-        B.nodes[4 * i + 1] = make_float4(b0.x, b1.x, b0.y, b1.y);
-        B.nodes[4 * i + 2] = make_float4(a0.z, a1.z, b0.z, b1.z);
-        B.nodes[4 * i + 3] = make_float4(__int_as_float(l), __int_as_float(r), 0.f, 0.f);
+__device__ __forceinline__ bool is_open(int code, const int2* __restrict__ range, int leaf_max) {
+    if (code < 0) return false;
+    const int2 r = range[code];
+    return r.y - r.x + 1 > leaf_max;
+}
+
+__device__ __forceinline__ WChild make_child(int code, const BuildBuffers& B) {
+    WChild c;
+    c.code = code;
+    if (code < 0) { c.lo = B.leaf_lo[~code]; c.hi = B.leaf_hi[~code]; }
+    else { c.lo = B.node_lo[code]; c.hi = B.node_hi[code]; }
+    return c;
+}
+
+__global__ void k_wide(BuildBuffers B, const int2* __restrict__ fin, int n_in, int2* fout, int* counters) {
+    for (int it = blockIdx.x * blockDim.x + threadIdx.x; it < n_in; it += gridDim.x * blockDim.x) {
+        const int src = fin[it].x, dst = fin[it].y;
+        WChild ch[4];
+        int n = 2;
+        ch[0] = make_child(B.left[src], B);
+        ch[1] = make_child(B.right[src], B);
+        while (n < 4) {
+            int best = -1;
+            float ba = -1.0f;
+            for (int c = 0; c < n; ++c) {
+                if (is_open(ch[c].code, B.range, B.leaf_max)) {
+                    const float a = half_area(ch[c].lo, ch[c].hi);
+                    if (a > ba) { ba = a; best = c; }
+                }
+            }
+            if (best < 0) break;
+            const int code = ch[best].code;
+            ch[best] = make_child(B.left[code], B);
+            ch[n++] = make_child(B.right[code], B);
+        }
+        float lo[3][4], hi[3][4];
+        int code4[4];
+        for (int c = 0; c < 4; ++c) {
+            if (c >= n) {
+                code4[c] = WIDE_EMPTY;
+                for (int k = 0; k < 3; ++k) { lo[k][c] = 0.f; hi[k][c] = 0.f; }
+                continue;
+            }
+            lo[0][c] = ch[c].lo.x; lo[1][c] = ch[c].lo.y; lo[2][c] = ch[c].lo.z;
+            hi[0][c] = ch[c].hi.x; hi[1][c] = ch[c].hi.y; hi[2][c] = ch[c].hi.z;
+            const int code = ch[c].code;
+            if (code < 0) {
+                code4[c] = code;                                    // BVH2 leaf: ~slot == count-1 of 0
+            } else if (!is_open(code, B.range, B.leaf_max)) {
+                const int2 r = B.range[code];
+                code4[c] = ~(((r.y - r.x) << LEAF_SHIFT) | r.x);
+            } else {
+                const int slot = atomicAdd(&counters[1], 1);
+                const int q = atomicAdd(&counters[0], 1);
+                fout[q] = make_int2(code, slot);
+                code4[c] = slot;
+            }
+        }
+        float4* o = B.nodes4 + 7 * (size_t)dst;
+        o[0] = make_float4(lo[0][0], lo[0][1], lo[0][2], lo[0][3]);
+        o[1] = make_float4(hi[0][0], hi[0][1], hi[0][2], hi[0][3]);
+        o[2] = make_float4(lo[1][0], lo[1][1], lo[1][2], lo[1][3]);
+        o[3] = make_float4(hi[1][0], hi[1][1], hi[1][2], hi[1][3]);
+        o[4] = make_float4(lo[2][0], lo[2][1], lo[2][2], lo[2][3]);
+        o[5] = make_float4(hi[2][0], hi[2][1], hi[2][2], hi[2][3]);
+        o[6] = make_float4(__int_as_float(code4[0]), __int_as_float(code4[1]), __int_as_float(code4[2]),
+                           __int_as_float(code4[3]));
     }
 }
 
@@ -314,14 +376,6 @@ __global__ void k_gather_prims(BuildBuffers B, int n, const uint32_t* __restrict
     }
 }
 
-__global__ void k_depth(const int* __restrict__ parent_leaf, const int* __restrict__ parent_int, int n, int* maxd) {
-    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
-        int d = 0, p = parent_leaf[k];
-        while (p >= 0) { ++d; p = parent_int[p]; }
-        atomicMax(maxd, d);
-    }
-}
-
 }  // namespace rtb
 
 using namespace rtb;
@@ -333,14 +387,16 @@ static int grid_for(int n, int block = 256) {
     return g < 1 ? 1 : (g > 148 * 16 ? 148 * 16 : g);
 }
 
-cudaError_t rtb_build_bvh(const BuildBuffers& Bc, cudaStream_t st) {
+cudaError_t rtb_build_bvh(const BuildBuffers& Bc, cudaStream_t st, int* root, int* n_nodes4, int* depth4) {
     BuildBuffers B = Bc;
     const int n = B.n_spheres + B.n_tris;
     if (n == 0) return cudaSuccess;
     k_prim_setup<<<grid_for(n), 256, 0, st>>>(B);
     if (n == 1) {
         cudaMemcpyAsync(B.prims, B.prims_unsorted, 3 * sizeof(float4), cudaMemcpyDeviceToDevice, st);
-        cudaMemsetAsync(B.max_depth, 0, sizeof(int), st);
+        *root = ~0;
+        *n_nodes4 = 0;
+        *depth4 = 0;
         return cudaGetLastError();
     }
     k_bounds_init<<<1, 32, 0, st>>>(B.bounds);
@@ -361,8 +417,31 @@ cudaError_t rtb_build_bvh(const BuildBuffers& Bc, cudaStream_t st) {
     k_karras<<<grid_for(n - 1), 256, 0, st>>>(B.keys[cur], n, B.left, B.right, B.parent_int, B.parent_leaf, B.range);
     cudaMemsetAsync(B.flags, 0, sizeof(int) * (n - 1), st);
     k_refit<<<grid_for(n), 256, 0, st>>>(B, n, slo, shi);
-    k_layout<<<grid_for(n - 1), 256, 0, st>>>(B, n, slo, shi);
-    cudaMemsetAsync(B.max_depth, 0, sizeof(int), st);
-    k_depth<<<grid_for(n), 256, 0, st>>>(B.parent_leaf, B.parent_int, n, B.max_depth);
+    // root: a leaf if the whole scene fits one leaf, else BVH4 node 0 from BVH2 node 0
+    if (n <= B.leaf_max) {
+        *root = ~(((n - 1) << LEAF_SHIFT) | 0);
+        *n_nodes4 = 0;
+        *depth4 = 0;
+        return cudaGetLastError();
+    }
+    int2 first = make_int2(0, 0);
+    int h_counters[2] = {0, 1};
+    cudaMemcpyAsync(B.frontier[0], &first, sizeof(int2), cudaMemcpyHostToDevice, st);
+    int n_in = 1, levels = 0, cur_f = 0;
+    while (n_in > 0) {
+        h_counters[0] = 0;
+        cudaMemcpyAsync(B.wide_counters, h_counters, sizeof(int), cudaMemcpyHostToDevice, st);
+        if (levels == 0) cudaMemcpyAsync(B.wide_counters + 1, h_counters + 1, sizeof(int), cudaMemcpyHostToDevice, st);
+        k_wide<<<grid_for(n_in), 256, 0, st>>>(B, B.frontier[cur_f], n_in, B.frontier[cur_f ^ 1], B.wide_counters);
+        cudaError_t e = cudaMemcpyAsync(h_counters, B.wide_counters, 2 * sizeof(int), cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) return e;
+        n_in = h_counters[0];
+        cur_f ^= 1;
+        ++levels;
+    }
+    *root = 0;
+    *n_nodes4 = h_counters[1];
+    *depth4 = levels;
     return cudaGetLastError();
 }

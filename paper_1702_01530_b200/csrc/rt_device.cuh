@@ -27,6 +27,7 @@ constexpr int MAX_DEPTH = 16;
 constexpr int BVH_STACK = 64;      // LBVH depth <= 30 Morton bits + 32 index bits
 constexpr int LEAF_SHIFT = 24;     // leaf encoding: ~((count-1) << 24 | first)
 constexpr int TILE = 16;
+constexpr int WIDE_EMPTY = 0x7fffffff;   // unused BVH4 child slot
 
 struct DevScene {
     const float4* __restrict__ nodes;

@@ -80,8 +80,9 @@ struct BuildBuffers {
     int* flags;                 // [N-1]
     float4* node_lo;            // [N-1]
     float4* node_hi;            // [N-1]
-    float4* nodes;              // [4(N-1)] final layout
-    int* max_depth;             // [1]
+    float4* nodes4;             // [7 * (N-1)] BVH4 nodes (upper bound; compacted by the caller)
+    int2* frontier[2];          // [N] collapse work lists (bvh2 node, bvh4 slot)
+    int* wide_counters;         // [2] next-frontier size, next BVH4 slot
     int2* range;                // [N-1] sorted primitive range of each internal node
     int leaf_max;               // collapse subtrees of <= leaf_max primitives into leaves
 };
@@ -95,4 +96,4 @@ cudaError_t rtb_launch_unpack(const void* gathered, const UnpackParams& U, cudaS
 cudaError_t rtb_launch_ffma(float* out, int iters, int grid, cudaStream_t st);
 // launchers (rt_build.cu)
 size_t rtb_sort_hist_entries(int n);
-cudaError_t rtb_build_bvh(const BuildBuffers& B, cudaStream_t st);
+cudaError_t rtb_build_bvh(const BuildBuffers& B, cudaStream_t st, int* root, int* n_nodes4, int* depth4);

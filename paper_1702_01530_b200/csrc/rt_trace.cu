@@ -96,8 +96,39 @@ __device__ __forceinline__ bool prim_t(const DevScene& S, int k, float3 o, float
     return tri_intersect(o, d, a, __ldg(&S.prims[3 * k + 1]), __ldg(&S.prims[3 * k + 2]), t) && t > T_MIN;
 }
 
-// Nearest hit over the BVH (or every BVH primitive when BRUTE) and the planes.
+// Box tests of the 4 children of one BVH4 node (7 float4: lo.x hi.x lo.y hi.y lo.z hi.z child).
+// Returns the hit mask; tn[c] = entry distance of hit children.
+__device__ __forceinline__ unsigned node4_hits(const float4* __restrict__ nodes, int node, const RayBox& rb, float tmax,
+                                               float tn[4], int4& child) {
+    const float4* q = nodes + 7 * node;
+    const float4 lx = __ldg(q), hx = __ldg(q + 1), ly = __ldg(q + 2), hy = __ldg(q + 3);
+    const float4 lz = __ldg(q + 4), hz = __ldg(q + 5);
+    child = __ldg(reinterpret_cast<const int4*>(q + 6));
+    tn[0] = box_enter(rb, lx.x, hx.x, ly.x, hy.x, lz.x, hz.x, tmax);
+    tn[1] = box_enter(rb, lx.y, hx.y, ly.y, hy.y, lz.y, hz.y, tmax);
+    tn[2] = box_enter(rb, lx.z, hx.z, ly.z, hy.z, lz.z, hz.z, tmax);
+    tn[3] = box_enter(rb, lx.w, hx.w, ly.w, hy.w, lz.w, hz.w, tmax);
+    unsigned m = 0;
+    m |= (tn[0] >= 0.0f && child.x != WIDE_EMPTY) ? 1u : 0u;
+    m |= (tn[1] >= 0.0f && child.y != WIDE_EMPTY) ? 2u : 0u;
+    m |= (tn[2] >= 0.0f && child.z != WIDE_EMPTY) ? 4u : 0u;
+    m |= (tn[3] >= 0.0f && child.w != WIDE_EMPTY) ? 8u : 0u;
+    return m;
+}
+
+__device__ __forceinline__ int pick4(const int4& c, int i) { return i == 0 ? c.x : i == 1 ? c.y : i == 2 ? c.z : c.w; }
+
+__device__ __forceinline__ void cswap(uint32_t& a, uint32_t& b) {
+    const uint32_t lo = min(a, b), hi = max(a, b);
+    a = lo;
+    b = hi;
+}
+
+// Nearest hit over the 4-wide BVH (or every BVH primitive when BRUTE) and the planes.
 // Acceptance: t > t_min and (t, gid) lexicographically smallest (reading 9).
+// Children are visited near-to-far: entry distances (>= 0, so their bit patterns order like
+// unsigned ints) carry the child slot in their 2 low bits and go through a 5-exchange sorting
+// network; the 3 farther hits are pushed on the shared-memory stack.
 template <bool COUNT, bool BRUTE>
 __device__ __forceinline__ Hit closest_hit(const DevScene& S, float3 o, float3 d, int* stk, Counters<COUNT>& cnt) {
     Hit h;
@@ -130,38 +161,36 @@ __device__ __forceinline__ Hit closest_hit(const DevScene& S, float3 o, float3 d
     int sp = 0;
     int node = S.root;
     while (true) {
-        while (node >= 0) {
+        if (node >= 0) {
             cnt.add(CNT_NODE_VISITS);
-            const float4 n0 = __ldg(&S.nodes[4 * node + 0]);
-            const float4 n1 = __ldg(&S.nodes[4 * node + 1]);
-            const float4 n2 = __ldg(&S.nodes[4 * node + 2]);
-            const int4 n3 = __ldg(reinterpret_cast<const int4*>(&S.nodes[4 * node + 3]));
-            const float t0 = box_enter(rb, n0.x, n0.y, n0.z, n0.w, n2.x, n2.y, h.t);
-            const float t1 = box_enter(rb, n1.x, n1.y, n1.z, n1.w, n2.z, n2.w, h.t);
-            const bool h0 = t0 >= 0.0f, h1 = t1 >= 0.0f;
-            if (h0 && h1) {
-                const bool swap = t1 < t0;
-                node = swap ? n3.y : n3.x;
-                stk[sp * 256] = swap ? n3.x : n3.y;
-                ++sp;
-            } else if (h0 | h1) {
-                node = h0 ? n3.x : n3.y;
-            } else {
-                if (sp == 0) return h;
-                --sp;
-                node = stk[sp * 256];
+            float tn[4];
+            int4 ch;
+            const unsigned m = node4_hits(S.nodes, node, rb, h.t, tn, ch);
+            if (m) {
+                uint32_t k0 = (m & 1) ? ((__float_as_uint(tn[0]) & ~3u) | 0u) : 0xffffffffu;
+                uint32_t k1 = (m & 2) ? ((__float_as_uint(tn[1]) & ~3u) | 1u) : 0xffffffffu;
+                uint32_t k2 = (m & 4) ? ((__float_as_uint(tn[2]) & ~3u) | 2u) : 0xffffffffu;
+                uint32_t k3 = (m & 8) ? ((__float_as_uint(tn[3]) & ~3u) | 3u) : 0xffffffffu;
+                cswap(k0, k1); cswap(k2, k3); cswap(k0, k2); cswap(k1, k3); cswap(k1, k2);
+                const int nh = __popc(m);
+                if (nh > 3) { stk[sp * 256] = pick4(ch, k3 & 3); ++sp; }
+                if (nh > 2) { stk[sp * 256] = pick4(ch, k2 & 3); ++sp; }
+                if (nh > 1) { stk[sp * 256] = pick4(ch, k1 & 3); ++sp; }
+                node = pick4(ch, k0 & 3);
+                continue;
             }
+        } else {
+            const int enc = ~node;
+            const int first = enc & ((1 << LEAF_SHIFT) - 1);
+            leaf(first, first + (enc >> LEAF_SHIFT));
         }
-        const int enc = ~node;
-        const int first = enc & ((1 << LEAF_SHIFT) - 1);
-        leaf(first, first + (enc >> LEAF_SHIFT));
         if (sp == 0) return h;
         --sp;
         node = stk[sp * 256];
     }
 }
 
-// Any hit with t_min < t < dist (binary visibility, reading 4).
+// Any hit with t_min < t < dist (binary visibility, reading 4); children in node order.
 template <bool COUNT, bool BRUTE>
 __device__ __forceinline__ bool occluded(const DevScene& S, float3 o, float3 d, float dist, int* stk, Counters<COUNT>& cnt) {
     for (int i = 0; i < S.n_planes; ++i) {
@@ -183,30 +212,28 @@ __device__ __forceinline__ bool occluded(const DevScene& S, float3 o, float3 d, 
     int sp = 0;
     int node = S.root;
     while (true) {
-        while (node >= 0) {
+        if (node >= 0) {
             cnt.add(CNT_NODE_VISITS);
-            const float4 n0 = __ldg(&S.nodes[4 * node + 0]);
-            const float4 n1 = __ldg(&S.nodes[4 * node + 1]);
-            const float4 n2 = __ldg(&S.nodes[4 * node + 2]);
-            const int4 n3 = __ldg(reinterpret_cast<const int4*>(&S.nodes[4 * node + 3]));
-            const float t0 = box_enter(rb, n0.x, n0.y, n0.z, n0.w, n2.x, n2.y, dist);
-            const float t1 = box_enter(rb, n1.x, n1.y, n1.z, n1.w, n2.z, n2.w, dist);
-            const bool h0 = t0 >= 0.0f, h1 = t1 >= 0.0f;
-            if (h0 && h1) {
-                node = n3.x;
-                stk[sp * 256] = n3.y;
-                ++sp;
-            } else if (h0 | h1) {
-                node = h0 ? n3.x : n3.y;
-            } else {
-                if (sp == 0) return false;
-                --sp;
-                node = stk[sp * 256];
+            float tn[4];
+            int4 ch;
+            unsigned m = node4_hits(S.nodes, node, rb, dist, tn, ch);
+            if (m) {
+                const int first_c = __ffs(m) - 1;
+                m &= m - 1;
+                while (m) {
+                    const int c = __ffs(m) - 1;
+                    m &= m - 1;
+                    stk[sp * 256] = pick4(ch, c);
+                    ++sp;
+                }
+                node = pick4(ch, first_c);
+                continue;
             }
+        } else {
+            const int enc = ~node;
+            const int first = enc & ((1 << LEAF_SHIFT) - 1);
+            if (leaf(first, first + (enc >> LEAF_SHIFT))) return true;
         }
-        const int enc = ~node;
-        const int first = enc & ((1 << LEAF_SHIFT) - 1);
-        if (leaf(first, first + (enc >> LEAF_SHIFT))) return true;
         if (sp == 0) return false;
         --sp;
         node = stk[sp * 256];
