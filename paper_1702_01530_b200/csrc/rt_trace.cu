@@ -18,7 +18,7 @@
 namespace rtb {
 
 #ifndef RT_MINB
-#define RT_MINB 3
+#define RT_MINB 4
 #endif
 
 template <bool COUNT>

@@ -293,7 +293,7 @@ def rt_scene_info(ctx):
 def rt_bvh_export(ctx):
     nn, npr = C.c_uint32(), C.c_uint32()
     _check(lib().rt_bvh_export(ctx, None, C.byref(nn), None, C.byref(npr)))
-    nodes = np.zeros((max(nn.value, 1), 16), np.float32)
+    nodes = np.zeros((max(nn.value, 1), 28), np.float32)
     gids = np.zeros(max(npr.value, 1), np.int32)
     _check(lib().rt_bvh_export(ctx, nodes.ctypes.data, C.byref(nn), gids.ctypes.data, C.byref(npr)))
     return nodes[:nn.value], gids[:npr.value]
