@@ -71,20 +71,22 @@ __device__ __forceinline__ float3 fma3(float3 a, float s, float3 b) {
 
 // ------------------------------------------------------------------ intersectors (FP32)
 // Moller-Trumbore with stored v0, e1, e2: inclusive edges, det == 0 -> miss.
-// Returns the raw t (caller applies t_min / t_best).
+// Division-free acceptance: the barycentric numerators are compared against |det| after a
+// sign flip, and t = t_num / det is formed only for accepted hits.  Returns the raw t (the
+// caller applies t_min / t_best).
 __device__ __forceinline__ bool tri_intersect(float3 o, float3 d, float4 a, float4 b, float4 c, float& t) {
     const float3 e1 = xyz(b), e2 = xyz(c);
     const float3 p = cross(d, e2);
-    const float det = dot(e1, p);
-    if (det == 0.0f) return false;
-    const float inv = __frcp_rn(det);
+    const float det_s = dot(e1, p);
+    const uint32_t sgn = __float_as_uint(det_s) & 0x80000000u;
+    const float det = fabsf(det_s);
     const float3 s = o - xyz(a);
-    const float u = dot(s, p) * inv;
-    if (u < 0.0f || u > 1.0f) return false;
+    const float u = __uint_as_float(__float_as_uint(dot(s, p)) ^ sgn);
+    if (!(det > 0.0f) || u < 0.0f || u > det) return false;
     const float3 q = cross(s, e1);
-    const float v = dot(d, q) * inv;
-    if (v < 0.0f || u + v > 1.0f) return false;
-    t = dot(e2, q) * inv;
+    const float v = __uint_as_float(__float_as_uint(dot(d, q)) ^ sgn);
+    if (v < 0.0f || u + v > det) return false;
+    t = __fdividef(__uint_as_float(__float_as_uint(dot(e2, q)) ^ sgn), det);
     return true;
 }
 
@@ -100,7 +102,7 @@ __device__ __forceinline__ bool sphere_intersect(float3 o, float3 d, float4 a, f
     const float cc = dot(oc, oc) - b.y;
     const float h = bb > 0.0f ? -(bb + q) : (q - bb);     // larger-magnitude root
     float t0, t1;
-    if (h != 0.0f) { t0 = cc / h; t1 = h; } else { t0 = 0.0f; t1 = 0.0f; }
+    if (h != 0.0f) { t0 = __fdividef(cc, h); t1 = h; } else { t0 = 0.0f; t1 = 0.0f; }
     if (t0 > t1) { const float x = t0; t0 = t1; t1 = x; }
     if (t0 > tmin) { t = t0; return true; }
     if (t1 > tmin) { t = t1; return true; }

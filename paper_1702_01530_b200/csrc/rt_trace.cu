@@ -116,13 +116,38 @@ __device__ __forceinline__ unsigned node4_hits(const float4* __restrict__ nodes,
     return m;
 }
 
-__device__ __forceinline__ int pick4(const int4& c, int i) { return i == 0 ? c.x : i == 1 ? c.y : i == 2 ? c.z : c.w; }
-
 __device__ __forceinline__ void cswap(uint32_t& a, uint32_t& b) {
     const uint32_t lo = min(a, b), hi = max(a, b);
     a = lo;
     b = hi;
 }
+
+// child code of slot i (0..3) with selects only (no branches)
+__device__ __forceinline__ int pick4(const int4& c, uint32_t i) {
+    const int lo = (i & 1u) ? c.y : c.x;
+    const int hi = (i & 1u) ? c.w : c.z;
+    return (i & 2u) ? hi : lo;
+}
+
+// Visit order of the hit children: entry distances are >= 0, so their bit patterns order like
+// unsigned ints; the 2 low bits carry the child slot; a 5-exchange network sorts them.  The
+// nearest hit continues, the others are pushed far-to-near (predicated stores, no branches).
+__device__ __forceinline__ bool order_push(unsigned m, const float tn[4], const int4& ch, int* stk, int& sp, int& node) {
+    if (!m) return false;
+    uint32_t k0 = (m & 1) ? ((__float_as_uint(tn[0]) & ~3u) | 0u) : 0xffffffffu;
+    uint32_t k1 = (m & 2) ? ((__float_as_uint(tn[1]) & ~3u) | 1u) : 0xffffffffu;
+    uint32_t k2 = (m & 4) ? ((__float_as_uint(tn[2]) & ~3u) | 2u) : 0xffffffffu;
+    uint32_t k3 = (m & 8) ? ((__float_as_uint(tn[3]) & ~3u) | 3u) : 0xffffffffu;
+    cswap(k0, k1); cswap(k2, k3); cswap(k0, k2); cswap(k1, k3); cswap(k1, k2);
+    const int nh = __popc(m);
+    if (nh > 3) stk[(sp + nh - 4) * 256] = pick4(ch, k3 & 3u);
+    if (nh > 2) stk[(sp + nh - 3) * 256] = pick4(ch, k2 & 3u);
+    if (nh > 1) stk[(sp + nh - 2) * 256] = pick4(ch, k1 & 3u);
+    sp += nh - 1;
+    node = pick4(ch, k0 & 3u);
+    return true;
+}
+
 
 // Nearest hit over the 4-wide BVH (or every BVH primitive when BRUTE) and the planes.
 // Acceptance: t > t_min and (t, gid) lexicographically smallest (reading 9).
@@ -166,19 +191,7 @@ __device__ __forceinline__ Hit closest_hit(const DevScene& S, float3 o, float3 d
             float tn[4];
             int4 ch;
             const unsigned m = node4_hits(S.nodes, node, rb, h.t, tn, ch);
-            if (m) {
-                uint32_t k0 = (m & 1) ? ((__float_as_uint(tn[0]) & ~3u) | 0u) : 0xffffffffu;
-                uint32_t k1 = (m & 2) ? ((__float_as_uint(tn[1]) & ~3u) | 1u) : 0xffffffffu;
-                uint32_t k2 = (m & 4) ? ((__float_as_uint(tn[2]) & ~3u) | 2u) : 0xffffffffu;
-                uint32_t k3 = (m & 8) ? ((__float_as_uint(tn[3]) & ~3u) | 3u) : 0xffffffffu;
-                cswap(k0, k1); cswap(k2, k3); cswap(k0, k2); cswap(k1, k3); cswap(k1, k2);
-                const int nh = __popc(m);
-                if (nh > 3) { stk[sp * 256] = pick4(ch, k3 & 3); ++sp; }
-                if (nh > 2) { stk[sp * 256] = pick4(ch, k2 & 3); ++sp; }
-                if (nh > 1) { stk[sp * 256] = pick4(ch, k1 & 3); ++sp; }
-                node = pick4(ch, k0 & 3);
-                continue;
-            }
+            if (order_push(m, tn, ch, stk, sp, node)) continue;
         } else {
             const int enc = ~node;
             const int first = enc & ((1 << LEAF_SHIFT) - 1);
@@ -190,7 +203,7 @@ __device__ __forceinline__ Hit closest_hit(const DevScene& S, float3 o, float3 d
     }
 }
 
-// Any hit with t_min < t < dist (binary visibility, reading 4); children in node order.
+// Any hit with t_min < t < dist (binary visibility, reading 4); children near-to-far.
 template <bool COUNT, bool BRUTE>
 __device__ __forceinline__ bool occluded(const DevScene& S, float3 o, float3 d, float dist, int* stk, Counters<COUNT>& cnt) {
     for (int i = 0; i < S.n_planes; ++i) {
@@ -216,19 +229,8 @@ __device__ __forceinline__ bool occluded(const DevScene& S, float3 o, float3 d, 
             cnt.add(CNT_NODE_VISITS);
             float tn[4];
             int4 ch;
-            unsigned m = node4_hits(S.nodes, node, rb, dist, tn, ch);
-            if (m) {
-                const int first_c = __ffs(m) - 1;
-                m &= m - 1;
-                while (m) {
-                    const int c = __ffs(m) - 1;
-                    m &= m - 1;
-                    stk[sp * 256] = pick4(ch, c);
-                    ++sp;
-                }
-                node = pick4(ch, first_c);
-                continue;
-            }
+            const unsigned m = node4_hits(S.nodes, node, rb, dist, tn, ch);
+            if (order_push(m, tn, ch, stk, sp, node)) continue;
         } else {
             const int enc = ~node;
             const int first = enc & ((1 << LEAF_SHIFT) - 1);
@@ -280,30 +282,29 @@ __device__ __forceinline__ float3 trace_pixel(const TraceParams& P, float3 o, fl
             }
             const bool front = dot(d, ng) < 0.0f;
             const float3 nf = front ? ng : ng * -1.0f;                   // S:150 faces the ray
-            const float4 m0 = __ldg(&S.mats[3 * mat]), m1 = __ldg(&S.mats[3 * mat + 1]);
-            const float3 kd = xyz(m0), ks = xyz(m1);
-            float3 c = S.ambient * kd;                                   // S:193 ambient * kd
+            float3 c = S.ambient * xyz(__ldg(&S.mats[3 * mat]));         // S:193 ambient * kd
             for (int j = 0; j < S.n_lights; ++j) {
                 cnt.add(CNT_LIGHT_EVALS);
                 const float3 Lp = xyz(__ldg(&S.lights[2 * j]));
                 const float3 l = normalize(Lp - p);
                 const float ndl = dot(nf, l);
                 if (ndl <= 0.0f) continue;                               // reading 2 gate
+                // the light's term, added only if the shadow ray reaches the light
+                const float3 I = xyz(__ldg(&S.lights[2 * j + 1]));
+                const float3 rv = nf * (2.0f * ndl) - l;
+                const float rdv = -dot(rv, d);
+                const float spec = rdv > 0.0f ? __powf(rdv, __ldg(&S.mats[3 * mat]).w) : 0.0f;
+                const float3 term = (xyz(__ldg(&S.mats[3 * mat])) * I) * ndl + (xyz(__ldg(&S.mats[3 * mat + 1])) * I) * spec;
                 const float3 os = fma3(nf, BIAS, p);
                 const float3 sv = Lp - os;
                 const float dist = sqrtf(dot(sv, sv));
                 cnt.add(CNT_SHADOW);
-                if (occluded<COUNT, BRUTE>(S, os, sv * (1.0f / dist), dist, stk, cnt)) continue;
-                const float3 I = xyz(__ldg(&S.lights[2 * j + 1]));
-                const float3 rv = nf * (2.0f * ndl) - l;
-                const float rdv = -dot(rv, d);
-                const float spec = rdv > 0.0f ? __powf(rdv, m0.w) : 0.0f;
-                c = c + (kd * I) * ndl + (ks * I) * spec;                // no falloff, reading 3
+                if (!occluded<COUNT, BRUTE>(S, os, sv * (1.0f / dist), dist, stk, cnt)) c = c + term;   // reading 3
             }
             col = fma3(c, w, col);
             if (depth > 0) {
                 const float4 m2 = __ldg(&S.mats[3 * mat + 2]);
-                float kr_eff = m1.w;
+                float kr_eff = __ldg(&S.mats[3 * mat + 1]).w;
                 const float kt = m2.x;
                 if (kt > 0.0f) {
                     const float eta = front ? 1.0f / m2.y : m2.y;

@@ -132,8 +132,14 @@ def test_determinism_and_counters(R):
     s = scenes.scene_c2().with_view(width=64, height=48)
     a = gpu_render(R, s, count=True)
     b = gpu_render(R, s)
-    np.testing.assert_array_equal(a["fb"], b["fb"])
-    np.testing.assert_array_equal(a["radiance"].view(np.uint32), b["radiance"].view(np.uint32))
+    b2 = gpu_render(R, s)
+    np.testing.assert_array_equal(b["fb"], b2["fb"])                       # same kernel: bit-exact
+    np.testing.assert_array_equal(b["radiance"].view(np.uint32), b2["radiance"].view(np.uint32))
+    np.testing.assert_array_equal(b["id"], b2["id"])
+    # the instrumented variant is a separate compilation (FMA contraction may differ in the last
+    # bit); it must agree to rounding and trace exactly the same rays
+    np.testing.assert_array_equal(a["id"], b["id"])
+    assert np.abs(a["radiance"] - b["radiance"]).max() <= 1e-6
     c = R.counters_dict(torch.from_numpy(a["counters"]))
     ref = Oracle(s).render(flags=False)
     oc = dict(zip(["primary", "reflection", "refraction", "shadow"], ref["counts"]))
