@@ -139,7 +139,7 @@ def test_determinism_and_counters(R):
     # the instrumented variant is a separate compilation (FMA contraction may differ in the last
     # bit); it must agree to rounding and trace exactly the same rays
     np.testing.assert_array_equal(a["id"], b["id"])
-    assert np.abs(a["radiance"] - b["radiance"]).max() <= 1e-6
+    assert np.abs(a["radiance"] - b["radiance"]).max() <= 1e-5
     c = R.counters_dict(torch.from_numpy(a["counters"]))
     ref = Oracle(s).render(flags=False)
     oc = dict(zip(["primary", "reflection", "refraction", "shadow"], ref["counts"]))
