@@ -28,6 +28,7 @@ constexpr int BVH_STACK = 64;      // LBVH depth <= 30 Morton bits + 32 index bi
 constexpr int LEAF_SHIFT = 24;     // leaf encoding: ~((count-1) << 24 | first)
 constexpr int TILE = 16;
 constexpr int WIDE_EMPTY = 0x7fffffff;   // unused BVH4 child slot
+constexpr int TRAV_DONE = (int)0x80000000;  // traversal finished (not a valid leaf code)
 
 struct DevScene {
     const float4* __restrict__ nodes;
@@ -118,14 +119,17 @@ __device__ __forceinline__ bool plane_intersect(float3 o, float3 d, float4 p, fl
     return true;
 }
 
-// Conservative slab-test setup.  Box planes are tested as fma(plane, 1/d, -(o -/+ m)/d),
-// i.e. against the box inflated by m = 1e-6 (|o|_1 + B) world units, which exceeds the
-// FP32 error of every primitive test by >10x, so the BVH never culls a primitive the
-// brute-force loop would accept (GPU LBVH == GPU brute force, bit-exact).
+// Conservative slab-test setup.  Each box plane is tested as fma(plane, 1/d, c) with per-ray
+// constants c = -(o -/+ m)/d chosen so that entry distances are rounded down and exit
+// distances up by m = 1e-6 (|o|_1 + B) world units -- far above the FP32 error of every
+// primitive test -- so the BVH never culls a primitive the brute-force loop would accept
+// (GPU LBVH == GPU brute force, bit-exact).  The near/far plane of each axis is
+// picked once per ray from the direction's sign (no per-box min/max of slab pairs).
 struct RayBox {
     float3 idir;
-    float3 nlo;   // -(o + m) * idir
-    float3 nhi;   // -(o - m) * idir
+    float3 cn;    // near-plane constants
+    float3 cf;    // far-plane constants
+    int sx, sy, sz;   // 1 if d < 0 on that axis (near plane = hi)
 };
 
 __device__ __forceinline__ float safe_inv(float x) {
@@ -137,19 +141,23 @@ __device__ __forceinline__ RayBox make_raybox(float3 o, float3 d, float bound) {
     RayBox rb;
     const float m = 1e-6f * (fabsf(o.x) + fabsf(o.y) + fabsf(o.z) + bound);
     rb.idir = f3(safe_inv(d.x), safe_inv(d.y), safe_inv(d.z));
-    rb.nlo = f3(-(o.x + m) * rb.idir.x, -(o.y + m) * rb.idir.y, -(o.z + m) * rb.idir.z);
-    rb.nhi = f3(-(o.x - m) * rb.idir.x, -(o.y - m) * rb.idir.y, -(o.z - m) * rb.idir.z);
+    const float3 clo = f3(-(o.x + m) * rb.idir.x, -(o.y + m) * rb.idir.y, -(o.z + m) * rb.idir.z);
+    const float3 chi = f3(-(o.x - m) * rb.idir.x, -(o.y - m) * rb.idir.y, -(o.z - m) * rb.idir.z);
+    rb.sx = rb.idir.x < 0.0f;
+    rb.sy = rb.idir.y < 0.0f;
+    rb.sz = rb.idir.z < 0.0f;
+    rb.cn = f3(rb.sx ? chi.x : clo.x, rb.sy ? chi.y : clo.y, rb.sz ? chi.z : clo.z);
+    rb.cf = f3(rb.sx ? clo.x : chi.x, rb.sy ? clo.y : chi.y, rb.sz ? clo.z : chi.z);
     return rb;
 }
 
-// Returns the entry distance (>= 0), or -1 when the (inflated) box is missed within [0, tmax].
-__device__ __forceinline__ float box_enter(const RayBox& rb, float lox, float hix, float loy, float hiy,
-                                           float loz, float hiz, float tmax) {
-    const float ax = fmaf(lox, rb.idir.x, rb.nlo.x), bx = fmaf(hix, rb.idir.x, rb.nhi.x);
-    const float ay = fmaf(loy, rb.idir.y, rb.nlo.y), by = fmaf(hiy, rb.idir.y, rb.nhi.y);
-    const float az = fmaf(loz, rb.idir.z, rb.nlo.z), bz = fmaf(hiz, rb.idir.z, rb.nhi.z);
-    const float tn = fmaxf(fmaxf(fminf(ax, bx), fminf(ay, by)), fmaxf(fminf(az, bz), 0.0f));
-    const float tf = fminf(fminf(fmaxf(ax, bx), fmaxf(ay, by)), fminf(fmaxf(az, bz), tmax));
+// Slab test of one box given its near/far planes; returns the entry distance (>= 0) or -1.
+__device__ __forceinline__ float slab(const RayBox& rb, float nx, float fx, float ny, float fy, float nz, float fz,
+                                      float tmax) {
+    const float tn = fmaxf(fmaxf(fmaf(nx, rb.idir.x, rb.cn.x), fmaf(ny, rb.idir.y, rb.cn.y)),
+                           fmaxf(fmaf(nz, rb.idir.z, rb.cn.z), 0.0f));
+    const float tf = fminf(fminf(fmaf(fx, rb.idir.x, rb.cf.x), fmaf(fy, rb.idir.y, rb.cf.y)),
+                           fminf(fmaf(fz, rb.idir.z, rb.cf.z), tmax));
     return tn <= tf ? tn : -1.0f;
 }
 

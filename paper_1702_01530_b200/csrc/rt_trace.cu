@@ -101,13 +101,14 @@ __device__ __forceinline__ bool prim_t(const DevScene& S, int k, float3 o, float
 __device__ __forceinline__ unsigned node4_hits(const float4* __restrict__ nodes, int node, const RayBox& rb, float tmax,
                                                float tn[4], int4& child) {
     const float4* q = nodes + 7 * node;
-    const float4 lx = __ldg(q), hx = __ldg(q + 1), ly = __ldg(q + 2), hy = __ldg(q + 3);
-    const float4 lz = __ldg(q + 4), hz = __ldg(q + 5);
+    const float4 nx = __ldg(q + rb.sx), fx = __ldg(q + 1 - rb.sx);
+    const float4 ny = __ldg(q + 2 + rb.sy), fy = __ldg(q + 3 - rb.sy);
+    const float4 nz = __ldg(q + 4 + rb.sz), fz = __ldg(q + 5 - rb.sz);
     child = __ldg(reinterpret_cast<const int4*>(q + 6));
-    tn[0] = box_enter(rb, lx.x, hx.x, ly.x, hy.x, lz.x, hz.x, tmax);
-    tn[1] = box_enter(rb, lx.y, hx.y, ly.y, hy.y, lz.y, hz.y, tmax);
-    tn[2] = box_enter(rb, lx.z, hx.z, ly.z, hy.z, lz.z, hz.z, tmax);
-    tn[3] = box_enter(rb, lx.w, hx.w, ly.w, hy.w, lz.w, hz.w, tmax);
+    tn[0] = slab(rb, nx.x, fx.x, ny.x, fy.x, nz.x, fz.x, tmax);
+    tn[1] = slab(rb, nx.y, fx.y, ny.y, fy.y, nz.y, fz.y, tmax);
+    tn[2] = slab(rb, nx.z, fx.z, ny.z, fy.z, nz.z, fz.z, tmax);
+    tn[3] = slab(rb, nx.w, fx.w, ny.w, fy.w, nz.w, fz.w, tmax);
     unsigned m = 0;
     m |= (tn[0] >= 0.0f && child.x != WIDE_EMPTY) ? 1u : 0u;
     m |= (tn[1] >= 0.0f && child.y != WIDE_EMPTY) ? 2u : 0u;
@@ -169,7 +170,7 @@ __device__ __forceinline__ Hit closest_hit(const DevScene& S, float3 o, float3 d
         }
     }
     if (S.n_bvh == 0) return h;
-    auto leaf = [&](int first, int last) {
+    auto leaf_test = [&](int first, int last) {
         for (int k = first; k <= last; ++k) {
             float t;
             int gid;
@@ -179,27 +180,33 @@ __device__ __forceinline__ Hit closest_hit(const DevScene& S, float3 o, float3 d
         }
     };
     if (BRUTE) {
-        leaf(0, S.n_bvh - 1);
+        leaf_test(0, S.n_bvh - 1);
         return h;
     }
     const RayBox rb = make_raybox(o, d, S.bound);
-    int sp = 0;
+    int sp = 0, leaf = 0;                 // leaf: postponed leaf code (< 0), 0 = none
     int node = S.root;
+    auto pop = [&]() { return sp > 0 ? stk[--sp * 256] : TRAV_DONE; };
     while (true) {
-        if (node >= 0) {
+        // inner nodes; a lane that reaches a leaf parks it and keeps walking inner nodes
+        // until every lane of the warp holds a leaf (Aila-Laine speculative while-while)
+        while (node >= 0) {
             cnt.add(CNT_NODE_VISITS);
             float tn[4];
             int4 ch;
             const unsigned m = node4_hits(S.nodes, node, rb, h.t, tn, ch);
-            if (order_push(m, tn, ch, stk, sp, node)) continue;
-        } else {
-            const int enc = ~node;
-            const int first = enc & ((1 << LEAF_SHIFT) - 1);
-            leaf(first, first + (enc >> LEAF_SHIFT));
+            if (!order_push(m, tn, ch, stk, sp, node)) node = pop();
+            if (node < 0 && node != TRAV_DONE && leaf == 0) { leaf = node; node = pop(); }
+            if (__all_sync(__activemask(), leaf != 0 || node < 0)) break;
         }
-        if (sp == 0) return h;
-        --sp;
-        node = stk[sp * 256];
+        if (leaf == 0 && node < 0 && node != TRAV_DONE) { leaf = node; node = pop(); }
+        if (leaf != 0) {
+            const int enc = ~leaf;
+            const int first = enc & ((1 << LEAF_SHIFT) - 1);
+            leaf_test(first, first + (enc >> LEAF_SHIFT));
+            leaf = 0;
+        }
+        if (node == TRAV_DONE) return h;
     }
 }
 
@@ -212,7 +219,7 @@ __device__ __forceinline__ bool occluded(const DevScene& S, float3 o, float3 d, 
         if (plane_intersect(o, d, __ldg(&S.planes[i]), t) && t > T_MIN && t < dist) return true;
     }
     if (S.n_bvh == 0) return false;
-    auto leaf = [&](int first, int last) -> bool {
+    auto leaf_test = [&](int first, int last) -> bool {
         for (int k = first; k <= last; ++k) {
             float t;
             int gid;
@@ -220,25 +227,29 @@ __device__ __forceinline__ bool occluded(const DevScene& S, float3 o, float3 d, 
         }
         return false;
     };
-    if (BRUTE) return leaf(0, S.n_bvh - 1);
+    if (BRUTE) return leaf_test(0, S.n_bvh - 1);
     const RayBox rb = make_raybox(o, d, S.bound);
-    int sp = 0;
+    int sp = 0, leaf = 0;
     int node = S.root;
+    auto pop = [&]() { return sp > 0 ? stk[--sp * 256] : TRAV_DONE; };
     while (true) {
-        if (node >= 0) {
+        while (node >= 0) {
             cnt.add(CNT_NODE_VISITS);
             float tn[4];
             int4 ch;
             const unsigned m = node4_hits(S.nodes, node, rb, dist, tn, ch);
-            if (order_push(m, tn, ch, stk, sp, node)) continue;
-        } else {
-            const int enc = ~node;
-            const int first = enc & ((1 << LEAF_SHIFT) - 1);
-            if (leaf(first, first + (enc >> LEAF_SHIFT))) return true;
+            if (!order_push(m, tn, ch, stk, sp, node)) node = pop();
+            if (node < 0 && node != TRAV_DONE && leaf == 0) { leaf = node; node = pop(); }
+            if (__all_sync(__activemask(), leaf != 0 || node < 0)) break;
         }
-        if (sp == 0) return false;
-        --sp;
-        node = stk[sp * 256];
+        if (leaf == 0 && node < 0 && node != TRAV_DONE) { leaf = node; node = pop(); }
+        if (leaf != 0) {
+            const int enc = ~leaf;
+            const int first = enc & ((1 << LEAF_SHIFT) - 1);
+            if (leaf_test(first, first + (enc >> LEAF_SHIFT))) return true;
+            leaf = 0;
+        }
+        if (node == TRAV_DONE) return false;
     }
 }
 
