@@ -184,29 +184,23 @@ __device__ __forceinline__ Hit closest_hit(const DevScene& S, float3 o, float3 d
         return h;
     }
     const RayBox rb = make_raybox(o, d, S.bound);
-    int sp = 0, leaf = 0;                 // leaf: postponed leaf code (< 0), 0 = none
+    int sp = 0;
     int node = S.root;
-    auto pop = [&]() { return sp > 0 ? stk[--sp * 256] : TRAV_DONE; };
     while (true) {
-        // inner nodes; a lane that reaches a leaf parks it and keeps walking inner nodes
-        // until every lane of the warp holds a leaf (Aila-Laine speculative while-while)
-        while (node >= 0) {
+        if (node >= 0) {
             cnt.add(CNT_NODE_VISITS);
             float tn[4];
             int4 ch;
             const unsigned m = node4_hits(S.nodes, node, rb, h.t, tn, ch);
-            if (!order_push(m, tn, ch, stk, sp, node)) node = pop();
-            if (node < 0 && node != TRAV_DONE && leaf == 0) { leaf = node; node = pop(); }
-            if (__all_sync(__activemask(), leaf != 0 || node < 0)) break;
-        }
-        if (leaf == 0 && node < 0 && node != TRAV_DONE) { leaf = node; node = pop(); }
-        if (leaf != 0) {
-            const int enc = ~leaf;
+            if (order_push(m, tn, ch, stk, sp, node)) continue;
+        } else {
+            const int enc = ~node;
             const int first = enc & ((1 << LEAF_SHIFT) - 1);
             leaf_test(first, first + (enc >> LEAF_SHIFT));
-            leaf = 0;
         }
-        if (node == TRAV_DONE) return h;
+        if (sp == 0) return h;
+        --sp;
+        node = stk[sp * 256];
     }
 }
 
@@ -229,27 +223,23 @@ __device__ __forceinline__ bool occluded(const DevScene& S, float3 o, float3 d, 
     };
     if (BRUTE) return leaf_test(0, S.n_bvh - 1);
     const RayBox rb = make_raybox(o, d, S.bound);
-    int sp = 0, leaf = 0;
+    int sp = 0;
     int node = S.root;
-    auto pop = [&]() { return sp > 0 ? stk[--sp * 256] : TRAV_DONE; };
     while (true) {
-        while (node >= 0) {
+        if (node >= 0) {
             cnt.add(CNT_NODE_VISITS);
             float tn[4];
             int4 ch;
             const unsigned m = node4_hits(S.nodes, node, rb, dist, tn, ch);
-            if (!order_push(m, tn, ch, stk, sp, node)) node = pop();
-            if (node < 0 && node != TRAV_DONE && leaf == 0) { leaf = node; node = pop(); }
-            if (__all_sync(__activemask(), leaf != 0 || node < 0)) break;
-        }
-        if (leaf == 0 && node < 0 && node != TRAV_DONE) { leaf = node; node = pop(); }
-        if (leaf != 0) {
-            const int enc = ~leaf;
+            if (order_push(m, tn, ch, stk, sp, node)) continue;
+        } else {
+            const int enc = ~node;
             const int first = enc & ((1 << LEAF_SHIFT) - 1);
             if (leaf_test(first, first + (enc >> LEAF_SHIFT))) return true;
-            leaf = 0;
         }
-        if (node == TRAV_DONE) return false;
+        if (sp == 0) return false;
+        --sp;
+        node = stk[sp * 256];
     }
 }
 
