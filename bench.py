@@ -56,10 +56,9 @@ def workload_desc(s):
 
 
 def gather_to_root(dist, shard_buf, gathered, world, rank, per):
-    """a7: every rank's packed tile shard -> rank 0's `gathered` buffer (rank-major), one
-    collective (NCCL ncclSend/Recv over NVLink on GPUs; gloo in the CPU tests)."""
-    glist = [gathered[r * per:(r + 1) * per] for r in range(world)] if rank == 0 else None
-    dist.gather(shard_buf, glist, dst=0)
+    """a7 (nccl path), see paper_1702_01530_b200/multigpu.py."""
+    from paper_1702_01530_b200.multigpu import gather_to_root as g
+    g(dist, shard_buf, gathered, world, rank, per)
 
 
 # ------------------------------------------------------------------------------ clocks
@@ -165,11 +164,30 @@ def run_reference(args, scene):
 
 
 # ------------------------------------------------------------------------------ GPU leg
+class SingleFrame:
+    """N = 1: the whole stereo frame straight into the framebuffers."""
+
+    mode = "single"
+    launches_per_frame = 1
+
+    def __init__(self, R, fb, width, height):
+        self.R, self.fb, self.W, self.H = R, fb, width, height
+
+    def render(self, depth):
+        self.R.render(self.W, self.H, depth, fb=self.fb)
+
+    def assemble(self):
+        pass
+
+    def close(self):
+        pass
+
+
 def run_ours(args, scene):
     import torch
     import torch.distributed as dist
 
-    from paper_1702_01530_b200 import rt
+    from paper_1702_01530_b200 import multigpu, rt
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -204,26 +222,14 @@ def run_ours(args, scene):
     rays_total = tot["primary"] + tot["reflection"] + tot["refraction"] + tot["shadow"]
     my_flops = algorithmic_flops(cnt)
 
-    # ---- buffers
+    # ---- frame assembly (a7): direct (N=1), fused peer stores or NCCL gather (N>1)
     fb = R.alloc_fb(W, H)                                    # root framebuffers (2, H, W, 4) u8
-    per = rt.rt_shard_bytes(W, H, world)
-    shard_buf = torch.empty(per, dtype=torch.uint8, device=dev) if world > 1 else None
-    gathered = torch.empty(world * per, dtype=torch.uint8, device=dev) if (world > 1 and rank == 0) else None
+    frame = SingleFrame(R, fb, W, H) if world == 1 else multigpu.make_frame(args.gather, R, fb, rank, world, dist, W, H)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
-    pitch = W * 4
-
-    def step():
-        if world == 1:
-            R.render(W, H, D, fb=fb)
-        else:
-            R.render(W, H, D, fb=False, shard=shard, shard_buf=shard_buf)
-            gather_to_root(dist, shard_buf, gathered, world, rank, per)
-            if rank == 0:
-                rt.rt_unpack_shards(R.ctx, gathered.data_ptr(), W, H, world, rt.RT_FORMAT_RGBA8,
-                                    rt.rt_fb(fb[0].data_ptr(), 0, pitch), rt.rt_fb(fb[1].data_ptr(), 0, pitch))
 
     for _ in range(max(3, args.warmup)):
-        step()
+        frame.render(D)
+        frame.assemble()
     torch.cuda.synchronize()
     barrier()
 
@@ -237,16 +243,9 @@ def run_ours(args, scene):
     for k in range(args.steps):
         flush.zero_()                                          # L2 flush between timed steps (untimed)
         ev_s[k].record()
-        if world == 1:
-            R.render(W, H, D, fb=fb)
-            ev_k[k].record()
-        else:
-            R.render(W, H, D, fb=False, shard=shard, shard_buf=shard_buf)
-            ev_k[k].record()
-            gather_to_root(dist, shard_buf, gathered, world, rank, per)
-            if rank == 0:
-                rt.rt_unpack_shards(R.ctx, gathered.data_ptr(), W, H, world, rt.RT_FORMAT_RGBA8,
-                                    rt.rt_fb(fb[0].data_ptr(), 0, pitch), rt.rt_fb(fb[1].data_ptr(), 0, pitch))
+        frame.render(D)
+        ev_k[k].record()
+        frame.assemble()
         ev_e[k].record()
     torch.cuda.synchronize()
     barrier()
@@ -256,11 +255,11 @@ def run_ours(args, scene):
     t = torch.tensor([step_ms.sum(), kern_ms.mean()], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms, kern_avg_ms_max = float(t[0]), float(t[1])
+    total_ms = float(t[0])
     ms_per_step = total_ms / args.steps
 
     # ---- end-to-end through the public C ABI with host buffers (camera in, frame out)
-    e2e = run_e2e(args, R, scene, rank, world, shard, per, dev, rays_total) if not args.no_e2e else None
+    e2e = run_e2e(args, R, scene, rank, world, frame, fb, dev, rays_total) if not args.no_e2e else None
 
     # ---- FFMA peak measured live (context for the roofline denominator)
     ffma_tflops, _ = rt.rt_bench_ffma(R.ctx, 2048)
@@ -271,7 +270,8 @@ def run_ours(args, scene):
         peak = 148 * FP32_LANES_PER_SM * 2 * sm_max * 1e6 / 1e12
         achieved = my_flops / (float(kern_ms.mean()) * 1e-3) / 1e12
         traffic = load_traffic(scene.name, world)
-        n_launch_per_step = 1 + (1 if world > 1 else 0)
+        par = f"tile-sharded x{world}" + {"single": "", "peer": " + fused peer-store gather to rank 0 (CUDA IPC over NVLink)",
+                                          "nccl": " + NCCL gather to rank 0 + unpack"}[frame.mode]
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True,
@@ -280,7 +280,7 @@ def run_ours(args, scene):
             "config": {"workload": workload_desc(scene), "width": W, "height": H, "max_depth": D,
                        "triangles": scene.n_tris, "rays_per_step": rays_total,
                        "rays_by_type": {k: tot[k] for k in ("primary", "reflection", "refraction", "shadow")},
-                       "parallelism": f"tile-sharded x{world}" + (" + NCCL gather to rank 0" if world > 1 else ""),
+                       "parallelism": par, "gather": frame.mode,
                        "l2": "flushed (256 MiB write) between timed steps; scene+BVH "
                              f"{info['device_bytes'] / 1e6:.0f} MB"},
             "stereo_fps": 1e3 / ms_per_step,
@@ -289,10 +289,10 @@ def run_ours(args, scene):
                          "kernel": "k_trace_stereo", "kernel_ms": float(kern_ms.mean()),
                          "kernel_share_of_step": float(kern_ms.mean()) / ms_per_step,
                          "algorithmic_flops_per_launch": my_flops,
-                         "peak_basis": f"148 SM x 128 FP32 lanes x 2 x {sm_max:.0f} MHz (sm_max); "
-                                       f"live FFMA microbenchmark {ffma_tflops:.1f} TFLOP/s"},
+                         "peak_basis": f"148 SM x 128 FP32 lanes x 2 x {sm_max:.0f} MHz (sm_max; B200_PROFILING "
+                                       f"unit counts); live FFMA microbenchmark {ffma_tflops:.1f} TFLOP/s"},
             "clocks": clocks,
-            "gpu_launches": args.steps * n_launch_per_step,
+            "gpu_launches": args.steps * frame.launches_per_frame,
             "scene_upload_ms": upload_ms, "bvh": info,
             "work_counts": tot,
         }
@@ -301,6 +301,7 @@ def run_ours(args, scene):
         if not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(scene, target_s=args.cpu_seconds)
         print(json.dumps(line), flush=True)
+    frame.close()
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
@@ -308,60 +309,57 @@ def run_ours(args, scene):
     return 0
 
 
-def run_e2e(args, R, scene, rank, world, shard, per, dev, rays_total):
+def run_e2e(args, R, scene, rank, world, frame, fb, dev, rays_total):
     """Same metric through the public C ABI: every step sets the camera from host values
-    (rt_set_stereo_camera), renders, and downloads the finished stereo frame into pinned host
-    memory with rt_download (copy stream, overlapped with the next frame's render)."""
+    (rt_set_stereo_camera), renders (+ assembles on rank 0 for N>1) and downloads the finished
+    stereo frame into pinned host memory with rt_download (copy stream, overlapped with the next
+    frame's render).  Two framebuffer slots alternate; a slot is re-rendered only after its
+    previous download completed."""
     import ctypes
 
     import torch
-    import torch.distributed as dist
 
     from paper_1702_01530_b200 import rt
 
     W, H, D = scene.width, scene.height, scene.max_depth
     nbytes = 2 * H * W * 4
-    nslot = 2
-    fbs = [R.alloc_fb(W, H) for _ in range(nslot)]
-    hosts = [rt.rt_host_alloc(nbytes) for _ in range(nslot)] if rank == 0 else []
-    pitch = W * 4
-    shard_buf = torch.empty(per, dtype=torch.uint8, device=dev) if world > 1 else None
-    gathered = torch.empty(world * per, dtype=torch.uint8, device=dev) if (world > 1 and rank == 0) else None
+    hosts = [rt.rt_host_alloc(nbytes) for _ in range(2)] if rank == 0 else []
     rig = scene.rig
-    pending = [None] * nslot
+    pending = [None, None]
+    fb2 = R.alloc_fb(W, H) if world == 1 else None
 
-    def frame(k):
-        slot = k % nslot
+    def frame_step(k):
+        slot = k % 2
         if pending[slot] is not None:
             rt.rt_wait(pending[slot])                         # host slot free again
             pending[slot] = None
         rt.rt_set_stereo_camera(R.ctx, rig.eye, rig.look_at, rig.up, rig.vfov_deg, rig.interocular,
                                 rig.convergence)
-        fb = fbs[slot]
         if world == 1:
-            rt.rt_render_stereo(R.ctx, W, H, D, rt.rt_fb(fb[0].data_ptr(), 0, pitch), rt.rt_fb(fb[1].data_ptr(), 0, pitch))
+            dst = fb if slot == 0 else fb2
+            pitch = W * 4
+            rt.rt_render_stereo(R.ctx, W, H, D, rt.rt_fb(dst[0].data_ptr(), 0, pitch), rt.rt_fb(dst[1].data_ptr(), 0, pitch))
         else:
-            R.render(W, H, D, fb=False, shard=shard, shard_buf=shard_buf)
-            gather_to_root(dist, shard_buf, gathered, world, rank, per)
-            if rank == 0:
-                rt.rt_unpack_shards(R.ctx, gathered.data_ptr(), W, H, world, rt.RT_FORMAT_RGBA8,
-                                    rt.rt_fb(fb[0].data_ptr(), 0, pitch), rt.rt_fb(fb[1].data_ptr(), 0, pitch))
+            dst = fb
+            frame.render(D)
+            frame.assemble()
         if rank == 0:
-            pending[slot] = rt.rt_download(R.ctx, fb.data_ptr(), hosts[slot], nbytes)
+            pending[slot] = rt.rt_download(R.ctx, dst.data_ptr(), hosts[slot], nbytes)
 
     for k in range(max(3, args.warmup)):
-        frame(k)
-    for i in range(nslot):
+        frame_step(k)
+    for i in range(2):
         if pending[i] is not None:
             rt.rt_wait(pending[i])
             pending[i] = None
     rt.rt_synchronize(R.ctx)
     if world > 1:
+        import torch.distributed as dist
         dist.barrier()
     t0 = time.perf_counter()
     for k in range(args.steps):
-        frame(k)
-    for i in range(nslot):
+        frame_step(k)
+    for i in range(2):
         if pending[i] is not None:
             rt.rt_wait(pending[i])
             pending[i] = None
@@ -369,22 +367,23 @@ def run_e2e(args, R, scene, rank, world, shard, per, dev, rays_total):
     dt = time.perf_counter() - t0
     tt = torch.tensor([dt], dtype=torch.float64, device=dev)
     if world > 1:
+        import torch.distributed as dist
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     dt = float(tt[0])
     ok = True
     if rank == 0:
-        # the last downloaded frame must equal the device framebuffer
-        slot = (args.steps - 1) % nslot
+        slot = (args.steps - 1) % 2
+        src = fb if (world > 1 or slot == 0) else fb2
         host = np.frombuffer((ctypes.c_uint8 * nbytes).from_address(hosts[slot]), np.uint8)
-        ok = bool(np.array_equal(host[:4096], fbs[slot].reshape(-1)[:4096].cpu().numpy()))
+        ok = bool(np.array_equal(host, src.reshape(-1).cpu().numpy()))
         for h in hosts:
             rt.rt_host_free(h)
     return {"value": rays_total / (dt / args.steps) / 1e6, "unit": UNIT,
             "h2d_bytes_per_step": 76, "d2h_bytes_per_step": nbytes if rank == 0 else 0,
             "ms_per_step": dt / args.steps * 1e3, "stereo_fps": args.steps / dt, "download_verified": ok,
-            "note": "per step: camera set from host (76-byte camera block travels in the kernel launch "
-                    "parameters), render, pinned async D2H of the RGBA8 stereo frame overlapped with the next "
-                    "render (2 slots); host wall clock around K steps incl. the final download"}
+            "note": "per step: camera set from host values (the 76-byte camera block travels in the kernel "
+                    "launch parameters), render, pinned async D2H (rt_download, copy stream) of the RGBA8 stereo "
+                    "frame overlapped with the next render; host wall clock around K steps incl. the last download"}
 
 
 def load_traffic(name, world):
@@ -405,6 +404,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="C4")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--gather", choices=["peer", "nccl"], default="peer",
+                    help="N>1 frame assembly: fused peer stores into rank 0's FB (default) or NCCL gather")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     args = ap.parse_args()

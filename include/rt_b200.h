@@ -110,6 +110,9 @@ typedef enum rt_counter {
 /* rt_render_params.flags */
 #define RT_RENDER_COUNT 1u       /* run the instrumented kernel variant (fills counters; slower) */
 #define RT_RENDER_BRUTE_FORCE 2u /* debug: test every primitive, no BVH (same FP32 intersectors) */
+#define RT_RENDER_PEER_STORE 4u  /* out_left/out_right are a PEER rank's framebuffers mapped with
+                                    rt_ipc_open: the pack epilogue stores over NVLink and the
+                                    kernel ends with a system-scope fence (fused render->gather) */
 
 typedef struct rt_render_params {
     uint32_t width, height;      /* per eye; 1 <= w,h <= 16384                              */

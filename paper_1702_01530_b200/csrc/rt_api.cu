@@ -514,7 +514,8 @@ rt_status rt_render_stereo_ex(rt_context* c, const rt_render_params* p, const rt
     if (p->max_depth > RT_MAX_DEPTH) return fail(RT_ERR_SIZE, "max_depth %u > %d", p->max_depth, RT_MAX_DEPTH);
     if (p->shard_world == 0 || p->shard_rank >= p->shard_world || p->shard_world > 4096)
         return fail(RT_ERR_INVALID_ARG, "shard %u of %u", p->shard_rank, p->shard_world);
-    if (p->flags & ~(RT_RENDER_COUNT | RT_RENDER_BRUTE_FORCE)) return fail(RT_ERR_INVALID_ARG, "unknown flags 0x%x", p->flags);
+    if (p->flags & ~(RT_RENDER_COUNT | RT_RENDER_BRUTE_FORCE | RT_RENDER_PEER_STORE))
+        return fail(RT_ERR_INVALID_ARG, "unknown flags 0x%x", p->flags);
     if ((p->flags & RT_RENDER_COUNT) && !out->counters) return fail(RT_ERR_INVALID_ARG, "RT_RENDER_COUNT needs counters");
     rt_status st;
     if ((st = check_fb(out->left, W, "out_left")) || (st = check_fb(out->right, W, "out_right"))) return st;
@@ -550,10 +551,11 @@ rt_status rt_render_stereo_ex(rt_context* c, const rt_render_params* p, const rt
     P.counters = out->counters ? out->counters : c->scratch_counters;
     P.stack_entries = 3 * (int)c->info[5] + 2;       // <= 3 pending siblings per BVH4 level
     P.n_tiles = (int)n_tiles;
+    P.peer_fence = (p->flags & RT_RENDER_PEER_STORE) ? 1 : 0;
     if (P.n_work == 0) return RT_OK;
     CUDA_TRY(cudaSetDevice(c->device));
     int occ = 0;
-    CUDA_TRY(rtb_trace_occupancy(p->flags, P.stack_entries, &occ));
+    CUDA_TRY(rtb_trace_occupancy(p->flags & (RT_RENDER_COUNT | RT_RENDER_BRUTE_FORCE), P.stack_entries, &occ));
     if (occ < 1) occ = 1;
     const long long max_blocks = ((long long)P.n_work + 255) / 256;
     const int grid = (int)std::min<long long>((long long)c->num_sms * occ, std::max<long long>(1, max_blocks));
@@ -571,7 +573,7 @@ rt_status rt_render_stereo_ex(rt_context* c, const rt_render_params* p, const rt
     }
     P.rq_overflow = c->rq_overflow;
     CUDA_TRY(cudaMemsetAsync(c->work_counter, 0, sizeof(int), c->stream));
-    CUDA_TRY(rtb_launch_trace(P, p->flags, grid, c->stream));
+    CUDA_TRY(rtb_launch_trace(P, p->flags & (RT_RENDER_COUNT | RT_RENDER_BRUTE_FORCE), grid, c->stream));
     return RT_OK;
 }
 

@@ -41,6 +41,7 @@ struct TraceParams {
     unsigned long long* counters;
     int stack_entries;      // BVH traversal stack depth (shared memory, [entry][thread])
     int n_tiles;            // 16x16 tiles in this shard (= n_work / 256)
+    int peer_fence;         // framebuffers live in a peer's memory: fence system-wide at exit
     float4* rq_overflow;    // per-CTA global spill of the tree-ray stack (2 float4 per entry)
     int rq_overflow_entries;
 };

@@ -378,6 +378,7 @@ __global__ void __launch_bounds__(256, RT_MINB) k_trace_stereo(const TraceParams
             }
         }
     }
+    if (P.peer_fence) __threadfence_system();        // peer framebuffer stores visible system-wide
     if (COUNT) {
 #pragma unroll
         for (int i = 0; i < RT_NUM_COUNTERS_INTERNAL; ++i) {

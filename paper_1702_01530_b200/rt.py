@@ -18,7 +18,7 @@ LIB_PATH = os.environ.get("RT_LIB_PATH") or os.path.join(_HERE, "lib", "librt_b2
 RT_OK, RT_ERR_INVALID_ARG, RT_ERR_CUDA, RT_ERR_OOM, RT_ERR_NO_SCENE, RT_ERR_NO_CAMERA, RT_ERR_SIZE, \
     RT_ERR_NOT_READY, RT_ERR_PEER = range(9)
 RT_FORMAT_RGBA8, RT_FORMAT_RGBA16F = 0, 1
-RT_RENDER_COUNT, RT_RENDER_BRUTE_FORCE = 1, 2
+RT_RENDER_COUNT, RT_RENDER_BRUTE_FORCE, RT_RENDER_PEER_STORE = 1, 2, 4
 RT_NUM_COUNTERS = 12
 RT_TILE = 16
 COUNTER_NAMES = ["primary", "reflection", "refraction", "shadow", "node_visits", "tri_tests", "sphere_tests",
@@ -347,14 +347,19 @@ class StereoRenderer:
         return t.empty((2, height, width, 4), dtype=dt, device=self.device)
 
     def render(self, width, height, max_depth, fmt=RT_FORMAT_RGBA8, fb=None, want_id=False, want_radiance=False,
-               count=False, brute=False, shard=(0, 1), shard_buf=None, shard_fmt=RT_FORMAT_RGBA8):
+               count=False, brute=False, shard=(0, 1), shard_buf=None, shard_fmt=RT_FORMAT_RGBA8, fb_ptrs=None,
+               peer=False):
         """Enqueue one stereo render; returns dict of torch device tensors (not synchronised)."""
         t = self.torch
         out = {}
         o = rt_outputs()
-        if fb is None and fb is not False:
+        if fb is None and fb_ptrs is None:
             fb = self.alloc_fb(width, height, fmt)
-        if fb is not False and fb is not None:
+        if fb_ptrs is not None:                     # raw device pointers (e.g. a peer's IPC-mapped FB)
+            lp, rp, pitch = fb_ptrs
+            o.left = rt_fb(lp, fmt, pitch)
+            o.right = rt_fb(rp, fmt, pitch)
+        elif fb is not False and fb is not None:
             pitch = fb.stride(1) * fb.element_size()
             o.left = rt_fb(fb[0].data_ptr(), fmt, pitch)
             o.right = rt_fb(fb[1].data_ptr(), fmt, pitch)
@@ -375,6 +380,8 @@ class StereoRenderer:
             flags |= RT_RENDER_COUNT
         if brute:
             flags |= RT_RENDER_BRUTE_FORCE
+        if peer:
+            flags |= RT_RENDER_PEER_STORE
         p = rt_render_params(width, height, max_depth, shard[0], shard[1], flags)
         rt_render_stereo_ex(self.ctx, p, o)
         if count:

@@ -25,7 +25,7 @@ def _free_port():
 
 def _worker(rank, world, port, W, H, q):
     sys.path.insert(0, ROOT)
-    import bench
+    import bench  # noqa: F401  (gather_to_root re-export)
     from paper_1702_01530_b200 import rt
     from tests.test_abi import expected_image, synth_shards
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
