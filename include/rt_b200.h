@@ -228,11 +228,14 @@ rt_status rt_unpack_shards(rt_context* ctx, const void* gathered, uint32_t width
                            uint32_t world, uint32_t format, rt_fb left, rt_fb right);
 
 /* ------------------------------------------------------------------ peer memory (fused gather) */
-/* CUDA IPC: export a DEVICE allocation of this process as a 64-byte handle, open a peer's
- * handle to get a device pointer that kernels of this context may store to (NVLink P2P,
- * or the same device), and close it.  Used by the fused render->gather path in which each
- * rank's pack epilogue writes its tiles straight into rank 0's framebuffers. */
-rt_status rt_ipc_get_handle(const void* dev_ptr, void* handle64);
+/* CUDA IPC: export the DEVICE allocation containing dev_ptr as a 64-byte handle plus the byte
+ * offset of dev_ptr inside that allocation (allocations from caching allocators such as
+ * torch's are sub-ranges of a larger cudaMalloc block; the handle always maps the block base),
+ * open a peer's handle to get a device pointer to the block base that kernels of this context
+ * may store to (NVLink P2P, or the same device), and close it.  Used by the fused
+ * render->gather path in which each rank's pack epilogue writes its tiles straight into rank
+ * 0's framebuffers (base + offset). */
+rt_status rt_ipc_get_handle(const void* dev_ptr, void* handle64, uint64_t* offset);
 rt_status rt_ipc_open(rt_context* ctx, const void* handle64, void** dev_ptr);
 rt_status rt_ipc_close(rt_context* ctx, void* dev_ptr);
 

@@ -3,6 +3,7 @@
 // Owns the per-context CUDA streams (render + copy), the device scene (SoA records + LBVH),
 // the camera block, the work counter of the persistent kernel, and the events of the pinned
 // download path.  No exception crosses the ABI: every entry point catches and maps to rt_status.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -751,13 +752,24 @@ rt_status rt_unpack_shards(rt_context* c, const void* gathered, uint32_t W, uint
 }
 
 // ------------------------------------------------------------------------------ peer memory
-rt_status rt_ipc_get_handle(const void* dev_ptr, void* handle64) {
-    if (!dev_ptr || !handle64) return fail(RT_ERR_INVALID_ARG, "rt_ipc_get_handle: NULL argument");
+rt_status rt_ipc_get_handle(const void* dev_ptr, void* handle64, uint64_t* offset) {
+    if (!dev_ptr || !handle64 || !offset) return fail(RT_ERR_INVALID_ARG, "rt_ipc_get_handle: NULL argument");
     static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+    // driver entry point through the runtime (the library does not link libcuda directly)
+    using GetRange = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
+        return fail(RT_ERR_PEER, "cuMemGetAddressRange entry point unavailable");
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    CUresult r = reinterpret_cast<GetRange>(fn)(&base, &size, (CUdeviceptr)dev_ptr);
+    if (r != CUDA_SUCCESS) return fail(RT_ERR_PEER, "cuMemGetAddressRange failed (%d)", (int)r);
     cudaIpcMemHandle_t h;
-    cudaError_t e = cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr));
+    cudaError_t e = cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base));
     if (e != cudaSuccess) return fail(RT_ERR_PEER, "cudaIpcGetMemHandle: %s", cudaGetErrorString(e));
     memcpy(handle64, &h, 64);
+    *offset = (uint64_t)((CUdeviceptr)dev_ptr - base);
     return RT_OK;
 }
 

@@ -67,7 +67,9 @@ class PeerFrame:
         if rank == 0:
             base = fb.data_ptr()
         else:
-            base = self.mapped = rt.rt_ipc_open(R.ctx, handle[0])
+            h, offset = handle[0]
+            self.mapped = rt.rt_ipc_open(R.ctx, h)
+            base = self.mapped + offset
         self.ptrs = (base, base + height * width * 4, width * 4)      # (2, H, W, 4) u8 layout
         self.launches_per_frame = 1
 

@@ -99,7 +99,7 @@ def lib():
             "rt_shard_bytes": [u32, u32, u32, u32, C.POINTER(u64)],
             "rt_unpack_shards_host": [vp, u32, u32, u32, u32, vp, vp, u64],
             "rt_unpack_shards": [vp, vp, u32, u32, u32, u32, rt_fb, rt_fb],
-            "rt_ipc_get_handle": [vp, vp], "rt_ipc_open": [vp, vp, C.POINTER(vp)], "rt_ipc_close": [vp, vp],
+            "rt_ipc_get_handle": [vp, vp, C.POINTER(u64)], "rt_ipc_open": [vp, vp, C.POINTER(vp)], "rt_ipc_close": [vp, vp],
             "rt_scene_info": [vp, vp],
             "rt_bvh_export": [vp, vp, C.POINTER(u32), vp, C.POINTER(u32)],
             "rt_bench_ffma": [vp, u32, C.POINTER(C.c_double), C.POINTER(C.c_double)],
@@ -267,9 +267,11 @@ def rt_unpack_shards(ctx, gathered_ptr, width, height, world, fmt, left_fb, righ
 
 
 def rt_ipc_get_handle(dev_ptr):
+    """-> (64-byte handle of the allocation containing dev_ptr, byte offset of dev_ptr in it)"""
     h = (C.c_char * 64)()
-    _check(lib().rt_ipc_get_handle(dev_ptr, C.cast(h, C.c_void_p)))
-    return bytes(h)
+    off = C.c_uint64()
+    _check(lib().rt_ipc_get_handle(dev_ptr, C.cast(h, C.c_void_p), C.byref(off)))
+    return bytes(h), off.value
 
 
 def rt_ipc_open(ctx, handle):
