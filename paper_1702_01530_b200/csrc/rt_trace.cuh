@@ -1,0 +1,233 @@
+// rt_trace.cuh -- device code shared by the trace kernels: work-item -> pixel mapping, output
+// packing, primitive tests, 4-wide BVH traversal (nearest hit and any hit).
+#pragma once
+#include "rt_device.cuh"
+#include "rt_internal.h"
+
+namespace rtb {
+
+template <bool COUNT>
+struct Counters {
+    uint32_t c[RT_NUM_COUNTERS_INTERNAL];
+    __device__ void zero() {
+#pragma unroll
+        for (int i = 0; i < RT_NUM_COUNTERS_INTERNAL; ++i) c[i] = 0;
+    }
+    __device__ __forceinline__ void add(int i, uint32_t n = 1) { if (COUNT) c[i] += n; }
+};
+
+struct Hit {
+    float t;
+    int gid;    // global primitive ID, -1 = miss
+    int slot;   // BVH prim slot (>= 0) or ~plane index (< 0)
+};
+
+// Work item -> (eye, px, py).  16x16 tiles, each tile = 8 warps of 8x4 pixels so a warp's
+// primary rays are spatially coherent.  Tiles are drawn from this rank's shard.
+template <typename Params>
+__device__ __forceinline__ bool map_work(const Params& P, int k, int& eye, int& px, int& py) {
+    const int lt = k >> 8;
+    const int within = k & 255;
+    int g;
+    if (P.shard_mode == 0) {
+        g = lt;
+    } else if (P.shard_mode == 1) {
+        const int grp = P.shard_rank / P.shard_half;
+        const int j = P.shard_rank % P.shard_half;
+        g = grp * P.tiles_per_eye + j + lt * P.shard_half;
+    } else {
+        g = P.shard_rank + lt * P.shard_world;
+    }
+    eye = g / P.tiles_per_eye;
+    const int t = g - eye * P.tiles_per_eye;
+    const int tx = t % P.tiles_x, ty = t / P.tiles_x;
+    const int w = within >> 5, lane = within & 31;
+    px = tx * TILE + (w & 1) * 8 + (lane & 7);
+    py = ty * TILE + (w >> 1) * 4 + (lane >> 3);
+    return px < P.W && py < P.H;
+}
+
+__device__ __forceinline__ uint32_t pack_rgba8(float3 c) {
+    const float r = __saturatef(c.x), g = __saturatef(c.y), b = __saturatef(c.z);
+    const uint32_t R = __float2uint_rd(fmaf(r, 255.0f, 0.5f));
+    const uint32_t G = __float2uint_rd(fmaf(g, 255.0f, 0.5f));
+    const uint32_t B = __float2uint_rd(fmaf(b, 255.0f, 0.5f));
+    return R | (G << 8) | (B << 16) | (0xFFu << 24);
+}
+
+__device__ __forceinline__ uint2 pack_rgba16f(float3 c) {
+    const __half r = __float2half_rn(__saturatef(c.x)), g = __float2half_rn(__saturatef(c.y));
+    const __half b = __float2half_rn(__saturatef(c.z)), a = __float2half_rn(1.0f);
+    return make_uint2((uint32_t)__half_as_ushort(r) | ((uint32_t)__half_as_ushort(g) << 16),
+                      (uint32_t)__half_as_ushort(b) | ((uint32_t)__half_as_ushort(a) << 16));
+}
+
+__device__ __forceinline__ void store_px(void* base, int fmt, long long pitch, int x, int y, float3 c) {
+    char* row = static_cast<char*>(base) + (long long)y * pitch;
+    if (fmt == RT_FORMAT_RGBA8) reinterpret_cast<uint32_t*>(row)[x] = pack_rgba8(c);
+    else reinterpret_cast<uint2*>(row)[x] = pack_rgba16f(c);
+}
+
+// Primitive test shared by the BVH leaves and the brute-force path (bit-identical results).
+template <bool COUNT>
+__device__ __forceinline__ bool prim_t(const DevScene& S, int k, float3 o, float3 d, float& t, int& gid,
+                                       Counters<COUNT>& cnt) {
+    const float4 a = __ldg(&S.prims[3 * k]);
+    gid = __float_as_int(a.w);
+    if (gid < S.n_spheres) {
+        cnt.add(CNT_SPHERE_TESTS);
+        return sphere_intersect(o, d, a, __ldg(&S.prims[3 * k + 1]), T_MIN, t);
+    }
+    cnt.add(CNT_TRI_TESTS);
+    return tri_intersect(o, d, a, __ldg(&S.prims[3 * k + 1]), __ldg(&S.prims[3 * k + 2]), t) && t > T_MIN;
+}
+
+// Box tests of the 4 children of one BVH4 node (7 float4: lo.x hi.x lo.y hi.y lo.z hi.z child).
+// Returns the hit mask; tn[c] = entry distance of hit children.
+__device__ __forceinline__ unsigned node4_hits(const float4* __restrict__ nodes, int node, const RayBox& rb, float tmax,
+                                               float tn[4], int4& child) {
+    const float4* q = nodes + 7 * node;
+    const float4 nx = __ldg(q + rb.sx), fx = __ldg(q + 1 - rb.sx);
+    const float4 ny = __ldg(q + 2 + rb.sy), fy = __ldg(q + 3 - rb.sy);
+    const float4 nz = __ldg(q + 4 + rb.sz), fz = __ldg(q + 5 - rb.sz);
+    child = __ldg(reinterpret_cast<const int4*>(q + 6));
+    tn[0] = slab(rb, nx.x, fx.x, ny.x, fy.x, nz.x, fz.x, tmax);
+    tn[1] = slab(rb, nx.y, fx.y, ny.y, fy.y, nz.y, fz.y, tmax);
+    tn[2] = slab(rb, nx.z, fx.z, ny.z, fy.z, nz.z, fz.z, tmax);
+    tn[3] = slab(rb, nx.w, fx.w, ny.w, fy.w, nz.w, fz.w, tmax);
+    unsigned m = 0;
+    m |= (tn[0] >= 0.0f && child.x != WIDE_EMPTY) ? 1u : 0u;
+    m |= (tn[1] >= 0.0f && child.y != WIDE_EMPTY) ? 2u : 0u;
+    m |= (tn[2] >= 0.0f && child.z != WIDE_EMPTY) ? 4u : 0u;
+    m |= (tn[3] >= 0.0f && child.w != WIDE_EMPTY) ? 8u : 0u;
+    return m;
+}
+
+__device__ __forceinline__ void cswap(uint32_t& a, uint32_t& b) {
+    const uint32_t lo = min(a, b), hi = max(a, b);
+    a = lo;
+    b = hi;
+}
+
+// child code of slot i (0..3) with selects only (no branches)
+__device__ __forceinline__ int pick4(const int4& c, uint32_t i) {
+    const int lo = (i & 1u) ? c.y : c.x;
+    const int hi = (i & 1u) ? c.w : c.z;
+    return (i & 2u) ? hi : lo;
+}
+
+// Visit order of the hit children: entry distances are >= 0, so their bit patterns order like
+// unsigned ints; the 2 low bits carry the child slot; a 5-exchange network sorts them.  The
+// nearest hit continues, the others are pushed far-to-near (predicated stores, no branches).
+__device__ __forceinline__ bool order_push(unsigned m, const float tn[4], const int4& ch, int* stk, int& sp, int& node) {
+    if (!m) return false;
+    uint32_t k0 = (m & 1) ? ((__float_as_uint(tn[0]) & ~3u) | 0u) : 0xffffffffu;
+    uint32_t k1 = (m & 2) ? ((__float_as_uint(tn[1]) & ~3u) | 1u) : 0xffffffffu;
+    uint32_t k2 = (m & 4) ? ((__float_as_uint(tn[2]) & ~3u) | 2u) : 0xffffffffu;
+    uint32_t k3 = (m & 8) ? ((__float_as_uint(tn[3]) & ~3u) | 3u) : 0xffffffffu;
+    cswap(k0, k1); cswap(k2, k3); cswap(k0, k2); cswap(k1, k3); cswap(k1, k2);
+    const int nh = __popc(m);
+    if (nh > 3) stk[(sp + nh - 4) * 256] = pick4(ch, k3 & 3u);
+    if (nh > 2) stk[(sp + nh - 3) * 256] = pick4(ch, k2 & 3u);
+    if (nh > 1) stk[(sp + nh - 2) * 256] = pick4(ch, k1 & 3u);
+    sp += nh - 1;
+    node = pick4(ch, k0 & 3u);
+    return true;
+}
+
+
+// Nearest hit over the 4-wide BVH (or every BVH primitive when BRUTE) and the planes.
+// Acceptance: t > t_min and (t, gid) lexicographically smallest (reading 9).
+// Children are visited near-to-far: entry distances (>= 0, so their bit patterns order like
+// unsigned ints) carry the child slot in their 2 low bits and go through a 5-exchange sorting
+// network; the 3 farther hits are pushed on the shared-memory stack.
+template <bool COUNT, bool BRUTE>
+__device__ __forceinline__ Hit closest_hit(const DevScene& S, float3 o, float3 d, int* stk, Counters<COUNT>& cnt) {
+    Hit h;
+    h.t = __int_as_float(0x7f800000);
+    h.gid = -1;
+    h.slot = 0;
+    for (int i = 0; i < S.n_planes; ++i) {
+        cnt.add(CNT_PLANE_TESTS);
+        float t;
+        if (plane_intersect(o, d, __ldg(&S.planes[i]), t) && t > T_MIN) {
+            const int gid = S.n_spheres + i;
+            if (t < h.t || (t == h.t && gid < h.gid)) { h.t = t; h.gid = gid; h.slot = ~i; }
+        }
+    }
+    if (S.n_bvh == 0) return h;
+    auto leaf_test = [&](int first, int last) {
+        for (int k = first; k <= last; ++k) {
+            float t;
+            int gid;
+            if (prim_t<COUNT>(S, k, o, d, t, gid, cnt) && (t < h.t || (t == h.t && gid < h.gid))) {
+                h.t = t; h.gid = gid; h.slot = k;
+            }
+        }
+    };
+    if (BRUTE) {
+        leaf_test(0, S.n_bvh - 1);
+        return h;
+    }
+    const RayBox rb = make_raybox(o, d, S.bound);
+    int sp = 0;
+    int node = S.root;
+    while (true) {
+        if (node >= 0) {
+            cnt.add(CNT_NODE_VISITS);
+            float tn[4];
+            int4 ch;
+            const unsigned m = node4_hits(S.nodes, node, rb, h.t, tn, ch);
+            if (order_push(m, tn, ch, stk, sp, node)) continue;
+        } else {
+            const int enc = ~node;
+            const int first = enc & ((1 << LEAF_SHIFT) - 1);
+            leaf_test(first, first + (enc >> LEAF_SHIFT));
+        }
+        if (sp == 0) return h;
+        --sp;
+        node = stk[sp * 256];
+    }
+}
+
+// Any hit with t_min < t < dist (binary visibility, reading 4); children near-to-far.
+template <bool COUNT, bool BRUTE>
+__device__ __forceinline__ bool occluded(const DevScene& S, float3 o, float3 d, float dist, int* stk, Counters<COUNT>& cnt) {
+    for (int i = 0; i < S.n_planes; ++i) {
+        cnt.add(CNT_PLANE_TESTS);
+        float t;
+        if (plane_intersect(o, d, __ldg(&S.planes[i]), t) && t > T_MIN && t < dist) return true;
+    }
+    if (S.n_bvh == 0) return false;
+    auto leaf_test = [&](int first, int last) -> bool {
+        for (int k = first; k <= last; ++k) {
+            float t;
+            int gid;
+            if (prim_t<COUNT>(S, k, o, d, t, gid, cnt) && t < dist) return true;
+        }
+        return false;
+    };
+    if (BRUTE) return leaf_test(0, S.n_bvh - 1);
+    const RayBox rb = make_raybox(o, d, S.bound);
+    int sp = 0;
+    int node = S.root;
+    while (true) {
+        if (node >= 0) {
+            cnt.add(CNT_NODE_VISITS);
+            float tn[4];
+            int4 ch;
+            const unsigned m = node4_hits(S.nodes, node, rb, dist, tn, ch);
+            if (order_push(m, tn, ch, stk, sp, node)) continue;
+        } else {
+            const int enc = ~node;
+            const int first = enc & ((1 << LEAF_SHIFT) - 1);
+            if (leaf_test(first, first + (enc >> LEAF_SHIFT))) return true;
+        }
+        if (sp == 0) return false;
+        --sp;
+        node = stk[sp * 256];
+    }
+}
+
+
+}  // namespace rtb
