@@ -79,20 +79,6 @@ struct rt_context {
     bool has_camera = false;
     double cam_eye[2][3], cam_f[3], cam_r[3], cam_u[3], cam_th, cam_sigma_unit;
     float vfov = 0;
-    float4* rq_overflow = nullptr;   // (megakernel path only)
-    size_t rq_overflow_bytes = 0;
-    bool has_refraction = false;     // any material with kt > 0 -> queues may grow per level
-    bool use_mega = false;           // env RT_PATH=mega: per-thread megakernel (A/B comparisons)
-    // wavefront buffers (grow-only)
-    float4* wq[2] = {nullptr, nullptr};
-    size_t wq_cap[2] = {0, 0};
-    int4* whits = nullptr;
-    size_t whits_cap = 0;
-    float4* wshadow = nullptr;
-    size_t wshadow_cap = 0;          // float4 elements (3 per shadow ray)
-    unsigned long long* wacc = nullptr;
-    size_t wacc_cap = 0;
-    int* wcounts = nullptr;          // [0..31] level ray counts, [32..95] shadow counts, [96] overflow
     int leaf_max = 1;                // LBVH leaf collapse threshold (env RT_LEAF_MAX, <= 16)
 };
 
@@ -138,7 +124,6 @@ rt_status rt_create(int device, void* cuda_stream, rt_context** out) {
     if (!c) return fail(RT_ERR_OOM, "rt_create: host allocation");
     c->device = device;
     if (const char* lm = getenv("RT_LEAF_MAX")) c->leaf_max = std::max(1, std::min(16, atoi(lm)));
-    if (const char* pm = getenv("RT_PATH")) c->use_mega = std::string(pm) == "mega";
     cudaError_t e = cudaSetDevice(device);
     if (e == cudaSuccess && cuda_stream) {
         c->stream = static_cast<cudaStream_t>(cuda_stream);
@@ -151,7 +136,6 @@ rt_status rt_create(int device, void* cuda_stream, rt_context** out) {
     if (e == cudaSuccess) e = cudaMalloc(&c->work_counter, 64 * sizeof(int));
     if (e == cudaSuccess) e = cudaMalloc(&c->scratch_counters, RT_NUM_COUNTERS * sizeof(unsigned long long));
     if (e == cudaSuccess) e = cudaMalloc(&c->ffma_out, 64);
-    if (e == cudaSuccess) e = cudaMalloc(&c->wcounts, 128 * sizeof(int));
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
     if (e != cudaSuccess) {
         rt_destroy(c);
@@ -170,13 +154,6 @@ rt_status rt_destroy(rt_context* c) {
     if (c->work_counter) cudaFree(c->work_counter);
     if (c->scratch_counters) cudaFree(c->scratch_counters);
     if (c->ffma_out) cudaFree(c->ffma_out);
-    if (c->rq_overflow) cudaFree(c->rq_overflow);
-    for (int i = 0; i < 2; ++i)
-        if (c->wq[i]) cudaFree(c->wq[i]);
-    if (c->whits) cudaFree(c->whits);
-    if (c->wshadow) cudaFree(c->wshadow);
-    if (c->wacc) cudaFree(c->wacc);
-    if (c->wcounts) cudaFree(c->wcounts);
     if (c->order_ev) cudaEventDestroy(c->order_ev);
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
@@ -196,7 +173,6 @@ rt_status rt_synchronize(rt_context* c) {
 rt_status rt_scene_upload(rt_context* c, const rt_primitives* P, const rt_material* mats, uint32_t n_mats,
                           const rt_light* lights, uint32_t n_lights, const rt_env* env) {
     if (!c || !P || !env) return fail(RT_ERR_INVALID_ARG, "rt_scene_upload: NULL context/primitives/env");
-    if (n_lights > 64) return fail(RT_ERR_INVALID_ARG, "rt_scene_upload: at most 64 lights");
     if ((n_mats && !mats) || (n_lights && !lights))
         return fail(RT_ERR_INVALID_ARG, "rt_scene_upload: NULL materials/lights with nonzero count");
     const uint32_t S = P->n_spheres, PL = P->n_planes, T = P->n_triangles, V = P->n_vertices;
@@ -425,8 +401,6 @@ rt_status rt_scene_upload(rt_context* c, const rt_primitives* P, const rt_materi
     c->info[5] = (uint64_t)depth4;
     c->info[6] = bytes;
     c->info[7] = (uint64_t)std::chrono::duration_cast<std::chrono::microseconds>(t1 - t0).count();
-    c->has_refraction = false;
-    for (uint32_t i = 0; i < n_mats; ++i) c->has_refraction |= mats[i].kt > 0.0f;
     c->has_scene = true;
     return RT_OK;
 }
@@ -525,109 +499,6 @@ rt_status check_fb(const rt_fb& fb, uint32_t W, const char* name) {
     return RT_OK;
 }
 
-
-// ------------------------------------------------------------------------------ wavefront path
-template <typename T>
-rt_status grow(rt_context* c, T** buf, size_t* cap, size_t need, const char* what) {
-    if (need <= *cap) return RT_OK;
-    if (*buf) {
-        cudaError_t e = cudaStreamSynchronize(c->stream);
-        if (e != cudaSuccess) return fail(RT_ERR_CUDA, "grow %s: %s", what, cudaGetErrorString(e));
-        cudaFree(*buf);
-        *buf = nullptr;
-        *cap = 0;
-    }
-    cudaError_t e = cudaMalloc(buf, need * sizeof(T));
-    if (e != cudaSuccess) return fail(RT_ERR_OOM, "cudaMalloc %s (%zu bytes): %s", what, need * sizeof(T), cudaGetErrorString(e));
-    *cap = need;
-    return RT_OK;
-}
-
-// Bounce levels 0..max_depth of k_extend -> k_shade -> k_occlude, then k_finalize.  Without a
-// refractive material every level holds at most one ray per pixel, so n_work-sized queues
-// suffice and nothing synchronises with the host; with refraction the level sizes are read back
-// (one sync per level) and the next queue grown to twice the level's rays.
-rt_status render_wave(rt_context* c, const TraceParams& T, unsigned flags) {
-    WaveParams P{};
-    P.sc = T.sc;
-    P.cam = T.cam;
-    P.W = T.W;
-    P.H = T.H;
-    P.max_depth = T.max_depth;
-    P.n_work = T.n_work;
-    P.tiles_x = T.tiles_x;
-    P.tiles_per_eye = T.tiles_per_eye;
-    P.shard_mode = T.shard_mode;
-    P.shard_rank = T.shard_rank;
-    P.shard_world = T.shard_world;
-    P.shard_half = T.shard_half;
-    for (int e = 0; e < 2; ++e) {
-        P.fb[e] = T.fb[e];
-        P.fb_fmt[e] = T.fb_fmt[e];
-        P.fb_pitch[e] = T.fb_pitch[e];
-    }
-    P.prim_id = T.prim_id;
-    P.radiance = T.radiance;
-    P.shard = T.shard;
-    P.shard_fmt = T.shard_fmt;
-    P.counters = T.counters;
-    P.stack_entries = T.stack_entries;
-    P.peer_fence = T.peer_fence;
-    const size_t nw = (size_t)P.n_work;
-    const int nl = std::max(1, P.sc.n_lights);
-    rt_status st;
-    if ((st = grow(c, &c->wq[0], &c->wq_cap[0], 2 * nw, "ray queue")) ||
-        (st = grow(c, &c->wq[1], &c->wq_cap[1], 2 * nw, "ray queue")) ||
-        (st = grow(c, &c->whits, &c->whits_cap, nw, "hits")) ||
-        (st = grow(c, &c->wacc, &c->wacc_cap, 3 * nw, "accumulators")) ||
-        (st = grow(c, &c->wshadow, &c->wshadow_cap, 3 * nw * nl, "shadow queue")))
-        return st;
-    int occ = 0;
-    CUDA_TRY(rtb_wave_occupancy(flags, P.stack_entries, &occ));
-    const int grid = c->num_sms * std::max(1, occ);
-    CUDA_TRY(cudaMemsetAsync(c->wcounts, 0, 128 * sizeof(int), c->stream));
-    CUDA_TRY(cudaMemsetAsync(c->wacc, 0, 3 * nw * sizeof(unsigned long long), c->stream));
-    P.acc = c->wacc;
-    P.overflow = c->wcounts + 96;
-    P.n_shadow = c->wcounts + 32;
-    P.hits = c->whits;
-    for (int L = 0; L <= P.max_depth; ++L) {
-        if (L > 0) CUDA_TRY(cudaMemsetAsync(c->wcounts + 32, 0, 64 * sizeof(int), c->stream));
-        if (c->has_refraction) {
-            size_t n_level = nw;
-            if (L > 0) {
-                int cnt = 0;
-                CUDA_TRY(cudaMemcpyAsync(&cnt, c->wcounts + L, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-                CUDA_TRY(cudaStreamSynchronize(c->stream));
-                if (cnt == 0) break;
-                n_level = (size_t)cnt;
-            }
-            // this level: <= n_level hits and shadow rays per light; next level <= 2 n_level rays
-            if ((st = grow(c, &c->whits, &c->whits_cap, n_level, "hits")) ||
-                (st = grow(c, &c->wq[(L + 1) & 1], &c->wq_cap[(L + 1) & 1], 4 * n_level, "ray queue")) ||
-                (st = grow(c, &c->wshadow, &c->wshadow_cap, 3 * n_level * nl, "shadow queue")))
-                return st;
-        }
-        P.level = L;
-        P.q_in = c->wq[L & 1];
-        P.n_in = c->wcounts + L;
-        P.q_out = c->wq[(L + 1) & 1];
-        P.n_out = c->wcounts + L + 1;
-        P.cap_rays = (int)std::min<size_t>(c->wq_cap[(L + 1) & 1] / 2, INT32_MAX);
-        P.hits = c->whits;
-        P.shadow = c->wshadow;
-        P.cap_shadow = (int)std::min<size_t>(c->wshadow_cap / (3 * (size_t)nl), INT32_MAX);
-        CUDA_TRY(rtb_wave_level(P, flags, grid, c->stream));
-    }
-    CUDA_TRY(rtb_wave_finalize(P, grid, c->stream));
-    if (c->has_refraction) {
-        int ovf = 0;
-        CUDA_TRY(cudaMemcpyAsync(&ovf, c->wcounts + 96, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-        CUDA_TRY(cudaStreamSynchronize(c->stream));
-        if (ovf) return fail(RT_ERR_CUDA, "wavefront queue overflow (sizing bug)");
-    }
-    return RT_OK;
-}
 }  // namespace
 
 extern "C" {
@@ -681,7 +552,6 @@ rt_status rt_render_stereo_ex(rt_context* c, const rt_render_params* p, const rt
     P.peer_fence = (p->flags & RT_RENDER_PEER_STORE) ? 1 : 0;
     if (P.n_work == 0) return RT_OK;
     CUDA_TRY(cudaSetDevice(c->device));
-    if (!c->use_mega) return render_wave(c, P, p->flags & (RT_RENDER_COUNT | RT_RENDER_BRUTE_FORCE));
     int occ = 0;
     CUDA_TRY(rtb_trace_occupancy(p->flags & (RT_RENDER_COUNT | RT_RENDER_BRUTE_FORCE), P.stack_entries, &occ));
     if (occ < 1) occ = 1;

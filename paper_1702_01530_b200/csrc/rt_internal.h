@@ -42,44 +42,6 @@ struct TraceParams {
     int stack_entries;      // BVH traversal stack depth (shared memory, [entry][thread])
     int n_tiles;            // 16x16 tiles in this shard (= n_work / 256)
     int peer_fence;         // framebuffers live in a peer's memory: fence system-wide at exit
-    float4* rq_overflow;    // per-CTA global spill of the tree-ray stack (2 float4 per entry)
-    int rq_overflow_entries;
-};
-
-// Wavefront path (rt_wave.cu): per bounce level L, k_extend (nearest hit of every tree ray of
-// the level), k_shade (local term, one shadow ray per lit light into per-light queues,
-// reflection/refraction children into the next level's queue), k_occlude (any hit of the
-// shadow queues); k_finalize packs the fixed-point accumulators.
-struct WaveParams {
-    rtb::DevScene sc;
-    rtb::DevCamera cam;
-    int W, H, max_depth, level;
-    int n_work;             // work items (pixels incl. tile padding) of this shard
-    int tiles_x, tiles_per_eye;
-    int shard_mode, shard_rank, shard_world, shard_half;
-    // queues (level L reads q_in/hits, writes q_out/shadow)
-    float4* q_in;           // [cap][2]: (o.xyz, w) (d.xyz, work item as int)
-    const int* n_in;        // device count of q_in (level 0: n_work, generated in place)
-    float4* q_out;
-    int* n_out;
-    int cap_rays;
-    int4* hits;             // [cap]: (t bits, slot, gid, -)
-    float4* shadow;         // [n_lights][cap][3]: (o.xyz, dist) (d.xyz, item) (contrib.xyz, -)
-    int* n_shadow;          // [n_lights]
-    int cap_shadow;
-    unsigned long long* acc;// [n_work][3] radiance, 2^-40 fixed point
-    int* overflow;          // set if a queue capacity was exceeded (sizing bug guard)
-    // outputs
-    void* fb[2];
-    int fb_fmt[2];
-    long long fb_pitch[2];
-    int* prim_id;
-    float4* radiance;
-    void* shard;
-    int shard_fmt;
-    unsigned long long* counters;
-    int stack_entries;
-    int peer_fence;
 };
 
 struct UnpackParams {
@@ -128,11 +90,6 @@ struct BuildBuffers {
 cudaError_t rtb_launch_trace(const TraceParams& P, unsigned flags, int grid, cudaStream_t st);
 cudaError_t rtb_trace_occupancy(unsigned flags, int stack_entries, int* blocks_per_sm);
 size_t rtb_trace_smem(int stack_entries);
-int rtb_rq_overflow_entries(int max_depth);
-// launchers (rt_wave.cu)
-cudaError_t rtb_wave_level(const WaveParams& P, unsigned flags, int grid, cudaStream_t st);
-cudaError_t rtb_wave_finalize(const WaveParams& P, int grid, cudaStream_t st);
-cudaError_t rtb_wave_occupancy(unsigned flags, int stack_entries, int* blocks_per_sm);
 cudaError_t rtb_launch_unpack(const void* gathered, const UnpackParams& U, cudaStream_t st);
 cudaError_t rtb_launch_ffma(float* out, int iters, int grid, cudaStream_t st);
 // launchers (rt_build.cu)

@@ -229,7 +229,6 @@ static const void* trace_fn(unsigned flags) {
 
 size_t rtb_trace_smem(int stack_entries) { return (size_t)stack_entries * 256 * sizeof(int); }
 
-int rtb_rq_overflow_entries(int) { return 0; }   // v3 keeps tree rays per thread
 
 cudaError_t rtb_launch_trace(const TraceParams& P, unsigned flags, int grid, cudaStream_t st) {
     const size_t smem = rtb_trace_smem(P.stack_entries);
