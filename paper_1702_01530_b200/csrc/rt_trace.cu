@@ -124,8 +124,8 @@ __device__ __forceinline__ float3 trace_pixel(const TraceParams& P, float3 o, fl
 // Persistent warps: each warp takes 32 consecutive work items (one 8x4 pixel block) per
 // atomic and traces one pixel tree per lane; the BVH stack is in shared memory.
 template <bool COUNT, bool BRUTE>
-__global__ void __launch_bounds__(256, RT_MINB) k_trace_stereo(const TraceParams P) {
-    extern __shared__ int s_stack[];                 // [stack_entries][256]
+__global__ void __launch_bounds__(RT_BLOCK, RT_MINB) k_trace_stereo(const TraceParams P) {
+    extern __shared__ int s_stack[];                 // [stack_entries][RT_BLOCK]
     Counters<COUNT> cnt;
     cnt.zero();
     const int lane = threadIdx.x & 31;
@@ -227,7 +227,7 @@ static const void* trace_fn(unsigned flags) {
                  : (brute ? (const void*)k_trace_stereo<false, true> : (const void*)k_trace_stereo<false, false>);
 }
 
-size_t rtb_trace_smem(int stack_entries) { return (size_t)stack_entries * 256 * sizeof(int); }
+size_t rtb_trace_smem(int stack_entries) { return (size_t)stack_entries * RT_BLOCK * sizeof(int); }
 
 
 cudaError_t rtb_launch_trace(const TraceParams& P, unsigned flags, int grid, cudaStream_t st) {
@@ -236,7 +236,7 @@ cudaError_t rtb_launch_trace(const TraceParams& P, unsigned flags, int grid, cud
     cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     void* args[] = {const_cast<TraceParams*>(&P)};
-    return cudaLaunchKernel(f, dim3(grid), dim3(256), args, smem, st);
+    return cudaLaunchKernel(f, dim3(grid), dim3(RT_BLOCK), args, smem, st);
 }
 
 cudaError_t rtb_trace_occupancy(unsigned flags, int stack_entries, int* blocks_per_sm) {
@@ -244,7 +244,7 @@ cudaError_t rtb_trace_occupancy(unsigned flags, int stack_entries, int* blocks_p
     const size_t smem = rtb_trace_smem(stack_entries);
     cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, f, 256, smem);
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, f, RT_BLOCK, smem);
 }
 
 cudaError_t rtb_launch_unpack(const void* gathered, const UnpackParams& U, cudaStream_t st) {

@@ -6,6 +6,10 @@
 
 namespace rtb {
 
+#ifndef RT_BLOCK
+#define RT_BLOCK 256      // threads per trace CTA (stack stride)
+#endif
+
 template <bool COUNT>
 struct Counters {
     uint32_t c[RT_NUM_COUNTERS_INTERNAL];
@@ -127,9 +131,9 @@ __device__ __forceinline__ bool order_push(unsigned m, const float tn[4], const 
     uint32_t k3 = (m & 8) ? ((__float_as_uint(tn[3]) & ~3u) | 3u) : 0xffffffffu;
     cswap(k0, k1); cswap(k2, k3); cswap(k0, k2); cswap(k1, k3); cswap(k1, k2);
     const int nh = __popc(m);
-    if (nh > 3) stk[(sp + nh - 4) * 256] = pick4(ch, k3 & 3u);
-    if (nh > 2) stk[(sp + nh - 3) * 256] = pick4(ch, k2 & 3u);
-    if (nh > 1) stk[(sp + nh - 2) * 256] = pick4(ch, k1 & 3u);
+    if (nh > 3) stk[(sp + nh - 4) * RT_BLOCK] = pick4(ch, k3 & 3u);
+    if (nh > 2) stk[(sp + nh - 3) * RT_BLOCK] = pick4(ch, k2 & 3u);
+    if (nh > 1) stk[(sp + nh - 2) * RT_BLOCK] = pick4(ch, k1 & 3u);
     sp += nh - 1;
     node = pick4(ch, k0 & 3u);
     return true;
@@ -186,7 +190,7 @@ __device__ __forceinline__ Hit closest_hit(const DevScene& S, float3 o, float3 d
         }
         if (sp == 0) return h;
         --sp;
-        node = stk[sp * 256];
+        node = stk[sp * RT_BLOCK];
     }
 }
 
@@ -225,7 +229,7 @@ __device__ __forceinline__ bool occluded(const DevScene& S, float3 o, float3 d, 
         }
         if (sp == 0) return false;
         --sp;
-        node = stk[sp * 256];
+        node = stk[sp * RT_BLOCK];
     }
 }
 
