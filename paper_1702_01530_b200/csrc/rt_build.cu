@@ -334,7 +334,9 @@ __global__ void k_wide(BuildBuffers B, const int2* __restrict__ fin, int n_in, i
         for (int c = 0; c < 4; ++c) {
             if (c >= n) {
                 code4[c] = WIDE_EMPTY;
-                for (int k = 0; k < 3; ++k) { lo[k][c] = 0.f; hi[k][c] = 0.f; }
+                // inverted box (lo = +1e30, hi = -1e30): every slab test rejects it, so the
+                // traversal needs no per-slot validity test
+                for (int k = 0; k < 3; ++k) { lo[k][c] = 1e30f; hi[k][c] = -1e30f; }
                 continue;
             }
             lo[0][c] = ch[c].lo.x; lo[1][c] = ch[c].lo.y; lo[2][c] = ch[c].lo.z;

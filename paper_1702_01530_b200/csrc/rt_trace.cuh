@@ -100,10 +100,10 @@ __device__ __forceinline__ unsigned node4_hits(const float4* __restrict__ nodes,
     tn[2] = slab(rb, nx.z, fx.z, ny.z, fy.z, nz.z, fz.z, tmax);
     tn[3] = slab(rb, nx.w, fx.w, ny.w, fy.w, nz.w, fz.w, tmax);
     unsigned m = 0;
-    m |= (tn[0] >= 0.0f && child.x != WIDE_EMPTY) ? 1u : 0u;
-    m |= (tn[1] >= 0.0f && child.y != WIDE_EMPTY) ? 2u : 0u;
-    m |= (tn[2] >= 0.0f && child.z != WIDE_EMPTY) ? 4u : 0u;
-    m |= (tn[3] >= 0.0f && child.w != WIDE_EMPTY) ? 8u : 0u;
+    m |= tn[0] >= 0.0f ? 1u : 0u;                          // empty slots hold inverted boxes
+    m |= tn[1] >= 0.0f ? 2u : 0u;
+    m |= tn[2] >= 0.0f ? 4u : 0u;
+    m |= tn[3] >= 0.0f ? 8u : 0u;
     return m;
 }
 
