@@ -239,6 +239,21 @@ rt_status rt_ipc_get_handle(const void* dev_ptr, void* handle64, uint64_t* offse
 rt_status rt_ipc_open(rt_context* ctx, const void* handle64, void** dev_ptr);
 rt_status rt_ipc_close(rt_context* ctx, void* dev_ptr);
 
+/* ------------------------------------------------------------------ stereo composition */
+/* PAPER.md:56 (§3: GPU post-processing of the stereo pair "for example, anaglyph/Anamorphic
+ * transformation").  Inputs are the two RGBA8 DEVICE framebuffers of one
+ * render (width x height each); asynchronous on the context stream.
+ *   RT_COMPOSE_ANAGLYPH: out is width x height RGBA8, out = (L.r, R.g, R.b, 255)
+ *   RT_COMPOSE_SBS:      out is (2*floor(width/2)) x height RGBA8; left half = the left image
+ *                        squeezed by column-pair means (per channel, round half up:
+ *                        (a + b + 1) >> 1), right half = the right image likewise; A = 255
+ * Errors: RT_ERR_INVALID_ARG (NULL, non-RGBA8 format, unknown mode, width < 2 for SBS),
+ * RT_ERR_SIZE (pitch too small), RT_ERR_CUDA. */
+#define RT_COMPOSE_ANAGLYPH 0u
+#define RT_COMPOSE_SBS 1u
+rt_status rt_compose(rt_context* ctx, rt_fb left, rt_fb right, uint32_t width, uint32_t height, uint32_t mode,
+                     rt_fb out);
+
 /* ------------------------------------------------------------------ introspection */
 /* Scene statistics after upload: [0] n_spheres [1] n_planes [2] n_triangles [3] bvh prims
  * [4] BVH4 nodes [5] BVH4 depth (levels) [6] device bytes of scene+BVH [7] build time us. */

@@ -80,6 +80,9 @@ def lib():
                                     C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(OracleEps), C.c_int32]
         L.oracle_render.restype = C.c_int
         L.oracle_version.restype = C.c_int
+        for fn in (L.oracle_compose_anaglyph, L.oracle_compose_sbs):
+            fn.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]
+            fn.restype = None
         _lib = L
     return _lib
 
@@ -211,3 +214,17 @@ class Oracle:
 
 def half_bits(x):
     return lib().oracle_half_bits(float(x))
+
+
+def compose(left, right, mode):
+    """SPEC compose_anaglyph / compose_sbs on (H, W, 4) uint8 arrays; mode 'anaglyph' | 'sbs'."""
+    L = np.ascontiguousarray(left, np.uint8)
+    R = np.ascontiguousarray(right, np.uint8)
+    H, W = L.shape[:2]
+    if mode == "anaglyph":
+        out = np.zeros((H, W, 4), np.uint8)
+        lib().oracle_compose_anaglyph(L.ctypes.data, R.ctypes.data, W, H, out.ctypes.data)
+    else:
+        out = np.zeros((H, 2 * (W // 2), 4), np.uint8)
+        lib().oracle_compose_sbs(L.ctypes.data, R.ctypes.data, W, H, out.ctypes.data)
+    return out

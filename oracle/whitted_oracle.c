@@ -590,4 +590,37 @@ int oracle_render(const oracle_scene* sc, const oracle_cam* cam, int32_t max_dep
     return 0;
 }
 
+/* PAPER.md:56 post-processing "anaglyph/Anamorphic transformation"; SPEC.md:445 compose_anaglyph:
+ * out(r,g,b) = (left.r, right.g, right.b), alpha 255.  RGBA8, W x H, row-major. */
+void oracle_compose_anaglyph(const uint8_t* L, const uint8_t* R, int32_t W, int32_t H, uint8_t* out)
+{
+    for (int64_t i = 0; i < (int64_t)W * H; ++i) {
+        out[4 * i + 0] = L[4 * i + 0];
+        out[4 * i + 1] = R[4 * i + 1];
+        out[4 * i + 2] = R[4 * i + 2];
+        out[4 * i + 3] = 255;
+    }
+}
+
+/* SPEC.md:455 compose_sbs: each channel squeezed to floor(W/2) columns by column-pair
+ * averaging (per-channel integer mean, round half up), left | right; out is 2*floor(W/2) x H. */
+void oracle_compose_sbs(const uint8_t* L, const uint8_t* R, int32_t W, int32_t H, uint8_t* out)
+{
+    int32_t half = W / 2, ow = 2 * half;
+    for (int32_t y = 0; y < H; ++y) {
+        for (int32_t x = 0; x < ow; ++x) {
+            const uint8_t* img = x < half ? L : R;
+            int32_t j = x < half ? x : x - half;
+            const uint8_t* a = img + 4 * ((int64_t)y * W + 2 * j);
+            const uint8_t* b = a + 4;
+            uint8_t* o = out + 4 * ((int64_t)y * ow + x);
+            for (int k = 0; k < 3; ++k) {
+                int sum = a[k] + b[k];
+                o[k] = (uint8_t)(sum / 2 + sum % 2);   /* mean rounded half up */
+            }
+            o[3] = 255;
+        }
+    }
+}
+
 int oracle_version(void) { return ORACLE_VERSION; }

@@ -775,6 +775,24 @@ rt_status rt_ipc_close(rt_context* c, void* dev_ptr) {
     return RT_OK;
 }
 
+// ------------------------------------------------------------------------------ composition
+rt_status rt_compose(rt_context* c, rt_fb left, rt_fb right, uint32_t W, uint32_t H, uint32_t mode, rt_fb out) {
+    if (!c || !left.dev_ptr || !right.dev_ptr || !out.dev_ptr) return fail(RT_ERR_INVALID_ARG, "rt_compose: NULL argument");
+    if (left.format != RT_FORMAT_RGBA8 || right.format != RT_FORMAT_RGBA8 || out.format != RT_FORMAT_RGBA8)
+        return fail(RT_ERR_INVALID_ARG, "rt_compose: RGBA8 framebuffers only");
+    if (mode != RT_COMPOSE_ANAGLYPH && mode != RT_COMPOSE_SBS) return fail(RT_ERR_INVALID_ARG, "rt_compose: mode %u", mode);
+    if (W == 0 || H == 0 || W > 16384 || H > 16384) return fail(RT_ERR_SIZE, "rt_compose: size %ux%u", W, H);
+    if (mode == RT_COMPOSE_SBS && W < 2) return fail(RT_ERR_INVALID_ARG, "rt_compose: SBS needs width >= 2");
+    const uint64_t out_w = mode == RT_COMPOSE_ANAGLYPH ? W : 2 * (W / 2);
+    rt_status st;
+    if ((st = check_fb(left, W, "left")) || (st = check_fb(right, W, "right")) || (st = check_fb(out, (uint32_t)out_w, "out")))
+        return st;
+    CUDA_TRY(cudaSetDevice(c->device));
+    CUDA_TRY(rtb_launch_compose(left.dev_ptr, right.dev_ptr, (long long)left.pitch_bytes, (long long)right.pitch_bytes,
+                                (int)W, (int)H, (int)mode, out.dev_ptr, (long long)out.pitch_bytes, c->stream));
+    return RT_OK;
+}
+
 // ------------------------------------------------------------------------------ introspection
 rt_status rt_scene_info(rt_context* c, uint64_t info[8]) {
     if (!c || !info) return fail(RT_ERR_INVALID_ARG, "rt_scene_info: NULL argument");

@@ -92,6 +92,8 @@ cudaError_t rtb_trace_occupancy(unsigned flags, int stack_entries, int* blocks_p
 size_t rtb_trace_smem(int stack_entries);
 cudaError_t rtb_launch_unpack(const void* gathered, const UnpackParams& U, cudaStream_t st);
 cudaError_t rtb_launch_ffma(float* out, int iters, int grid, cudaStream_t st);
+cudaError_t rtb_launch_compose(const void* L, const void* R, long long lp, long long rp, int W, int H, int mode,
+                               void* out, long long op, cudaStream_t st);
 // launchers (rt_build.cu)
 size_t rtb_sort_hist_entries(int n);
 cudaError_t rtb_build_bvh(const BuildBuffers& B, cudaStream_t st, int* root, int* n_nodes4, int* depth4);

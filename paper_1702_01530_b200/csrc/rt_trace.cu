@@ -202,6 +202,32 @@ __global__ void k_unpack_shards(const void* __restrict__ gathered, UnpackParams 
     }
 }
 
+// Stereo-pair composition (PAPER.md:56 post-processing): anaglyph
+// (L.r, R.g, R.b) or anamorphic side-by-side (column-pair means, round half up).
+__global__ void k_compose(const uchar4* __restrict__ L, const uchar4* __restrict__ R, long long lp, long long rp,
+                          int W, int H, int mode, uchar4* __restrict__ out, long long op) {
+    const int out_w = mode == 0 ? W : 2 * (W / 2);
+    const long long n = (long long)out_w * H;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const int y = (int)(i / out_w), x = (int)(i - (long long)y * out_w);
+        const uchar4* lrow = reinterpret_cast<const uchar4*>(reinterpret_cast<const char*>(L) + y * lp);
+        const uchar4* rrow = reinterpret_cast<const uchar4*>(reinterpret_cast<const char*>(R) + y * rp);
+        uchar4 o;
+        if (mode == 0) {
+            const uchar4 a = lrow[x], b = rrow[x];
+            o = make_uchar4(a.x, b.y, b.z, 255);
+        } else {
+            const int half = W / 2;
+            const uchar4* row = x < half ? lrow : rrow;
+            const int c = (x < half ? x : x - half) * 2;
+            const uchar4 a = row[c], b = row[c + 1];
+            o = make_uchar4((unsigned char)((a.x + b.x + 1) >> 1), (unsigned char)((a.y + b.y + 1) >> 1),
+                            (unsigned char)((a.z + b.z + 1) >> 1), 255);
+        }
+        reinterpret_cast<uchar4*>(reinterpret_cast<char*>(out) + y * op)[x] = o;
+    }
+}
+
 // FFMA peak microbenchmark: 8 independent FMA chains per thread.
 __global__ void __launch_bounds__(256) k_ffma_peak(float* out, int iters, float a, float b) {
     float x0 = threadIdx.x, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3, x4 = x0 + 4, x5 = x0 + 5, x6 = x0 + 6, x7 = x0 + 7;
@@ -249,6 +275,13 @@ cudaError_t rtb_trace_occupancy(unsigned flags, int stack_entries, int* blocks_p
 
 cudaError_t rtb_launch_unpack(const void* gathered, const UnpackParams& U, cudaStream_t st) {
     k_unpack_shards<<<148 * 8, 256, 0, st>>>(gathered, U);
+    return cudaGetLastError();
+}
+
+cudaError_t rtb_launch_compose(const void* L, const void* R, long long lp, long long rp, int W, int H, int mode,
+                               void* out, long long op, cudaStream_t st) {
+    k_compose<<<148 * 4, 256, 0, st>>>(static_cast<const uchar4*>(L), static_cast<const uchar4*>(R), lp, rp, W, H, mode,
+                                       static_cast<uchar4*>(out), op);
     return cudaGetLastError();
 }
 

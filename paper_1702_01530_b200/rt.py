@@ -20,6 +20,7 @@ RT_OK, RT_ERR_INVALID_ARG, RT_ERR_CUDA, RT_ERR_OOM, RT_ERR_NO_SCENE, RT_ERR_NO_C
 RT_FORMAT_RGBA8, RT_FORMAT_RGBA16F = 0, 1
 RT_RENDER_COUNT, RT_RENDER_BRUTE_FORCE, RT_RENDER_PEER_STORE = 1, 2, 4
 RT_NUM_COUNTERS = 12
+RT_COMPOSE_ANAGLYPH, RT_COMPOSE_SBS = 0, 1
 RT_TILE = 16
 COUNTER_NAMES = ["primary", "reflection", "refraction", "shadow", "node_visits", "tri_tests", "sphere_tests",
                  "plane_tests", "shade_hits", "light_evals", "misses", "pixels"]
@@ -29,7 +30,7 @@ EXPORTED = ["rt_create", "rt_destroy", "rt_synchronize", "rt_last_error", "rt_ve
             "rt_set_stereo_camera", "rt_render_stereo", "rt_render_stereo_ex", "rt_download", "rt_wait", "rt_query",
             "rt_host_alloc", "rt_host_free", "rt_upload", "rt_shard_tiles", "rt_shard_bytes", "rt_unpack_shards_host",
             "rt_unpack_shards", "rt_ipc_get_handle", "rt_ipc_open", "rt_ipc_close", "rt_scene_info", "rt_bvh_export",
-            "rt_bench_ffma"]
+            "rt_bench_ffma", "rt_compose"]
 
 
 class RtError(RuntimeError):
@@ -103,6 +104,7 @@ def lib():
             "rt_scene_info": [vp, vp],
             "rt_bvh_export": [vp, vp, C.POINTER(u32), vp, C.POINTER(u32)],
             "rt_bench_ffma": [vp, u32, C.POINTER(C.c_double), C.POINTER(C.c_double)],
+            "rt_compose": [vp, rt_fb, rt_fb, u32, u32, u32, rt_fb],
         }
         for name, args in sig.items():
             fn = getattr(L, name)
@@ -299,6 +301,10 @@ def rt_bvh_export(ctx):
     gids = np.zeros(max(npr.value, 1), np.int32)
     _check(lib().rt_bvh_export(ctx, nodes.ctypes.data, C.byref(nn), gids.ctypes.data, C.byref(npr)))
     return nodes[:nn.value], gids[:npr.value]
+
+
+def rt_compose(ctx, left_fb, right_fb, width, height, mode, out_fb):
+    _check(lib().rt_compose(ctx, left_fb, right_fb, width, height, mode, out_fb))
 
 
 def rt_bench_ffma(ctx, iters=2048):

@@ -305,3 +305,21 @@ def test_bvh_structure(R):
     assert np.all(covered == 1)
     assert len(seen) == info["bvh_nodes"]
     assert depth_max == info["bvh_depth"] and depth_max < 40
+
+
+@pytest.mark.parametrize("W,H", [(93, 61), (1920, 1080)])
+def test_compose_anaglyph_sbs(R, W, H):
+    """NEXT-1 (PAPER.md:56 post-processing): GPU composition of the GPU stereo
+    pair == the oracle's composition of the same bytes (integer formulas, bit-exact)."""
+    from oracle.oracle import compose
+    s = scenes.scene_c2().with_view(width=W, height=H, max_depth=2)
+    g = gpu_render(R, s)
+    fb = torch.from_numpy(g["fb"]).cuda()
+    pitch = W * 4
+    for mode, name in ((rt.RT_COMPOSE_ANAGLYPH, "anaglyph"), (rt.RT_COMPOSE_SBS, "sbs")):
+        ow = W if name == "anaglyph" else 2 * (W // 2)
+        out = torch.zeros((H, ow, 4), dtype=torch.uint8, device="cuda")
+        rt.rt_compose(R.ctx, rt.rt_fb(fb[0].data_ptr(), 0, pitch), rt.rt_fb(fb[1].data_ptr(), 0, pitch), W, H, mode,
+                      rt.rt_fb(out.data_ptr(), 0, ow * 4))
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(out.cpu().numpy(), compose(g["fb"][0], g["fb"][1], name))

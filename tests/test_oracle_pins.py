@@ -555,3 +555,33 @@ def test_refraction_slab_snell_closed_form():
     s = mk_scene(spheres=[[0, 0, 0, 1]], mats=[material(0.0, 0.0, 1, kt=0.5, ior=1.0)], background=bg)
     rgb, _ = Oracle(s).trace_ray([0.1, 0.2, 5], [0, 0, -1], 2)
     np.testing.assert_allclose(rgb, 0.25 * bg, atol=1e-9)
+
+
+def test_compose_spec_examples(golden):
+    """SPEC.md:448-450 (compose_anaglyph) and S:458-460 (compose_sbs) worked examples and
+    properties: identical channels -> identity / identical halves; locality."""
+    from oracle.oracle import compose
+    for case in golden["anaglyph"]["cases"]:
+        L = np.array(case["L"] + [255], np.uint8).reshape(1, 1, 4)
+        R = np.array(case["R"] + [255], np.uint8).reshape(1, 1, 4)
+        np.testing.assert_array_equal(compose(L, R, "anaglyph")[0, 0, :3], case["out"])
+    a, b = golden["sbs"]["cols"]
+    L = np.array([[[a, a, a, 255], [b, b, b, 255]]], np.uint8)
+    out = compose(L, L, "sbs")
+    assert out.shape == (1, 2, 4) and np.all(out[0, :, :3] == golden["sbs"]["out"])
+    rng = np.random.default_rng(5)
+    X = rng.integers(0, 256, (5, 7, 4), dtype=np.uint8)
+    X[..., 3] = 255
+    np.testing.assert_array_equal(compose(X, X, "anaglyph"), X)
+    s = compose(X, X, "sbs")
+    assert s.shape == (5, 6, 4)
+    np.testing.assert_array_equal(s[:, :3], s[:, 3:])
+    # round half up on an odd pair sum; floor(W/2) columns (last column of odd W dropped)
+    Y = np.zeros((1, 3, 4), np.uint8)
+    Y[0, 0, :3], Y[0, 1, :3], Y[0, 2, :3] = 1, 2, 200
+    assert compose(Y, Y, "sbs")[0, 0, 0] == 2
+    # locality: one changed input pixel changes exactly one anaglyph pixel
+    Z = X.copy()
+    Z[2, 3, 0] ^= 0xFF
+    d = np.any(compose(Z, X, "anaglyph") != compose(X, X, "anaglyph"), -1)
+    assert d.sum() == 1 and d[2, 3]
