@@ -548,6 +548,7 @@ rt_status rt_render_stereo_ex(rt_context* c, const rt_render_params* p, const rt
     P.shard_fmt = (int)out->shard_format;
     P.counters = out->counters ? out->counters : c->scratch_counters;
     P.stack_entries = 3 * (int)c->info[5] + 2;       // <= 3 pending siblings per BVH4 level
+    if (P.stack_entries > rtb::STACK_CAP) return fail(RT_ERR_SIZE, "BVH too deep (%d levels)", (int)c->info[5]);
     P.n_tiles = (int)n_tiles;
     P.peer_fence = (p->flags & RT_RENDER_PEER_STORE) ? 1 : 0;
     if (P.n_work == 0) return RT_OK;

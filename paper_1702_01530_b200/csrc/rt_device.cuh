@@ -24,7 +24,7 @@ namespace rtb {
 constexpr float T_MIN = 1e-4f;     // SPEC.md:156 t_min
 constexpr float BIAS = 1e-4f;      // SPEC.md:156 shadow_bias (also reflection/refraction origins)
 constexpr int MAX_DEPTH = 16;
-constexpr int BVH_STACK = 64;      // LBVH depth <= 30 Morton bits + 32 index bits
+constexpr int STACK_CAP = 3 * 64 + 2;   // BVH4 traversal stack: 3 siblings per level, depth <= 64
 constexpr int LEAF_SHIFT = 24;     // leaf encoding: ~((count-1) << 24 | first)
 constexpr int TILE = 16;
 constexpr int WIDE_EMPTY = 0x7fffffff;   // unused BVH4 child slot

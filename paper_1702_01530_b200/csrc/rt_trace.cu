@@ -25,7 +25,7 @@ namespace rtb {
 // Radiance accumulates as sum over tree nodes of path_weight * local_term, which equals the
 // recursive definition c = local + kt*T(refr) + kr_eff*T(refl) (reading 17).
 template <bool COUNT, bool BRUTE>
-__device__ __forceinline__ float3 trace_pixel(const TraceParams& P, float3 o, float3 d, int& prim_id, int* stk,
+__device__ __forceinline__ float3 trace_pixel(const TraceParams& P, float3 o, float3 d, int& prim_id, TravStack& stk,
                                               Counters<COUNT>& cnt) {
     const DevScene& S = P.sc;
     float4 st_a[MAX_DEPTH], st_b[MAX_DEPTH];   // refraction children: (o, w) (d, depth)
@@ -129,7 +129,8 @@ __global__ void __launch_bounds__(RT_BLOCK, RT_MINB) k_trace_stereo(const TraceP
     Counters<COUNT> cnt;
     cnt.zero();
     const int lane = threadIdx.x & 31;
-    int* const stk = s_stack + threadIdx.x;
+    int lstack[STACK_CAP > RT_SMEM_STACK ? STACK_CAP - RT_SMEM_STACK : 1];
+    TravStack stk{s_stack + threadIdx.x, lstack};
     while (true) {
         int base = 0;
         if (lane == 0) base = atomicAdd(P.work_counter, 32);
@@ -253,7 +254,9 @@ static const void* trace_fn(unsigned flags) {
                  : (brute ? (const void*)k_trace_stereo<false, true> : (const void*)k_trace_stereo<false, false>);
 }
 
-size_t rtb_trace_smem(int stack_entries) { return (size_t)stack_entries * RT_BLOCK * sizeof(int); }
+size_t rtb_trace_smem(int stack_entries) {
+    return (size_t)(stack_entries < RT_SMEM_STACK ? stack_entries : RT_SMEM_STACK) * RT_BLOCK * sizeof(int);
+}
 
 
 cudaError_t rtb_launch_trace(const TraceParams& P, unsigned flags, int grid, cudaStream_t st) {

@@ -9,6 +9,22 @@ namespace rtb {
 #ifndef RT_BLOCK
 #define RT_BLOCK 256      // threads per trace CTA (stack stride)
 #endif
+#ifndef RT_SMEM_STACK
+#define RT_SMEM_STACK 16  // traversal-stack entries kept in shared memory; deeper ones in local
+#endif
+
+// Per-thread traversal stack: the first RT_SMEM_STACK entries live in shared memory laid out
+// [entry][thread] (conflict-free), deeper entries in thread-local memory (L1-cached).  Keeping the
+// shared part short leaves most of the 228 KB L1/shared array to cache BVH nodes.
+struct TravStack {
+    int* s;   // shared: s[i * RT_BLOCK]
+    int* l;   // local:  l[i - RT_SMEM_STACK]
+    __device__ __forceinline__ void set(int i, int v) {
+        if (i < RT_SMEM_STACK) s[i * RT_BLOCK] = v;
+        else l[i - RT_SMEM_STACK] = v;
+    }
+    __device__ __forceinline__ int get(int i) const { return i < RT_SMEM_STACK ? s[i * RT_BLOCK] : l[i - RT_SMEM_STACK]; }
+};
 
 template <bool COUNT>
 struct Counters {
@@ -123,7 +139,7 @@ __device__ __forceinline__ int pick4(const int4& c, uint32_t i) {
 // Visit order of the hit children: entry distances are >= 0, so their bit patterns order like
 // unsigned ints; the 2 low bits carry the child slot; a 5-exchange network sorts them.  The
 // nearest hit continues, the others are pushed far-to-near (predicated stores, no branches).
-__device__ __forceinline__ bool order_push(unsigned m, const float tn[4], const int4& ch, int* stk, int& sp, int& node) {
+__device__ __forceinline__ bool order_push(unsigned m, const float tn[4], const int4& ch, TravStack& stk, int& sp, int& node) {
     if (!m) return false;
     uint32_t k0 = (m & 1) ? ((__float_as_uint(tn[0]) & ~3u) | 0u) : 0xffffffffu;
     uint32_t k1 = (m & 2) ? ((__float_as_uint(tn[1]) & ~3u) | 1u) : 0xffffffffu;
@@ -131,9 +147,9 @@ __device__ __forceinline__ bool order_push(unsigned m, const float tn[4], const 
     uint32_t k3 = (m & 8) ? ((__float_as_uint(tn[3]) & ~3u) | 3u) : 0xffffffffu;
     cswap(k0, k1); cswap(k2, k3); cswap(k0, k2); cswap(k1, k3); cswap(k1, k2);
     const int nh = __popc(m);
-    if (nh > 3) stk[(sp + nh - 4) * RT_BLOCK] = pick4(ch, k3 & 3u);
-    if (nh > 2) stk[(sp + nh - 3) * RT_BLOCK] = pick4(ch, k2 & 3u);
-    if (nh > 1) stk[(sp + nh - 2) * RT_BLOCK] = pick4(ch, k1 & 3u);
+    if (nh > 3) stk.set(sp + nh - 4, pick4(ch, k3 & 3u));
+    if (nh > 2) stk.set(sp + nh - 3, pick4(ch, k2 & 3u));
+    if (nh > 1) stk.set(sp + nh - 2, pick4(ch, k1 & 3u));
     sp += nh - 1;
     node = pick4(ch, k0 & 3u);
     return true;
@@ -146,7 +162,7 @@ __device__ __forceinline__ bool order_push(unsigned m, const float tn[4], const 
 // unsigned ints) carry the child slot in their 2 low bits and go through a 5-exchange sorting
 // network; the 3 farther hits are pushed on the shared-memory stack.
 template <bool COUNT, bool BRUTE>
-__device__ __forceinline__ Hit closest_hit(const DevScene& S, float3 o, float3 d, int* stk, Counters<COUNT>& cnt) {
+__device__ __forceinline__ Hit closest_hit(const DevScene& S, float3 o, float3 d, TravStack& stk, Counters<COUNT>& cnt) {
     Hit h;
     h.t = __int_as_float(0x7f800000);
     h.gid = -1;
@@ -190,13 +206,13 @@ __device__ __forceinline__ Hit closest_hit(const DevScene& S, float3 o, float3 d
         }
         if (sp == 0) return h;
         --sp;
-        node = stk[sp * RT_BLOCK];
+        node = stk.get(sp);
     }
 }
 
 // Any hit with t_min < t < dist (binary visibility, reading 4); children near-to-far.
 template <bool COUNT, bool BRUTE>
-__device__ __forceinline__ bool occluded(const DevScene& S, float3 o, float3 d, float dist, int* stk, Counters<COUNT>& cnt) {
+__device__ __forceinline__ bool occluded(const DevScene& S, float3 o, float3 d, float dist, TravStack& stk, Counters<COUNT>& cnt) {
     for (int i = 0; i < S.n_planes; ++i) {
         cnt.add(CNT_PLANE_TESTS);
         float t;
@@ -229,7 +245,7 @@ __device__ __forceinline__ bool occluded(const DevScene& S, float3 o, float3 d, 
         }
         if (sp == 0) return false;
         --sp;
-        node = stk[sp * RT_BLOCK];
+        node = stk.get(sp);
     }
 }
 
