@@ -157,6 +157,14 @@ rt_status rt_scene_upload(rt_context* ctx, const rt_primitives* prims,
                           const rt_material* mats, uint32_t n_mats,
                           const rt_light* lights, uint32_t n_lights, const rt_env* env);
 
+/* NEXT-3 (PAPER.md:125 ref [12] dynamic meshes): move the triangle vertices of
+ * the uploaded scene (HOST array of 3*n_vertices floats, same count and connectivity as the
+ * upload) and refit the device BVH bottom-up on the device (same topology and leaf order, new
+ * boxes) instead of rebuilding it.  Validation as at upload (finite values, no degenerate
+ * triangle).  Blocks until the refit is done (host array may be freed on return).
+ * Errors: RT_ERR_NO_SCENE, RT_ERR_INVALID_ARG (count mismatch, validation), RT_ERR_CUDA. */
+rt_status rt_scene_update_vertices(rt_context* ctx, const float* vertices, uint32_t n_vertices);
+
 /* PAPER.md:33 (§2: "two projections ... from two cameras, corresponding to eyes of the
  * observer") with SPEC.md:422-430 derive_eyes: `eye` is the cyclopean midpoint, the eyes
  * sit at eye -/+ (interocular/2) * r^, r^ = normalize(f^ x up).  vfov is vertical, in

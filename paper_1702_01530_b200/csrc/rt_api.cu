@@ -80,6 +80,15 @@ struct rt_context {
     double cam_eye[2][3], cam_f[3], cam_r[3], cam_u[3], cam_th, cam_sigma_unit;
     float vfov = 0;
     int leaf_max = 1;                // LBVH leaf collapse threshold (env RT_LEAF_MAX, <= 16)
+    // refit state (rt_scene_update_vertices)
+    int* d_prim_orig = nullptr;
+    float* d_vertices = nullptr;
+    uint32_t* d_tri = nullptr;
+    float4* d_spheres = nullptr;
+    uint32_t n_vertices = 0;
+    std::vector<int> level_start;
+    std::vector<uint32_t> h_tri;
+    double sphere_bound = 0.0;
 };
 
 namespace {
@@ -333,12 +342,15 @@ rt_status rt_scene_upload(rt_context* c, const rt_primitives* P, const rt_materi
     float4* d_prims = nullptr;
     float4* d_nodes = nullptr;
     const size_t Nn = N > 1 ? N - 1 : 0;
-    if ((st = dalloc(c, 3 * (size_t)N, &d_prims))) {
+    int* d_prim_orig = nullptr;
+    if ((st = dalloc(c, 3 * (size_t)N, &d_prims)) || (st = dalloc(c, (size_t)N, &d_prim_orig))) {
         free_scene(c);
         return st;
     }
     B.prims = d_prims;
     int root = ~0, n_nodes4 = 0, depth4 = 0;
+    B.prim_orig = d_prim_orig;
+    std::vector<int> level_start(66, 0);
     if (N > 0) {
         if ((st = salloc(48 * (size_t)N, (void**)&B.prims_unsorted)) || (st = salloc(16 * (size_t)N, (void**)&B.aabb_lo)) ||
             (st = salloc(16 * (size_t)N, (void**)&B.aabb_hi)) || (st = salloc(16 * (size_t)N, (void**)&B.centroid)) ||
@@ -358,7 +370,7 @@ rt_status rt_scene_upload(rt_context* c, const rt_primitives* P, const rt_materi
             return st;
         }
         B.leaf_max = c->leaf_max;
-        cudaError_t e = rtb_build_bvh(B, c->stream, &root, &n_nodes4, &depth4);
+        cudaError_t e = rtb_build_bvh(B, c->stream, &root, &n_nodes4, &depth4, level_start.data());
         if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
         if (e == cudaSuccess && n_nodes4 > 0) {        // compact the BVH4 into an exact-size buffer
             if ((st = dalloc(c, 7 * (size_t)n_nodes4, &d_nodes))) {
@@ -402,6 +414,45 @@ rt_status rt_scene_upload(rt_context* c, const rt_primitives* P, const rt_materi
     c->info[6] = bytes;
     c->info[7] = (uint64_t)std::chrono::duration_cast<std::chrono::microseconds>(t1 - t0).count();
     c->has_scene = true;
+    return RT_OK;
+}
+
+// ------------------------------------------------------------------------------ refit (NEXT-3)
+rt_status rt_scene_update_vertices(rt_context* c, const float* vertices, uint32_t n_vertices) {
+    if (!c || (!vertices && n_vertices)) return fail(RT_ERR_INVALID_ARG, "rt_scene_update_vertices: NULL argument");
+    if (!c->has_scene) return fail(RT_ERR_NO_SCENE, "rt_scene_update_vertices: no scene");
+    if (n_vertices != c->n_vertices)
+        return fail(RT_ERR_INVALID_ARG, "rt_scene_update_vertices: %u vertices, scene has %u", n_vertices, c->n_vertices);
+    if (n_vertices == 0) return RT_OK;
+    double bound = c->sphere_bound;
+    for (uint32_t i = 0; i < n_vertices; ++i) {
+        const float* v = vertices + 3 * i;
+        if (!finite3(v)) return fail(RT_ERR_INVALID_ARG, "vertex %u: non-finite value", i);
+        bound = std::max(bound, std::fabs((double)v[0]) + std::fabs((double)v[1]) + std::fabs((double)v[2]));
+    }
+    const size_t T = c->h_tri.size() / 3;
+    for (size_t j = 0; j < T; ++j) {                    // SPEC.md:111 degenerate faces stay rejected
+        const uint32_t* t = c->h_tri.data() + 3 * j;
+        double lo[3], hi[3], e1[3], e2[3];
+        for (int k = 0; k < 3; ++k) {
+            const double a = vertices[3 * t[0] + k], b = vertices[3 * t[1] + k], cc = vertices[3 * t[2] + k];
+            lo[k] = std::min(a, std::min(b, cc));
+            hi[k] = std::max(a, std::max(b, cc));
+            e1[k] = b - a;
+            e2[k] = cc - a;
+        }
+        const double cx = e1[1] * e2[2] - e1[2] * e2[1], cy = e1[2] * e2[0] - e1[0] * e2[2], cz = e1[0] * e2[1] - e1[1] * e2[0];
+        const double area = 0.5 * std::sqrt(cx * cx + cy * cy + cz * cz);
+        const double diag2 = (hi[0] - lo[0]) * (hi[0] - lo[0]) + (hi[1] - lo[1]) * (hi[1] - lo[1]) + (hi[2] - lo[2]) * (hi[2] - lo[2]);
+        if (!(area > 1e-12 * diag2)) return fail(RT_ERR_INVALID_ARG, "triangle %zu: degenerate after update", j);
+    }
+    CUDA_TRY(cudaSetDevice(c->device));
+    CUDA_TRY(cudaMemcpyAsync(c->d_vertices, vertices, 12 * (size_t)n_vertices, cudaMemcpyHostToDevice, c->stream));
+    CUDA_TRY(rtb_refit_bvh(const_cast<float4*>(c->sc.prims), const_cast<float4*>(c->sc.nodes), c->d_prim_orig,
+                           c->sc.n_bvh, c->sc.n_spheres, c->d_spheres, c->d_tri, c->d_vertices, c->level_start.data(),
+                           (int)c->level_start.size() - 1, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));       // host vertices may be freed on return
+    c->sc.bound = (float)(bound * (1.0 + 1e-6));
     return RT_OK;
 }
 

@@ -378,6 +378,86 @@ __global__ void k_gather_prims(BuildBuffers B, int n, const uint32_t* __restrict
     }
 }
 
+// ---------------------------------------------------------------- refit (NEXT-3: moving vertices)
+// New vertex positions -> leaf-order triangle records (v0, e1, e2); topology and leaf order kept.
+__global__ void k_update_prims(float4* prims, const int* __restrict__ prim_orig, int n, int n_spheres,
+                               const uint32_t* __restrict__ tri_idx, const float* __restrict__ vtx) {
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+        const int o = prim_orig[k];
+        if (o < n_spheres) continue;
+        const int j = o - n_spheres;
+        const uint32_t a = tri_idx[3 * j], b = tri_idx[3 * j + 1], c = tri_idx[3 * j + 2];
+        const float3 v0 = f3(vtx[3 * a], vtx[3 * a + 1], vtx[3 * a + 2]);
+        const float3 v1 = f3(vtx[3 * b], vtx[3 * b + 1], vtx[3 * b + 2]);
+        const float3 v2 = f3(vtx[3 * c], vtx[3 * c + 1], vtx[3 * c + 2]);
+        const float4 r0 = prims[3 * k], r1 = prims[3 * k + 1];
+        prims[3 * k] = make_float4(v0.x, v0.y, v0.z, r0.w);
+        prims[3 * k + 1] = make_float4(v1.x - v0.x, v1.y - v0.y, v1.z - v0.z, r1.w);
+        prims[3 * k + 2] = make_float4(v2.x - v0.x, v2.y - v0.y, v2.z - v0.z, 0.f);
+    }
+}
+
+__device__ __forceinline__ void prim_box(int k, const int* __restrict__ prim_orig, int n_spheres,
+                                         const float4* __restrict__ spheres, const uint32_t* __restrict__ tri_idx,
+                                         const float* __restrict__ vtx, float3& lo, float3& hi) {
+    const int o = prim_orig[k];
+    if (o < n_spheres) {
+        const float4 s = spheres[o];
+        lo = f3(__fsub_rd(s.x, s.w), __fsub_rd(s.y, s.w), __fsub_rd(s.z, s.w));
+        hi = f3(__fadd_ru(s.x, s.w), __fadd_ru(s.y, s.w), __fadd_ru(s.z, s.w));
+        return;
+    }
+    const int j = o - n_spheres;
+    const uint32_t a = tri_idx[3 * j], b = tri_idx[3 * j + 1], c = tri_idx[3 * j + 2];
+    lo = f3(fminf(vtx[3 * a], fminf(vtx[3 * b], vtx[3 * c])), fminf(vtx[3 * a + 1], fminf(vtx[3 * b + 1], vtx[3 * c + 1])),
+            fminf(vtx[3 * a + 2], fminf(vtx[3 * b + 2], vtx[3 * c + 2])));
+    hi = f3(fmaxf(vtx[3 * a], fmaxf(vtx[3 * b], vtx[3 * c])), fmaxf(vtx[3 * a + 1], fmaxf(vtx[3 * b + 1], vtx[3 * c + 1])),
+            fmaxf(vtx[3 * a + 2], fmaxf(vtx[3 * b + 2], vtx[3 * c + 2])));
+}
+
+// Bottom-up refit of one BVH4 level (nodes [begin, end)); deeper levels are already refit, and
+// empty slots keep their inverted boxes, which are neutral under min/max.
+__global__ void k_refit4(float4* nodes, int begin, int end, const int* __restrict__ prim_orig, int n_spheres,
+                         const float4* __restrict__ spheres, const uint32_t* __restrict__ tri_idx,
+                         const float* __restrict__ vtx) {
+    for (int i = begin + blockIdx.x * blockDim.x + threadIdx.x; i < end; i += gridDim.x * blockDim.x) {
+        float4* q = nodes + 7 * (size_t)i;
+        const int4 ch = *reinterpret_cast<const int4*>(q + 6);
+        float lo[3][4], hi[3][4];
+        const int codes[4] = {ch.x, ch.y, ch.z, ch.w};
+        for (int c = 0; c < 4; ++c) {
+            float3 l = f3(1e30f, 1e30f, 1e30f), h = f3(-1e30f, -1e30f, -1e30f);
+            const int code = codes[c];
+            if (code == WIDE_EMPTY) {
+            } else if (code < 0) {
+                const int enc = ~code;
+                const int first = enc & ((1 << LEAF_SHIFT) - 1), last = first + (enc >> LEAF_SHIFT);
+                for (int k = first; k <= last; ++k) {
+                    float3 pl, ph;
+                    prim_box(k, prim_orig, n_spheres, spheres, tri_idx, vtx, pl, ph);
+                    l = f3(fminf(l.x, pl.x), fminf(l.y, pl.y), fminf(l.z, pl.z));
+                    h = f3(fmaxf(h.x, ph.x), fmaxf(h.y, ph.y), fmaxf(h.z, ph.z));
+                }
+            } else {
+                const float4* r = nodes + 7 * (size_t)code;
+                const float4 lx = r[0], hx = r[1], ly = r[2], hy = r[3], lz = r[4], hz = r[5];
+                l = f3(fminf(fminf(lx.x, lx.y), fminf(lx.z, lx.w)), fminf(fminf(ly.x, ly.y), fminf(ly.z, ly.w)),
+                       fminf(fminf(lz.x, lz.y), fminf(lz.z, lz.w)));
+                h = f3(fmaxf(fmaxf(hx.x, hx.y), fmaxf(hx.z, hx.w)), fmaxf(fmaxf(hy.x, hy.y), fmaxf(hy.z, hy.w)),
+                       fmaxf(fmaxf(hz.x, hz.y), fmaxf(hz.z, hz.w)));
+            }
+            lo[0][c] = l.x; lo[1][c] = l.y; lo[2][c] = l.z;
+            hi[0][c] = h.x; hi[1][c] = h.y; hi[2][c] = h.z;
+        }
+        q[0] = make_float4(lo[0][0], lo[0][1], lo[0][2], lo[0][3]);
+        q[1] = make_float4(hi[0][0], hi[0][1], hi[0][2], hi[0][3]);
+        q[2] = make_float4(lo[1][0], lo[1][1], lo[1][2], lo[1][3]);
+        q[3] = make_float4(hi[1][0], hi[1][1], hi[1][2], hi[1][3]);
+        q[4] = make_float4(lo[2][0], lo[2][1], lo[2][2], lo[2][3]);
+        q[5] = make_float4(hi[2][0], hi[2][1], hi[2][2], hi[2][3]);
+    }
+}
+
 }  // namespace rtb
 
 using namespace rtb;
@@ -389,13 +469,15 @@ static int grid_for(int n, int block = 256) {
     return g < 1 ? 1 : (g > 148 * 16 ? 148 * 16 : g);
 }
 
-cudaError_t rtb_build_bvh(const BuildBuffers& Bc, cudaStream_t st, int* root, int* n_nodes4, int* depth4) {
+cudaError_t rtb_build_bvh(const BuildBuffers& Bc, cudaStream_t st, int* root, int* n_nodes4, int* depth4,
+                          int* level_start) {
     BuildBuffers B = Bc;
     const int n = B.n_spheres + B.n_tris;
     if (n == 0) return cudaSuccess;
     k_prim_setup<<<grid_for(n), 256, 0, st>>>(B);
     if (n == 1) {
         cudaMemcpyAsync(B.prims, B.prims_unsorted, 3 * sizeof(float4), cudaMemcpyDeviceToDevice, st);
+        cudaMemsetAsync(B.prim_orig, 0, sizeof(int), st);
         *root = ~0;
         *n_nodes4 = 0;
         *depth4 = 0;
@@ -416,6 +498,7 @@ cudaError_t rtb_build_bvh(const BuildBuffers& Bc, cudaStream_t st, int* root, in
     float4* slo = B.leaf_lo;
     float4* shi = B.leaf_hi;
     k_gather_prims<<<grid_for(n), 256, 0, st>>>(B, n, B.vals[cur], slo, shi);
+    cudaMemcpyAsync(B.prim_orig, B.vals[cur], sizeof(int) * n, cudaMemcpyDeviceToDevice, st);
     k_karras<<<grid_for(n - 1), 256, 0, st>>>(B.keys[cur], n, B.left, B.right, B.parent_int, B.parent_leaf, B.range);
     cudaMemsetAsync(B.flags, 0, sizeof(int) * (n - 1), st);
     k_refit<<<grid_for(n), 256, 0, st>>>(B, n, slo, shi);
@@ -428,6 +511,7 @@ cudaError_t rtb_build_bvh(const BuildBuffers& Bc, cudaStream_t st, int* root, in
     }
     int2 first = make_int2(0, 0);
     int h_counters[2] = {0, 1};
+    if (level_start) { level_start[0] = 0; level_start[1] = 1; }
     cudaMemcpyAsync(B.frontier[0], &first, sizeof(int2), cudaMemcpyHostToDevice, st);
     int n_in = 1, levels = 0, cur_f = 0;
     while (n_in > 0) {
@@ -441,9 +525,22 @@ cudaError_t rtb_build_bvh(const BuildBuffers& Bc, cudaStream_t st, int* root, in
         n_in = h_counters[0];
         cur_f ^= 1;
         ++levels;
+        if (level_start && levels + 1 <= 65) level_start[levels + 1] = h_counters[1];
     }
     *root = 0;
     *n_nodes4 = h_counters[1];
     *depth4 = levels;
+    return cudaGetLastError();
+}
+
+cudaError_t rtb_refit_bvh(float4* prims, float4* nodes4, const int* prim_orig, int n, int n_spheres,
+                          const float4* spheres, const uint32_t* tri_idx, const float* vtx,
+                          const int* level_start, int levels, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    k_update_prims<<<grid_for(n), 256, 0, st>>>(prims, prim_orig, n, n_spheres, tri_idx, vtx);
+    for (int L = levels - 1; L >= 0; --L) {
+        const int b = level_start[L], e = level_start[L + 1];
+        if (e > b) k_refit4<<<grid_for(e - b), 256, 0, st>>>(nodes4, b, e, prim_orig, n_spheres, spheres, tri_idx, vtx);
+    }
     return cudaGetLastError();
 }

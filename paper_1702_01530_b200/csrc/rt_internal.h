@@ -83,6 +83,7 @@ struct BuildBuffers {
     int2* frontier[2];          // [N] collapse work lists (bvh2 node, bvh4 slot)
     int* wide_counters;         // [2] next-frontier size, next BVH4 slot
     int2* range;                // [N-1] sorted primitive range of each internal node
+    int* prim_orig;             // out: leaf slot -> original primitive index (kept for refit)
     int leaf_max;               // collapse subtrees of <= leaf_max primitives into leaves
 };
 
@@ -96,4 +97,8 @@ cudaError_t rtb_launch_compose(const void* L, const void* R, long long lp, long 
                                void* out, long long op, cudaStream_t st);
 // launchers (rt_build.cu)
 size_t rtb_sort_hist_entries(int n);
-cudaError_t rtb_build_bvh(const BuildBuffers& B, cudaStream_t st, int* root, int* n_nodes4, int* depth4);
+cudaError_t rtb_build_bvh(const BuildBuffers& B, cudaStream_t st, int* root, int* n_nodes4, int* depth4,
+                          int* level_start /* [66] BVH4 node index where each level starts */);
+cudaError_t rtb_refit_bvh(float4* prims, float4* nodes4, const int* prim_orig, int n, int n_spheres,
+                          const float4* spheres, const uint32_t* tri_idx, const float* vtx,
+                          const int* level_start, int levels, cudaStream_t st);

@@ -30,7 +30,7 @@ EXPORTED = ["rt_create", "rt_destroy", "rt_synchronize", "rt_last_error", "rt_ve
             "rt_set_stereo_camera", "rt_render_stereo", "rt_render_stereo_ex", "rt_download", "rt_wait", "rt_query",
             "rt_host_alloc", "rt_host_free", "rt_upload", "rt_shard_tiles", "rt_shard_bytes", "rt_unpack_shards_host",
             "rt_unpack_shards", "rt_ipc_get_handle", "rt_ipc_open", "rt_ipc_close", "rt_scene_info", "rt_bvh_export",
-            "rt_bench_ffma", "rt_compose"]
+            "rt_bench_ffma", "rt_compose", "rt_scene_update_vertices"]
 
 
 class RtError(RuntimeError):
@@ -105,6 +105,7 @@ def lib():
             "rt_bvh_export": [vp, vp, C.POINTER(u32), vp, C.POINTER(u32)],
             "rt_bench_ffma": [vp, u32, C.POINTER(C.c_double), C.POINTER(C.c_double)],
             "rt_compose": [vp, rt_fb, rt_fb, u32, u32, u32, rt_fb],
+            "rt_scene_update_vertices": [vp, vp, u32],
         }
         for name, args in sig.items():
             fn = getattr(L, name)
@@ -186,6 +187,11 @@ def rt_scene_upload(ctx, scene):
     a = SceneArrays(scene)
     _check(lib().rt_scene_upload(ctx, C.byref(a.prims), C.cast(a.mats, C.c_void_p), a.n_mats,
                                  C.cast(a.lights, C.c_void_p), a.n_lights, C.byref(a.env)))
+
+
+def rt_scene_update_vertices(ctx, vertices):
+    v = np.ascontiguousarray(np.asarray(vertices, np.float64).reshape(-1, 3), dtype=np.float32)
+    _check(lib().rt_scene_update_vertices(ctx, v.ctypes.data, len(v)))
 
 
 def rt_set_stereo_camera(ctx, eye, look_at, up, vfov_deg, interocular, convergence):
