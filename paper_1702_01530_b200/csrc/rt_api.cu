@@ -413,6 +413,23 @@ rt_status rt_scene_upload(rt_context* c, const rt_primitives* P, const rt_materi
     c->info[5] = (uint64_t)depth4;
     c->info[6] = bytes;
     c->info[7] = (uint64_t)std::chrono::duration_cast<std::chrono::microseconds>(t1 - t0).count();
+    // kept for rt_scene_update_vertices (NEXT-3 refit)
+    c->d_prim_orig = d_prim_orig;
+    c->d_vertices = d_vertices;
+    c->d_tri = d_tri;
+    c->d_spheres = d_spheres;
+    c->n_vertices = T ? V : 0;
+    c->level_start.assign(level_start.begin(), level_start.begin() + std::min(66, depth4 + 1));
+    c->sphere_bound = 0.0;
+    for (uint32_t i = 0; i < S; ++i) {
+        const float* sp = P->spheres + 4 * i;
+        c->sphere_bound = std::max(c->sphere_bound, std::fabs((double)sp[0]) + std::fabs((double)sp[1]) +
+                                                        std::fabs((double)sp[2]) + 3.0 * sp[3]);
+    }
+    if (T) c->h_tri.assign(P->tri_indices, P->tri_indices + 3 * (size_t)T);
+    else c->h_tri.clear();
+    c->has_refraction = false;
+    for (uint32_t i = 0; i < n_mats; ++i) c->has_refraction |= mats[i].kt > 0.0f;
     c->has_scene = true;
     return RT_OK;
 }
