@@ -428,8 +428,6 @@ rt_status rt_scene_upload(rt_context* c, const rt_primitives* P, const rt_materi
     }
     if (T) c->h_tri.assign(P->tri_indices, P->tri_indices + 3 * (size_t)T);
     else c->h_tri.clear();
-    c->has_refraction = false;
-    for (uint32_t i = 0; i < n_mats; ++i) c->has_refraction |= mats[i].kt > 0.0f;
     c->has_scene = true;
     return RT_OK;
 }
