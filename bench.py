@@ -370,6 +370,24 @@ def run_e2e(args, R, scene, rank, world, frame, fb, dev, rays_total):
         import torch.distributed as dist
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     dt = float(tt[0])
+    # paper-structure stage split (PAPER.md:15, :106-107 -- ~60 % compute / up to 40 % transfer on
+    # the paper's GPU): serialised render vs download times of one frame on this box
+    stages = None
+    if rank == 0 and world == 1:
+        rt.rt_synchronize(R.ctx)
+        t0 = time.perf_counter()
+        for _ in range(5):
+            rt.rt_wait(rt.rt_download(R.ctx, fb.data_ptr(), hosts[0], nbytes))
+        d_ms = (time.perf_counter() - t0) / 5 * 1e3
+        t0 = time.perf_counter()
+        for _ in range(5):
+            rt.rt_render_stereo(R.ctx, W, H, D, rt.rt_fb(fb[0].data_ptr(), 0, W * 4), rt.rt_fb(fb[1].data_ptr(), 0, W * 4))
+            rt.rt_synchronize(R.ctx)
+        r_ms = (time.perf_counter() - t0) / 5 * 1e3
+        stages = {"render_ms": r_ms, "download_ms": d_ms, "compute_fraction_serialised": r_ms / (r_ms + d_ms),
+                  "transfer_fraction_serialised": d_ms / (r_ms + d_ms),
+                  "transfer_hidden_by_overlap": True,
+                  "paper": "~60 % compute / up to 40 % CPU<->GPU transfer (PAPER.md:15, :106-107), unnamed NVIDIA GPU"}
     ok = True
     if rank == 0:
         slot = (args.steps - 1) % 2
@@ -381,6 +399,7 @@ def run_e2e(args, R, scene, rank, world, frame, fb, dev, rays_total):
     return {"value": rays_total / (dt / args.steps) / 1e6, "unit": UNIT,
             "h2d_bytes_per_step": 76, "d2h_bytes_per_step": nbytes if rank == 0 else 0,
             "ms_per_step": dt / args.steps * 1e3, "stereo_fps": args.steps / dt, "download_verified": ok,
+            "stages": stages,
             "note": "per step: camera set from host values (the 76-byte camera block travels in the kernel "
                     "launch parameters), render, pinned async D2H (rt_download, copy stream) of the RGBA8 stereo "
                     "frame overlapped with the next render; host wall clock around K steps incl. the last download"}
