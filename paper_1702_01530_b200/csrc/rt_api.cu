@@ -80,6 +80,7 @@ struct rt_context {
     double cam_eye[2][3], cam_f[3], cam_r[3], cam_u[3], cam_th, cam_sigma_unit;
     float vfov = 0;
     int leaf_max = 1;                // LBVH leaf collapse threshold (env RT_LEAF_MAX, <= 16)
+    int treelet_passes = 3;          // SAH treelet restructuring passes (env RT_TREELETS)
     // refit state (rt_scene_update_vertices)
     int* d_prim_orig = nullptr;
     float* d_vertices = nullptr;
@@ -133,6 +134,7 @@ rt_status rt_create(int device, void* cuda_stream, rt_context** out) {
     if (!c) return fail(RT_ERR_OOM, "rt_create: host allocation");
     c->device = device;
     if (const char* lm = getenv("RT_LEAF_MAX")) c->leaf_max = std::max(1, std::min(16, atoi(lm)));
+    if (const char* tp = getenv("RT_TREELETS")) c->treelet_passes = std::max(0, std::min(8, atoi(tp)));
     cudaError_t e = cudaSetDevice(device);
     if (e == cudaSuccess && cuda_stream) {
         c->stream = static_cast<cudaStream_t>(cuda_stream);
@@ -364,12 +366,14 @@ rt_status rt_scene_upload(rt_context* c, const rt_primitives* P, const rt_materi
             (st = salloc(16 * Nn, (void**)&B.node_lo)) || (st = salloc(16 * Nn, (void**)&B.node_hi)) ||
             (st = salloc(8 * Nn, (void**)&B.range)) || (st = salloc(112 * Nn, (void**)&B.nodes4)) ||
             (st = salloc(8 * (size_t)N, (void**)&B.frontier[0])) || (st = salloc(8 * (size_t)N, (void**)&B.frontier[1])) ||
-            (st = salloc(16, (void**)&B.wide_counters))) {
+            (st = salloc(16, (void**)&B.wide_counters)) || (st = salloc(4 * Nn, (void**)&B.cost)) ||
+            (st = salloc(4 * Nn, (void**)&B.count))) {
             free_scratch();
             free_scene(c);
             return st;
         }
         B.leaf_max = c->leaf_max;
+        B.treelet_passes = c->treelet_passes;
         cudaError_t e = rtb_build_bvh(B, c->stream, &root, &n_nodes4, &depth4, level_start.data());
         if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
         if (e == cudaSuccess && n_nodes4 > 0) {        // compact the BVH4 into an exact-size buffer

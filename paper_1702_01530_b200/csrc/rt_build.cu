@@ -11,6 +11,7 @@
 //                    from common-prefix lengths (__clzll)
 //   k_refit          bottom-up AABB union with atomic arrival counters
 //   k_gather_prims   primitive records in leaf order
+//   k_treelets       SAH treelet restructuring of the BVH2 (Karras & Aila 2013), optional passes
 //   k_wide           BVH2 -> 4-wide BVH collapse (level by level), small subtrees -> leaves
 // The result is a deterministic function of the input arrays.
 #include <cfloat>
@@ -279,6 +280,172 @@ __global__ void k_refit(BuildBuffers B, int n, const float4* __restrict__ slo, c
     }
 }
 
+// ---------------------------------------------------------------- treelet restructuring
+// Karras & Aila 2013 (TRBVH), one thread per treelet: bottom-up (atomic arrival counters as
+// in k_refit); at every internal node with >= 7 primitives the treelet of 7 leaves is formed by
+// repeatedly opening the largest-area treelet leaf, the SAH-optimal binary topology over the 7
+// leaves is found by dynamic programming over all 127 subsets, and the treelet's 6 internal
+// nodes are rewired when that lowers the SAH cost.  Leaf order (Morton) and the root index are
+// unchanged; only parent/child links, boxes, costs and counts of treelet nodes change.
+constexpr float SAH_CI = 1.2f;   // internal-node (box test) cost
+constexpr float SAH_CT = 1.0f;   // primitive test cost
+
+__device__ __forceinline__ float area3(float3 lo, float3 hi) {
+    const float x = hi.x - lo.x, y = hi.y - lo.y, z = hi.z - lo.z;
+    return x * y + y * z + z * x;
+}
+
+struct TNode {
+    float3 lo, hi;
+    float cost;
+    int count;
+};
+
+__device__ __forceinline__ TNode tnode(const BuildBuffers& B, int code) {
+    TNode t;
+    if (code < 0) {
+        const float4 a = B.leaf_lo[~code], b = B.leaf_hi[~code];
+        t.lo = f3(a.x, a.y, a.z);
+        t.hi = f3(b.x, b.y, b.z);
+        t.cost = SAH_CT * area3(t.lo, t.hi);
+        t.count = 1;
+    } else {
+        const float4 a = __ldcg(&B.node_lo[code]), b = __ldcg(&B.node_hi[code]);
+        t.lo = f3(a.x, a.y, a.z);
+        t.hi = f3(b.x, b.y, b.z);
+        t.cost = __ldcg(&B.cost[code]);
+        t.count = __ldcg(&B.count[code]);
+    }
+    return t;
+}
+
+__device__ __forceinline__ void set_parent(const BuildBuffers& B, int child, int parent) {
+    if (child < 0) __stcg(&B.parent_leaf[~child], parent);
+    else __stcg(&B.parent_int[child], parent);
+}
+
+__device__ void treelet_node(const BuildBuffers& B, int p) {
+    const int l = __ldcg(&B.left[p]), r = __ldcg(&B.right[p]);
+    const TNode tl = tnode(B, l), tr = tnode(B, r);
+    const int cnt = tl.count + tr.count;
+    const float3 plo = f3(fminf(tl.lo.x, tr.lo.x), fminf(tl.lo.y, tr.lo.y), fminf(tl.lo.z, tr.lo.z));
+    const float3 phi = f3(fmaxf(tl.hi.x, tr.hi.x), fmaxf(tl.hi.y, tr.hi.y), fmaxf(tl.hi.z, tr.hi.z));
+    const float pcost = SAH_CI * area3(plo, phi) + tl.cost + tr.cost;
+    bool done = false;
+    if (cnt >= 7) {
+        int leaves[7], inner[6];
+        TNode lt[7];
+        int nl = 2, ni = 1;
+        inner[0] = p;
+        leaves[0] = l; lt[0] = tl;
+        leaves[1] = r; lt[1] = tr;
+        while (nl < 7) {
+            int best = -1;
+            float ba = -1.0f;
+            for (int i = 0; i < nl; ++i)
+                if (leaves[i] >= 0) {
+                    const float a = area3(lt[i].lo, lt[i].hi);
+                    if (a > ba) { ba = a; best = i; }
+                }
+            if (best < 0) break;
+            const int c = leaves[best];
+            inner[ni++] = c;
+            const int cl = __ldcg(&B.left[c]), cr = __ldcg(&B.right[c]);
+            leaves[best] = cl; lt[best] = tnode(B, cl);
+            leaves[nl] = cr; lt[nl] = tnode(B, cr);
+            ++nl;
+        }
+        if (nl == 7) {
+            float sa[128], copt[128];
+            unsigned char part[128];
+            for (int s = 1; s < 128; ++s) {
+                float3 lo = f3(3.4e38f, 3.4e38f, 3.4e38f), hi = f3(-3.4e38f, -3.4e38f, -3.4e38f);
+                for (int i = 0; i < 7; ++i)
+                    if (s & (1 << i)) {
+                        lo = f3(fminf(lo.x, lt[i].lo.x), fminf(lo.y, lt[i].lo.y), fminf(lo.z, lt[i].lo.z));
+                        hi = f3(fmaxf(hi.x, lt[i].hi.x), fmaxf(hi.y, lt[i].hi.y), fmaxf(hi.z, lt[i].hi.z));
+                    }
+                sa[s] = area3(lo, hi);
+            }
+            for (int s = 1; s < 128; ++s) {
+                if (__popc(s) == 1) {
+                    copt[s] = lt[__ffs(s) - 1].cost;
+                    part[s] = 0;
+                    continue;
+                }
+                const int low = s & -s, rest = s ^ low;
+                float best = 3.4e38f;
+                int bt = low;
+                for (int tp = rest;; tp = (tp - 1) & rest) {
+                    const int t = tp | low;
+                    if (t != s) {
+                        const float c = copt[t] + copt[s ^ t];
+                        if (c < best) { best = c; bt = t; }
+                    }
+                    if (tp == 0) break;
+                }
+                copt[s] = SAH_CI * sa[s] + best;
+                part[s] = (unsigned char)bt;
+            }
+            if (copt[127] < pcost * (1.0f - 1e-5f)) {
+                // rewire: depth-first over the optimal partition, reusing the 6 inner nodes
+                int st_s[7], st_n[7], sp = 0, next = 1;
+                st_s[sp] = 127; st_n[sp] = p; ++sp;
+                while (sp > 0) {
+                    --sp;
+                    const int sset = st_s[sp], node = st_n[sp];
+                    const int halves[2] = {part[sset], sset ^ part[sset]};
+                    int codes[2];
+                    for (int h = 0; h < 2; ++h) {
+                        if (__popc(halves[h]) == 1) {
+                            codes[h] = leaves[__ffs(halves[h]) - 1];
+                        } else {
+                            codes[h] = inner[next++];
+                            st_s[sp] = halves[h]; st_n[sp] = codes[h]; ++sp;
+                        }
+                        set_parent(B, codes[h], node);
+                    }
+                    __stcg(&B.left[node], codes[0]);
+                    __stcg(&B.right[node], codes[1]);
+                    float3 lo = f3(3.4e38f, 3.4e38f, 3.4e38f), hi = f3(-3.4e38f, -3.4e38f, -3.4e38f);
+                    int c = 0;
+                    for (int i = 0; i < 7; ++i)
+                        if (sset & (1 << i)) {
+                            lo = f3(fminf(lo.x, lt[i].lo.x), fminf(lo.y, lt[i].lo.y), fminf(lo.z, lt[i].lo.z));
+                            hi = f3(fmaxf(hi.x, lt[i].hi.x), fmaxf(hi.y, lt[i].hi.y), fmaxf(hi.z, lt[i].hi.z));
+                            c += lt[i].count;
+                        }
+                    __stcg(&B.node_lo[node], make_float4(lo.x, lo.y, lo.z, 0.f));
+                    __stcg(&B.node_hi[node], make_float4(hi.x, hi.y, hi.z, 0.f));
+                    __stcg(&B.cost[node], copt[sset]);
+                    __stcg(&B.count[node], c);
+                }
+                done = true;
+            }
+        }
+    }
+    if (!done) {
+        __stcg(&B.node_lo[p], make_float4(plo.x, plo.y, plo.z, 0.f));
+        __stcg(&B.node_hi[p], make_float4(phi.x, phi.y, phi.z, 0.f));
+        __stcg(&B.cost[p], pcost);
+        __stcg(&B.count[p], cnt);
+    }
+}
+
+__global__ void k_treelets(BuildBuffers B, int n) {
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+        int p = __ldcg(&B.parent_leaf[k]);
+        while (p >= 0) {
+            __threadfence();
+            if (atomicAdd(&B.flags[p], 1) == 0) break;    // first arrival: the sibling finishes p
+            __threadfence();
+            treelet_node(B, p);
+            __threadfence();
+            p = __ldcg(&B.parent_int[p]);
+        }
+    }
+}
+
 // ---------------------------------------------------------------- BVH2 -> BVH4 collapse
 // Node layout (rt_device.cuh): 7 float4 = lo.x[4] hi.x[4] lo.y[4] hi.y[4] lo.z[4] hi.z[4] child[4].
 // A BVH2 internal child covering <= leaf_max primitives becomes a leaf over its contiguous
@@ -502,6 +669,14 @@ cudaError_t rtb_build_bvh(const BuildBuffers& Bc, cudaStream_t st, int* root, in
     k_karras<<<grid_for(n - 1), 256, 0, st>>>(B.keys[cur], n, B.left, B.right, B.parent_int, B.parent_leaf, B.range);
     cudaMemsetAsync(B.flags, 0, sizeof(int) * (n - 1), st);
     k_refit<<<grid_for(n), 256, 0, st>>>(B, n, slo, shi);
+    // treelet restructuring passes (SAH); leaf collapse by sorted range needs the original
+    // Morton topology, so restructuring runs only without it
+    if (B.leaf_max == 1) {
+        for (int pass = 0; pass < B.treelet_passes; ++pass) {
+            cudaMemsetAsync(B.flags, 0, sizeof(int) * (n - 1), st);
+            k_treelets<<<grid_for(n), 256, 0, st>>>(B, n);
+        }
+    }
     // root: a leaf if the whole scene fits one leaf, else BVH4 node 0 from BVH2 node 0
     if (n <= B.leaf_max) {
         *root = ~(((n - 1) << LEAF_SHIFT) | 0);

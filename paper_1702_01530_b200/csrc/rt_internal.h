@@ -85,6 +85,9 @@ struct BuildBuffers {
     int2* range;                // [N-1] sorted primitive range of each internal node
     int* prim_orig;             // out: leaf slot -> original primitive index (kept for refit)
     int leaf_max;               // collapse subtrees of <= leaf_max primitives into leaves
+    float* cost;                // [N-1] SAH cost of each internal node's subtree (treelets)
+    int* count;                 // [N-1] primitives below each internal node (treelets)
+    int treelet_passes;         // 0 = plain LBVH
 };
 
 // launchers (rt_trace.cu)
