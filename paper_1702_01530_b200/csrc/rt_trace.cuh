@@ -9,6 +9,9 @@ namespace rtb {
 #ifndef RT_BLOCK
 #define RT_BLOCK 256      // threads per trace CTA (stack stride)
 #endif
+#ifndef RT_SHADOW_SORT
+#define RT_SHADOW_SORT 1  // any-hit (shadow) rays also visit children near-to-far
+#endif
 #ifndef RT_SMEM_STACK
 #define RT_SMEM_STACK 16  // traversal-stack entries kept in shared memory; deeper ones in local
 #endif
@@ -156,6 +159,23 @@ __device__ __forceinline__ bool order_push(unsigned m, const float tn[4], const 
 }
 
 
+// Any-hit rays: push the hit children in slot order (no distance sort).
+__device__ __forceinline__ bool plain_push(unsigned m, const int4& ch, TravStack& stk, int& sp, int& node) {
+    if (!m) return false;
+    const int nh = __popc(m);
+    const uint32_t c0 = __ffs(m) - 1;
+    m &= m - 1;
+    int k = sp;
+    while (m) {
+        const uint32_t c = __ffs(m) - 1;
+        m &= m - 1;
+        stk.set(k++, pick4(ch, c));
+    }
+    sp += nh - 1;
+    node = pick4(ch, c0);
+    return true;
+}
+
 // Nearest hit over the 4-wide BVH (or every BVH primitive when BRUTE) and the planes.
 // Acceptance: t > t_min and (t, gid) lexicographically smallest (reading 9).
 // Children are visited near-to-far: entry distances (>= 0, so their bit patterns order like
@@ -237,7 +257,11 @@ __device__ __forceinline__ bool occluded(const DevScene& S, float3 o, float3 d, 
             float tn[4];
             int4 ch;
             const unsigned m = node4_hits(S.nodes, node, rb, dist, tn, ch);
+#if RT_SHADOW_SORT
             if (order_push(m, tn, ch, stk, sp, node)) continue;
+#else
+            if (plain_push(m, ch, stk, sp, node)) continue;
+#endif
         } else {
             const int enc = ~node;
             const int first = enc & ((1 << LEAF_SHIFT) - 1);
