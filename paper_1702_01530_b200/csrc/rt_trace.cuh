@@ -10,7 +10,7 @@ namespace rtb {
 #define RT_BLOCK 256      // threads per trace CTA (stack stride)
 #endif
 #ifndef RT_SHADOW_SORT
-#define RT_SHADOW_SORT 1  // any-hit (shadow) rays also visit children near-to-far
+#define RT_SHADOW_SORT 0  // 1: any-hit (shadow) rays also visit children near-to-far (measured slower)
 #endif
 #ifndef RT_SMEM_STACK
 #define RT_SMEM_STACK 16  // traversal-stack entries kept in shared memory; deeper ones in local
