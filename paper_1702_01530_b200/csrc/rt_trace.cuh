@@ -12,6 +12,9 @@ namespace rtb {
 #ifndef RT_SHADOW_SORT
 #define RT_SHADOW_SORT 0  // 1: any-hit (shadow) rays also visit children near-to-far (measured slower)
 #endif
+#ifndef RT_PLAIN_PUSH_LOOP
+#define RT_PLAIN_PUSH_LOOP 1
+#endif
 #ifndef RT_SMEM_STACK
 #define RT_SMEM_STACK 16  // traversal-stack entries kept in shared memory; deeper ones in local
 #endif
@@ -159,9 +162,11 @@ __device__ __forceinline__ bool order_push(unsigned m, const float tn[4], const 
 }
 
 
-// Any-hit rays: push the hit children in slot order (no distance sort).
+// Any-hit rays: continue with the lowest hit slot, push the others in slot order (no distance
+// sort); unrolled with predicated stores.
 __device__ __forceinline__ bool plain_push(unsigned m, const int4& ch, TravStack& stk, int& sp, int& node) {
     if (!m) return false;
+#if RT_PLAIN_PUSH_LOOP
     const int nh = __popc(m);
     const uint32_t c0 = __ffs(m) - 1;
     m &= m - 1;
@@ -173,6 +178,18 @@ __device__ __forceinline__ bool plain_push(unsigned m, const int4& ch, TravStack
     }
     sp += nh - 1;
     node = pick4(ch, c0);
+#else
+    const int codes[4] = {ch.x, ch.y, ch.z, ch.w};
+    int first = -1;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        if (m & (1u << c)) {
+            if (first < 0) first = codes[c];
+            else stk.set(sp++, codes[c]);
+        }
+    }
+    node = first;
+#endif
     return true;
 }
 
