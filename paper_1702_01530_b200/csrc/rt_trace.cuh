@@ -12,6 +12,9 @@ namespace rtb {
 #ifndef RT_SHADOW_SORT
 #define RT_SHADOW_SORT 0  // 1: any-hit (shadow) rays also visit children near-to-far (measured slower)
 #endif
+#ifndef RT_CLOSEST_SORT
+#define RT_CLOSEST_SORT 1  // nearest-hit rays visit hit children near-to-far
+#endif
 #ifndef RT_PLAIN_PUSH_LOOP
 #define RT_PLAIN_PUSH_LOOP 1
 #endif
@@ -235,7 +238,11 @@ __device__ __forceinline__ Hit closest_hit(const DevScene& S, float3 o, float3 d
             float tn[4];
             int4 ch;
             const unsigned m = node4_hits(S.nodes, node, rb, h.t, tn, ch);
+#if RT_CLOSEST_SORT
             if (order_push(m, tn, ch, stk, sp, node)) continue;
+#else
+            if (plain_push(m, ch, stk, sp, node)) continue;
+#endif
         } else {
             const int enc = ~node;
             const int first = enc & ((1 << LEAF_SHIFT) - 1);
