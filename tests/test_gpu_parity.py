@@ -350,3 +350,79 @@ def test_refit_moving_mesh(R):
     assert_parity(st)
     with pytest.raises(rt.RtError):
         rt.rt_scene_update_vertices(R.ctx, moved.vertices[:-1])
+
+
+def test_zero_separation_identical_eyes(R):
+    """interocular -> 0 gives identical left/right images (bit-exact on the GPU)."""
+    s = scenes.scene_c3().with_view(width=80, height=45)
+    r = s.rig
+    s0 = s.with_view(rig=Rig(r.eye, r.look_at, r.up, r.vfov_deg, 0.0, r.convergence))
+    g = gpu_render(R, s0)
+    np.testing.assert_array_equal(g["fb"][0], g["fb"][1])
+    np.testing.assert_array_equal(g["id"][0], g["id"][1])
+
+
+@pytest.mark.parametrize("variant", ["parallel_rig", "no_lights", "many_lights", "tiny"])
+def test_scene_and_rig_variants(R, variant):
+    """Parity on rig / lighting / size edge cases: parallel rig (C <= 0, R#13), ambient-only,
+    16 lights, 1x1 and 1x37 images."""
+    base = scenes.scene_c2().with_view(width=48, height=36, max_depth=3)
+    r = base.rig
+    if variant == "parallel_rig":
+        s = base.with_view(rig=Rig(r.eye, r.look_at, r.up, r.vfov_deg, 0.3, 0.0))
+    elif variant == "no_lights":
+        s = base.with_view()
+        s.lights = np.zeros((0, 6))
+        s = s.finalize()
+    elif variant == "many_lights":
+        s = base.with_view()
+        rng = np.random.default_rng(9)
+        s.lights = np.concatenate([rng.uniform(-12, 12, (16, 3)) + [0, 14, 0], rng.uniform(0.02, 0.1, (16, 3))], 1)
+        s = s.finalize()
+    else:
+        for w, h in ((1, 1), (1, 37)):
+            full_parity(R, base.with_view(width=w, height=h), f"tiny {w}x{h}")
+        return
+    full_parity(R, s, variant)
+
+
+def test_reupload_replaces_scene(R):
+    """A second rt_scene_upload fully replaces the first (no stale BVH / materials)."""
+    a = scenes.scene_c1().with_view(width=40, height=30)
+    b = scenes.paper_scene(5).with_view(width=40, height=30)
+    ga = gpu_render(R, a)
+    gb = gpu_render(R, b)
+    gb2 = gpu_render(R, b)
+    np.testing.assert_array_equal(gb["fb"], gb2["fb"])
+    ref = Oracle(b).render()
+    assert_parity(compare(ref, gb["id"], gb["fb"], gb["radiance"], "paper5 after C1"))
+    assert not np.array_equal(ga["fb"], gb["fb"])
+
+
+def test_download_many_outstanding(R):
+    """rt_download: several frames in flight on the copy stream, polled with rt_query."""
+    import ctypes
+    s = scenes.scene_c1()
+    R.upload(s)
+    R.set_camera(s.rig)
+    nbytes = 2 * s.height * s.width * 4
+    fbs, hosts, evs = [], [], []
+    try:
+        for k in range(4):
+            out = R.render(s.width, s.height, k % 2)
+            fbs.append(out["fb"])
+            hosts.append(rt.rt_host_alloc(nbytes))
+            evs.append(rt.rt_download(R.ctx, out["fb"].data_ptr(), hosts[-1], nbytes))
+        import time
+        t0 = time.time()
+        while not all(rt.rt_query(e) for e in evs):
+            assert time.time() - t0 < 30
+            time.sleep(0.001)
+        torch.cuda.synchronize()
+        for fb, h, e in zip(fbs, hosts, evs):
+            got = np.frombuffer((ctypes.c_uint8 * nbytes).from_address(h), np.uint8)
+            np.testing.assert_array_equal(got, fb.cpu().numpy().reshape(-1))
+            rt.rt_wait(e)
+    finally:
+        for h in hosts:
+            rt.rt_host_free(h)
