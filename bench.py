@@ -194,10 +194,18 @@ def run_ours(args, scene):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
+    # RT_BENCH_SHARE_DEVICE=1 (tests only): every rank on cuda:0 with a gloo process group, so the
+    # multi-rank path (peer-store frames, barriers, max over ranks, e2e) runs on a one-GPU box
+    share = os.environ.get("RT_BENCH_SHARE_DEVICE") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     def barrier():
         if world > 1:
@@ -326,23 +334,30 @@ def run_e2e(args, R, scene, rank, world, frame, fb, dev, rays_total):
     hosts = [rt.rt_host_alloc(nbytes) for _ in range(2)] if rank == 0 else []
     rig = scene.rig
     pending = [None, None]
-    fb2 = R.alloc_fb(W, H) if world == 1 else None
+    fb2 = R.alloc_fb(W, H)
+    fbs = [fb, fb2]
+    frames = [frame]
+    if world > 1:
+        import torch.distributed as dist
+        from paper_1702_01530_b200 import multigpu
+        frames.append(multigpu.make_frame(frame.mode, R, fb2, rank, world, dist, W, H))
 
     def frame_step(k):
         slot = k % 2
         if pending[slot] is not None:
-            rt.rt_wait(pending[slot])                         # host slot free again
+            rt.rt_wait(pending[slot])                         # slot's previous download is done
             pending[slot] = None
+        if world > 1:
+            dist.barrier()                                     # ... before any rank writes that slot again
         rt.rt_set_stereo_camera(R.ctx, rig.eye, rig.look_at, rig.up, rig.vfov_deg, rig.interocular,
                                 rig.convergence)
+        dst = fbs[slot]
         if world == 1:
-            dst = fb if slot == 0 else fb2
             pitch = W * 4
             rt.rt_render_stereo(R.ctx, W, H, D, rt.rt_fb(dst[0].data_ptr(), 0, pitch), rt.rt_fb(dst[1].data_ptr(), 0, pitch))
         else:
-            dst = fb
-            frame.render(D)
-            frame.assemble()
+            frames[slot].render(D)
+            frames[slot].assemble()
         if rank == 0:
             pending[slot] = rt.rt_download(R.ctx, dst.data_ptr(), hosts[slot], nbytes)
 
@@ -391,11 +406,13 @@ def run_e2e(args, R, scene, rank, world, frame, fb, dev, rays_total):
     ok = True
     if rank == 0:
         slot = (args.steps - 1) % 2
-        src = fb if (world > 1 or slot == 0) else fb2
+        src = fbs[slot]
         host = np.frombuffer((ctypes.c_uint8 * nbytes).from_address(hosts[slot]), np.uint8)
         ok = bool(np.array_equal(host, src.reshape(-1).cpu().numpy()))
         for h in hosts:
             rt.rt_host_free(h)
+    for f in frames[1:]:
+        f.close()
     return {"value": rays_total / (dt / args.steps) / 1e6, "unit": UNIT,
             "h2d_bytes_per_step": 76, "d2h_bytes_per_step": nbytes if rank == 0 else 0,
             "ms_per_step": dt / args.steps * 1e3, "stereo_fps": args.steps / dt, "download_verified": ok,
