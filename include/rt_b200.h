@@ -143,6 +143,8 @@ rt_status rt_synchronize(rt_context* ctx);
 /* Thread-local message of the last failed call on this thread ("" if none). */
 const char* rt_last_error(void);
 int rt_version(void);
+/* Children per BVH node of this build (4 or 8), i.e. rt_bvh_export's node = 7*width floats. */
+int rt_bvh_width(void);
 
 /* ------------------------------------------------------------------ scene */
 /* PAPER.md:64-66,82 (§4: scene of objects + light sources, copied to the GPU) and
@@ -266,8 +268,9 @@ rt_status rt_compose(rt_context* ctx, rt_fb left, rt_fb right, uint32_t width, u
 /* Scene statistics after upload: [0] n_spheres [1] n_planes [2] n_triangles [3] bvh prims
  * [4] BVH4 nodes [5] BVH4 depth (levels) [6] device bytes of scene+BVH [7] build time us. */
 rt_status rt_scene_info(rt_context* ctx, uint64_t info[8]);
-/* Copy the device BVH (4-wide nodes, 28 floats each: lo.x[4] hi.x[4] lo.y[4] hi.y[4] lo.z[4]
- * hi.z[4] child[4] as int32; child >= 0 node, 0x7fffffff empty, < 0 leaf ~((count-1)<<24 | first))
+/* Copy the device BVH (W = rt_bvh_width() children per node, 7*W floats each: lo.x[W] hi.x[W]
+ * lo.y[W] hi.y[W] lo.z[W] hi.z[W] child[W] as int32; child >= 0 node, 0x7fffffff empty (box
+ * inverted), < 0 leaf ~((count-1)<<24 | first))
  * and the leaf-order primitive global IDs to
  * HOST arrays for structural tests; pass NULL to query sizes via *n_nodes / *n_prims. */
 rt_status rt_bvh_export(rt_context* ctx, float* nodes, uint32_t* n_nodes, int32_t* prim_gid, uint32_t* n_prims);

@@ -122,6 +122,8 @@ extern "C" {
 
 int rt_version(void) { return RT_ABI_VERSION; }
 
+int rt_bvh_width(void) { return rtb::BVH_W; }
+
 const char* rt_last_error(void) { return g_err.c_str(); }
 
 rt_status rt_create(int device, void* cuda_stream, rt_context** out) {
@@ -364,7 +366,7 @@ rt_status rt_scene_upload(rt_context* c, const rt_primitives* P, const rt_materi
             (st = salloc(4 * Nn, (void**)&B.right)) || (st = salloc(4 * Nn, (void**)&B.parent_int)) ||
             (st = salloc(4 * (size_t)N, (void**)&B.parent_leaf)) || (st = salloc(4 * Nn, (void**)&B.flags)) ||
             (st = salloc(16 * Nn, (void**)&B.node_lo)) || (st = salloc(16 * Nn, (void**)&B.node_hi)) ||
-            (st = salloc(8 * Nn, (void**)&B.range)) || (st = salloc(112 * Nn, (void**)&B.nodes4)) ||
+            (st = salloc(8 * Nn, (void**)&B.range)) || (st = salloc(16 * rtb::NODE_F4 * Nn, (void**)&B.nodes4)) ||
             (st = salloc(8 * (size_t)N, (void**)&B.frontier[0])) || (st = salloc(8 * (size_t)N, (void**)&B.frontier[1])) ||
             (st = salloc(16, (void**)&B.wide_counters)) || (st = salloc(4 * Nn, (void**)&B.cost)) ||
             (st = salloc(4 * Nn, (void**)&B.count))) {
@@ -377,12 +379,12 @@ rt_status rt_scene_upload(rt_context* c, const rt_primitives* P, const rt_materi
         cudaError_t e = rtb_build_bvh(B, c->stream, &root, &n_nodes4, &depth4, level_start.data());
         if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
         if (e == cudaSuccess && n_nodes4 > 0) {        // compact the BVH4 into an exact-size buffer
-            if ((st = dalloc(c, 7 * (size_t)n_nodes4, &d_nodes))) {
+            if ((st = dalloc(c, rtb::NODE_F4 * (size_t)n_nodes4, &d_nodes))) {
                 free_scratch();
                 free_scene(c);
                 return st;
             }
-            e = cudaMemcpy(d_nodes, B.nodes4, 112 * (size_t)n_nodes4, cudaMemcpyDeviceToDevice);
+            e = cudaMemcpy(d_nodes, B.nodes4, 16 * rtb::NODE_F4 * (size_t)n_nodes4, cudaMemcpyDeviceToDevice);
         }
         free_scratch();
         if (e != cudaSuccess) {
@@ -617,7 +619,7 @@ rt_status rt_render_stereo_ex(rt_context* c, const rt_render_params* p, const rt
     P.shard = out->shard;
     P.shard_fmt = (int)out->shard_format;
     P.counters = out->counters ? out->counters : c->scratch_counters;
-    P.stack_entries = 3 * (int)c->info[5] + 2;       // <= 3 pending siblings per BVH4 level
+    P.stack_entries = (rtb::BVH_W - 1) * (int)c->info[5] + 2;   // <= W-1 pending siblings per level
     if (P.stack_entries > rtb::STACK_CAP) return fail(RT_ERR_SIZE, "BVH too deep (%d levels)", (int)c->info[5]);
     P.n_tiles = (int)n_tiles;
     P.peer_fence = (p->flags & RT_RENDER_PEER_STORE) ? 1 : 0;
@@ -878,7 +880,7 @@ rt_status rt_bvh_export(rt_context* c, float* nodes, uint32_t* n_nodes, int32_t*
     const uint32_t nn = (uint32_t)c->info[4], np = (uint32_t)c->sc.n_bvh;
     CUDA_TRY(cudaSetDevice(c->device));
     CUDA_TRY(cudaStreamSynchronize(c->stream));
-    if (nodes && nn) CUDA_TRY(cudaMemcpy(nodes, c->sc.nodes, (size_t)nn * 112, cudaMemcpyDeviceToHost));
+    if (nodes && nn) CUDA_TRY(cudaMemcpy(nodes, c->sc.nodes, (size_t)nn * 16 * rtb::NODE_F4, cudaMemcpyDeviceToHost));
     if (prim_gid && np) {
         std::vector<float4> p(3 * (size_t)np);
         CUDA_TRY(cudaMemcpy(p.data(), c->sc.prims, p.size() * sizeof(float4), cudaMemcpyDeviceToHost));

@@ -478,11 +478,11 @@ __device__ __forceinline__ WChild make_child(int code, const BuildBuffers& B) {
 __global__ void k_wide(BuildBuffers B, const int2* __restrict__ fin, int n_in, int2* fout, int* counters) {
     for (int it = blockIdx.x * blockDim.x + threadIdx.x; it < n_in; it += gridDim.x * blockDim.x) {
         const int src = fin[it].x, dst = fin[it].y;
-        WChild ch[4];
+        WChild ch[BVH_W];
         int n = 2;
         ch[0] = make_child(B.left[src], B);
         ch[1] = make_child(B.right[src], B);
-        while (n < 4) {
+        while (n < BVH_W) {
             int best = -1;
             float ba = -1.0f;
             for (int c = 0; c < n; ++c) {
@@ -496,40 +496,32 @@ __global__ void k_wide(BuildBuffers B, const int2* __restrict__ fin, int n_in, i
             ch[best] = make_child(B.left[code], B);
             ch[n++] = make_child(B.right[code], B);
         }
-        float lo[3][4], hi[3][4];
-        int code4[4];
-        for (int c = 0; c < 4; ++c) {
+        float* o = reinterpret_cast<float*>(B.nodes4 + NODE_F4 * (size_t)dst);
+        int* oc = reinterpret_cast<int*>(o) + 6 * BVH_W;
+        for (int c = 0; c < BVH_W; ++c) {
             if (c >= n) {
-                code4[c] = WIDE_EMPTY;
                 // inverted box (lo = +1e30, hi = -1e30): every slab test rejects it, so the
                 // traversal needs no per-slot validity test
-                for (int k = 0; k < 3; ++k) { lo[k][c] = 1e30f; hi[k][c] = -1e30f; }
+                for (int k = 0; k < 3; ++k) { o[(2 * k) * BVH_W + c] = 1e30f; o[(2 * k + 1) * BVH_W + c] = -1e30f; }
+                oc[c] = WIDE_EMPTY;
                 continue;
             }
-            lo[0][c] = ch[c].lo.x; lo[1][c] = ch[c].lo.y; lo[2][c] = ch[c].lo.z;
-            hi[0][c] = ch[c].hi.x; hi[1][c] = ch[c].hi.y; hi[2][c] = ch[c].hi.z;
+            o[0 * BVH_W + c] = ch[c].lo.x; o[1 * BVH_W + c] = ch[c].hi.x;
+            o[2 * BVH_W + c] = ch[c].lo.y; o[3 * BVH_W + c] = ch[c].hi.y;
+            o[4 * BVH_W + c] = ch[c].lo.z; o[5 * BVH_W + c] = ch[c].hi.z;
             const int code = ch[c].code;
             if (code < 0) {
-                code4[c] = code;                                    // BVH2 leaf: ~slot == count-1 of 0
+                oc[c] = code;                                       // BVH2 leaf: ~slot (count 1)
             } else if (!is_open(code, B.range, B.leaf_max)) {
                 const int2 r = B.range[code];
-                code4[c] = ~(((r.y - r.x) << LEAF_SHIFT) | r.x);
+                oc[c] = ~(((r.y - r.x) << LEAF_SHIFT) | r.x);
             } else {
                 const int slot = atomicAdd(&counters[1], 1);
                 const int q = atomicAdd(&counters[0], 1);
                 fout[q] = make_int2(code, slot);
-                code4[c] = slot;
+                oc[c] = slot;
             }
         }
-        float4* o = B.nodes4 + 7 * (size_t)dst;
-        o[0] = make_float4(lo[0][0], lo[0][1], lo[0][2], lo[0][3]);
-        o[1] = make_float4(hi[0][0], hi[0][1], hi[0][2], hi[0][3]);
-        o[2] = make_float4(lo[1][0], lo[1][1], lo[1][2], lo[1][3]);
-        o[3] = make_float4(hi[1][0], hi[1][1], hi[1][2], hi[1][3]);
-        o[4] = make_float4(lo[2][0], lo[2][1], lo[2][2], lo[2][3]);
-        o[5] = make_float4(hi[2][0], hi[2][1], hi[2][2], hi[2][3]);
-        o[6] = make_float4(__int_as_float(code4[0]), __int_as_float(code4[1]), __int_as_float(code4[2]),
-                           __int_as_float(code4[3]));
     }
 }
 
@@ -588,13 +580,11 @@ __global__ void k_refit4(float4* nodes, int begin, int end, const int* __restric
                          const float4* __restrict__ spheres, const uint32_t* __restrict__ tri_idx,
                          const float* __restrict__ vtx) {
     for (int i = begin + blockIdx.x * blockDim.x + threadIdx.x; i < end; i += gridDim.x * blockDim.x) {
-        float4* q = nodes + 7 * (size_t)i;
-        const int4 ch = *reinterpret_cast<const int4*>(q + 6);
-        float lo[3][4], hi[3][4];
-        const int codes[4] = {ch.x, ch.y, ch.z, ch.w};
-        for (int c = 0; c < 4; ++c) {
+        float* q = reinterpret_cast<float*>(nodes + NODE_F4 * (size_t)i);
+        const int* qc = reinterpret_cast<const int*>(q) + 6 * BVH_W;
+        for (int c = 0; c < BVH_W; ++c) {
             float3 l = f3(1e30f, 1e30f, 1e30f), h = f3(-1e30f, -1e30f, -1e30f);
-            const int code = codes[c];
+            const int code = qc[c];
             if (code == WIDE_EMPTY) {
             } else if (code < 0) {
                 const int enc = ~code;
@@ -606,22 +596,16 @@ __global__ void k_refit4(float4* nodes, int begin, int end, const int* __restric
                     h = f3(fmaxf(h.x, ph.x), fmaxf(h.y, ph.y), fmaxf(h.z, ph.z));
                 }
             } else {
-                const float4* r = nodes + 7 * (size_t)code;
-                const float4 lx = r[0], hx = r[1], ly = r[2], hy = r[3], lz = r[4], hz = r[5];
-                l = f3(fminf(fminf(lx.x, lx.y), fminf(lx.z, lx.w)), fminf(fminf(ly.x, ly.y), fminf(ly.z, ly.w)),
-                       fminf(fminf(lz.x, lz.y), fminf(lz.z, lz.w)));
-                h = f3(fmaxf(fmaxf(hx.x, hx.y), fmaxf(hx.z, hx.w)), fmaxf(fmaxf(hy.x, hy.y), fmaxf(hy.z, hy.w)),
-                       fmaxf(fmaxf(hz.x, hz.y), fmaxf(hz.z, hz.w)));
+                const float* r = reinterpret_cast<const float*>(nodes + NODE_F4 * (size_t)code);
+                for (int k = 0; k < BVH_W; ++k) {
+                    l = f3(fminf(l.x, r[0 * BVH_W + k]), fminf(l.y, r[2 * BVH_W + k]), fminf(l.z, r[4 * BVH_W + k]));
+                    h = f3(fmaxf(h.x, r[1 * BVH_W + k]), fmaxf(h.y, r[3 * BVH_W + k]), fmaxf(h.z, r[5 * BVH_W + k]));
+                }
             }
-            lo[0][c] = l.x; lo[1][c] = l.y; lo[2][c] = l.z;
-            hi[0][c] = h.x; hi[1][c] = h.y; hi[2][c] = h.z;
+            q[0 * BVH_W + c] = l.x; q[1 * BVH_W + c] = h.x;
+            q[2 * BVH_W + c] = l.y; q[3 * BVH_W + c] = h.y;
+            q[4 * BVH_W + c] = l.z; q[5 * BVH_W + c] = h.z;
         }
-        q[0] = make_float4(lo[0][0], lo[0][1], lo[0][2], lo[0][3]);
-        q[1] = make_float4(hi[0][0], hi[0][1], hi[0][2], hi[0][3]);
-        q[2] = make_float4(lo[1][0], lo[1][1], lo[1][2], lo[1][3]);
-        q[3] = make_float4(hi[1][0], hi[1][1], hi[1][2], hi[1][3]);
-        q[4] = make_float4(lo[2][0], lo[2][1], lo[2][2], lo[2][3]);
-        q[5] = make_float4(hi[2][0], hi[2][1], hi[2][2], hi[2][3]);
     }
 }
 

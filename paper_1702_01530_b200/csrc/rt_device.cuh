@@ -24,7 +24,12 @@ namespace rtb {
 constexpr float T_MIN = 1e-4f;     // SPEC.md:156 t_min
 constexpr float BIAS = 1e-4f;      // SPEC.md:156 shadow_bias (also reflection/refraction origins)
 constexpr int MAX_DEPTH = 16;
-constexpr int STACK_CAP = 3 * 64 + 2;   // BVH4 traversal stack: 3 siblings per level, depth <= 64
+#ifndef RT_BVH_WIDTH
+#define RT_BVH_WIDTH 4
+#endif
+constexpr int BVH_W = RT_BVH_WIDTH;                    // children per node (4 or 8)
+constexpr int NODE_F4 = 7 * BVH_W / 4;                 // float4 per node: lo/hi x,y,z + child codes
+constexpr int STACK_CAP = (BVH_W - 1) * 64 + 2;       // traversal stack: W-1 siblings per level, depth <= 64
 constexpr int LEAF_SHIFT = 24;     // leaf encoding: ~((count-1) << 24 | first)
 constexpr int TILE = 16;
 constexpr int WIDE_EMPTY = 0x7fffffff;   // unused BVH4 child slot

@@ -196,6 +196,70 @@ __device__ __forceinline__ bool plain_push(unsigned m, const int4& ch, TravStack
     return true;
 }
 
+// ---------------------------------------------------------------- 8-wide nodes
+// 14 float4: lo.x[8] hi.x[8] lo.y[8] hi.y[8] lo.z[8] hi.z[8] child[8]; near/far planes picked per
+// ray by direction sign (two float4 per array); child codes are loaded only for pushed children.
+__device__ __forceinline__ unsigned node8_hits(const float4* __restrict__ nodes, int node, const RayBox& rb, float tmax,
+                                               float tn[8]) {
+    const float4* q = nodes + 14 * node;
+#pragma unroll
+    for (int g = 0; g < 2; ++g) {
+        const float4 nx = __ldg(q + 2 * rb.sx + g), fx = __ldg(q + 2 - 2 * rb.sx + g);
+        const float4 ny = __ldg(q + 4 + 2 * rb.sy + g), fy = __ldg(q + 6 - 2 * rb.sy + g);
+        const float4 nz = __ldg(q + 8 + 2 * rb.sz + g), fz = __ldg(q + 10 - 2 * rb.sz + g);
+        tn[4 * g + 0] = slab(rb, nx.x, fx.x, ny.x, fy.x, nz.x, fz.x, tmax);
+        tn[4 * g + 1] = slab(rb, nx.y, fx.y, ny.y, fy.y, nz.y, fz.y, tmax);
+        tn[4 * g + 2] = slab(rb, nx.z, fx.z, ny.z, fy.z, nz.z, fz.z, tmax);
+        tn[4 * g + 3] = slab(rb, nx.w, fx.w, ny.w, fy.w, nz.w, fz.w, tmax);
+    }
+    unsigned m = 0;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) m |= tn[c] >= 0.0f ? (1u << c) : 0u;   // empty slots: inverted boxes
+    return m;
+}
+
+__device__ __forceinline__ int child8(const float4* __restrict__ nodes, int node, uint32_t slot) {
+    return __ldg(reinterpret_cast<const int*>(nodes + 14 * node + 12) + slot);
+}
+
+// Nearest-first order of the hit children: (distance bits | 3-bit slot) keys through Batcher's
+// 19-exchange odd-even merge network; the nearest continues, the others are pushed far-to-near.
+__device__ __forceinline__ bool order_push8(unsigned m, const float tn[8], const float4* __restrict__ nodes, TravStack& stk,
+                                            int& sp, int& node) {
+    if (!m) return false;
+    uint32_t k[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) k[c] = (m & (1u << c)) ? ((__float_as_uint(tn[c]) & ~7u) | (uint32_t)c) : 0xffffffffu;
+    cswap(k[0], k[1]); cswap(k[2], k[3]); cswap(k[4], k[5]); cswap(k[6], k[7]);
+    cswap(k[0], k[2]); cswap(k[1], k[3]); cswap(k[4], k[6]); cswap(k[5], k[7]);
+    cswap(k[1], k[2]); cswap(k[5], k[6]);
+    cswap(k[0], k[4]); cswap(k[1], k[5]); cswap(k[2], k[6]); cswap(k[3], k[7]);
+    cswap(k[2], k[4]); cswap(k[3], k[5]);
+    cswap(k[1], k[2]); cswap(k[3], k[4]); cswap(k[5], k[6]);
+    const int nh = __popc(m);
+    const int parent = node;
+#pragma unroll
+    for (int i = 7; i >= 1; --i)
+        if (i < nh) stk.set(sp + nh - 1 - i, child8(nodes, parent, k[i] & 7u));
+    sp += nh - 1;
+    node = child8(nodes, parent, k[0] & 7u);
+    return true;
+}
+
+__device__ __forceinline__ bool plain_push8(unsigned m, const float4* __restrict__ nodes, TravStack& stk, int& sp, int& node) {
+    if (!m) return false;
+    const int parent = node;
+    const uint32_t c0 = __ffs(m) - 1;
+    m &= m - 1;
+    while (m) {
+        const uint32_t c = __ffs(m) - 1;
+        m &= m - 1;
+        stk.set(sp++, child8(nodes, parent, c));
+    }
+    node = child8(nodes, parent, c0);
+    return true;
+}
+
 // Nearest hit over the 4-wide BVH (or every BVH primitive when BRUTE) and the planes.
 // Acceptance: t > t_min and (t, gid) lexicographically smallest (reading 9).
 // Children are visited near-to-far: entry distances (>= 0, so their bit patterns order like
@@ -235,6 +299,11 @@ __device__ __forceinline__ Hit closest_hit(const DevScene& S, float3 o, float3 d
     while (true) {
         if (node >= 0) {
             cnt.add(CNT_NODE_VISITS);
+#if RT_BVH_WIDTH == 8
+            float tn[8];
+            const unsigned m = node8_hits(S.nodes, node, rb, h.t, tn);
+            if (order_push8(m, tn, S.nodes, stk, sp, node)) continue;
+#else
             float tn[4];
             int4 ch;
             const unsigned m = node4_hits(S.nodes, node, rb, h.t, tn, ch);
@@ -242,6 +311,7 @@ __device__ __forceinline__ Hit closest_hit(const DevScene& S, float3 o, float3 d
             if (order_push(m, tn, ch, stk, sp, node)) continue;
 #else
             if (plain_push(m, ch, stk, sp, node)) continue;
+#endif
 #endif
         } else {
             const int enc = ~node;
@@ -278,6 +348,11 @@ __device__ __forceinline__ bool occluded(const DevScene& S, float3 o, float3 d, 
     while (true) {
         if (node >= 0) {
             cnt.add(CNT_NODE_VISITS);
+#if RT_BVH_WIDTH == 8
+            float tn[8];
+            const unsigned m = node8_hits(S.nodes, node, rb, dist, tn);
+            if (plain_push8(m, S.nodes, stk, sp, node)) continue;
+#else
             float tn[4];
             int4 ch;
             const unsigned m = node4_hits(S.nodes, node, rb, dist, tn, ch);
@@ -285,6 +360,7 @@ __device__ __forceinline__ bool occluded(const DevScene& S, float3 o, float3 d, 
             if (order_push(m, tn, ch, stk, sp, node)) continue;
 #else
             if (plain_push(m, ch, stk, sp, node)) continue;
+#endif
 #endif
         } else {
             const int enc = ~node;

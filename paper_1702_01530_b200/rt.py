@@ -30,7 +30,7 @@ EXPORTED = ["rt_create", "rt_destroy", "rt_synchronize", "rt_last_error", "rt_ve
             "rt_set_stereo_camera", "rt_render_stereo", "rt_render_stereo_ex", "rt_download", "rt_wait", "rt_query",
             "rt_host_alloc", "rt_host_free", "rt_upload", "rt_shard_tiles", "rt_shard_bytes", "rt_unpack_shards_host",
             "rt_unpack_shards", "rt_ipc_get_handle", "rt_ipc_open", "rt_ipc_close", "rt_scene_info", "rt_bvh_export",
-            "rt_bench_ffma", "rt_compose", "rt_scene_update_vertices"]
+            "rt_bench_ffma", "rt_compose", "rt_scene_update_vertices", "rt_bvh_width"]
 
 
 class RtError(RuntimeError):
@@ -114,6 +114,7 @@ def lib():
         L.rt_last_error.restype = C.c_char_p
         L.rt_last_error.argtypes = []
         L.rt_version.restype = C.c_int
+        L.rt_bvh_width.restype = C.c_int
         _lib = L
     return _lib
 
@@ -135,6 +136,10 @@ def _f3(x):
 # ---------------------------------------------------------------- raw entry points (same names)
 def rt_version():
     return lib().rt_version()
+
+
+def rt_bvh_width():
+    return lib().rt_bvh_width()
 
 
 def rt_last_error():
@@ -303,7 +308,7 @@ def rt_scene_info(ctx):
 def rt_bvh_export(ctx):
     nn, npr = C.c_uint32(), C.c_uint32()
     _check(lib().rt_bvh_export(ctx, None, C.byref(nn), None, C.byref(npr)))
-    nodes = np.zeros((max(nn.value, 1), 28), np.float32)
+    nodes = np.zeros((max(nn.value, 1), 7 * lib().rt_bvh_width()), np.float32)
     gids = np.zeros(max(npr.value, 1), np.int32)
     _check(lib().rt_bvh_export(ctx, nodes.ctypes.data, C.byref(nn), gids.ctypes.data, C.byref(npr)))
     return nodes[:nn.value], gids[:npr.value]

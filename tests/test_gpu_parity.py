@@ -278,10 +278,12 @@ def test_bvh_structure(R):
     n = s.n_spheres + s.n_tris
     assert info["bvh_prims"] == n and 0 < info["bvh_nodes"] < n
     assert sorted(gids.tolist()) == list(range(s.n_spheres)) + list(range(s.n_spheres + s.n_planes, s.n_spheres + s.n_planes + s.n_tris))
-    child = nodes[:, 24:28].view(np.int32)
+    Wd = rt.rt_bvh_width()
+    child = nodes[:, 6 * Wd:7 * Wd].view(np.int32)
+
     def box(i, c):
-        return (np.array([nodes[i, 0 + c], nodes[i, 8 + c], nodes[i, 16 + c]]),
-                np.array([nodes[i, 4 + c], nodes[i, 12 + c], nodes[i, 20 + c]]))
+        return (np.array([nodes[i, 0 * Wd + c], nodes[i, 2 * Wd + c], nodes[i, 4 * Wd + c]]),
+                np.array([nodes[i, 1 * Wd + c], nodes[i, 3 * Wd + c], nodes[i, 5 * Wd + c]]))
     covered = np.zeros(n, int)
     stack, seen, depth_max = [(0, 1)], set(), 0
     while stack:
@@ -289,7 +291,7 @@ def test_bvh_structure(R):
         assert i not in seen
         seen.add(i)
         depth_max = max(depth_max, dep)
-        for c in range(4):
+        for c in range(Wd):
             code = int(child[i, c])
             if code == 0x7FFFFFFF:
                 continue
@@ -299,7 +301,7 @@ def test_bvh_structure(R):
                 covered[first:first + cnt] += 1
             else:
                 blo, bhi = box(i, c)
-                sub = [box(code, k) for k in range(4) if int(child[code, k]) != 0x7FFFFFFF]
+                sub = [box(code, k) for k in range(Wd) if int(child[code, k]) != 0x7FFFFFFF]
                 assert np.all(blo <= np.min([b[0] for b in sub], 0)) and np.all(bhi >= np.max([b[1] for b in sub], 0))
                 stack.append((code, dep + 1))
     assert np.all(covered == 1)
