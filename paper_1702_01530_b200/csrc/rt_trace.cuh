@@ -12,6 +12,9 @@ namespace rtb {
 #ifndef RT_SHADOW_SORT
 #define RT_SHADOW_SORT 0  // 1: any-hit (shadow) rays also visit children near-to-far (measured slower)
 #endif
+#ifndef RT_W8_FULL_SORT
+#define RT_W8_FULL_SORT 1
+#endif
 #ifndef RT_CLOSEST_SORT
 #define RT_CLOSEST_SORT 1  // nearest-hit rays visit hit children near-to-far
 #endif
@@ -230,12 +233,20 @@ __device__ __forceinline__ bool order_push8(unsigned m, const float tn[8], const
     uint32_t k[8];
 #pragma unroll
     for (int c = 0; c < 8; ++c) k[c] = (m & (1u << c)) ? ((__float_as_uint(tn[c]) & ~7u) | (uint32_t)c) : 0xffffffffu;
+#if RT_W8_FULL_SORT
     cswap(k[0], k[1]); cswap(k[2], k[3]); cswap(k[4], k[5]); cswap(k[6], k[7]);
     cswap(k[0], k[2]); cswap(k[1], k[3]); cswap(k[4], k[6]); cswap(k[5], k[7]);
     cswap(k[1], k[2]); cswap(k[5], k[6]);
     cswap(k[0], k[4]); cswap(k[1], k[5]); cswap(k[2], k[6]); cswap(k[3], k[7]);
     cswap(k[2], k[4]); cswap(k[3], k[5]);
     cswap(k[1], k[2]); cswap(k[3], k[4]); cswap(k[5], k[6]);
+#else
+    // nearest first, the second nearest next; the rest in slot order
+    cswap(k[0], k[1]); cswap(k[2], k[3]); cswap(k[4], k[5]); cswap(k[6], k[7]);
+    cswap(k[0], k[2]); cswap(k[4], k[6]); cswap(k[0], k[4]);     // k[0] = min
+    cswap(k[1], k[2]); cswap(k[5], k[6]); cswap(k[1], k[5]);     // k[1] = min of the losers of k[0]'s path
+    cswap(k[3], k[7]); cswap(k[1], k[3]);
+#endif
     const int nh = __popc(m);
     const int parent = node;
 #pragma unroll
