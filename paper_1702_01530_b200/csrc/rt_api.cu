@@ -81,6 +81,7 @@ struct rt_context {
     float vfov = 0;
     int leaf_max = 1;                // LBVH leaf collapse threshold (env RT_LEAF_MAX, <= 16)
     int treelet_passes = 3;          // SAH treelet restructuring passes (env RT_TREELETS)
+    int grid_limit = 0;              // cap on trace CTAs (env RT_GRID_LIMIT; 0 = full machine)
     // refit state (rt_scene_update_vertices)
     int* d_prim_orig = nullptr;
     float* d_vertices = nullptr;
@@ -137,6 +138,7 @@ rt_status rt_create(int device, void* cuda_stream, rt_context** out) {
     c->device = device;
     if (const char* lm = getenv("RT_LEAF_MAX")) c->leaf_max = std::max(1, std::min(16, atoi(lm)));
     if (const char* tp = getenv("RT_TREELETS")) c->treelet_passes = std::max(0, std::min(8, atoi(tp)));
+    if (const char* gl = getenv("RT_GRID_LIMIT")) c->grid_limit = std::max(0, atoi(gl));
     cudaError_t e = cudaSetDevice(device);
     if (e == cudaSuccess && cuda_stream) {
         c->stream = static_cast<cudaStream_t>(cuda_stream);
@@ -629,7 +631,8 @@ rt_status rt_render_stereo_ex(rt_context* c, const rt_render_params* p, const rt
     CUDA_TRY(rtb_trace_occupancy(p->flags & (RT_RENDER_COUNT | RT_RENDER_BRUTE_FORCE), P.stack_entries, &occ));
     if (occ < 1) occ = 1;
     const long long max_blocks = ((long long)P.n_work + 255) / 256;
-    const int grid = (int)std::min<long long>((long long)c->num_sms * occ, std::max<long long>(1, max_blocks));
+    int grid = (int)std::min<long long>((long long)c->num_sms * occ, std::max<long long>(1, max_blocks));
+    if (c->grid_limit > 0) grid = std::min(grid, c->grid_limit);   // experiment knob (paper's "network size")
     CUDA_TRY(cudaMemsetAsync(c->work_counter, 0, sizeof(int), c->stream));
     CUDA_TRY(rtb_launch_trace(P, p->flags & (RT_RENDER_COUNT | RT_RENDER_BRUTE_FORCE), grid, c->stream));
     return RT_OK;
