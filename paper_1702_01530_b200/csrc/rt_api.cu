@@ -82,6 +82,8 @@ struct rt_context {
     int leaf_max = 1;                // LBVH leaf collapse threshold (env RT_LEAF_MAX, <= 16)
     int treelet_passes = 3;          // SAH treelet restructuring passes (env RT_TREELETS)
     int grid_limit = 0;              // cap on trace CTAs (env RT_GRID_LIMIT; 0 = full machine)
+    void* arena = nullptr;           // BVH build scratch (grow-only)
+    size_t arena_bytes = 0;
     // refit state (rt_scene_update_vertices)
     int* d_prim_orig = nullptr;
     float* d_vertices = nullptr;
@@ -167,6 +169,7 @@ rt_status rt_destroy(rt_context* c) {
     if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
     free_scene(c);
     if (c->work_counter) cudaFree(c->work_counter);
+    if (c->arena) cudaFree(c->arena);
     if (c->scratch_counters) cudaFree(c->scratch_counters);
     if (c->ffma_out) cudaFree(c->ffma_out);
     if (c->order_ev) cudaEventDestroy(c->order_ev);
@@ -332,19 +335,19 @@ rt_status rt_scene_upload(rt_context* c, const rt_primitives* P, const rt_materi
     B.n_spheres = (int)S;
     B.n_planes = (int)PL;
     B.n_tris = (int)T;
-    std::vector<void*> scratch;
+    // BVH build scratch: carved from a grow-only per-context arena (no cudaMalloc/cudaFree per
+    // upload once it is large enough); sizes are summed in a first pass, pointers set in a second
+    size_t arena_off = 0;
+    bool measuring = true;
     auto salloc = [&](size_t bytes, void** p) -> rt_status {
         *p = nullptr;
         if (!bytes) return RT_OK;
-        cudaError_t e = cudaMalloc(p, bytes);
-        if (e != cudaSuccess) return fail(RT_ERR_OOM, "BVH scratch cudaMalloc(%zu): %s", bytes, cudaGetErrorString(e));
-        scratch.push_back(*p);
+        const size_t off = arena_off;
+        arena_off += (bytes + 255) & ~size_t(255);
+        if (!measuring) *p = static_cast<char*>(c->arena) + off;
         return RT_OK;
     };
-    auto free_scratch = [&]() {
-        for (void* p : scratch) cudaFree(p);
-        scratch.clear();
-    };
+    auto free_scratch = [&]() {};
     float4* d_prims = nullptr;
     float4* d_nodes = nullptr;
     const size_t Nn = N > 1 ? N - 1 : 0;
@@ -358,24 +361,41 @@ rt_status rt_scene_upload(rt_context* c, const rt_primitives* P, const rt_materi
     B.prim_orig = d_prim_orig;
     std::vector<int> level_start(66, 0);
     if (N > 0) {
-        if ((st = salloc(48 * (size_t)N, (void**)&B.prims_unsorted)) || (st = salloc(16 * (size_t)N, (void**)&B.aabb_lo)) ||
-            (st = salloc(16 * (size_t)N, (void**)&B.aabb_hi)) || (st = salloc(16 * (size_t)N, (void**)&B.centroid)) ||
-            (st = salloc(16 * (size_t)N, (void**)&B.leaf_lo)) || (st = salloc(16 * (size_t)N, (void**)&B.leaf_hi)) ||
-            (st = salloc(64, (void**)&B.bounds)) || (st = salloc(4 * (size_t)N, (void**)&B.keys[0])) ||
-            (st = salloc(4 * (size_t)N, (void**)&B.keys[1])) || (st = salloc(4 * (size_t)N, (void**)&B.vals[0])) ||
-            (st = salloc(4 * (size_t)N, (void**)&B.vals[1])) ||
-            (st = salloc(4 * rtb_sort_hist_entries(N), (void**)&B.hist)) || (st = salloc(4 * Nn, (void**)&B.left)) ||
-            (st = salloc(4 * Nn, (void**)&B.right)) || (st = salloc(4 * Nn, (void**)&B.parent_int)) ||
-            (st = salloc(4 * (size_t)N, (void**)&B.parent_leaf)) || (st = salloc(4 * Nn, (void**)&B.flags)) ||
-            (st = salloc(16 * Nn, (void**)&B.node_lo)) || (st = salloc(16 * Nn, (void**)&B.node_hi)) ||
-            (st = salloc(8 * Nn, (void**)&B.range)) || (st = salloc(16 * rtb::NODE_F4 * Nn, (void**)&B.nodes4)) ||
-            (st = salloc(8 * (size_t)N, (void**)&B.frontier[0])) || (st = salloc(8 * (size_t)N, (void**)&B.frontier[1])) ||
-            (st = salloc(16, (void**)&B.wide_counters)) || (st = salloc(4 * Nn, (void**)&B.cost)) ||
-            (st = salloc(4 * Nn, (void**)&B.count))) {
-            free_scratch();
-            free_scene(c);
-            return st;
+        auto alloc_all = [&]() -> rt_status {
+            rt_status st2 = RT_OK;
+            if ((st2 = salloc(48 * (size_t)N, (void**)&B.prims_unsorted)) || (st2 = salloc(16 * (size_t)N, (void**)&B.aabb_lo)) ||
+            (st2 = salloc(16 * (size_t)N, (void**)&B.aabb_hi)) || (st2 = salloc(16 * (size_t)N, (void**)&B.centroid)) ||
+            (st2 = salloc(16 * (size_t)N, (void**)&B.leaf_lo)) || (st2 = salloc(16 * (size_t)N, (void**)&B.leaf_hi)) ||
+            (st2 = salloc(64, (void**)&B.bounds)) || (st2 = salloc(4 * (size_t)N, (void**)&B.keys[0])) ||
+            (st2 = salloc(4 * (size_t)N, (void**)&B.keys[1])) || (st2 = salloc(4 * (size_t)N, (void**)&B.vals[0])) ||
+            (st2 = salloc(4 * (size_t)N, (void**)&B.vals[1])) ||
+            (st2 = salloc(4 * rtb_sort_hist_entries(N), (void**)&B.hist)) || (st2 = salloc(4 * Nn, (void**)&B.left)) ||
+            (st2 = salloc(4 * Nn, (void**)&B.right)) || (st2 = salloc(4 * Nn, (void**)&B.parent_int)) ||
+            (st2 = salloc(4 * (size_t)N, (void**)&B.parent_leaf)) || (st2 = salloc(4 * Nn, (void**)&B.flags)) ||
+            (st2 = salloc(16 * Nn, (void**)&B.node_lo)) || (st2 = salloc(16 * Nn, (void**)&B.node_hi)) ||
+            (st2 = salloc(8 * Nn, (void**)&B.range)) || (st2 = salloc(16 * rtb::NODE_F4 * Nn, (void**)&B.nodes4)) ||
+            (st2 = salloc(8 * (size_t)N, (void**)&B.frontier[0])) || (st2 = salloc(8 * (size_t)N, (void**)&B.frontier[1])) ||
+            (st2 = salloc(16, (void**)&B.wide_counters)) || (st2 = salloc(4 * Nn, (void**)&B.cost)) ||
+            (st2 = salloc(4 * Nn, (void**)&B.count))) {
+            return st2;
         }
+        return RT_OK;
+        };
+        alloc_all();                               // measure
+        if (arena_off > c->arena_bytes) {
+            if (c->arena) cudaFree(c->arena);
+            c->arena = nullptr;
+            c->arena_bytes = 0;
+            cudaError_t ea = cudaMalloc(&c->arena, arena_off);
+            if (ea != cudaSuccess) {
+                free_scene(c);
+                return fail(RT_ERR_OOM, "BVH scratch arena cudaMalloc(%zu): %s", arena_off, cudaGetErrorString(ea));
+            }
+            c->arena_bytes = arena_off;
+        }
+        measuring = false;
+        arena_off = 0;
+        alloc_all();                               // assign
         B.leaf_max = c->leaf_max;
         B.treelet_passes = c->treelet_passes;
         cudaError_t e = rtb_build_bvh(B, c->stream, &root, &n_nodes4, &depth4, level_start.data());
