@@ -12,6 +12,9 @@ namespace rtb {
 #ifndef RT_SHADOW_SORT
 #define RT_SHADOW_SORT 0  // 1: any-hit (shadow) rays also visit children near-to-far (measured slower)
 #endif
+#ifndef RT_FFMA2
+#define RT_FFMA2 1  // packed FP32 FMA (FFMA2) for the BVH4 slab planes
+#endif
 #ifndef RT_W8_FULL_SORT
 #define RT_W8_FULL_SORT 1
 #endif
@@ -123,10 +126,32 @@ __device__ __forceinline__ unsigned node4_hits(const float4* __restrict__ nodes,
     const float4 ny = __ldg(q + 2 + rb.sy), fy = __ldg(q + 3 - rb.sy);
     const float4 nz = __ldg(q + 4 + rb.sz), fz = __ldg(q + 5 - rb.sz);
     child = __ldg(reinterpret_cast<const int4*>(q + 6));
+#if RT_FFMA2
+    // packed FP32 FMA (sm_100 FFMA2): two children's plane distances per instruction
+    const float2 ix = make_float2(rb.idir.x, rb.idir.x), iy = make_float2(rb.idir.y, rb.idir.y);
+    const float2 iz = make_float2(rb.idir.z, rb.idir.z);
+    const float2 cnx = make_float2(rb.cn.x, rb.cn.x), cny = make_float2(rb.cn.y, rb.cn.y), cnz = make_float2(rb.cn.z, rb.cn.z);
+    const float2 cfx = make_float2(rb.cf.x, rb.cf.x), cfy = make_float2(rb.cf.y, rb.cf.y), cfz = make_float2(rb.cf.z, rb.cf.z);
+    const float2 a0 = __ffma2_rn(make_float2(nx.x, nx.y), ix, cnx), a1 = __ffma2_rn(make_float2(nx.z, nx.w), ix, cnx);
+    const float2 b0 = __ffma2_rn(make_float2(ny.x, ny.y), iy, cny), b1 = __ffma2_rn(make_float2(ny.z, ny.w), iy, cny);
+    const float2 c0 = __ffma2_rn(make_float2(nz.x, nz.y), iz, cnz), c1 = __ffma2_rn(make_float2(nz.z, nz.w), iz, cnz);
+    const float2 d0 = __ffma2_rn(make_float2(fx.x, fx.y), ix, cfx), d1 = __ffma2_rn(make_float2(fx.z, fx.w), ix, cfx);
+    const float2 e0 = __ffma2_rn(make_float2(fy.x, fy.y), iy, cfy), e1 = __ffma2_rn(make_float2(fy.z, fy.w), iy, cfy);
+    const float2 g0 = __ffma2_rn(make_float2(fz.x, fz.y), iz, cfz), g1 = __ffma2_rn(make_float2(fz.z, fz.w), iz, cfz);
+    const float tn0 = fmaxf(fmaxf(a0.x, b0.x), fmaxf(c0.x, 0.0f)), tf0 = fminf(fminf(d0.x, e0.x), fminf(g0.x, tmax));
+    const float tn1 = fmaxf(fmaxf(a0.y, b0.y), fmaxf(c0.y, 0.0f)), tf1 = fminf(fminf(d0.y, e0.y), fminf(g0.y, tmax));
+    const float tn2 = fmaxf(fmaxf(a1.x, b1.x), fmaxf(c1.x, 0.0f)), tf2 = fminf(fminf(d1.x, e1.x), fminf(g1.x, tmax));
+    const float tn3 = fmaxf(fmaxf(a1.y, b1.y), fmaxf(c1.y, 0.0f)), tf3 = fminf(fminf(d1.y, e1.y), fminf(g1.y, tmax));
+    tn[0] = tn0 <= tf0 ? tn0 : -1.0f;
+    tn[1] = tn1 <= tf1 ? tn1 : -1.0f;
+    tn[2] = tn2 <= tf2 ? tn2 : -1.0f;
+    tn[3] = tn3 <= tf3 ? tn3 : -1.0f;
+#else
     tn[0] = slab(rb, nx.x, fx.x, ny.x, fy.x, nz.x, fz.x, tmax);
     tn[1] = slab(rb, nx.y, fx.y, ny.y, fy.y, nz.y, fz.y, tmax);
     tn[2] = slab(rb, nx.z, fx.z, ny.z, fy.z, nz.z, fz.z, tmax);
     tn[3] = slab(rb, nx.w, fx.w, ny.w, fy.w, nz.w, fz.w, tmax);
+#endif
     unsigned m = 0;
     m |= tn[0] >= 0.0f ? 1u : 0u;                          // empty slots hold inverted boxes
     m |= tn[1] >= 0.0f ? 2u : 0u;
