@@ -573,11 +573,12 @@ uint32_t shard_count(const ShardGeom& g, uint32_t rank, uint32_t world) {
     return (int)rank < total ? (uint32_t)((total - (int)rank + (int)world - 1) / (int)world) : 0u;
 }
 
+// global tile id G: eye = G & 1, tile = G >> 1 (eyes interleaved)
 uint32_t shard_tile(const ShardGeom& g, uint32_t rank, uint32_t world, uint32_t lt) {
     if (g.mode == 0) return lt;
     if (g.mode == 1) {
         const int grp = (int)rank / g.half, j = (int)rank % g.half;
-        return (uint32_t)(grp * g.tiles_per_eye + j + (int)lt * g.half);
+        return (uint32_t)(2 * (j + (int)lt * g.half) + grp);
     }
     return rank + lt * world;
 }
@@ -785,8 +786,8 @@ rt_status rt_unpack_shards_host(const void* gathered, uint32_t W, uint32_t H, ui
         const uint32_t n = shard_count(g, r, world);
         for (uint32_t lt = 0; lt < n; ++lt) {
             const uint32_t gt = shard_tile(g, r, world, lt);
-            const int eye = (int)gt / g.tiles_per_eye;
-            const int t = (int)gt - eye * g.tiles_per_eye;
+            const int eye = (int)(gt & 1u);
+            const int t = (int)(gt >> 1);
             char* dst = static_cast<char*>(eye ? right : left);
             if (!dst) continue;
             for (int w = 0; w < 256; ++w) {

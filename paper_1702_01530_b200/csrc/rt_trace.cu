@@ -183,13 +183,13 @@ __global__ void k_unpack_shards(const void* __restrict__ gathered, UnpackParams 
         } else if (U.shard_mode == 1) {
             const int grp = rank / U.shard_half, j = rank % U.shard_half;
             if (j + lt * U.shard_half >= U.tiles_per_eye) continue;
-            g = grp * U.tiles_per_eye + j + lt * U.shard_half;
+            g = 2 * (j + lt * U.shard_half) + grp;
         } else {
             g = rank + lt * U.world;
             if (g >= 2 * U.tiles_per_eye) continue;
         }
-        const int eye = g / U.tiles_per_eye;
-        const int t = g - eye * U.tiles_per_eye;
+        const int eye = g & 1;
+        const int t = g >> 1;
         const int px = (t % U.tiles_x) * TILE + (within % TILE);
         const int py = (t / U.tiles_x) * TILE + (within / TILE);
         if (px >= U.W || py >= U.H) continue;

@@ -63,18 +63,20 @@ template <typename Params>
 __device__ __forceinline__ bool map_work(const Params& P, int k, int& eye, int& px, int& py) {
     const int lt = k >> 8;
     const int within = k & 255;
+    // global tile id G interleaves the eyes (eye = G & 1, tile = G >> 1): both eyes of a tile
+    // are traced back to back, which keeps their (nearly identical) BVH paths hot in L1/L2
     int g;
     if (P.shard_mode == 0) {
         g = lt;
     } else if (P.shard_mode == 1) {
         const int grp = P.shard_rank / P.shard_half;
         const int j = P.shard_rank % P.shard_half;
-        g = grp * P.tiles_per_eye + j + lt * P.shard_half;
+        g = 2 * (j + lt * P.shard_half) + grp;
     } else {
         g = P.shard_rank + lt * P.shard_world;
     }
-    eye = g / P.tiles_per_eye;
-    const int t = g - eye * P.tiles_per_eye;
+    eye = g & 1;
+    const int t = g >> 1;
     const int tx = t % P.tiles_x, ty = t / P.tiles_x;
     const int w = within >> 5, lane = within & 31;
     px = tx * TILE + (w & 1) * 8 + (lane & 7);

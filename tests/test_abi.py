@@ -63,8 +63,8 @@ def test_shard_map_exact_cover(W, H, world):
         counts.append(len(ids))
     assert np.all(owners >= 0)
     assert max(counts) - min(counts) <= 1 or T < world
-    if world == 2:
-        assert np.all(owners[:T] == 0) and np.all(owners[T:] == 1)
+    if world == 2:                                  # G = 2*tile + eye
+        assert np.all(owners[0::2] == 0) and np.all(owners[1::2] == 1)
     per = rt.rt_shard_bytes(W, H, world)
     assert per == max(counts) * 256 * 4
     assert rt.rt_shard_bytes(W, H, world, rt.RT_FORMAT_RGBA16F) == 2 * per
@@ -78,7 +78,7 @@ def synth_shards(W, H, world):
     buf = np.zeros((world, per), np.uint32)
     for r in range(world):
         for lt, g in enumerate(rt.rt_shard_tiles(W, H, r, world)):
-            eye, t = divmod(int(g), T)
+            eye, t = int(g) & 1, int(g) >> 1
             w = np.arange(256)
             px = (t % tx) * 16 + w % 16
             py = (t // tx) * 16 + w // 16
