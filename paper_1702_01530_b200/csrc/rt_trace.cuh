@@ -12,9 +12,6 @@ namespace rtb {
 #ifndef RT_SHADOW_SORT
 #define RT_SHADOW_SORT 0  // 1: any-hit (shadow) rays also visit children near-to-far (measured slower)
 #endif
-#ifndef RT_EAGER_LEAVES
-#define RT_EAGER_LEAVES 1  // intersect leaf children when their parent is visited
-#endif
 #ifndef RT_FFMA2
 #define RT_FFMA2 1  // packed FP32 FMA (FFMA2) for the BVH4 slab planes
 #endif
@@ -169,11 +166,6 @@ __device__ __forceinline__ void cswap(uint32_t& a, uint32_t& b) {
     const uint32_t lo = min(a, b), hi = max(a, b);
     a = lo;
     b = hi;
-}
-
-// bit c set when child c of the node is a leaf (negative code; empty slots are never hit)
-__device__ __forceinline__ unsigned leaf_mask(const int4& c) {
-    return (c.x < 0 ? 1u : 0u) | (c.y < 0 ? 2u : 0u) | (c.z < 0 ? 4u : 0u) | (c.w < 0 ? 8u : 0u);
 }
 
 // child code of slot i (0..3) with selects only (no branches)
@@ -352,20 +344,7 @@ __device__ __forceinline__ Hit closest_hit(const DevScene& S, float3 o, float3 d
 #else
             float tn[4];
             int4 ch;
-            unsigned m = node4_hits(S.nodes, node, rb, h.t, tn, ch);
-#if RT_EAGER_LEAVES
-            // leaf children the ray enters are intersected right away (uniform work for the warp,
-            // no stack round trip); the shrunken t_best then prunes the inner children
-            unsigned lm = m & leaf_mask(ch);
-            m &= ~lm;
-            while (lm) {
-                const int enc = ~pick4(ch, __ffs(lm) - 1);
-                lm &= lm - 1;
-                const int first = enc & ((1 << LEAF_SHIFT) - 1);
-                leaf_test(first, first + (enc >> LEAF_SHIFT));
-            }
-            m &= (tn[0] <= h.t ? 1u : 0u) | (tn[1] <= h.t ? 2u : 0u) | (tn[2] <= h.t ? 4u : 0u) | (tn[3] <= h.t ? 8u : 0u);
-#endif
+            const unsigned m = node4_hits(S.nodes, node, rb, h.t, tn, ch);
 #if RT_CLOSEST_SORT
             if (order_push(m, tn, ch, stk, sp, node)) continue;
 #else
@@ -414,17 +393,7 @@ __device__ __forceinline__ bool occluded(const DevScene& S, float3 o, float3 d, 
 #else
             float tn[4];
             int4 ch;
-            unsigned m = node4_hits(S.nodes, node, rb, dist, tn, ch);
-#if RT_EAGER_LEAVES
-            unsigned lm = m & leaf_mask(ch);
-            m &= ~lm;
-            while (lm) {
-                const int enc = ~pick4(ch, __ffs(lm) - 1);
-                lm &= lm - 1;
-                const int first = enc & ((1 << LEAF_SHIFT) - 1);
-                if (leaf_test(first, first + (enc >> LEAF_SHIFT))) return true;
-            }
-#endif
+            const unsigned m = node4_hits(S.nodes, node, rb, dist, tn, ch);
 #if RT_SHADOW_SORT
             if (order_push(m, tn, ch, stk, sp, node)) continue;
 #else
