@@ -54,6 +54,17 @@ def test_c2_small(R):
     full_parity(R, scenes.scene_c2().with_view(width=100, height=75), "C2 100x75 d5")
 
 
+def test_c2_full_baseline_size(R):
+    """BASELINE.json configs[1] at its full size (640x480 per eye, depth 5), every pixel."""
+    full_parity(R, scenes.scene_c2(), "C2 640x480 d5 full")
+
+
+def test_max_width(R):
+    """Maximum supported width (16384) on a short strip: sampled parity and ragged tiles."""
+    s = scenes.scene_c1().with_view(width=16384, height=5, max_depth=1)
+    sampled_parity(R, s, 300, 21, "C1 16384x5")
+
+
 def test_c3_small(R):
     full_parity(R, scenes.scene_c3().with_view(width=96, height=54), "C3 96x54 d4")
 
@@ -162,12 +173,13 @@ def test_rgba16f_pack(R):
 
 
 def test_rgba8_pack_formula(R):
-    """S:494 quantisation of the GPU's own radiance."""
+    """S:494 quantisation of the GPU's own radiance, bit-exact: the integer decision is replayed in
+    the kernel's precision (fmaf(c, 255, 0.5) rounded once to FP32, then floor)."""
     s = scenes.scene_c2().with_view(width=48, height=32)
     g = gpu_render(R, s)
-    exp = np.floor(np.clip(g["radiance"][..., :3].astype(np.float64), 0, 1) * 255 + 0.5)
-    assert np.abs(g["fb"][..., :3] - exp).max() <= 1      # fp32 fma rounding at .5 boundaries
-    assert (g["fb"][..., :3] == exp).mean() > 0.999
+    c = np.clip(g["radiance"][..., :3], np.float32(0), np.float32(1)).astype(np.float32)
+    fma = (c.astype(np.float64) * 255.0 + 0.5).astype(np.float32)    # exact product+sum, one FP32 rounding
+    np.testing.assert_array_equal(g["fb"][..., :3], np.floor(fma).astype(np.uint8))
     assert np.all(g["fb"][..., 3] == 255)
 
 
