@@ -59,7 +59,9 @@ __device__ __forceinline__ float3 trace_pixel(const TraceParams& P, float3 o, fl
                 const float4 a = __ldg(&S.prims[3 * h.slot]);
                 const float4 b = __ldg(&S.prims[3 * h.slot + 1]);
                 mat = __float_as_int(b.w);
-                if (h.gid < S.n_spheres) ng = (p - xyz(a)) * (1.0f / b.x);
+                // (p - c) / r in FP32 is off unit length by the hit point's rounding (~1e-5 relative),
+                // which a Phong exponent of 256 amplifies to ~1e-2: renormalise like triangles
+                if (h.gid < S.n_spheres) ng = normalize(p - xyz(a));
                 else ng = normalize(cross(xyz(b), xyz(__ldg(&S.prims[3 * h.slot + 2]))));
             }
             const bool front = dot(d, ng) < 0.0f;
