@@ -17,7 +17,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "liboracle.so")
 
-FRAG_COMPETE, FRAG_BOUNDARY, FRAG_GRAZE, FRAG_RANGE, FRAG_SHADE, FRAG_SHADOW = 1, 2, 4, 8, 16, 32
+FRAG_COMPETE, FRAG_BOUNDARY, FRAG_GRAZE, FRAG_RANGE, FRAG_SHADE, FRAG_SHADOW, FRAG_UNSTABLE = 1, 2, 4, 8, 16, 32, 64
 ID_FRAGILE_MASK = FRAG_COMPETE | FRAG_BOUNDARY | FRAG_GRAZE | FRAG_RANGE
 
 
@@ -43,10 +43,10 @@ class OracleCam(C.Structure):
 
 class OracleEps(C.Structure):
     _fields_ = [("eps_t", C.c_double), ("eps_sphere", C.c_double), ("eps_edge", C.c_double),
-                ("eps_abs", C.c_double)]
+                ("eps_abs", C.c_double), ("perturb", C.c_double), ("perturb_tol", C.c_double)]
 
 
-DEFAULT_EPS = dict(eps_t=1e-4, eps_sphere=1e-4, eps_edge=1e-5, eps_abs=1e-5)
+DEFAULT_EPS = dict(eps_t=1e-4, eps_sphere=1e-4, eps_edge=1e-5, eps_abs=1e-5, perturb=1e-6, perturb_tol=1e-3)
 
 _lib = None
 

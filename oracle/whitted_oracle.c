@@ -73,6 +73,8 @@ typedef struct {
     double eps_sphere; /* angular band around sphere silhouettes               (1e-4) */
     double eps_edge;   /* angular band around triangle edges                   (1e-5) */
     double eps_abs;    /* absolute band (x (1+|o|)) around t_min               (1e-5) */
+    double perturb;    /* F7: primary-ray perturbation angle (rad), 0 = off    (1e-6) */
+    double perturb_tol;/* F7: radiance change that marks the pixel unstable    (1e-3) */
 } oracle_eps;
 
 enum {
@@ -81,7 +83,9 @@ enum {
     FRAG_GRAZE = 4,      /* F4: |n.d| <= eps_t at the hit                                   */
     FRAG_RANGE = 8,      /* F5: a candidate t near t_min or near the shadow segment end     */
     FRAG_SHADE = 16,     /* F6: n.l gate or TIR decision within eps_t                        */
-    FRAG_SHADOW = 32     /* a shadow ray whose visibility is not robustly decided           */
+    FRAG_SHADOW = 32,    /* a shadow ray whose visibility is not robustly decided           */
+    FRAG_UNSTABLE = 64   /* F7: radiance moves > perturb_tol when the primary ray turns by   */
+                         /*     perturb rad (error amplified along the ray tree)            */
 };
 
 typedef struct {
@@ -571,6 +575,29 @@ int oracle_render(const oracle_scene* sc, const oracle_cam* cam, int32_t max_dep
         unsigned pf = 0;
         double mg = INFINITY;
         v3 c = trace(&cx, ld3(o), ld3(d), max_depth, 1, &id, &pf, &mg);
+        if (eps && eps->perturb > 0.0) {
+            /* F7 (reading 22): curved mirrors and glass amplify angular error at every
+             * bounce (~2D/r), so a deep ray can cross a silhouette that the unperturbed tree misses
+             * by more than the band.  Re-trace with the primary ray turned by `perturb` rad in four
+             * directions; a clamped radiance change above perturb_tol marks the pixel unstable. */
+            v3 dv = ld3(d);
+            v3 a = fabs(dv.y) < 0.9 ? mk(0, 1, 0) : mk(1, 0, 0);
+            v3 u = nrm(cross(dv, a)), w = cross(dv, u);
+            v3 dirs[4] = {u, scl(u, -1.0), w, scl(w, -1.0)};
+            for (int q = 0; q < 4 && !(cx.flags & FRAG_UNSTABLE); ++q) {
+                trace_ctx cq;
+                memset(&cq, 0, sizeof cq);
+                cq.sc = sc;
+                v3 dq = nrm(add(dv, scl(dirs[q], eps->perturb)));
+                v3 cc = trace(&cq, ld3(o), dq, max_depth, 0, NULL, NULL, NULL);
+                double dc[3] = {cc.x, cc.y, cc.z}, c0[3] = {c.x, c.y, c.z};
+                for (int k = 0; k < 3; ++k) {
+                    double x0 = c0[k] < 0 ? 0 : (c0[k] > 1 ? 1 : c0[k]);
+                    double x1 = dc[k] < 0 ? 0 : (dc[k] > 1 ? 1 : dc[k]);
+                    if (fabs(x1 - x0) > eps->perturb_tol) cx.flags |= FRAG_UNSTABLE;
+                }
+            }
+        }
         if (radiance) { radiance[3 * k] = c.x; radiance[3 * k + 1] = c.y; radiance[3 * k + 2] = c.z; }
         if (rgba8) {
             rgba8[4 * k] = q8(c.x); rgba8[4 * k + 1] = q8(c.y); rgba8[4 * k + 2] = q8(c.z);

@@ -10,7 +10,7 @@ import math
 import numpy as np
 import pytest
 
-from oracle.oracle import FRAG_BOUNDARY, Oracle, half_bits
+from oracle.oracle import FRAG_BOUNDARY, FRAG_UNSTABLE, Oracle, half_bits
 from paper_1702_01530_b200 import scenes
 from paper_1702_01530_b200.scenes import Rig, Scene, material
 
@@ -507,6 +507,53 @@ def test_fragility_flags():
     assert out["pflags"][0, 2, 2] == 0 and out["id"][0, 2, 2] == -1
     out = Oracle(mk_scene(spheres=[[0.999, 0, 0, 1]], rig=rig, w=W, h=H)).render()
     assert out["pflags"][0, 2, 2] == 0 and out["id"][0, 2, 2] == 0
+
+
+def _perturbed_dirs(d, delta):
+    a = np.array([0.0, 1, 0]) if abs(d[1]) < 0.9 else np.array([1.0, 0, 0])
+    u = np.cross(d, a)
+    u /= np.linalg.norm(u)
+    w = np.cross(d, u)
+    return [(d + delta * q) / np.linalg.norm(d + delta * q) for q in (u, -u, w, -w)]
+
+
+def test_unstable_flag_smooth_scene_never_fires():
+    """R#22 (F7): on a lone diffuse sphere the radiance is a smooth function of the ray direction
+    away from the silhouette (|dL/dtheta| * 1e-6 << 1e-3), so F7 may only fire on pixels
+    that F1-F6 already flag (rim / terminator)."""
+    rig = Rig(np.array([0.0, 0, 5]), np.zeros(3), np.array([0.0, 1, 0]), 40.0, 0.2, 5.0)
+    sc = mk_scene(spheres=[[0, 0, 0, 1]], mats=[material((0.8, 0.5, 0.3), 0.5, 20)], lights=[[3, 3, 5, 1, 1, 1]],
+                  ambient=0.1, rig=rig, w=48, h=40, depth=2)
+    out = Oracle(sc).render()
+    unstable = (out["tflags"] & FRAG_UNSTABLE) != 0
+    assert not np.any(unstable & (out["tflags"] == FRAG_UNSTABLE))
+    # F7 off: never set
+    out0 = Oracle(sc).render(eps=dict(perturb=0.0))
+    assert not np.any(out0["tflags"] & FRAG_UNSTABLE)
+
+
+def test_unstable_flag_matches_definition():
+    """R#22 (F7): in C2 (mirror + glass spheres over a reflective floor, Phong n = 128/256) angular
+    error grows at every curved bounce, so some pixels that no structural band (F1-F6) catches
+    are unstable.  Check the flag against its definition by tracing the four perturbed primaries
+    independently (numpy basis, single-ray entry point): flagged <=> some clamped channel moves
+    by more than 1e-3."""
+    sc = scenes.scene_c2().with_view(width=160, height=120)
+    o = Oracle(sc)
+    out = o.render()
+    tf = out["tflags"]
+    only7 = tf == FRAG_UNSTABLE
+    assert only7.sum() >= 10, "expected amplification-only unstable pixels"
+    cam = o.camera()
+    rng = np.random.default_rng(7)
+    cand = [tuple(p) for p in np.argwhere(only7)[:20]]
+    cand += [(int(rng.integers(2)), int(rng.integers(120)), int(rng.integers(160))) for _ in range(20)]
+    for eye, py, px in cand:
+        org, d = o.primary_ray(cam, int(eye), int(px), int(py))
+        base = np.clip(out["radiance"][eye, py, px], 0, 1)
+        moved = max(np.abs(np.clip(o.trace_ray(org, dq, sc.max_depth)[0], 0, 1) - base).max()
+                    for dq in _perturbed_dirs(d, 1e-6))
+        assert bool(tf[eye, py, px] & FRAG_UNSTABLE) == (moved > 1e-3), (eye, py, px, moved)
 
 
 def test_scene_generators(golden):
