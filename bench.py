@@ -120,6 +120,17 @@ def oracle_sample(scene, n_per_eye, seed, threads):
     return int(out["counts"].sum()), dt, len(pix)
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def cpu_baseline(scene, target_s=15.0, seed=99):
     """The oracle as it stands, timed on this host's cores on a bounded pixel sample."""
     threads = os.cpu_count() or 1
@@ -127,7 +138,12 @@ def cpu_baseline(scene, target_s=15.0, seed=99):
     per_px = dt / n
     n_eye = int(max(8, min(4096, target_s / max(per_px, 1e-9) / 2)))
     rays, dt, n = oracle_sample(scene, n_eye, seed + 1, threads)
+    # single-core rate on a smaller sample (SURVEY §8(d) "also report 1-core numbers")
+    n1 = int(max(2, min(n_eye, target_s / 3 / max(per_px * threads, 1e-9) / 2)))
+    r1, d1, _ = oracle_sample(scene, n1, seed + 2, 1)
     return {"value": rays / dt / 1e6, "unit": UNIT, "cores": threads, "kind": "oracle",
+            "cpu_model": cpu_model(), "one_core_value": r1 / d1 / 1e6,
+            "one_core_sample": f"{2 * n1} seeded pixels, 1 thread, {d1:.1f} s",
             "sample": f"{n} seeded pixels ({n // 2} per eye) of {scene.name} {scene.width}x{scene.height} stereo, "
                       f"depth {scene.max_depth}: {rays} rays in {dt:.1f} s (double precision, brute force, "
                       f"OpenMP {threads} threads)",
@@ -260,10 +276,11 @@ def run_ours(args, scene):
     clocks = clk.stop()
     step_ms = np.array([ev_s[k].elapsed_time(ev_e[k]) for k in range(args.steps)])
     kern_ms = np.array([ev_s[k].elapsed_time(ev_k[k]) for k in range(args.steps)])
-    t = torch.tensor([step_ms.sum(), kern_ms.mean()], dtype=torch.float64, device=dev)
+    t = torch.tensor([step_ms.sum(), kern_ms.mean(), np.median(step_ms), step_ms.min()], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t[0])
+    med_ms, best_ms = float(t[2]), float(t[3])
     ms_per_step = total_ms / args.steps
 
     # ---- end-to-end through the public C ABI with host buffers (camera in, frame out)
@@ -292,6 +309,8 @@ def run_ours(args, scene):
                        "l2": "flushed (256 MiB write) between timed steps; scene+BVH "
                              f"{info['device_bytes'] / 1e6:.0f} MB"},
             "stereo_fps": 1e3 / ms_per_step,
+            "ms_median": med_ms, "ms_best": best_ms,
+            "mrays_median": rays_total / (med_ms * 1e-3) / 1e6, "mrays_best": rays_total / (best_ms * 1e-3) / 1e6,
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": "k_trace_stereo", "kernel_ms": float(kern_ms.mean()),
@@ -332,7 +351,24 @@ def run_e2e(args, R, scene, rank, world, frame, fb, dev, rays_total):
     W, H, D = scene.width, scene.height, scene.max_depth
     nbytes = 2 * H * W * 4
     hosts = [rt.rt_host_alloc(nbytes) for _ in range(2)] if rank == 0 else []
-    rig = scene.rig
+    # C5: sustained camera orbit, frame k uses orbit camera k mod 60; the rays of
+    # every orbit frame are counted up front (instrumented pass, untimed)
+    orbit = scene.name.startswith("C5")
+    n_rig = 60 if orbit else 1
+    rigs = [scenes.c5_rig(k) for k in range(n_rig)] if orbit else [scene.rig]
+    rays_of = [rays_total] * n_rig
+    if orbit:
+        for k, rg in enumerate(rigs):
+            R.set_camera(rg)
+            out = R.render(W, H, D, fb=False, count=True, shard=(rank, world))
+            torch.cuda.synchronize()
+            c = R.counters_dict(out["counters"])
+            v = torch.tensor([c["primary"] + c["reflection"] + c["refraction"] + c["shadow"]], dtype=torch.float64,
+                             device=dev)
+            if world > 1:
+                import torch.distributed as dist
+                dist.all_reduce(v)
+            rays_of[k] = int(v.item())
     pending = [None, None]
     fb2 = R.alloc_fb(W, H)
     fbs = [fb, fb2]
@@ -349,6 +385,7 @@ def run_e2e(args, R, scene, rank, world, frame, fb, dev, rays_total):
             pending[slot] = None
         if world > 1:
             dist.barrier()                                     # ... before any rank writes that slot again
+        rig = rigs[k % n_rig]
         rt.rt_set_stereo_camera(R.ctx, rig.eye, rig.look_at, rig.up, rig.vfov_deg, rig.interocular,
                                 rig.convergence)
         dst = fbs[slot]
@@ -413,7 +450,10 @@ def run_e2e(args, R, scene, rank, world, frame, fb, dev, rays_total):
             rt.rt_host_free(h)
     for f in frames[1:]:
         f.close()
-    return {"value": rays_total / (dt / args.steps) / 1e6, "unit": UNIT,
+    rays_timed = sum(rays_of[k % n_rig] for k in range(args.steps))
+    return {"value": rays_timed / dt / 1e6, "unit": UNIT,
+            "camera": "C5 orbit: frame k uses orbit camera k mod 60 (rays counted per orbit frame)" if orbit
+            else "fixed (the config's rig)",
             "h2d_bytes_per_step": 76, "d2h_bytes_per_step": nbytes if rank == 0 else 0,
             "ms_per_step": dt / args.steps * 1e3, "stereo_fps": args.steps / dt, "download_verified": ok,
             "stages": stages,

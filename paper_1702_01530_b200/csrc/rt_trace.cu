@@ -30,7 +30,7 @@ namespace rtb {
 // recursive definition c = local + kt*T(refr) + kr_eff*T(refl) (reading 17).
 template <bool COUNT, bool BRUTE>
 __device__ __forceinline__ float3 trace_pixel(const TraceParams& P, float3 o, float3 d, int& prim_id, TravStack& stk,
-                                              Counters<COUNT>& cnt) {
+                                              Counters<COUNT>& cnt, int* occ_hint) {
     const DevScene& S = P.sc;
     float4 st_a[MAX_DEPTH], st_b[MAX_DEPTH];   // refraction children: (o, w) (d, depth)
     int sp = 0;
@@ -83,7 +83,8 @@ __device__ __forceinline__ float3 trace_pixel(const TraceParams& P, float3 o, fl
                 const float3 sv = Lp - os;
                 const float dist = sqrtf(dot(sv, sv));
                 cnt.add(CNT_SHADOW);
-                if (!occluded<COUNT, BRUTE>(S, os, sv * (1.0f / dist), dist, stk, cnt)) c = c + term;   // reading 3
+                int* hint = (RT_OCC_CACHE && j < RT_OCC_LIGHTS) ? occ_hint + j * RT_BLOCK : nullptr;
+                if (!occluded<COUNT, BRUTE>(S, os, sv * (1.0f / dist), dist, stk, cnt, hint)) c = c + term;   // reading 3
             }
             col = fma3(c, w, col);
             if (depth > 0) {
@@ -136,7 +137,14 @@ __global__ void __launch_bounds__(RT_BLOCK, RT_MINB) k_trace_stereo(const TraceP
     cnt.zero();
     const int lane = threadIdx.x & 31;
     int lstack[STACK_CAP > RT_SMEM_STACK ? STACK_CAP - RT_SMEM_STACK : 1];
+#if RT_SMEM_PTX
+    TravStack stk{(uint32_t)__cvta_generic_to_shared(s_stack + threadIdx.x), lstack};
+#else
     TravStack stk{s_stack + threadIdx.x, lstack};
+#endif
+    __shared__ int s_occ[RT_OCC_LIGHTS * RT_BLOCK];  // [light][thread] last-occluder hints
+#pragma unroll
+    for (int j = 0; j < RT_OCC_LIGHTS; ++j) s_occ[j * RT_BLOCK + threadIdx.x] = -1;
 #if RT_WORK_MODE == 2
     // CTA tile ring: the 8 warps of a CTA share 16x16 tiles (one 8x4 block each) so an SM's L1
     // serves neighbouring rays; tiles come from the global counter, block claims from shared memory
@@ -192,7 +200,7 @@ __global__ void __launch_bounds__(RT_BLOCK, RT_MINB) k_trace_stereo(const TraceP
             const float sy = fmaf(-2.0f * (py + 0.5f), 1.0f / P.H, 1.0f) * P.cam.th;
             const float3 d = normalize(P.cam.f + P.cam.r * (sx + P.cam.sigma[eye]) + P.cam.u * sy);
             int pid = -1;
-            const float3 c = trace_pixel<COUNT, BRUTE>(P, P.cam.eye[eye], d, pid, stk, cnt);
+            const float3 c = trace_pixel<COUNT, BRUTE>(P, P.cam.eye[eye], d, pid, stk, cnt, s_occ + threadIdx.x);
             const long long pix = ((long long)eye * P.H + py) * P.W + px;
             if (P.fb[eye]) store_px(P.fb[eye], P.fb_fmt[eye], P.fb_pitch[eye], px, py, c);
             if (P.prim_id) P.prim_id[pix] = pid;

@@ -28,17 +28,49 @@ namespace rtb {
 #define RT_SMEM_STACK 16  // traversal-stack entries kept in shared memory; deeper ones in local
 #endif
 
+#ifndef RT_SMEM_PTX
+#define RT_SMEM_PTX 1     // shared stack addressed with a 32-bit shared-window address held in a register
+#endif
+#ifndef RT_OCC_CACHE
+#define RT_OCC_CACHE 1    // per-thread, per-light last-occluder hint for shadow rays
+#endif
+#define RT_OCC_LIGHTS 4   // lights with an occluder hint slot (light j uses slot j; others none)
+
 // Per-thread traversal stack: the first RT_SMEM_STACK entries live in shared memory laid out
 // [entry][thread] (conflict-free), deeper entries in thread-local memory (L1-cached).  Keeping the
 // shared part short leaves most of the 228 KB L1/shared array to cache BVH nodes.
 struct TravStack {
+#if RT_SMEM_PTX
+    // 32-bit shared-window address of this thread's entry 0: STS/LDS take it directly instead of
+    // rebuilding the generic->shared conversion (S2R CgaCtaId + LEA) at every push and pop
+    uint32_t sa;
+#else
     int* s;   // shared: s[i * RT_BLOCK]
+#endif
     int* l;   // local:  l[i - RT_SMEM_STACK]
     __device__ __forceinline__ void set(int i, int v) {
-        if (i < RT_SMEM_STACK) s[i * RT_BLOCK] = v;
-        else l[i - RT_SMEM_STACK] = v;
+        if (i < RT_SMEM_STACK) {
+#if RT_SMEM_PTX
+            asm volatile("st.shared.b32 [%0], %1;" ::"r"(sa + (uint32_t)i * (RT_BLOCK * 4u)), "r"(v));
+#else
+            s[i * RT_BLOCK] = v;
+#endif
+        } else {
+            l[i - RT_SMEM_STACK] = v;
+        }
     }
-    __device__ __forceinline__ int get(int i) const { return i < RT_SMEM_STACK ? s[i * RT_BLOCK] : l[i - RT_SMEM_STACK]; }
+    __device__ __forceinline__ int get(int i) const {
+        if (i < RT_SMEM_STACK) {
+#if RT_SMEM_PTX
+            int v;
+            asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(sa + (uint32_t)i * (RT_BLOCK * 4u)));
+            return v;
+#else
+            return s[i * RT_BLOCK];
+#endif
+        }
+        return l[i - RT_SMEM_STACK];
+    }
 };
 
 template <bool COUNT>
@@ -362,20 +394,38 @@ __device__ __forceinline__ Hit closest_hit(const DevScene& S, float3 o, float3 d
     }
 }
 
-// Any hit with t_min < t < dist (binary visibility, reading 4); children near-to-far.
+// Any hit with t_min < t < dist (binary visibility, reading 4).  `hint` (shared memory, may be
+// null) holds the BVH slot of this thread's last occluder for the same light: it is tested first
+// and, if it blocks the segment, the answer is already exact (visibility is a boolean, so which
+// occluder proves it does not matter); otherwise the traversal runs and records its occluder.
 template <bool COUNT, bool BRUTE>
-__device__ __forceinline__ bool occluded(const DevScene& S, float3 o, float3 d, float dist, TravStack& stk, Counters<COUNT>& cnt) {
+__device__ __forceinline__ bool occluded(const DevScene& S, float3 o, float3 d, float dist, TravStack& stk, Counters<COUNT>& cnt,
+                                         int* hint = nullptr) {
     for (int i = 0; i < S.n_planes; ++i) {
         cnt.add(CNT_PLANE_TESTS);
         float t;
         if (plane_intersect(o, d, __ldg(&S.planes[i]), t) && t > T_MIN && t < dist) return true;
     }
     if (S.n_bvh == 0) return false;
+    if (BRUTE) hint = nullptr;
+#if RT_OCC_CACHE
+    if (hint) {
+        const int k = *hint;
+        float t;
+        int gid;
+        if (k >= 0 && prim_t<COUNT>(S, k, o, d, t, gid, cnt) && t < dist) return true;
+    }
+#endif
     auto leaf_test = [&](int first, int last) -> bool {
         for (int k = first; k <= last; ++k) {
             float t;
             int gid;
-            if (prim_t<COUNT>(S, k, o, d, t, gid, cnt) && t < dist) return true;
+            if (prim_t<COUNT>(S, k, o, d, t, gid, cnt) && t < dist) {
+#if RT_OCC_CACHE
+                if (hint) *hint = k;
+#endif
+                return true;
+            }
         }
         return false;
     };

@@ -632,3 +632,26 @@ def test_compose_spec_examples(golden):
     Z[2, 3, 0] ^= 0xFF
     d = np.any(compose(Z, X, "anaglyph") != compose(X, X, "anaglyph"), -1)
     assert d.sum() == 1 and d[2, 3]
+
+
+@pytest.mark.parametrize("cfg,n,depth", [("C1", 100, None), ("C2", 60, None), ("paper3", 40, 3)])
+def test_double_precision_adequacy_mpmath(cfg, n, depth):
+    """SURVEY §8(c) 'double-precision adequacy': the oracle (double) equals an independent 40-digit
+    mpmath evaluation of the same definition (tests/mp_whitted.py: Cramer-rule triangles, written
+    from §8(c) steps 1-5) within 1e-9 on seeded non-fragile pixels."""
+    from tests import mp_whitted
+    sc = scenes.paper_scene(3) if cfg == "paper3" else scenes.make_scene(cfg)
+    if depth is not None:
+        sc = sc.with_view(max_depth=depth)
+    pix = scenes.sample_pixels(sc.width, sc.height, n // 2, seed=11)
+    out = Oracle(sc).render(pixels=pix)
+    ms = mp_whitted.MpScene(sc)
+    checked = 0
+    for k, (eye, px, py) in enumerate(pix):
+        if out["tflags"][k]:
+            continue
+        o, d = mp_whitted.primary_ray(sc.rig, sc.width, sc.height, int(eye), int(px), int(py))
+        ref = np.array([float(x) for x in ms.trace(o, d, sc.max_depth)])
+        np.testing.assert_allclose(out["radiance"][k], ref, atol=1e-9, rtol=0, err_msg=str((eye, px, py)))
+        checked += 1
+    assert checked >= 0.6 * len(pix)
