@@ -496,19 +496,15 @@ __global__ void k_wide(BuildBuffers B, const int2* __restrict__ fin, int n_in, i
             ch[best] = make_child(B.left[code], B);
             ch[n++] = make_child(B.right[code], B);
         }
-        float* o = reinterpret_cast<float*>(B.nodes4 + NODE_F4 * (size_t)dst);
-        int* oc = reinterpret_cast<int*>(o) + 6 * BVH_W;
+        float3 lo[BVH_W], hi[BVH_W];
+        int oc[BVH_W];
         for (int c = 0; c < BVH_W; ++c) {
             if (c >= n) {
-                // inverted box (lo = +1e30, hi = -1e30): every slab test rejects it, so the
-                // traversal needs no per-slot validity test
-                for (int k = 0; k < 3; ++k) { o[(2 * k) * BVH_W + c] = 1e30f; o[(2 * k + 1) * BVH_W + c] = -1e30f; }
                 oc[c] = WIDE_EMPTY;
                 continue;
             }
-            o[0 * BVH_W + c] = ch[c].lo.x; o[1 * BVH_W + c] = ch[c].hi.x;
-            o[2 * BVH_W + c] = ch[c].lo.y; o[3 * BVH_W + c] = ch[c].hi.y;
-            o[4 * BVH_W + c] = ch[c].lo.z; o[5 * BVH_W + c] = ch[c].hi.z;
+            lo[c] = f3(ch[c].lo.x, ch[c].lo.y, ch[c].lo.z);
+            hi[c] = f3(ch[c].hi.x, ch[c].hi.y, ch[c].hi.z);
             const int code = ch[c].code;
             if (code < 0) {
                 oc[c] = code;                                       // BVH2 leaf: ~slot (count 1)
@@ -522,6 +518,7 @@ __global__ void k_wide(BuildBuffers B, const int2* __restrict__ fin, int n_in, i
                 oc[c] = slot;
             }
         }
+        node_write(B.nodes4 + NODE_F4 * (size_t)dst, lo, hi, oc);
     }
 }
 
@@ -580,11 +577,13 @@ __global__ void k_refit4(float4* nodes, int begin, int end, const int* __restric
                          const float4* __restrict__ spheres, const uint32_t* __restrict__ tri_idx,
                          const float* __restrict__ vtx) {
     for (int i = begin + blockIdx.x * blockDim.x + threadIdx.x; i < end; i += gridDim.x * blockDim.x) {
-        float* q = reinterpret_cast<float*>(nodes + NODE_F4 * (size_t)i);
-        const int* qc = reinterpret_cast<const int*>(q) + 6 * BVH_W;
+        float4* q = nodes + NODE_F4 * (size_t)i;
+        float3 L[BVH_W], Hh[BVH_W];
+        int codes[BVH_W];
         for (int c = 0; c < BVH_W; ++c) {
             float3 l = f3(1e30f, 1e30f, 1e30f), h = f3(-1e30f, -1e30f, -1e30f);
-            const int code = qc[c];
+            const int code = node_code(q, c);
+            codes[c] = code;
             if (code == WIDE_EMPTY) {
             } else if (code < 0) {
                 const int enc = ~code;
@@ -596,16 +595,18 @@ __global__ void k_refit4(float4* nodes, int begin, int end, const int* __restric
                     h = f3(fmaxf(h.x, ph.x), fmaxf(h.y, ph.y), fmaxf(h.z, ph.z));
                 }
             } else {
-                const float* r = reinterpret_cast<const float*>(nodes + NODE_F4 * (size_t)code);
+                const float4* r = nodes + NODE_F4 * (size_t)code;
                 for (int k = 0; k < BVH_W; ++k) {
-                    l = f3(fminf(l.x, r[0 * BVH_W + k]), fminf(l.y, r[2 * BVH_W + k]), fminf(l.z, r[4 * BVH_W + k]));
-                    h = f3(fmaxf(h.x, r[1 * BVH_W + k]), fmaxf(h.y, r[3 * BVH_W + k]), fmaxf(h.z, r[5 * BVH_W + k]));
+                    float3 bl, bh;
+                    node_child_box(r, k, bl, bh);
+                    l = f3(fminf(l.x, bl.x), fminf(l.y, bl.y), fminf(l.z, bl.z));
+                    h = f3(fmaxf(h.x, bh.x), fmaxf(h.y, bh.y), fmaxf(h.z, bh.z));
                 }
             }
-            q[0 * BVH_W + c] = l.x; q[1 * BVH_W + c] = h.x;
-            q[2 * BVH_W + c] = l.y; q[3 * BVH_W + c] = h.y;
-            q[4 * BVH_W + c] = l.z; q[5 * BVH_W + c] = h.z;
+            L[c] = l;
+            Hh[c] = h;
         }
+        node_write(q, L, Hh, codes);
     }
 }
 

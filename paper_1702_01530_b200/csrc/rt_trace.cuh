@@ -155,11 +155,66 @@ __device__ __forceinline__ bool prim_t(const DevScene& S, int k, float3 o, float
 // Returns the hit mask; tn[c] = entry distance of hit children.
 __device__ __forceinline__ unsigned node4_hits(const float4* __restrict__ nodes, int node, const RayBox& rb, float tmax,
                                                float tn[4], int4& child) {
-    const float4* q = nodes + 7 * node;
+#if RT_NODE_F16
+    const float4* q = nodes + (size_t)NODE_F4 * node;
+    const float4 a = __ldg(q);
+    child = __ldg(reinterpret_cast<const int4*>(q + 1));
+    const uint4 X = __ldg(reinterpret_cast<const uint4*>(q + 2));
+    const uint4 Y = __ldg(reinterpret_cast<const uint4*>(q + 3));
+    const uint4 Z = __ldg(reinterpret_cast<const uint4*>(q + 4));
+    const uint32_t Sw = __float_as_uint(a.w);
+    // near / far binary16 pairs by the ray's direction signs
+    const uint32_t nx0 = rb.sx ? X.z : X.x, nx1 = rb.sx ? X.w : X.y, fx0 = rb.sx ? X.x : X.z, fx1 = rb.sx ? X.y : X.w;
+    const uint32_t ny0 = rb.sy ? Y.z : Y.x, ny1 = rb.sy ? Y.w : Y.y, fy0 = rb.sy ? Y.x : Y.z, fy1 = rb.sy ? Y.y : Y.w;
+    const uint32_t nz0 = rb.sz ? Z.z : Z.x, nz1 = rb.sz ? Z.w : Z.y, fz0 = rb.sz ? Z.x : Z.z, fz1 = rb.sz ? Z.y : Z.w;
+    // plane - shifted origin = h * S + (O - origin): one mixed-precision FMA (binary16 h, S;
+    // FP32 addend), rounded once; then times idir (packed FMUL2)
+    auto dec = [&](uint32_t w, float k) {
+        float2 r;
+        asm("{\n\t.reg .f16 l, h, s, t;\n\tmov.b32 {l, h}, %2;\n\tmov.b32 {s, t}, %3;\n\t"
+            "fma.rn.f32.f16 %0, l, s, %4;\n\tfma.rn.f32.f16 %1, h, s, %4;\n\t}"
+            : "=f"(r.x), "=f"(r.y) : "r"(w), "r"(Sw), "f"(k));
+        return r;
+    };
+    const float2 ix = make_float2(rb.idir.x, rb.idir.x), iy = make_float2(rb.idir.y, rb.idir.y);
+    const float2 iz = make_float2(rb.idir.z, rb.idir.z);
+    const float knx = a.x - rb.cn.x, kny = a.y - rb.cn.y, knz = a.z - rb.cn.z;
+    const float kfx = a.x - rb.cf.x, kfy = a.y - rb.cf.y, kfz = a.z - rb.cf.z;
+    const float2 a0 = __fmul2_rn(dec(nx0, knx), ix), a1 = __fmul2_rn(dec(nx1, knx), ix);
+    const float2 b0 = __fmul2_rn(dec(ny0, kny), iy), b1 = __fmul2_rn(dec(ny1, kny), iy);
+    const float2 c0 = __fmul2_rn(dec(nz0, knz), iz), c1 = __fmul2_rn(dec(nz1, knz), iz);
+    const float2 d0 = __fmul2_rn(dec(fx0, kfx), ix), d1 = __fmul2_rn(dec(fx1, kfx), ix);
+    const float2 e0 = __fmul2_rn(dec(fy0, kfy), iy), e1 = __fmul2_rn(dec(fy1, kfy), iy);
+    const float2 g0 = __fmul2_rn(dec(fz0, kfz), iz), g1 = __fmul2_rn(dec(fz1, kfz), iz);
+    const float tn0 = fmaxf(fmaxf(a0.x, b0.x), fmaxf(c0.x, 0.0f)), tf0 = fminf(fminf(d0.x, e0.x), fminf(g0.x, tmax));
+    const float tn1 = fmaxf(fmaxf(a0.y, b0.y), fmaxf(c0.y, 0.0f)), tf1 = fminf(fminf(d0.y, e0.y), fminf(g0.y, tmax));
+    const float tn2 = fmaxf(fmaxf(a1.x, b1.x), fmaxf(c1.x, 0.0f)), tf2 = fminf(fminf(d1.x, e1.x), fminf(g1.x, tmax));
+    const float tn3 = fmaxf(fmaxf(a1.y, b1.y), fmaxf(c1.y, 0.0f)), tf3 = fminf(fminf(d1.y, e1.y), fminf(g1.y, tmax));
+    tn[0] = tn0 <= tf0 ? tn0 : -1.0f;
+    tn[1] = tn1 <= tf1 ? tn1 : -1.0f;
+    tn[2] = tn2 <= tf2 ? tn2 : -1.0f;
+    tn[3] = tn3 <= tf3 ? tn3 : -1.0f;
+    unsigned m = 0;
+    m |= tn[0] >= 0.0f ? 1u : 0u;
+    m |= tn[1] >= 0.0f ? 2u : 0u;
+    m |= tn[2] >= 0.0f ? 4u : 0u;
+    m |= tn[3] >= 0.0f ? 8u : 0u;
+    return m;
+#elif RT_NODE_BASES
+    const size_t off = (size_t)(uint32_t)node * (16u * NODE_F4);
+    auto ld = [&](const char* b) { return __ldg(reinterpret_cast<const float4*>(b + off)); };
+    const float4 nx = ld(rb.pn[0]), fx = ld(rb.pf[0]);
+    const float4 ny = ld(rb.pn[1]), fy = ld(rb.pf[1]);
+    const float4 nz = ld(rb.pn[2]), fz = ld(rb.pf[2]);
+    child = __ldg(reinterpret_cast<const int4*>(nodes + (size_t)NODE_F4 * node + 6));
+#else
+    const float4* q = nodes + (size_t)NODE_F4 * node;
     const float4 nx = __ldg(q + rb.sx), fx = __ldg(q + 1 - rb.sx);
     const float4 ny = __ldg(q + 2 + rb.sy), fy = __ldg(q + 3 - rb.sy);
     const float4 nz = __ldg(q + 4 + rb.sz), fz = __ldg(q + 5 - rb.sz);
     child = __ldg(reinterpret_cast<const int4*>(q + 6));
+#endif
+#if !RT_NODE_F16
 #if RT_FFMA2
     // packed FP32 FMA (sm_100 FFMA2): two children's plane distances per instruction
     const float2 ix = make_float2(rb.idir.x, rb.idir.x), iy = make_float2(rb.idir.y, rb.idir.y);
@@ -192,6 +247,7 @@ __device__ __forceinline__ unsigned node4_hits(const float4* __restrict__ nodes,
     m |= tn[2] >= 0.0f ? 4u : 0u;
     m |= tn[3] >= 0.0f ? 8u : 0u;
     return m;
+#endif
 }
 
 __device__ __forceinline__ void cswap(uint32_t& a, uint32_t& b) {
@@ -363,7 +419,8 @@ __device__ __forceinline__ Hit closest_hit(const DevScene& S, float3 o, float3 d
         leaf_test(0, S.n_bvh - 1);
         return h;
     }
-    const RayBox rb = make_raybox(o, d, S.bound);
+    RayBox rb = make_raybox(o, d, S.bound);
+    set_node_bases(rb, S.nodes);
     int sp = 0;
     int node = S.root;
     while (true) {
@@ -430,7 +487,8 @@ __device__ __forceinline__ bool occluded(const DevScene& S, float3 o, float3 d, 
         return false;
     };
     if (BRUTE) return leaf_test(0, S.n_bvh - 1);
-    const RayBox rb = make_raybox(o, d, S.bound);
+    RayBox rb = make_raybox(o, d, S.bound);
+    set_node_bases(rb, S.nodes);
     int sp = 0;
     int node = S.root;
     while (true) {
