@@ -40,7 +40,16 @@ __device__ __forceinline__ float3 trace_pixel(const TraceParams& P, float3 o, fl
     float3 col = f3(0.f, 0.f, 0.f);
     cnt.add(CNT_PRIMARY);
     while (true) {
+#if RT_PACKET
+        // the first pass of the loop (primary rays) runs with every traced lane of the warp, and
+        // so do later passes that are still converged: those trace as warp packets
+        const bool packet = !BRUTE && (RT_PACKET_ALL || primary);
+        Hit h;
+        if (packet) h = closest_hit_packet<COUNT>(S, o, d, __activemask(), stk, cnt);
+        else h = closest_hit<COUNT, BRUTE>(S, o, d, stk, cnt);
+#else
         const Hit h = closest_hit<COUNT, BRUTE>(S, o, d, stk, cnt);
+#endif
         if (primary) { prim_id = h.gid; primary = false; }
         bool cont = false;
         if (h.gid < 0) {
@@ -67,11 +76,34 @@ __device__ __forceinline__ float3 trace_pixel(const TraceParams& P, float3 o, fl
             const bool front = dot(d, ng) < 0.0f;
             const float3 nf = front ? ng : ng * -1.0f;                   // S:150 faces the ray
             float3 c = S.ambient * xyz(__ldg(&S.mats[3 * mat]));         // S:193 ambient * kd
+#if RT_PACKET
+            // shadow rays of a packet pass: every lane of the pass takes part in each light's
+            // packet (lanes with the light behind their surface only ride along)
+            const unsigned pmask = packet ? __activemask() : 0u;
+#endif
             for (int j = 0; j < S.n_lights; ++j) {
                 cnt.add(CNT_LIGHT_EVALS);
                 const float3 Lp = xyz(__ldg(&S.lights[2 * j]));
                 const float3 l = normalize(Lp - p);
                 const float ndl = dot(nf, l);
+#if RT_PACKET
+                if (packet) {
+                    const float3 I = xyz(__ldg(&S.lights[2 * j + 1]));
+                    const float3 rv = nf * (2.0f * ndl) - l;
+                    const float rdv = -dot(rv, d);
+                    const float spec = rdv > 0.0f ? __powf(rdv, __ldg(&S.mats[3 * mat]).w) : 0.0f;
+                    const float3 term = (xyz(__ldg(&S.mats[3 * mat])) * I) * ndl + (xyz(__ldg(&S.mats[3 * mat + 1])) * I) * spec;
+                    const float3 os = fma3(nf, BIAS, p);
+                    const float3 sv = Lp - os;
+                    const float dist = sqrtf(dot(sv, sv));
+                    const bool lit = ndl > 0.0f;                         // reading 2 gate
+                    if (lit) cnt.add(CNT_SHADOW);
+                    int* hint = (RT_OCC_CACHE && j < RT_OCC_LIGHTS) ? occ_hint + j * RT_BLOCK : nullptr;
+                    if (!occluded_packet<COUNT>(S, os, sv * (1.0f / dist), dist, lit, pmask, stk, cnt, hint) && lit)
+                        c = c + term;                                    // reading 3
+                    continue;
+                }
+#endif
                 if (ndl <= 0.0f) continue;                               // reading 2 gate
                 // the light's term, added only if the shadow ray reaches the light
                 const float3 I = xyz(__ldg(&S.lights[2 * j + 1]));

@@ -35,6 +35,15 @@ namespace rtb {
 #define RT_OCC_CACHE 1    // per-thread, per-light last-occluder hint for shadow rays
 #endif
 #define RT_OCC_LIGHTS 4   // lights with an occluder hint slot (light j uses slot j; others none)
+#ifndef RT_PACKET
+#define RT_PACKET 0       // warp-packet traversal for coherent rays (primary rays and their shadow rays)
+#endif
+#ifndef RT_PACKET_ALL
+#define RT_PACKET_ALL 0   // 1: secondary rays and their shadow rays also traverse as warp packets
+#endif
+#if RT_PACKET && (!RT_SMEM_PTX || RT_BVH_WIDTH != 4 || RT_NODE_F16)
+#error "RT_PACKET needs RT_SMEM_PTX and plain 4-wide nodes"
+#endif
 
 // Per-thread traversal stack: the first RT_SMEM_STACK entries live in shared memory laid out
 // [entry][thread] (conflict-free), deeper entries in thread-local memory (L1-cached).  Keeping the
@@ -519,5 +528,177 @@ __device__ __forceinline__ bool occluded(const DevScene& S, float3 o, float3 d, 
     }
 }
 
+#if RT_PACKET
+// ---------------------------------------------------------------- warp packets
+// Coherent rays (a warp's 8x4 block of primary rays, and their shadow rays towards one point
+// light) traverse the BVH as one packet: the warp walks a single, warp-uniform node sequence --
+// the depth-first union of the nodes its rays need -- each lane box-testing its own ray against
+// the node's 4 children, and a child is entered when any lane hits it (its own t_best / segment
+// end as the far limit, so every ray still sees every node its single-ray traversal would:
+// results stay identical to brute force).  Node and primitive addresses are uniform, so each
+// fetch is one broadcast L1 transaction, and no lane idles on another lane's loop count or
+// node/leaf branch.  The price is box tests of nodes some rays do not need.
+
+// Warp-uniform stack of a packet in the warp's own slice of the per-thread shared stack
+// ([entry][thread] layout: entry e -> row e >> 5, column 32 w + (e & 31)), idle while a packet
+// runs.  Every lane writes the same value to the same word (one broadcast store) and reads back
+// its own write; each iteration that pushes passes a warp-synchronous vote first, so no lane can
+// overwrite an entry another lane has still to read.
+struct WarpStack {
+    uint32_t sa;   // shared address of (row 0, column 32 w)
+    __device__ __forceinline__ explicit WarpStack(const TravStack& t) : sa(t.sa - 4u * (threadIdx.x & 31u)) {}
+    __device__ __forceinline__ uint32_t addr(int e) const {
+        return sa + (uint32_t)(((e >> 5) * RT_BLOCK + (e & 31)) * 4);
+    }
+    __device__ __forceinline__ void set(int e, int v) const {
+        asm volatile("st.shared.b32 [%0], %1;" ::"r"(addr(e)), "r"(v));
+    }
+    __device__ __forceinline__ int get(int e) const {
+        int v;
+        asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(addr(e)));
+        return v;
+    }
+};
+
+// Nearest hit of every lane in `mask` (all of them must call; each with its own ray).  The union
+// of hit children is visited in the near-to-far order of the lowest lane that hit any of them.
+template <bool COUNT>
+__device__ __forceinline__ Hit closest_hit_packet(const DevScene& S, float3 o, float3 d, unsigned mask,
+                                                  const TravStack& stk, Counters<COUNT>& cnt) {
+    Hit h;
+    h.t = __int_as_float(0x7f800000);
+    h.gid = -1;
+    h.slot = 0;
+    for (int i = 0; i < S.n_planes; ++i) {
+        cnt.add(CNT_PLANE_TESTS);
+        float t;
+        if (plane_intersect(o, d, __ldg(&S.planes[i]), t) && t > T_MIN) {
+            const int gid = S.n_spheres + i;
+            if (t < h.t || (t == h.t && gid < h.gid)) { h.t = t; h.gid = gid; h.slot = ~i; }
+        }
+    }
+    if (S.n_bvh == 0) return h;
+    const RayBox rb = make_raybox(o, d, S.bound);
+    const WarpStack ws(stk);
+    int sp = 0;
+    int node = S.root;
+    while (true) {
+        if (node >= 0) {
+            cnt.add(CNT_NODE_VISITS);
+            float tn[4];
+            int4 ch;
+            const unsigned m = node4_hits(S.nodes, node, rb, h.t, tn, ch);
+            const unsigned hb = __ballot_sync(mask, m != 0u);
+            if (hb) {
+                const unsigned U = __reduce_or_sync(mask, m);
+                // this lane's near-to-far order of all 4 slots (missed slots last, in slot order)
+                uint32_t k0 = (m & 1) ? ((__float_as_uint(tn[0]) & ~3u) | 0u) : 0xfffffffcu;
+                uint32_t k1 = (m & 2) ? ((__float_as_uint(tn[1]) & ~3u) | 1u) : 0xfffffffdu;
+                uint32_t k2 = (m & 4) ? ((__float_as_uint(tn[2]) & ~3u) | 2u) : 0xfffffffeu;
+                uint32_t k3 = (m & 8) ? ((__float_as_uint(tn[3]) & ~3u) | 3u) : 0xffffffffu;
+                cswap(k0, k1); cswap(k2, k3); cswap(k0, k2); cswap(k1, k3); cswap(k1, k2);
+                const uint32_t ord = __shfl_sync(mask, (k0 & 3u) | (k1 & 3u) << 2 | (k2 & 3u) << 4 | (k3 & 3u) << 6,
+                                                 __ffs(hb) - 1);
+                uint32_t lst = 0;
+                int n = 0;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const uint32_t s = (ord >> (2 * i)) & 3u;
+                    if ((U >> s) & 1u) { lst |= s << (2 * n); ++n; }
+                }
+                for (int i = n - 1; i >= 1; --i) ws.set(sp++, pick4(ch, (lst >> (2 * i)) & 3u));
+                node = pick4(ch, lst & 3u);
+                continue;
+            }
+        } else {
+            const int enc = ~node;
+            const int first = enc & ((1 << LEAF_SHIFT) - 1);
+            const int last = first + (enc >> LEAF_SHIFT);
+            for (int k = first; k <= last; ++k) {
+                float t;
+                int gid;
+                if (prim_t<COUNT>(S, k, o, d, t, gid, cnt) && (t < h.t || (t == h.t && gid < h.gid))) {
+                    h.t = t; h.gid = gid; h.slot = k;
+                }
+            }
+        }
+        if (sp == 0) return h;
+        --sp;
+        node = ws.get(sp);
+    }
+}
+
+// Any hit (t_min < t < dist) for the lanes of `mask` with `need` set; every lane of `mask` must
+// call.  A lane drops out of the box tests (far limit -1) once its segment is blocked; the packet
+// ends when no lane is left or the union is exhausted.  Children are pushed in slot order.
+template <bool COUNT>
+__device__ __forceinline__ bool occluded_packet(const DevScene& S, float3 o, float3 d, float dist, bool need, unsigned mask,
+                                                const TravStack& stk, Counters<COUNT>& cnt, int* hint) {
+    bool occ = false;
+    if (need) {
+        for (int i = 0; i < S.n_planes; ++i) {
+            cnt.add(CNT_PLANE_TESTS);
+            float t;
+            if (plane_intersect(o, d, __ldg(&S.planes[i]), t) && t > T_MIN && t < dist) { occ = true; break; }
+        }
+#if RT_OCC_CACHE
+        if (!occ && hint && S.n_bvh) {
+            const int k = *hint;
+            float t;
+            int gid;
+            if (k >= 0 && prim_t<COUNT>(S, k, o, d, t, gid, cnt) && t < dist) occ = true;
+        }
+#endif
+    }
+    bool alive = need && !occ;
+    if (S.n_bvh == 0 || !__any_sync(mask, alive)) return occ;
+    const RayBox rb = make_raybox(o, d, S.bound);
+    const WarpStack ws(stk);
+    int sp = 0;
+    int node = S.root;
+    while (true) {
+        if (node >= 0) {
+            if (alive) cnt.add(CNT_NODE_VISITS);
+            float tn[4];
+            int4 ch;
+            const unsigned m = node4_hits(S.nodes, node, rb, alive ? dist : -1.0f, tn, ch);
+            const unsigned U = __reduce_or_sync(mask, m);
+            if (U) {
+                const uint32_t c0 = __ffs(U) - 1;
+                unsigned r = U & (U - 1);
+                while (r) {
+                    const uint32_t c = __ffs(r) - 1;
+                    r &= r - 1;
+                    ws.set(sp++, pick4(ch, c));
+                }
+                node = pick4(ch, c0);
+                continue;
+            }
+        } else {
+            if (alive) {
+                const int enc = ~node;
+                const int first = enc & ((1 << LEAF_SHIFT) - 1);
+                const int last = first + (enc >> LEAF_SHIFT);
+                for (int k = first; k <= last; ++k) {
+                    float t;
+                    int gid;
+                    if (prim_t<COUNT>(S, k, o, d, t, gid, cnt) && t < dist) {
+#if RT_OCC_CACHE
+                        if (hint) *hint = k;
+#endif
+                        alive = false;
+                        occ = true;
+                        break;
+                    }
+                }
+            }
+            if (!__any_sync(mask, alive)) return occ;
+        }
+        if (sp == 0) return occ;
+        --sp;
+        node = ws.get(sp);
+    }
+}
+#endif  // RT_PACKET
 
 }  // namespace rtb
