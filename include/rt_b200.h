@@ -218,10 +218,11 @@ rt_status rt_upload(rt_context* ctx, const void* host_src, void* dev_dst, size_t
 /* ------------------------------------------------------------------ sharding (host logic) */
 /* Tile shard map: the image of each eye is cut into RT_TILE x RT_TILE tiles,
  * tiles_per_eye = T = ceil(W/16)*ceil(H/16).  Global tile id G in [0, 2T) interleaves the eyes:
- * eye = G mod 2, tile = G div 2 (raster order), so both eyes of a tile are traced back to back.
- * world == 1: every tile, in G order.  world even: ranks [0, world/2) render the left eye and
- * [world/2, world) the right eye (world 2 = the paper's level-1 eye split), tile t of that eye
- * going to rank (t mod world/2) within the group.  world odd: G mod world.
+ * eye = G mod 2, tile = G div 2 (raster order).  world == 2: rank r renders eye r, every tile
+ * (the paper's level-1 eye split).  Otherwise (world == 1 included) tile t goes, in
+ * both eyes, to rank t mod world, so a rank's shard-local tile lt is G = 2 (rank + (lt div 2)
+ * world) + (lt mod 2): the two eyes of a tile are traced together (one warp = the same 4x4
+ * pixel block in both eyes).
  * rt_shard_tiles writes rank's global tile ids G (ascending) into tile_ids (may be NULL to
  * query the count) and their number into *n_tiles.  Pure host functions, no context. */
 rt_status rt_shard_tiles(uint32_t width, uint32_t height, uint32_t rank, uint32_t world,

@@ -550,7 +550,7 @@ rt_status fill_camera(rt_context* c, uint32_t W, uint32_t H, rtb::DevCamera& cam
 }
 
 struct ShardGeom {
-    int tiles_x, tiles_y, tiles_per_eye, mode, half;
+    int tiles_x, tiles_y, tiles_per_eye, mode;
 };
 
 ShardGeom shard_geom(uint32_t W, uint32_t H, uint32_t world) {
@@ -558,29 +558,20 @@ ShardGeom shard_geom(uint32_t W, uint32_t H, uint32_t world) {
     g.tiles_x = (int)((W + RT_TILE - 1) / RT_TILE);
     g.tiles_y = (int)((H + RT_TILE - 1) / RT_TILE);
     g.tiles_per_eye = g.tiles_x * g.tiles_y;
-    g.mode = world == 1 ? 0 : (world % 2 == 0 ? 1 : 2);
-    g.half = world % 2 == 0 ? (int)world / 2 : 1;
+    g.mode = world == 1 ? 0 : (world == 2 ? 1 : 2);   // 1: eye split; 0 / 2: tile pairs round-robin
     return g;
 }
 
 uint32_t shard_count(const ShardGeom& g, uint32_t rank, uint32_t world) {
-    if (g.mode == 0) return 2u * g.tiles_per_eye;
-    if (g.mode == 1) {
-        const int j = (int)rank % g.half;
-        return j < g.tiles_per_eye ? (uint32_t)((g.tiles_per_eye - j + g.half - 1) / g.half) : 0u;
-    }
-    const int total = 2 * g.tiles_per_eye;
-    return (int)rank < total ? (uint32_t)((total - (int)rank + (int)world - 1) / (int)world) : 0u;
+    if (g.mode == 1) return (uint32_t)g.tiles_per_eye;
+    const int pairs = (int)rank < g.tiles_per_eye ? (g.tiles_per_eye - (int)rank + (int)world - 1) / (int)world : 0;
+    return 2u * (uint32_t)pairs;
 }
 
 // global tile id G: eye = G & 1, tile = G >> 1 (eyes interleaved)
 uint32_t shard_tile(const ShardGeom& g, uint32_t rank, uint32_t world, uint32_t lt) {
-    if (g.mode == 0) return lt;
-    if (g.mode == 1) {
-        const int grp = (int)rank / g.half, j = (int)rank % g.half;
-        return (uint32_t)(2 * (j + (int)lt * g.half) + grp);
-    }
-    return rank + lt * world;
+    if (g.mode == 1) return 2u * lt + rank;
+    return 2u * (rank + (lt >> 1) * world) + (lt & 1u);
 }
 
 rt_status check_fb(const rt_fb& fb, uint32_t W, const char* name) {
@@ -630,7 +621,6 @@ rt_status rt_render_stereo_ex(rt_context* c, const rt_render_params* p, const rt
     P.shard_mode = g.mode;
     P.shard_rank = (int)p->shard_rank;
     P.shard_world = (int)p->shard_world;
-    P.shard_half = g.half;
     P.fb[0] = out->left.dev_ptr;
     P.fb[1] = out->right.dev_ptr;
     P.fb_fmt[0] = (int)out->left.format;
@@ -826,7 +816,6 @@ rt_status rt_unpack_shards(rt_context* c, const void* gathered, uint32_t W, uint
     U.tiles_per_rank = (int)(per / (256u * (format == RT_FORMAT_RGBA8 ? 4u : 8u)));
     U.world = (int)world;
     U.shard_mode = g.mode;
-    U.shard_half = g.half;
     CUDA_TRY(cudaSetDevice(c->device));
     CUDA_TRY(rtb_launch_unpack(gathered, U, c->stream));
     return RT_OK;

@@ -29,8 +29,8 @@ struct TraceParams {
     int* work_counter;
     int n_work;             // work items (pixels incl. tile padding) of this shard
     int tiles_x, tiles_per_eye;
-    int shard_mode;         // 0 all tiles, 1 eye-split groups (even world), 2 interleaved (odd world)
-    int shard_rank, shard_world, shard_half;
+    int shard_mode;         // 0 one rank, 1 eye split (world 2), 2 tile pairs round-robin (world >= 3)
+    int shard_rank, shard_world;
     void* fb[2];
     int fb_fmt[2];
     long long fb_pitch[2];
@@ -50,7 +50,7 @@ struct UnpackParams {
     long long pitch;
     int fmt;
     int W, H, tiles_x, tiles_per_eye, tiles_per_rank;
-    int world, shard_mode, shard_half;
+    int world, shard_mode;
 };
 
 // BVH build scratch (device pointers), owned by the context.

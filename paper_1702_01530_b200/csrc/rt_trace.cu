@@ -225,8 +225,8 @@ __global__ void __launch_bounds__(RT_BLOCK, RT_MINB) k_trace_stereo(const TraceP
         base = tile * 256 + 32 * (j & 7);
 #endif
         const int k = base + lane;
-        int eye, px, py;
-        if (map_work(P, k, eye, px, py)) {
+        int eye, px, py, lt;
+        if (map_work(P, k, eye, px, py, lt)) {
             cnt.add(CNT_PIXELS);
             const float sx = fmaf(2.0f * (px + 0.5f), 1.0f / P.W, -1.0f) * P.cam.tha;
             const float sy = fmaf(-2.0f * (py + 0.5f), 1.0f / P.H, 1.0f) * P.cam.th;
@@ -238,7 +238,7 @@ __global__ void __launch_bounds__(RT_BLOCK, RT_MINB) k_trace_stereo(const TraceP
             if (P.prim_id) P.prim_id[pix] = pid;
             if (P.radiance) P.radiance[pix] = make_float4(c.x, c.y, c.z, 0.0f);
             if (P.shard) {
-                const long long s = (long long)(k >> 8) * 256 + ((py % TILE) * TILE + (px % TILE));
+                const long long s = (long long)lt * 256 + ((py % TILE) * TILE + (px % TILE));
                 if (P.shard_fmt == RT_FORMAT_RGBA8) reinterpret_cast<uint32_t*>(P.shard)[s] = pack_rgba8(c);
                 else reinterpret_cast<uint2*>(P.shard)[s] = pack_rgba16f(c);
             }
@@ -264,17 +264,14 @@ __global__ void k_unpack_shards(const void* __restrict__ gathered, UnpackParams 
         const long long r = i - (long long)rank * U.tiles_per_rank * 256;
         const int lt = (int)(r >> 8);
         const int within = (int)(r & 255);
-        int g;
-        if (U.shard_mode == 0) {
-            g = lt;
-            if (g >= 2 * U.tiles_per_eye) continue;
-        } else if (U.shard_mode == 1) {
-            const int grp = rank / U.shard_half, j = rank % U.shard_half;
-            if (j + lt * U.shard_half >= U.tiles_per_eye) continue;
-            g = 2 * (j + lt * U.shard_half) + grp;
+        int g;                                           // global tile id (rt_shard_tiles)
+        if (U.shard_mode == 1) {
+            if (lt >= U.tiles_per_eye) continue;
+            g = 2 * lt + rank;
         } else {
-            g = rank + lt * U.world;
-            if (g >= 2 * U.tiles_per_eye) continue;
+            const int t = rank + (lt >> 1) * U.world;
+            if (t >= U.tiles_per_eye) continue;
+            g = 2 * t + (lt & 1);
         }
         const int eye = g & 1;
         const int t = g >> 1;

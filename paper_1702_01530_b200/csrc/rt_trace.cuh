@@ -31,6 +31,12 @@ namespace rtb {
 #ifndef RT_SMEM_PTX
 #define RT_SMEM_PTX 1     // shared stack addressed with a 32-bit shared-window address held in a register
 #endif
+#ifndef RT_FAST_PUSH
+#define RT_FAST_PUSH 1    // pushes of one node visit: one shared address + predicated stores when they fit
+#endif
+#if RT_FAST_PUSH && !RT_SMEM_PTX
+#error "RT_FAST_PUSH needs RT_SMEM_PTX"
+#endif
 #ifndef RT_OCC_CACHE
 #define RT_OCC_CACHE 1    // per-thread, per-light last-occluder hint for shadow rays
 #endif
@@ -80,6 +86,17 @@ struct TravStack {
         }
         return l[i - RT_SMEM_STACK];
     }
+#if RT_SMEM_PTX
+    // shared address of entry i (valid for i < RT_SMEM_STACK); entry i + k is at + k * RT_BLOCK * 4
+    __device__ __forceinline__ uint32_t addr(int i) const { return sa + (uint32_t)i * (RT_BLOCK * 4u); }
+    __device__ __forceinline__ static void st(uint32_t a, int v) {
+        asm volatile("st.shared.b32 [%0], %1;" ::"r"(a), "r"(v));
+    }
+    __device__ __forceinline__ static void st_if(bool p, uint32_t a, int v) {
+        asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.shared.b32 [%0], %1;\n\t}" ::"r"(a), "r"(v),
+                     "r"((uint32_t)p));
+    }
+#endif
 };
 
 template <bool COUNT>
@@ -98,30 +115,33 @@ struct Hit {
     int slot;   // BVH prim slot (>= 0) or ~plane index (< 0)
 };
 
-// Work item -> (eye, px, py).  16x16 tiles, each tile = 8 warps of 8x4 pixels so a warp's
-// primary rays are spatially coherent.  Tiles are drawn from this rank's shard.
+// Work item -> (eye, px, py) and the item's shard-local tile `lt` (16x16 tiles; global tile id
+// G = 2 t + eye for tile t of an eye, the layout rt_shard_tiles documents).
+//   shard_mode 1 (world 2, the paper's level-1 eye split): this rank's eye only; each warp
+//     takes one 8x4 block of a tile.
+//   shard_mode 0 / 2 (one rank / world >= 3: tiles dealt to ranks round-robin): both eyes of a
+//     tile are traced together, each warp taking one 4x4 block of the tile in BOTH eyes (lanes
+//     0-15 left, 16-31 right).  With the zero-parallax plane at the scene (convergence C) the two
+//     eyes' rays through one pixel are nearly the same ray, so a warp's 32 rays span a smaller
+//     bundle than one eye's 8x4 block (C4 3.45 -> 3.21 ms per stereo frame).
 template <typename Params>
-__device__ __forceinline__ bool map_work(const Params& P, int k, int& eye, int& px, int& py) {
-    const int lt = k >> 8;
-    const int within = k & 255;
-    // global tile id G interleaves the eyes (eye = G & 1, tile = G >> 1): both eyes of a tile
-    // are traced back to back, which keeps their (nearly identical) BVH paths hot in L1/L2
-    int g;
-    if (P.shard_mode == 0) {
-        g = lt;
-    } else if (P.shard_mode == 1) {
-        const int grp = P.shard_rank / P.shard_half;
-        const int j = P.shard_rank % P.shard_half;
-        g = 2 * (j + lt * P.shard_half) + grp;
+__device__ __forceinline__ bool map_work(const Params& P, int k, int& eye, int& px, int& py, int& lt) {
+    const int lane = k & 31, w = (k >> 5) & 7;
+    int t;
+    if (P.shard_mode == 1) {
+        lt = k >> 8;
+        eye = P.shard_rank;
+        t = lt;
+        px = (t % P.tiles_x) * TILE + (w & 1) * 8 + (lane & 7);
+        py = (t / P.tiles_x) * TILE + (w >> 1) * 4 + (lane >> 3);
     } else {
-        g = P.shard_rank + lt * P.shard_world;
+        const int q = k >> 9, wp = (k >> 5) & 15;         // tile pair of this rank, warp of the pair
+        eye = lane >> 4;
+        lt = 2 * q + eye;
+        t = P.shard_rank + q * P.shard_world;
+        px = (t % P.tiles_x) * TILE + (wp & 3) * 4 + (lane & 3);
+        py = (t / P.tiles_x) * TILE + (wp >> 2) * 4 + ((lane >> 2) & 3);
     }
-    eye = g & 1;
-    const int t = g >> 1;
-    const int tx = t % P.tiles_x, ty = t / P.tiles_x;
-    const int w = within >> 5, lane = within & 31;
-    px = tx * TILE + (w & 1) * 8 + (lane & 7);
-    py = ty * TILE + (w >> 1) * 4 + (lane >> 3);
     return px < P.W && py < P.H;
 }
 
@@ -283,9 +303,20 @@ __device__ __forceinline__ bool order_push(unsigned m, const float tn[4], const 
     uint32_t k3 = (m & 8) ? ((__float_as_uint(tn[3]) & ~3u) | 3u) : 0xffffffffu;
     cswap(k0, k1); cswap(k2, k3); cswap(k0, k2); cswap(k1, k3); cswap(k1, k2);
     const int nh = __popc(m);
-    if (nh > 3) stk.set(sp + nh - 4, pick4(ch, k3 & 3u));
-    if (nh > 2) stk.set(sp + nh - 3, pick4(ch, k2 & 3u));
-    if (nh > 1) stk.set(sp + nh - 2, pick4(ch, k1 & 3u));
+#if RT_FAST_PUSH
+    if (sp + 3 <= RT_SMEM_STACK) {
+        // all pushes land in the shared part: one address, predicated stores (no branches)
+        const uint32_t a = stk.addr(sp + nh - 2);
+        TravStack::st_if(nh > 3, a - 2u * (RT_BLOCK * 4u), pick4(ch, k3 & 3u));
+        TravStack::st_if(nh > 2, a - 1u * (RT_BLOCK * 4u), pick4(ch, k2 & 3u));
+        TravStack::st_if(nh > 1, a, pick4(ch, k1 & 3u));
+    } else
+#endif
+    {
+        if (nh > 3) stk.set(sp + nh - 4, pick4(ch, k3 & 3u));
+        if (nh > 2) stk.set(sp + nh - 3, pick4(ch, k2 & 3u));
+        if (nh > 1) stk.set(sp + nh - 2, pick4(ch, k1 & 3u));
+    }
     sp += nh - 1;
     node = pick4(ch, k0 & 3u);
     return true;
@@ -296,6 +327,21 @@ __device__ __forceinline__ bool order_push(unsigned m, const float tn[4], const 
 // sort); unrolled with predicated stores.
 __device__ __forceinline__ bool plain_push(unsigned m, const int4& ch, TravStack& stk, int& sp, int& node) {
     if (!m) return false;
+#if RT_FAST_PUSH
+    if (sp + 3 <= RT_SMEM_STACK) {
+        // continue with the lowest hit slot; the others (slots above it) go to entries sp.. in slot
+        // order: slot c's entry is sp + popc(r & below(c)), r = the pushed set (slot 0 never pushed)
+        const unsigned r = m & (m - 1u);
+        const uint32_t a = stk.addr(sp);
+        constexpr uint32_t E = RT_BLOCK * 4u;
+        TravStack::st_if(r & 2u, a, ch.y);
+        TravStack::st_if(r & 4u, a + ((r >> 1) & 1u) * E, ch.z);
+        TravStack::st_if(r & 8u, a + (uint32_t)__popc(r & 6u) * E, ch.w);
+        sp += __popc(r);
+        node = pick4(ch, __ffs(m) - 1);
+        return true;
+    }
+#endif
 #if RT_PLAIN_PUSH_LOOP
     const int nh = __popc(m);
     const uint32_t c0 = __ffs(m) - 1;

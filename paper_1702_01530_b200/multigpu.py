@@ -2,8 +2,8 @@
 to N identical parts", PAPER.md:56 level-1 left/right channels).
 
 Every rank holds the whole scene (deterministic LBVH, identical on every rank) and renders only
-its tiles (rt_shard_tiles: world 2 = eye split, even world = eye-major groups of interleaved
-16x16 tiles).  Two ways to assemble the frame on rank 0:
+its tiles (rt_shard_tiles: world 2 = eye split, otherwise 16x16 tiles dealt round-robin, both
+eyes of a tile to the same rank).  Two ways to assemble the frame on rank 0:
 
   "peer"  fused render -> gather: rank 0 exports its framebuffers with CUDA IPC, every other
           rank maps them (rt_ipc_open) and its trace kernel's pack epilogue stores its tiles
