@@ -48,7 +48,17 @@ __device__ __forceinline__ float3 trace_pixel(const TraceParams& P, float3 o, fl
         if (packet) h = closest_hit_packet<COUNT>(S, o, d, __activemask(), stk, cnt);
         else h = closest_hit<COUNT, BRUTE>(S, o, d, stk, cnt);
 #else
+#if RT_SHADOW_STATS
+        const uint32_t s0 = cnt.steps;
+#endif
         const Hit h = closest_hit<COUNT, BRUTE>(S, o, d, stk, cnt);
+#if RT_SHADOW_STATS
+        if (COUNT) {   // warp-level divergence statistics: c[2] += max lane steps, c[9] += sum
+            const uint32_t T = cnt.steps - s0, am = __activemask();
+            const uint32_t mx = __reduce_max_sync(am, T), sm = __reduce_add_sync(am, T);
+            if ((threadIdx.x & 31) == __ffs(am) - 1) { cnt.c[2] += mx; cnt.c[9] += sm; }
+        }
+#endif
 #endif
         if (primary) { prim_id = h.gid; primary = false; }
         bool cont = false;
@@ -81,8 +91,13 @@ __device__ __forceinline__ float3 trace_pixel(const TraceParams& P, float3 o, fl
             // packet (lanes with the light behind their surface only ride along)
             const unsigned pmask = packet ? __activemask() : 0u;
 #endif
+#if RT_SHADOW_STATS
+            uint32_t tsum = 0;
+#endif
             for (int j = 0; j < S.n_lights; ++j) {
+#if !RT_SHADOW_STATS
                 cnt.add(CNT_LIGHT_EVALS);
+#endif
                 const float3 Lp = xyz(__ldg(&S.lights[2 * j]));
                 const float3 l = normalize(Lp - p);
                 const float ndl = dot(nf, l);
@@ -116,8 +131,26 @@ __device__ __forceinline__ float3 trace_pixel(const TraceParams& P, float3 o, fl
                 const float dist = sqrtf(dot(sv, sv));
                 cnt.add(CNT_SHADOW);
                 int* hint = (RT_OCC_CACHE && j < RT_OCC_LIGHTS) ? occ_hint + j * RT_BLOCK : nullptr;
+#if RT_SHADOW_STATS
+                const uint32_t s0 = cnt.steps;
+                const bool occ = occluded<COUNT, BRUTE>(S, os, sv * (1.0f / dist), dist, stk, cnt, hint);
+                if (COUNT) {   // c[6] += per-light warp max of shadow steps, c[7] += their sum
+                    const uint32_t T = cnt.steps - s0, am = __activemask();
+                    const uint32_t mx = __reduce_max_sync(am, T), sm = __reduce_add_sync(am, T);
+                    if ((threadIdx.x & 31) == __ffs(am) - 1) { cnt.c[6] += mx; cnt.c[7] += sm; }
+                    tsum += T;
+                }
+                if (!occ) c = c + term;
+#else
                 if (!occluded<COUNT, BRUTE>(S, os, sv * (1.0f / dist), dist, stk, cnt, hint)) c = c + term;   // reading 3
+#endif
             }
+#if RT_SHADOW_STATS
+            if (COUNT) {       // c[10] += warp max over lanes of all their shadow steps at this hit
+                const uint32_t am = __activemask(), mx = __reduce_max_sync(am, tsum);
+                if ((threadIdx.x & 31) == __ffs(am) - 1) cnt.c[10] += mx;
+            }
+#endif
             col = fma3(c, w, col);
             if (depth > 0) {
                 const float4 m2 = __ldg(&S.mats[3 * mat + 2]);

@@ -10,7 +10,8 @@ namespace rtb {
 #define RT_BLOCK 256      // threads per trace CTA (stack stride)
 #endif
 #ifndef RT_SHADOW_SORT
-#define RT_SHADOW_SORT 0  // 1: any-hit (shadow) rays also visit children near-to-far (measured slower)
+#define RT_SHADOW_SORT 0  // 1: any-hit (shadow) rays also visit children near-to-far (measured slower);
+                          // 2: far-to-near (towards the light first)
 #endif
 #ifndef RT_FFMA2
 #define RT_FFMA2 1  // packed FP32 FMA (FFMA2) for the BVH4 slab planes
@@ -36,6 +37,9 @@ namespace rtb {
 #endif
 #if RT_FAST_PUSH && !RT_SMEM_PTX
 #error "RT_FAST_PUSH needs RT_SMEM_PTX"
+#endif
+#ifndef RT_SHADOW_STATS
+#define RT_SHADOW_STATS 0  // 1: instrumented build records warp-level traversal divergence (experiments)
 #endif
 #ifndef RT_OCC_CACHE
 #define RT_OCC_CACHE 1    // per-thread, per-light last-occluder hint for shadow rays
@@ -102,11 +106,22 @@ struct TravStack {
 template <bool COUNT>
 struct Counters {
     uint32_t c[RT_NUM_COUNTERS_INTERNAL];
+#if RT_SHADOW_STATS
+    uint32_t steps;   // traversal loop iterations of this thread (divergence statistics build only)
+#endif
     __device__ void zero() {
+#if RT_SHADOW_STATS
+        steps = 0;
+#endif
 #pragma unroll
         for (int i = 0; i < RT_NUM_COUNTERS_INTERNAL; ++i) c[i] = 0;
     }
     __device__ __forceinline__ void add(int i, uint32_t n = 1) { if (COUNT) c[i] += n; }
+    __device__ __forceinline__ void step() {
+#if RT_SHADOW_STATS
+        if (COUNT) ++steps;
+#endif
+    }
 };
 
 struct Hit {
@@ -479,6 +494,7 @@ __device__ __forceinline__ Hit closest_hit(const DevScene& S, float3 o, float3 d
     int sp = 0;
     int node = S.root;
     while (true) {
+        cnt.step();
         if (node >= 0) {
             cnt.add(CNT_NODE_VISITS);
 #if RT_BVH_WIDTH == 8
@@ -547,6 +563,7 @@ __device__ __forceinline__ bool occluded(const DevScene& S, float3 o, float3 d, 
     int sp = 0;
     int node = S.root;
     while (true) {
+        cnt.step();
         if (node >= 0) {
             cnt.add(CNT_NODE_VISITS);
 #if RT_BVH_WIDTH == 8
@@ -557,7 +574,13 @@ __device__ __forceinline__ bool occluded(const DevScene& S, float3 o, float3 d, 
             float tn[4];
             int4 ch;
             const unsigned m = node4_hits(S.nodes, node, rb, dist, tn, ch);
-#if RT_SHADOW_SORT
+#if RT_SHADOW_SORT == 2
+            if (m) {   // far-first: entry distances mirrored (0x7effffff - bits; misses stay last)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) tn[c] = __int_as_float(0x7effffff - __float_as_int(tn[c]));
+            }
+            if (order_push(m, tn, ch, stk, sp, node)) continue;
+#elif RT_SHADOW_SORT
             if (order_push(m, tn, ch, stk, sp, node)) continue;
 #else
             if (plain_push(m, ch, stk, sp, node)) continue;
@@ -629,6 +652,7 @@ __device__ __forceinline__ Hit closest_hit_packet(const DevScene& S, float3 o, f
     int sp = 0;
     int node = S.root;
     while (true) {
+        cnt.step();
         if (node >= 0) {
             cnt.add(CNT_NODE_VISITS);
             float tn[4];
