@@ -113,6 +113,8 @@ typedef enum rt_counter {
 #define RT_RENDER_PEER_STORE 4u  /* out_left/out_right are a PEER rank's framebuffers mapped with
                                     rt_ipc_open: the pack epilogue stores over NVLink and the
                                     kernel ends with a system-scope fence (fused render->gather) */
+#define RT_RENDER_KDTREE 8u      /* NEXT-4 ablation: traverse the kd-tree of rt_kdtree_build
+                                    instead of the BVH4 (same intersectors, same results) */
 
 typedef struct rt_render_params {
     uint32_t width, height;      /* per eye; 1 <= w,h <= 16384                              */
@@ -276,6 +278,17 @@ rt_status rt_scene_info(rt_context* ctx, uint64_t info[8]);
  * and the leaf-order primitive global IDs to
  * HOST arrays for structural tests; pass NULL to query sizes via *n_nodes / *n_prims. */
 rt_status rt_bvh_export(rt_context* ctx, float* nodes, uint32_t* n_nodes, int32_t* prim_gid, uint32_t* n_prims);
+/* NEXT-4 ablation (Table 1 "Kd-trees"): build a binned-SAH kd-tree (32 bins,
+ * C_trav 1, C_isect 1.5, empty-space bonus 0.8; primitives straddling a split referenced on
+ * both sides) over the uploaded scene's BVH primitive records, on the HOST from a copy of them,
+ * and upload it for RT_RENDER_KDTREE renders.  The product path (BVH4) is unaffected.
+ *   max_leaf: primitives at or below which a node always becomes a leaf (>= 1)
+ *   max_depth: depth limit, 0 = round(8 + 1.3 log2 N)
+ *   info (HOST, may be NULL): [0] nodes [1] leaf references [2] depth [3] leaves
+ *        [4] device bytes [5] host build time us
+ * Synchronous.  Replaced by the next call; freed with the scene.
+ * Errors: RT_ERR_INVALID_ARG, RT_ERR_NO_SCENE, RT_ERR_OOM, RT_ERR_CUDA. */
+rt_status rt_kdtree_build(rt_context* ctx, uint32_t max_leaf, uint32_t max_depth, uint64_t info[6]);
 /* FFMA throughput microbenchmark (roofline denominator): runs `iters` FMA chains on every
  * SM and returns achieved FP32 TFLOP/s and the kernel time in ms. */
 rt_status rt_bench_ffma(rt_context* ctx, uint32_t iters, double* tflops, double* ms);

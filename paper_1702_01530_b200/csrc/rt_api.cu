@@ -93,6 +93,8 @@ struct rt_context {
     std::vector<int> level_start;
     std::vector<uint32_t> h_tri;
     double sphere_bound = 0.0;
+    // NEXT-4 kd-tree ablation (rt_kdtree_build)
+    DevBuf kd_nodes_buf, kd_refs_buf;
 };
 
 namespace {
@@ -111,6 +113,8 @@ rt_status dalloc(rt_context* c, size_t count, T** out) {
 }
 
 void free_scene(rt_context* c) {
+    c->kd_nodes_buf.release();
+    c->kd_refs_buf.release();
     for (auto& b : c->scene_bufs) b.release();
     c->scene_bufs.clear();
     c->has_scene = false;
@@ -598,8 +602,12 @@ rt_status rt_render_stereo_ex(rt_context* c, const rt_render_params* p, const rt
     if (p->max_depth > RT_MAX_DEPTH) return fail(RT_ERR_SIZE, "max_depth %u > %d", p->max_depth, RT_MAX_DEPTH);
     if (p->shard_world == 0 || p->shard_rank >= p->shard_world || p->shard_world > 4096)
         return fail(RT_ERR_INVALID_ARG, "shard %u of %u", p->shard_rank, p->shard_world);
-    if (p->flags & ~(RT_RENDER_COUNT | RT_RENDER_BRUTE_FORCE | RT_RENDER_PEER_STORE))
+    if (p->flags & ~(RT_RENDER_COUNT | RT_RENDER_BRUTE_FORCE | RT_RENDER_PEER_STORE | RT_RENDER_KDTREE))
         return fail(RT_ERR_INVALID_ARG, "unknown flags 0x%x", p->flags);
+    if ((p->flags & RT_RENDER_KDTREE) && (p->flags & RT_RENDER_BRUTE_FORCE))
+        return fail(RT_ERR_INVALID_ARG, "RT_RENDER_KDTREE and RT_RENDER_BRUTE_FORCE are exclusive");
+    if ((p->flags & RT_RENDER_KDTREE) && c->sc.n_bvh > 0 && !c->sc.kd_nodes)
+        return fail(RT_ERR_INVALID_ARG, "RT_RENDER_KDTREE needs rt_kdtree_build after the upload");
     if ((p->flags & RT_RENDER_COUNT) && !out->counters) return fail(RT_ERR_INVALID_ARG, "RT_RENDER_COUNT needs counters");
     rt_status st;
     if ((st = check_fb(out->left, W, "out_left")) || (st = check_fb(out->right, W, "out_right"))) return st;
@@ -639,13 +647,14 @@ rt_status rt_render_stereo_ex(rt_context* c, const rt_render_params* p, const rt
     if (P.n_work == 0) return RT_OK;
     CUDA_TRY(cudaSetDevice(c->device));
     int occ = 0;
-    CUDA_TRY(rtb_trace_occupancy(p->flags & (RT_RENDER_COUNT | RT_RENDER_BRUTE_FORCE), P.stack_entries, &occ));
+    const unsigned kflags = p->flags & (RT_RENDER_COUNT | RT_RENDER_BRUTE_FORCE | RT_RENDER_KDTREE);
+    CUDA_TRY(rtb_trace_occupancy(kflags, P.stack_entries, &occ));
     if (occ < 1) occ = 1;
     const long long max_blocks = ((long long)P.n_work + 255) / 256;
     int grid = (int)std::min<long long>((long long)c->num_sms * occ, std::max<long long>(1, max_blocks));
     if (c->grid_limit > 0) grid = std::min(grid, c->grid_limit);   // experiment knob (paper's "network size")
     CUDA_TRY(cudaMemsetAsync(c->work_counter, 0, sizeof(int), c->stream));
-    CUDA_TRY(rtb_launch_trace(P, p->flags & (RT_RENDER_COUNT | RT_RENDER_BRUTE_FORCE), grid, c->stream));
+    CUDA_TRY(rtb_launch_trace(P, kflags, grid, c->stream));
     return RT_OK;
 }
 
@@ -880,6 +889,57 @@ rt_status rt_compose(rt_context* c, rt_fb left, rt_fb right, uint32_t W, uint32_
 }
 
 // ------------------------------------------------------------------------------ introspection
+rt_status rt_kdtree_build(rt_context* c, uint32_t max_leaf, uint32_t max_depth, uint64_t info[6]) {
+    if (!c) return fail(RT_ERR_INVALID_ARG, "rt_kdtree_build: NULL context");
+    if (max_leaf < 1 || max_leaf > 4096) return fail(RT_ERR_INVALID_ARG, "rt_kdtree_build: max_leaf %u", max_leaf);
+    if (max_depth > 60) return fail(RT_ERR_INVALID_ARG, "rt_kdtree_build: max_depth %u > 60", max_depth);
+    if (!c->has_scene) return fail(RT_ERR_NO_SCENE, "rt_kdtree_build: no scene");
+    CUDA_TRY(cudaSetDevice(c->device));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    const int n = c->sc.n_bvh;
+    const auto t0 = std::chrono::steady_clock::now();
+    rtb::KdHost K;
+    if (n > 0) {
+        std::vector<float4> prims(3 * (size_t)n);
+        CUDA_TRY(cudaMemcpy(prims.data(), c->sc.prims, prims.size() * sizeof(float4), cudaMemcpyDeviceToHost));
+        rtb::kd_build_host(prims.data(), n, c->sc.n_spheres, (int)max_leaf, (int)max_depth, K);
+    }
+    const double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+    c->kd_nodes_buf.release();
+    c->kd_refs_buf.release();
+    c->sc.kd_nodes = nullptr;
+    c->sc.kd_refs = nullptr;
+    if (n > 0) {
+        DevBuf a, b;
+        a.bytes = K.nodes.size() * sizeof(int2);
+        b.bytes = std::max<size_t>(K.refs.size(), 1) * sizeof(int);
+        cudaError_t e = cudaMalloc(&a.p, a.bytes);
+        if (e == cudaSuccess) e = cudaMalloc(&b.p, b.bytes);
+        if (e != cudaSuccess) {
+            a.release();
+            b.release();
+            return fail(RT_ERR_OOM, "rt_kdtree_build: cudaMalloc: %s", cudaGetErrorString(e));
+        }
+        c->kd_nodes_buf = a;
+        c->kd_refs_buf = b;
+        CUDA_TRY(cudaMemcpy(a.p, K.nodes.data(), a.bytes, cudaMemcpyHostToDevice));
+        if (!K.refs.empty()) CUDA_TRY(cudaMemcpy(b.p, K.refs.data(), K.refs.size() * sizeof(int), cudaMemcpyHostToDevice));
+        c->sc.kd_nodes = static_cast<const int2*>(a.p);
+        c->sc.kd_refs = static_cast<const int*>(b.p);
+        c->sc.kd_lo = make_float3(K.lo[0], K.lo[1], K.lo[2]);
+        c->sc.kd_hi = make_float3(K.hi[0], K.hi[1], K.hi[2]);
+    }
+    if (info) {
+        info[0] = K.nodes.size();
+        info[1] = K.refs.size();
+        info[2] = (uint64_t)K.depth;
+        info[3] = (uint64_t)K.leaves;
+        info[4] = K.nodes.size() * sizeof(int2) + K.refs.size() * sizeof(int);
+        info[5] = (uint64_t)us;
+    }
+    return RT_OK;
+}
+
 rt_status rt_scene_info(rt_context* c, uint64_t info[8]) {
     if (!c || !info) return fail(RT_ERR_INVALID_ARG, "rt_scene_info: NULL argument");
     if (!c->has_scene) return fail(RT_ERR_NO_SCENE, "rt_scene_info: no scene");

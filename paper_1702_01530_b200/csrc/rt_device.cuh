@@ -150,6 +150,10 @@ struct DevScene {
     float bound;        // max |x|+|y|+|z| over the BVH bounds (box-test margin scale)
     float3 ambient;
     float3 background;
+    // NEXT-4 ablation: kd-tree over the same primitive records (null unless rt_kdtree_build ran)
+    const int2* __restrict__ kd_nodes;
+    const int* __restrict__ kd_refs;
+    float3 kd_lo, kd_hi;
 };
 
 struct DevCamera {

@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <vector>
+
 #include "../../include/rt_b200.h"
 #include "rt_device.cuh"
 
@@ -89,6 +91,17 @@ struct BuildBuffers {
     int* count;                 // [N-1] primitives below each internal node (treelets)
     int treelet_passes;         // 0 = plain LBVH
 };
+
+namespace rtb {
+// NEXT-4 kd-tree ablation (rt_kdtree.cu): host-built binned-SAH kd-tree over the primitive records
+struct KdHost {
+    std::vector<int2> nodes;    // preorder; see rt_kdtree.cu for the encoding
+    std::vector<int> refs;      // leaf reference lists (BVH primitive slots)
+    int depth = 0, leaves = 0;
+    float lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};   // root cell
+};
+void kd_build_host(const float4* prims, int n, int n_spheres, int max_leaf, int max_depth, KdHost& out);
+}  // namespace rtb
 
 // launchers (rt_trace.cu)
 cudaError_t rtb_launch_trace(const TraceParams& P, unsigned flags, int grid, cudaStream_t st);

@@ -28,9 +28,10 @@ namespace rtb {
 // registers, the refraction child is pushed on a per-thread stack (<= max_depth entries).
 // Radiance accumulates as sum over tree nodes of path_weight * local_term, which equals the
 // recursive definition c = local + kt*T(refr) + kr_eff*T(refl) (reading 17).
-template <bool COUNT, bool BRUTE>
+template <bool COUNT, int ACC>
 __device__ __forceinline__ float3 trace_pixel(const TraceParams& P, float3 o, float3 d, int& prim_id, TravStack& stk,
                                               Counters<COUNT>& cnt, int* occ_hint) {
+    constexpr bool BRUTE = ACC == ACC_BRUTE;
     const DevScene& S = P.sc;
     float4 st_a[MAX_DEPTH], st_b[MAX_DEPTH];   // refraction children: (o, w) (d, depth)
     int sp = 0;
@@ -46,12 +47,12 @@ __device__ __forceinline__ float3 trace_pixel(const TraceParams& P, float3 o, fl
         const bool packet = !BRUTE && (RT_PACKET_ALL || primary);
         Hit h;
         if (packet) h = closest_hit_packet<COUNT>(S, o, d, __activemask(), stk, cnt);
-        else h = closest_hit<COUNT, BRUTE>(S, o, d, stk, cnt);
+        else h = closest_hit<COUNT, ACC>(S, o, d, stk, cnt);
 #else
 #if RT_SHADOW_STATS
         const uint32_t s0 = cnt.steps;
 #endif
-        const Hit h = closest_hit<COUNT, BRUTE>(S, o, d, stk, cnt);
+        const Hit h = closest_hit<COUNT, ACC>(S, o, d, stk, cnt);
 #if RT_SHADOW_STATS
         if (COUNT) {   // warp-level divergence statistics: c[2] += max lane steps, c[9] += sum
             const uint32_t T = cnt.steps - s0, am = __activemask();
@@ -133,7 +134,7 @@ __device__ __forceinline__ float3 trace_pixel(const TraceParams& P, float3 o, fl
                 int* hint = (RT_OCC_CACHE && j < RT_OCC_LIGHTS) ? occ_hint + j * RT_BLOCK : nullptr;
 #if RT_SHADOW_STATS
                 const uint32_t s0 = cnt.steps;
-                const bool occ = occluded<COUNT, BRUTE>(S, os, sv * (1.0f / dist), dist, stk, cnt, hint);
+                const bool occ = occluded<COUNT, ACC>(S, os, sv * (1.0f / dist), dist, stk, cnt, hint);
                 if (COUNT) {   // c[6] += per-light warp max of shadow steps, c[7] += their sum
                     const uint32_t T = cnt.steps - s0, am = __activemask();
                     const uint32_t mx = __reduce_max_sync(am, T), sm = __reduce_add_sync(am, T);
@@ -142,7 +143,7 @@ __device__ __forceinline__ float3 trace_pixel(const TraceParams& P, float3 o, fl
                 }
                 if (!occ) c = c + term;
 #else
-                if (!occluded<COUNT, BRUTE>(S, os, sv * (1.0f / dist), dist, stk, cnt, hint)) c = c + term;   // reading 3
+                if (!occluded<COUNT, ACC>(S, os, sv * (1.0f / dist), dist, stk, cnt, hint)) c = c + term;   // reading 3
 #endif
             }
 #if RT_SHADOW_STATS
@@ -195,7 +196,7 @@ __device__ __forceinline__ float3 trace_pixel(const TraceParams& P, float3 o, fl
 
 // Persistent warps: each warp takes 32 consecutive work items (one 8x4 pixel block) per
 // atomic and traces one pixel tree per lane; the BVH stack is in shared memory.
-template <bool COUNT, bool BRUTE>
+template <bool COUNT, int ACC>
 __global__ void __launch_bounds__(RT_BLOCK, RT_MINB) k_trace_stereo(const TraceParams P) {
     extern __shared__ int s_stack[];                 // [stack_entries][RT_BLOCK]
     Counters<COUNT> cnt;
@@ -265,7 +266,7 @@ __global__ void __launch_bounds__(RT_BLOCK, RT_MINB) k_trace_stereo(const TraceP
             const float sy = fmaf(-2.0f * (py + 0.5f), 1.0f / P.H, 1.0f) * P.cam.th;
             const float3 d = normalize(P.cam.f + P.cam.r * (sx + P.cam.sigma[eye]) + P.cam.u * sy);
             int pid = -1;
-            const float3 c = trace_pixel<COUNT, BRUTE>(P, P.cam.eye[eye], d, pid, stk, cnt, s_occ + threadIdx.x);
+            const float3 c = trace_pixel<COUNT, ACC>(P, P.cam.eye[eye], d, pid, stk, cnt, s_occ + threadIdx.x);
             const long long pix = ((long long)eye * P.H + py) * P.W + px;
             if (P.fb[eye]) store_px(P.fb[eye], P.fb_fmt[eye], P.fb_pitch[eye], px, py, c);
             if (P.prim_id) P.prim_id[pix] = pid;
@@ -367,9 +368,15 @@ __global__ void __launch_bounds__(256) k_ffma_peak(float* out, int iters, float 
 using namespace rtb;
 
 static const void* trace_fn(unsigned flags) {
-    const bool count = flags & RT_RENDER_COUNT, brute = flags & RT_RENDER_BRUTE_FORCE;
-    return count ? (brute ? (const void*)k_trace_stereo<true, true> : (const void*)k_trace_stereo<true, false>)
-                 : (brute ? (const void*)k_trace_stereo<false, true> : (const void*)k_trace_stereo<false, false>);
+    const bool count = flags & RT_RENDER_COUNT;
+    const int acc = (flags & RT_RENDER_BRUTE_FORCE) ? ACC_BRUTE : (flags & RT_RENDER_KDTREE) ? ACC_KD : ACC_BVH;
+    if (count)
+        return acc == ACC_BRUTE ? (const void*)k_trace_stereo<true, ACC_BRUTE>
+             : acc == ACC_KD    ? (const void*)k_trace_stereo<true, ACC_KD>
+                                : (const void*)k_trace_stereo<true, ACC_BVH>;
+    return acc == ACC_BRUTE ? (const void*)k_trace_stereo<false, ACC_BRUTE>
+         : acc == ACC_KD    ? (const void*)k_trace_stereo<false, ACC_KD>
+                            : (const void*)k_trace_stereo<false, ACC_BVH>;
 }
 
 size_t rtb_trace_smem(int stack_entries) {

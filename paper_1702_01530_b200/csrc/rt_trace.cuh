@@ -456,13 +456,118 @@ __device__ __forceinline__ bool plain_push8(unsigned m, const float4* __restrict
     return true;
 }
 
+
+// ---------------------------------------------------------------- NEXT-4: kd-tree ablation
+// Stack traversal of the host-built kd-tree (rt_kdtree.cu): front-to-back cells, each split
+// distance widened by the slab test's margin m |1/d_axis| on both sides, so every leaf cell a
+// hit can lie in is visited; cells are pruned only when their (widened) entry lies beyond the
+// best hit (t_entry <= t_best survives, as in the BVH), and leaf references are tested with the
+// same primitive test.  Nearest (t, ID) hits therefore equal brute force exactly.
+enum { ACC_BVH = 0, ACC_BRUTE = 1, ACC_KD = 2 };
+constexpr int KD_STACK = 64;
+
+struct KdRay {
+    float o[3], id[3], m;
+};
+
+// root interval [t0, t1] of the kd cell (conservative), false if the ray misses it
+__device__ __forceinline__ bool kd_setup(const DevScene& S, float3 o, float3 d, float tmax, KdRay& k, float& t0, float& t1) {
+    const RayBox rb = make_raybox(o, d, S.bound);
+    const float nx = rb.sx ? S.kd_hi.x : S.kd_lo.x, fx = rb.sx ? S.kd_lo.x : S.kd_hi.x;
+    const float ny = rb.sy ? S.kd_hi.y : S.kd_lo.y, fy = rb.sy ? S.kd_lo.y : S.kd_hi.y;
+    const float nz = rb.sz ? S.kd_hi.z : S.kd_lo.z, fz = rb.sz ? S.kd_lo.z : S.kd_hi.z;
+    t0 = fmaxf(fmaxf(fmaf(nx, rb.idir.x, rb.cn.x), fmaf(ny, rb.idir.y, rb.cn.y)), fmaxf(fmaf(nz, rb.idir.z, rb.cn.z), 0.0f));
+    t1 = fminf(fminf(fmaf(fx, rb.idir.x, rb.cf.x), fmaf(fy, rb.idir.y, rb.cf.y)), fminf(fmaf(fz, rb.idir.z, rb.cf.z), tmax));
+    k.o[0] = o.x; k.o[1] = o.y; k.o[2] = o.z;
+    k.id[0] = rb.idir.x; k.id[1] = rb.idir.y; k.id[2] = rb.idir.z;
+    k.m = 1e-6f * (fabsf(o.x) + fabsf(o.y) + fabsf(o.z) + S.bound);
+    return t0 <= t1;
+}
+
+// ANY: stop at the first primitive with t_min < t < limit.  Otherwise nearest hit into h.
+template <bool COUNT, bool ANY>
+__device__ __forceinline__ bool kd_trace(const DevScene& S, float3 o, float3 d, float limit, Hit& h, Counters<COUNT>& cnt,
+                                         int* hint) {
+    KdRay k;
+    float t0, t1;
+    if (!kd_setup(S, o, d, limit, k, t0, t1)) return false;
+    int st_node[KD_STACK];
+    float st_t0[KD_STACK], st_t1[KD_STACK];
+    int sp = 0;
+    int node = 0;
+    while (true) {
+        int2 n = __ldg(&S.kd_nodes[node]);
+        while ((n.x & 3) != 3) {
+            cnt.add(CNT_NODE_VISITS);
+            const int axis = n.x & 3;
+            const float oa = axis == 0 ? k.o[0] : (axis == 1 ? k.o[1] : k.o[2]);
+            const float ia = axis == 0 ? k.id[0] : (axis == 1 ? k.id[1] : k.id[2]);
+            const float ts = (__int_as_float(n.y) - oa) * ia;
+            const float e = k.m * fabsf(ia);
+            const float ts_lo = ts - e, ts_hi = ts + e;
+            const int left = node + 1, right = n.x >> 2;
+            const int nearc = ia >= 0.0f ? left : right, farc = ia >= 0.0f ? right : left;
+            const float tcut = ANY ? t1 : fminf(t1, h.t);
+            const bool vn = t0 <= fminf(tcut, ts_hi);
+            const bool vf = fmaxf(t0, ts_lo) <= tcut;
+            if (vn && vf) {
+                if (sp < KD_STACK) {
+                    st_node[sp] = farc; st_t0[sp] = fmaxf(t0, ts_lo); st_t1[sp] = t1; ++sp;
+                }
+                node = nearc;
+                t1 = fminf(t1, ts_hi);
+            } else if (vn) {
+                node = nearc;
+                t1 = fminf(t1, ts_hi);
+            } else if (vf) {
+                node = farc;
+                t0 = fmaxf(t0, ts_lo);
+            } else {
+                node = -1;
+                break;
+            }
+            n = __ldg(&S.kd_nodes[node]);
+        }
+        if (node >= 0) {
+            const int cnt_refs = n.x >> 2, first = n.y;
+            for (int i = 0; i < cnt_refs; ++i) {
+                const int kk = __ldg(&S.kd_refs[first + i]);
+                float t;
+                int gid;
+                if (prim_t<COUNT>(S, kk, o, d, t, gid, cnt)) {
+                    if (ANY) {
+                        if (t < limit) {
+                            if (hint) *hint = kk;
+                            return true;
+                        }
+                    } else if (t < h.t || (t == h.t && gid < h.gid)) {
+                        h.t = t; h.gid = gid; h.slot = kk;
+                    }
+                }
+            }
+        }
+        // next cell: front-to-back pops, pruned by the best hit so far
+        bool found = false;
+        while (sp > 0) {
+            --sp;
+            if (st_t0[sp] <= (ANY ? st_t1[sp] : fminf(st_t1[sp], h.t))) {
+                node = st_node[sp]; t0 = st_t0[sp]; t1 = st_t1[sp];
+                found = true;
+                break;
+            }
+        }
+        if (!found) return false;
+    }
+}
+
 // Nearest hit over the 4-wide BVH (or every BVH primitive when BRUTE) and the planes.
 // Acceptance: t > t_min and (t, gid) lexicographically smallest (reading 9).
 // Children are visited near-to-far: entry distances (>= 0, so their bit patterns order like
 // unsigned ints) carry the child slot in their 2 low bits and go through a 5-exchange sorting
 // network; the 3 farther hits are pushed on the shared-memory stack.
-template <bool COUNT, bool BRUTE>
+template <bool COUNT, int ACC>
 __device__ __forceinline__ Hit closest_hit(const DevScene& S, float3 o, float3 d, TravStack& stk, Counters<COUNT>& cnt) {
+    constexpr bool BRUTE = ACC == ACC_BRUTE;
     Hit h;
     h.t = __int_as_float(0x7f800000);
     h.gid = -1;
@@ -476,6 +581,10 @@ __device__ __forceinline__ Hit closest_hit(const DevScene& S, float3 o, float3 d
         }
     }
     if (S.n_bvh == 0) return h;
+    if constexpr (ACC == ACC_KD) {
+        kd_trace<COUNT, false>(S, o, d, __int_as_float(0x7f800000), h, cnt, nullptr);
+        return h;
+    }
     auto leaf_test = [&](int first, int last) {
         for (int k = first; k <= last; ++k) {
             float t;
@@ -526,9 +635,10 @@ __device__ __forceinline__ Hit closest_hit(const DevScene& S, float3 o, float3 d
 // null) holds the BVH slot of this thread's last occluder for the same light: it is tested first
 // and, if it blocks the segment, the answer is already exact (visibility is a boolean, so which
 // occluder proves it does not matter); otherwise the traversal runs and records its occluder.
-template <bool COUNT, bool BRUTE>
+template <bool COUNT, int ACC>
 __device__ __forceinline__ bool occluded(const DevScene& S, float3 o, float3 d, float dist, TravStack& stk, Counters<COUNT>& cnt,
                                          int* hint = nullptr) {
+    constexpr bool BRUTE = ACC == ACC_BRUTE;
     for (int i = 0; i < S.n_planes; ++i) {
         cnt.add(CNT_PLANE_TESTS);
         float t;
@@ -544,6 +654,11 @@ __device__ __forceinline__ bool occluded(const DevScene& S, float3 o, float3 d, 
         if (k >= 0 && prim_t<COUNT>(S, k, o, d, t, gid, cnt) && t < dist) return true;
     }
 #endif
+    if constexpr (ACC == ACC_KD) {
+        Hit h;
+        h.t = dist; h.gid = -1; h.slot = 0;
+        return kd_trace<COUNT, true>(S, o, d, dist, h, cnt, hint);
+    }
     auto leaf_test = [&](int first, int last) -> bool {
         for (int k = first; k <= last; ++k) {
             float t;

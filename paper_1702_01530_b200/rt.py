@@ -18,7 +18,7 @@ LIB_PATH = os.environ.get("RT_LIB_PATH") or os.path.join(_HERE, "lib", "librt_b2
 RT_OK, RT_ERR_INVALID_ARG, RT_ERR_CUDA, RT_ERR_OOM, RT_ERR_NO_SCENE, RT_ERR_NO_CAMERA, RT_ERR_SIZE, \
     RT_ERR_NOT_READY, RT_ERR_PEER = range(9)
 RT_FORMAT_RGBA8, RT_FORMAT_RGBA16F = 0, 1
-RT_RENDER_COUNT, RT_RENDER_BRUTE_FORCE, RT_RENDER_PEER_STORE = 1, 2, 4
+RT_RENDER_COUNT, RT_RENDER_BRUTE_FORCE, RT_RENDER_PEER_STORE, RT_RENDER_KDTREE = 1, 2, 4, 8
 RT_NUM_COUNTERS = 12
 RT_COMPOSE_ANAGLYPH, RT_COMPOSE_SBS = 0, 1
 RT_TILE = 16
@@ -30,7 +30,7 @@ EXPORTED = ["rt_create", "rt_destroy", "rt_synchronize", "rt_last_error", "rt_ve
             "rt_set_stereo_camera", "rt_render_stereo", "rt_render_stereo_ex", "rt_download", "rt_wait", "rt_query",
             "rt_host_alloc", "rt_host_free", "rt_upload", "rt_shard_tiles", "rt_shard_bytes", "rt_unpack_shards_host",
             "rt_unpack_shards", "rt_ipc_get_handle", "rt_ipc_open", "rt_ipc_close", "rt_scene_info", "rt_bvh_export",
-            "rt_bench_ffma", "rt_compose", "rt_scene_update_vertices", "rt_bvh_width"]
+            "rt_bench_ffma", "rt_compose", "rt_scene_update_vertices", "rt_bvh_width", "rt_kdtree_build"]
 
 
 class RtError(RuntimeError):
@@ -106,6 +106,7 @@ def lib():
             "rt_bench_ffma": [vp, u32, C.POINTER(C.c_double), C.POINTER(C.c_double)],
             "rt_compose": [vp, rt_fb, rt_fb, u32, u32, u32, rt_fb],
             "rt_scene_update_vertices": [vp, vp, u32],
+            "rt_kdtree_build": [vp, u32, u32, vp],
         }
         for name, args in sig.items():
             fn = getattr(L, name)
@@ -314,6 +315,14 @@ def rt_bvh_export(ctx):
     return nodes[:nn.value], gids[:npr.value]
 
 
+def rt_kdtree_build(ctx, max_leaf=1, max_depth=0):
+    """NEXT-4 ablation: host-built SAH kd-tree over the uploaded scene (see rt_b200.h)."""
+    a = np.zeros(6, np.uint64)
+    _check(lib().rt_kdtree_build(ctx, max_leaf, max_depth, a.ctypes.data))
+    keys = ["kd_nodes", "kd_refs", "kd_depth", "kd_leaves", "kd_device_bytes", "kd_build_us"]
+    return dict(zip(keys, (int(x) for x in a)))
+
+
 def rt_compose(ctx, left_fb, right_fb, width, height, mode, out_fb):
     _check(lib().rt_compose(ctx, left_fb, right_fb, width, height, mode, out_fb))
 
@@ -367,7 +376,7 @@ class StereoRenderer:
 
     def render(self, width, height, max_depth, fmt=RT_FORMAT_RGBA8, fb=None, want_id=False, want_radiance=False,
                count=False, brute=False, shard=(0, 1), shard_buf=None, shard_fmt=RT_FORMAT_RGBA8, fb_ptrs=None,
-               peer=False):
+               peer=False, kdtree=False):
         """Enqueue one stereo render; returns dict of torch device tensors (not synchronised)."""
         t = self.torch
         out = {}
@@ -401,6 +410,8 @@ class StereoRenderer:
             flags |= RT_RENDER_BRUTE_FORCE
         if peer:
             flags |= RT_RENDER_PEER_STORE
+        if kdtree:
+            flags |= RT_RENDER_KDTREE
         p = rt_render_params(width, height, max_depth, shard[0], shard[1], flags)
         rt_render_stereo_ex(self.ctx, p, o)
         if count:
