@@ -24,6 +24,8 @@ for s in (scenes.scene_c1(), scenes.scene_c2().with_view(width=40, height=30, ma
         fb = torch.zeros((2, s.height, s.width, 4), dtype=torch.uint8, device="cuda")
         rt.rt_unpack_shards(R.ctx, g.data_ptr(), s.width, s.height, world, 0,
                             rt.rt_fb(fb[0].data_ptr(), 0, s.width * 4), rt.rt_fb(fb[1].data_ptr(), 0, s.width * 4))
+    rt.rt_kdtree_build(R.ctx, 2, 0)                      # NEXT-4 kd-tree ablation kernel
+    R.render(s.width, s.height, s.max_depth, want_id=True, kdtree=True)
     if s.n_tris:
         rt.rt_scene_update_vertices(R.ctx, s.vertices * 1.01)
         R.render(s.width, s.height, s.max_depth)

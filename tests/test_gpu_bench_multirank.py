@@ -15,7 +15,10 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def test_bench_two_ranks_one_gpu():
+@pytest.mark.parametrize("world", [2, 4])
+def test_bench_ranks_one_gpu(world):
+    """world 2 = the eye split (shard mode 1); world 4 = tile pairs dealt round-robin (mode 2),
+    the layout of the 4- and 8-GPU scaling runs."""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     s = socket.socket()
@@ -23,15 +26,15 @@ def test_bench_two_ranks_one_gpu():
     port = s.getsockname()[1]
     s.close()
     env = dict(os.environ, RT_BENCH_SHARE_DEVICE="1")
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(world),
            "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
-           "--gpus", "2", "--steps", "5", "--warmup", "3", "--config", "C3", "--no-cpu-baseline"]
+           "--gpus", str(world), "--steps", "5", "--warmup", "3", "--config", "C3", "--no-cpu-baseline"]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
     assert r.returncode == 0, r.stderr[-3000:]
     lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
     assert len(lines) == 1
     b = lines[0]
-    assert b["n_gpus"] == 2 and b["config"]["gather"] == "peer" and b["value"] > 0
+    assert b["n_gpus"] == world and b["config"]["gather"] == "peer" and b["value"] > 0
     assert b["e2e"]["download_verified"] is True
     assert b["gpu_launches"] == 5
     for k in ("metric", "unit", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling", "dtype", "roofline",
