@@ -38,6 +38,9 @@ namespace rtb {
 #if RT_FAST_PUSH && !RT_SMEM_PTX
 #error "RT_FAST_PUSH needs RT_SMEM_PTX"
 #endif
+#ifndef RT_WW
+#define RT_WW 0            // while-while traversal: bit 0 nearest-hit rays, bit 1 any-hit rays (BVH4)
+#endif
 #ifndef RT_SHADOW_STATS
 #define RT_SHADOW_STATS 0  // 1: instrumented build records warp-level traversal divergence (experiments)
 #endif
@@ -602,6 +605,29 @@ __device__ __forceinline__ Hit closest_hit(const DevScene& S, float3 o, float3 d
     set_node_bases(rb, S.nodes);
     int sp = 0;
     int node = S.root;
+#if (RT_WW & 1) && RT_BVH_WIDTH == 4
+    // while-while (Aila & Laine 2009): a lane descends through inner nodes until it holds a
+    // leaf (or is done); the warp then tests the leaves of all lanes together, so the node and
+    // leaf code are not both issued in every step of a mixed warp
+    while (true) {
+        while (node >= 0) {
+            cnt.step();
+            cnt.add(CNT_NODE_VISITS);
+            float tn[4];
+            int4 ch;
+            const unsigned m = node4_hits(S.nodes, node, rb, h.t, tn, ch);
+            if (order_push(m, tn, ch, stk, sp, node)) continue;
+            if (sp == 0) return h;
+            node = stk.get(--sp);
+        }
+        cnt.step();
+        const int enc = ~node;
+        const int first = enc & ((1 << LEAF_SHIFT) - 1);
+        leaf_test(first, first + (enc >> LEAF_SHIFT));
+        if (sp == 0) return h;
+        node = stk.get(--sp);
+    }
+#endif
     while (true) {
         cnt.step();
         if (node >= 0) {
@@ -677,6 +703,26 @@ __device__ __forceinline__ bool occluded(const DevScene& S, float3 o, float3 d, 
     set_node_bases(rb, S.nodes);
     int sp = 0;
     int node = S.root;
+#if (RT_WW & 2) && RT_BVH_WIDTH == 4 && !RT_SHADOW_SORT
+    while (true) {
+        while (node >= 0) {
+            cnt.step();
+            cnt.add(CNT_NODE_VISITS);
+            float tn[4];
+            int4 ch;
+            const unsigned m = node4_hits(S.nodes, node, rb, dist, tn, ch);
+            if (plain_push(m, ch, stk, sp, node)) continue;
+            if (sp == 0) return false;
+            node = stk.get(--sp);
+        }
+        cnt.step();
+        const int enc = ~node;
+        const int first = enc & ((1 << LEAF_SHIFT) - 1);
+        if (leaf_test(first, first + (enc >> LEAF_SHIFT))) return true;
+        if (sp == 0) return false;
+        node = stk.get(--sp);
+    }
+#endif
     while (true) {
         cnt.step();
         if (node >= 0) {
