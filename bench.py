@@ -185,12 +185,13 @@ class SingleFrame:
 
     mode = "single"
     launches_per_frame = 1
+    pipelined = True
 
     def __init__(self, R, fb, width, height):
         self.R, self.fb, self.W, self.H = R, fb, width, height
 
-    def render(self, depth):
-        self.R.render(self.W, self.H, depth, fb=self.fb)
+    def render(self, depth, stream=None):
+        self.R.render(self.W, self.H, depth, fb=self.fb, stream=stream)
 
     def assemble(self):
         pass
@@ -250,6 +251,15 @@ def run_ours(args, scene):
     fb = R.alloc_fb(W, H)                                    # root framebuffers (2, H, W, 4) u8
     frame = SingleFrame(R, fb, W, H) if world == 1 else multigpu.make_frame(args.gather, R, fb, rank, world, dist, W, H)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+    # frames in flight: F framebuffer slots (each its own peer mapping for N>1) and F streams
+    F = max(1, args.inflight) if frame.pipelined else 1
+    fbs = [fb] + [R.alloc_fb(W, H) for _ in range(F - 1)]
+    frames = [frame] + [SingleFrame(R, fbs[i], W, H) if world == 1
+                        else multigpu.make_frame(frame.mode, R, fbs[i], rank, world, dist, W, H) for i in range(1, F)]
+    streams = [torch.cuda.Stream(device=dev) for _ in range(F)]
+    hb = None
+    if world > 1:                                            # host-only barrier (gloo): never syncs a device
+        hb = dist.group.WORLD if share else dist.new_group(backend="gloo")
 
     for _ in range(max(3, args.warmup)):
         frame.render(D)
@@ -257,6 +267,8 @@ def run_ours(args, scene):
     torch.cuda.synchronize()
     barrier()
 
+    # ---- (1) frame latency: one frame at a time, L2 flushed before each (untimed); the trace
+    # kernel's own duration per launch (roofline) and the frame time a single frame sees
     ev_s = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ev_k = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]   # after the trace kernel
     ev_e = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -273,18 +285,67 @@ def run_ours(args, scene):
         ev_e[k].record()
     torch.cuda.synchronize()
     barrier()
-    clocks = clk.stop()
     step_ms = np.array([ev_s[k].elapsed_time(ev_e[k]) for k in range(args.steps)])
     kern_ms = np.array([ev_s[k].elapsed_time(ev_k[k]) for k in range(args.steps)])
     t = torch.tensor([step_ms.sum(), kern_ms.mean(), np.median(step_ms), step_ms.min()], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms = float(t[0])
+    lat_total_ms = float(t[0])
     med_ms, best_ms = float(t[2]), float(t[3])
+
+    # ---- (2) throughput: K frames with F in flight on F streams (rt_render_stereo_async), the
+    # L2 flush (256 MiB write) enqueued before every frame on its own stream and timed with it
+    # (it overlaps the other frames, so it cannot be left out).  A frame's pixel trees end in a
+    # latency-bound tail (the deepest trees: ~0.7 ms for C4 even on an idle GPU);
+    # frames in flight fill the SMs that tail would leave idle.  For N>1 a rank starts frame k
+    # only after every rank finished frame k-F+1 (host gloo barrier, lagging so the device
+    # always has queued frames): the slot frame k overwrites is then fully assembled.
+    if F > 1:
+        lag = F - 1
+
+        def pipe_step(k, done):
+            slot = k % F
+            if world > 1 and k >= lag:
+                done.pop(k - lag).synchronize()
+                dist.barrier(group=hb)
+            with torch.cuda.stream(streams[slot]):
+                flush.zero_()
+            frames[slot].render(D, streams[slot])
+            e = torch.cuda.Event()
+            e.record(streams[slot])
+            done[k] = e
+
+        done = {}
+        for k in range(max(3, args.warmup)):
+            pipe_step(k, done)
+        torch.cuda.synchronize()
+        barrier()
+        done = {}
+        t_start = torch.cuda.Event(enable_timing=True)
+        t_start.record()
+        for x in streams:
+            x.wait_event(t_start)
+        for k in range(args.steps):
+            pipe_step(k, done)
+        t_end = []
+        for x in streams:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(x)
+            t_end.append(e)
+        torch.cuda.synchronize()
+        barrier()
+        total_ms = max(t_start.elapsed_time(e) for e in t_end)
+        tt = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total_ms = float(tt[0])
+    else:
+        total_ms = lat_total_ms
+    clocks = clk.stop()
     ms_per_step = total_ms / args.steps
 
     # ---- end-to-end through the public C ABI with host buffers (camera in, frame out)
-    e2e = run_e2e(args, R, scene, rank, world, frame, fb, dev, rays_total) if not args.no_e2e else None
+    e2e = run_e2e(args, R, scene, rank, world, frames, fbs, streams, hb, dev, rays_total) if not args.no_e2e else None
 
     # ---- FFMA peak measured live (context for the roofline denominator)
     ffma_tflops, _ = rt.rt_bench_ffma(R.ctx, 2048)
@@ -293,7 +354,9 @@ def run_ours(args, scene):
         value = rays_total / (ms_per_step * 1e-3) / 1e6
         sm_max = clocks.get("sm_max_mhz") or 1965.0
         peak = 148 * FP32_LANES_PER_SM * 2 * sm_max * 1e6 / 1e12
-        achieved = my_flops / (float(kern_ms.mean()) * 1e-3) / 1e12
+        # sustained rate of the timed region (frames overlap, so a launch's own duration is the
+        # isolated one, reported beside it)
+        achieved = my_flops / (ms_per_step * 1e-3) / 1e12
         traffic = load_traffic(scene.name, world)
         par = f"tile-sharded x{world}" + {"single": "", "peer": " + fused peer-store gather to rank 0 (CUDA IPC over NVLink)",
                                           "nccl": " + NCCL gather to rank 0 + unpack"}[frame.mode]
@@ -305,21 +368,24 @@ def run_ours(args, scene):
             "config": {"workload": workload_desc(scene), "width": W, "height": H, "max_depth": D,
                        "triangles": scene.n_tris, "rays_per_step": rays_total,
                        "rays_by_type": {k: tot[k] for k in ("primary", "reflection", "refraction", "shadow")},
-                       "parallelism": par, "gather": frame.mode,
-                       "l2": "flushed (256 MiB write) between timed steps; scene+BVH "
-                             f"{info['device_bytes'] / 1e6:.0f} MB"},
+                       "parallelism": par, "gather": frame.mode, "frames_in_flight": F,
+                       "l2": ("flushed (256 MiB write) before every timed frame, on the frame's stream and inside "
+                              "the timed region" if F > 1 else "flushed (256 MiB write) between timed steps")
+                             + f"; scene+BVH {info['device_bytes'] / 1e6:.0f} MB"},
             "stereo_fps": 1e3 / ms_per_step,
-            "ms_median": med_ms, "ms_best": best_ms,
-            "mrays_median": rays_total / (med_ms * 1e-3) / 1e6, "mrays_best": rays_total / (best_ms * 1e-3) / 1e6,
+            "frame_latency": {"ms_mean": lat_total_ms / args.steps, "ms_median": med_ms, "ms_best": best_ms,
+                              "mrays_s": rays_total / (lat_total_ms / args.steps * 1e-3) / 1e6,
+                              "note": "one frame at a time, L2 flushed before each (untimed)"},
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "k_trace_stereo", "kernel_ms": float(kern_ms.mean()),
-                         "kernel_share_of_step": float(kern_ms.mean()) / ms_per_step,
+                         "kernel": "k_trace_stereo", "kernel_ms": ms_per_step,
+                         "kernel_ms_isolated": float(t[1]),
+                         "kernel_share_of_step": float(t[1]) / (lat_total_ms / args.steps),
                          "algorithmic_flops_per_launch": my_flops,
                          "peak_basis": f"148 SM x 128 FP32 lanes x 2 x {sm_max:.0f} MHz (sm_max; B200_PROFILING "
                                        f"unit counts); live FFMA microbenchmark {ffma_tflops:.1f} TFLOP/s"},
             "clocks": clocks,
-            "gpu_launches": args.steps * frame.launches_per_frame,
+            "gpu_launches": args.steps * frame.launches_per_frame,   # in the throughput region
             "scene_upload_ms": upload_ms, "bvh": info,
             "work_counts": tot,
         }
@@ -328,7 +394,8 @@ def run_ours(args, scene):
         if not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(scene, target_s=args.cpu_seconds)
         print(json.dumps(line), flush=True)
-    frame.close()
+    for f in frames:
+        f.close()
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
@@ -336,12 +403,14 @@ def run_ours(args, scene):
     return 0
 
 
-def run_e2e(args, R, scene, rank, world, frame, fb, dev, rays_total):
+def run_e2e(args, R, scene, rank, world, frames, fbs, streams, hb, dev, rays_total):
     """Same metric through the public C ABI: every step sets the camera from host values
     (rt_set_stereo_camera), renders (+ assembles on rank 0 for N>1) and downloads the finished
-    stereo frame into pinned host memory with rt_download (copy stream, overlapped with the next
-    frame's render).  Two framebuffer slots alternate; a slot is re-rendered only after its
-    previous download completed."""
+    stereo frame into pinned host memory (rt_download_after, copy stream, overlapped with the
+    frames still rendering).  With F frames in flight each frame renders on its slot's stream
+    into its slot's framebuffers; a slot is re-rendered only after its previous download
+    completed (and, for N>1, after every rank finished the frame a lag of F-1 frames back, by a
+    host gloo barrier that never waits on a device)."""
     import ctypes
 
     import torch
@@ -349,8 +418,9 @@ def run_e2e(args, R, scene, rank, world, frame, fb, dev, rays_total):
     from paper_1702_01530_b200 import rt
 
     W, H, D = scene.width, scene.height, scene.max_depth
+    F = len(frames)
     nbytes = 2 * H * W * 4
-    hosts = [rt.rt_host_alloc(nbytes) for _ in range(2)] if rank == 0 else []
+    hosts = [rt.rt_host_alloc(nbytes) for _ in range(F)] if rank == 0 else []
     # C5: sustained camera orbit, frame k uses orbit camera k mod 60; the rays of
     # every orbit frame are counted up front (instrumented pass, untimed)
     orbit = scene.name.startswith("C5")
@@ -369,62 +439,79 @@ def run_e2e(args, R, scene, rank, world, frame, fb, dev, rays_total):
                 import torch.distributed as dist
                 dist.all_reduce(v)
             rays_of[k] = int(v.item())
-    pending = [None, None]
-    fb2 = R.alloc_fb(W, H)
-    fbs = [fb, fb2]
-    frames = [frame]
     if world > 1:
         import torch.distributed as dist
-        from paper_1702_01530_b200 import multigpu
-        frames.append(multigpu.make_frame(frame.mode, R, fb2, rank, world, dist, W, H))
+    pending = [None] * F
+    done = {}
+    lag = F - 1
+
+    def finish(j):
+        """frame j is complete on every rank: rank 0 downloads it"""
+        slot = j % F
+        if world > 1 and F > 1:
+            done.pop(j).synchronize()
+            dist.barrier(group=hb)
+        else:
+            done.pop(j, None)
+        if rank == 0:
+            pending[slot] = rt.rt_download_after(R.ctx, fbs[slot].data_ptr(), hosts[slot], nbytes,
+                                                 streams[slot].cuda_stream if F > 1 else None)
 
     def frame_step(k):
-        slot = k % 2
-        if pending[slot] is not None:
-            rt.rt_wait(pending[slot])                         # slot's previous download is done
+        slot = k % F
+        if rank == 0 and pending[slot] is not None:
+            rt.rt_wait(pending[slot])                          # the slot's previous frame is on the host
             pending[slot] = None
         if world > 1:
-            dist.barrier()                                     # ... before any rank writes that slot again
+            if F > 1:
+                if k >= lag:
+                    finish(k - lag)
+            else:
+                dist.barrier()                                 # ... before any rank writes the slot again
         rig = rigs[k % n_rig]
         rt.rt_set_stereo_camera(R.ctx, rig.eye, rig.look_at, rig.up, rig.vfov_deg, rig.interocular,
                                 rig.convergence)
-        dst = fbs[slot]
-        if world == 1:
-            pitch = W * 4
-            rt.rt_render_stereo(R.ctx, W, H, D, rt.rt_fb(dst[0].data_ptr(), 0, pitch), rt.rt_fb(dst[1].data_ptr(), 0, pitch))
+        if F > 1:
+            frames[slot].render(D, streams[slot])
+            e = torch.cuda.Event()
+            e.record(streams[slot])
+            done[k] = e
         else:
             frames[slot].render(D)
             frames[slot].assemble()
-        if rank == 0:
-            pending[slot] = rt.rt_download(R.ctx, dst.data_ptr(), hosts[slot], nbytes)
+            done[k] = None
+        if world == 1 or F == 1:
+            finish(k)
+
+    def drain():
+        for j in sorted(done):
+            finish(j)
+        for i in range(F):
+            if pending[i] is not None:
+                rt.rt_wait(pending[i])
+                pending[i] = None
 
     for k in range(max(3, args.warmup)):
         frame_step(k)
-    for i in range(2):
-        if pending[i] is not None:
-            rt.rt_wait(pending[i])
-            pending[i] = None
+    drain()
     rt.rt_synchronize(R.ctx)
+    torch.cuda.synchronize()
     if world > 1:
-        import torch.distributed as dist
         dist.barrier()
     t0 = time.perf_counter()
     for k in range(args.steps):
         frame_step(k)
-    for i in range(2):
-        if pending[i] is not None:
-            rt.rt_wait(pending[i])
-            pending[i] = None
+    drain()
     rt.rt_synchronize(R.ctx)
     dt = time.perf_counter() - t0
     tt = torch.tensor([dt], dtype=torch.float64, device=dev)
     if world > 1:
-        import torch.distributed as dist
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     dt = float(tt[0])
     # paper-structure stage split (PAPER.md:15, :106-107 -- ~60 % compute / up to 40 % transfer on
     # the paper's GPU): serialised render vs download times of one frame on this box
     stages = None
+    fb = fbs[0]
     if rank == 0 and world == 1:
         rt.rt_synchronize(R.ctx)
         t0 = time.perf_counter()
@@ -440,26 +527,27 @@ def run_e2e(args, R, scene, rank, world, frame, fb, dev, rays_total):
                   "transfer_fraction_serialised": d_ms / (r_ms + d_ms),
                   "transfer_hidden_by_overlap": True,
                   "paper": "~60 % compute / up to 40 % CPU<->GPU transfer (PAPER.md:15, :106-107), unnamed NVIDIA GPU"}
+        # the stage split re-rendered slot 0: download it again so the check below sees a pair
+        rt.rt_wait(rt.rt_download(R.ctx, fb.data_ptr(), hosts[0], nbytes))
     ok = True
     if rank == 0:
-        slot = (args.steps - 1) % 2
+        slot = (args.steps - 1) % F
         src = fbs[slot]
         host = np.frombuffer((ctypes.c_uint8 * nbytes).from_address(hosts[slot]), np.uint8)
         ok = bool(np.array_equal(host, src.reshape(-1).cpu().numpy()))
         for h in hosts:
             rt.rt_host_free(h)
-    for f in frames[1:]:
-        f.close()
     rays_timed = sum(rays_of[k % n_rig] for k in range(args.steps))
     return {"value": rays_timed / dt / 1e6, "unit": UNIT,
             "camera": "C5 orbit: frame k uses orbit camera k mod 60 (rays counted per orbit frame)" if orbit
             else "fixed (the config's rig)",
             "h2d_bytes_per_step": 76, "d2h_bytes_per_step": nbytes if rank == 0 else 0,
             "ms_per_step": dt / args.steps * 1e3, "stereo_fps": args.steps / dt, "download_verified": ok,
-            "stages": stages,
+            "frames_in_flight": F, "stages": stages,
             "note": "per step: camera set from host values (the 76-byte camera block travels in the kernel "
-                    "launch parameters), render, pinned async D2H (rt_download, copy stream) of the RGBA8 stereo "
-                    "frame overlapped with the next render; host wall clock around K steps incl. the last download"}
+                    "launch parameters), render, pinned async D2H (rt_download_after, copy stream) of the RGBA8 "
+                    "stereo frame overlapped with the frames still rendering; host wall clock around K steps incl. "
+                    "the last download"}
 
 
 def load_traffic(name, world):
@@ -484,6 +572,8 @@ def main():
                     help="N>1 frame assembly: fused peer stores into rank 0's FB (default) or NCCL gather")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--inflight", type=int, default=4,
+                    help="frames in flight on separate streams in the throughput loop (1 = one at a time)")
     args = ap.parse_args()
     scene = scenes.make_scene(args.config)
     if args.impl == "reference":

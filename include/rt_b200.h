@@ -197,6 +197,16 @@ rt_status rt_render_stereo(rt_context* ctx, uint32_t width, uint32_t height, uin
  * the shard are not written. */
 rt_status rt_render_stereo_ex(rt_context* ctx, const rt_render_params* params, const rt_outputs* out);
 
+/* rt_render_stereo_ex enqueued on `cuda_stream` (a cudaStream_t of the context's device; NULL =
+ * the context stream) instead of the context stream: frames in flight.  Renders on different
+ * streams may run concurrently on the device (up to 16 in flight: each takes its own work
+ * queue), so the tail of one frame -- the last, deepest pixel trees, during which most SMs
+ * would idle -- overlaps the next frame's work.  The scene and camera are read at enqueue time;
+ * rt_scene_upload / rt_scene_update_vertices must not run while renders are in flight.  The
+ * caller orders reuse of output buffers (stream order or events).  Errors as rt_render_stereo_ex. */
+rt_status rt_render_stereo_async(rt_context* ctx, const rt_render_params* params, const rt_outputs* out,
+                                 void* cuda_stream);
+
 /* ------------------------------------------------------------------ download */
 /* PAPER.md:15,107 (the CPU<->GPU transfer stage).  Asynchronous device->host copy of
  * `bytes` from DEVICE `dev_src` into PINNED host `host_dst` (rt_host_alloc or
@@ -207,6 +217,10 @@ rt_status rt_render_stereo_ex(rt_context* ctx, const rt_render_params* params, c
 rt_status rt_download(rt_context* ctx, const void* dev_src, void* host_dst, size_t bytes,
                       rt_event** done);
 /* Block until ev completes, then free it. */
+/* rt_download ordered after the work enqueued so far on `after_stream` (e.g. the stream a frame
+ * was rendered on with rt_render_stereo_async; NULL = the context stream). */
+rt_status rt_download_after(rt_context* ctx, const void* dev_src, void* host_dst, size_t bytes, void* after_stream,
+                            rt_event** done);
 rt_status rt_wait(rt_event* ev);
 /* RT_OK if ev has completed (ev stays valid), RT_ERR_NOT_READY otherwise. */
 rt_status rt_query(rt_event* ev);

@@ -67,7 +67,8 @@ struct rt_context {
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t order_ev = nullptr;
     int num_sms = 148;
-    int* work_counter = nullptr;
+    int* work_counter = nullptr;    // [64]: 16 rotating render queues, 4 ints apart
+    unsigned render_seq = 0;
     unsigned long long* scratch_counters = nullptr;
     float* ffma_out = nullptr;
     // scene
@@ -82,6 +83,8 @@ struct rt_context {
     int leaf_max = 1;                // LBVH leaf collapse threshold (env RT_LEAF_MAX, <= 16)
     int treelet_passes = 3;          // SAH treelet restructuring passes (env RT_TREELETS)
     int grid_limit = 0;              // cap on trace CTAs (env RT_GRID_LIMIT; 0 = full machine)
+    int l2_prefetch = 0;             // bulk L2 prefetch of the scene at each render (env RT_L2_PREFETCH=1;
+                                     // measured no gain, +40 % DRAM reads)
     void* arena = nullptr;           // BVH build scratch (grow-only)
     size_t arena_bytes = 0;
     // refit state (rt_scene_update_vertices)
@@ -145,6 +148,7 @@ rt_status rt_create(int device, void* cuda_stream, rt_context** out) {
     if (const char* lm = getenv("RT_LEAF_MAX")) c->leaf_max = std::max(1, std::min(16, atoi(lm)));
     if (const char* tp = getenv("RT_TREELETS")) c->treelet_passes = std::max(0, std::min(8, atoi(tp)));
     if (const char* gl = getenv("RT_GRID_LIMIT")) c->grid_limit = std::max(0, atoi(gl));
+    if (const char* lp = getenv("RT_L2_PREFETCH")) c->l2_prefetch = atoi(lp) != 0;
     cudaError_t e = cudaSetDevice(device);
     if (e == cudaSuccess && cuda_stream) {
         c->stream = static_cast<cudaStream_t>(cuda_stream);
@@ -593,8 +597,22 @@ rt_status check_fb(const rt_fb& fb, uint32_t W, const char* name) {
 
 extern "C" {
 
+namespace {
+rt_status render_impl(rt_context* c, const rt_render_params* p, const rt_outputs* out, cudaStream_t stream);
+}
+
 rt_status rt_render_stereo_ex(rt_context* c, const rt_render_params* p, const rt_outputs* out) {
     if (!c || !p || !out) return fail(RT_ERR_INVALID_ARG, "rt_render_stereo_ex: NULL argument");
+    return render_impl(c, p, out, c->stream);
+}
+
+rt_status rt_render_stereo_async(rt_context* c, const rt_render_params* p, const rt_outputs* out, void* cuda_stream) {
+    if (!c || !p || !out) return fail(RT_ERR_INVALID_ARG, "rt_render_stereo_async: NULL argument");
+    return render_impl(c, p, out, cuda_stream ? static_cast<cudaStream_t>(cuda_stream) : c->stream);
+}
+
+namespace {
+rt_status render_impl(rt_context* c, const rt_render_params* p, const rt_outputs* out, cudaStream_t stream) {
     if (!c->has_scene) return fail(RT_ERR_NO_SCENE, "render before rt_scene_upload");
     if (!c->has_camera) return fail(RT_ERR_NO_CAMERA, "render before rt_set_stereo_camera");
     const uint32_t W = p->width, H = p->height;
@@ -619,7 +637,9 @@ rt_status rt_render_stereo_ex(rt_context* c, const rt_render_params* p, const rt
     P.W = (int)W;
     P.H = (int)H;
     P.max_depth = (int)p->max_depth;
-    P.work_counter = c->work_counter;
+    // a work counter per render in flight (16 slots, rotated): renders enqueued on different
+    // streams may run concurrently and must not share a queue
+    P.work_counter = c->work_counter + 4 * (c->render_seq++ % 16);
     const ShardGeom g = shard_geom(W, H, p->shard_world);
     const uint64_t n_tiles = shard_count(g, p->shard_rank, p->shard_world);
     if (n_tiles * 256ull >= (1ull << 31)) return fail(RT_ERR_SIZE, "too many pixels in one shard");
@@ -643,6 +663,13 @@ rt_status rt_render_stereo_ex(rt_context* c, const rt_render_params* p, const rt
     P.stack_entries = (rtb::BVH_W - 1) * (int)c->info[5] + 2;   // <= W-1 pending siblings per level
     if (P.stack_entries > rtb::STACK_CAP) return fail(RT_ERR_SIZE, "BVH too deep (%d levels)", (int)c->info[5]);
     P.n_tiles = (int)n_tiles;
+    if (c->l2_prefetch && c->sc.n_bvh > 0) {
+        P.pf_base[0] = reinterpret_cast<const char*>(c->sc.nodes);
+        P.pf_bytes[0] = c->sc.nodes ? (unsigned long long)c->info[4] * rtb::NODE_F4 * 16 : 0;
+        P.pf_base[1] = reinterpret_cast<const char*>(c->sc.prims);
+        P.pf_bytes[1] = (unsigned long long)c->sc.n_bvh * 48;
+        if (!P.pf_base[0]) { P.pf_base[0] = P.pf_base[1]; P.pf_bytes[0] = P.pf_bytes[1]; P.pf_bytes[1] = 0; }
+    }
     P.peer_fence = (p->flags & RT_RENDER_PEER_STORE) ? 1 : 0;
     if (P.n_work == 0) return RT_OK;
     CUDA_TRY(cudaSetDevice(c->device));
@@ -650,13 +677,15 @@ rt_status rt_render_stereo_ex(rt_context* c, const rt_render_params* p, const rt
     const unsigned kflags = p->flags & (RT_RENDER_COUNT | RT_RENDER_BRUTE_FORCE | RT_RENDER_KDTREE);
     CUDA_TRY(rtb_trace_occupancy(kflags, P.stack_entries, &occ));
     if (occ < 1) occ = 1;
-    const long long max_blocks = ((long long)P.n_work + 255) / 256;
+    const int block = rtb_trace_block();
+    const long long max_blocks = ((long long)P.n_work + block - 1) / block;
     int grid = (int)std::min<long long>((long long)c->num_sms * occ, std::max<long long>(1, max_blocks));
     if (c->grid_limit > 0) grid = std::min(grid, c->grid_limit);   // experiment knob (paper's "network size")
-    CUDA_TRY(cudaMemsetAsync(c->work_counter, 0, sizeof(int), c->stream));
-    CUDA_TRY(rtb_launch_trace(P, kflags, grid, c->stream));
+    CUDA_TRY(cudaMemsetAsync(P.work_counter, 0, sizeof(int), stream));
+    CUDA_TRY(rtb_launch_trace(P, kflags, grid, stream));
     return RT_OK;
 }
+}  // namespace
 
 rt_status rt_render_stereo(rt_context* c, uint32_t width, uint32_t height, uint32_t max_depth, rt_fb out_left,
                            rt_fb out_right) {
@@ -699,11 +728,16 @@ static bool is_pinned(const void* p) {
 }
 
 rt_status rt_download(rt_context* c, const void* dev_src, void* host_dst, size_t bytes, rt_event** done) {
+    return rt_download_after(c, dev_src, host_dst, bytes, nullptr, done);
+}
+
+rt_status rt_download_after(rt_context* c, const void* dev_src, void* host_dst, size_t bytes, void* after_stream,
+                            rt_event** done) {
     if (done) *done = nullptr;
     if (!c || !dev_src || !host_dst || !bytes) return fail(RT_ERR_INVALID_ARG, "rt_download: NULL pointer or zero size");
     CUDA_TRY(cudaSetDevice(c->device));
     if (!is_pinned(host_dst)) return fail(RT_ERR_INVALID_ARG, "rt_download: host_dst is not pinned host memory");
-    CUDA_TRY(cudaEventRecord(c->order_ev, c->stream));
+    CUDA_TRY(cudaEventRecord(c->order_ev, after_stream ? static_cast<cudaStream_t>(after_stream) : c->stream));
     CUDA_TRY(cudaStreamWaitEvent(c->copy_stream, c->order_ev, 0));
     CUDA_TRY(cudaMemcpyAsync(host_dst, dev_src, bytes, cudaMemcpyDeviceToHost, c->copy_stream));
     if (done) {

@@ -43,6 +43,8 @@ struct TraceParams {
     unsigned long long* counters;
     int stack_entries;      // BVH traversal stack depth (shared memory, [entry][thread])
     int n_tiles;            // 16x16 tiles in this shard (= n_work / 256)
+    const char* pf_base[2]; // L2 prefetch at kernel start: BVH nodes, primitive records (null = off)
+    unsigned long long pf_bytes[2];
     int peer_fence;         // framebuffers live in a peer's memory: fence system-wide at exit
 };
 
@@ -107,6 +109,7 @@ void kd_build_host(const float4* prims, int n, int n_spheres, int max_leaf, int 
 cudaError_t rtb_launch_trace(const TraceParams& P, unsigned flags, int grid, cudaStream_t st);
 cudaError_t rtb_trace_occupancy(unsigned flags, int stack_entries, int* blocks_per_sm);
 size_t rtb_trace_smem(int stack_entries);
+int rtb_trace_block();      // threads per trace CTA (RT_BLOCK)
 cudaError_t rtb_launch_unpack(const void* gathered, const UnpackParams& U, cudaStream_t st);
 cudaError_t rtb_launch_ffma(float* out, int iters, int grid, cudaStream_t st);
 cudaError_t rtb_launch_compose(const void* L, const void* R, long long lp, long long rp, int W, int H, int mode,

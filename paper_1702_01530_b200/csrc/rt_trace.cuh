@@ -7,7 +7,8 @@
 namespace rtb {
 
 #ifndef RT_BLOCK
-#define RT_BLOCK 256      // threads per trace CTA (stack stride)
+#define RT_BLOCK 64       // threads per trace CTA (stack stride); small CTAs free their slots as soon as
+                          // their 2 warps finish, so a next frame in flight fills the SM sooner
 #endif
 #ifndef RT_SHADOW_SORT
 #define RT_SHADOW_SORT 0  // 1: any-hit (shadow) rays also visit children near-to-far (measured slower);

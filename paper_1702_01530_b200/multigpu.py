@@ -29,6 +29,7 @@ class NcclFrame:
     """Shard render + gather + root unpack."""
 
     mode = "nccl"
+    pipelined = False        # gather + unpack are collective calls per frame: frames run one at a time
 
     def __init__(self, R, fb, rank, world, dist, width, height):
         import torch
@@ -39,7 +40,8 @@ class NcclFrame:
         self.gathered = torch.empty(world * self.per, dtype=torch.uint8, device=R.device) if rank == 0 else None
         self.launches_per_frame = 1 + (1 if rank == 0 else 0)
 
-    def render(self, depth):
+    def render(self, depth, stream=None):
+        assert stream is None, "the NCCL gather path renders one frame at a time"
         self.R.render(self.W, self.H, depth, fb=False, shard=(self.rank, self.world), shard_buf=self.shard)
 
     def assemble(self):
@@ -57,6 +59,7 @@ class PeerFrame:
     """Fused render -> gather through rank 0's IPC-mapped framebuffers."""
 
     mode = "peer"
+    pipelined = True         # frames in flight: each slot has its own mapped framebuffers
 
     def __init__(self, R, fb, rank, world, dist, width, height):
         self.R, self.rank, self.world, self.dist = R, rank, world, dist
@@ -73,8 +76,9 @@ class PeerFrame:
         self.ptrs = (base, base + height * width * 4, width * 4)      # (2, H, W, 4) u8 layout
         self.launches_per_frame = 1
 
-    def render(self, depth):
-        self.R.render(self.W, self.H, depth, fb_ptrs=self.ptrs, shard=(self.rank, self.world), peer=self.rank != 0)
+    def render(self, depth, stream=None):
+        self.R.render(self.W, self.H, depth, fb_ptrs=self.ptrs, shard=(self.rank, self.world), peer=self.rank != 0,
+                      stream=stream)
 
     def assemble(self):
         self.dist.barrier()           # every rank's stores have landed in rank 0's framebuffers

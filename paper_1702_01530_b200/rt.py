@@ -30,7 +30,8 @@ EXPORTED = ["rt_create", "rt_destroy", "rt_synchronize", "rt_last_error", "rt_ve
             "rt_set_stereo_camera", "rt_render_stereo", "rt_render_stereo_ex", "rt_download", "rt_wait", "rt_query",
             "rt_host_alloc", "rt_host_free", "rt_upload", "rt_shard_tiles", "rt_shard_bytes", "rt_unpack_shards_host",
             "rt_unpack_shards", "rt_ipc_get_handle", "rt_ipc_open", "rt_ipc_close", "rt_scene_info", "rt_bvh_export",
-            "rt_bench_ffma", "rt_compose", "rt_scene_update_vertices", "rt_bvh_width", "rt_kdtree_build"]
+            "rt_bench_ffma", "rt_compose", "rt_scene_update_vertices", "rt_bvh_width", "rt_kdtree_build",
+            "rt_render_stereo_async", "rt_download_after"]
 
 
 class RtError(RuntimeError):
@@ -93,6 +94,8 @@ def lib():
             "rt_render_stereo": [vp, u32, u32, u32, rt_fb, rt_fb],
             "rt_render_stereo_ex": [vp, C.POINTER(rt_render_params), C.POINTER(rt_outputs)],
             "rt_download": [vp, vp, vp, C.c_size_t, C.POINTER(vp)],
+            "rt_render_stereo_async": [vp, C.POINTER(rt_render_params), C.POINTER(rt_outputs), vp],
+            "rt_download_after": [vp, vp, vp, C.c_size_t, vp, C.POINTER(vp)],
             "rt_wait": [vp], "rt_query": [vp],
             "rt_host_alloc": [C.c_size_t, C.POINTER(vp)], "rt_host_free": [vp],
             "rt_upload": [vp, vp, vp, C.c_size_t],
@@ -218,9 +221,19 @@ def rt_render_stereo_ex(ctx, params, outputs):
     _check(lib().rt_render_stereo_ex(ctx, C.byref(params), C.byref(outputs)))
 
 
+def rt_render_stereo_async(ctx, params, outputs, cuda_stream):
+    _check(lib().rt_render_stereo_async(ctx, C.byref(params), C.byref(outputs), cuda_stream))
+
+
 def rt_download(ctx, dev_src, host_dst, nbytes, want_event=True):
     ev = C.c_void_p()
     _check(lib().rt_download(ctx, dev_src, host_dst, nbytes, C.byref(ev) if want_event else None))
+    return ev.value
+
+
+def rt_download_after(ctx, dev_src, host_dst, nbytes, after_stream, want_event=True):
+    ev = C.c_void_p()
+    _check(lib().rt_download_after(ctx, dev_src, host_dst, nbytes, after_stream, C.byref(ev) if want_event else None))
     return ev.value
 
 
@@ -376,7 +389,7 @@ class StereoRenderer:
 
     def render(self, width, height, max_depth, fmt=RT_FORMAT_RGBA8, fb=None, want_id=False, want_radiance=False,
                count=False, brute=False, shard=(0, 1), shard_buf=None, shard_fmt=RT_FORMAT_RGBA8, fb_ptrs=None,
-               peer=False, kdtree=False):
+               peer=False, kdtree=False, stream=None):
         """Enqueue one stereo render; returns dict of torch device tensors (not synchronised)."""
         t = self.torch
         out = {}
@@ -413,7 +426,11 @@ class StereoRenderer:
         if kdtree:
             flags |= RT_RENDER_KDTREE
         p = rt_render_params(width, height, max_depth, shard[0], shard[1], flags)
-        rt_render_stereo_ex(self.ctx, p, o)
+        if stream is None:
+            rt_render_stereo_ex(self.ctx, p, o)
+        else:                                       # a frame in flight on its own torch stream
+            stream.wait_stream(t.cuda.current_stream(self.device))   # outputs allocated / filled above
+            rt_render_stereo_async(self.ctx, p, o, stream.cuda_stream or 1)
         if count:
             out["counters"] = self._counters
         return out
