@@ -38,7 +38,14 @@ FLOPS_PER = {"primary": 20, "ray_setup": 3, "node_visits": 48, "tri_tests": 44, 
              "plane_tests": 12, "shade_hits": 20, "light_evals": 67, "reflection": 16, "refraction": 24,
              "misses": 6, "pixels": 9}
 FP32_LANES_PER_SM = 128      # B200 SM: 4 SMSPs x 32 FP32 lanes
-L2_FLUSH_BYTES = 256 << 20   # > 126 MB L2
+L2_FLUSH_MIN = 160 << 20     # > the 126.5 MiB L2 of a B200
+
+
+def l2_flush_bytes(dev):
+    """A write of 1.25x the device's L2 (at least 160 MiB) evicts every line of the scene."""
+    import torch
+    l2 = int(getattr(torch.cuda.get_device_properties(dev), "L2_cache_size", 0) or 0)
+    return max(L2_FLUSH_MIN, ((l2 * 5 // 4) + (1 << 20) - 1) >> 20 << 20)
 
 
 def algorithmic_flops(c):
@@ -250,7 +257,8 @@ def run_ours(args, scene):
     # ---- frame assembly (a7): direct (N=1), fused peer stores or NCCL gather (N>1)
     fb = R.alloc_fb(W, H)                                    # root framebuffers (2, H, W, 4) u8
     frame = SingleFrame(R, fb, W, H) if world == 1 else multigpu.make_frame(args.gather, R, fb, rank, world, dist, W, H)
-    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+    flush_bytes = l2_flush_bytes(dev)
+    flush = torch.empty(flush_bytes // 4, dtype=torch.float32, device=dev)
     # frames in flight: F framebuffer slots (each its own peer mapping for N>1) and F streams
     F = max(1, args.inflight) if frame.pipelined else 1
     fbs = [fb] + [R.alloc_fb(W, H) for _ in range(F - 1)]
@@ -294,7 +302,7 @@ def run_ours(args, scene):
     med_ms, best_ms = float(t[2]), float(t[3])
 
     # ---- (2) throughput: K frames with F in flight on F streams (rt_render_stereo_async), the
-    # L2 flush (256 MiB write) enqueued before every frame on its own stream and timed with it
+    # L2 flush (1.25x L2 write) enqueued before every frame on its own stream and timed with it
     # (it overlaps the other frames, so it cannot be left out).  A frame's pixel trees end in a
     # latency-bound tail (the deepest trees: ~0.7 ms for C4 even on an idle GPU);
     # frames in flight fill the SMs that tail would leave idle.  For N>1 a rank starts frame k
@@ -369,8 +377,9 @@ def run_ours(args, scene):
                        "triangles": scene.n_tris, "rays_per_step": rays_total,
                        "rays_by_type": {k: tot[k] for k in ("primary", "reflection", "refraction", "shadow")},
                        "parallelism": par, "gather": frame.mode, "frames_in_flight": F,
-                       "l2": ("flushed (256 MiB write) before every timed frame, on the frame's stream and inside "
-                              "the timed region" if F > 1 else "flushed (256 MiB write) between timed steps")
+                       "l2": (f"flushed ({flush_bytes >> 20} MiB write, 1.25x L2) before every timed frame, on the "
+                              "frame's stream and inside the timed region" if F > 1
+                              else f"flushed ({flush_bytes >> 20} MiB write) between timed steps")
                              + f"; scene+BVH {info['device_bytes'] / 1e6:.0f} MB"},
             "stereo_fps": 1e3 / ms_per_step,
             "frame_latency": {"ms_mean": lat_total_ms / args.steps, "ms_median": med_ms, "ms_best": best_ms,

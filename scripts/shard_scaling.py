@@ -25,7 +25,7 @@ INFLIGHT = int(os.environ.get("RT_INFLIGHT", "4"))
 def main():
     names = sys.argv[1:] or ["C4"]
     R = rt.StereoRenderer(0)
-    flush = torch.empty(256 * 2**20 // 4, dtype=torch.float32, device="cuda")
+    flush = torch.empty(int(os.environ.get("RT_FLUSH_MIB", "256")) * 2**20 // 4, dtype=torch.float32, device="cuda")
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     res = {}
     for name in names:
