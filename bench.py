@@ -207,6 +207,27 @@ class SingleFrame:
         pass
 
 
+def frame_sync(dist, world, share, dev):
+    """Cross-rank synchronisation point of the frames-in-flight loops: returns once every rank
+    has reached it, without waiting on any render stream.  NCCL: a one-element all-reduce on an
+    otherwise idle stream, waited for by the host (tens of microseconds over NVLink; a gloo
+    barrier costs 0.5-1.8 ms per call at 2-8 local ranks, more than a frame).  Share-device test
+    mode (gloo process group): dist.barrier."""
+    if world == 1:
+        return None
+    if share:
+        return dist.barrier
+    import torch
+    st = torch.cuda.Stream(device=dev)
+    flag = torch.zeros(1, dtype=torch.int32, device=dev)
+
+    def sync():
+        with torch.cuda.stream(st):
+            dist.all_reduce(flag, async_op=True).wait()
+        st.synchronize()
+    return sync
+
+
 def run_ours(args, scene):
     import torch
     import torch.distributed as dist
@@ -265,9 +286,7 @@ def run_ours(args, scene):
     frames = [frame] + [SingleFrame(R, fbs[i], W, H) if world == 1
                         else multigpu.make_frame(frame.mode, R, fbs[i], rank, world, dist, W, H) for i in range(1, F)]
     streams = [torch.cuda.Stream(device=dev) for _ in range(F)]
-    hb = None
-    if world > 1:                                            # host-only barrier (gloo): never syncs a device
-        hb = dist.group.WORLD if share else dist.new_group(backend="gloo")
+    hb = frame_sync(dist, world, share, dev)                 # cross-rank "frame done" point, N>1
 
     for _ in range(max(3, args.warmup)):
         frame.render(D)
@@ -306,8 +325,9 @@ def run_ours(args, scene):
     # (it overlaps the other frames, so it cannot be left out).  A frame's pixel trees end in a
     # latency-bound tail (the deepest trees: ~0.7 ms for C4 even on an idle GPU);
     # frames in flight fill the SMs that tail would leave idle.  For N>1 a rank starts frame k
-    # only after every rank finished frame k-F+1 (host gloo barrier, lagging so the device
-    # always has queued frames): the slot frame k overwrites is then fully assembled.
+    # only after every rank finished frame k-F+1 (frame_sync, lagging so the device
+    # always has queued frames): the slot frame k overwrites is then fully assembled.  The
+    # synchronisation point is an NCCL all-reduce the host waits for (frame_sync).
     if F > 1:
         lag = F - 1
 
@@ -315,7 +335,7 @@ def run_ours(args, scene):
             slot = k % F
             if world > 1 and k >= lag:
                 done.pop(k - lag).synchronize()
-                dist.barrier(group=hb)
+                hb()
             with torch.cuda.stream(streams[slot]):
                 flush.zero_()
             frames[slot].render(D, streams[slot])
@@ -419,7 +439,7 @@ def run_e2e(args, R, scene, rank, world, frames, fbs, streams, hb, dev, rays_tot
     frames still rendering).  With F frames in flight each frame renders on its slot's stream
     into its slot's framebuffers; a slot is re-rendered only after its previous download
     completed (and, for N>1, after every rank finished the frame a lag of F-1 frames back, by a
-    host gloo barrier that never waits on a device)."""
+    cross-rank sync point (frame_sync) that never waits on a render stream)."""
     import ctypes
 
     import torch
@@ -459,7 +479,7 @@ def run_e2e(args, R, scene, rank, world, frames, fbs, streams, hb, dev, rays_tot
         slot = j % F
         if world > 1 and F > 1:
             done.pop(j).synchronize()
-            dist.barrier(group=hb)
+            hb()
         else:
             done.pop(j, None)
         if rank == 0:
