@@ -264,6 +264,9 @@ rt_status rt_unpack_shards(rt_context* ctx, const void* gathered, uint32_t width
  * render->gather path in which each rank's pack epilogue writes its tiles straight into rank
  * 0's framebuffers (base + offset). */
 rt_status rt_ipc_get_handle(const void* dev_ptr, void* handle64, uint64_t* offset);
+/* rt_ipc_open of a handle this context already mapped returns the same mapping (framebuffers
+ * that share one allocation share one handle); mappings are reference counted: call
+ * rt_ipc_close once per rt_ipc_open.  rt_destroy closes what is left. */
 rt_status rt_ipc_open(rt_context* ctx, const void* handle64, void** dev_ptr);
 rt_status rt_ipc_close(rt_context* ctx, void* dev_ptr);
 

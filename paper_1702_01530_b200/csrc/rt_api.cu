@@ -96,6 +96,12 @@ struct rt_context {
     std::vector<int> level_start;
     std::vector<uint32_t> h_tri;
     double sphere_bound = 0.0;
+    struct IpcMap {
+        std::string key;            // the 64-byte cudaIpcMemHandle_t
+        void* ptr;
+        int refs;
+    };
+    std::vector<IpcMap> ipc_maps;    // peer allocations mapped by rt_ipc_open (reference counted)
     // NEXT-4 kd-tree ablation (rt_kdtree_build)
     DevBuf kd_nodes_buf, kd_refs_buf;
 };
@@ -176,6 +182,8 @@ rt_status rt_destroy(rt_context* c) {
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
     free_scene(c);
+    for (auto& m : c->ipc_maps) cudaIpcCloseMemHandle(m.ptr);
+    c->ipc_maps.clear();
     if (c->work_counter) cudaFree(c->work_counter);
     if (c->arena) cudaFree(c->arena);
     if (c->scratch_counters) cudaFree(c->scratch_counters);
@@ -889,16 +897,32 @@ rt_status rt_ipc_get_handle(const void* dev_ptr, void* handle64, uint64_t* offse
 rt_status rt_ipc_open(rt_context* c, const void* handle64, void** dev_ptr) {
     if (!c || !handle64 || !dev_ptr) return fail(RT_ERR_INVALID_ARG, "rt_ipc_open: NULL argument");
     CUDA_TRY(cudaSetDevice(c->device));
+    // one mapping per exported allocation per process: several framebuffers can share one
+    // caching-allocator block (one handle, different offsets), and CUDA maps a handle once
+    std::string key(static_cast<const char*>(handle64), 64);
+    for (auto& m : c->ipc_maps)
+        if (m.key == key) {
+            ++m.refs;
+            *dev_ptr = m.ptr;
+            return RT_OK;
+        }
     cudaIpcMemHandle_t h;
     memcpy(&h, handle64, 64);
     cudaError_t e = cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess);
     if (e != cudaSuccess) return fail(RT_ERR_PEER, "cudaIpcOpenMemHandle: %s", cudaGetErrorString(e));
+    c->ipc_maps.push_back({key, *dev_ptr, 1});
     return RT_OK;
 }
 
 rt_status rt_ipc_close(rt_context* c, void* dev_ptr) {
     if (!c || !dev_ptr) return fail(RT_ERR_INVALID_ARG, "rt_ipc_close: NULL argument");
     CUDA_TRY(cudaSetDevice(c->device));
+    for (size_t i = 0; i < c->ipc_maps.size(); ++i)
+        if (c->ipc_maps[i].ptr == dev_ptr) {
+            if (--c->ipc_maps[i].refs > 0) return RT_OK;
+            c->ipc_maps.erase(c->ipc_maps.begin() + (long)i);
+            break;
+        }
     cudaError_t e = cudaIpcCloseMemHandle(dev_ptr);
     if (e != cudaSuccess) return fail(RT_ERR_PEER, "cudaIpcCloseMemHandle: %s", cudaGetErrorString(e));
     return RT_OK;

@@ -35,20 +35,26 @@ def _worker(rank, world, port, q):
     R = rt.StereoRenderer(0)
     R.upload(s)
     R.set_camera(s.rig)
-    fb = R.alloc_fb(s.width, s.height)
-    fb.zero_()
+    # three small framebuffer slots (frames in flight): they share caching-allocator blocks, so
+    # several mappings of one IPC handle at different offsets
+    fbs = [R.alloc_fb(s.width, s.height) for _ in range(3)]
+    for fb in fbs:
+        fb.zero_()
     torch.cuda.synchronize()
     dist.barrier()
-    frame = multigpu.PeerFrame(R, fb, rank, world, dist, s.width, s.height)
-    frame.render(s.max_depth)
+    frames = [multigpu.PeerFrame(R, fb, rank, world, dist, s.width, s.height) for fb in fbs]
+    streams = [torch.cuda.Stream() for _ in fbs]
+    for f, st in zip(frames, streams):
+        f.render(s.max_depth, st)
     torch.cuda.synchronize()
-    frame.assemble()
+    frames[0].assemble()
     if rank == 0:
         ref = R.render(s.width, s.height, s.max_depth)["fb"]
         torch.cuda.synchronize()
-        q.put(bool(torch.equal(ref, fb)))
+        q.put(all(bool(torch.equal(ref, fb)) for fb in fbs))
     dist.barrier()
-    frame.close()
+    for f in frames:
+        f.close()
     R.close()
     dist.destroy_process_group()
 
