@@ -44,6 +44,13 @@ __device__ __forceinline__ float3 trace_pixel(const TraceParams& P, float3 o, fl
     float3 col = f3(0.f, 0.f, 0.f);
     cnt.add(CNT_PRIMARY);
     while (true) {
+#if RT_TREE_STATS
+        if (COUNT) {   // ray-tree loop utilisation: c[6] += warp iterations, c[7] += lane iterations
+            const unsigned am = __activemask();
+            if ((threadIdx.x & 31) == __ffs(am) - 1) cnt.c[6] += 1;
+            cnt.c[7] += 1;
+        }
+#endif
 #if RT_PACKET
         // the first pass of the loop (primary rays) runs with every traced lane of the warp, and
         // so do later passes that are still converged: those trace as warp packets

@@ -42,6 +42,9 @@ namespace rtb {
 #ifndef RT_WW
 #define RT_WW 0            // while-while traversal: bit 0 nearest-hit rays, bit 1 any-hit rays (BVH4)
 #endif
+#ifndef RT_TREE_STATS
+#define RT_TREE_STATS 0    // 1: instrumented build records ray-tree loop lane utilisation (experiments)
+#endif
 #ifndef RT_SHADOW_STATS
 #define RT_SHADOW_STATS 0  // 1: instrumented build records warp-level traversal divergence (experiments)
 #endif
