@@ -431,6 +431,11 @@ class StereoRenderer:
         else:                                       # a frame in flight on its own torch stream
             stream.wait_stream(t.cuda.current_stream(self.device))   # outputs allocated / filled above
             rt_render_stereo_async(self.ctx, p, o, stream.cuda_stream or 1)
+            for v in out.values():                  # keep the caching allocator from reusing them early
+                if hasattr(v, "record_stream"):
+                    v.record_stream(stream)
+            if count:
+                self._counters.record_stream(stream)
         if count:
             out["counters"] = self._counters
         return out
