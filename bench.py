@@ -415,6 +415,11 @@ def run_ours(args, scene):
                                        f"unit counts); live FFMA microbenchmark {ffma_tflops:.1f} TFLOP/s"},
             "clocks": clocks,
             "gpu_launches": args.steps * frame.launches_per_frame,   # in the throughput region
+            "paper_context": {"hardware": "'a video graphics card NVIDIA', model unstated (PAPER.md:66)",
+                              "timings": "no Mrays/s or frames/s published; 'few milliseconds' per frame for scenes of "
+                                         "1-6 small polyhedra and one light (PAPER.md:104); ~60 % compute / up to 40 % "
+                                         "CPU<->GPU transfer (PAPER.md:15, :106-107); (4:1) network 2.5x faster than "
+                                         "(1:1) (PAPER.md:109)", "note": "context, not the target (BASELINE.md)"},
             "scene_upload_ms": upload_ms, "bvh": info,
             "work_counts": tot,
         }
