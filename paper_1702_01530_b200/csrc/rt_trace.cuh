@@ -192,14 +192,19 @@ __device__ __forceinline__ void store_px(void* base, int fmt, long long pitch, i
 template <bool COUNT>
 __device__ __forceinline__ bool prim_t(const DevScene& S, int k, float3 o, float3 d, float& t, int& gid,
                                        Counters<COUNT>& cnt) {
+    // all three 16-byte records up front, before the type test: both kinds read records 0 and 2
+    // (a sphere keeps r^2 in record 2), so the loads are not sunk into the branches and a leaf
+    // costs one memory round trip instead of two
     const float4 a = __ldg(&S.prims[3 * k]);
+    const float4 b = __ldg(&S.prims[3 * k + 1]);
+    const float4 c = __ldg(&S.prims[3 * k + 2]);
     gid = __float_as_int(a.w);
     if (gid < S.n_spheres) {
         cnt.add(CNT_SPHERE_TESTS);
-        return sphere_intersect(o, d, a, __ldg(&S.prims[3 * k + 1]), T_MIN, t);
+        return sphere_intersect(o, d, a, c.x, T_MIN, t);
     }
     cnt.add(CNT_TRI_TESTS);
-    return tri_intersect(o, d, a, __ldg(&S.prims[3 * k + 1]), __ldg(&S.prims[3 * k + 2]), t) && t > T_MIN;
+    return tri_intersect(o, d, a, b, c, t) && t > T_MIN;
 }
 
 // Box tests of the 4 children of one BVH4 node (7 float4: lo.x hi.x lo.y hi.y lo.z hi.z child).
