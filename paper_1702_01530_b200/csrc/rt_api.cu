@@ -1045,9 +1045,20 @@ rt_status rt_bvh_export(rt_context* c, float* nodes, uint32_t* n_nodes, int32_t*
         }
     }
 #else
-    if (nodes && nn)
+    if (nodes && nn) {
         CUDA_TRY(cudaMemcpy2D(nodes, 16 * rtb::NODE_DATA_F4, c->sc.nodes, 16 * rtb::NODE_F4, 16 * rtb::NODE_DATA_F4, nn,
                               cudaMemcpyDeviceToHost));
+        if (rtb::node_slot(6) != 6) {       // device slot order -> the documented export order
+            // (plain float copies: the caller's array need not be 16-byte aligned)
+            constexpr int A = rtb::BVH_W;                     // floats per array (lo.x[W] ...)
+            float tmp[7 * A];
+            for (uint32_t i = 0; i < nn; ++i) {
+                float* q = nodes + (size_t)i * 7 * A;
+                for (int a = 0; a < 7; ++a) memcpy(tmp + a * A, q + rtb::node_slot(a) * A, sizeof(float) * A);
+                memcpy(q, tmp, sizeof tmp);
+            }
+        }
+    }
 #endif
     if (prim_gid && np) {
         std::vector<float4> p(3 * (size_t)np);

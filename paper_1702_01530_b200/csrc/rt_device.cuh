@@ -44,6 +44,18 @@ constexpr int BVH_W = RT_BVH_WIDTH;                    // children per node (4 o
 constexpr int NODE_DATA_F4 = 7 * BVH_W / 4;            // float4 of decoded node data: lo/hi x,y,z + child codes
 constexpr int NODE_F4 = RT_NODE_F16 ? 5 : (RT_NODE_PAD && BVH_W == 4) ? 8 : NODE_DATA_F4;   // node stride
 constexpr int STACK_CAP = (BVH_W - 1) * 64 + 2;       // traversal stack: W-1 siblings per level, depth <= 64
+#ifndef RT_CH_MID
+#define RT_CH_MID 1
+#endif
+// Storage slot (16-byte unit for BVH4) of array a = 0 lo.x, 1 hi.x, 2 lo.y, 3 hi.y, 4 lo.z, 5 hi.z,
+// 6 child codes.  RT_CH_MID (BVH4): the child codes sit in slot 3, between lo.y and hi.y.  A 112-byte
+// node starts on a 32-byte sector boundary or 16 bytes past one; either way the codes then share
+// their sector with lo.y or hi.y -- both always loaded (the near and far y planes) -- so the codes'
+// load, which ptxas issues only after the box tests, hits a sector already on its way to L1
+// instead of costing a second L2 round trip.
+__host__ __device__ constexpr int node_slot(int a) {
+    return (RT_CH_MID && BVH_W == 4) ? (a == 6 ? 3 : (a >= 3 ? a + 1 : a)) : a;
+}
 constexpr int LEAF_SHIFT = 24;     // leaf encoding: ~((count-1) << 24 | first)
 constexpr int TILE = 16;
 constexpr int WIDE_EMPTY = 0x7fffffff;   // unused BVH4 child slot
@@ -86,16 +98,19 @@ __device__ inline void node_write(float4* q, const float3* lo, const float3* hi,
     }
 #else
     float* o = reinterpret_cast<float*>(q);
-    int* oc = reinterpret_cast<int*>(o) + 6 * BVH_W;
+    int* oc = reinterpret_cast<int*>(o) + node_slot(6) * BVH_W;
     for (int c = 0; c < BVH_W; ++c) {
         if (code[c] == WIDE_EMPTY) {
             // inverted box (lo = +1e30, hi = -1e30): every slab test rejects it, so the
             // traversal needs no per-slot validity test
-            for (int k = 0; k < 3; ++k) { o[(2 * k) * BVH_W + c] = 1e30f; o[(2 * k + 1) * BVH_W + c] = -1e30f; }
+            for (int k = 0; k < 3; ++k) {
+                o[node_slot(2 * k) * BVH_W + c] = 1e30f;
+                o[node_slot(2 * k + 1) * BVH_W + c] = -1e30f;
+            }
         } else {
-            o[0 * BVH_W + c] = lo[c].x; o[1 * BVH_W + c] = hi[c].x;
-            o[2 * BVH_W + c] = lo[c].y; o[3 * BVH_W + c] = hi[c].y;
-            o[4 * BVH_W + c] = lo[c].z; o[5 * BVH_W + c] = hi[c].z;
+            o[node_slot(0) * BVH_W + c] = lo[c].x; o[node_slot(1) * BVH_W + c] = hi[c].x;
+            o[node_slot(2) * BVH_W + c] = lo[c].y; o[node_slot(3) * BVH_W + c] = hi[c].y;
+            o[node_slot(4) * BVH_W + c] = lo[c].z; o[node_slot(5) * BVH_W + c] = hi[c].z;
         }
         oc[c] = code[c];
     }
@@ -106,7 +121,7 @@ __device__ inline int node_code(const float4* q, int c) {
 #if RT_NODE_F16
     return reinterpret_cast<const int*>(q + 1)[c];
 #else
-    return reinterpret_cast<const int*>(q)[6 * BVH_W + c];
+    return reinterpret_cast<const int*>(q)[node_slot(6) * BVH_W + c];
 #endif
 }
 
@@ -130,8 +145,8 @@ __device__ inline void node_child_box(const float4* q, int c, float3& lo, float3
     hi = make_float3(h[0], h[1], h[2]);
 #else
     const float* r = reinterpret_cast<const float*>(q);
-    lo = make_float3(r[0 * BVH_W + c], r[2 * BVH_W + c], r[4 * BVH_W + c]);
-    hi = make_float3(r[1 * BVH_W + c], r[3 * BVH_W + c], r[5 * BVH_W + c]);
+    lo = make_float3(r[node_slot(0) * BVH_W + c], r[node_slot(2) * BVH_W + c], r[node_slot(4) * BVH_W + c]);
+    hi = make_float3(r[node_slot(1) * BVH_W + c], r[node_slot(3) * BVH_W + c], r[node_slot(5) * BVH_W + c]);
 #endif
 }
 
@@ -287,9 +302,9 @@ __device__ __forceinline__ const char* opaque_ptr(const char* p) {
 __device__ __forceinline__ void set_node_bases(RayBox& rb, const float4* nodes) {
 #if RT_NODE_BASES
     const char* b = reinterpret_cast<const char*>(nodes);
-    rb.pn[0] = opaque_ptr(b + 16 * rb.sx);       rb.pf[0] = opaque_ptr(b + 16 * (1 - rb.sx));
-    rb.pn[1] = opaque_ptr(b + 16 * (2 + rb.sy)); rb.pf[1] = opaque_ptr(b + 16 * (3 - rb.sy));
-    rb.pn[2] = opaque_ptr(b + 16 * (4 + rb.sz)); rb.pf[2] = opaque_ptr(b + 16 * (5 - rb.sz));
+    rb.pn[0] = opaque_ptr(b + 16 * node_slot(rb.sx));     rb.pf[0] = opaque_ptr(b + 16 * node_slot(1 - rb.sx));
+    rb.pn[1] = opaque_ptr(b + 16 * node_slot(2 + rb.sy)); rb.pf[1] = opaque_ptr(b + 16 * node_slot(3 - rb.sy));
+    rb.pn[2] = opaque_ptr(b + 16 * node_slot(4 + rb.sz)); rb.pf[2] = opaque_ptr(b + 16 * node_slot(5 - rb.sz));
 #else
     (void)rb;
     (void)nodes;

@@ -262,13 +262,13 @@ __device__ __forceinline__ unsigned node4_hits(const float4* __restrict__ nodes,
     const float4 nx = ld(rb.pn[0]), fx = ld(rb.pf[0]);
     const float4 ny = ld(rb.pn[1]), fy = ld(rb.pf[1]);
     const float4 nz = ld(rb.pn[2]), fz = ld(rb.pf[2]);
-    child = __ldg(reinterpret_cast<const int4*>(nodes + (size_t)NODE_F4 * node + 6));
+    child = __ldg(reinterpret_cast<const int4*>(nodes + (size_t)NODE_F4 * node + node_slot(6)));
 #else
     const float4* q = nodes + (size_t)NODE_F4 * node;
-    const float4 nx = __ldg(q + rb.sx), fx = __ldg(q + 1 - rb.sx);
-    const float4 ny = __ldg(q + 2 + rb.sy), fy = __ldg(q + 3 - rb.sy);
-    const float4 nz = __ldg(q + 4 + rb.sz), fz = __ldg(q + 5 - rb.sz);
-    child = __ldg(reinterpret_cast<const int4*>(q + 6));
+    const float4 nx = __ldg(q + node_slot(rb.sx)), fx = __ldg(q + node_slot(1 - rb.sx));
+    const float4 ny = __ldg(q + node_slot(2 + rb.sy)), fy = __ldg(q + node_slot(3 - rb.sy));
+    const float4 nz = __ldg(q + node_slot(4 + rb.sz)), fz = __ldg(q + node_slot(5 - rb.sz));
+    child = __ldg(reinterpret_cast<const int4*>(q + node_slot(6)));
 #endif
 #if !RT_NODE_F16
 #if RT_FFMA2
