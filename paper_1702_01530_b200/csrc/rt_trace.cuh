@@ -48,6 +48,9 @@ namespace rtb {
 #ifndef RT_SHADOW_STATS
 #define RT_SHADOW_STATS 0  // 1: instrumented build records warp-level traversal divergence (experiments)
 #endif
+#ifndef RT_TOP_REG
+#define RT_TOP_REG 1      // BVH4: the top stack entry lives in a register (pop = register move)
+#endif
 #ifndef RT_OCC_CACHE
 #define RT_OCC_CACHE 1    // per-thread, per-light last-occluder hint for shadow rays
 #endif
@@ -396,6 +399,72 @@ __device__ __forceinline__ bool plain_push(unsigned m, const int4& ch, TravStack
     return true;
 }
 
+
+#if RT_TOP_REG
+// Stack with its top entry cached in a register: logical entries [0, sp) are memory entries
+// [0, sp-1) plus `top`.  A pop is a register move; the LDS/LDL that refills `top` is issued
+// right away but its latency overlaps the popped node's visit instead of preceding it.
+__device__ __forceinline__ bool order_push_top(unsigned m, const float tn[4], const int4& ch, TravStack& stk, int& sp,
+                                               int& top, int& node) {
+    if (!m) return false;
+    uint32_t k0 = (m & 1) ? ((__float_as_uint(tn[0]) & ~3u) | 0u) : 0xffffffffu;
+    uint32_t k1 = (m & 2) ? ((__float_as_uint(tn[1]) & ~3u) | 1u) : 0xffffffffu;
+    uint32_t k2 = (m & 4) ? ((__float_as_uint(tn[2]) & ~3u) | 2u) : 0xffffffffu;
+    uint32_t k3 = (m & 8) ? ((__float_as_uint(tn[3]) & ~3u) | 3u) : 0xffffffffu;
+    cswap(k0, k1); cswap(k2, k3); cswap(k0, k2); cswap(k1, k3); cswap(k1, k2);
+    const int nh = __popc(m);
+    if (nh > 1) {
+        // old top -> memory entry sp-1; k3, k2 -> entries sp.. (far first); k1 -> top
+        if (sp + 2 <= RT_SMEM_STACK) {
+            const uint32_t a = stk.addr(sp);
+            constexpr uint32_t E = RT_BLOCK * 4u;
+            TravStack::st_if(sp > 0, a - E, top);
+            TravStack::st_if(nh > 3, a, pick4(ch, k3 & 3u));
+            TravStack::st_if(nh > 2, a + (uint32_t)(nh - 3) * E, pick4(ch, k2 & 3u));
+        } else {
+            if (sp > 0) stk.set(sp - 1, top);
+            if (nh > 3) stk.set(sp, pick4(ch, k3 & 3u));
+            if (nh > 2) stk.set(sp + nh - 3, pick4(ch, k2 & 3u));
+        }
+        top = pick4(ch, k1 & 3u);
+        sp += nh - 1;
+    }
+    node = pick4(ch, k0 & 3u);
+    return true;
+}
+
+__device__ __forceinline__ bool plain_push_top(unsigned m, const int4& ch, TravStack& stk, int& sp, int& top, int& node) {
+    if (!m) return false;
+    const unsigned r = m & (m - 1u);                       // pushed slots (all hits but the lowest)
+    if (r) {
+        const int hi = 31 - __clz(r);                      // highest pushed slot -> top
+        const unsigned rr = r & ~(1u << hi);               // the others -> memory, slot order
+        if (sp + 2 <= RT_SMEM_STACK) {
+            const uint32_t a = stk.addr(sp);
+            constexpr uint32_t E = RT_BLOCK * 4u;
+            TravStack::st_if(sp > 0, a - E, top);
+            TravStack::st_if(rr & 2u, a, ch.y);
+            TravStack::st_if(rr & 4u, a + ((rr >> 1) & 1u) * E, ch.z);
+        } else {
+            if (sp > 0) stk.set(sp - 1, top);
+            if (rr & 2u) stk.set(sp, ch.y);
+            if (rr & 4u) stk.set(sp + (int)((rr >> 1) & 1u), ch.z);
+        }
+        top = pick4(ch, (uint32_t)hi);
+        sp += __popc(r);
+    }
+    node = pick4(ch, __ffs(m) - 1);
+    return true;
+}
+
+__device__ __forceinline__ bool pop_top(TravStack& stk, int& sp, int& top, int& node) {
+    if (sp == 0) return false;
+    node = top;
+    if (--sp > 0) top = stk.get(sp - 1);
+    return true;
+}
+#endif
+
 // ---------------------------------------------------------------- 8-wide nodes
 // 14 float4: lo.x[8] hi.x[8] lo.y[8] hi.y[8] lo.z[8] hi.z[8] child[8]; near/far planes picked per
 // ray by direction sign (two float4 per array); child codes are loaded only for pushed children.
@@ -614,6 +683,7 @@ __device__ __forceinline__ Hit closest_hit(const DevScene& S, float3 o, float3 d
     set_node_bases(rb, S.nodes);
     int sp = 0;
     int node = S.root;
+    int top = 0;          // cached top stack entry (RT_TOP_REG)
 #if (RT_WW & 1) && RT_BVH_WIDTH == 4
     // while-while (Aila & Laine 2009): a lane descends through inner nodes until it holds a
     // leaf (or is done); the warp then tests the leaves of all lanes together, so the node and
@@ -649,7 +719,9 @@ __device__ __forceinline__ Hit closest_hit(const DevScene& S, float3 o, float3 d
             float tn[4];
             int4 ch;
             const unsigned m = node4_hits(S.nodes, node, rb, h.t, tn, ch);
-#if RT_CLOSEST_SORT
+#if RT_TOP_REG && RT_CLOSEST_SORT
+            if (order_push_top(m, tn, ch, stk, sp, top, node)) continue;
+#elif RT_CLOSEST_SORT
             if (order_push(m, tn, ch, stk, sp, node)) continue;
 #else
             if (plain_push(m, ch, stk, sp, node)) continue;
@@ -660,9 +732,13 @@ __device__ __forceinline__ Hit closest_hit(const DevScene& S, float3 o, float3 d
             const int first = enc & ((1 << LEAF_SHIFT) - 1);
             leaf_test(first, first + (enc >> LEAF_SHIFT));
         }
+#if RT_TOP_REG && RT_BVH_WIDTH == 4 && RT_CLOSEST_SORT
+        if (!pop_top(stk, sp, top, node)) return h;
+#else
         if (sp == 0) return h;
         --sp;
         node = stk.get(sp);
+#endif
     }
 }
 
@@ -712,6 +788,7 @@ __device__ __forceinline__ bool occluded(const DevScene& S, float3 o, float3 d, 
     set_node_bases(rb, S.nodes);
     int sp = 0;
     int node = S.root;
+    int top = 0;          // cached top stack entry (RT_TOP_REG)
 #if (RT_WW & 2) && RT_BVH_WIDTH == 4 && !RT_SHADOW_SORT
     while (true) {
         while (node >= 0) {
@@ -752,6 +829,8 @@ __device__ __forceinline__ bool occluded(const DevScene& S, float3 o, float3 d, 
             if (order_push(m, tn, ch, stk, sp, node)) continue;
 #elif RT_SHADOW_SORT
             if (order_push(m, tn, ch, stk, sp, node)) continue;
+#elif RT_TOP_REG
+            if (plain_push_top(m, ch, stk, sp, top, node)) continue;
 #else
             if (plain_push(m, ch, stk, sp, node)) continue;
 #endif
@@ -761,9 +840,13 @@ __device__ __forceinline__ bool occluded(const DevScene& S, float3 o, float3 d, 
             const int first = enc & ((1 << LEAF_SHIFT) - 1);
             if (leaf_test(first, first + (enc >> LEAF_SHIFT))) return true;
         }
+#if RT_TOP_REG && RT_BVH_WIDTH == 4 && !RT_SHADOW_SORT
+        if (!pop_top(stk, sp, top, node)) return false;
+#else
         if (sp == 0) return false;
         --sp;
         node = stk.get(sp);
+#endif
     }
 }
 
