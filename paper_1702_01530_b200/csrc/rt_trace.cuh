@@ -48,6 +48,9 @@ namespace rtb {
 #ifndef RT_SHADOW_STATS
 #define RT_SHADOW_STATS 0  // 1: instrumented build records warp-level traversal divergence (experiments)
 #endif
+#ifndef RT_CH_EARLY
+#define RT_CH_EARLY 0     // 1: the hit mask depends on the child codes, so ptxas loads them with the planes
+#endif
 #ifndef RT_TOP_REG
 #define RT_TOP_REG 1      // BVH4: the top stack entry lives in a register (pop = register move)
 #endif
@@ -306,6 +309,17 @@ __device__ __forceinline__ unsigned node4_hits(const float4* __restrict__ nodes,
     m |= tn[2] >= 0.0f ? 4u : 0u;
     m |= tn[3] >= 0.0f ? 8u : 0u;
     return m;
+#endif
+}
+
+// An impossible child code (0x7ffffffe: no node index, leaf code or WIDE_EMPTY) folded into the
+// hit mask keeps ptxas from sinking the child-code load below the "any child hit?" branch.
+__device__ __forceinline__ unsigned ch_dep(const int4& ch) {
+#if RT_CH_EARLY
+    return ch.x == 0x7ffffffe ? 1u : 0u;
+#else
+    (void)ch;
+    return 0u;
 #endif
 }
 
@@ -718,7 +732,7 @@ __device__ __forceinline__ Hit closest_hit(const DevScene& S, float3 o, float3 d
 #else
             float tn[4];
             int4 ch;
-            const unsigned m = node4_hits(S.nodes, node, rb, h.t, tn, ch);
+            const unsigned m = node4_hits(S.nodes, node, rb, h.t, tn, ch) | ch_dep(ch);
 #if RT_TOP_REG && RT_CLOSEST_SORT
             if (order_push_top(m, tn, ch, stk, sp, top, node)) continue;
 #elif RT_CLOSEST_SORT
@@ -820,7 +834,7 @@ __device__ __forceinline__ bool occluded(const DevScene& S, float3 o, float3 d, 
 #else
             float tn[4];
             int4 ch;
-            const unsigned m = node4_hits(S.nodes, node, rb, dist, tn, ch);
+            const unsigned m = node4_hits(S.nodes, node, rb, dist, tn, ch) | ch_dep(ch);
 #if RT_SHADOW_SORT == 2
             if (m) {   // far-first: entry distances mirrored (0x7effffff - bits; misses stay last)
 #pragma unroll
