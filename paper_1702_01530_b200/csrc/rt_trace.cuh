@@ -51,6 +51,9 @@ namespace rtb {
 #ifndef RT_CH_EARLY
 #define RT_CH_EARLY 0     // 1: the hit mask depends on the child codes, so ptxas loads them with the planes
 #endif
+#ifndef RT_LEAN_MASK
+#define RT_LEAN_MASK 1    // BVH4 hit mask built from the slab predicates (no -1 sentinel distances)
+#endif
 #ifndef RT_TOP_REG
 #define RT_TOP_REG 1      // BVH4: the top stack entry lives in a register (pop = register move)
 #endif
@@ -293,6 +296,15 @@ __device__ __forceinline__ unsigned node4_hits(const float4* __restrict__ nodes,
     const float tn1 = fmaxf(fmaxf(a0.y, b0.y), fmaxf(c0.y, 0.0f)), tf1 = fminf(fminf(d0.y, e0.y), fminf(g0.y, tmax));
     const float tn2 = fmaxf(fmaxf(a1.x, b1.x), fmaxf(c1.x, 0.0f)), tf2 = fminf(fminf(d1.x, e1.x), fminf(g1.x, tmax));
     const float tn3 = fmaxf(fmaxf(a1.y, b1.y), fmaxf(c1.y, 0.0f)), tf3 = fminf(fminf(d1.y, e1.y), fminf(g1.y, tmax));
+#if RT_LEAN_MASK
+    // the hit mask straight from the four slab predicates; tn[] stays the raw entry distance
+    // (>= 0) and is only read for the children the mask marks as hit
+    tn[0] = tn0;
+    tn[1] = tn1;
+    tn[2] = tn2;
+    tn[3] = tn3;
+    return (tn0 <= tf0 ? 1u : 0u) | (tn1 <= tf1 ? 2u : 0u) | (tn2 <= tf2 ? 4u : 0u) | (tn3 <= tf3 ? 8u : 0u);
+#endif
     tn[0] = tn0 <= tf0 ? tn0 : -1.0f;
     tn[1] = tn1 <= tf1 ? tn1 : -1.0f;
     tn[2] = tn2 <= tf2 ? tn2 : -1.0f;
