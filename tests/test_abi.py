@@ -46,6 +46,24 @@ def test_create_without_device_fails_cleanly():
     assert rt.rt_last_error() != ""
 
 
+def test_null_arguments_are_rejected_without_a_device():
+    """Every entry point validates its pointers before touching CUDA (error behaviour documented
+    in include/rt_b200.h): NULL context / outputs -> RT_ERR_INVALID_ARG."""
+    import ctypes as C
+    L = rt.lib()
+    p = rt.rt_render_params(64, 48, 1, 0, 1, 0)
+    o = rt.rt_outputs()
+    assert L.rt_render_stereo_ex(None, C.byref(p), C.byref(o)) == rt.RT_ERR_INVALID_ARG
+    assert L.rt_render_stereo_async(None, C.byref(p), C.byref(o), None) == rt.RT_ERR_INVALID_ARG
+    assert L.rt_download_after(None, None, None, 0, None, None) == rt.RT_ERR_INVALID_ARG
+    assert L.rt_download(None, None, None, 0, None) == rt.RT_ERR_INVALID_ARG
+    assert L.rt_kdtree_build(None, 1, 0, None) == rt.RT_ERR_INVALID_ARG
+    assert L.rt_ipc_open(None, None, None) == rt.RT_ERR_INVALID_ARG
+    assert L.rt_ipc_close(None, None) == rt.RT_ERR_INVALID_ARG
+    assert L.rt_scene_info(None, None) == rt.RT_ERR_INVALID_ARG
+    assert "NULL" in rt.rt_last_error() or rt.rt_last_error() != ""
+
+
 @pytest.mark.parametrize("W,H", [(64, 48), (67, 45), (1920, 1080), (17, 1), (1, 1), (33, 200)])
 @pytest.mark.parametrize("world", [1, 2, 3, 4, 5, 8])
 def test_shard_map_exact_cover(W, H, world):
