@@ -14,6 +14,9 @@
 // the SIMT loss is inside BVH traversal, not in idle ray-tree tails, and v2's barriers stalled.
 #include "rt_trace.cuh"
 
+#ifndef RT_TERM_AFTER
+#define RT_TERM_AFTER 0   // 1: form a light's Phong term after its shadow ray (only when unoccluded)
+#endif
 #ifndef RT_LIT_COMPACT
 #define RT_LIT_COMPACT 0  // 1: each lane traces its own lit lights back to back (measured slower)
 #endif
@@ -166,6 +169,27 @@ __device__ __forceinline__ float3 trace_pixel(const TraceParams& P, float3 o, fl
                 }
 #endif
                 if (ndl <= 0.0f) continue;                               // reading 2 gate
+#if RT_TERM_AFTER
+                {
+                // the light's term is formed after the shadow ray, only if it reaches the light
+                // (nothing but the running sum stays live across the traversal)
+                const float3 os = fma3(nf, BIAS, p);
+                const float3 sv = Lp - os;
+                const float dist = sqrtf(dot(sv, sv));
+                cnt.add(CNT_SHADOW);
+                int* hint = (RT_OCC_CACHE && j < RT_OCC_LIGHTS) ? occ_hint + j * RT_BLOCK : nullptr;
+                if (!occluded<COUNT, ACC>(S, os, sv * (1.0f / dist), dist, stk, cnt, hint)) {   // reading 3
+                    const float3 l2 = normalize(Lp - p);
+                    const float ndl2 = dot(nf, l2);
+                    const float3 I = xyz(__ldg(&S.lights[2 * j + 1]));
+                    const float3 rv = nf * (2.0f * ndl2) - l2;
+                    const float rdv = -dot(rv, d);
+                    const float spec = rdv > 0.0f ? __powf(rdv, __ldg(&S.mats[3 * mat]).w) : 0.0f;
+                    c = c + ((xyz(__ldg(&S.mats[3 * mat])) * I) * ndl2 + (xyz(__ldg(&S.mats[3 * mat + 1])) * I) * spec);
+                }
+                continue;
+                }
+#endif
                 // the light's term, added only if the shadow ray reaches the light
                 const float3 I = xyz(__ldg(&S.lights[2 * j + 1]));
                 const float3 rv = nf * (2.0f * ndl) - l;
