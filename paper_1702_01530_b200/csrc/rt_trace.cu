@@ -14,12 +14,6 @@
 // the SIMT loss is inside BVH traversal, not in idle ray-tree tails, and v2's barriers stalled.
 #include "rt_trace.cuh"
 
-#ifndef RT_TERM_AFTER
-#define RT_TERM_AFTER 0   // 1: form a light's Phong term after its shadow ray (only when unoccluded)
-#endif
-#ifndef RT_LIT_COMPACT
-#define RT_LIT_COMPACT 0  // 1: each lane traces its own lit lights back to back (measured slower)
-#endif
 #ifndef RT_WORK_MODE
 #define RT_WORK_MODE 0   // 0: warps take 8x4 blocks; 1: warps take whole tiles; 2: CTA tile ring
 #endif
@@ -111,38 +105,6 @@ __device__ __forceinline__ float3 trace_pixel(const TraceParams& P, float3 o, fl
 #if RT_SHADOW_STATS
             uint32_t tsum = 0;
 #endif
-#if RT_LIT_COMPACT && !RT_PACKET && !RT_SHADOW_STATS
-            // Each lane walks its OWN lit lights in order: pass k traces the k-th light whose
-            // n.l > 0 at this lane's hit point, so a warp runs max_lane(#lit) shadow passes instead
-            // of one per light, and a lane whose light is behind it no longer idles through that
-            // light's pass.  Same lights, same order per lane: results are unchanged.
-            if (S.n_lights <= 32) {
-                unsigned litm = 0;
-                for (int j = 0; j < S.n_lights; ++j) {
-                    cnt.add(CNT_LIGHT_EVALS);
-                    const float3 Lp = xyz(__ldg(&S.lights[2 * j]));
-                    if (dot(nf, normalize(Lp - p)) > 0.0f) litm |= 1u << j;      // reading 2 gate
-                }
-                while (litm) {
-                    const int j = __ffs(litm) - 1;
-                    litm &= litm - 1u;
-                    const float3 Lp = xyz(__ldg(&S.lights[2 * j]));
-                    const float3 l = normalize(Lp - p);
-                    const float ndl = dot(nf, l);
-                    const float3 I = xyz(__ldg(&S.lights[2 * j + 1]));
-                    const float3 rv = nf * (2.0f * ndl) - l;
-                    const float rdv = -dot(rv, d);
-                    const float spec = rdv > 0.0f ? __powf(rdv, __ldg(&S.mats[3 * mat]).w) : 0.0f;
-                    const float3 term = (xyz(__ldg(&S.mats[3 * mat])) * I) * ndl + (xyz(__ldg(&S.mats[3 * mat + 1])) * I) * spec;
-                    const float3 os = fma3(nf, BIAS, p);
-                    const float3 sv = Lp - os;
-                    const float dist = sqrtf(dot(sv, sv));
-                    cnt.add(CNT_SHADOW);
-                    int* hint = (RT_OCC_CACHE && j < RT_OCC_LIGHTS) ? occ_hint + j * RT_BLOCK : nullptr;
-                    if (!occluded<COUNT, ACC>(S, os, sv * (1.0f / dist), dist, stk, cnt, hint)) c = c + term;   // reading 3
-                }
-            } else
-#endif
             for (int j = 0; j < S.n_lights; ++j) {
 #if !RT_SHADOW_STATS
                 cnt.add(CNT_LIGHT_EVALS);
@@ -169,27 +131,6 @@ __device__ __forceinline__ float3 trace_pixel(const TraceParams& P, float3 o, fl
                 }
 #endif
                 if (ndl <= 0.0f) continue;                               // reading 2 gate
-#if RT_TERM_AFTER
-                {
-                // the light's term is formed after the shadow ray, only if it reaches the light
-                // (nothing but the running sum stays live across the traversal)
-                const float3 os = fma3(nf, BIAS, p);
-                const float3 sv = Lp - os;
-                const float dist = sqrtf(dot(sv, sv));
-                cnt.add(CNT_SHADOW);
-                int* hint = (RT_OCC_CACHE && j < RT_OCC_LIGHTS) ? occ_hint + j * RT_BLOCK : nullptr;
-                if (!occluded<COUNT, ACC>(S, os, sv * (1.0f / dist), dist, stk, cnt, hint)) {   // reading 3
-                    const float3 l2 = normalize(Lp - p);
-                    const float ndl2 = dot(nf, l2);
-                    const float3 I = xyz(__ldg(&S.lights[2 * j + 1]));
-                    const float3 rv = nf * (2.0f * ndl2) - l2;
-                    const float rdv = -dot(rv, d);
-                    const float spec = rdv > 0.0f ? __powf(rdv, __ldg(&S.mats[3 * mat]).w) : 0.0f;
-                    c = c + ((xyz(__ldg(&S.mats[3 * mat])) * I) * ndl2 + (xyz(__ldg(&S.mats[3 * mat + 1])) * I) * spec);
-                }
-                continue;
-                }
-#endif
                 // the light's term, added only if the shadow ray reaches the light
                 const float3 I = xyz(__ldg(&S.lights[2 * j + 1]));
                 const float3 rv = nf * (2.0f * ndl) - l;

@@ -39,17 +39,11 @@ namespace rtb {
 #if RT_FAST_PUSH && !RT_SMEM_PTX
 #error "RT_FAST_PUSH needs RT_SMEM_PTX"
 #endif
-#ifndef RT_WW
-#define RT_WW 0            // while-while traversal: bit 0 nearest-hit rays, bit 1 any-hit rays (BVH4)
-#endif
 #ifndef RT_TREE_STATS
 #define RT_TREE_STATS 0    // 1: instrumented build records ray-tree loop lane utilisation (experiments)
 #endif
 #ifndef RT_SHADOW_STATS
 #define RT_SHADOW_STATS 0  // 1: instrumented build records warp-level traversal divergence (experiments)
-#endif
-#ifndef RT_CH_EARLY
-#define RT_CH_EARLY 0     // 1: the hit mask depends on the child codes, so ptxas loads them with the planes
 #endif
 #ifndef RT_LEAN_MASK
 #define RT_LEAN_MASK 1    // BVH4 hit mask built from the slab predicates (no -1 sentinel distances)
@@ -321,17 +315,6 @@ __device__ __forceinline__ unsigned node4_hits(const float4* __restrict__ nodes,
     m |= tn[2] >= 0.0f ? 4u : 0u;
     m |= tn[3] >= 0.0f ? 8u : 0u;
     return m;
-#endif
-}
-
-// An impossible child code (0x7ffffffe: no node index, leaf code or WIDE_EMPTY) folded into the
-// hit mask keeps ptxas from sinking the child-code load below the "any child hit?" branch.
-__device__ __forceinline__ unsigned ch_dep(const int4& ch) {
-#if RT_CH_EARLY
-    return ch.x == 0x7ffffffe ? 1u : 0u;
-#else
-    (void)ch;
-    return 0u;
 #endif
 }
 
@@ -710,29 +693,6 @@ __device__ __forceinline__ Hit closest_hit(const DevScene& S, float3 o, float3 d
     int sp = 0;
     int node = S.root;
     int top = 0;          // cached top stack entry (RT_TOP_REG)
-#if (RT_WW & 1) && RT_BVH_WIDTH == 4
-    // while-while (Aila & Laine 2009): a lane descends through inner nodes until it holds a
-    // leaf (or is done); the warp then tests the leaves of all lanes together, so the node and
-    // leaf code are not both issued in every step of a mixed warp
-    while (true) {
-        while (node >= 0) {
-            cnt.step();
-            cnt.add(CNT_NODE_VISITS);
-            float tn[4];
-            int4 ch;
-            const unsigned m = node4_hits(S.nodes, node, rb, h.t, tn, ch);
-            if (order_push(m, tn, ch, stk, sp, node)) continue;
-            if (sp == 0) return h;
-            node = stk.get(--sp);
-        }
-        cnt.step();
-        const int enc = ~node;
-        const int first = enc & ((1 << LEAF_SHIFT) - 1);
-        leaf_test(first, first + (enc >> LEAF_SHIFT));
-        if (sp == 0) return h;
-        node = stk.get(--sp);
-    }
-#endif
     while (true) {
         cnt.step();
         if (node >= 0) {
@@ -744,7 +704,7 @@ __device__ __forceinline__ Hit closest_hit(const DevScene& S, float3 o, float3 d
 #else
             float tn[4];
             int4 ch;
-            const unsigned m = node4_hits(S.nodes, node, rb, h.t, tn, ch) | ch_dep(ch);
+            const unsigned m = node4_hits(S.nodes, node, rb, h.t, tn, ch);
 #if RT_TOP_REG && RT_CLOSEST_SORT
             if (order_push_top(m, tn, ch, stk, sp, top, node)) continue;
 #elif RT_CLOSEST_SORT
@@ -815,26 +775,6 @@ __device__ __forceinline__ bool occluded(const DevScene& S, float3 o, float3 d, 
     int sp = 0;
     int node = S.root;
     int top = 0;          // cached top stack entry (RT_TOP_REG)
-#if (RT_WW & 2) && RT_BVH_WIDTH == 4 && !RT_SHADOW_SORT
-    while (true) {
-        while (node >= 0) {
-            cnt.step();
-            cnt.add(CNT_NODE_VISITS);
-            float tn[4];
-            int4 ch;
-            const unsigned m = node4_hits(S.nodes, node, rb, dist, tn, ch);
-            if (plain_push(m, ch, stk, sp, node)) continue;
-            if (sp == 0) return false;
-            node = stk.get(--sp);
-        }
-        cnt.step();
-        const int enc = ~node;
-        const int first = enc & ((1 << LEAF_SHIFT) - 1);
-        if (leaf_test(first, first + (enc >> LEAF_SHIFT))) return true;
-        if (sp == 0) return false;
-        node = stk.get(--sp);
-    }
-#endif
     while (true) {
         cnt.step();
         if (node >= 0) {
@@ -846,7 +786,7 @@ __device__ __forceinline__ bool occluded(const DevScene& S, float3 o, float3 d, 
 #else
             float tn[4];
             int4 ch;
-            const unsigned m = node4_hits(S.nodes, node, rb, dist, tn, ch) | ch_dep(ch);
+            const unsigned m = node4_hits(S.nodes, node, rb, dist, tn, ch);
 #if RT_SHADOW_SORT == 2
             if (m) {   // far-first: entry distances mirrored (0x7effffff - bits; misses stay last)
 #pragma unroll
