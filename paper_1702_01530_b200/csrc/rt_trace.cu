@@ -14,12 +14,6 @@
 // the SIMT loss is inside BVH traversal, not in idle ray-tree tails, and v2's barriers stalled.
 #include "rt_trace.cuh"
 
-#ifndef RT_WORK_MODE
-#define RT_WORK_MODE 0   // 0: warps take 8x4 blocks; 1: warps take whole tiles; 2: CTA tile ring
-#endif
-#if RT_WORK_MODE == 2 && RT_BLOCK != 256
-#error "RT_WORK_MODE 2 (CTA tile ring) needs 8-warp CTAs (-DRT_BLOCK=256)"
-#endif
 
 namespace rtb {
 
@@ -238,53 +232,11 @@ __global__ void __launch_bounds__(RT_BLOCK, RT_MINB) k_trace_stereo(const TraceP
     __shared__ int s_occ[RT_OCC_LIGHTS * RT_BLOCK];  // [light][thread] last-occluder hints
 #pragma unroll
     for (int j = 0; j < RT_OCC_LIGHTS; ++j) s_occ[j * RT_BLOCK + threadIdx.x] = -1;
-#if RT_WORK_MODE == 2
-    // CTA tile ring: the 8 warps of a CTA share 16x16 tiles (one 8x4 block each) so an SM's L1
-    // serves neighbouring rays; tiles come from the global counter, block claims from shared memory
-    __shared__ int s_claim;
-    __shared__ int s_tile[16];
-    __shared__ int s_seq[16];
-    if (threadIdx.x == 0) s_claim = 0;
-    if (threadIdx.x < 16) s_seq[threadIdx.x] = -1;
-    __syncthreads();
-#endif
-#if RT_WORK_MODE == 1
-    int w_tile = 0, w_sub = 8;
-#endif
     while (true) {
         int base = 0;
-#if RT_WORK_MODE == 0
         if (lane == 0) base = atomicAdd(P.work_counter, 32);
         base = __shfl_sync(0xffffffffu, base, 0);
         if (base >= P.n_work) break;
-#elif RT_WORK_MODE == 1
-        if (w_sub == 8) {                                  // this warp takes a whole tile
-            if (lane == 0) w_tile = atomicAdd(P.work_counter, 1);
-            w_tile = __shfl_sync(0xffffffffu, w_tile, 0);
-            w_sub = 0;
-        }
-        if (w_tile >= P.n_tiles) break;
-        base = w_tile * 256 + 32 * w_sub++;
-#else
-        int j = 0, tile = 0;
-        if (lane == 0) {
-            j = atomicAdd(&s_claim, 1);
-            const int q = j >> 3, slot = q & 15;
-            if ((j & 7) == 0) {
-                tile = atomicAdd(P.work_counter, 1);
-                s_tile[slot] = tile;
-                __threadfence_block();
-                atomicExch(&s_seq[slot], q);
-            } else {
-                while (atomicAdd(&s_seq[slot], 0) != q) { }
-                tile = s_tile[slot];
-            }
-        }
-        j = __shfl_sync(0xffffffffu, j, 0);
-        tile = __shfl_sync(0xffffffffu, tile, 0);
-        if (tile >= P.n_tiles) break;
-        base = tile * 256 + 32 * (j & 7);
-#endif
         const int k = base + lane;
         int eye, px, py, lt;
         if (map_work(P, k, eye, px, py, lt)) {
