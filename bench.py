@@ -2,13 +2,18 @@
 """Benchmark of the stereo Whitted hot path (BASELINE.json metric on configs[3] = C4).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C4]
+                    [--inflight F] [--gather peer|nccl] [--no-e2e] [--no-cpu-baseline]
 
 One "step" = one stereo frame of the whole hot path: primary rays,
 LBVH traversal + intersection, shading with shadow rays, reflection/refraction to max_depth,
-pack to RGBA8, and for N>1 the gather of the tile shards to rank 0 (NCCL) + root unpack.
+pack to RGBA8, and for N>1 the assembly of every rank's tiles in rank 0's framebuffers (fused
+peer stores over NVLink by default, or NCCL gather + root unpack with --gather nccl).
 The scene (upload + LBVH build, a1-a2) is resident before the timed region; its cost is
-reported separately as scene_upload_ms.  Multi-GPU: launched by torchrun, one process per
-GPU, image tiles sharded across ranks (strong scaling: the frame is fixed), max over ranks.
+reported separately as scene_upload_ms.  Two timed regions: one frame at a time (latency and
+the kernel's own duration, L2 flushed before each frame outside the events) and the throughput
+loop behind `value` (F = 4 frames in flight on 4 streams, L2 flush per frame inside the timed
+region).  Multi-GPU: launched by torchrun, one process per GPU, image tiles sharded across ranks
+(strong scaling: the frame is fixed), device-timed, max over ranks.
 
 Rank 0 prints ONE JSON line.  `--impl reference` times the CPU oracle (oracle/, brute force,
 double precision) on bounded pixel samples of the same workload instead.
