@@ -122,14 +122,31 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------ CPU oracle legs
-def oracle_sample(scene, n_per_eye, seed, threads):
+def oracle_sample(scene, n_per_eye, seed, threads, keep=None):
     from oracle.oracle import Oracle
     pix = scenes.sample_pixels(scene.width, scene.height, n_per_eye, seed)
     o = Oracle(scene)
     t0 = time.perf_counter()
     out = o.render(pixels=pix, flags=False, threads=threads)
     dt = time.perf_counter() - t0
+    if keep is not None:
+        keep.update(out=out, pix=pix)
     return int(out["counts"].sum()), dt, len(pix)
+
+
+def sample_agreement(gpu, keep):
+    """Raw agreement of the GPU frame with the oracle on the timed sample (no fragile-pixel
+    exclusion: the north-star criteria with exclusions are the GPU tests' job)."""
+    out, pix = keep["out"], keep["pix"]
+    e, x, y = pix[:, 0], pix[:, 1], pix[:, 2]
+    gid = gpu["id"][e, y, x]
+    d8 = np.abs(gpu["fb"][e, y, x][:, :3].astype(int) - out["rgba8"].reshape(-1, 4)[:, :3].astype(int)).max(1)
+    err = np.abs(np.clip(gpu["radiance"][e, y, x][:, :3].astype(np.float64), 0, 1)
+                 - np.clip(out["radiance"].reshape(-1, 3), 0, 1)).max(1)
+    return {"pixels": int(len(pix)), "id_equal_frac": float((gid == out["id"].reshape(-1)).mean()),
+            "rgb_within_2_frac": float((d8 <= 2).mean()), "max_abs_radiance_err": float(err.max()),
+            "p999_abs_radiance_err": float(np.quantile(err, 0.999)),
+            "note": "raw, on the cpu_baseline sample, fragile pixels included"}
 
 
 def cpu_model():
@@ -143,13 +160,15 @@ def cpu_model():
     return None
 
 
-def cpu_baseline(scene, target_s=15.0, seed=99):
-    """The oracle as it stands, timed on this host's cores on a bounded pixel sample."""
+def cpu_baseline(scene, target_s=15.0, seed=99, gpu=None):
+    """The oracle as it stands, timed on this host's cores on a bounded pixel sample (and, given
+    the GPU's full frame, the raw agreement of the two on that sample)."""
     threads = os.cpu_count() or 1
     rays, dt, n = oracle_sample(scene, 8, seed, threads)          # calibration
     per_px = dt / n
     n_eye = int(max(8, min(4096, target_s / max(per_px, 1e-9) / 2)))
-    rays, dt, n = oracle_sample(scene, n_eye, seed + 1, threads)
+    keep = {}
+    rays, dt, n = oracle_sample(scene, n_eye, seed + 1, threads, keep)
     # single-core rate on a smaller sample (SURVEY §8(d) "also report 1-core numbers")
     n1 = int(max(2, min(n_eye, target_s / 3 / max(per_px * threads, 1e-9) / 2)))
     r1, d1, _ = oracle_sample(scene, n1, seed + 2, 1)
@@ -159,7 +178,8 @@ def cpu_baseline(scene, target_s=15.0, seed=99):
             "sample": f"{n} seeded pixels ({n // 2} per eye) of {scene.name} {scene.width}x{scene.height} stereo, "
                       f"depth {scene.max_depth}: {rays} rays in {dt:.1f} s (double precision, brute force, "
                       f"OpenMP {threads} threads)",
-            "frame_s_extrapolated": dt / n * 2 * scene.width * scene.height}
+            "frame_s_extrapolated": dt / n * 2 * scene.width * scene.height,
+            **({"gpu_agreement": sample_agreement(gpu, keep)} if gpu is not None else {})}
 
 
 def run_reference(args, scene):
@@ -431,7 +451,12 @@ def run_ours(args, scene):
         if e2e is not None:
             line["e2e"] = e2e
         if not args.no_cpu_baseline:
-            line["cpu_baseline"] = cpu_baseline(scene, target_s=args.cpu_seconds)
+            # the GPU's full frame (untimed, ids + radiance), compared with the oracle on the
+            # baseline's own sample
+            g = R.render(W, H, D, want_id=True, want_radiance=True)
+            torch.cuda.synchronize()
+            gpu = {k: v.cpu().numpy() for k, v in g.items()}
+            line["cpu_baseline"] = cpu_baseline(scene, target_s=args.cpu_seconds, gpu=gpu)
         print(json.dumps(line), flush=True)
     for f in frames:
         f.close()
