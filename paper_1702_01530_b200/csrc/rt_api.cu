@@ -17,12 +17,23 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/rt_b200.h"
 #include "rt_internal.h"
 
 namespace {
 
 thread_local std::string g_err;
+
+// NVTX range over a C-ABI call (SURVEY §5 tracing): visible in Nsight Systems timelines, free
+// when no tool is attached (NVTX3 is header-only)
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 rt_status fail(rt_status s, const char* fmt, ...) {
     char buf[1024];
@@ -206,6 +217,7 @@ rt_status rt_synchronize(rt_context* c) {
 // ------------------------------------------------------------------------------ scene upload
 rt_status rt_scene_upload(rt_context* c, const rt_primitives* P, const rt_material* mats, uint32_t n_mats,
                           const rt_light* lights, uint32_t n_lights, const rt_env* env) {
+    NvtxRange nvtx_("rt_scene_upload");
     if (!c || !P || !env) return fail(RT_ERR_INVALID_ARG, "rt_scene_upload: NULL context/primitives/env");
     if ((n_mats && !mats) || (n_lights && !lights))
         return fail(RT_ERR_INVALID_ARG, "rt_scene_upload: NULL materials/lights with nonzero count");
@@ -478,6 +490,7 @@ rt_status rt_scene_upload(rt_context* c, const rt_primitives* P, const rt_materi
 
 // ------------------------------------------------------------------------------ refit (NEXT-3)
 rt_status rt_scene_update_vertices(rt_context* c, const float* vertices, uint32_t n_vertices) {
+    NvtxRange nvtx_("rt_scene_update_vertices");
     if (!c || (!vertices && n_vertices)) return fail(RT_ERR_INVALID_ARG, "rt_scene_update_vertices: NULL argument");
     if (!c->has_scene) return fail(RT_ERR_NO_SCENE, "rt_scene_update_vertices: no scene");
     if (n_vertices != c->n_vertices)
@@ -610,11 +623,13 @@ rt_status render_impl(rt_context* c, const rt_render_params* p, const rt_outputs
 }
 
 rt_status rt_render_stereo_ex(rt_context* c, const rt_render_params* p, const rt_outputs* out) {
+    NvtxRange nvtx_("rt_render_stereo_ex");
     if (!c || !p || !out) return fail(RT_ERR_INVALID_ARG, "rt_render_stereo_ex: NULL argument");
     return render_impl(c, p, out, c->stream);
 }
 
 rt_status rt_render_stereo_async(rt_context* c, const rt_render_params* p, const rt_outputs* out, void* cuda_stream) {
+    NvtxRange nvtx_("rt_render_stereo_async");
     if (!c || !p || !out) return fail(RT_ERR_INVALID_ARG, "rt_render_stereo_async: NULL argument");
     return render_impl(c, p, out, cuda_stream ? static_cast<cudaStream_t>(cuda_stream) : c->stream);
 }
@@ -741,6 +756,7 @@ rt_status rt_download(rt_context* c, const void* dev_src, void* host_dst, size_t
 
 rt_status rt_download_after(rt_context* c, const void* dev_src, void* host_dst, size_t bytes, void* after_stream,
                             rt_event** done) {
+    NvtxRange nvtx_("rt_download");
     if (done) *done = nullptr;
     if (!c || !dev_src || !host_dst || !bytes) return fail(RT_ERR_INVALID_ARG, "rt_download: NULL pointer or zero size");
     CUDA_TRY(cudaSetDevice(c->device));
@@ -845,6 +861,7 @@ rt_status rt_unpack_shards_host(const void* gathered, uint32_t W, uint32_t H, ui
 
 rt_status rt_unpack_shards(rt_context* c, const void* gathered, uint32_t W, uint32_t H, uint32_t world, uint32_t format,
                            rt_fb left, rt_fb right) {
+    NvtxRange nvtx_("rt_unpack_shards");
     if (!c || !gathered) return fail(RT_ERR_INVALID_ARG, "rt_unpack_shards: NULL argument");
     uint64_t per = 0;
     rt_status st = rt_shard_bytes(W, H, world, format, &per);
@@ -930,6 +947,7 @@ rt_status rt_ipc_close(rt_context* c, void* dev_ptr) {
 
 // ------------------------------------------------------------------------------ composition
 rt_status rt_compose(rt_context* c, rt_fb left, rt_fb right, uint32_t W, uint32_t H, uint32_t mode, rt_fb out) {
+    NvtxRange nvtx_("rt_compose");
     if (!c || !left.dev_ptr || !right.dev_ptr || !out.dev_ptr) return fail(RT_ERR_INVALID_ARG, "rt_compose: NULL argument");
     if (left.format != RT_FORMAT_RGBA8 || right.format != RT_FORMAT_RGBA8 || out.format != RT_FORMAT_RGBA8)
         return fail(RT_ERR_INVALID_ARG, "rt_compose: RGBA8 framebuffers only");
@@ -948,6 +966,7 @@ rt_status rt_compose(rt_context* c, rt_fb left, rt_fb right, uint32_t W, uint32_
 
 // ------------------------------------------------------------------------------ introspection
 rt_status rt_kdtree_build(rt_context* c, uint32_t max_leaf, uint32_t max_depth, uint64_t info[6]) {
+    NvtxRange nvtx_("rt_kdtree_build");
     if (!c) return fail(RT_ERR_INVALID_ARG, "rt_kdtree_build: NULL context");
     if (max_leaf < 1 || max_leaf > 4096) return fail(RT_ERR_INVALID_ARG, "rt_kdtree_build: max_leaf %u", max_leaf);
     if (max_depth > 60) return fail(RT_ERR_INVALID_ARG, "rt_kdtree_build: max_depth %u > 60", max_depth);
