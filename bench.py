@@ -636,10 +636,16 @@ def main():
                     help="N>1 frame assembly: fused peer stores into rank 0's FB (default) or NCCL gather")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--width", type=int, default=0, help="override the config's per-eye width")
+    ap.add_argument("--height", type=int, default=0, help="override the config's per-eye height")
+    ap.add_argument("--depth", type=int, default=-1, help="override the config's max_depth")
     ap.add_argument("--inflight", type=int, default=4,
                     help="frames in flight on separate streams in the throughput loop (1 = one at a time)")
     args = ap.parse_args()
     scene = scenes.make_scene(args.config)
+    if args.width > 0 or args.height > 0 or args.depth >= 0:
+        scene = scene.with_view(width=args.width or scene.width, height=args.height or scene.height,
+                                max_depth=args.depth if args.depth >= 0 else scene.max_depth)
     if args.impl == "reference":
         return run_reference(args, scene)
     return run_ours(args, scene)
