@@ -87,7 +87,7 @@ def main():
         summary["complexity"][f"paper{n}"] = med
         print(f"paper{n}: {rs[0]['triangles']:4d} tris  in {med['transfer_in_ns']:.3f} ms  compute {med['compute_ns']:.3f} ms"
               f"  out {med['transfer_out_ns']:.3f} ms  compute fraction {med['compute_fraction']:.2f}", flush=True)
-    for limit in (1, 2, 4, 8, 16, 37, 74, 148, 296, 592):
+    for limit in (1, 2, 4, 8, 16, 37, 74, 148, 296, 592, 1184, 2368):
         ms = grid_run(limit)
         summary["grid"][limit] = ms
         print(f"trace CTAs {limit:4d}: {ms:.3f} ms", flush=True)
