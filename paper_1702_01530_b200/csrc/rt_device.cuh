@@ -239,7 +239,7 @@ __device__ __forceinline__ bool plane_intersect(float3 o, float3 d, float4 p, fl
     const float3 n = xyz(p);
     const float den = dot(n, d);
     if (den == 0.0f) return false;
-    t = (p.w - dot(n, o)) / den;
+    t = __fdividef(p.w - dot(n, o), den);   // like the sphere and triangle tests: no IEEE-division slow-path call (and the spills around it)
     return true;
 }
 
