@@ -115,11 +115,11 @@ __device__ __forceinline__ float3 trace_pixel(const TraceParams& P, float3 o, fl
                     const float3 term = (xyz(__ldg(&S.mats[3 * mat])) * I) * ndl + (xyz(__ldg(&S.mats[3 * mat + 1])) * I) * spec;
                     const float3 os = fma3(nf, BIAS, p);
                     const float3 sv = Lp - os;
-                    const float dist = sqrtf(dot(sv, sv));
+                    const float dist = sqrt_dist(dot(sv, sv));
                     const bool lit = ndl > 0.0f;                         // reading 2 gate
                     if (lit) cnt.add(CNT_SHADOW);
                     int* hint = (RT_OCC_CACHE && j < RT_OCC_LIGHTS) ? occ_hint + j * RT_BLOCK : nullptr;
-                    if (!occluded_packet<COUNT>(S, os, sv * (1.0f / dist), dist, lit, pmask, stk, cnt, hint) && lit)
+                    if (!occluded_packet<COUNT>(S, os, sv * rcp_dist(dist), dist, lit, pmask, stk, cnt, hint) && lit)
                         c = c + term;                                    // reading 3
                     continue;
                 }
@@ -133,12 +133,12 @@ __device__ __forceinline__ float3 trace_pixel(const TraceParams& P, float3 o, fl
                 const float3 term = (xyz(__ldg(&S.mats[3 * mat])) * I) * ndl + (xyz(__ldg(&S.mats[3 * mat + 1])) * I) * spec;
                 const float3 os = fma3(nf, BIAS, p);
                 const float3 sv = Lp - os;
-                const float dist = sqrtf(dot(sv, sv));
+                const float dist = sqrt_dist(dot(sv, sv));
                 cnt.add(CNT_SHADOW);
                 int* hint = (RT_OCC_CACHE && j < RT_OCC_LIGHTS) ? occ_hint + j * RT_BLOCK : nullptr;
 #if RT_SHADOW_STATS
                 const uint32_t s0 = cnt.steps;
-                const bool occ = occluded<COUNT, ACC>(S, os, sv * (1.0f / dist), dist, stk, cnt, hint);
+                const bool occ = occluded<COUNT, ACC>(S, os, sv * rcp_dist(dist), dist, stk, cnt, hint);
                 if (COUNT) {   // c[6] += per-light warp max of shadow steps, c[7] += their sum
                     const uint32_t T = cnt.steps - s0, am = __activemask();
                     const uint32_t mx = __reduce_max_sync(am, T), sm = __reduce_add_sync(am, T);
@@ -147,7 +147,7 @@ __device__ __forceinline__ float3 trace_pixel(const TraceParams& P, float3 o, fl
                 }
                 if (!occ) c = c + term;
 #else
-                if (!occluded<COUNT, ACC>(S, os, sv * (1.0f / dist), dist, stk, cnt, hint)) c = c + term;   // reading 3
+                if (!occluded<COUNT, ACC>(S, os, sv * rcp_dist(dist), dist, stk, cnt, hint)) c = c + term;   // reading 3
 #endif
             }
 #if RT_SHADOW_STATS
@@ -162,14 +162,14 @@ __device__ __forceinline__ float3 trace_pixel(const TraceParams& P, float3 o, fl
                 float kr_eff = __ldg(&S.mats[3 * mat + 1]).w;
                 const float kt = m2.x;
                 if (kt > 0.0f) {
-                    const float eta = front ? 1.0f / m2.y : m2.y;
+                    const float eta = front ? rcp_dist(m2.y) : m2.y;
                     const float cosi = -dot(d, nf);
                     const float kk = 1.0f - eta * eta * (1.0f - cosi * cosi);
                     if (kk < 0.0f) {
                         kr_eff += kt;                                    // reading 5 TIR
                     } else {
                         cnt.add(CNT_REFRACTION);
-                        const float3 td = normalize(d * eta + nf * (eta * cosi - sqrtf(kk)));
+                        const float3 td = normalize(d * eta + nf * (eta * cosi - sqrt_dist(kk)));
                         const float3 to = fma3(nf, -BIAS, p);
                         st_a[sp] = make_float4(to.x, to.y, to.z, w * kt);
                         st_b[sp] = make_float4(td.x, td.y, td.z, __int_as_float(depth - 1));
