@@ -235,7 +235,8 @@ rt_status rt_upload(rt_context* ctx, const void* host_src, void* dev_dst, size_t
 /* Tile shard map: the image of each eye is cut into RT_TILE x RT_TILE tiles,
  * tiles_per_eye = T = ceil(W/16)*ceil(H/16).  Global tile id G in [0, 2T) interleaves the eyes:
  * eye = G mod 2, tile = G div 2 (raster order).  world == 2: rank r renders eye r, every tile
- * (the paper's level-1 eye split).  Otherwise (world == 1 included) tile t goes, in
+ * (the paper's level-1 eye split; environment RT_SHARD_PAIRS=1, read once per
+ * process and required to match on every rank, deals tile pairs at world 2 too).  Otherwise (world == 1 included) tile t goes, in
  * both eyes, to rank t mod world, so a rank's shard-local tile lt is G = 2 (rank + (lt div 2)
  * world) + (lt mod 2): the two eyes of a tile are traced together (one warp = the same 4x4
  * pixel block in both eyes).

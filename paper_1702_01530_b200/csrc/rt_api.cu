@@ -587,7 +587,10 @@ ShardGeom shard_geom(uint32_t W, uint32_t H, uint32_t world) {
     g.tiles_x = (int)((W + RT_TILE - 1) / RT_TILE);
     g.tiles_y = (int)((H + RT_TILE - 1) / RT_TILE);
     g.tiles_per_eye = g.tiles_x * g.tiles_y;
-    g.mode = world == 1 ? 0 : (world == 2 ? 1 : 2);   // 1: eye split; 0 / 2: tile pairs round-robin
+    // 1: eye split; 0 / 2: tile pairs round-robin.  RT_SHARD_PAIRS=1 (experiment knob; every
+    // rank and the root must see the same value) deals tile pairs at world 2 as well.
+    static const bool pairs_at_2 = [] { const char* e = getenv("RT_SHARD_PAIRS"); return e && atoi(e) != 0; }();
+    g.mode = world == 1 ? 0 : (world == 2 && !pairs_at_2 ? 1 : 2);
     return g;
 }
 

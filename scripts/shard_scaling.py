@@ -20,6 +20,7 @@ from paper_1702_01530_b200 import rt, scenes  # noqa: E402
 
 NOFLUSH = os.environ.get("RT_NOFLUSH") == "1"   # warm-L2 comparison only (the bench always flushes)
 INFLIGHT = int(os.environ.get("RT_INFLIGHT", "4"))
+K_FRAMES = int(os.environ.get("RT_K", "24"))        # frames per pipelined measurement (the drain is amortised over K)
 
 
 def main():
@@ -51,7 +52,7 @@ def main():
                         ts.append(ev[0].elapsed_time(ev[1]))
                 per_rank.append(float(np.median(ts)))
                 # the bench's throughput regime: INFLIGHT frames in flight, flush before each
-                K = 24
+                K = K_FRAMES
                 for rep in range(2):
                     torch.cuda.synchronize()
                     st = torch.cuda.Event(enable_timing=True)

@@ -9,6 +9,7 @@ import pytest
 from paper_1702_01530_b200 import rt
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+PAIRS_AT_2 = os.environ.get("RT_SHARD_PAIRS", "0") not in ("", "0")   # library knob, read once
 
 
 def header_symbols():
@@ -81,8 +82,9 @@ def test_shard_map_exact_cover(W, H, world):
         counts.append(len(ids))
     assert np.all(owners >= 0)
     # tiles are dealt in eye pairs: ranks differ by at most one tile pair
-    assert max(counts) - min(counts) <= (1 if world == 2 else 2) or T < world
-    if world == 2:                                  # G = 2*tile + eye
+    eye_split = world == 2 and not PAIRS_AT_2
+    assert max(counts) - min(counts) <= (1 if eye_split else 2) or T < world
+    if eye_split:                                   # G = 2*tile + eye
         assert np.all(owners[0::2] == 0) and np.all(owners[1::2] == 1)
     per = rt.rt_shard_bytes(W, H, world)
     assert per == max(counts) * 256 * 4
@@ -117,6 +119,29 @@ def test_host_unpack_roundtrip(world):
     L, R = rt.rt_unpack_shards_host(g.view(np.uint8).reshape(-1), W, H, world)
     got = np.stack([L, R]).view(np.uint32)[..., 0]
     np.testing.assert_array_equal(got, expected_image(W, H))
+
+
+def test_shard_pairs_knob_at_world_2():
+    """RT_SHARD_PAIRS=1 deals tile pairs round-robin at world 2 too: both eyes of a
+    tile on one rank, exact cover, and the host unpack still reassembles the image."""
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, sys; sys.path.insert(0, %r); sys.path.insert(0, %r)\n"
+        "from paper_1702_01530_b200 import rt\n"
+        "import test_abi as t\n"
+        "W, H = 93, 61; T = 6 * 4\n"
+        "a, b = (rt.rt_shard_tiles(W, H, r, 2).astype(int) for r in (0, 1))\n"
+        "assert sorted(np.concatenate([a, b]).tolist()) == list(range(2 * T))\n"
+        "assert set(a >> 1).isdisjoint(set(b >> 1))\n"
+        "assert all(((g >> 1) %% 2) == 0 for g in a) and all(((g >> 1) %% 2) == 1 for g in b)\n"
+        "g = t.synth_shards(W, H, 2)\n"
+        "L, R = rt.rt_unpack_shards_host(g.view(np.uint8).reshape(-1), W, H, 2)\n"
+        "np.testing.assert_array_equal(np.stack([L, R]).view(np.uint32)[..., 0], t.expected_image(W, H))\n"
+        "print('ok')\n") % (ROOT, os.path.join(ROOT, "tests"))
+    env = dict(os.environ, RT_SHARD_PAIRS="1")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr
 
 
 def test_product_package_never_touches_the_oracle():
