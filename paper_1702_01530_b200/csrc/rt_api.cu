@@ -94,8 +94,8 @@ struct rt_context {
     int leaf_max = 1;                // LBVH leaf collapse threshold (env RT_LEAF_MAX, <= 16)
     int treelet_passes = 3;          // SAH treelet restructuring passes (env RT_TREELETS)
     int grid_limit = 0;              // cap on trace CTAs (env RT_GRID_LIMIT; 0 = full machine)
-    int l2_prefetch = 0;             // bulk L2 prefetch of the scene at each render (env RT_L2_PREFETCH=1;
-                                     // measured no gain, +40 % DRAM reads)
+    int l2_prefetch = 0;             // bulk L2 prefetch of the scene at each render (env RT_L2_PREFETCH=1,
+                                     // 2 = nodes only; measured no gain, +40 % DRAM reads)
     void* arena = nullptr;           // BVH build scratch (grow-only)
     size_t arena_bytes = 0;
     // refit state (rt_scene_update_vertices)
@@ -165,7 +165,7 @@ rt_status rt_create(int device, void* cuda_stream, rt_context** out) {
     if (const char* lm = getenv("RT_LEAF_MAX")) c->leaf_max = std::max(1, std::min(16, atoi(lm)));
     if (const char* tp = getenv("RT_TREELETS")) c->treelet_passes = std::max(0, std::min(8, atoi(tp)));
     if (const char* gl = getenv("RT_GRID_LIMIT")) c->grid_limit = std::max(0, atoi(gl));
-    if (const char* lp = getenv("RT_L2_PREFETCH")) c->l2_prefetch = atoi(lp) != 0;
+    if (const char* lp = getenv("RT_L2_PREFETCH")) c->l2_prefetch = atoi(lp);
     cudaError_t e = cudaSetDevice(device);
     if (e == cudaSuccess && cuda_stream) {
         c->stream = static_cast<cudaStream_t>(cuda_stream);
@@ -693,7 +693,7 @@ rt_status render_impl(rt_context* c, const rt_render_params* p, const rt_outputs
         P.pf_base[0] = reinterpret_cast<const char*>(c->sc.nodes);
         P.pf_bytes[0] = c->sc.nodes ? (unsigned long long)c->info[4] * rtb::NODE_F4 * 16 : 0;
         P.pf_base[1] = reinterpret_cast<const char*>(c->sc.prims);
-        P.pf_bytes[1] = (unsigned long long)c->sc.n_bvh * 48;
+        P.pf_bytes[1] = c->l2_prefetch == 2 ? 0 : (unsigned long long)c->sc.n_bvh * 48;   // 2: nodes only
         if (!P.pf_base[0]) { P.pf_base[0] = P.pf_base[1]; P.pf_bytes[0] = P.pf_bytes[1]; P.pf_bytes[1] = 0; }
     }
     P.peer_fence = (p->flags & RT_RENDER_PEER_STORE) ? 1 : 0;
