@@ -103,6 +103,9 @@ struct KdHost {
     float lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};   // root cell
 };
 void kd_build_host(const float4* prims, int n, int n_spheres, int max_leaf, int max_depth, KdHost& out);
+// experiment (rt_sah.cu, env RT_HOST_SAH=1): host binned-SAH BVH2 over the leaf boxes
+void sah_build_host(const float4* leaf_lo, const float4* leaf_hi, int n, int* left, int* right, float4* node_lo,
+                    float4* node_hi);
 }  // namespace rtb
 
 // launchers (rt_trace.cu)
