@@ -93,6 +93,7 @@ struct rt_context {
     float vfov = 0;
     int leaf_max = 1;                // LBVH leaf collapse threshold (env RT_LEAF_MAX, <= 16)
     int treelet_passes = 3;          // SAH treelet restructuring passes (env RT_TREELETS)
+    int sah_subtrees = 1;            // SAH rebuild of small LBVH subtrees (env RT_SAH_SUBTREES=0: off)
     int grid_limit = 0;              // cap on trace CTAs (env RT_GRID_LIMIT; 0 = full machine)
     int l2_prefetch = 0;             // bulk L2 prefetch of the scene at each render (env RT_L2_PREFETCH=1,
                                      // 2 = nodes only; measured no gain, +40 % DRAM reads)
@@ -164,6 +165,7 @@ rt_status rt_create(int device, void* cuda_stream, rt_context** out) {
     c->device = device;
     if (const char* lm = getenv("RT_LEAF_MAX")) c->leaf_max = std::max(1, std::min(16, atoi(lm)));
     if (const char* tp = getenv("RT_TREELETS")) c->treelet_passes = std::max(0, std::min(8, atoi(tp)));
+    if (const char* ss = getenv("RT_SAH_SUBTREES")) c->sah_subtrees = atoi(ss) != 0;
     if (const char* gl = getenv("RT_GRID_LIMIT")) c->grid_limit = std::max(0, atoi(gl));
     if (const char* lp = getenv("RT_L2_PREFETCH")) c->l2_prefetch = atoi(lp);
     cudaError_t e = cudaSetDevice(device);
@@ -426,6 +428,7 @@ rt_status rt_scene_upload(rt_context* c, const rt_primitives* P, const rt_materi
         alloc_all();                               // assign
         B.leaf_max = c->leaf_max;
         B.treelet_passes = c->treelet_passes;
+        B.sah_subtrees = c->sah_subtrees;
         cudaError_t e = rtb_build_bvh(B, c->stream, &root, &n_nodes4, &depth4, level_start.data());
         if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
         if (e == cudaSuccess && n_nodes4 > 0) {        // compact the BVH4 into an exact-size buffer

@@ -11,6 +11,8 @@
 //                    from common-prefix lengths (__clzll)
 //   k_refit          bottom-up AABB union with atomic arrival counters
 //   k_gather_prims   primitive records in leaf order
+//   k_sah_subtrees   maximal subtrees of <= 4096 primitives rebuilt by binned SAH, one CTA each
+//                    in shared memory (k_sah_roots finds them)
 //   k_treelets       SAH treelet restructuring of the BVH2 (Karras & Aila 2013), optional passes
 //   k_wide           BVH2 -> 4-wide BVH collapse (level by level), small subtrees -> leaves
 // The result is a deterministic function of the input arrays.
@@ -525,6 +527,238 @@ __global__ void k_wide(BuildBuffers B, const int2* __restrict__ fin, int n_in, i
     }
 }
 
+// ---------------------------------------------------------------- SAH subtrees
+// Every maximal LBVH subtree of at most SAH_T primitives (a contiguous Morton range [a, b] of
+// leaf slots) is rebuilt top-down by binned SAH (3 axes x SAH_BINS bins, centroid binning) by one
+// CTA in shared memory; the subtree keeps its root id and reuses its internal node ids, so the
+// nodes above it are unchanged.  Partitions are stable and the ids are taken in a fixed order:
+// the result is deterministic.  Runs before the treelet passes (parents are rewritten for them).
+constexpr int SAH_T = 4096;
+constexpr int SAH_BINS = 32;
+constexpr int SAH_THREADS = 256;
+
+__global__ void k_sah_roots(BuildBuffers B, int n, int* roots, int* n_roots) {
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n - 1; v += gridDim.x * blockDim.x) {
+        const int2 r = B.range[v];
+        if (r.y - r.x + 1 > SAH_T) continue;
+        const int p = B.parent_int[v];
+        if (p >= 0) {
+            const int2 q = B.range[p];
+            if (q.y - q.x + 1 <= SAH_T) continue;
+        }
+        roots[atomicAdd(n_roots, 1)] = v;
+    }
+}
+
+struct SahShared {
+    float lo[3][SAH_T], hi[3][SAH_T];   // item boxes (item k = leaf slot a + k)
+    short idx[SAH_T], tmp[SAH_T];
+    int ids[SAH_T];                     // internal node ids of the subtree, root first
+    int3 stack[SAH_T];                  // (begin, end, node)
+    unsigned int bmin[3][SAH_BINS][3], bmax[3][SAH_BINS][3];
+    int bcnt[3][SAH_BINS];
+    float red[SAH_THREADS / 32][12];
+    float nb[12];
+    int sp, next_id, best_axis, best_bin, nl, warp_off[SAH_THREADS / 32 + 1];
+};
+
+__device__ __forceinline__ int sah_bin(float c, float lo, float k) {
+    return min(SAH_BINS - 1, max(0, (int)((c - lo) * k)));
+}
+
+__global__ void __launch_bounds__(SAH_THREADS) k_sah_subtrees(BuildBuffers B, const int* __restrict__ roots) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    SahShared& S = *reinterpret_cast<SahShared*>(smem_raw);
+    const int root = roots[blockIdx.x];
+    const int2 rg = B.range[root];
+    const int a = rg.x, m = rg.y - rg.x + 1;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    for (int k = tid; k < m; k += SAH_THREADS) {
+        const float4 l = B.leaf_lo[a + k], h = B.leaf_hi[a + k];
+        S.lo[0][k] = l.x; S.lo[1][k] = l.y; S.lo[2][k] = l.z;
+        S.hi[0][k] = h.x; S.hi[1][k] = h.y; S.hi[2][k] = h.z;
+        S.idx[k] = (short)k;
+    }
+    if (tid == 0) {                                      // the old subtree's internal ids, root first
+        int cnt = 0, sp = 0;
+        S.stack[sp++].x = root;
+        while (sp) {
+            const int v = S.stack[--sp].x;
+            S.ids[cnt++] = v;
+            const int l = B.left[v], r = B.right[v];
+            if (l >= 0) S.stack[sp++].x = l;
+            if (r >= 0) S.stack[sp++].x = r;
+        }
+        S.sp = 1;
+        S.stack[0] = make_int3(0, m, root);
+        S.next_id = 1;
+    }
+    __syncthreads();
+    while (S.sp > 0) {
+        const int3 t = S.stack[S.sp - 1];
+        __syncthreads();
+        if (tid == 0) --S.sp;
+        const int begin = t.x, end = t.y, node = t.z, cnt = end - begin;
+        // node box and centroid bounds
+        float v[12];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) { v[q] = FLT_MAX; v[3 + q] = -FLT_MAX; v[6 + q] = FLT_MAX; v[9 + q] = -FLT_MAX; }
+        for (int i = begin + tid; i < end; i += SAH_THREADS) {
+            const int k = S.idx[i];
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                const float l = S.lo[q][k], h = S.hi[q][k], c = 0.5f * (l + h);
+                v[q] = fminf(v[q], l); v[3 + q] = fmaxf(v[3 + q], h);
+                v[6 + q] = fminf(v[6 + q], c); v[9 + q] = fmaxf(v[9 + q], c);
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < 12; ++q) {
+            const bool mx = (q >= 3 && q < 6) || q >= 9;
+            for (int off = 16; off > 0; off >>= 1) {
+                const float o = __shfl_xor_sync(0xffffffffu, v[q], off);
+                v[q] = mx ? fmaxf(v[q], o) : fminf(v[q], o);
+            }
+        }
+        if (lane == 0)
+            for (int q = 0; q < 12; ++q) S.red[wid][q] = v[q];
+        for (int q = tid; q < 3 * SAH_BINS * 3; q += SAH_THREADS) {
+            (&S.bmin[0][0][0])[q] = 0xffffffffu;
+            (&S.bmax[0][0][0])[q] = 0u;
+        }
+        for (int q = tid; q < 3 * SAH_BINS; q += SAH_THREADS) (&S.bcnt[0][0])[q] = 0;
+        __syncthreads();
+        if (tid < 12) {
+            const bool mx = (tid >= 3 && tid < 6) || tid >= 9;
+            float x = S.red[0][tid];
+            for (int w = 1; w < SAH_THREADS / 32; ++w) x = mx ? fmaxf(x, S.red[w][tid]) : fminf(x, S.red[w][tid]);
+            S.nb[tid] = x;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            B.node_lo[node] = make_float4(S.nb[0], S.nb[1], S.nb[2], 0.f);
+            B.node_hi[node] = make_float4(S.nb[3], S.nb[4], S.nb[5], 0.f);
+        }
+        // bin centroids on every axis with extent
+        float kq[3];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            const float ext = S.nb[9 + q] - S.nb[6 + q];
+            kq[q] = ext > 0.0f ? SAH_BINS * (1.0f - 1e-6f) / ext : 0.0f;
+        }
+        if (cnt > 2) {
+            for (int i = begin + tid; i < end; i += SAH_THREADS) {
+                const int k = S.idx[i];
+#pragma unroll
+                for (int q = 0; q < 3; ++q) {
+                    if (kq[q] == 0.0f) continue;
+                    const int b = sah_bin(0.5f * (S.lo[q][k] + S.hi[q][k]), S.nb[6 + q], kq[q]);
+                    atomicAdd(&S.bcnt[q][b], 1);
+#pragma unroll
+                    for (int e = 0; e < 3; ++e) {
+                        atomicMin(&S.bmin[q][b][e], f2ord(S.lo[e][k]));
+                        atomicMax(&S.bmax[q][b][e], f2ord(S.hi[e][k]));
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        if (tid == 0) {
+            int ba = -1, bb = 0, bnl = 0;
+            float bc = FLT_MAX;
+            if (cnt > 2) {
+                for (int q = 0; q < 3; ++q) {
+                    if (kq[q] == 0.0f) continue;
+                    float ra[SAH_BINS];
+                    int rc[SAH_BINS];
+                    float l3[3] = {FLT_MAX, FLT_MAX, FLT_MAX}, h3[3] = {-FLT_MAX, -FLT_MAX, -FLT_MAX};
+                    int c = 0;
+                    for (int b = SAH_BINS - 1; b > 0; --b) {
+                        if (S.bcnt[q][b]) {
+                            for (int e = 0; e < 3; ++e) {
+                                l3[e] = fminf(l3[e], ord2f(S.bmin[q][b][e]));
+                                h3[e] = fmaxf(h3[e], ord2f(S.bmax[q][b][e]));
+                            }
+                        }
+                        c += S.bcnt[q][b];
+                        ra[b] = c ? area3(f3(l3[0], l3[1], l3[2]), f3(h3[0], h3[1], h3[2])) : 0.0f;
+                        rc[b] = c;
+                    }
+                    for (int e = 0; e < 3; ++e) { l3[e] = FLT_MAX; h3[e] = -FLT_MAX; }
+                    c = 0;
+                    for (int b = 0; b < SAH_BINS - 1; ++b) {
+                        if (S.bcnt[q][b]) {
+                            for (int e = 0; e < 3; ++e) {
+                                l3[e] = fminf(l3[e], ord2f(S.bmin[q][b][e]));
+                                h3[e] = fmaxf(h3[e], ord2f(S.bmax[q][b][e]));
+                            }
+                        }
+                        c += S.bcnt[q][b];
+                        if (c == 0 || rc[b + 1] == 0) continue;
+                        const float cost = area3(f3(l3[0], l3[1], l3[2]), f3(h3[0], h3[1], h3[2])) * c + ra[b + 1] * rc[b + 1];
+                        if (cost < bc) { bc = cost; ba = q; bb = b; bnl = c; }
+                    }
+                }
+            }
+            S.best_axis = ba;
+            S.best_bin = bb;
+            S.nl = ba >= 0 ? bnl : cnt / 2;                  // no split found: halve the list
+        }
+        __syncthreads();
+        const int ax = S.best_axis, bbin = S.best_bin, nl = S.nl;
+        // stable partition into tmp, then back
+        int lbase = 0, rbase = 0;
+        for (int c0 = begin; c0 < end; c0 += SAH_THREADS) {
+            const int i = c0 + tid;
+            bool left = false;
+            if (i < end) {
+                const int k = S.idx[i];
+                left = ax >= 0 ? sah_bin(0.5f * (S.lo[ax][k] + S.hi[ax][k]), S.nb[6 + ax], kq[ax]) <= bbin
+                               : (i - begin) < nl;
+            }
+            const unsigned bal = __ballot_sync(0xffffffffu, left);
+            if (lane == 0) S.warp_off[wid] = __popc(bal);
+            __syncthreads();
+            if (tid == 0) {
+                int acc = 0;
+                for (int w = 0; w < SAH_THREADS / 32; ++w) { const int x = S.warp_off[w]; S.warp_off[w] = acc; acc += x; }
+                S.warp_off[SAH_THREADS / 32] = acc;
+            }
+            __syncthreads();
+            const int lrank = S.warp_off[wid] + __popc(bal & ((1u << lane) - 1u));
+            const int chunk_l = S.warp_off[SAH_THREADS / 32];
+            if (i < end) {
+                const int pos = left ? begin + lbase + lrank : begin + nl + rbase + (i - c0 - lrank);
+                S.tmp[pos] = S.idx[i];
+            }
+            lbase += chunk_l;
+            rbase += min(SAH_THREADS, end - c0) - chunk_l;
+            __syncthreads();
+        }
+        for (int i = begin + tid; i < end; i += SAH_THREADS) S.idx[i] = S.tmp[i];
+        __syncthreads();
+        if (tid == 0) {
+            const int mid = begin + nl;
+            int code[2];
+            const int rb[2] = {begin, mid}, re[2] = {mid, end};
+            for (int h = 0; h < 2; ++h) {
+                if (re[h] - rb[h] == 1) {
+                    code[h] = ~(a + S.idx[rb[h]]);
+                    B.parent_leaf[a + S.idx[rb[h]]] = node;
+                } else {
+                    code[h] = S.ids[S.next_id++];
+                    B.parent_int[code[h]] = node;
+                    B.range[code[h]] = make_int2(0, re[h] - rb[h] - 1);   // size only (leaf_max 1)
+                    S.stack[S.sp++] = make_int3(rb[h], re[h], code[h]);
+                }
+            }
+            B.left[node] = code[0];
+            B.right[node] = code[1];
+        }
+        __syncthreads();
+    }
+}
+
 // leaf-order records and leaf AABBs (slot k = sorted position k)
 __global__ void k_gather_prims(BuildBuffers B, int n, const uint32_t* __restrict__ order, float4* slo, float4* shi) {
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
@@ -657,8 +891,22 @@ cudaError_t rtb_build_bvh(const BuildBuffers& Bc, cudaStream_t st, int* root, in
     k_karras<<<grid_for(n - 1), 256, 0, st>>>(B.keys[cur], n, B.left, B.right, B.parent_int, B.parent_leaf, B.range);
     cudaMemsetAsync(B.flags, 0, sizeof(int) * (n - 1), st);
     k_refit<<<grid_for(n), 256, 0, st>>>(B, n, slo, shi);
-    // treelet restructuring passes (SAH); leaf collapse by sorted range needs the original
-    // Morton topology, so restructuring runs only without it
+    // SAH subtrees, then treelet restructuring passes (SAH); leaf collapse by sorted range needs
+    // the original Morton topology, so both run only without it
+    if (B.leaf_max == 1 && n > 2 && B.sah_subtrees) {
+        int* roots = B.frontier[0] ? reinterpret_cast<int*>(B.frontier[0]) : nullptr;   // scratch [N] int2
+        int* n_roots = B.wide_counters;
+        cudaMemsetAsync(n_roots, 0, sizeof(int), st);
+        k_sah_roots<<<grid_for(n - 1), 256, 0, st>>>(B, n, roots, n_roots);
+        int h_roots = 0;
+        cudaMemcpyAsync(&h_roots, n_roots, sizeof(int), cudaMemcpyDeviceToHost, st);
+        cudaError_t e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) return e;
+        const size_t smem = sizeof(SahShared);
+        e = cudaFuncSetAttribute(k_sah_subtrees, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        if (h_roots > 0) k_sah_subtrees<<<h_roots, SAH_THREADS, smem, st>>>(B, roots);
+    }
     if (B.leaf_max == 1) {
         for (int pass = 0; pass < B.treelet_passes; ++pass) {
             cudaMemsetAsync(B.flags, 0, sizeof(int) * (n - 1), st);
