@@ -11,8 +11,8 @@
 //                    from common-prefix lengths (__clzll)
 //   k_refit          bottom-up AABB union with atomic arrival counters
 //   k_gather_prims   primitive records in leaf order
-//   k_sah_subtrees   maximal subtrees of <= 4096 primitives rebuilt by binned SAH, one CTA each
-//                    in shared memory (k_sah_roots finds them)
+//   k_sah_subtrees   maximal subtrees of <= 16384 primitives rebuilt by binned SAH, one CTA each
+//                    (k_sah_roots finds them)
 //   k_treelets       SAH treelet restructuring of the BVH2 (Karras & Aila 2013), optional passes
 //   k_wide           BVH2 -> 4-wide BVH collapse (level by level), small subtrees -> leaves
 // The result is a deterministic function of the input arrays.
@@ -530,10 +530,10 @@ __global__ void k_wide(BuildBuffers B, const int2* __restrict__ fin, int n_in, i
 // ---------------------------------------------------------------- SAH subtrees
 // Every maximal LBVH subtree of at most SAH_T primitives (a contiguous Morton range [a, b] of
 // leaf slots) is rebuilt top-down by binned SAH (3 axes x SAH_BINS bins, centroid binning) by one
-// CTA in shared memory; the subtree keeps its root id and reuses its internal node ids, so the
+// CTA (bins in shared memory, item order in global scratch); the subtree keeps its root id and reuses its internal node ids, so the
 // nodes above it are unchanged.  Partitions are stable and the ids are taken in a fixed order:
 // the result is deterministic.  Runs before the treelet passes (parents are rewritten for them).
-constexpr int SAH_T = 4096;
+constexpr int SAH_T = 16384;
 constexpr int SAH_BINS = 32;
 constexpr int SAH_THREADS = 256;
 
@@ -551,10 +551,7 @@ __global__ void k_sah_roots(BuildBuffers B, int n, int* roots, int* n_roots) {
 }
 
 struct SahShared {
-    float lo[3][SAH_T], hi[3][SAH_T];   // item boxes (item k = leaf slot a + k)
-    short idx[SAH_T], tmp[SAH_T];
-    int ids[SAH_T];                     // internal node ids of the subtree, root first
-    int3 stack[SAH_T];                  // (begin, end, node)
+    int3 stack[40];                     // (begin, end, node); the smaller child is taken first
     unsigned int bmin[3][SAH_BINS][3], bmax[3][SAH_BINS][3];
     int bcnt[3][SAH_BINS];
     float red[SAH_THREADS / 32][12];
@@ -566,28 +563,32 @@ __device__ __forceinline__ int sah_bin(float c, float lo, float k) {
     return min(SAH_BINS - 1, max(0, (int)((c - lo) * k)));
 }
 
-__global__ void __launch_bounds__(SAH_THREADS) k_sah_subtrees(BuildBuffers B, const int* __restrict__ roots) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    SahShared& S = *reinterpret_cast<SahShared*>(smem_raw);
+// Item arrays live in global scratch at the subtree's slot range [a, a + m): idx / tmp (item
+// order, permuted by the partitions), ids (the old subtree's internal ids, root first; also the
+// DFS stack that collects them); item boxes are read from the leaf boxes.
+__global__ void __launch_bounds__(SAH_THREADS) k_sah_subtrees(BuildBuffers B, const int* __restrict__ roots,
+                                                              int* gidx, int* gtmp, int* gids, int* gdfs) {
+    __shared__ SahShared S;
     const int root = roots[blockIdx.x];
     const int2 rg = B.range[root];
     const int a = rg.x, m = rg.y - rg.x + 1;
+    int* idx = gidx + a;
+    int* tmp = gtmp + a;
+    int* ids = gids + a;
+    const float4* llo = B.leaf_lo + a;
+    const float4* lhi = B.leaf_hi + a;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    for (int k = tid; k < m; k += SAH_THREADS) {
-        const float4 l = B.leaf_lo[a + k], h = B.leaf_hi[a + k];
-        S.lo[0][k] = l.x; S.lo[1][k] = l.y; S.lo[2][k] = l.z;
-        S.hi[0][k] = h.x; S.hi[1][k] = h.y; S.hi[2][k] = h.z;
-        S.idx[k] = (short)k;
-    }
+    for (int k = tid; k < m; k += SAH_THREADS) idx[k] = k;
     if (tid == 0) {                                      // the old subtree's internal ids, root first
+        int* dfs = gdfs + a;
         int cnt = 0, sp = 0;
-        S.stack[sp++].x = root;
+        dfs[sp++] = root;
         while (sp) {
-            const int v = S.stack[--sp].x;
-            S.ids[cnt++] = v;
+            const int v = dfs[--sp];
+            ids[cnt++] = v;
             const int l = B.left[v], r = B.right[v];
-            if (l >= 0) S.stack[sp++].x = l;
-            if (r >= 0) S.stack[sp++].x = r;
+            if (l >= 0) dfs[sp++] = l;
+            if (r >= 0) dfs[sp++] = r;
         }
         S.sp = 1;
         S.stack[0] = make_int3(0, m, root);
@@ -604,11 +605,13 @@ __global__ void __launch_bounds__(SAH_THREADS) k_sah_subtrees(BuildBuffers B, co
 #pragma unroll
         for (int q = 0; q < 3; ++q) { v[q] = FLT_MAX; v[3 + q] = -FLT_MAX; v[6 + q] = FLT_MAX; v[9 + q] = -FLT_MAX; }
         for (int i = begin + tid; i < end; i += SAH_THREADS) {
-            const int k = S.idx[i];
+            const int k = idx[i];
+            const float4 l4 = llo[k], h4 = lhi[k];
+            const float l[3] = {l4.x, l4.y, l4.z}, h[3] = {h4.x, h4.y, h4.z};
 #pragma unroll
             for (int q = 0; q < 3; ++q) {
-                const float l = S.lo[q][k], h = S.hi[q][k], c = 0.5f * (l + h);
-                v[q] = fminf(v[q], l); v[3 + q] = fmaxf(v[3 + q], h);
+                const float c = 0.5f * (l[q] + h[q]);
+                v[q] = fminf(v[q], l[q]); v[3 + q] = fmaxf(v[3 + q], h[q]);
                 v[6 + q] = fminf(v[6 + q], c); v[9 + q] = fmaxf(v[9 + q], c);
             }
         }
@@ -648,16 +651,18 @@ __global__ void __launch_bounds__(SAH_THREADS) k_sah_subtrees(BuildBuffers B, co
         }
         if (cnt > 2) {
             for (int i = begin + tid; i < end; i += SAH_THREADS) {
-                const int k = S.idx[i];
+                const int k = idx[i];
+                const float4 l4 = llo[k], h4 = lhi[k];
+                const float l[3] = {l4.x, l4.y, l4.z}, h[3] = {h4.x, h4.y, h4.z};
 #pragma unroll
                 for (int q = 0; q < 3; ++q) {
                     if (kq[q] == 0.0f) continue;
-                    const int b = sah_bin(0.5f * (S.lo[q][k] + S.hi[q][k]), S.nb[6 + q], kq[q]);
+                    const int b = sah_bin(0.5f * (l[q] + h[q]), S.nb[6 + q], kq[q]);
                     atomicAdd(&S.bcnt[q][b], 1);
 #pragma unroll
                     for (int e = 0; e < 3; ++e) {
-                        atomicMin(&S.bmin[q][b][e], f2ord(S.lo[e][k]));
-                        atomicMax(&S.bmax[q][b][e], f2ord(S.hi[e][k]));
+                        atomicMin(&S.bmin[q][b][e], f2ord(l[e]));
+                        atomicMax(&S.bmax[q][b][e], f2ord(h[e]));
                     }
                 }
             }
@@ -711,10 +716,16 @@ __global__ void __launch_bounds__(SAH_THREADS) k_sah_subtrees(BuildBuffers B, co
         for (int c0 = begin; c0 < end; c0 += SAH_THREADS) {
             const int i = c0 + tid;
             bool left = false;
+            int k = 0;
             if (i < end) {
-                const int k = S.idx[i];
-                left = ax >= 0 ? sah_bin(0.5f * (S.lo[ax][k] + S.hi[ax][k]), S.nb[6 + ax], kq[ax]) <= bbin
-                               : (i - begin) < nl;
+                k = idx[i];
+                if (ax >= 0) {
+                    const float4 l4 = llo[k], h4 = lhi[k];
+                    const float c = 0.5f * ((ax == 0 ? l4.x : ax == 1 ? l4.y : l4.z) + (ax == 0 ? h4.x : ax == 1 ? h4.y : h4.z));
+                    left = sah_bin(c, S.nb[6 + ax], kq[ax]) <= bbin;
+                } else {
+                    left = (i - begin) < nl;
+                }
             }
             const unsigned bal = __ballot_sync(0xffffffffu, left);
             if (lane == 0) S.warp_off[wid] = __popc(bal);
@@ -729,13 +740,13 @@ __global__ void __launch_bounds__(SAH_THREADS) k_sah_subtrees(BuildBuffers B, co
             const int chunk_l = S.warp_off[SAH_THREADS / 32];
             if (i < end) {
                 const int pos = left ? begin + lbase + lrank : begin + nl + rbase + (i - c0 - lrank);
-                S.tmp[pos] = S.idx[i];
+                tmp[pos] = k;
             }
             lbase += chunk_l;
             rbase += min(SAH_THREADS, end - c0) - chunk_l;
             __syncthreads();
         }
-        for (int i = begin + tid; i < end; i += SAH_THREADS) S.idx[i] = S.tmp[i];
+        for (int i = begin + tid; i < end; i += SAH_THREADS) idx[i] = tmp[i];
         __syncthreads();
         if (tid == 0) {
             const int mid = begin + nl;
@@ -743,15 +754,18 @@ __global__ void __launch_bounds__(SAH_THREADS) k_sah_subtrees(BuildBuffers B, co
             const int rb[2] = {begin, mid}, re[2] = {mid, end};
             for (int h = 0; h < 2; ++h) {
                 if (re[h] - rb[h] == 1) {
-                    code[h] = ~(a + S.idx[rb[h]]);
-                    B.parent_leaf[a + S.idx[rb[h]]] = node;
+                    code[h] = ~(a + idx[rb[h]]);
+                    B.parent_leaf[a + idx[rb[h]]] = node;
                 } else {
-                    code[h] = S.ids[S.next_id++];
+                    code[h] = ids[S.next_id++];
                     B.parent_int[code[h]] = node;
                     B.range[code[h]] = make_int2(0, re[h] - rb[h] - 1);   // size only (leaf_max 1)
-                    S.stack[S.sp++] = make_int3(rb[h], re[h], code[h]);
                 }
             }
+            // larger child pushed first, the smaller taken next: the stack stays O(log m) deep
+            const int big = (re[0] - rb[0]) >= (re[1] - rb[1]) ? 0 : 1;
+            for (int h : {big, 1 - big})
+                if (re[h] - rb[h] > 1) S.stack[S.sp++] = make_int3(rb[h], re[h], code[h]);
             B.left[node] = code[0];
             B.right[node] = code[1];
         }
@@ -902,10 +916,13 @@ cudaError_t rtb_build_bvh(const BuildBuffers& Bc, cudaStream_t st, int* root, in
         cudaMemcpyAsync(&h_roots, n_roots, sizeof(int), cudaMemcpyDeviceToHost, st);
         cudaError_t e = cudaStreamSynchronize(st);
         if (e != cudaSuccess) return e;
-        const size_t smem = sizeof(SahShared);
-        e = cudaFuncSetAttribute(k_sah_subtrees, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        if (h_roots > 0) k_sah_subtrees<<<h_roots, SAH_THREADS, smem, st>>>(B, roots);
+        // scratch: the sort keys / values are free once the leaves are gathered and the
+        // hierarchy built; the DFS stack borrows frontier[1] (N int2, unused until k_wide)
+        if (h_roots > 0)
+            k_sah_subtrees<<<h_roots, SAH_THREADS, 0, st>>>(B, roots, reinterpret_cast<int*>(B.keys[0]),
+                                                           reinterpret_cast<int*>(B.keys[1]),
+                                                           reinterpret_cast<int*>(B.vals[0]),
+                                                           reinterpret_cast<int*>(B.frontier[1]));
     }
     if (B.leaf_max == 1) {
         for (int pass = 0; pass < B.treelet_passes; ++pass) {

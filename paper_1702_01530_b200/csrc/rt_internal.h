@@ -92,7 +92,7 @@ struct BuildBuffers {
     float* cost;                // [N-1] SAH cost of each internal node's subtree (treelets)
     int* count;                 // [N-1] primitives below each internal node (treelets)
     int treelet_passes;         // 0 = plain LBVH
-    int sah_subtrees;           // rebuild LBVH subtrees of <= 4096 primitives by binned SAH
+    int sah_subtrees;           // rebuild LBVH subtrees of <= 16384 primitives by binned SAH
 };
 
 namespace rtb {
