@@ -530,9 +530,11 @@ __global__ void k_wide(BuildBuffers B, const int2* __restrict__ fin, int n_in, i
 // ---------------------------------------------------------------- SAH subtrees
 // Every maximal LBVH subtree of at most SAH_T primitives (a contiguous Morton range [a, b] of
 // leaf slots) is rebuilt top-down by binned SAH (3 axes x SAH_BINS bins, centroid binning) by one
-// CTA (bins in shared memory, item order in global scratch); the subtree keeps its root id and reuses its internal node ids, so the
-// nodes above it are unchanged.  Partitions are stable and the ids are taken in a fixed order:
-// the result is deterministic.  Runs before the treelet passes (parents are rewritten for them).
+// CTA (bins in shared memory, item order in global scratch); the subtree keeps its root id and
+// reuses its internal node ids, so the nodes above it are unchanged.  Partitions are stable and
+// the ids are taken in a fixed order: the result is deterministic.  Runs before the treelet
+// passes (parents are rewritten for them).  C4: node visits 16.2 -> 15.5 per ray, bench +4.3 %,
+// build 45 -> ~210 ms (DESIGN.md §5 v21).
 constexpr int SAH_T = 16384;
 constexpr int SAH_BINS = 32;
 constexpr int SAH_THREADS = 256;
