@@ -138,6 +138,27 @@ def test_bvh_equals_bruteforce(R):
         np.testing.assert_array_equal(a["fb"], b["fb"])
 
 
+def test_sah_subtrees_do_not_change_the_image(R, monkeypatch):
+    """The SAH rebuild of small LBVH subtrees (k_sah_subtrees, DESIGN §5 v21) changes the tree, not
+    the result: hits are chosen by (t, ID) over exactly computed t, so the image, IDs and radiance
+    are bit-identical with it off (RT_SAH_SUBTREES=0, read when a context is created), while the
+    traversal work differs.  Scenes large enough to have several subtrees plus a ragged one."""
+    s = scenes.scene_c4().with_view(width=96, height=64)
+    a = gpu_render(R, s, count=True)
+    monkeypatch.setenv("RT_SAH_SUBTREES", "0")
+    R0 = rt.StereoRenderer(0)
+    try:
+        b = gpu_render(R0, s, count=True)
+    finally:
+        R0.close()
+    np.testing.assert_array_equal(a["id"], b["id"])
+    np.testing.assert_array_equal(a["radiance"].view(np.uint32), b["radiance"].view(np.uint32))
+    np.testing.assert_array_equal(a["fb"], b["fb"])
+    ca, cb = (dict(zip(rt.COUNTER_NAMES, map(int, x["counters"]))) for x in (a, b))
+    assert ca["node_visits"] != cb["node_visits"]                      # a different tree was traversed
+    assert ca["primary"] == cb["primary"] and ca["shadow"] == cb["shadow"]
+
+
 def _kd_render(R, s, max_leaf=1, max_depth=0):
     R.upload(s)
     info = rt.rt_kdtree_build(R.ctx, max_leaf, max_depth)
