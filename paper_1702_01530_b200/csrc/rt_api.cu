@@ -55,6 +55,8 @@ rt_status fail(rt_status s, const char* fmt, ...) {
         }                                                                                        \
     } while (0)
 
+constexpr int RENDER_SLOTS = 16;
+
 struct DevBuf {
     void* p = nullptr;
     size_t bytes = 0;
@@ -80,6 +82,13 @@ struct rt_context {
     int num_sms = 148;
     int* work_counter = nullptr;    // [64]: 16 rotating render queues, 4 ints apart
     unsigned render_seq = 0;
+    // completion event of the last render that used each work-queue slot: a render that reuses a
+    // slot waits for it on the device (cudaStreamWaitEvent), and scene changes wait for all of them
+    cudaEvent_t slot_ev[RENDER_SLOTS] = {};
+    bool slot_used[RENDER_SLOTS] = {};
+    // pinned staging of rt_scene_upload / rt_scene_update_vertices (grow-only)
+    void* staging = nullptr;
+    size_t staging_bytes = 0;
     unsigned long long* scratch_counters = nullptr;
     float* ffma_out = nullptr;
     // scene
@@ -144,6 +153,50 @@ void free_scene(rt_context* c) {
 
 bool finite3(const float* p) { return std::isfinite(p[0]) && std::isfinite(p[1]) && std::isfinite(p[2]); }
 
+// Block until every render enqueued so far (on any stream) has finished: the scene buffers they
+// read may then be freed or rewritten (rt_scene_upload, rt_scene_update_vertices, rt_destroy).
+cudaError_t wait_renders(rt_context* c) {
+    cudaError_t r = cudaSuccess;
+    for (int i = 0; i < RENDER_SLOTS; ++i)
+        if (c->slot_used[i]) {
+            const cudaError_t e = cudaEventSynchronize(c->slot_ev[i]);
+            if (e != cudaSuccess && r == cudaSuccess) r = e;
+            c->slot_used[i] = false;
+        }
+    return r;
+}
+
+// Host arrays -> pinned staging -> device, asynchronously on the context stream (SURVEY §8(b):
+// "copied to pinned staging").  reserve() sizes the staging once per call; the caller
+// synchronises the stream before the staging is reused or the host arrays are released.
+struct Stager {
+    rt_context* c;
+    size_t need = 0, off = 0;
+    explicit Stager(rt_context* ctx) : c(ctx) {}
+    static size_t pad(size_t b) { return (b + 255) & ~size_t(255); }
+    void plan(size_t bytes) { need += pad(bytes); }
+    rt_status reserve() {
+        if (need <= c->staging_bytes) return RT_OK;
+        if (c->staging) cudaFreeHost(c->staging);
+        c->staging = nullptr;
+        c->staging_bytes = 0;
+        const cudaError_t e = cudaHostAlloc(&c->staging, need, cudaHostAllocPortable);
+        if (e != cudaSuccess) {
+            c->staging = nullptr;
+            return fail(RT_ERR_OOM, "pinned staging cudaHostAlloc(%zu): %s", need, cudaGetErrorString(e));
+        }
+        c->staging_bytes = need;
+        return RT_OK;
+    }
+    cudaError_t copy(void* dst, const void* src, size_t bytes) {
+        if (!bytes) return cudaSuccess;
+        char* s = static_cast<char*>(c->staging) + off;
+        memcpy(s, src, bytes);
+        off += pad(bytes);
+        return cudaMemcpyAsync(dst, s, bytes, cudaMemcpyHostToDevice, c->stream);
+    }
+};
+
 }  // namespace
 
 extern "C" {
@@ -177,7 +230,9 @@ rt_status rt_create(int device, void* cuda_stream, rt_context** out) {
     }
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->order_ev, cudaEventDisableTiming);
-    if (e == cudaSuccess) e = cudaMalloc(&c->work_counter, 64 * sizeof(int));
+    for (int i = 0; i < RENDER_SLOTS && e == cudaSuccess; ++i)
+        e = cudaEventCreateWithFlags(&c->slot_ev[i], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaMalloc(&c->work_counter, 4 * RENDER_SLOTS * sizeof(int));
     if (e == cudaSuccess) e = cudaMalloc(&c->scratch_counters, RT_NUM_COUNTERS * sizeof(unsigned long long));
     if (e == cudaSuccess) e = cudaMalloc(&c->ffma_out, 64);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
@@ -192,6 +247,7 @@ rt_status rt_create(int device, void* cuda_stream, rt_context** out) {
 rt_status rt_destroy(rt_context* c) {
     if (!c) return RT_OK;
     cudaSetDevice(c->device);
+    wait_renders(c);
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
     free_scene(c);
@@ -202,6 +258,9 @@ rt_status rt_destroy(rt_context* c) {
     if (c->scratch_counters) cudaFree(c->scratch_counters);
     if (c->ffma_out) cudaFree(c->ffma_out);
     if (c->order_ev) cudaEventDestroy(c->order_ev);
+    for (auto& ev : c->slot_ev)
+        if (ev) cudaEventDestroy(ev);
+    if (c->staging) cudaFreeHost(c->staging);
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
     delete c;
@@ -303,6 +362,7 @@ rt_status rt_scene_upload(rt_context* c, const rt_primitives* P, const rt_materi
     }
 
     CUDA_TRY(cudaSetDevice(c->device));
+    CUDA_TRY(wait_renders(c));                     // renders in flight on any stream still read the scene
     CUDA_TRY(cudaStreamSynchronize(c->stream));
     free_scene(c);
     const auto t0 = std::chrono::steady_clock::now();
@@ -322,38 +382,41 @@ rt_status rt_scene_upload(rt_context* c, const rt_primitives* P, const rt_materi
         free_scene(c);
         return st;
     }
-    if (S) {
-        CUDA_TRY(cudaMemcpy(d_spheres, P->spheres, 16 * (size_t)S, cudaMemcpyHostToDevice));
-        CUDA_TRY(cudaMemcpy(d_smat, P->sphere_mat, 4 * (size_t)S, cudaMemcpyHostToDevice));
+    // host-side records (planes normalised, materials / lights as float4 rows)
+    std::vector<int> pm(PL);
+    for (uint32_t i = 0; i < PL; ++i) pm[i] = (int)P->plane_mat[i];
+    std::vector<float4> m(3 * (size_t)n_mats);
+    for (uint32_t i = 0; i < n_mats; ++i) {
+        const rt_material& x = mats[i];
+        m[3 * i] = make_float4(x.kd[0], x.kd[1], x.kd[2], x.shininess);
+        m[3 * i + 1] = make_float4(x.ks[0], x.ks[1], x.ks[2], x.kr);
+        m[3 * i + 2] = make_float4(x.kt, x.ior, 0.f, 0.f);
     }
-    if (T) {
-        CUDA_TRY(cudaMemcpy(d_vertices, P->vertices, 12 * (size_t)V, cudaMemcpyHostToDevice));
-        CUDA_TRY(cudaMemcpy(d_tri, P->tri_indices, 12 * (size_t)T, cudaMemcpyHostToDevice));
-        CUDA_TRY(cudaMemcpy(d_trimat, P->tri_mat, 4 * (size_t)T, cudaMemcpyHostToDevice));
+    std::vector<float4> l(2 * (size_t)n_lights);
+    for (uint32_t i = 0; i < n_lights; ++i) {
+        l[2 * i] = make_float4(lights[i].pos[0], lights[i].pos[1], lights[i].pos[2], 0.f);
+        l[2 * i + 1] = make_float4(lights[i].intensity[0], lights[i].intensity[1], lights[i].intensity[2], 0.f);
     }
-    if (PL) {
-        std::vector<int> pm(PL);
-        for (uint32_t i = 0; i < PL; ++i) pm[i] = (int)P->plane_mat[i];
-        CUDA_TRY(cudaMemcpy(d_planes, planes.data(), 16 * (size_t)PL, cudaMemcpyHostToDevice));
-        CUDA_TRY(cudaMemcpy(d_pmat, pm.data(), 4 * (size_t)PL, cudaMemcpyHostToDevice));
-    }
-    if (n_mats) {
-        std::vector<float4> m(3 * (size_t)n_mats);
-        for (uint32_t i = 0; i < n_mats; ++i) {
-            const rt_material& x = mats[i];
-            m[3 * i] = make_float4(x.kd[0], x.kd[1], x.kd[2], x.shininess);
-            m[3 * i + 1] = make_float4(x.ks[0], x.ks[1], x.ks[2], x.kr);
-            m[3 * i + 2] = make_float4(x.kt, x.ior, 0.f, 0.f);
+    // every array through the pinned staging buffer, DMA'd on the context stream; the build
+    // below runs on the same stream, and the stream is synchronised before returning
+    {
+        Stager sg(c);
+        const size_t sz[9] = {16 * (size_t)S, 4 * (size_t)S, T ? 12 * (size_t)V : 0, 12 * (size_t)T, 4 * (size_t)T,
+                              16 * (size_t)PL, 4 * (size_t)PL, m.size() * sizeof(float4), l.size() * sizeof(float4)};
+        for (size_t b : sz) sg.plan(b);
+        if ((st = sg.reserve())) {
+            free_scene(c);
+            return st;
         }
-        CUDA_TRY(cudaMemcpy(d_mats, m.data(), m.size() * sizeof(float4), cudaMemcpyHostToDevice));
-    }
-    if (n_lights) {
-        std::vector<float4> l(2 * (size_t)n_lights);
-        for (uint32_t i = 0; i < n_lights; ++i) {
-            l[2 * i] = make_float4(lights[i].pos[0], lights[i].pos[1], lights[i].pos[2], 0.f);
-            l[2 * i + 1] = make_float4(lights[i].intensity[0], lights[i].intensity[1], lights[i].intensity[2], 0.f);
-        }
-        CUDA_TRY(cudaMemcpy(d_lights, l.data(), l.size() * sizeof(float4), cudaMemcpyHostToDevice));
+        CUDA_TRY(sg.copy(d_spheres, P->spheres, sz[0]));
+        CUDA_TRY(sg.copy(d_smat, P->sphere_mat, sz[1]));
+        CUDA_TRY(sg.copy(d_vertices, P->vertices, sz[2]));
+        CUDA_TRY(sg.copy(d_tri, P->tri_indices, sz[3]));
+        CUDA_TRY(sg.copy(d_trimat, P->tri_mat, sz[4]));
+        CUDA_TRY(sg.copy(d_planes, planes.data(), sz[5]));
+        CUDA_TRY(sg.copy(d_pmat, pm.data(), sz[6]));
+        CUDA_TRY(sg.copy(d_mats, m.data(), sz[7]));
+        CUDA_TRY(sg.copy(d_lights, l.data(), sz[8]));
     }
     // ---- LBVH build buffers
     BuildBuffers B{};
@@ -437,14 +500,17 @@ rt_status rt_scene_upload(rt_context* c, const rt_primitives* P, const rt_materi
                 free_scene(c);
                 return st;
             }
-            e = cudaMemcpy(d_nodes, B.nodes4, 16 * rtb::NODE_F4 * (size_t)n_nodes4, cudaMemcpyDeviceToDevice);
+            e = cudaMemcpyAsync(d_nodes, B.nodes4, 16 * rtb::NODE_F4 * (size_t)n_nodes4, cudaMemcpyDeviceToDevice,
+                                c->stream);
         }
+        if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);   // staging and build scratch free again
         free_scratch();
         if (e != cudaSuccess) {
             free_scene(c);
             return fail(RT_ERR_CUDA, "LBVH build: %s", cudaGetErrorString(e));
         }
     }
+    CUDA_TRY(cudaStreamSynchronize(c->stream));       // the staged copies have landed (N == 0 case)
     const auto t1 = std::chrono::steady_clock::now();
 
     rtb::DevScene& D = c->sc;
@@ -522,7 +588,15 @@ rt_status rt_scene_update_vertices(rt_context* c, const float* vertices, uint32_
         if (!(area > 1e-12 * diag2)) return fail(RT_ERR_INVALID_ARG, "triangle %zu: degenerate after update", j);
     }
     CUDA_TRY(cudaSetDevice(c->device));
-    CUDA_TRY(cudaMemcpyAsync(c->d_vertices, vertices, 12 * (size_t)n_vertices, cudaMemcpyHostToDevice, c->stream));
+    CUDA_TRY(wait_renders(c));                     // renders in flight read the nodes the refit rewrites
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    {
+        Stager sg(c);
+        sg.plan(12 * (size_t)n_vertices);
+        rt_status st;
+        if ((st = sg.reserve())) return st;
+        CUDA_TRY(sg.copy(c->d_vertices, vertices, 12 * (size_t)n_vertices));
+    }
     CUDA_TRY(rtb_refit_bvh(const_cast<float4*>(c->sc.prims), const_cast<float4*>(c->sc.nodes), c->d_prim_orig,
                            c->sc.n_bvh, c->sc.n_spheres, c->d_spheres, c->d_tri, c->d_vertices, c->level_start.data(),
                            (int)c->level_start.size() - 1, c->stream));
@@ -666,9 +740,11 @@ rt_status render_impl(rt_context* c, const rt_render_params* p, const rt_outputs
     P.W = (int)W;
     P.H = (int)H;
     P.max_depth = (int)p->max_depth;
-    // a work counter per render in flight (16 slots, rotated): renders enqueued on different
-    // streams may run concurrently and must not share a queue
-    P.work_counter = c->work_counter + 4 * (c->render_seq++ % 16);
+    // a work counter per render in flight (RENDER_SLOTS slots, rotated): renders enqueued on
+    // different streams may run concurrently and must not share a queue; a render that reuses a
+    // slot waits on the device for the slot's previous render (launch below)
+    const int slot = (int)(c->render_seq % RENDER_SLOTS);
+    P.work_counter = c->work_counter + 4 * slot;
     const ShardGeom g = shard_geom(W, H, p->shard_world);
     const uint64_t n_tiles = shard_count(g, p->shard_rank, p->shard_world);
     if (n_tiles * 256ull >= (1ull << 31)) return fail(RT_ERR_SIZE, "too many pixels in one shard");
@@ -710,8 +786,12 @@ rt_status render_impl(rt_context* c, const rt_render_params* p, const rt_outputs
     const long long max_blocks = ((long long)P.n_work + block - 1) / block;
     int grid = (int)std::min<long long>((long long)c->num_sms * occ, std::max<long long>(1, max_blocks));
     if (c->grid_limit > 0) grid = std::min(grid, c->grid_limit);   // experiment knob (paper's "network size")
+    if (c->slot_used[slot]) CUDA_TRY(cudaStreamWaitEvent(stream, c->slot_ev[slot], 0));
     CUDA_TRY(cudaMemsetAsync(P.work_counter, 0, sizeof(int), stream));
     CUDA_TRY(rtb_launch_trace(P, kflags, grid, stream));
+    CUDA_TRY(cudaEventRecord(c->slot_ev[slot], stream));
+    c->slot_used[slot] = true;
+    ++c->render_seq;
     return RT_OK;
 }
 }  // namespace
@@ -978,13 +1058,16 @@ rt_status rt_kdtree_build(rt_context* c, uint32_t max_leaf, uint32_t max_depth, 
     if (max_depth > 60) return fail(RT_ERR_INVALID_ARG, "rt_kdtree_build: max_depth %u > 60", max_depth);
     if (!c->has_scene) return fail(RT_ERR_NO_SCENE, "rt_kdtree_build: no scene");
     CUDA_TRY(cudaSetDevice(c->device));
+    CUDA_TRY(wait_renders(c));                     // kd renders in flight read the buffers replaced below
     CUDA_TRY(cudaStreamSynchronize(c->stream));
     const int n = c->sc.n_bvh;
     const auto t0 = std::chrono::steady_clock::now();
     rtb::KdHost K;
     if (n > 0) {
         std::vector<float4> prims(3 * (size_t)n);
-        CUDA_TRY(cudaMemcpy(prims.data(), c->sc.prims, prims.size() * sizeof(float4), cudaMemcpyDeviceToHost));
+        CUDA_TRY(cudaMemcpyAsync(prims.data(), c->sc.prims, prims.size() * sizeof(float4), cudaMemcpyDeviceToHost,
+                                 c->stream));
+        CUDA_TRY(cudaStreamSynchronize(c->stream));
         rtb::kd_build_host(prims.data(), n, c->sc.n_spheres, (int)max_leaf, (int)max_depth, K);
     }
     const double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
@@ -1005,8 +1088,10 @@ rt_status rt_kdtree_build(rt_context* c, uint32_t max_leaf, uint32_t max_depth, 
         }
         c->kd_nodes_buf = a;
         c->kd_refs_buf = b;
-        CUDA_TRY(cudaMemcpy(a.p, K.nodes.data(), a.bytes, cudaMemcpyHostToDevice));
-        if (!K.refs.empty()) CUDA_TRY(cudaMemcpy(b.p, K.refs.data(), K.refs.size() * sizeof(int), cudaMemcpyHostToDevice));
+        CUDA_TRY(cudaMemcpyAsync(a.p, K.nodes.data(), a.bytes, cudaMemcpyHostToDevice, c->stream));
+        if (!K.refs.empty())
+            CUDA_TRY(cudaMemcpyAsync(b.p, K.refs.data(), K.refs.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+        CUDA_TRY(cudaStreamSynchronize(c->stream));       // pageable sources: complete before they go away
         c->sc.kd_nodes = static_cast<const int2*>(a.p);
         c->sc.kd_refs = static_cast<const int*>(b.p);
         c->sc.kd_lo = make_float3(K.lo[0], K.lo[1], K.lo[2]);

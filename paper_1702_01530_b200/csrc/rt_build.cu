@@ -552,14 +552,21 @@ __global__ void k_sah_roots(BuildBuffers B, int n, int* roots, int* n_roots) {
     }
 }
 
+// BVH2 depth budget of the SAH rebuild: a binned SAH split can peel off one primitive per level,
+// so below (budget - ceil(log2 count)) levels a task is split at the median instead; the BVH2 (and
+// therefore the BVH4 and its traversal stack, STACK_CAP) stays within SAH_MAX_DEPTH levels.
+constexpr int SAH_MAX_DEPTH = 60;
+
 struct SahShared {
-    int3 stack[40];                     // (begin, end, node); the smaller child is taken first
+    int4 stack[40];                     // (begin, end, node, depth); the smaller child is taken first
     unsigned int bmin[3][SAH_BINS][3], bmax[3][SAH_BINS][3];
     int bcnt[3][SAH_BINS];
     float red[SAH_THREADS / 32][12];
     float nb[12];
     int sp, next_id, best_axis, best_bin, nl, warp_off[SAH_THREADS / 32 + 1];
 };
+
+__device__ __forceinline__ int ceil_log2(int n) { return n <= 1 ? 0 : 32 - __clz(n - 1); }
 
 __device__ __forceinline__ int sah_bin(float c, float lo, float k) {
     return min(SAH_BINS - 1, max(0, (int)((c - lo) * k)));
@@ -592,16 +599,20 @@ __global__ void __launch_bounds__(SAH_THREADS) k_sah_subtrees(BuildBuffers B, co
             if (l >= 0) dfs[sp++] = l;
             if (r >= 0) dfs[sp++] = r;
         }
+        int d0 = 0;                                      // depth of the subtree root in the BVH2
+        for (int v = B.parent_int[root]; v >= 0; v = B.parent_int[v]) ++d0;
         S.sp = 1;
-        S.stack[0] = make_int3(0, m, root);
+        S.stack[0] = make_int4(0, m, root, d0);
         S.next_id = 1;
     }
     __syncthreads();
     while (S.sp > 0) {
-        const int3 t = S.stack[S.sp - 1];
+        const int4 t = S.stack[S.sp - 1];
         __syncthreads();
         if (tid == 0) --S.sp;
-        const int begin = t.x, end = t.y, node = t.z, cnt = end - begin;
+        const int begin = t.x, end = t.y, node = t.z, cnt = end - begin, depth = t.w;
+        // depth budget reached: median split (balanced below this node)
+        const bool median = depth + ceil_log2(cnt) >= SAH_MAX_DEPTH;
         // node box and centroid bounds
         float v[12];
 #pragma unroll
@@ -651,7 +662,7 @@ __global__ void __launch_bounds__(SAH_THREADS) k_sah_subtrees(BuildBuffers B, co
             const float ext = S.nb[9 + q] - S.nb[6 + q];
             kq[q] = ext > 0.0f ? SAH_BINS * (1.0f - 1e-6f) / ext : 0.0f;
         }
-        if (cnt > 2) {
+        if (cnt > 2 && !median) {
             for (int i = begin + tid; i < end; i += SAH_THREADS) {
                 const int k = idx[i];
                 const float4 l4 = llo[k], h4 = lhi[k];
@@ -673,7 +684,7 @@ __global__ void __launch_bounds__(SAH_THREADS) k_sah_subtrees(BuildBuffers B, co
         if (tid == 0) {
             int ba = -1, bb = 0, bnl = 0;
             float bc = FLT_MAX;
-            if (cnt > 2) {
+            if (cnt > 2 && !median) {
                 for (int q = 0; q < 3; ++q) {
                     if (kq[q] == 0.0f) continue;
                     float ra[SAH_BINS];
@@ -767,7 +778,7 @@ __global__ void __launch_bounds__(SAH_THREADS) k_sah_subtrees(BuildBuffers B, co
             // larger child pushed first, the smaller taken next: the stack stays O(log m) deep
             const int big = (re[0] - rb[0]) >= (re[1] - rb[1]) ? 0 : 1;
             for (int h : {big, 1 - big})
-                if (re[h] - rb[h] > 1) S.stack[S.sp++] = make_int3(rb[h], re[h], code[h]);
+                if (re[h] - rb[h] > 1) S.stack[S.sp++] = make_int4(rb[h], re[h], code[h], depth + 1);
             B.left[node] = code[0];
             B.right[node] = code[1];
         }

@@ -85,3 +85,60 @@ def test_download_after_stream(R):
         assert np.array_equal(got, fb.cpu().numpy().reshape(-1))
     finally:
         rt.rt_host_free(host)
+
+
+def test_more_renders_in_flight_than_work_queues(R):
+    """40 renders on 3 streams with no host synchronisation between them: more than the
+    library's 16 work-queue slots, so slots are reused while an earlier render on another stream
+    may still drain its queue.  The reuse waits for that render on the device (per-slot
+    completion events), so every frame equals the same frame rendered alone."""
+    s = scenes.scene_c2().with_view(width=96, height=64, max_depth=3)
+    R.upload(s)
+    rigs = [scenes.c5_rig(k) for k in range(5)]
+    ref = []
+    for rg in rigs:
+        R.set_camera(rg)
+        ref.append(R.render(s.width, s.height, s.max_depth)["fb"].clone())
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream() for _ in range(3)]
+    fbs = [R.alloc_fb(s.width, s.height) for _ in range(40)]
+    for f in fbs:
+        f.zero_()
+    torch.cuda.synchronize()
+    for k in range(40):
+        R.set_camera(rigs[k % len(rigs)])
+        R.render(s.width, s.height, s.max_depth, fb=fbs[k], stream=streams[k % 3])
+    torch.cuda.synchronize()
+    for k in range(40):
+        assert torch.equal(fbs[k], ref[k % len(rigs)]), f"render {k} (slot {k % 16}) differs"
+
+
+def test_scene_change_waits_for_renders_in_flight(R):
+    """rt_scene_upload / rt_scene_update_vertices free or rewrite buffers that renders still in
+    flight on other streams read: they wait for those renders first, so frames enqueued before
+    the change show the old scene, bit for bit."""
+    a = scenes.scene_c3().with_view(width=160, height=96)
+    b = scenes.paper_scene(5).with_view(width=160, height=96)
+    R.upload(a)
+    R.set_camera(a.rig)
+    ref_a = R.render(a.width, a.height, a.max_depth)["fb"].clone()
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream() for _ in range(4)]
+    fbs = [R.alloc_fb(a.width, a.height) for _ in range(8)]
+    torch.cuda.synchronize()
+    for k in range(8):
+        R.render(a.width, a.height, a.max_depth, fb=fbs[k], stream=streams[k % 4])
+    R.upload(b)                                   # no host sync before the new scene replaces a
+    torch.cuda.synchronize()
+    for k in range(8):
+        assert torch.equal(fbs[k], ref_a), f"frame {k} saw the replaced scene"
+    # refit while renders are in flight: the earlier frames keep the unmoved geometry
+    R.upload(a)
+    R.set_camera(a.rig)
+    torch.cuda.synchronize()
+    for k in range(8):
+        R.render(a.width, a.height, a.max_depth, fb=fbs[k], stream=streams[k % 4])
+    rt.rt_scene_update_vertices(R.ctx, a.vertices * 1.05)
+    torch.cuda.synchronize()
+    for k in range(8):
+        assert torch.equal(fbs[k], ref_a), f"frame {k} saw the refit"
