@@ -39,7 +39,9 @@ from paper_1702_01530_b200 import scenes  # noqa: E402
 METRIC = "Mrays/s and stereo frames/s at 1/2/4/8 B200; % FP32 roofline"
 UNIT = "Mrays/s"
 # Algorithmic FP32 flops per counted unit (frozen; FMA = 2).
-FLOPS_PER = {"primary": 20, "ray_setup": 3, "node_visits": 48, "tri_tests": 44, "sphere_tests": 18,
+# The slab test is counted per REAL child box tested (box_tests, instrumented build), not as 4 per
+# BVH4 node visit: empty child slots hold inverted boxes that the layout tests for free.
+FLOPS_PER = {"primary": 20, "ray_setup": 3, "box_tests": 12, "tri_tests": 44, "sphere_tests": 18,
              "plane_tests": 12, "shade_hits": 20, "light_evals": 67, "reflection": 16, "refraction": 24,
              "misses": 6, "pixels": 9}
 FP32_LANES_PER_SM = 128      # B200 SM: 4 SMSPs x 32 FP32 lanes
@@ -400,17 +402,23 @@ def run_ours(args, scene):
     # ---- end-to-end through the public C ABI with host buffers (camera in, frame out)
     e2e = run_e2e(args, R, scene, rank, world, frames, fbs, streams, hb, dev, rays_total) if not args.no_e2e else None
 
-    # ---- FFMA peak measured live (context for the roofline denominator)
+    # ---- machine ceilings measured live (B0): FFMA / FFMA2 / FMNMX rates and the
+    # L1 / shared-memory bandwidth per SM per clock (rt_bench_ceilings), and the FFMA peak
     ffma_tflops, _ = rt.rt_bench_ffma(R.ctx, 2048)
+    ceil = rt.rt_bench_ceilings(R.ctx)
 
     if rank == 0:
         value = rays_total / (ms_per_step * 1e-3) / 1e6
         sm_max = clocks.get("sm_max_mhz") or 1965.0
         peak = 148 * FP32_LANES_PER_SM * 2 * sm_max * 1e6 / 1e12
-        # sustained rate of the timed region (frames overlap, so a launch's own duration is the
-        # isolated one, reported beside it)
-        achieved = my_flops / (ms_per_step * 1e-3) / 1e12
+        # the dominant kernel's own duration: the event-timed trace launch of the one-frame-at-a-time
+        # loop (L2 flushed before it); the in-flight loop overlaps 4 launches, so its per-frame time
+        # is a throughput, not a launch duration, and is reported separately
+        kernel_ms = float(t[1])
+        achieved = my_flops / (kernel_ms * 1e-3) / 1e12
+        achieved_inflight = my_flops / (ms_per_step * 1e-3) / 1e12
         traffic = load_traffic(scene.name, world)
+        prof = load_profile(scene.name, world)
         par = f"tile-sharded x{world}" + {"single": "", "peer": " + fused peer-store gather to rank 0 (CUDA IPC over NVLink)",
                                           "nccl": " + NCCL gather to rank 0 + unpack"}[frame.mode]
         line = {
@@ -427,17 +435,31 @@ def run_ours(args, scene):
                               else f"flushed ({flush_bytes >> 20} MiB write) between timed steps")
                              + f"; scene+BVH {info['device_bytes'] / 1e6:.0f} MB"},
             "stereo_fps": 1e3 / ms_per_step,
+            "value_definitions": {
+                "value": "whole-job throughput: rays of K frames / device time of the K frames with 4 frames in "
+                         "flight (L2 flushed before each, inside the timed region)",
+                "frame_latency.mrays_s_median": "SURVEY §8(d) Mrays/s: rays per frame / median time of one frame "
+                                                "rendered alone (L2 flushed before it, untimed)"},
             "frame_latency": {"ms_mean": lat_total_ms / args.steps, "ms_median": med_ms, "ms_best": best_ms,
                               "mrays_s": rays_total / (lat_total_ms / args.steps * 1e-3) / 1e6,
+                              "mrays_s_median": rays_total / (med_ms * 1e-3) / 1e6,
+                              "stereo_fps_median": 1e3 / med_ms,
                               "note": "one frame at a time, L2 flushed before each (untimed)"},
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "k_trace_stereo", "kernel_ms": ms_per_step,
-                         "kernel_ms_isolated": float(t[1]),
-                         "kernel_share_of_step": float(t[1]) / (lat_total_ms / args.steps),
+                         "kernel": "k_trace_stereo", "kernel_ms": kernel_ms,
+                         "kernel_ms_basis": "mean event-timed duration of the trace launch, one frame at a time",
+                         "kernel_share_of_step": kernel_ms / (lat_total_ms / args.steps),
                          "algorithmic_flops_per_launch": my_flops,
+                         "flops_basis": "SURVEY §8(d) frozen per-unit flops x this launch's instrumented counts "
+                                        "(box_tests = real child boxes tested)",
+                         "inflight": {"ms_per_frame": ms_per_step, "achieved": achieved_inflight,
+                                      "frac": achieved_inflight / peak,
+                                      "note": "4 launches overlap: per-frame throughput time, not a launch duration"},
                          "peak_basis": f"148 SM x 128 FP32 lanes x 2 x {sm_max:.0f} MHz (sm_max; B200_PROFILING "
-                                       f"unit counts); live FFMA microbenchmark {ffma_tflops:.1f} TFLOP/s"},
+                                       f"unit counts); live FFMA microbenchmark {ffma_tflops:.1f} TFLOP/s",
+                         "ceilings_b0": ceil,
+                         **l1_roofline(prof, ceil, kernel_ms, sm_max)},
             "clocks": clocks,
             "gpu_launches": args.steps * frame.launches_per_frame,   # in the throughput region
             "paper_context": {"hardware": "'a video graphics card NVIDIA', model unstated (PAPER.md:66)",
@@ -612,6 +634,30 @@ def run_e2e(args, R, scene, rank, world, frames, fbs, streams, hb, dev, rays_tot
                     "launch parameters), render, pinned async D2H (rt_download_after, copy stream) of the RGBA8 "
                     "stereo frame overlapped with the frames still rendering; host wall clock around K steps incl. "
                     "the last download"}
+
+
+def load_profile(name, world):
+    """ncu counters of one trace launch (profiles/trace_profile.json, written by scripts/ncu_summary.py
+    from the committed --set full capture): dram / L1 bytes, pipe utilisation, launch duration."""
+    p = os.path.join(ROOT, "profiles", "trace_profile.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get(f"{name}/x{world}", d.get(name))
+    except (OSError, ValueError):
+        return None
+
+
+def l1_roofline(prof, ceil, kernel_ms, sm_mhz):
+    """Second ceiling: the trace kernel's L1 bytes per launch (ncu l1tex__t_bytes of
+    the committed capture) over its live-timed duration, against 148 SMs x the B0-measured L1 bytes
+    per clock x the SM clock."""
+    if not prof or not prof.get("l1tex_t_bytes") or not ceil.get("l1_bytes_clk_sm"):
+        return {"l1": None}
+    peak = 148 * ceil["l1_bytes_clk_sm"] * sm_mhz * 1e6 / 1e9
+    ach = prof["l1tex_t_bytes"] / (kernel_ms * 1e-3) / 1e9
+    return {"l1": {"achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                   "bytes_per_launch": prof["l1tex_t_bytes"], "source": prof.get("source")}}
 
 
 def load_traffic(name, world):

@@ -38,7 +38,7 @@ extern "C" {
 #define RT_ABI_VERSION 1
 #define RT_MAX_DEPTH 16          /* max_depth limit (stack sizing)                 */
 #define RT_TILE 16               /* shard tile edge in pixels (16x16 tiles)        */
-#define RT_NUM_COUNTERS 12       /* see rt_counter                                  */
+#define RT_NUM_COUNTERS 13       /* see rt_counter                                  */
 
 typedef enum rt_status {
     RT_OK = 0,
@@ -99,12 +99,13 @@ typedef struct rt_fb {
 /* Counter slots of rt_outputs.counters (uint64, accumulated, never reset by the library). */
 typedef enum rt_counter {
     RT_CNT_PRIMARY = 0, RT_CNT_REFLECTION = 1, RT_CNT_REFRACTION = 2, RT_CNT_SHADOW = 3,
-    RT_CNT_NODE_VISITS = 4,      /* BVH4 nodes visited (4 box tests each)             */
+    RT_CNT_NODE_VISITS = 4,      /* BVH4 nodes visited                                */
     RT_CNT_TRI_TESTS = 5, RT_CNT_SPHERE_TESTS = 6, RT_CNT_PLANE_TESTS = 7,
     RT_CNT_SHADE_HITS = 8,       /* nearest-hit shading points                        */
     RT_CNT_LIGHT_EVALS = 9,      /* (hit, light) pairs evaluated                      */
     RT_CNT_MISSES = 10,          /* tree rays that hit nothing                        */
-    RT_CNT_PIXELS = 11
+    RT_CNT_PIXELS = 11,
+    RT_CNT_BOX_TESTS = 12        /* child-box slab tests of real (non-empty) children  */
 } rt_counter;
 
 /* rt_render_params.flags */
@@ -310,6 +311,24 @@ rt_status rt_kdtree_build(rt_context* ctx, uint32_t max_leaf, uint32_t max_depth
 /* FFMA throughput microbenchmark (roofline denominator): runs `iters` FMA chains on every
  * SM and returns achieved FP32 TFLOP/s and the kernel time in ms. */
 rt_status rt_bench_ffma(rt_context* ctx, uint32_t iters, double* tflops, double* ms);
+/* B0 machine ceilings (the FP32 roofline denominator and the second ceiling,
+ * L1/shared-memory bandwidth, "verify in B0").  One 1024-thread CTA per SM times its own body
+ * with the SM cycle counter, so out[0..5] are per SM per clock (median over SMs), independent of
+ * the clock the run sees; out[6] is the SM clock seen (MHz).  Synchronous on the context stream.
+ *   [RT_CEIL_FFMA_FLOP_CLK]   FP32 flops/clk/SM of 3-register FFMA chains (FMA = 2 flops)
+ *   [RT_CEIL_FFMA2_FLOP_CLK]  flops/clk/SM of packed FFMA2 chains (4 flops per instruction lane)
+ *   [RT_CEIL_FMNMX_CLK]       2-input FP32 max thread-operations/clk/SM (ALU pipe)
+ *   [RT_CEIL_FMNMX3_CLK]      3-input FP32 max thread-operations/clk/SM (ALU pipe)
+ *   [RT_CEIL_L1_BYTES_CLK]    bytes/clk/SM of 128-bit global loads that hit L1
+ *   [RT_CEIL_SMEM_BYTES_CLK]  bytes/clk/SM of conflict-free 128-bit shared loads
+ *   [RT_CEIL_SM_MHZ]          SM clock during the FFMA probe
+ * Errors: RT_ERR_INVALID_ARG, RT_ERR_CUDA. */
+#define RT_NUM_CEILINGS 7
+enum {
+    RT_CEIL_FFMA_FLOP_CLK = 0, RT_CEIL_FFMA2_FLOP_CLK = 1, RT_CEIL_FMNMX_CLK = 2, RT_CEIL_FMNMX3_CLK = 3,
+    RT_CEIL_L1_BYTES_CLK = 4, RT_CEIL_SMEM_BYTES_CLK = 5, RT_CEIL_SM_MHZ = 6
+};
+rt_status rt_bench_ceilings(rt_context* ctx, double out[RT_NUM_CEILINGS]);
 
 #ifdef __cplusplus
 }

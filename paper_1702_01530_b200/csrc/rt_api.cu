@@ -1121,40 +1121,6 @@ rt_status rt_bvh_export(rt_context* c, float* nodes, uint32_t* n_nodes, int32_t*
     const uint32_t nn = (uint32_t)c->info[4], np = (uint32_t)c->sc.n_bvh;
     CUDA_TRY(cudaSetDevice(c->device));
     CUDA_TRY(cudaStreamSynchronize(c->stream));
-#if RT_NODE_F16
-    if (nodes && nn) {
-        // compressed nodes: decode to the 7 x float4 layout, rounding outward like the device decode
-        std::vector<float4> raw((size_t)nn * rtb::NODE_F4);
-        CUDA_TRY(cudaMemcpy(raw.data(), c->sc.nodes, raw.size() * sizeof(float4), cudaMemcpyDeviceToHost));
-        for (uint32_t i = 0; i < nn; ++i) {
-            const float4* q = &raw[(size_t)i * rtb::NODE_F4];
-            float* o = nodes + (size_t)i * 4 * rtb::NODE_DATA_F4;
-            uint32_t sw;
-            memcpy(&sw, &q[0].w, 4);
-            const double S = (double)__half2float(__ushort_as_half((unsigned short)(sw & 0xFFFFu)));
-            const float O[3] = {q[0].x, q[0].y, q[0].z};
-            int codes[4];
-            memcpy(codes, &q[1], 16);
-            for (int a = 0; a < 3; ++a) {
-                uint32_t w[4];
-                memcpy(w, &q[2 + a], 16);
-                for (int ch = 0; ch < 4; ++ch) {
-                    if (codes[ch] == rtb::WIDE_EMPTY) { o[(2 * a) * 4 + ch] = 1e30f; o[(2 * a + 1) * 4 + ch] = -1e30f; continue; }
-                    const uint32_t wl = w[ch >> 1], wh = w[2 + (ch >> 1)];
-                    const double hl = __half2float(__ushort_as_half((unsigned short)((ch & 1) ? wl >> 16 : wl & 0xFFFFu)));
-                    const double hh = __half2float(__ushort_as_half((unsigned short)((ch & 1) ? wh >> 16 : wh & 0xFFFFu)));
-                    const double lo = O[a] + hl * S, hi = O[a] + hh * S;
-                    float fl = (float)lo, fh = (float)hi;
-                    if ((double)fl > lo) fl = nextafterf(fl, -INFINITY);
-                    if ((double)fh < hi) fh = nextafterf(fh, INFINITY);
-                    o[(2 * a) * 4 + ch] = fl;
-                    o[(2 * a + 1) * 4 + ch] = fh;
-                }
-            }
-            memcpy(o + 24, codes, 16);
-        }
-    }
-#else
     if (nodes && nn) {
         CUDA_TRY(cudaMemcpy2D(nodes, 16 * rtb::NODE_DATA_F4, c->sc.nodes, 16 * rtb::NODE_F4, 16 * rtb::NODE_DATA_F4, nn,
                               cudaMemcpyDeviceToHost));
@@ -1169,7 +1135,6 @@ rt_status rt_bvh_export(rt_context* c, float* nodes, uint32_t* n_nodes, int32_t*
             }
         }
     }
-#endif
     if (prim_gid && np) {
         std::vector<float4> p(3 * (size_t)np);
         CUDA_TRY(cudaMemcpy(p.data(), c->sc.prims, p.size() * sizeof(float4), cudaMemcpyDeviceToHost));
@@ -1203,6 +1168,14 @@ rt_status rt_bench_ffma(rt_context* c, uint32_t iters, double* tflops, double* m
     const double flops = 2.0 * 8 * 16 * (double)iters * grid * 256;
     *ms = t;
     *tflops = flops / (t * 1e-3) / 1e12;
+    return RT_OK;
+}
+
+rt_status rt_bench_ceilings(rt_context* c, double out[RT_NUM_CEILINGS]) {
+    if (!c || !out) return fail(RT_ERR_INVALID_ARG, "rt_bench_ceilings: NULL argument");
+    CUDA_TRY(cudaSetDevice(c->device));
+    for (int i = 0; i < RT_NUM_CEILINGS; ++i) out[i] = 0.0;
+    CUDA_TRY(rtb_probe_ceilings(c->num_sms, c->stream, out));
     return RT_OK;
 }
 

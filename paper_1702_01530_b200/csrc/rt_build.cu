@@ -943,22 +943,6 @@ cudaError_t rtb_build_bvh(const BuildBuffers& Bc, cudaStream_t st, int* root, in
             k_treelets<<<grid_for(n), 256, 0, st>>>(B, n);
         }
     }
-    // experiment: replace the LBVH topology by a host binned-SAH BVH2 over the same leaves
-    if (B.leaf_max == 1 && getenv("RT_HOST_SAH") && atoi(getenv("RT_HOST_SAH")) != 0) {
-        std::vector<float4> hlo(n), hhi(n), nlo(n - 1), nhi(n - 1);
-        std::vector<int> l(n - 1), r(n - 1);
-        cudaMemcpyAsync(hlo.data(), slo, sizeof(float4) * n, cudaMemcpyDeviceToHost, st);
-        cudaMemcpyAsync(hhi.data(), shi, sizeof(float4) * n, cudaMemcpyDeviceToHost, st);
-        cudaError_t e = cudaStreamSynchronize(st);
-        if (e != cudaSuccess) return e;
-        sah_build_host(hlo.data(), hhi.data(), n, l.data(), r.data(), nlo.data(), nhi.data());
-        cudaMemcpyAsync(B.left, l.data(), sizeof(int) * (n - 1), cudaMemcpyHostToDevice, st);
-        cudaMemcpyAsync(B.right, r.data(), sizeof(int) * (n - 1), cudaMemcpyHostToDevice, st);
-        cudaMemcpyAsync(B.node_lo, nlo.data(), sizeof(float4) * (n - 1), cudaMemcpyHostToDevice, st);
-        cudaMemcpyAsync(B.node_hi, nhi.data(), sizeof(float4) * (n - 1), cudaMemcpyHostToDevice, st);
-        e = cudaStreamSynchronize(st);                   // host vectors die at scope end
-        if (e != cudaSuccess) return e;
-    }
     // root: a leaf if the whole scene fits one leaf, else BVH4 node 0 from BVH2 node 0
     if (n <= B.leaf_max) {
         *root = ~(((n - 1) << LEAF_SHIFT) | 0);

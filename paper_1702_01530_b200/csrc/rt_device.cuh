@@ -1,13 +1,12 @@
 // rt_device.cuh -- device-side data layout and FP32 intersectors of the B200 stereo ray tracer.
 //
 // Layout in HBM:
-//   nodes  : BVH4 nodes (BVH_W = 4; 8 with -DRT_BVH_WIDTH=8), default 7 x float4 = 112 B each:
-//              lo.x[4] hi.x[4] lo.y[4] hi.y[4] lo.z[4] hi.z[4] child[4]
+//   nodes  : BVH4 nodes, 7 x float4 = 112 B each, stored in slot order
+//              lo.x[4] hi.x[4] lo.y[4] child[4] hi.y[4] lo.z[4] hi.z[4]   (node_slot below)
 //            child >= 0 internal node, WIDE_EMPTY unused slot (inverted box), child < 0 leaf:
 //            ~child = (count-1) << 24 | first_prim.
-//            -DRT_NODE_F16=1 (NEXT-4 compressed nodes): 5 x float4 = 80 B each:
-//              (O.xyz, S as binary16) (child[4]) then per axis (lo01, lo23, hi01, hi23) as binary16
-//              pairs; plane = O + h * S, h rounded outward (lo down, hi up), S = 2^e per node.
+//            (Measured and rejected layouts -- 8-wide, binary16-compressed, 128-B padded nodes --
+//            are in git history before the round-2 pruning.)
 //   prims  : 3 x float4 = 48 B per BVH primitive, in leaf (Morton) order
 //              triangle: (v0.xyz, gid) (e1.xyz, mat) (e2.xyz, 0)        -- SPEC:170 Moller-Trumbore
 //              sphere  : (c.xyz,  gid) (r, r^2, 0, mat) (r^2, 0, 0, 0)
@@ -25,36 +24,18 @@ namespace rtb {
 constexpr float T_MIN = 1e-4f;     // SPEC.md:156 t_min
 constexpr float BIAS = 1e-4f;      // SPEC.md:156 shadow_bias (also reflection/refraction origins)
 constexpr int MAX_DEPTH = 16;
-#ifndef RT_BVH_WIDTH
-#define RT_BVH_WIDTH 4
-#endif
-constexpr int BVH_W = RT_BVH_WIDTH;                    // children per node (4 or 8)
-#ifndef RT_NODE_BASES
-#define RT_NODE_BASES 0
-#endif
-#ifndef RT_NODE_PAD
-#define RT_NODE_PAD 0
-#endif
-#ifndef RT_NODE_F16
-#define RT_NODE_F16 0
-#endif
-#if RT_NODE_F16 && RT_BVH_WIDTH != 4
-#error "RT_NODE_F16 requires RT_BVH_WIDTH 4"
-#endif
-constexpr int NODE_DATA_F4 = 7 * BVH_W / 4;            // float4 of decoded node data: lo/hi x,y,z + child codes
-constexpr int NODE_F4 = RT_NODE_F16 ? 5 : (RT_NODE_PAD && BVH_W == 4) ? 8 : NODE_DATA_F4;   // node stride
+constexpr int BVH_W = 4;                               // children per node
+constexpr int NODE_DATA_F4 = 7;                        // float4 per node: lo/hi x,y,z + child codes
+constexpr int NODE_F4 = NODE_DATA_F4;                  // node stride in float4
 constexpr int STACK_CAP = (BVH_W - 1) * 64 + 2;       // traversal stack: W-1 siblings per level, depth <= 64
-#ifndef RT_CH_MID
-#define RT_CH_MID 1
-#endif
-// Storage slot (16-byte unit for BVH4) of array a = 0 lo.x, 1 hi.x, 2 lo.y, 3 hi.y, 4 lo.z, 5 hi.z,
-// 6 child codes.  RT_CH_MID (BVH4): the child codes sit in slot 3, between lo.y and hi.y.  A 112-byte
+// Storage slot (16-byte unit) of array a = 0 lo.x, 1 hi.x, 2 lo.y, 3 hi.y, 4 lo.z, 5 hi.z,
+// 6 child codes.  The child codes sit in slot 3, between lo.y and hi.y.  A 112-byte
 // node starts on a 32-byte sector boundary or 16 bytes past one; either way the codes then share
 // their sector with lo.y or hi.y -- both always loaded (the near and far y planes) -- so the codes'
 // load, which ptxas issues only after the box tests, hits a sector already on its way to L1
 // instead of costing a second L2 round trip.
 __host__ __device__ constexpr int node_slot(int a) {
-    return (RT_CH_MID && BVH_W == 4) ? (a == 6 ? 3 : (a >= 3 ? a + 1 : a)) : a;
+    return a == 6 ? 3 : (a >= 3 ? a + 1 : a);
 }
 constexpr int LEAF_SHIFT = 24;     // leaf encoding: ~((count-1) << 24 | first)
 constexpr int TILE = 16;
@@ -64,39 +45,6 @@ constexpr int TRAV_DONE = (int)0x80000000;  // traversal finished (not a valid l
 // ------------------------------------------------------------------ node codec (build / refit)
 // Writes one node from its children's boxes and codes (code == WIDE_EMPTY: unused slot).
 __device__ inline void node_write(float4* q, const float3* lo, const float3* hi, const int* code) {
-#if RT_NODE_F16
-    float3 O = make_float3(3.0e38f, 3.0e38f, 3.0e38f);
-    for (int c = 0; c < 4; ++c)
-        if (code[c] != WIDE_EMPTY) O = make_float3(fminf(O.x, lo[c].x), fminf(O.y, lo[c].y), fminf(O.z, lo[c].z));
-    double E = 0.0;
-    for (int c = 0; c < 4; ++c)
-        if (code[c] != WIDE_EMPTY)
-            E = fmax(E, fmax((double)hi[c].x - O.x, fmax((double)hi[c].y - O.y, (double)hi[c].z - O.z)));
-    int e = E > 0.0 ? ilogb(E) + 1 - 14 : -14;           // E / 2^e < 2^14: offsets stay finite in binary16
-    e = e < -14 ? -14 : (e > 15 ? 15 : e);                // S a normal binary16 (no subnormal flush)
-    const double S = ldexp(1.0, e);
-    const uint32_t Sh = __half_as_ushort(__float2half_rn((float)S));   // exact power of two
-    // integer stores: leaf / empty codes are NaN bit patterns as floats
-    float* qf = reinterpret_cast<float*>(q);
-    qf[0] = O.x; qf[1] = O.y; qf[2] = O.z;
-    reinterpret_cast<uint32_t*>(q)[3] = Sh;
-    *reinterpret_cast<int4*>(q + 1) = make_int4(code[0], code[1], code[2], code[3]);
-    for (int a = 0; a < 3; ++a) {
-        uint32_t hl[4], hh[4];
-        for (int c = 0; c < 4; ++c) {
-            if (code[c] == WIDE_EMPTY) { hl[c] = 0x7C00u; hh[c] = 0xFC00u; continue; }   // +inf / -inf: never hit
-            const float l = a == 0 ? lo[c].x : (a == 1 ? lo[c].y : lo[c].z);
-            const float h = a == 0 ? hi[c].x : (a == 1 ? hi[c].y : hi[c].z);
-            const float o = a == 0 ? O.x : (a == 1 ? O.y : O.z);
-            // outward rounding: O + hl*S <= lo and O + hh*S >= hi exactly
-            hl[c] = __half_as_ushort(__float2half_rd(__double2float_rd(((double)l - o) / S)));
-            hh[c] = __half_as_ushort(__float2half_ru(__double2float_ru(((double)h - o) / S)));
-            if (hh[c] > 0 && hh[c] < 0x0400u) hh[c] = 0x0400u;   // subnormal hi -> min normal (flush-safe, outward)
-        }
-        *reinterpret_cast<uint4*>(q + 2 + a) = make_uint4(hl[0] | hl[1] << 16, hl[2] | hl[3] << 16, hh[0] | hh[1] << 16,
-                                                         hh[2] | hh[3] << 16);
-    }
-#else
     float* o = reinterpret_cast<float*>(q);
     int* oc = reinterpret_cast<int*>(o) + node_slot(6) * BVH_W;
     for (int c = 0; c < BVH_W; ++c) {
@@ -114,40 +62,17 @@ __device__ inline void node_write(float4* q, const float3* lo, const float3* hi,
         }
         oc[c] = code[c];
     }
-#endif
 }
 
 __device__ inline int node_code(const float4* q, int c) {
-#if RT_NODE_F16
-    return reinterpret_cast<const int*>(q + 1)[c];
-#else
     return reinterpret_cast<const int*>(q)[node_slot(6) * BVH_W + c];
-#endif
 }
 
 // Box of child c as stored (decoded outward-rounded for compressed nodes; empty = inverted).
 __device__ inline void node_child_box(const float4* q, int c, float3& lo, float3& hi) {
-#if RT_NODE_F16
-    if (node_code(q, c) == WIDE_EMPTY) { lo = make_float3(1e30f, 1e30f, 1e30f); hi = make_float3(-1e30f, -1e30f, -1e30f); return; }
-    const float4 a = q[0];
-    const double S = (double)__half2float(__ushort_as_half((unsigned short)(__float_as_uint(a.w) & 0xFFFFu)));
-    float l[3], h[3];
-    const float o[3] = {a.x, a.y, a.z};
-    for (int k = 0; k < 3; ++k) {
-        const float4 w = q[2 + k];
-        const uint32_t wl = __float_as_uint(c < 2 ? w.x : w.y), wh = __float_as_uint(c < 2 ? w.z : w.w);
-        const float fl = __half2float(__ushort_as_half((unsigned short)((c & 1) ? wl >> 16 : wl & 0xFFFFu)));
-        const float fh = __half2float(__ushort_as_half((unsigned short)((c & 1) ? wh >> 16 : wh & 0xFFFFu)));
-        l[k] = __double2float_rd((double)o[k] + (double)fl * S);
-        h[k] = __double2float_ru((double)o[k] + (double)fh * S);
-    }
-    lo = make_float3(l[0], l[1], l[2]);
-    hi = make_float3(h[0], h[1], h[2]);
-#else
     const float* r = reinterpret_cast<const float*>(q);
     lo = make_float3(r[node_slot(0) * BVH_W + c], r[node_slot(2) * BVH_W + c], r[node_slot(4) * BVH_W + c]);
     hi = make_float3(r[node_slot(1) * BVH_W + c], r[node_slot(3) * BVH_W + c], r[node_slot(5) * BVH_W + c]);
-#endif
 }
 
 struct DevScene {
@@ -192,21 +117,14 @@ __device__ __forceinline__ float3 cross(float3 a, float3 b) {
 __device__ __forceinline__ float3 normalize(float3 a) { return a * rsqrtf(dot(a, a)); }
 // sqrt and reciprocal through the MUFU approximations (~2 ulp), like normalize above: the IEEE
 // versions carry a slow-path call whose register saves spill the traversal state around them
-#ifndef RT_FAST_INV
-#define RT_FAST_INV 0    // 1: MUFU reciprocal for 1/d too (C2 -5 %, but C4 +4 %, C3 +4 %)
-#endif
-#ifndef RT_FAST_DIST
-#define RT_FAST_DIST 1   // shadow-ray length and refraction: MUFU sqrt/reciprocal
-#endif
-#ifndef RT_FAST_SPH
-#define RT_FAST_SPH 1    // sphere test: MUFU-based sqrt
-#endif
 __device__ __forceinline__ float fsqrt(float x) { return x > 0.0f ? x * rsqrtf(x) : 0.0f; }
 __device__ __forceinline__ float frcp(float x) { return __fdividef(1.0f, x); }
-__device__ __forceinline__ float sqrt_sph(float x) { return RT_FAST_SPH ? fsqrt(x) : sqrtf(x); }
-__device__ __forceinline__ float sqrt_dist(float x) { return RT_FAST_DIST ? fsqrt(x) : sqrtf(x); }
-__device__ __forceinline__ float rcp_dist(float x) { return RT_FAST_DIST ? frcp(x) : 1.0f / x; }
-__device__ __forceinline__ float rcp_inv(float x) { return RT_FAST_INV ? frcp(x) : 1.0f / x; }
+__device__ __forceinline__ float sqrt_sph(float x) { return fsqrt(x); }     // sphere test
+__device__ __forceinline__ float sqrt_dist(float x) { return fsqrt(x); }    // shadow-ray length, refraction
+__device__ __forceinline__ float rcp_dist(float x) { return frcp(x); }
+// 1/d of the ray setup: the compiler's reciprocal (MUFU under --use_fast_math); an explicit
+// __fdividef here measured C2 -5 % but C4 and C3 +4 % (DESIGN.md §5 v19)
+__device__ __forceinline__ float rcp_inv(float x) { return 1.0f / x; }
 __device__ __forceinline__ float3 fma3(float3 a, float s, float3 b) {
     return f3(fmaf(a.x, s, b.x), fmaf(a.y, s, b.y), fmaf(a.z, s, b.z));
 }
@@ -271,13 +189,6 @@ struct RayBox {
     float3 cn;    // near-plane constants
     float3 cf;    // far-plane constants
     int sx, sy, sz;   // 1 if d < 0 on that axis (near plane = hi)
-#if RT_NODE_BASES
-    // per-ray byte bases of the near / far plane arrays (nodes + 16 * plane index): a node's plane
-    // address is then one IMAD.WIDE (node * stride + base) on the FMA pipe instead of an
-    // IMAD + 64-bit IADD3 pair on the ALU pipe per load
-    const char* pn[3];
-    const char* pf[3];
-#endif
 };
 
 __device__ __forceinline__ float safe_inv(float x) {
@@ -295,48 +206,9 @@ __device__ __forceinline__ RayBox make_raybox(float3 o, float3 d, float bound) {
     rb.sx = rb.idir.x < 0.0f;
     rb.sy = rb.idir.y < 0.0f;
     rb.sz = rb.idir.z < 0.0f;
-#if RT_NODE_F16
-    // compressed nodes: cn / cf hold the shifted origins o -/+ m of the near / far planes; the
-    // plane distance is (O + h S - origin) * idir, formed per node
-    (void)clo;
-    (void)chi;
-    rb.cn = f3(rb.sx ? o.x - m : o.x + m, rb.sy ? o.y - m : o.y + m, rb.sz ? o.z - m : o.z + m);
-    rb.cf = f3(rb.sx ? o.x + m : o.x - m, rb.sy ? o.y + m : o.y - m, rb.sz ? o.z + m : o.z - m);
-#else
     rb.cn = f3(rb.sx ? chi.x : clo.x, rb.sy ? chi.y : clo.y, rb.sz ? chi.z : clo.z);
     rb.cf = f3(rb.sx ? clo.x : chi.x, rb.sy ? clo.y : chi.y, rb.sz ? clo.z : chi.z);
-#endif
     return rb;
-}
-
-#if RT_NODE_BASES
-__device__ __forceinline__ const char* opaque_ptr(const char* p) {
-    const char* q;
-    asm("mov.b64 %0, %1;" : "=l"(q) : "l"(p));    // keep the per-ray base from being re-associated
-    return q;
-}
-#endif
-
-__device__ __forceinline__ void set_node_bases(RayBox& rb, const float4* nodes) {
-#if RT_NODE_BASES
-    const char* b = reinterpret_cast<const char*>(nodes);
-    rb.pn[0] = opaque_ptr(b + 16 * node_slot(rb.sx));     rb.pf[0] = opaque_ptr(b + 16 * node_slot(1 - rb.sx));
-    rb.pn[1] = opaque_ptr(b + 16 * node_slot(2 + rb.sy)); rb.pf[1] = opaque_ptr(b + 16 * node_slot(3 - rb.sy));
-    rb.pn[2] = opaque_ptr(b + 16 * node_slot(4 + rb.sz)); rb.pf[2] = opaque_ptr(b + 16 * node_slot(5 - rb.sz));
-#else
-    (void)rb;
-    (void)nodes;
-#endif
-}
-
-// Slab test of one box given its near/far planes; returns the entry distance (>= 0) or -1.
-__device__ __forceinline__ float slab(const RayBox& rb, float nx, float fx, float ny, float fy, float nz, float fz,
-                                      float tmax) {
-    const float tn = fmaxf(fmaxf(fmaf(nx, rb.idir.x, rb.cn.x), fmaf(ny, rb.idir.y, rb.cn.y)),
-                           fmaxf(fmaf(nz, rb.idir.z, rb.cn.z), 0.0f));
-    const float tf = fminf(fminf(fmaf(fx, rb.idir.x, rb.cf.x), fmaf(fy, rb.idir.y, rb.cf.y)),
-                           fminf(fmaf(fz, rb.idir.z, rb.cf.z), tmax));
-    return tn <= tf ? tn : -1.0f;
 }
 
 }  // namespace rtb

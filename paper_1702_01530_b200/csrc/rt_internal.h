@@ -21,6 +21,7 @@ enum {
     CNT_LIGHT_EVALS = RT_CNT_LIGHT_EVALS,
     CNT_MISSES = RT_CNT_MISSES,
     CNT_PIXELS = RT_CNT_PIXELS,
+    CNT_BOX_TESTS = RT_CNT_BOX_TESTS,
 };
 #define RT_NUM_COUNTERS_INTERNAL RT_NUM_COUNTERS
 
@@ -104,9 +105,6 @@ struct KdHost {
     float lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};   // root cell
 };
 void kd_build_host(const float4* prims, int n, int n_spheres, int max_leaf, int max_depth, KdHost& out);
-// experiment (rt_sah.cu, env RT_HOST_SAH=1): host binned-SAH BVH2 over the leaf boxes
-void sah_build_host(const float4* leaf_lo, const float4* leaf_hi, int n, int* left, int* right, float4* node_lo,
-                    float4* node_hi);
 }  // namespace rtb
 
 // launchers (rt_trace.cu)
@@ -116,6 +114,8 @@ size_t rtb_trace_smem(int stack_entries);
 int rtb_trace_block();      // threads per trace CTA (RT_BLOCK)
 cudaError_t rtb_launch_unpack(const void* gathered, const UnpackParams& U, cudaStream_t st);
 cudaError_t rtb_launch_ffma(float* out, int iters, int grid, cudaStream_t st);
+// B0 ceilings (rt_probe.cu)
+cudaError_t rtb_probe_ceilings(int num_sms, cudaStream_t st, double out[RT_NUM_CEILINGS]);
 cudaError_t rtb_launch_compose(const void* L, const void* R, long long lp, long long rp, int W, int H, int mode,
                                void* out, long long op, cudaStream_t st);
 // launchers (rt_build.cu)

@@ -17,9 +17,7 @@
 
 namespace rtb {
 
-#ifndef RT_MINB
-#define RT_MINB (1024 / RT_BLOCK)   // 64 registers: 1024 threads per SM
-#endif
+constexpr int RT_MINB = 1024 / RT_BLOCK;   // 64 registers: 1024 threads per SM
 
 // Trace the whole ray tree of one pixel.  Iterative: the reflection child continues in
 // registers, the refraction child is pushed on a per-thread stack (<= max_depth entries).
@@ -38,33 +36,7 @@ __device__ __forceinline__ float3 trace_pixel(const TraceParams& P, float3 o, fl
     float3 col = f3(0.f, 0.f, 0.f);
     cnt.add(CNT_PRIMARY);
     while (true) {
-#if RT_TREE_STATS
-        if (COUNT) {   // ray-tree loop utilisation: c[6] += warp iterations, c[7] += lane iterations
-            const unsigned am = __activemask();
-            if ((threadIdx.x & 31) == __ffs(am) - 1) cnt.c[6] += 1;
-            cnt.c[7] += 1;
-        }
-#endif
-#if RT_PACKET
-        // the first pass of the loop (primary rays) runs with every traced lane of the warp, and
-        // so do later passes that are still converged: those trace as warp packets
-        const bool packet = !BRUTE && (RT_PACKET_ALL || primary);
-        Hit h;
-        if (packet) h = closest_hit_packet<COUNT>(S, o, d, __activemask(), stk, cnt);
-        else h = closest_hit<COUNT, ACC>(S, o, d, stk, cnt);
-#else
-#if RT_SHADOW_STATS
-        const uint32_t s0 = cnt.steps;
-#endif
         const Hit h = closest_hit<COUNT, ACC>(S, o, d, stk, cnt);
-#if RT_SHADOW_STATS
-        if (COUNT) {   // warp-level divergence statistics: c[2] += max lane steps, c[9] += sum
-            const uint32_t T = cnt.steps - s0, am = __activemask();
-            const uint32_t mx = __reduce_max_sync(am, T), sm = __reduce_add_sync(am, T);
-            if ((threadIdx.x & 31) == __ffs(am) - 1) { cnt.c[2] += mx; cnt.c[9] += sm; }
-        }
-#endif
-#endif
         if (primary) { prim_id = h.gid; primary = false; }
         bool cont = false;
         if (h.gid < 0) {
@@ -91,39 +63,11 @@ __device__ __forceinline__ float3 trace_pixel(const TraceParams& P, float3 o, fl
             const bool front = dot(d, ng) < 0.0f;
             const float3 nf = front ? ng : ng * -1.0f;                   // S:150 faces the ray
             float3 c = S.ambient * xyz(__ldg(&S.mats[3 * mat]));         // S:193 ambient * kd
-#if RT_PACKET
-            // shadow rays of a packet pass: every lane of the pass takes part in each light's
-            // packet (lanes with the light behind their surface only ride along)
-            const unsigned pmask = packet ? __activemask() : 0u;
-#endif
-#if RT_SHADOW_STATS
-            uint32_t tsum = 0;
-#endif
             for (int j = 0; j < S.n_lights; ++j) {
-#if !RT_SHADOW_STATS
                 cnt.add(CNT_LIGHT_EVALS);
-#endif
                 const float3 Lp = xyz(__ldg(&S.lights[2 * j]));
                 const float3 l = normalize(Lp - p);
                 const float ndl = dot(nf, l);
-#if RT_PACKET
-                if (packet) {
-                    const float3 I = xyz(__ldg(&S.lights[2 * j + 1]));
-                    const float3 rv = nf * (2.0f * ndl) - l;
-                    const float rdv = -dot(rv, d);
-                    const float spec = rdv > 0.0f ? __powf(rdv, __ldg(&S.mats[3 * mat]).w) : 0.0f;
-                    const float3 term = (xyz(__ldg(&S.mats[3 * mat])) * I) * ndl + (xyz(__ldg(&S.mats[3 * mat + 1])) * I) * spec;
-                    const float3 os = fma3(nf, BIAS, p);
-                    const float3 sv = Lp - os;
-                    const float dist = sqrt_dist(dot(sv, sv));
-                    const bool lit = ndl > 0.0f;                         // reading 2 gate
-                    if (lit) cnt.add(CNT_SHADOW);
-                    int* hint = (RT_OCC_CACHE && j < RT_OCC_LIGHTS) ? occ_hint + j * RT_BLOCK : nullptr;
-                    if (!occluded_packet<COUNT>(S, os, sv * rcp_dist(dist), dist, lit, pmask, stk, cnt, hint) && lit)
-                        c = c + term;                                    // reading 3
-                    continue;
-                }
-#endif
                 if (ndl <= 0.0f) continue;                               // reading 2 gate
                 // the light's term, added only if the shadow ray reaches the light
                 const float3 I = xyz(__ldg(&S.lights[2 * j + 1]));
@@ -135,27 +79,9 @@ __device__ __forceinline__ float3 trace_pixel(const TraceParams& P, float3 o, fl
                 const float3 sv = Lp - os;
                 const float dist = sqrt_dist(dot(sv, sv));
                 cnt.add(CNT_SHADOW);
-                int* hint = (RT_OCC_CACHE && j < RT_OCC_LIGHTS) ? occ_hint + j * RT_BLOCK : nullptr;
-#if RT_SHADOW_STATS
-                const uint32_t s0 = cnt.steps;
-                const bool occ = occluded<COUNT, ACC>(S, os, sv * rcp_dist(dist), dist, stk, cnt, hint);
-                if (COUNT) {   // c[6] += per-light warp max of shadow steps, c[7] += their sum
-                    const uint32_t T = cnt.steps - s0, am = __activemask();
-                    const uint32_t mx = __reduce_max_sync(am, T), sm = __reduce_add_sync(am, T);
-                    if ((threadIdx.x & 31) == __ffs(am) - 1) { cnt.c[6] += mx; cnt.c[7] += sm; }
-                    tsum += T;
-                }
-                if (!occ) c = c + term;
-#else
+                int* hint = j < RT_OCC_LIGHTS ? occ_hint + j * RT_BLOCK : nullptr;
                 if (!occluded<COUNT, ACC>(S, os, sv * rcp_dist(dist), dist, stk, cnt, hint)) c = c + term;   // reading 3
-#endif
             }
-#if RT_SHADOW_STATS
-            if (COUNT) {       // c[10] += warp max over lanes of all their shadow steps at this hit
-                const uint32_t am = __activemask(), mx = __reduce_max_sync(am, tsum);
-                if ((threadIdx.x & 31) == __ffs(am) - 1) cnt.c[10] += mx;
-            }
-#endif
             col = fma3(c, w, col);
             if (depth > 0) {
                 const float4 m2 = __ldg(&S.mats[3 * mat + 2]);
@@ -207,11 +133,7 @@ __global__ void __launch_bounds__(RT_BLOCK, RT_MINB) k_trace_stereo(const TraceP
     cnt.zero();
     const int lane = threadIdx.x & 31;
     int lstack[STACK_CAP > RT_SMEM_STACK ? STACK_CAP - RT_SMEM_STACK : 1];
-#if RT_SMEM_PTX
     TravStack stk{(uint32_t)__cvta_generic_to_shared(s_stack + threadIdx.x), lstack};
-#else
-    TravStack stk{s_stack + threadIdx.x, lstack};
-#endif
     // Warm L2 with the scene before tracing: every frame starts with the scene + BVH cold in L2
     // (the bench flushes it between frames, as a fresh frame after other work would find it),
     // and demand misses then arrive one dependent traversal load at a time, latency-bound.

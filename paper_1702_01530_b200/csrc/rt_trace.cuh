@@ -6,133 +6,56 @@
 
 namespace rtb {
 
-#ifndef RT_BLOCK
-#define RT_BLOCK 64       // threads per trace CTA (stack stride); small CTAs free their slots as soon as
-                          // their 2 warps finish, so a next frame in flight fills the SM sooner
-#endif
-#ifndef RT_SHADOW_SORT
-#define RT_SHADOW_SORT 0  // 1: any-hit (shadow) rays also visit children near-to-far (measured slower);
-                          // 2: far-to-near (towards the light first)
-#endif
-#ifndef RT_FFMA2
-#define RT_FFMA2 1  // packed FP32 FMA (FFMA2) for the BVH4 slab planes
-#endif
-#ifndef RT_W8_FULL_SORT
-#define RT_W8_FULL_SORT 1
-#endif
-#ifndef RT_CLOSEST_SORT
-#define RT_CLOSEST_SORT 1  // nearest-hit rays visit hit children near-to-far
-#endif
-#ifndef RT_PLAIN_PUSH_LOOP
-#define RT_PLAIN_PUSH_LOOP 1
-#endif
-#ifndef RT_SMEM_STACK
-#define RT_SMEM_STACK 16  // traversal-stack entries kept in shared memory; deeper ones in local
-#endif
-
-#ifndef RT_SMEM_PTX
-#define RT_SMEM_PTX 1     // shared stack addressed with a 32-bit shared-window address held in a register
-#endif
-#ifndef RT_FAST_PUSH
-#define RT_FAST_PUSH 1    // pushes of one node visit: one shared address + predicated stores when they fit
-#endif
-#if RT_FAST_PUSH && !RT_SMEM_PTX
-#error "RT_FAST_PUSH needs RT_SMEM_PTX"
-#endif
-#ifndef RT_TREE_STATS
-#define RT_TREE_STATS 0    // 1: instrumented build records ray-tree loop lane utilisation (experiments)
-#endif
-#ifndef RT_SHADOW_STATS
-#define RT_SHADOW_STATS 0  // 1: instrumented build records warp-level traversal divergence (experiments)
-#endif
-#ifndef RT_LEAN_MASK
-#define RT_LEAN_MASK 1    // BVH4 hit mask built from the slab predicates (no -1 sentinel distances)
-#endif
-#ifndef RT_TOP_REG
-#define RT_TOP_REG 1      // BVH4: the top stack entry lives in a register (pop = register move)
-#endif
-#ifndef RT_OCC_CACHE
-#define RT_OCC_CACHE 1    // per-thread, per-light last-occluder hint for shadow rays
-#endif
-#define RT_OCC_LIGHTS 4   // lights with an occluder hint slot (light j uses slot j; others none)
-#ifndef RT_PACKET
-#define RT_PACKET 0       // warp-packet traversal for coherent rays (primary rays and their shadow rays)
-#endif
-#ifndef RT_PACKET_ALL
-#define RT_PACKET_ALL 0   // 1: secondary rays and their shadow rays also traverse as warp packets
-#endif
-#if RT_PACKET && (!RT_SMEM_PTX || RT_BVH_WIDTH != 4 || RT_NODE_F16)
-#error "RT_PACKET needs RT_SMEM_PTX and plain 4-wide nodes"
-#endif
+constexpr int RT_BLOCK = 64;      // threads per trace CTA (stack stride); small CTAs free their slots as soon as
+                                  // their 2 warps finish, so a next frame in flight fills the SM sooner
+constexpr int RT_SMEM_STACK = 16; // traversal-stack entries kept in shared memory; deeper ones in local
+constexpr int RT_OCC_LIGHTS = 4;  // lights with a last-occluder hint slot (light j uses slot j; others none)
 
 // Per-thread traversal stack: the first RT_SMEM_STACK entries live in shared memory laid out
 // [entry][thread] (conflict-free), deeper entries in thread-local memory (L1-cached).  Keeping the
 // shared part short leaves most of the 228 KB L1/shared array to cache BVH nodes.
 struct TravStack {
-#if RT_SMEM_PTX
     // 32-bit shared-window address of this thread's entry 0: STS/LDS take it directly instead of
     // rebuilding the generic->shared conversion (S2R CgaCtaId + LEA) at every push and pop
     uint32_t sa;
-#else
-    int* s;   // shared: s[i * RT_BLOCK]
-#endif
     int* l;   // local:  l[i - RT_SMEM_STACK]
     __device__ __forceinline__ void set(int i, int v) {
-        if (i < RT_SMEM_STACK) {
-#if RT_SMEM_PTX
-            asm volatile("st.shared.b32 [%0], %1;" ::"r"(sa + (uint32_t)i * (RT_BLOCK * 4u)), "r"(v));
-#else
-            s[i * RT_BLOCK] = v;
-#endif
-        } else {
-            l[i - RT_SMEM_STACK] = v;
-        }
+        if (i < RT_SMEM_STACK) asm volatile("st.shared.b32 [%0], %1;" ::"r"(sa + (uint32_t)i * (RT_BLOCK * 4u)), "r"(v));
+        else l[i - RT_SMEM_STACK] = v;
     }
     __device__ __forceinline__ int get(int i) const {
         if (i < RT_SMEM_STACK) {
-#if RT_SMEM_PTX
             int v;
             asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(sa + (uint32_t)i * (RT_BLOCK * 4u)));
             return v;
-#else
-            return s[i * RT_BLOCK];
-#endif
         }
         return l[i - RT_SMEM_STACK];
     }
-#if RT_SMEM_PTX
     // shared address of entry i (valid for i < RT_SMEM_STACK); entry i + k is at + k * RT_BLOCK * 4
     __device__ __forceinline__ uint32_t addr(int i) const { return sa + (uint32_t)i * (RT_BLOCK * 4u); }
-    __device__ __forceinline__ static void st(uint32_t a, int v) {
-        asm volatile("st.shared.b32 [%0], %1;" ::"r"(a), "r"(v));
-    }
     __device__ __forceinline__ static void st_if(bool p, uint32_t a, int v) {
         asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.shared.b32 [%0], %1;\n\t}" ::"r"(a), "r"(v),
                      "r"((uint32_t)p));
     }
-#endif
 };
 
 template <bool COUNT>
 struct Counters {
     uint32_t c[RT_NUM_COUNTERS_INTERNAL];
-#if RT_SHADOW_STATS
-    uint32_t steps;   // traversal loop iterations of this thread (divergence statistics build only)
-#endif
     __device__ void zero() {
-#if RT_SHADOW_STATS
-        steps = 0;
-#endif
 #pragma unroll
         for (int i = 0; i < RT_NUM_COUNTERS_INTERNAL; ++i) c[i] = 0;
     }
     __device__ __forceinline__ void add(int i, uint32_t n = 1) { if (COUNT) c[i] += n; }
-    __device__ __forceinline__ void step() {
-#if RT_SHADOW_STATS
-        if (COUNT) ++steps;
-#endif
-    }
 };
+
+// Instrumented builds: real (non-empty) child boxes tested at a BVH4 node visit -- the slab
+// tests the method performs; the inverted boxes of empty slots are layout, not work (§8(d) flops).
+template <bool COUNT>
+__device__ __forceinline__ void count_boxes(Counters<COUNT>& cnt, const int4& ch) {
+    if (COUNT)
+        cnt.add(CNT_BOX_TESTS, (ch.x != WIDE_EMPTY) + (ch.y != WIDE_EMPTY) + (ch.z != WIDE_EMPTY) + (ch.w != WIDE_EMPTY));
+}
 
 struct Hit {
     float t;
@@ -210,71 +133,16 @@ __device__ __forceinline__ bool prim_t(const DevScene& S, int k, float3 o, float
     return tri_intersect(o, d, a, b, c, t) && t > T_MIN;
 }
 
-// Box tests of the 4 children of one BVH4 node (7 float4: lo.x hi.x lo.y hi.y lo.z hi.z child).
-// Returns the hit mask; tn[c] = entry distance of hit children.
+// Box tests of the 4 children of one BVH4 node (7 float4 in node_slot order).  Returns the hit
+// mask straight from the four slab predicates; tn[c] = raw entry distance (>= 0), read only for
+// the children the mask marks as hit.  Empty slots hold inverted boxes, which every test rejects.
 __device__ __forceinline__ unsigned node4_hits(const float4* __restrict__ nodes, int node, const RayBox& rb, float tmax,
                                                float tn[4], int4& child) {
-#if RT_NODE_F16
-    const float4* q = nodes + (size_t)NODE_F4 * node;
-    const float4 a = __ldg(q);
-    child = __ldg(reinterpret_cast<const int4*>(q + 1));
-    const uint4 X = __ldg(reinterpret_cast<const uint4*>(q + 2));
-    const uint4 Y = __ldg(reinterpret_cast<const uint4*>(q + 3));
-    const uint4 Z = __ldg(reinterpret_cast<const uint4*>(q + 4));
-    const uint32_t Sw = __float_as_uint(a.w);
-    // near / far binary16 pairs by the ray's direction signs
-    const uint32_t nx0 = rb.sx ? X.z : X.x, nx1 = rb.sx ? X.w : X.y, fx0 = rb.sx ? X.x : X.z, fx1 = rb.sx ? X.y : X.w;
-    const uint32_t ny0 = rb.sy ? Y.z : Y.x, ny1 = rb.sy ? Y.w : Y.y, fy0 = rb.sy ? Y.x : Y.z, fy1 = rb.sy ? Y.y : Y.w;
-    const uint32_t nz0 = rb.sz ? Z.z : Z.x, nz1 = rb.sz ? Z.w : Z.y, fz0 = rb.sz ? Z.x : Z.z, fz1 = rb.sz ? Z.y : Z.w;
-    // plane - shifted origin = h * S + (O - origin): one mixed-precision FMA (binary16 h, S;
-    // FP32 addend), rounded once; then times idir (packed FMUL2)
-    auto dec = [&](uint32_t w, float k) {
-        float2 r;
-        asm("{\n\t.reg .f16 l, h, s, t;\n\tmov.b32 {l, h}, %2;\n\tmov.b32 {s, t}, %3;\n\t"
-            "fma.rn.f32.f16 %0, l, s, %4;\n\tfma.rn.f32.f16 %1, h, s, %4;\n\t}"
-            : "=f"(r.x), "=f"(r.y) : "r"(w), "r"(Sw), "f"(k));
-        return r;
-    };
-    const float2 ix = make_float2(rb.idir.x, rb.idir.x), iy = make_float2(rb.idir.y, rb.idir.y);
-    const float2 iz = make_float2(rb.idir.z, rb.idir.z);
-    const float knx = a.x - rb.cn.x, kny = a.y - rb.cn.y, knz = a.z - rb.cn.z;
-    const float kfx = a.x - rb.cf.x, kfy = a.y - rb.cf.y, kfz = a.z - rb.cf.z;
-    const float2 a0 = __fmul2_rn(dec(nx0, knx), ix), a1 = __fmul2_rn(dec(nx1, knx), ix);
-    const float2 b0 = __fmul2_rn(dec(ny0, kny), iy), b1 = __fmul2_rn(dec(ny1, kny), iy);
-    const float2 c0 = __fmul2_rn(dec(nz0, knz), iz), c1 = __fmul2_rn(dec(nz1, knz), iz);
-    const float2 d0 = __fmul2_rn(dec(fx0, kfx), ix), d1 = __fmul2_rn(dec(fx1, kfx), ix);
-    const float2 e0 = __fmul2_rn(dec(fy0, kfy), iy), e1 = __fmul2_rn(dec(fy1, kfy), iy);
-    const float2 g0 = __fmul2_rn(dec(fz0, kfz), iz), g1 = __fmul2_rn(dec(fz1, kfz), iz);
-    const float tn0 = fmaxf(fmaxf(a0.x, b0.x), fmaxf(c0.x, 0.0f)), tf0 = fminf(fminf(d0.x, e0.x), fminf(g0.x, tmax));
-    const float tn1 = fmaxf(fmaxf(a0.y, b0.y), fmaxf(c0.y, 0.0f)), tf1 = fminf(fminf(d0.y, e0.y), fminf(g0.y, tmax));
-    const float tn2 = fmaxf(fmaxf(a1.x, b1.x), fmaxf(c1.x, 0.0f)), tf2 = fminf(fminf(d1.x, e1.x), fminf(g1.x, tmax));
-    const float tn3 = fmaxf(fmaxf(a1.y, b1.y), fmaxf(c1.y, 0.0f)), tf3 = fminf(fminf(d1.y, e1.y), fminf(g1.y, tmax));
-    tn[0] = tn0 <= tf0 ? tn0 : -1.0f;
-    tn[1] = tn1 <= tf1 ? tn1 : -1.0f;
-    tn[2] = tn2 <= tf2 ? tn2 : -1.0f;
-    tn[3] = tn3 <= tf3 ? tn3 : -1.0f;
-    unsigned m = 0;
-    m |= tn[0] >= 0.0f ? 1u : 0u;
-    m |= tn[1] >= 0.0f ? 2u : 0u;
-    m |= tn[2] >= 0.0f ? 4u : 0u;
-    m |= tn[3] >= 0.0f ? 8u : 0u;
-    return m;
-#elif RT_NODE_BASES
-    const size_t off = (size_t)(uint32_t)node * (16u * NODE_F4);
-    auto ld = [&](const char* b) { return __ldg(reinterpret_cast<const float4*>(b + off)); };
-    const float4 nx = ld(rb.pn[0]), fx = ld(rb.pf[0]);
-    const float4 ny = ld(rb.pn[1]), fy = ld(rb.pf[1]);
-    const float4 nz = ld(rb.pn[2]), fz = ld(rb.pf[2]);
-    child = __ldg(reinterpret_cast<const int4*>(nodes + (size_t)NODE_F4 * node + node_slot(6)));
-#else
     const float4* q = nodes + (size_t)NODE_F4 * node;
     const float4 nx = __ldg(q + node_slot(rb.sx)), fx = __ldg(q + node_slot(1 - rb.sx));
     const float4 ny = __ldg(q + node_slot(2 + rb.sy)), fy = __ldg(q + node_slot(3 - rb.sy));
     const float4 nz = __ldg(q + node_slot(4 + rb.sz)), fz = __ldg(q + node_slot(5 - rb.sz));
     child = __ldg(reinterpret_cast<const int4*>(q + node_slot(6)));
-#endif
-#if !RT_NODE_F16
-#if RT_FFMA2
     // packed FP32 FMA (sm_100 FFMA2): two children's plane distances per instruction
     const float2 ix = make_float2(rb.idir.x, rb.idir.x), iy = make_float2(rb.idir.y, rb.idir.y);
     const float2 iz = make_float2(rb.idir.z, rb.idir.z);
@@ -290,32 +158,11 @@ __device__ __forceinline__ unsigned node4_hits(const float4* __restrict__ nodes,
     const float tn1 = fmaxf(fmaxf(a0.y, b0.y), fmaxf(c0.y, 0.0f)), tf1 = fminf(fminf(d0.y, e0.y), fminf(g0.y, tmax));
     const float tn2 = fmaxf(fmaxf(a1.x, b1.x), fmaxf(c1.x, 0.0f)), tf2 = fminf(fminf(d1.x, e1.x), fminf(g1.x, tmax));
     const float tn3 = fmaxf(fmaxf(a1.y, b1.y), fmaxf(c1.y, 0.0f)), tf3 = fminf(fminf(d1.y, e1.y), fminf(g1.y, tmax));
-#if RT_LEAN_MASK
-    // the hit mask straight from the four slab predicates; tn[] stays the raw entry distance
-    // (>= 0) and is only read for the children the mask marks as hit
     tn[0] = tn0;
     tn[1] = tn1;
     tn[2] = tn2;
     tn[3] = tn3;
     return (tn0 <= tf0 ? 1u : 0u) | (tn1 <= tf1 ? 2u : 0u) | (tn2 <= tf2 ? 4u : 0u) | (tn3 <= tf3 ? 8u : 0u);
-#endif
-    tn[0] = tn0 <= tf0 ? tn0 : -1.0f;
-    tn[1] = tn1 <= tf1 ? tn1 : -1.0f;
-    tn[2] = tn2 <= tf2 ? tn2 : -1.0f;
-    tn[3] = tn3 <= tf3 ? tn3 : -1.0f;
-#else
-    tn[0] = slab(rb, nx.x, fx.x, ny.x, fy.x, nz.x, fz.x, tmax);
-    tn[1] = slab(rb, nx.y, fx.y, ny.y, fy.y, nz.y, fz.y, tmax);
-    tn[2] = slab(rb, nx.z, fx.z, ny.z, fy.z, nz.z, fz.z, tmax);
-    tn[3] = slab(rb, nx.w, fx.w, ny.w, fy.w, nz.w, fz.w, tmax);
-#endif
-    unsigned m = 0;
-    m |= tn[0] >= 0.0f ? 1u : 0u;                          // empty slots hold inverted boxes
-    m |= tn[1] >= 0.0f ? 2u : 0u;
-    m |= tn[2] >= 0.0f ? 4u : 0u;
-    m |= tn[3] >= 0.0f ? 8u : 0u;
-    return m;
-#endif
 }
 
 __device__ __forceinline__ void cswap(uint32_t& a, uint32_t& b) {
@@ -331,88 +178,13 @@ __device__ __forceinline__ int pick4(const int4& c, uint32_t i) {
     return (i & 2u) ? hi : lo;
 }
 
-// Visit order of the hit children: entry distances are >= 0, so their bit patterns order like
-// unsigned ints; the 2 low bits carry the child slot; a 5-exchange network sorts them.  The
-// nearest hit continues, the others are pushed far-to-near (predicated stores, no branches).
-__device__ __forceinline__ bool order_push(unsigned m, const float tn[4], const int4& ch, TravStack& stk, int& sp, int& node) {
-    if (!m) return false;
-    uint32_t k0 = (m & 1) ? ((__float_as_uint(tn[0]) & ~3u) | 0u) : 0xffffffffu;
-    uint32_t k1 = (m & 2) ? ((__float_as_uint(tn[1]) & ~3u) | 1u) : 0xffffffffu;
-    uint32_t k2 = (m & 4) ? ((__float_as_uint(tn[2]) & ~3u) | 2u) : 0xffffffffu;
-    uint32_t k3 = (m & 8) ? ((__float_as_uint(tn[3]) & ~3u) | 3u) : 0xffffffffu;
-    cswap(k0, k1); cswap(k2, k3); cswap(k0, k2); cswap(k1, k3); cswap(k1, k2);
-    const int nh = __popc(m);
-#if RT_FAST_PUSH
-    if (sp + 3 <= RT_SMEM_STACK) {
-        // all pushes land in the shared part: one address, predicated stores (no branches)
-        const uint32_t a = stk.addr(sp + nh - 2);
-        TravStack::st_if(nh > 3, a - 2u * (RT_BLOCK * 4u), pick4(ch, k3 & 3u));
-        TravStack::st_if(nh > 2, a - 1u * (RT_BLOCK * 4u), pick4(ch, k2 & 3u));
-        TravStack::st_if(nh > 1, a, pick4(ch, k1 & 3u));
-    } else
-#endif
-    {
-        if (nh > 3) stk.set(sp + nh - 4, pick4(ch, k3 & 3u));
-        if (nh > 2) stk.set(sp + nh - 3, pick4(ch, k2 & 3u));
-        if (nh > 1) stk.set(sp + nh - 2, pick4(ch, k1 & 3u));
-    }
-    sp += nh - 1;
-    node = pick4(ch, k0 & 3u);
-    return true;
-}
-
-
-// Any-hit rays: continue with the lowest hit slot, push the others in slot order (no distance
-// sort); unrolled with predicated stores.
-__device__ __forceinline__ bool plain_push(unsigned m, const int4& ch, TravStack& stk, int& sp, int& node) {
-    if (!m) return false;
-#if RT_FAST_PUSH
-    if (sp + 3 <= RT_SMEM_STACK) {
-        // continue with the lowest hit slot; the others (slots above it) go to entries sp.. in slot
-        // order: slot c's entry is sp + popc(r & below(c)), r = the pushed set (slot 0 never pushed)
-        const unsigned r = m & (m - 1u);
-        const uint32_t a = stk.addr(sp);
-        constexpr uint32_t E = RT_BLOCK * 4u;
-        TravStack::st_if(r & 2u, a, ch.y);
-        TravStack::st_if(r & 4u, a + ((r >> 1) & 1u) * E, ch.z);
-        TravStack::st_if(r & 8u, a + (uint32_t)__popc(r & 6u) * E, ch.w);
-        sp += __popc(r);
-        node = pick4(ch, __ffs(m) - 1);
-        return true;
-    }
-#endif
-#if RT_PLAIN_PUSH_LOOP
-    const int nh = __popc(m);
-    const uint32_t c0 = __ffs(m) - 1;
-    m &= m - 1;
-    int k = sp;
-    while (m) {
-        const uint32_t c = __ffs(m) - 1;
-        m &= m - 1;
-        stk.set(k++, pick4(ch, c));
-    }
-    sp += nh - 1;
-    node = pick4(ch, c0);
-#else
-    const int codes[4] = {ch.x, ch.y, ch.z, ch.w};
-    int first = -1;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-        if (m & (1u << c)) {
-            if (first < 0) first = codes[c];
-            else stk.set(sp++, codes[c]);
-        }
-    }
-    node = first;
-#endif
-    return true;
-}
-
-
-#if RT_TOP_REG
-// Stack with its top entry cached in a register: logical entries [0, sp) are memory entries
+// Traversal stack with its top entry cached in a register: logical entries [0, sp) are memory entries
 // [0, sp-1) plus `top`.  A pop is a register move; the LDS/LDL that refills `top` is issued
 // right away but its latency overlaps the popped node's visit instead of preceding it.
+// Nearest-hit rays: visit order of the hit children.  Entry distances are >= 0, so their bit
+// patterns order like unsigned ints; the 2 low bits carry the child slot and a 5-exchange network
+// sorts them.  The nearest continues, the second nearest becomes the cached top, the others are
+// pushed far-to-near with predicated stores (no branches).
 __device__ __forceinline__ bool order_push_top(unsigned m, const float tn[4], const int4& ch, TravStack& stk, int& sp,
                                                int& top, int& node) {
     if (!m) return false;
@@ -442,6 +214,8 @@ __device__ __forceinline__ bool order_push_top(unsigned m, const float tn[4], co
     return true;
 }
 
+// Any-hit (shadow) rays: continue with the lowest hit slot, push the others in slot order (no
+// distance sort: measured 7 % faster, and fewer triangle tests).
 __device__ __forceinline__ bool plain_push_top(unsigned m, const int4& ch, TravStack& stk, int& sp, int& top, int& node) {
     if (!m) return false;
     const unsigned r = m & (m - 1u);                       // pushed slots (all hits but the lowest)
@@ -472,80 +246,6 @@ __device__ __forceinline__ bool pop_top(TravStack& stk, int& sp, int& top, int& 
     if (--sp > 0) top = stk.get(sp - 1);
     return true;
 }
-#endif
-
-// ---------------------------------------------------------------- 8-wide nodes
-// 14 float4: lo.x[8] hi.x[8] lo.y[8] hi.y[8] lo.z[8] hi.z[8] child[8]; near/far planes picked per
-// ray by direction sign (two float4 per array); child codes are loaded only for pushed children.
-__device__ __forceinline__ unsigned node8_hits(const float4* __restrict__ nodes, int node, const RayBox& rb, float tmax,
-                                               float tn[8]) {
-    const float4* q = nodes + 14 * node;
-#pragma unroll
-    for (int g = 0; g < 2; ++g) {
-        const float4 nx = __ldg(q + 2 * rb.sx + g), fx = __ldg(q + 2 - 2 * rb.sx + g);
-        const float4 ny = __ldg(q + 4 + 2 * rb.sy + g), fy = __ldg(q + 6 - 2 * rb.sy + g);
-        const float4 nz = __ldg(q + 8 + 2 * rb.sz + g), fz = __ldg(q + 10 - 2 * rb.sz + g);
-        tn[4 * g + 0] = slab(rb, nx.x, fx.x, ny.x, fy.x, nz.x, fz.x, tmax);
-        tn[4 * g + 1] = slab(rb, nx.y, fx.y, ny.y, fy.y, nz.y, fz.y, tmax);
-        tn[4 * g + 2] = slab(rb, nx.z, fx.z, ny.z, fy.z, nz.z, fz.z, tmax);
-        tn[4 * g + 3] = slab(rb, nx.w, fx.w, ny.w, fy.w, nz.w, fz.w, tmax);
-    }
-    unsigned m = 0;
-#pragma unroll
-    for (int c = 0; c < 8; ++c) m |= tn[c] >= 0.0f ? (1u << c) : 0u;   // empty slots: inverted boxes
-    return m;
-}
-
-__device__ __forceinline__ int child8(const float4* __restrict__ nodes, int node, uint32_t slot) {
-    return __ldg(reinterpret_cast<const int*>(nodes + 14 * node + 12) + slot);
-}
-
-// Nearest-first order of the hit children: (distance bits | 3-bit slot) keys through Batcher's
-// 19-exchange odd-even merge network; the nearest continues, the others are pushed far-to-near.
-__device__ __forceinline__ bool order_push8(unsigned m, const float tn[8], const float4* __restrict__ nodes, TravStack& stk,
-                                            int& sp, int& node) {
-    if (!m) return false;
-    uint32_t k[8];
-#pragma unroll
-    for (int c = 0; c < 8; ++c) k[c] = (m & (1u << c)) ? ((__float_as_uint(tn[c]) & ~7u) | (uint32_t)c) : 0xffffffffu;
-#if RT_W8_FULL_SORT
-    cswap(k[0], k[1]); cswap(k[2], k[3]); cswap(k[4], k[5]); cswap(k[6], k[7]);
-    cswap(k[0], k[2]); cswap(k[1], k[3]); cswap(k[4], k[6]); cswap(k[5], k[7]);
-    cswap(k[1], k[2]); cswap(k[5], k[6]);
-    cswap(k[0], k[4]); cswap(k[1], k[5]); cswap(k[2], k[6]); cswap(k[3], k[7]);
-    cswap(k[2], k[4]); cswap(k[3], k[5]);
-    cswap(k[1], k[2]); cswap(k[3], k[4]); cswap(k[5], k[6]);
-#else
-    // nearest first, the second nearest next; the rest in slot order
-    cswap(k[0], k[1]); cswap(k[2], k[3]); cswap(k[4], k[5]); cswap(k[6], k[7]);
-    cswap(k[0], k[2]); cswap(k[4], k[6]); cswap(k[0], k[4]);     // k[0] = min
-    cswap(k[1], k[2]); cswap(k[5], k[6]); cswap(k[1], k[5]);     // k[1] = min of the losers of k[0]'s path
-    cswap(k[3], k[7]); cswap(k[1], k[3]);
-#endif
-    const int nh = __popc(m);
-    const int parent = node;
-#pragma unroll
-    for (int i = 7; i >= 1; --i)
-        if (i < nh) stk.set(sp + nh - 1 - i, child8(nodes, parent, k[i] & 7u));
-    sp += nh - 1;
-    node = child8(nodes, parent, k[0] & 7u);
-    return true;
-}
-
-__device__ __forceinline__ bool plain_push8(unsigned m, const float4* __restrict__ nodes, TravStack& stk, int& sp, int& node) {
-    if (!m) return false;
-    const int parent = node;
-    const uint32_t c0 = __ffs(m) - 1;
-    m &= m - 1;
-    while (m) {
-        const uint32_t c = __ffs(m) - 1;
-        m &= m - 1;
-        stk.set(sp++, child8(nodes, parent, c));
-    }
-    node = child8(nodes, parent, c0);
-    return true;
-}
-
 
 // ---------------------------------------------------------------- NEXT-4: kd-tree ablation
 // Stack traversal of the host-built kd-tree (rt_kdtree.cu): front-to-back cells, each split
@@ -650,11 +350,9 @@ __device__ __forceinline__ bool kd_trace(const DevScene& S, float3 o, float3 d, 
     }
 }
 
-// Nearest hit over the 4-wide BVH (or every BVH primitive when BRUTE) and the planes.
-// Acceptance: t > t_min and (t, gid) lexicographically smallest (reading 9).
-// Children are visited near-to-far: entry distances (>= 0, so their bit patterns order like
-// unsigned ints) carry the child slot in their 2 low bits and go through a 5-exchange sorting
-// network; the 3 farther hits are pushed on the shared-memory stack.
+// Nearest hit over the 4-wide BVH (or every BVH primitive when BRUTE, the kd-tree when KD) and
+// the planes.  Acceptance: t > t_min and (t, gid) lexicographically smallest (
+// reading 9).  Children are visited near-to-far (order_push_top).
 template <bool COUNT, int ACC>
 __device__ __forceinline__ Hit closest_hit(const DevScene& S, float3 o, float3 d, TravStack& stk, Counters<COUNT>& cnt) {
     constexpr bool BRUTE = ACC == ACC_BRUTE;
@@ -688,43 +386,24 @@ __device__ __forceinline__ Hit closest_hit(const DevScene& S, float3 o, float3 d
         leaf_test(0, S.n_bvh - 1);
         return h;
     }
-    RayBox rb = make_raybox(o, d, S.bound);
-    set_node_bases(rb, S.nodes);
+    const RayBox rb = make_raybox(o, d, S.bound);
     int sp = 0;
     int node = S.root;
-    int top = 0;          // cached top stack entry (RT_TOP_REG)
+    int top = 0;          // cached top stack entry
     while (true) {
-        cnt.step();
         if (node >= 0) {
             cnt.add(CNT_NODE_VISITS);
-#if RT_BVH_WIDTH == 8
-            float tn[8];
-            const unsigned m = node8_hits(S.nodes, node, rb, h.t, tn);
-            if (order_push8(m, tn, S.nodes, stk, sp, node)) continue;
-#else
             float tn[4];
             int4 ch;
             const unsigned m = node4_hits(S.nodes, node, rb, h.t, tn, ch);
-#if RT_TOP_REG && RT_CLOSEST_SORT
+            count_boxes(cnt, ch);
             if (order_push_top(m, tn, ch, stk, sp, top, node)) continue;
-#elif RT_CLOSEST_SORT
-            if (order_push(m, tn, ch, stk, sp, node)) continue;
-#else
-            if (plain_push(m, ch, stk, sp, node)) continue;
-#endif
-#endif
         } else {
             const int enc = ~node;
             const int first = enc & ((1 << LEAF_SHIFT) - 1);
             leaf_test(first, first + (enc >> LEAF_SHIFT));
         }
-#if RT_TOP_REG && RT_BVH_WIDTH == 4 && RT_CLOSEST_SORT
         if (!pop_top(stk, sp, top, node)) return h;
-#else
-        if (sp == 0) return h;
-        --sp;
-        node = stk.get(sp);
-#endif
     }
 }
 
@@ -743,14 +422,12 @@ __device__ __forceinline__ bool occluded(const DevScene& S, float3 o, float3 d, 
     }
     if (S.n_bvh == 0) return false;
     if (BRUTE) hint = nullptr;
-#if RT_OCC_CACHE
     if (hint) {
         const int k = *hint;
         float t;
         int gid;
         if (k >= 0 && prim_t<COUNT>(S, k, o, d, t, gid, cnt) && t < dist) return true;
     }
-#endif
     if constexpr (ACC == ACC_KD) {
         Hit h;
         h.t = dist; h.gid = -1; h.slot = 0;
@@ -761,233 +438,32 @@ __device__ __forceinline__ bool occluded(const DevScene& S, float3 o, float3 d, 
             float t;
             int gid;
             if (prim_t<COUNT>(S, k, o, d, t, gid, cnt) && t < dist) {
-#if RT_OCC_CACHE
                 if (hint) *hint = k;
-#endif
                 return true;
             }
         }
         return false;
     };
     if (BRUTE) return leaf_test(0, S.n_bvh - 1);
-    RayBox rb = make_raybox(o, d, S.bound);
-    set_node_bases(rb, S.nodes);
+    const RayBox rb = make_raybox(o, d, S.bound);
     int sp = 0;
     int node = S.root;
-    int top = 0;          // cached top stack entry (RT_TOP_REG)
+    int top = 0;          // cached top stack entry
     while (true) {
-        cnt.step();
         if (node >= 0) {
             cnt.add(CNT_NODE_VISITS);
-#if RT_BVH_WIDTH == 8
-            float tn[8];
-            const unsigned m = node8_hits(S.nodes, node, rb, dist, tn);
-            if (plain_push8(m, S.nodes, stk, sp, node)) continue;
-#else
             float tn[4];
             int4 ch;
             const unsigned m = node4_hits(S.nodes, node, rb, dist, tn, ch);
-#if RT_SHADOW_SORT == 2
-            if (m) {   // far-first: entry distances mirrored (0x7effffff - bits; misses stay last)
-#pragma unroll
-                for (int c = 0; c < 4; ++c) tn[c] = __int_as_float(0x7effffff - __float_as_int(tn[c]));
-            }
-            if (order_push(m, tn, ch, stk, sp, node)) continue;
-#elif RT_SHADOW_SORT
-            if (order_push(m, tn, ch, stk, sp, node)) continue;
-#elif RT_TOP_REG
+            count_boxes(cnt, ch);
             if (plain_push_top(m, ch, stk, sp, top, node)) continue;
-#else
-            if (plain_push(m, ch, stk, sp, node)) continue;
-#endif
-#endif
         } else {
             const int enc = ~node;
             const int first = enc & ((1 << LEAF_SHIFT) - 1);
             if (leaf_test(first, first + (enc >> LEAF_SHIFT))) return true;
         }
-#if RT_TOP_REG && RT_BVH_WIDTH == 4 && !RT_SHADOW_SORT
         if (!pop_top(stk, sp, top, node)) return false;
-#else
-        if (sp == 0) return false;
-        --sp;
-        node = stk.get(sp);
-#endif
     }
 }
-
-#if RT_PACKET
-// ---------------------------------------------------------------- warp packets
-// Coherent rays (a warp's 8x4 block of primary rays, and their shadow rays towards one point
-// light) traverse the BVH as one packet: the warp walks a single, warp-uniform node sequence --
-// the depth-first union of the nodes its rays need -- each lane box-testing its own ray against
-// the node's 4 children, and a child is entered when any lane hits it (its own t_best / segment
-// end as the far limit, so every ray still sees every node its single-ray traversal would:
-// results stay identical to brute force).  Node and primitive addresses are uniform, so each
-// fetch is one broadcast L1 transaction, and no lane idles on another lane's loop count or
-// node/leaf branch.  The price is box tests of nodes some rays do not need.
-
-// Warp-uniform stack of a packet in the warp's own slice of the per-thread shared stack
-// ([entry][thread] layout: entry e -> row e >> 5, column 32 w + (e & 31)), idle while a packet
-// runs.  Every lane writes the same value to the same word (one broadcast store) and reads back
-// its own write; each iteration that pushes passes a warp-synchronous vote first, so no lane can
-// overwrite an entry another lane has still to read.
-struct WarpStack {
-    uint32_t sa;   // shared address of (row 0, column 32 w)
-    __device__ __forceinline__ explicit WarpStack(const TravStack& t) : sa(t.sa - 4u * (threadIdx.x & 31u)) {}
-    __device__ __forceinline__ uint32_t addr(int e) const {
-        return sa + (uint32_t)(((e >> 5) * RT_BLOCK + (e & 31)) * 4);
-    }
-    __device__ __forceinline__ void set(int e, int v) const {
-        asm volatile("st.shared.b32 [%0], %1;" ::"r"(addr(e)), "r"(v));
-    }
-    __device__ __forceinline__ int get(int e) const {
-        int v;
-        asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(addr(e)));
-        return v;
-    }
-};
-
-// Nearest hit of every lane in `mask` (all of them must call; each with its own ray).  The union
-// of hit children is visited in the near-to-far order of the lowest lane that hit any of them.
-template <bool COUNT>
-__device__ __forceinline__ Hit closest_hit_packet(const DevScene& S, float3 o, float3 d, unsigned mask,
-                                                  const TravStack& stk, Counters<COUNT>& cnt) {
-    Hit h;
-    h.t = __int_as_float(0x7f800000);
-    h.gid = -1;
-    h.slot = 0;
-    for (int i = 0; i < S.n_planes; ++i) {
-        cnt.add(CNT_PLANE_TESTS);
-        float t;
-        if (plane_intersect(o, d, __ldg(&S.planes[i]), t) && t > T_MIN) {
-            const int gid = S.n_spheres + i;
-            if (t < h.t || (t == h.t && gid < h.gid)) { h.t = t; h.gid = gid; h.slot = ~i; }
-        }
-    }
-    if (S.n_bvh == 0) return h;
-    const RayBox rb = make_raybox(o, d, S.bound);
-    const WarpStack ws(stk);
-    int sp = 0;
-    int node = S.root;
-    while (true) {
-        cnt.step();
-        if (node >= 0) {
-            cnt.add(CNT_NODE_VISITS);
-            float tn[4];
-            int4 ch;
-            const unsigned m = node4_hits(S.nodes, node, rb, h.t, tn, ch);
-            const unsigned hb = __ballot_sync(mask, m != 0u);
-            if (hb) {
-                const unsigned U = __reduce_or_sync(mask, m);
-                // this lane's near-to-far order of all 4 slots (missed slots last, in slot order)
-                uint32_t k0 = (m & 1) ? ((__float_as_uint(tn[0]) & ~3u) | 0u) : 0xfffffffcu;
-                uint32_t k1 = (m & 2) ? ((__float_as_uint(tn[1]) & ~3u) | 1u) : 0xfffffffdu;
-                uint32_t k2 = (m & 4) ? ((__float_as_uint(tn[2]) & ~3u) | 2u) : 0xfffffffeu;
-                uint32_t k3 = (m & 8) ? ((__float_as_uint(tn[3]) & ~3u) | 3u) : 0xffffffffu;
-                cswap(k0, k1); cswap(k2, k3); cswap(k0, k2); cswap(k1, k3); cswap(k1, k2);
-                const uint32_t ord = __shfl_sync(mask, (k0 & 3u) | (k1 & 3u) << 2 | (k2 & 3u) << 4 | (k3 & 3u) << 6,
-                                                 __ffs(hb) - 1);
-                uint32_t lst = 0;
-                int n = 0;
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const uint32_t s = (ord >> (2 * i)) & 3u;
-                    if ((U >> s) & 1u) { lst |= s << (2 * n); ++n; }
-                }
-                for (int i = n - 1; i >= 1; --i) ws.set(sp++, pick4(ch, (lst >> (2 * i)) & 3u));
-                node = pick4(ch, lst & 3u);
-                continue;
-            }
-        } else {
-            const int enc = ~node;
-            const int first = enc & ((1 << LEAF_SHIFT) - 1);
-            const int last = first + (enc >> LEAF_SHIFT);
-            for (int k = first; k <= last; ++k) {
-                float t;
-                int gid;
-                if (prim_t<COUNT>(S, k, o, d, t, gid, cnt) && (t < h.t || (t == h.t && gid < h.gid))) {
-                    h.t = t; h.gid = gid; h.slot = k;
-                }
-            }
-        }
-        if (sp == 0) return h;
-        --sp;
-        node = ws.get(sp);
-    }
-}
-
-// Any hit (t_min < t < dist) for the lanes of `mask` with `need` set; every lane of `mask` must
-// call.  A lane drops out of the box tests (far limit -1) once its segment is blocked; the packet
-// ends when no lane is left or the union is exhausted.  Children are pushed in slot order.
-template <bool COUNT>
-__device__ __forceinline__ bool occluded_packet(const DevScene& S, float3 o, float3 d, float dist, bool need, unsigned mask,
-                                                const TravStack& stk, Counters<COUNT>& cnt, int* hint) {
-    bool occ = false;
-    if (need) {
-        for (int i = 0; i < S.n_planes; ++i) {
-            cnt.add(CNT_PLANE_TESTS);
-            float t;
-            if (plane_intersect(o, d, __ldg(&S.planes[i]), t) && t > T_MIN && t < dist) { occ = true; break; }
-        }
-#if RT_OCC_CACHE
-        if (!occ && hint && S.n_bvh) {
-            const int k = *hint;
-            float t;
-            int gid;
-            if (k >= 0 && prim_t<COUNT>(S, k, o, d, t, gid, cnt) && t < dist) occ = true;
-        }
-#endif
-    }
-    bool alive = need && !occ;
-    if (S.n_bvh == 0 || !__any_sync(mask, alive)) return occ;
-    const RayBox rb = make_raybox(o, d, S.bound);
-    const WarpStack ws(stk);
-    int sp = 0;
-    int node = S.root;
-    while (true) {
-        if (node >= 0) {
-            if (alive) cnt.add(CNT_NODE_VISITS);
-            float tn[4];
-            int4 ch;
-            const unsigned m = node4_hits(S.nodes, node, rb, alive ? dist : -1.0f, tn, ch);
-            const unsigned U = __reduce_or_sync(mask, m);
-            if (U) {
-                const uint32_t c0 = __ffs(U) - 1;
-                unsigned r = U & (U - 1);
-                while (r) {
-                    const uint32_t c = __ffs(r) - 1;
-                    r &= r - 1;
-                    ws.set(sp++, pick4(ch, c));
-                }
-                node = pick4(ch, c0);
-                continue;
-            }
-        } else {
-            if (alive) {
-                const int enc = ~node;
-                const int first = enc & ((1 << LEAF_SHIFT) - 1);
-                const int last = first + (enc >> LEAF_SHIFT);
-                for (int k = first; k <= last; ++k) {
-                    float t;
-                    int gid;
-                    if (prim_t<COUNT>(S, k, o, d, t, gid, cnt) && t < dist) {
-#if RT_OCC_CACHE
-                        if (hint) *hint = k;
-#endif
-                        alive = false;
-                        occ = true;
-                        break;
-                    }
-                }
-            }
-            if (!__any_sync(mask, alive)) return occ;
-        }
-        if (sp == 0) return occ;
-        --sp;
-        node = ws.get(sp);
-    }
-}
-#endif  // RT_PACKET
 
 }  // namespace rtb

@@ -19,11 +19,11 @@ RT_OK, RT_ERR_INVALID_ARG, RT_ERR_CUDA, RT_ERR_OOM, RT_ERR_NO_SCENE, RT_ERR_NO_C
     RT_ERR_NOT_READY, RT_ERR_PEER = range(9)
 RT_FORMAT_RGBA8, RT_FORMAT_RGBA16F = 0, 1
 RT_RENDER_COUNT, RT_RENDER_BRUTE_FORCE, RT_RENDER_PEER_STORE, RT_RENDER_KDTREE = 1, 2, 4, 8
-RT_NUM_COUNTERS = 12
+RT_NUM_COUNTERS = 13
 RT_COMPOSE_ANAGLYPH, RT_COMPOSE_SBS = 0, 1
 RT_TILE = 16
 COUNTER_NAMES = ["primary", "reflection", "refraction", "shadow", "node_visits", "tri_tests", "sphere_tests",
-                 "plane_tests", "shade_hits", "light_evals", "misses", "pixels"]
+                 "plane_tests", "shade_hits", "light_evals", "misses", "pixels", "box_tests"]
 
 # Every symbol include/rt_b200.h declares (checked by tests/test_abi.py).
 EXPORTED = ["rt_create", "rt_destroy", "rt_synchronize", "rt_last_error", "rt_version", "rt_scene_upload",
@@ -31,7 +31,7 @@ EXPORTED = ["rt_create", "rt_destroy", "rt_synchronize", "rt_last_error", "rt_ve
             "rt_host_alloc", "rt_host_free", "rt_upload", "rt_shard_tiles", "rt_shard_bytes", "rt_unpack_shards_host",
             "rt_unpack_shards", "rt_ipc_get_handle", "rt_ipc_open", "rt_ipc_close", "rt_scene_info", "rt_bvh_export",
             "rt_bench_ffma", "rt_compose", "rt_scene_update_vertices", "rt_bvh_width", "rt_kdtree_build",
-            "rt_render_stereo_async", "rt_download_after"]
+            "rt_render_stereo_async", "rt_download_after", "rt_bench_ceilings"]
 
 
 class RtError(RuntimeError):
@@ -110,6 +110,7 @@ def lib():
             "rt_compose": [vp, rt_fb, rt_fb, u32, u32, u32, rt_fb],
             "rt_scene_update_vertices": [vp, vp, u32],
             "rt_kdtree_build": [vp, u32, u32, vp],
+            "rt_bench_ceilings": [vp, vp],
         }
         for name, args in sig.items():
             fn = getattr(L, name)
@@ -344,6 +345,17 @@ def rt_bench_ffma(ctx, iters=2048):
     tf, ms = C.c_double(), C.c_double()
     _check(lib().rt_bench_ffma(ctx, iters, C.byref(tf), C.byref(ms)))
     return tf.value, ms.value
+
+
+CEILING_NAMES = ["ffma_flop_clk_sm", "ffma2_flop_clk_sm", "fmnmx_clk_sm", "fmnmx3_clk_sm", "l1_bytes_clk_sm",
+                 "smem_bytes_clk_sm", "sm_mhz"]
+
+
+def rt_bench_ceilings(ctx):
+    """B0 machine ceilings per SM per clock (see rt_b200.h) -> dict"""
+    a = np.zeros(len(CEILING_NAMES), np.float64)
+    _check(lib().rt_bench_ceilings(ctx, a.ctypes.data))
+    return dict(zip(CEILING_NAMES, (float(x) for x in a)))
 
 
 # ---------------------------------------------------------------- convenience wrapper (torch memory)

@@ -22,9 +22,10 @@ def test_cpu_baseline_fields():
 
 
 def test_algorithmic_flops_constants():
-    """SURVEY §8(d) frozen per-unit constants (BVH4 node visit = 4 box tests = 48)."""
+    """SURVEY §8(d) frozen per-unit constants: a slab test of a real child box = 12 flops; node
+    visits themselves carry no flops (their empty slots are layout, not work)."""
     b = _bench()
     c = {k: 0 for k in ("primary", "reflection", "refraction", "shadow", "node_visits", "tri_tests", "sphere_tests",
-                        "plane_tests", "shade_hits", "light_evals", "misses", "pixels")}
-    c.update(primary=1, node_visits=1)
-    assert b.algorithmic_flops(c) == 20 + 3 + 48
+                        "plane_tests", "shade_hits", "light_evals", "misses", "pixels", "box_tests")}
+    c.update(primary=1, node_visits=1, box_tests=3)
+    assert b.algorithmic_flops(c) == 20 + 3 + 3 * 12
