@@ -46,6 +46,8 @@ class OracleEps(C.Structure):
                 ("eps_abs", C.c_double), ("perturb", C.c_double), ("perturb_tol", C.c_double)]
 
 
+CAND_K = 8          # near-tie candidate IDs kept per ID-fragile pixel
+
 DEFAULT_EPS = dict(eps_t=1e-4, eps_sphere=1e-4, eps_edge=1e-5, eps_abs=1e-5, perturb=1e-6, perturb_tol=1e-3)
 
 _lib = None
@@ -77,8 +79,17 @@ def lib():
         L.oracle_half_bits.restype = C.c_uint16
         L.oracle_render.argtypes = [C.POINTER(OracleScene), C.POINTER(OracleCam), C.c_int32, C.c_int64,
                                     C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
-                                    C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(OracleEps), C.c_int32]
+                                    C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(OracleEps), C.c_int32,
+                                    C.c_void_p, C.c_int32, C.c_void_p]
         L.oracle_render.restype = C.c_int
+        L.oracle_trace_ray_ex.argtypes = [C.POINTER(OracleScene), dp, dp, C.c_int32, C.POINTER(OracleEps), dp,
+                                          C.POINTER(C.c_longlong), C.POINTER(C.c_uint32)]
+        L.oracle_trace_ray_ex.restype = None
+        L.oracle_ray_flags.argtypes = [C.POINTER(OracleScene), dp, dp, C.c_int32, C.c_double, C.POINTER(OracleEps), dp]
+        L.oracle_ray_flags.restype = C.c_uint32
+        L.oracle_ray_candidates.argtypes = [C.POINTER(OracleScene), dp, dp, C.POINTER(OracleEps), C.c_void_p,
+                                            C.c_int32]
+        L.oracle_ray_candidates.restype = C.c_int32
         L.oracle_version.restype = C.c_int
         for fn in (L.oracle_compose_anaglyph, L.oracle_compose_sbs):
             fn.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]
@@ -167,6 +178,41 @@ class Oracle:
         self.L.oracle_trace_ray(C.byref(self.st), _dptr(o), _dptr(d), depth, _dptr(rgb), cnt)
         return rgb, np.array(list(cnt), np.int64)
 
+    @staticmethod
+    def _eps(eps):
+        return OracleEps(**{**DEFAULT_EPS, **(eps or {})})
+
+    def trace_ray_ex(self, o, d, depth, eps=None):
+        """One ray with the fragility analysis: (unclamped rgb, counts, tree flags)."""
+        o = np.ascontiguousarray(o, np.float64)
+        d = np.ascontiguousarray(d, np.float64)
+        rgb = np.zeros(3)
+        cnt = (C.c_longlong * 4)()
+        fl = C.c_uint32()
+        e = self._eps(eps)
+        self.L.oracle_trace_ray_ex(C.byref(self.st), _dptr(o), _dptr(d), depth, C.byref(e), _dptr(rgb), cnt,
+                                   C.byref(fl))
+        return rgb, np.array(list(cnt), np.int64), fl.value
+
+    def ray_flags(self, o, d, kind="nearest", dist=0.0, eps=None):
+        """Fragility flags of one nearest (F1-F5) or shadow (over (t_min, dist)) query -> (flags, margin)."""
+        o = np.ascontiguousarray(o, np.float64)
+        d = np.ascontiguousarray(d, np.float64)
+        mg = C.c_double(0.0)
+        e = self._eps(eps)
+        f = self.L.oracle_ray_flags(C.byref(self.st), _dptr(o), _dptr(d), 0 if kind == "nearest" else 1, float(dist),
+                                    C.byref(e), C.byref(mg))
+        return int(f), mg.value
+
+    def ray_candidates(self, o, d, eps=None, kmax=CAND_K):
+        """Near-tie candidate IDs of the nearest query along (o, d) (-1 = miss) -> (sorted list, count)."""
+        o = np.ascontiguousarray(o, np.float64)
+        d = np.ascontiguousarray(d, np.float64)
+        buf = np.full(kmax, -2, np.int32)
+        e = self._eps(eps)
+        n = self.L.oracle_ray_candidates(C.byref(self.st), _dptr(o), _dptr(d), C.byref(e), buf.ctypes.data, kmax)
+        return sorted(int(x) for x in buf[:min(n, kmax)]), int(n)
+
     def render(self, rig=None, width=None, height=None, max_depth=None, pixels=None, eps=None,
                flags=True, threads=0):
         """Render both eyes (pixels=None) or a list of (eye, px, py) triples.
@@ -193,21 +239,25 @@ class Oracle:
         tf = np.zeros(n, np.uint32)
         mg = np.zeros(n)
         cnt = np.zeros(4, np.int64)
+        cand = np.full((n, CAND_K), -2, np.int32)
+        ncand = np.zeros(n, np.int32)
         e = None
         if flags:
-            e = OracleEps(**{**DEFAULT_EPS, **(eps or {})})
+            e = self._eps(eps)
         rc = self.L.oracle_render(C.byref(self.st), C.byref(cam), max_depth, n,
                                   None if pix is None else pix.ctypes.data,
                                   rad.ctypes.data, q8.ctypes.data, h16.ctypes.data, ids.ctypes.data,
                                   pf.ctypes.data, tf.ctypes.data, mg.ctypes.data, cnt.ctypes.data,
-                                  None if e is None else C.byref(e), int(threads))
+                                  None if e is None else C.byref(e), int(threads),
+                                  cand.ctypes.data if flags else None, CAND_K, ncand.ctypes.data if flags else None)
         if rc != 0:
             raise ValueError("oracle_render failed")
-        out = dict(radiance=rad, rgba8=q8, rgba16=h16, id=ids, pflags=pf, tflags=tf, margin=mg, counts=cnt)
+        out = dict(radiance=rad, rgba8=q8, rgba16=h16, id=ids, pflags=pf, tflags=tf, margin=mg, counts=cnt,
+                   cand=cand, ncand=ncand)
         if pixels is None:
-            for k in ("radiance", "rgba8", "rgba16"):
+            for k in ("radiance", "rgba8", "rgba16", "cand"):
                 out[k] = out[k].reshape(2, height, width, -1)
-            for k in ("id", "pflags", "tflags", "margin"):
+            for k in ("id", "pflags", "tflags", "margin", "ncand"):
                 out[k] = out[k].reshape(2, height, width)
         return out
 

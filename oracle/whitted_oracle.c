@@ -403,6 +403,106 @@ static unsigned shadow_fragility(const oracle_scene* sc, v3 o, v3 d, double dist
     return fl;
 }
 
+/* ---------------------------------------------------------- near-tie candidates
+ * R#22: the IDs a nearest query may legitimately return when its ray is turned by up
+ * to the exclusion band, instead of excluding an ID-fragile pixel from the ID check altogether.
+ * A primitive is a candidate if the band-widened ray meets it no farther than the nearest
+ * primitive the band-widened ray meets robustly (whole band inside it), +eps_t relative:
+ *   sphere   : closest-approach distance D <= r + eps_sphere*tc (robust: D <= r - eps_sphere*tc,
+ *              or the origin inside the sphere); its t is the entry root (or tc when D > r);
+ *   plane    : hit (robust unless grazing, |n.d| <= eps_t);
+ *   triangle : the ray/plane point within b = eps_edge*t/max(|n.d|, eps_t) of the triangle (an
+ *              angular turn a moves the point by a*t/|n.d| in the plane; robust: inside and more
+ *              than b from every edge).
+ * A robust hit at t_r bounds the candidates at t_r (1 + eps_t + eps_edge tan(theta_r)): the turn
+ * moves the robust surface's own t by up to eps_edge tan(theta_r) relative (theta_r = its angle
+ * of incidence), and eps_t is the competing-hit band of F1.
+ * Candidates must lie beyond t_min - band_abs; one within band_abs of t_min is never robust (F5).
+ * -1 (miss) is a candidate when nothing is hit robustly.  Returns the candidate count; the IDs
+ * (ascending, -1 last) go to cand[0..min(count, kmax)). */
+static int ray_candidates(const oracle_scene* sc, v3 o, v3 d, const oracle_eps* eps, int32_t* cand, int kmax)
+{
+    int n = n_prims(sc), nc = 0;
+    double ab = abs_band(o, eps);
+    double tlim = INFINITY;
+    int robust_any = 0;
+    /* pass 1: the nearest robust hit bounds the candidates */
+    for (int pass = 0; pass < 2; ++pass) {
+        for (int i = 0; i < n; ++i) {
+            double t = 0.0, tan_th = 0.0;
+            int hit = 0, robust = 0;
+            if (i < sc->n_spheres) {
+                const double* sp = sc->spheres + 4 * i;
+                v3 oc = sub(o, ld3(sp));
+                double r = sp[3];
+                if (dot(oc, oc) <= r * r) {                       /* origin inside: exit root */
+                    double t0, t1;
+                    if (sphere_roots(o, d, sp, &t0, &t1)) { t = t1; hit = 1; robust = 1; }
+                } else {
+                    double tc = -dot(oc, d);
+                    if (tc > 0.0) {
+                        double D = len(add(oc, scl(d, tc)));
+                        if (D <= r + eps->eps_sphere * tc) {
+                            hit = 1;
+                            robust = D <= r - eps->eps_sphere * tc;
+                            t = tc;
+                            double t0, t1;
+                            if (D <= r && sphere_roots(o, d, sp, &t0, &t1)) t = t0;
+                        }
+                    }
+                }
+            } else if (i < sc->n_spheres + sc->n_planes) {
+                const double* pl = sc->planes + 4 * (i - sc->n_spheres);
+                if (plane_t(o, d, pl, &t)) {
+                    double cosn = fabs(dot(nrm(ld3(pl)), d));
+                    hit = 1;
+                    robust = cosn > eps->eps_t;
+                    tan_th = robust ? sqrt(1.0 - cosn * cosn) / cosn : 0.0;
+                }
+            } else {
+                v3 v0, v1, v2;
+                tri_verts(sc, i - sc->n_spheres - sc->n_planes, &v0, &v1, &v2);
+                v3 nn = cross(sub(v1, v0), sub(v2, v0));
+                double den = dot(nn, d);
+                if (den != 0.0) {
+                    t = dot(nn, sub(v0, o)) / den;
+                    double cosn = fabs(den) / len(nn);
+                    double b = eps->eps_edge * fabs(t) / (cosn > eps->eps_t ? cosn : eps->eps_t);
+                    v3 q = add(o, scl(d, t));
+                    double e = seg_dist(q, v0, v1), e2 = seg_dist(q, v1, v2), e3 = seg_dist(q, v2, v0);
+                    if (e2 < e) e = e2;
+                    if (e3 < e) e = e3;
+                    /* inside test of q in the triangle's plane (same-side of every edge) */
+                    double s0 = dot(cross(sub(v1, v0), sub(q, v0)), nn);
+                    double s1 = dot(cross(sub(v2, v1), sub(q, v1)), nn);
+                    double s2 = dot(cross(sub(v0, v2), sub(q, v2)), nn);
+                    int inside = s0 >= 0.0 && s1 >= 0.0 && s2 >= 0.0;
+                    hit = inside || e <= b;
+                    robust = inside && e > b && cosn > eps->eps_t;
+                    tan_th = robust ? sqrt(1.0 - cosn * cosn) / cosn : 0.0;
+                }
+            }
+            if (!hit || t <= T_MIN - ab) continue;
+            if (fabs(t - T_MIN) <= ab) robust = 0;                 /* F5: the t_min decision */
+            if (pass == 0) {
+                if (robust) {
+                    double lim = t * (1.0 + eps->eps_t + eps->eps_edge * tan_th);
+                    robust_any = 1;
+                    if (lim < tlim) tlim = lim;
+                }
+            } else if (t <= tlim) {
+                if (nc < kmax) cand[nc] = i;
+                ++nc;
+            }
+        }
+    }
+    if (!robust_any) {
+        if (nc < kmax) cand[nc] = -1;
+        ++nc;
+    }
+    return nc;
+}
+
 /* ------------------------------------------------------------------ trace */
 typedef struct {
     const oracle_scene* sc;
@@ -502,6 +602,48 @@ void oracle_trace_ray(const oracle_scene* sc, const double o[3], const double d[
     }
 }
 
+/* Trace one ray with the fragility analysis on (pins of F1-F6 and the shadow flags): rgb =
+ * unclamped radiance, *flags = union of the flags of every ray of the tree (R#22). */
+void oracle_trace_ray_ex(const oracle_scene* sc, const double o[3], const double d[3], int32_t depth,
+                         const oracle_eps* eps, double rgb[3], long long counts[4], uint32_t* flags)
+{
+    trace_ctx cx;
+    memset(&cx, 0, sizeof cx);
+    cx.sc = sc;
+    cx.eps = eps;
+    v3 c = trace(&cx, ld3(o), nrm(ld3(d)), depth, 0, NULL, NULL, NULL);
+    rgb[0] = c.x; rgb[1] = c.y; rgb[2] = c.z;
+    if (counts) {
+        counts[0] = cx.cnt.primary; counts[1] = cx.cnt.reflection;
+        counts[2] = cx.cnt.refraction; counts[3] = cx.cnt.shadow;
+    }
+    if (flags) *flags = cx.flags;
+}
+
+/* Fragility of ONE query (pins of the classifier):
+ *   kind 0: nearest-hit query along (o, d) -> F1-F5 flags of its answer (+ min boundary margin)
+ *   kind 1: shadow (any-hit) query over (t_min, dist) -> FRAG_SHADOW or 0 */
+uint32_t oracle_ray_flags(const oracle_scene* sc, const double o3[3], const double d3[3], int32_t kind,
+                          double dist, const oracle_eps* eps, double* margin)
+{
+    v3 o = ld3(o3), d = nrm(ld3(d3));
+    if (kind == 1) return shadow_fragility(sc, o, d, dist, eps);
+    double dn[3] = {d.x, d.y, d.z}, t;
+    int32_t id;
+    oracle_nearest(sc, o3, dn, &t, &id);
+    double mg = INFINITY;
+    uint32_t f = nearest_fragility(sc, o, d, t, id, eps, &mg);
+    if (margin) *margin = mg;
+    return f;
+}
+
+/* Near-tie candidate IDs of the nearest query along (o, d) (see ray_candidates). */
+int32_t oracle_ray_candidates(const oracle_scene* sc, const double o3[3], const double d3[3],
+                              const oracle_eps* eps, int32_t* cand, int32_t kmax)
+{
+    return ray_candidates(sc, ld3(o3), nrm(ld3(d3)), eps, cand, kmax);
+}
+
 /* byte = clamp(round(c*255)), round half away from zero (= floor(x+0.5), x>=0). */
 static uint8_t q8(double c)
 {
@@ -541,12 +683,16 @@ uint16_t oracle_half_bits(double c)
  *   margin    : n min relative boundary distance seen by the primary ray (may be NULL)
  *   counts    : 4 totals (primary, reflection, refraction, shadow)     (may be NULL)
  *   eps       : fragility thresholds, NULL -> no fragility analysis
+ *   cand      : n*cand_k near-tie candidate IDs of the primary ray, only for pixels with an
+ *               ID-fragile primary (F1-F5); padding -2                 (may be NULL; needs eps)
+ *   ncand     : n candidate counts (0 for ID-robust pixels)            (may be NULL)
  */
 int oracle_render(const oracle_scene* sc, const oracle_cam* cam, int32_t max_depth,
                   int64_t n_pix, const int32_t* pix,
                   double* radiance, uint8_t* rgba8, uint16_t* rgba16, int32_t* prim_id,
                   uint32_t* pflags, uint32_t* tflags, double* margin,
-                  long long* counts, const oracle_eps* eps, int32_t n_threads)
+                  long long* counts, const oracle_eps* eps, int32_t n_threads,
+                  int32_t* cand, int32_t cand_k, int32_t* ncand)
 {
     int64_t n = pix ? n_pix : 2LL * cam->width * cam->height;
     long long c0 = 0, c1 = 0, c2 = 0, c3 = 0;
@@ -606,6 +752,13 @@ int oracle_render(const oracle_scene* sc, const oracle_cam* cam, int32_t max_dep
         if (rgba16) {
             rgba16[4 * k] = oracle_half_bits(c.x); rgba16[4 * k + 1] = oracle_half_bits(c.y);
             rgba16[4 * k + 2] = oracle_half_bits(c.z); rgba16[4 * k + 3] = 0x3C00;
+        }
+        if (cand && cand_k > 0) {
+            for (int q = 0; q < cand_k; ++q) cand[k * cand_k + q] = -2;
+            int32_t nc = 0;
+            if (eps && (pf & (FRAG_COMPETE | FRAG_BOUNDARY | FRAG_GRAZE | FRAG_RANGE)))
+                nc = ray_candidates(sc, ld3(o), ld3(d), eps, cand + k * cand_k, cand_k);
+            if (ncand) ncand[k] = nc;
         }
         if (prim_id) prim_id[k] = id;
         if (pflags) pflags[k] = pf;

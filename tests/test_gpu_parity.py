@@ -112,18 +112,25 @@ def sampled_parity(R, s, n_per_eye, seed, label):
 
 
 def test_c3_full_sampled(R):
-    sampled_parity(R, scenes.scene_c3(), 400, 11, "C3 1080p sampled")
+    """BASELINE.json configs[2] at full size (1080p stereo, 10k tris + 100 spheres, depth 4):
+    32 768 seeded pixels per eye (1/64 of the frame; 1/8 of it in the committed report,
+    scripts/parity_report.py)."""
+    sampled_parity(R, scenes.scene_c3(), 32768, 11, "C3 1080p sampled")
 
 
 @pytest.mark.slow
 def test_c4_full_sampled(R):
-    sampled_parity(R, scenes.scene_c4(), 48, 12, "C4 1080p sampled")
+    """The headline config (configs[3]: 1080p stereo, 1M triangles, depth 4) in bench's launch
+    configuration: 2048 seeded pixels per eye."""
+    sampled_parity(R, scenes.scene_c4(), 2048, 12, "C4 1080p sampled")
 
 
 @pytest.mark.slow
 def test_c5_frames_sampled(R):
-    for f in (0, 30):
-        sampled_parity(R, scenes.scene_c5(frame=f), 16, 13 + f, f"C5 4K frame {f} sampled")
+    """configs[4] (4K stereo, 1M triangles, depth 6, camera orbit): the first, middle and last
+    orbit frames, 512 seeded pixels per eye each."""
+    for f in (0, 30, 59):
+        sampled_parity(R, scenes.scene_c5(frame=f), 512, 13 + f, f"C5 4K frame {f} sampled")
 
 
 def test_bvh_equals_bruteforce(R):
