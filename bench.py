@@ -6,8 +6,9 @@
 
 One "step" = one stereo frame of the whole hot path: primary rays,
 LBVH traversal + intersection, shading with shadow rays, reflection/refraction to max_depth,
-pack to RGBA8, and for N>1 the assembly of every rank's tiles in rank 0's framebuffers (fused
-peer stores over NVLink by default, or NCCL gather + root unpack with --gather nccl).
+pack to RGBA8, and for N>1 the assembly of every rank's tiles in rank 0's framebuffers inside
+the library (rt_dist_init: fused peer stores over NVLink by default, or NCCL gather + root
+unpack with --gather nccl).
 The scene (upload + LBVH build, a1-a2) is resident before the timed region; its cost is
 reported separately as scene_upload_ms.  Two timed regions: one frame at a time (latency and
 the kernel's own duration, L2 flushed before each frame outside the events) and the throughput
@@ -67,12 +68,6 @@ def algorithmic_flops(c):
 def workload_desc(s):
     return (f"{s.name}: {s.width}x{s.height} per eye stereo pair, {s.n_tris} triangles + {s.n_spheres} spheres + "
             f"{s.n_planes} planes via LBVH, {len(s.lights)} point lights, depth {s.max_depth}")
-
-
-def gather_to_root(dist, shard_buf, gathered, world, rank, per):
-    """a7 (nccl path), see paper_1702_01530_b200/multigpu.py."""
-    from paper_1702_01530_b200.multigpu import gather_to_root as g
-    g(dist, shard_buf, gathered, world, rank, per)
 
 
 # ------------------------------------------------------------------------------ clocks
@@ -214,47 +209,6 @@ def run_reference(args, scene):
 
 
 # ------------------------------------------------------------------------------ GPU leg
-class SingleFrame:
-    """N = 1: the whole stereo frame straight into the framebuffers."""
-
-    mode = "single"
-    launches_per_frame = 1
-    pipelined = True
-
-    def __init__(self, R, fb, width, height):
-        self.R, self.fb, self.W, self.H = R, fb, width, height
-
-    def render(self, depth, stream=None):
-        self.R.render(self.W, self.H, depth, fb=self.fb, stream=stream)
-
-    def assemble(self):
-        pass
-
-    def close(self):
-        pass
-
-
-def frame_sync(dist, world, share, dev):
-    """Cross-rank synchronisation point of the frames-in-flight loops: returns once every rank
-    has reached it, without waiting on any render stream.  NCCL: a one-element all-reduce on an
-    otherwise idle stream, waited for by the host (tens of microseconds over NVLink; a gloo
-    barrier costs 0.5-1.8 ms per call at 2-8 local ranks, more than a frame).  Share-device test
-    mode (gloo process group): dist.barrier."""
-    if world == 1:
-        return None
-    if share:
-        return dist.barrier
-    import torch
-    st = torch.cuda.Stream(device=dev)
-    flag = torch.zeros(1, dtype=torch.int32, device=dev)
-
-    def sync():
-        with torch.cuda.stream(st):
-            dist.all_reduce(flag, async_op=True).wait()
-        st.synchronize()
-    return sync
-
-
 def run_ours(args, scene):
     import torch
     import torch.distributed as dist
@@ -302,22 +256,22 @@ def run_ours(args, scene):
     rays_total = tot["primary"] + tot["reflection"] + tot["refraction"] + tot["shadow"]
     my_flops = algorithmic_flops(cnt)
 
-    # ---- frame assembly (a7): direct (N=1), fused peer stores or NCCL gather (N>1)
-    fb = R.alloc_fb(W, H)                                    # root framebuffers (2, H, W, 4) u8
-    frame = SingleFrame(R, fb, W, H) if world == 1 else multigpu.make_frame(args.gather, R, fb, rank, world, dist, W, H)
+    # ---- frame assembly (a7) inside the library for N>1: every rank joins the world (Python only
+    # broadcasts the job id); a frame render then traces this rank's tiles and rank 0's
+    # framebuffers receive the whole frame (peer stores over NVLink, or NCCL gather + unpack)
+    dist_info = multigpu.join_world(R, rank, world, dist, args.gather) if world > 1 else \
+        {"rank": 0, "world": 1, "transport": "none"}
     flush_bytes = l2_flush_bytes(dev)
     flush = torch.empty(flush_bytes // 4, dtype=torch.float32, device=dev)
-    # frames in flight: F framebuffer slots (each its own peer mapping for N>1) and F streams
-    F = max(1, args.inflight) if frame.pipelined else 1
-    fbs = [fb] + [R.alloc_fb(W, H) for _ in range(F - 1)]
-    frames = [frame] + [SingleFrame(R, fbs[i], W, H) if world == 1
-                        else multigpu.make_frame(frame.mode, R, fbs[i], rank, world, dist, W, H) for i in range(1, F)]
+    # frames in flight: F framebuffer slots on rank 0 and F streams per rank
+    F = max(1, args.inflight)
+    fbs = [R.alloc_fb(W, H) if rank == 0 else None for _ in range(F)]
+    frames = [multigpu.Frame(R, fbs[i], W, H) for i in range(F)]
+    frame = frames[0]
     streams = [torch.cuda.Stream(device=dev) for _ in range(F)]
-    hb = frame_sync(dist, world, share, dev)                 # cross-rank "frame done" point, N>1
 
     for _ in range(max(3, args.warmup)):
         frame.render(D)
-        frame.assemble()
     torch.cuda.synchronize()
     barrier()
 
@@ -333,9 +287,8 @@ def run_ours(args, scene):
     for k in range(args.steps):
         flush.zero_()                                          # L2 flush between timed steps (untimed)
         ev_s[k].record()
-        frame.render(D)
+        frame.render(D)                                        # N>1, rank 0: + the wait for every rank
         ev_k[k].record()
-        frame.assemble()
         ev_e[k].record()
     torch.cuda.synchronize()
     barrier()
@@ -351,37 +304,27 @@ def run_ours(args, scene):
     # L2 flush (1.25x L2 write) enqueued before every frame on its own stream and timed with it
     # (it overlaps the other frames, so it cannot be left out).  A frame's pixel trees end in a
     # latency-bound tail (the deepest trees: ~0.7 ms for C4 even on an idle GPU);
-    # frames in flight fill the SMs that tail would leave idle.  For N>1 a rank starts frame k
-    # only after every rank finished frame k-F+1 (frame_sync, lagging so the device
-    # always has queued frames): the slot frame k overwrites is then fully assembled.  The
-    # synchronisation point is an NCCL all-reduce the host waits for (frame_sync).
+    # frames in flight fill the SMs that tail would leave idle.  For N>1 the library orders the
+    # frames across ranks on the device (rank 0 posts "slot free" before a frame, the other ranks
+    # wait for it and post their completion; rank 0's stream waits for every post), so the host
+    # just enqueues.
     if F > 1:
-        lag = F - 1
-
-        def pipe_step(k, done):
+        def pipe_step(k):
             slot = k % F
-            if world > 1 and k >= lag:
-                done.pop(k - lag).synchronize()
-                hb()
             with torch.cuda.stream(streams[slot]):
                 flush.zero_()
             frames[slot].render(D, streams[slot])
-            e = torch.cuda.Event()
-            e.record(streams[slot])
-            done[k] = e
 
-        done = {}
         for k in range(max(3, args.warmup)):
-            pipe_step(k, done)
+            pipe_step(k)
         torch.cuda.synchronize()
         barrier()
-        done = {}
         t_start = torch.cuda.Event(enable_timing=True)
         t_start.record()
         for x in streams:
             x.wait_event(t_start)
         for k in range(args.steps):
-            pipe_step(k, done)
+            pipe_step(k)
         t_end = []
         for x in streams:
             e = torch.cuda.Event(enable_timing=True)
@@ -400,7 +343,7 @@ def run_ours(args, scene):
     ms_per_step = total_ms / args.steps
 
     # ---- end-to-end through the public C ABI with host buffers (camera in, frame out)
-    e2e = run_e2e(args, R, scene, rank, world, frames, fbs, streams, hb, dev, rays_total) if not args.no_e2e else None
+    e2e = run_e2e(args, R, scene, rank, world, frames, fbs, streams, dev, rays_total) if not args.no_e2e else None
 
     # ---- machine ceilings measured live (B0): FFMA / FFMA2 / FMNMX rates and the
     # L1 / shared-memory bandwidth per SM per clock (rt_bench_ceilings), and the FFMA peak
@@ -419,8 +362,10 @@ def run_ours(args, scene):
         achieved_inflight = my_flops / (ms_per_step * 1e-3) / 1e12
         traffic = load_traffic(scene.name, world)
         prof = load_profile(scene.name, world)
-        par = f"tile-sharded x{world}" + {"single": "", "peer": " + fused peer-store gather to rank 0 (CUDA IPC over NVLink)",
-                                          "nccl": " + NCCL gather to rank 0 + unpack"}[frame.mode]
+        par = f"tile-sharded x{world}" + {"none": "", "peer": " + fused peer-store assembly on rank 0 inside the library "
+                                                              "(rt_dist_init: CUDA IPC over NVLink, device-side flags)",
+                                          "nccl": " + NCCL gather to rank 0 + unpack inside the library (rt_dist_init)"}[
+            dist_info["transport"]]
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True,
@@ -429,7 +374,8 @@ def run_ours(args, scene):
             "config": {"workload": workload_desc(scene), "width": W, "height": H, "max_depth": D,
                        "triangles": scene.n_tris, "rays_per_step": rays_total,
                        "rays_by_type": {k: tot[k] for k in ("primary", "reflection", "refraction", "shadow")},
-                       "parallelism": par, "gather": frame.mode, "frames_in_flight": F,
+                       "parallelism": par, "gather": dist_info["transport"] if world > 1 else "single",
+                       "frames_in_flight": F,
                        "l2": (f"flushed ({flush_bytes >> 20} MiB write, 1.25x L2) before every timed frame, on the "
                               "frame's stream and inside the timed region" if F > 1
                               else f"flushed ({flush_bytes >> 20} MiB write) between timed steps")
@@ -461,7 +407,9 @@ def run_ours(args, scene):
                          "ceilings_b0": ceil,
                          **l1_roofline(prof, ceil, kernel_ms, sm_max)},
             "clocks": clocks,
-            "gpu_launches": args.steps * frame.launches_per_frame,   # in the throughput region
+            # our kernels per frame in the throughput region: the trace kernel; N>1 on rank 0 also
+            # the slot post and the completion wait (peer transport) or the unpack (NCCL)
+            "gpu_launches": args.steps * (1 if world == 1 else (3 if dist_info["transport"] == "peer" else 2)),
             "paper_context": {"hardware": "'a video graphics card NVIDIA', model unstated (PAPER.md:66)",
                               "timings": "no Mrays/s or frames/s published; 'few milliseconds' per frame for scenes of "
                                          "1-6 small polyhedra and one light (PAPER.md:104); ~60 % compute / up to 40 % "
@@ -472,7 +420,7 @@ def run_ours(args, scene):
         }
         if e2e is not None:
             line["e2e"] = e2e
-        if not args.no_cpu_baseline:
+        if not args.no_cpu_baseline and world == 1:
             # the GPU's full frame (untimed, ids + radiance), compared with the oracle on the
             # baseline's own sample
             g = R.render(W, H, D, want_id=True, want_radiance=True)
@@ -480,23 +428,22 @@ def run_ours(args, scene):
             gpu = {k: v.cpu().numpy() for k, v in g.items()}
             line["cpu_baseline"] = cpu_baseline(scene, target_s=args.cpu_seconds, gpu=gpu)
         print(json.dumps(line), flush=True)
-    for f in frames:
-        f.close()
     if world > 1:
+        rt.rt_dist_finalize(R.ctx)
         dist.barrier()
         dist.destroy_process_group()
     R.close()
     return 0
 
 
-def run_e2e(args, R, scene, rank, world, frames, fbs, streams, hb, dev, rays_total):
+def run_e2e(args, R, scene, rank, world, frames, fbs, streams, dev, rays_total):
     """Same metric through the public C ABI: every step sets the camera from host values
-    (rt_set_stereo_camera), renders (+ assembles on rank 0 for N>1) and downloads the finished
-    stereo frame into pinned host memory (rt_download_after, copy stream, overlapped with the
-    frames still rendering).  With F frames in flight each frame renders on its slot's stream
-    into its slot's framebuffers; a slot is re-rendered only after its previous download
-    completed (and, for N>1, after every rank finished the frame a lag of F-1 frames back, by a
-    cross-rank sync point (frame_sync) that never waits on a render stream)."""
+    (rt_set_stereo_camera), renders (for N>1 the library assembles the frame on rank 0) and rank 0
+    downloads the finished stereo frame into pinned host memory (rt_download_after on the copy
+    stream, ordered after the frame's stream -- after the completion wait for every rank --
+    and overlapped with the frames still rendering).  With F frames in flight each frame renders
+    on its slot's stream into its slot's framebuffers; rank 0 re-renders a slot only after the
+    slot's previous download completed (host wait), which the other ranks follow on the device."""
     import ctypes
 
     import torch
@@ -528,50 +475,22 @@ def run_e2e(args, R, scene, rank, world, frames, fbs, streams, hb, dev, rays_tot
     if world > 1:
         import torch.distributed as dist
     pending = [None] * F
-    done = {}
-    lag = F - 1
-
-    def finish(j):
-        """frame j is complete on every rank: rank 0 downloads it"""
-        slot = j % F
-        if world > 1 and F > 1:
-            done.pop(j).synchronize()
-            hb()
-        else:
-            done.pop(j, None)
-        if rank == 0:
-            pending[slot] = rt.rt_download_after(R.ctx, fbs[slot].data_ptr(), hosts[slot], nbytes,
-                                                 streams[slot].cuda_stream if F > 1 else None)
 
     def frame_step(k):
         slot = k % F
         if rank == 0 and pending[slot] is not None:
             rt.rt_wait(pending[slot])                          # the slot's previous frame is on the host
             pending[slot] = None
-        if world > 1:
-            if F > 1:
-                if k >= lag:
-                    finish(k - lag)
-            else:
-                dist.barrier()                                 # ... before any rank writes the slot again
         rig = rigs[k % n_rig]
         rt.rt_set_stereo_camera(R.ctx, rig.eye, rig.look_at, rig.up, rig.vfov_deg, rig.interocular,
                                 rig.convergence)
-        if F > 1:
-            frames[slot].render(D, streams[slot])
-            e = torch.cuda.Event()
-            e.record(streams[slot])
-            done[k] = e
-        else:
-            frames[slot].render(D)
-            frames[slot].assemble()
-            done[k] = None
-        if world == 1 or F == 1:
-            finish(k)
+        st = streams[slot] if F > 1 else None
+        frames[slot].render(D, st)
+        if rank == 0:
+            pending[slot] = rt.rt_download_after(R.ctx, fbs[slot].data_ptr(), hosts[slot], nbytes,
+                                                 st.cuda_stream if st is not None else None)
 
     def drain():
-        for j in sorted(done):
-            finish(j)
         for i in range(F):
             if pending[i] is not None:
                 rt.rt_wait(pending[i])
@@ -589,6 +508,7 @@ def run_e2e(args, R, scene, rank, world, frames, fbs, streams, hb, dev, rays_tot
         frame_step(k)
     drain()
     rt.rt_synchronize(R.ctx)
+    torch.cuda.synchronize()
     dt = time.perf_counter() - t0
     tt = torch.tensor([dt], dtype=torch.float64, device=dev)
     if world > 1:

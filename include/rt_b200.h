@@ -257,6 +257,55 @@ rt_status rt_unpack_shards_host(const void* gathered, uint32_t width, uint32_t h
 rt_status rt_unpack_shards(rt_context* ctx, const void* gathered, uint32_t width, uint32_t height,
                            uint32_t world, uint32_t format, rt_fb left, rt_fb right);
 
+/* ------------------------------------------------------------------ multi-GPU frames */
+/* PAPER.md:48 (§3, Fig. 1: "dividing the picture to N identical parts", one processor each) and
+ * PAPER.md:56 (§3, Fig. 2: level 1 = the left/right channels); SURVEY.md §8(b), §8(e).
+ * One process per GPU of ONE node, each with its own context holding the same scene and camera.
+ * After rt_dist_init, every rt_render_stereo / _ex / _async call whose params ask for the whole
+ * frame (shard_world == 1) renders this rank's tiles of that frame (the rt_shard_tiles map: world
+ * 2 = one eye per rank) and the library assembles the frame in RANK 0's out_left / out_right:
+ *   RT_DIST_PEER (default): the other ranks map rank 0's framebuffers (CUDA IPC; NVLink P2P) and
+ *     their pack epilogues store each finished pixel straight into them.  Ordering is on the
+ *     device: rank 0's stream posts that the frame's framebuffers are free before its own tiles,
+ *     each other rank's stream waits for that post, renders, and posts its completion into rank
+ *     0's memory; rank 0's stream waits for every post, so work enqueued after the render on
+ *     rank 0's stream (e.g. rt_download_after) sees the whole frame.  No gather, no unpack.
+ *   RT_DIST_NCCL: every rank packs its tiles, NCCL gathers the shards on rank 0 (libnccl.so.2,
+ *     loaded at run time), rank 0 unpacks them into its framebuffers.  Chosen automatically if
+ *     any rank cannot map rank 0's memory; requires one GPU per rank.
+ * Contract: every rank issues the same sequence of frame renders (same size, depth and format);
+ * frames are matched by their position in that sequence, up to 16 in flight.  On ranks != 0 the
+ * out_* framebuffers are ignored (NULL allowed) except their format under RT_DIST_NCCL; ID /
+ * radiance / shard planes are rejected (render an explicit shard, shard_world > 1, which stays a
+ * local render of those tiles).  Rank 0's framebuffers must stay allocated until the frame's work
+ * on rank 0's stream completes.  Device-side waits are bounded (env RT_DIST_TIMEOUT_S, default
+ * 60 s): a rank that never posts makes later calls fail with RT_ERR_PEER, not a hung GPU. */
+#define RT_DIST_ID_BYTES 128
+#define RT_DIST_PEER 0u          /* fused peer-store assembly (default)                     */
+#define RT_DIST_NCCL 1u          /* NCCL gather of packed shards + root unpack              */
+/* A 128-byte job id for rt_dist_init, created once (by rank 0) and handed to every rank by the
+ * caller (e.g. a torch.distributed broadcast).  It is an NCCL unique id when libnccl.so.2 loads
+ * (the NCCL transport's communicator), otherwise random bytes; it also names the job's host
+ * rendezvous (POSIX shared memory /rtb200_<hash>).  id: HOST buffer of RT_DIST_ID_BYTES. */
+rt_status rt_dist_unique_id(void* id);
+/* Join rank `rank` of `world` ranks (collective: blocks until every rank joined, bounded by the
+ * timeout).  flags: RT_DIST_PEER or RT_DIST_NCCL (rank 0's choice wins).
+ * Errors: RT_ERR_INVALID_ARG (rank/world, already joined), RT_ERR_PEER (rendezvous, NCCL),
+ * RT_ERR_CUDA. */
+rt_status rt_dist_init(rt_context* ctx, int rank, int world, const void* id, uint32_t flags);
+/* Leave the world (collective): waits for this rank's device work, releases the peer mappings,
+ * the device flags and the rendezvous.  Reports RT_ERR_PEER if a frame timed out. */
+rt_status rt_dist_finalize(rt_context* ctx);
+/* info[0] rank, [1] world (1 without rt_dist_init), [2] transport (RT_DIST_*; -1 none),
+ * [3] frames rendered in the world. */
+rt_status rt_dist_info(rt_context* ctx, int32_t info[4]);
+/* Test support, no device work: runs the host half of the protocol -- the shared-memory
+ * rendezvous of rt_dist_init, `frames` synthetic frame descriptors through the 16-slot ring
+ * (rank 0 publishing, the others reading, flow-controlled), and the leave of rt_dist_finalize --
+ * and returns a checksum of the descriptors this rank published or read (equal on every rank iff
+ * every rank saw every frame in order).  Errors: RT_ERR_INVALID_ARG, RT_ERR_PEER (timeout). */
+rt_status rt_dist_host_selftest(int rank, int world, const void* id, uint32_t frames, uint64_t* checksum);
+
 /* ------------------------------------------------------------------ peer memory (fused gather) */
 /* CUDA IPC: export the DEVICE allocation containing dev_ptr as a 64-byte handle plus the byte
  * offset of dev_ptr inside that allocation (allocations from caching allocators such as

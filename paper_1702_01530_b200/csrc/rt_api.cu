@@ -17,25 +17,13 @@
 #include <string>
 #include <vector>
 
-#include <nvtx3/nvToolsExt.h>
-
-#include "../../include/rt_b200.h"
-#include "rt_internal.h"
+#include "rt_context.h"
 
 namespace {
-
 thread_local std::string g_err;
+}  // namespace
 
-// NVTX range over a C-ABI call (SURVEY §5 tracing): visible in Nsight Systems timelines, free
-// when no tool is attached (NVTX3 is header-only)
-struct NvtxRange {
-    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
-    ~NvtxRange() { nvtxRangePop(); }
-    NvtxRange(const NvtxRange&) = delete;
-    NvtxRange& operator=(const NvtxRange&) = delete;
-};
-
-rt_status fail(rt_status s, const char* fmt, ...) {
+rt_status rtb_fail(rt_status s, const char* fmt, ...) {
     char buf[1024];
     va_list ap;
     va_start(ap, fmt);
@@ -44,88 +32,6 @@ rt_status fail(rt_status s, const char* fmt, ...) {
     g_err = buf;
     return s;
 }
-
-#define CUDA_TRY(call)                                                                           \
-    do {                                                                                         \
-        cudaError_t e_ = (call);                                                                 \
-        if (e_ != cudaSuccess) {                                                                 \
-            if (e_ == cudaErrorMemoryAllocation)                                                 \
-                return fail(RT_ERR_OOM, "%s: %s", #call, cudaGetErrorString(e_));                \
-            return fail(RT_ERR_CUDA, "%s: %s", #call, cudaGetErrorString(e_));                   \
-        }                                                                                        \
-    } while (0)
-
-constexpr int RENDER_SLOTS = 16;
-
-struct DevBuf {
-    void* p = nullptr;
-    size_t bytes = 0;
-    void release() {
-        if (p) cudaFree(p);
-        p = nullptr;
-        bytes = 0;
-    }
-};
-
-}  // namespace
-
-struct rt_event {
-    cudaEvent_t ev = nullptr;
-};
-
-struct rt_context {
-    int device = 0;
-    cudaStream_t stream = nullptr;
-    bool own_stream = false;
-    cudaStream_t copy_stream = nullptr;
-    cudaEvent_t order_ev = nullptr;
-    int num_sms = 148;
-    int* work_counter = nullptr;    // [64]: 16 rotating render queues, 4 ints apart
-    unsigned render_seq = 0;
-    // completion event of the last render that used each work-queue slot: a render that reuses a
-    // slot waits for it on the device (cudaStreamWaitEvent), and scene changes wait for all of them
-    cudaEvent_t slot_ev[RENDER_SLOTS] = {};
-    bool slot_used[RENDER_SLOTS] = {};
-    // pinned staging of rt_scene_upload / rt_scene_update_vertices (grow-only)
-    void* staging = nullptr;
-    size_t staging_bytes = 0;
-    unsigned long long* scratch_counters = nullptr;
-    float* ffma_out = nullptr;
-    // scene
-    bool has_scene = false;
-    std::vector<DevBuf> scene_bufs;
-    rtb::DevScene sc{};
-    uint64_t info[8] = {0};
-    // camera
-    bool has_camera = false;
-    double cam_eye[2][3], cam_f[3], cam_r[3], cam_u[3], cam_th, cam_sigma_unit;
-    float vfov = 0;
-    int leaf_max = 1;                // LBVH leaf collapse threshold (env RT_LEAF_MAX, <= 16)
-    int treelet_passes = 3;          // SAH treelet restructuring passes (env RT_TREELETS)
-    int sah_subtrees = 1;            // SAH rebuild of small LBVH subtrees (env RT_SAH_SUBTREES=0: off)
-    int grid_limit = 0;              // cap on trace CTAs (env RT_GRID_LIMIT; 0 = full machine)
-    int l2_prefetch = 0;             // bulk L2 prefetch of the scene at each render (env RT_L2_PREFETCH=1,
-                                     // 2 = nodes only; measured no gain, +40 % DRAM reads)
-    void* arena = nullptr;           // BVH build scratch (grow-only)
-    size_t arena_bytes = 0;
-    // refit state (rt_scene_update_vertices)
-    int* d_prim_orig = nullptr;
-    float* d_vertices = nullptr;
-    uint32_t* d_tri = nullptr;
-    float4* d_spheres = nullptr;
-    uint32_t n_vertices = 0;
-    std::vector<int> level_start;
-    std::vector<uint32_t> h_tri;
-    double sphere_bound = 0.0;
-    struct IpcMap {
-        std::string key;            // the 64-byte cudaIpcMemHandle_t
-        void* ptr;
-        int refs;
-    };
-    std::vector<IpcMap> ipc_maps;    // peer allocations mapped by rt_ipc_open (reference counted)
-    // NEXT-4 kd-tree ablation (rt_kdtree_build)
-    DevBuf kd_nodes_buf, kd_refs_buf;
-};
 
 namespace {
 
@@ -136,7 +42,7 @@ rt_status dalloc(rt_context* c, size_t count, T** out) {
     DevBuf b;
     b.bytes = count * sizeof(T);
     cudaError_t e = cudaMalloc(&b.p, b.bytes);
-    if (e != cudaSuccess) return fail(RT_ERR_OOM, "cudaMalloc(%zu bytes): %s", b.bytes, cudaGetErrorString(e));
+    if (e != cudaSuccess) return rtb_fail(RT_ERR_OOM, "cudaMalloc(%zu bytes): %s", b.bytes, cudaGetErrorString(e));
     c->scene_bufs.push_back(b);
     *out = static_cast<T*>(b.p);
     return RT_OK;
@@ -183,7 +89,7 @@ struct Stager {
         const cudaError_t e = cudaHostAlloc(&c->staging, need, cudaHostAllocPortable);
         if (e != cudaSuccess) {
             c->staging = nullptr;
-            return fail(RT_ERR_OOM, "pinned staging cudaHostAlloc(%zu): %s", need, cudaGetErrorString(e));
+            return rtb_fail(RT_ERR_OOM, "pinned staging cudaHostAlloc(%zu): %s", need, cudaGetErrorString(e));
         }
         c->staging_bytes = need;
         return RT_OK;
@@ -208,19 +114,18 @@ int rt_bvh_width(void) { return rtb::BVH_W; }
 const char* rt_last_error(void) { return g_err.c_str(); }
 
 rt_status rt_create(int device, void* cuda_stream, rt_context** out) {
-    if (!out) return fail(RT_ERR_INVALID_ARG, "rt_create: out is NULL");
+    if (!out) return rtb_fail(RT_ERR_INVALID_ARG, "rt_create: out is NULL");
     *out = nullptr;
     int ndev = 0;
     CUDA_TRY(cudaGetDeviceCount(&ndev));
-    if (device < 0 || device >= ndev) return fail(RT_ERR_INVALID_ARG, "rt_create: device %d of %d", device, ndev);
+    if (device < 0 || device >= ndev) return rtb_fail(RT_ERR_INVALID_ARG, "rt_create: device %d of %d", device, ndev);
     rt_context* c = new (std::nothrow) rt_context();
-    if (!c) return fail(RT_ERR_OOM, "rt_create: host allocation");
+    if (!c) return rtb_fail(RT_ERR_OOM, "rt_create: host allocation");
     c->device = device;
     if (const char* lm = getenv("RT_LEAF_MAX")) c->leaf_max = std::max(1, std::min(16, atoi(lm)));
     if (const char* tp = getenv("RT_TREELETS")) c->treelet_passes = std::max(0, std::min(8, atoi(tp)));
     if (const char* ss = getenv("RT_SAH_SUBTREES")) c->sah_subtrees = atoi(ss) != 0;
     if (const char* gl = getenv("RT_GRID_LIMIT")) c->grid_limit = std::max(0, atoi(gl));
-    if (const char* lp = getenv("RT_L2_PREFETCH")) c->l2_prefetch = atoi(lp);
     cudaError_t e = cudaSetDevice(device);
     if (e == cudaSuccess && cuda_stream) {
         c->stream = static_cast<cudaStream_t>(cuda_stream);
@@ -238,7 +143,7 @@ rt_status rt_create(int device, void* cuda_stream, rt_context** out) {
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
     if (e != cudaSuccess) {
         rt_destroy(c);
-        return fail(RT_ERR_CUDA, "rt_create: %s", cudaGetErrorString(e));
+        return rtb_fail(RT_ERR_CUDA, "rt_create: %s", cudaGetErrorString(e));
     }
     *out = c;
     return RT_OK;
@@ -248,6 +153,7 @@ rt_status rt_destroy(rt_context* c) {
     if (!c) return RT_OK;
     cudaSetDevice(c->device);
     wait_renders(c);
+    rtb_dist_destroy(c);
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
     free_scene(c);
@@ -268,7 +174,7 @@ rt_status rt_destroy(rt_context* c) {
 }
 
 rt_status rt_synchronize(rt_context* c) {
-    if (!c) return fail(RT_ERR_INVALID_ARG, "rt_synchronize: NULL context");
+    if (!c) return rtb_fail(RT_ERR_INVALID_ARG, "rt_synchronize: NULL context");
     CUDA_TRY(cudaSetDevice(c->device));
     CUDA_TRY(cudaStreamSynchronize(c->stream));
     CUDA_TRY(cudaStreamSynchronize(c->copy_stream));
@@ -279,66 +185,66 @@ rt_status rt_synchronize(rt_context* c) {
 rt_status rt_scene_upload(rt_context* c, const rt_primitives* P, const rt_material* mats, uint32_t n_mats,
                           const rt_light* lights, uint32_t n_lights, const rt_env* env) {
     NvtxRange nvtx_("rt_scene_upload");
-    if (!c || !P || !env) return fail(RT_ERR_INVALID_ARG, "rt_scene_upload: NULL context/primitives/env");
+    if (!c || !P || !env) return rtb_fail(RT_ERR_INVALID_ARG, "rt_scene_upload: NULL context/primitives/env");
     if ((n_mats && !mats) || (n_lights && !lights))
-        return fail(RT_ERR_INVALID_ARG, "rt_scene_upload: NULL materials/lights with nonzero count");
+        return rtb_fail(RT_ERR_INVALID_ARG, "rt_scene_upload: NULL materials/lights with nonzero count");
     const uint32_t S = P->n_spheres, PL = P->n_planes, T = P->n_triangles, V = P->n_vertices;
     if ((S && (!P->spheres || !P->sphere_mat)) || (PL && (!P->planes || !P->plane_mat)) ||
         (T && (!P->tri_indices || !P->tri_mat || !P->vertices)))
-        return fail(RT_ERR_INVALID_ARG, "rt_scene_upload: NULL primitive array with nonzero count");
+        return rtb_fail(RT_ERR_INVALID_ARG, "rt_scene_upload: NULL primitive array with nonzero count");
     if ((uint64_t)S + T >= (1ull << rtb::LEAF_SHIFT) || (uint64_t)S + PL + T >= (1ull << 31))
-        return fail(RT_ERR_INVALID_ARG, "rt_scene_upload: too many primitives (%u spheres + %u triangles)", S, T);
+        return rtb_fail(RT_ERR_INVALID_ARG, "rt_scene_upload: too many primitives (%u spheres + %u triangles)", S, T);
     // ---- validation (SPEC.md:76 ValidationError analogue; SPEC.md:111 degenerate faces)
     for (uint32_t i = 0; i < n_mats; ++i) {
         const rt_material& m = mats[i];
         if (!finite3(m.kd) || !finite3(m.ks) || !std::isfinite(m.shininess) || !std::isfinite(m.kr) ||
             !std::isfinite(m.kt) || !std::isfinite(m.ior))
-            return fail(RT_ERR_INVALID_ARG, "material %u: non-finite value", i);
+            return rtb_fail(RT_ERR_INVALID_ARG, "material %u: non-finite value", i);
         for (int k = 0; k < 3; ++k)
-            if (m.kd[k] < 0 || m.ks[k] < 0) return fail(RT_ERR_INVALID_ARG, "material %u: negative kd/ks", i);
-        if (m.shininess < 1.0f) return fail(RT_ERR_INVALID_ARG, "material %u: shininess < 1", i);
+            if (m.kd[k] < 0 || m.ks[k] < 0) return rtb_fail(RT_ERR_INVALID_ARG, "material %u: negative kd/ks", i);
+        if (m.shininess < 1.0f) return rtb_fail(RT_ERR_INVALID_ARG, "material %u: shininess < 1", i);
         if (m.kr < 0 || m.kr > 1 || m.kt < 0 || m.kt > 1 || m.kr + m.kt > 1.0f)
-            return fail(RT_ERR_INVALID_ARG, "material %u: kr/kt outside [0,1] or kr+kt > 1", i);
-        if (!(m.ior > 0)) return fail(RT_ERR_INVALID_ARG, "material %u: ior <= 0", i);
+            return rtb_fail(RT_ERR_INVALID_ARG, "material %u: kr/kt outside [0,1] or kr+kt > 1", i);
+        if (!(m.ior > 0)) return rtb_fail(RT_ERR_INVALID_ARG, "material %u: ior <= 0", i);
     }
     for (uint32_t i = 0; i < n_lights; ++i) {
         if (!finite3(lights[i].pos) || !finite3(lights[i].intensity))
-            return fail(RT_ERR_INVALID_ARG, "light %u: non-finite value", i);
+            return rtb_fail(RT_ERR_INVALID_ARG, "light %u: non-finite value", i);
         for (int k = 0; k < 3; ++k)
-            if (lights[i].intensity[k] < 0) return fail(RT_ERR_INVALID_ARG, "light %u: negative intensity", i);
+            if (lights[i].intensity[k] < 0) return rtb_fail(RT_ERR_INVALID_ARG, "light %u: negative intensity", i);
     }
     if (!finite3(env->ambient) || !finite3(env->background))
-        return fail(RT_ERR_INVALID_ARG, "env: non-finite ambient/background");
+        return rtb_fail(RT_ERR_INVALID_ARG, "env: non-finite ambient/background");
     for (int k = 0; k < 3; ++k)
         if (env->ambient[k] < 0 || env->background[k] < 0)
-            return fail(RT_ERR_INVALID_ARG, "env: negative ambient/background (SPEC.md:35 colours are >= 0)");
+            return rtb_fail(RT_ERR_INVALID_ARG, "env: negative ambient/background (SPEC.md:35 colours are >= 0)");
     double bound = 0.0;
     for (uint32_t i = 0; i < S; ++i) {
         const float* s = P->spheres + 4 * i;
-        if (!finite3(s) || !std::isfinite(s[3])) return fail(RT_ERR_INVALID_ARG, "sphere %u: non-finite value", i);
-        if (!(s[3] > 0)) return fail(RT_ERR_INVALID_ARG, "sphere %u: radius <= 0", i);
-        if (P->sphere_mat[i] >= n_mats) return fail(RT_ERR_INVALID_ARG, "sphere %u: material %u >= %u", i, P->sphere_mat[i], n_mats);
+        if (!finite3(s) || !std::isfinite(s[3])) return rtb_fail(RT_ERR_INVALID_ARG, "sphere %u: non-finite value", i);
+        if (!(s[3] > 0)) return rtb_fail(RT_ERR_INVALID_ARG, "sphere %u: radius <= 0", i);
+        if (P->sphere_mat[i] >= n_mats) return rtb_fail(RT_ERR_INVALID_ARG, "sphere %u: material %u >= %u", i, P->sphere_mat[i], n_mats);
         bound = std::max(bound, std::fabs((double)s[0]) + std::fabs((double)s[1]) + std::fabs((double)s[2]) + 3.0 * s[3]);
     }
     std::vector<float> planes(4 * (size_t)PL);
     for (uint32_t i = 0; i < PL; ++i) {
         const float* p = P->planes + 4 * i;
-        if (!finite3(p) || !std::isfinite(p[3])) return fail(RT_ERR_INVALID_ARG, "plane %u: non-finite value", i);
+        if (!finite3(p) || !std::isfinite(p[3])) return rtb_fail(RT_ERR_INVALID_ARG, "plane %u: non-finite value", i);
         const double n = std::sqrt((double)p[0] * p[0] + (double)p[1] * p[1] + (double)p[2] * p[2]);
-        if (!(n > 0)) return fail(RT_ERR_INVALID_ARG, "plane %u: zero normal", i);
-        if (P->plane_mat[i] >= n_mats) return fail(RT_ERR_INVALID_ARG, "plane %u: material %u >= %u", i, P->plane_mat[i], n_mats);
+        if (!(n > 0)) return rtb_fail(RT_ERR_INVALID_ARG, "plane %u: zero normal", i);
+        if (P->plane_mat[i] >= n_mats) return rtb_fail(RT_ERR_INVALID_ARG, "plane %u: material %u >= %u", i, P->plane_mat[i], n_mats);
         for (int k = 0; k < 4; ++k) planes[4 * i + k] = (float)(p[k] / n);
     }
     if (T) {
         for (uint32_t i = 0; i < V; ++i) {
             const float* v = P->vertices + 3 * i;
-            if (!finite3(v)) return fail(RT_ERR_INVALID_ARG, "vertex %u: non-finite value", i);
+            if (!finite3(v)) return rtb_fail(RT_ERR_INVALID_ARG, "vertex %u: non-finite value", i);
         }
         for (uint32_t j = 0; j < T; ++j) {
             const uint32_t* t = P->tri_indices + 3 * j;
             if (t[0] >= V || t[1] >= V || t[2] >= V)
-                return fail(RT_ERR_INVALID_ARG, "triangle %u: vertex index >= %u", j, V);
-            if (P->tri_mat[j] >= n_mats) return fail(RT_ERR_INVALID_ARG, "triangle %u: material %u >= %u", j, P->tri_mat[j], n_mats);
+                return rtb_fail(RT_ERR_INVALID_ARG, "triangle %u: vertex index >= %u", j, V);
+            if (P->tri_mat[j] >= n_mats) return rtb_fail(RT_ERR_INVALID_ARG, "triangle %u: material %u >= %u", j, P->tri_mat[j], n_mats);
             double lo[3], hi[3], e1[3], e2[3];
             for (int k = 0; k < 3; ++k) {
                 const double a = P->vertices[3 * t[0] + k], b = P->vertices[3 * t[1] + k], cc = P->vertices[3 * t[2] + k];
@@ -353,7 +259,7 @@ rt_status rt_scene_upload(rt_context* c, const rt_primitives* P, const rt_materi
             const double area = 0.5 * std::sqrt(cx * cx + cy * cy + cz * cz);
             const double diag2 = (hi[0] - lo[0]) * (hi[0] - lo[0]) + (hi[1] - lo[1]) * (hi[1] - lo[1]) +
                                  (hi[2] - lo[2]) * (hi[2] - lo[2]);
-            if (!(area > 1e-12 * diag2)) return fail(RT_ERR_INVALID_ARG, "triangle %u: degenerate (area %g)", j, area);
+            if (!(area > 1e-12 * diag2)) return rtb_fail(RT_ERR_INVALID_ARG, "triangle %u: degenerate (area %g)", j, area);
         }
         for (uint32_t i = 0; i < V; ++i) {
             const float* v = P->vertices + 3 * i;
@@ -482,7 +388,7 @@ rt_status rt_scene_upload(rt_context* c, const rt_primitives* P, const rt_materi
             cudaError_t ea = cudaMalloc(&c->arena, arena_off);
             if (ea != cudaSuccess) {
                 free_scene(c);
-                return fail(RT_ERR_OOM, "BVH scratch arena cudaMalloc(%zu): %s", arena_off, cudaGetErrorString(ea));
+                return rtb_fail(RT_ERR_OOM, "BVH scratch arena cudaMalloc(%zu): %s", arena_off, cudaGetErrorString(ea));
             }
             c->arena_bytes = arena_off;
         }
@@ -507,7 +413,7 @@ rt_status rt_scene_upload(rt_context* c, const rt_primitives* P, const rt_materi
         free_scratch();
         if (e != cudaSuccess) {
             free_scene(c);
-            return fail(RT_ERR_CUDA, "LBVH build: %s", cudaGetErrorString(e));
+            return rtb_fail(RT_ERR_CUDA, "LBVH build: %s", cudaGetErrorString(e));
         }
     }
     CUDA_TRY(cudaStreamSynchronize(c->stream));       // the staged copies have landed (N == 0 case)
@@ -560,15 +466,15 @@ rt_status rt_scene_upload(rt_context* c, const rt_primitives* P, const rt_materi
 // ------------------------------------------------------------------------------ refit (NEXT-3)
 rt_status rt_scene_update_vertices(rt_context* c, const float* vertices, uint32_t n_vertices) {
     NvtxRange nvtx_("rt_scene_update_vertices");
-    if (!c || (!vertices && n_vertices)) return fail(RT_ERR_INVALID_ARG, "rt_scene_update_vertices: NULL argument");
-    if (!c->has_scene) return fail(RT_ERR_NO_SCENE, "rt_scene_update_vertices: no scene");
+    if (!c || (!vertices && n_vertices)) return rtb_fail(RT_ERR_INVALID_ARG, "rt_scene_update_vertices: NULL argument");
+    if (!c->has_scene) return rtb_fail(RT_ERR_NO_SCENE, "rt_scene_update_vertices: no scene");
     if (n_vertices != c->n_vertices)
-        return fail(RT_ERR_INVALID_ARG, "rt_scene_update_vertices: %u vertices, scene has %u", n_vertices, c->n_vertices);
+        return rtb_fail(RT_ERR_INVALID_ARG, "rt_scene_update_vertices: %u vertices, scene has %u", n_vertices, c->n_vertices);
     if (n_vertices == 0) return RT_OK;
     double bound = c->sphere_bound;
     for (uint32_t i = 0; i < n_vertices; ++i) {
         const float* v = vertices + 3 * i;
-        if (!finite3(v)) return fail(RT_ERR_INVALID_ARG, "vertex %u: non-finite value", i);
+        if (!finite3(v)) return rtb_fail(RT_ERR_INVALID_ARG, "vertex %u: non-finite value", i);
         bound = std::max(bound, std::fabs((double)v[0]) + std::fabs((double)v[1]) + std::fabs((double)v[2]));
     }
     const size_t T = c->h_tri.size() / 3;
@@ -585,7 +491,7 @@ rt_status rt_scene_update_vertices(rt_context* c, const float* vertices, uint32_
         const double cx = e1[1] * e2[2] - e1[2] * e2[1], cy = e1[2] * e2[0] - e1[0] * e2[2], cz = e1[0] * e2[1] - e1[1] * e2[0];
         const double area = 0.5 * std::sqrt(cx * cx + cy * cy + cz * cz);
         const double diag2 = (hi[0] - lo[0]) * (hi[0] - lo[0]) + (hi[1] - lo[1]) * (hi[1] - lo[1]) + (hi[2] - lo[2]) * (hi[2] - lo[2]);
-        if (!(area > 1e-12 * diag2)) return fail(RT_ERR_INVALID_ARG, "triangle %zu: degenerate after update", j);
+        if (!(area > 1e-12 * diag2)) return rtb_fail(RT_ERR_INVALID_ARG, "triangle %zu: degenerate after update", j);
     }
     CUDA_TRY(cudaSetDevice(c->device));
     CUDA_TRY(wait_renders(c));                     // renders in flight read the nodes the refit rewrites
@@ -608,20 +514,20 @@ rt_status rt_scene_update_vertices(rt_context* c, const float* vertices, uint32_
 // ------------------------------------------------------------------------------ camera
 rt_status rt_set_stereo_camera(rt_context* c, const float eye[3], const float look_at[3], const float up[3],
                                float vfov_deg, float interocular, float convergence) {
-    if (!c || !eye || !look_at || !up) return fail(RT_ERR_INVALID_ARG, "rt_set_stereo_camera: NULL argument");
+    if (!c || !eye || !look_at || !up) return rtb_fail(RT_ERR_INVALID_ARG, "rt_set_stereo_camera: NULL argument");
     if (!finite3(eye) || !finite3(look_at) || !finite3(up) || !std::isfinite(vfov_deg) || !std::isfinite(interocular) ||
         std::isnan(convergence) || convergence == -INFINITY)
-        return fail(RT_ERR_INVALID_ARG, "rt_set_stereo_camera: non-finite input");
-    if (!(vfov_deg > 0.0f && vfov_deg < 180.0f)) return fail(RT_ERR_INVALID_ARG, "vfov %g outside (0,180)", vfov_deg);
-    if (interocular < 0.0f) return fail(RT_ERR_INVALID_ARG, "negative interocular distance");
+        return rtb_fail(RT_ERR_INVALID_ARG, "rt_set_stereo_camera: non-finite input");
+    if (!(vfov_deg > 0.0f && vfov_deg < 180.0f)) return rtb_fail(RT_ERR_INVALID_ARG, "vfov %g outside (0,180)", vfov_deg);
+    if (interocular < 0.0f) return rtb_fail(RT_ERR_INVALID_ARG, "negative interocular distance");
     // SPEC.md:425 (derive_eyes), in double
     double f[3] = {(double)look_at[0] - eye[0], (double)look_at[1] - eye[1], (double)look_at[2] - eye[2]};
     const double fl = std::sqrt(f[0] * f[0] + f[1] * f[1] + f[2] * f[2]);
-    if (!(fl > 0)) return fail(RT_ERR_INVALID_ARG, "eye == look_at");
+    if (!(fl > 0)) return rtb_fail(RT_ERR_INVALID_ARG, "eye == look_at");
     for (double& x : f) x /= fl;
     double r[3] = {f[1] * up[2] - f[2] * up[1], f[2] * up[0] - f[0] * up[2], f[0] * up[1] - f[1] * up[0]};
     const double rl = std::sqrt(r[0] * r[0] + r[1] * r[1] + r[2] * r[2]);
-    if (!(rl > 0)) return fail(RT_ERR_INVALID_ARG, "up is parallel to the view direction");
+    if (!(rl > 0)) return rtb_fail(RT_ERR_INVALID_ARG, "up is parallel to the view direction");
     for (double& x : r) x /= rl;
     const double u[3] = {r[1] * f[2] - r[2] * f[1], r[2] * f[0] - r[0] * f[2], r[0] * f[1] - r[1] * f[0]};
     const double s = interocular;
@@ -686,11 +592,11 @@ uint32_t shard_tile(const ShardGeom& g, uint32_t rank, uint32_t world, uint32_t 
 rt_status check_fb(const rt_fb& fb, uint32_t W, const char* name) {
     if (!fb.dev_ptr) return RT_OK;
     if (fb.format != RT_FORMAT_RGBA8 && fb.format != RT_FORMAT_RGBA16F)
-        return fail(RT_ERR_INVALID_ARG, "%s: unknown format %u", name, fb.format);
+        return rtb_fail(RT_ERR_INVALID_ARG, "%s: unknown format %u", name, fb.format);
     const uint64_t need = (uint64_t)W * (fb.format == RT_FORMAT_RGBA8 ? 4 : 8);
-    if (fb.pitch_bytes < need) return fail(RT_ERR_SIZE, "%s: pitch %llu < %llu", name, (unsigned long long)fb.pitch_bytes, (unsigned long long)need);
+    if (fb.pitch_bytes < need) return rtb_fail(RT_ERR_SIZE, "%s: pitch %llu < %llu", name, (unsigned long long)fb.pitch_bytes, (unsigned long long)need);
     if (fb.pitch_bytes % (fb.format == RT_FORMAT_RGBA8 ? 4 : 8))
-        return fail(RT_ERR_INVALID_ARG, "%s: pitch not a multiple of the pixel size", name);
+        return rtb_fail(RT_ERR_INVALID_ARG, "%s: pitch not a multiple of the pixel size", name);
     return RT_OK;
 }
 
@@ -698,42 +604,42 @@ rt_status check_fb(const rt_fb& fb, uint32_t W, const char* name) {
 
 extern "C" {
 
-namespace {
-rt_status render_impl(rt_context* c, const rt_render_params* p, const rt_outputs* out, cudaStream_t stream);
-}
-
 rt_status rt_render_stereo_ex(rt_context* c, const rt_render_params* p, const rt_outputs* out) {
     NvtxRange nvtx_("rt_render_stereo_ex");
-    if (!c || !p || !out) return fail(RT_ERR_INVALID_ARG, "rt_render_stereo_ex: NULL argument");
-    return render_impl(c, p, out, c->stream);
+    if (!c || !p || !out) return rtb_fail(RT_ERR_INVALID_ARG, "rt_render_stereo_ex: NULL argument");
+    if (c->dist) return rtb_dist_render(c, p, out, c->stream);
+    return rtb_render_local(c, p, out, c->stream);
 }
 
 rt_status rt_render_stereo_async(rt_context* c, const rt_render_params* p, const rt_outputs* out, void* cuda_stream) {
     NvtxRange nvtx_("rt_render_stereo_async");
-    if (!c || !p || !out) return fail(RT_ERR_INVALID_ARG, "rt_render_stereo_async: NULL argument");
-    return render_impl(c, p, out, cuda_stream ? static_cast<cudaStream_t>(cuda_stream) : c->stream);
+    if (!c || !p || !out) return rtb_fail(RT_ERR_INVALID_ARG, "rt_render_stereo_async: NULL argument");
+    cudaStream_t st = cuda_stream ? static_cast<cudaStream_t>(cuda_stream) : c->stream;
+    if (c->dist) return rtb_dist_render(c, p, out, st);
+    return rtb_render_local(c, p, out, st);
 }
 
-namespace {
-rt_status render_impl(rt_context* c, const rt_render_params* p, const rt_outputs* out, cudaStream_t stream) {
-    if (!c->has_scene) return fail(RT_ERR_NO_SCENE, "render before rt_scene_upload");
-    if (!c->has_camera) return fail(RT_ERR_NO_CAMERA, "render before rt_set_stereo_camera");
+}  // extern "C"
+
+rt_status rtb_render_local(rt_context* c, const rt_render_params* p, const rt_outputs* out, cudaStream_t stream) {
+    if (!c->has_scene) return rtb_fail(RT_ERR_NO_SCENE, "render before rt_scene_upload");
+    if (!c->has_camera) return rtb_fail(RT_ERR_NO_CAMERA, "render before rt_set_stereo_camera");
     const uint32_t W = p->width, H = p->height;
-    if (W == 0 || H == 0 || W > 16384 || H > 16384) return fail(RT_ERR_SIZE, "image size %ux%u", W, H);
-    if (p->max_depth > RT_MAX_DEPTH) return fail(RT_ERR_SIZE, "max_depth %u > %d", p->max_depth, RT_MAX_DEPTH);
+    if (W == 0 || H == 0 || W > 16384 || H > 16384) return rtb_fail(RT_ERR_SIZE, "image size %ux%u", W, H);
+    if (p->max_depth > RT_MAX_DEPTH) return rtb_fail(RT_ERR_SIZE, "max_depth %u > %d", p->max_depth, RT_MAX_DEPTH);
     if (p->shard_world == 0 || p->shard_rank >= p->shard_world || p->shard_world > 4096)
-        return fail(RT_ERR_INVALID_ARG, "shard %u of %u", p->shard_rank, p->shard_world);
+        return rtb_fail(RT_ERR_INVALID_ARG, "shard %u of %u", p->shard_rank, p->shard_world);
     if (p->flags & ~(RT_RENDER_COUNT | RT_RENDER_BRUTE_FORCE | RT_RENDER_PEER_STORE | RT_RENDER_KDTREE))
-        return fail(RT_ERR_INVALID_ARG, "unknown flags 0x%x", p->flags);
+        return rtb_fail(RT_ERR_INVALID_ARG, "unknown flags 0x%x", p->flags);
     if ((p->flags & RT_RENDER_KDTREE) && (p->flags & RT_RENDER_BRUTE_FORCE))
-        return fail(RT_ERR_INVALID_ARG, "RT_RENDER_KDTREE and RT_RENDER_BRUTE_FORCE are exclusive");
+        return rtb_fail(RT_ERR_INVALID_ARG, "RT_RENDER_KDTREE and RT_RENDER_BRUTE_FORCE are exclusive");
     if ((p->flags & RT_RENDER_KDTREE) && c->sc.n_bvh > 0 && !c->sc.kd_nodes)
-        return fail(RT_ERR_INVALID_ARG, "RT_RENDER_KDTREE needs rt_kdtree_build after the upload");
-    if ((p->flags & RT_RENDER_COUNT) && !out->counters) return fail(RT_ERR_INVALID_ARG, "RT_RENDER_COUNT needs counters");
+        return rtb_fail(RT_ERR_INVALID_ARG, "RT_RENDER_KDTREE needs rt_kdtree_build after the upload");
+    if ((p->flags & RT_RENDER_COUNT) && !out->counters) return rtb_fail(RT_ERR_INVALID_ARG, "RT_RENDER_COUNT needs counters");
     rt_status st;
     if ((st = check_fb(out->left, W, "out_left")) || (st = check_fb(out->right, W, "out_right"))) return st;
     if (out->shard && out->shard_format != RT_FORMAT_RGBA8 && out->shard_format != RT_FORMAT_RGBA16F)
-        return fail(RT_ERR_INVALID_ARG, "shard: unknown format");
+        return rtb_fail(RT_ERR_INVALID_ARG, "shard: unknown format");
     TraceParams P{};
     P.sc = c->sc;
     fill_camera(c, W, H, P.cam);
@@ -747,7 +653,7 @@ rt_status render_impl(rt_context* c, const rt_render_params* p, const rt_outputs
     P.work_counter = c->work_counter + 4 * slot;
     const ShardGeom g = shard_geom(W, H, p->shard_world);
     const uint64_t n_tiles = shard_count(g, p->shard_rank, p->shard_world);
-    if (n_tiles * 256ull >= (1ull << 31)) return fail(RT_ERR_SIZE, "too many pixels in one shard");
+    if (n_tiles * 256ull >= (1ull << 31)) return rtb_fail(RT_ERR_SIZE, "too many pixels in one shard");
     P.n_work = (int)(n_tiles * 256);
     P.tiles_x = g.tiles_x;
     P.tiles_per_eye = g.tiles_per_eye;
@@ -766,15 +672,8 @@ rt_status render_impl(rt_context* c, const rt_render_params* p, const rt_outputs
     P.shard_fmt = (int)out->shard_format;
     P.counters = out->counters ? out->counters : c->scratch_counters;
     P.stack_entries = (rtb::BVH_W - 1) * (int)c->info[5] + 2;   // <= W-1 pending siblings per level
-    if (P.stack_entries > rtb::STACK_CAP) return fail(RT_ERR_SIZE, "BVH too deep (%d levels)", (int)c->info[5]);
+    if (P.stack_entries > rtb::STACK_CAP) return rtb_fail(RT_ERR_SIZE, "BVH too deep (%d levels)", (int)c->info[5]);
     P.n_tiles = (int)n_tiles;
-    if (c->l2_prefetch && c->sc.n_bvh > 0) {
-        P.pf_base[0] = reinterpret_cast<const char*>(c->sc.nodes);
-        P.pf_bytes[0] = c->sc.nodes ? (unsigned long long)c->info[4] * rtb::NODE_F4 * 16 : 0;
-        P.pf_base[1] = reinterpret_cast<const char*>(c->sc.prims);
-        P.pf_bytes[1] = c->l2_prefetch == 2 ? 0 : (unsigned long long)c->sc.n_bvh * 48;   // 2: nodes only
-        if (!P.pf_base[0]) { P.pf_base[0] = P.pf_base[1]; P.pf_bytes[0] = P.pf_bytes[1]; P.pf_bytes[1] = 0; }
-    }
     P.peer_fence = (p->flags & RT_RENDER_PEER_STORE) ? 1 : 0;
     if (P.n_work == 0) return RT_OK;
     CUDA_TRY(cudaSetDevice(c->device));
@@ -794,7 +693,7 @@ rt_status render_impl(rt_context* c, const rt_render_params* p, const rt_outputs
     ++c->render_seq;
     return RT_OK;
 }
-}  // namespace
+extern "C" {
 
 rt_status rt_render_stereo(rt_context* c, uint32_t width, uint32_t height, uint32_t max_depth, rt_fb out_left,
                            rt_fb out_right) {
@@ -812,11 +711,11 @@ rt_status rt_render_stereo(rt_context* c, uint32_t width, uint32_t height, uint3
 
 // ------------------------------------------------------------------------------ download
 rt_status rt_host_alloc(size_t bytes, void** out) {
-    if (!out || !bytes) return fail(RT_ERR_INVALID_ARG, "rt_host_alloc: NULL out or zero size");
+    if (!out || !bytes) return rtb_fail(RT_ERR_INVALID_ARG, "rt_host_alloc: NULL out or zero size");
     cudaError_t e = cudaHostAlloc(out, bytes, cudaHostAllocPortable);
     if (e != cudaSuccess) {
         *out = nullptr;
-        return fail(RT_ERR_OOM, "cudaHostAlloc(%zu): %s", bytes, cudaGetErrorString(e));
+        return rtb_fail(RT_ERR_OOM, "cudaHostAlloc(%zu): %s", bytes, cudaGetErrorString(e));
     }
     return RT_OK;
 }
@@ -844,21 +743,21 @@ rt_status rt_download_after(rt_context* c, const void* dev_src, void* host_dst, 
                             rt_event** done) {
     NvtxRange nvtx_("rt_download");
     if (done) *done = nullptr;
-    if (!c || !dev_src || !host_dst || !bytes) return fail(RT_ERR_INVALID_ARG, "rt_download: NULL pointer or zero size");
+    if (!c || !dev_src || !host_dst || !bytes) return rtb_fail(RT_ERR_INVALID_ARG, "rt_download: NULL pointer or zero size");
     CUDA_TRY(cudaSetDevice(c->device));
-    if (!is_pinned(host_dst)) return fail(RT_ERR_INVALID_ARG, "rt_download: host_dst is not pinned host memory");
+    if (!is_pinned(host_dst)) return rtb_fail(RT_ERR_INVALID_ARG, "rt_download: host_dst is not pinned host memory");
     CUDA_TRY(cudaEventRecord(c->order_ev, after_stream ? static_cast<cudaStream_t>(after_stream) : c->stream));
     CUDA_TRY(cudaStreamWaitEvent(c->copy_stream, c->order_ev, 0));
     CUDA_TRY(cudaMemcpyAsync(host_dst, dev_src, bytes, cudaMemcpyDeviceToHost, c->copy_stream));
     if (done) {
         rt_event* ev = new (std::nothrow) rt_event();
-        if (!ev) return fail(RT_ERR_OOM, "rt_download: event allocation");
+        if (!ev) return rtb_fail(RT_ERR_OOM, "rt_download: event allocation");
         cudaError_t e = cudaEventCreateWithFlags(&ev->ev, cudaEventDisableTiming);
         if (e == cudaSuccess) e = cudaEventRecord(ev->ev, c->copy_stream);
         if (e != cudaSuccess) {
             if (ev->ev) cudaEventDestroy(ev->ev);
             delete ev;
-            return fail(RT_ERR_CUDA, "rt_download: %s", cudaGetErrorString(e));
+            return rtb_fail(RT_ERR_CUDA, "rt_download: %s", cudaGetErrorString(e));
         }
         *done = ev;
     }
@@ -866,37 +765,37 @@ rt_status rt_download_after(rt_context* c, const void* dev_src, void* host_dst, 
 }
 
 rt_status rt_upload(rt_context* c, const void* host_src, void* dev_dst, size_t bytes) {
-    if (!c || !host_src || !dev_dst || !bytes) return fail(RT_ERR_INVALID_ARG, "rt_upload: NULL pointer or zero size");
+    if (!c || !host_src || !dev_dst || !bytes) return rtb_fail(RT_ERR_INVALID_ARG, "rt_upload: NULL pointer or zero size");
     CUDA_TRY(cudaSetDevice(c->device));
-    if (!is_pinned(host_src)) return fail(RT_ERR_INVALID_ARG, "rt_upload: host_src is not pinned host memory");
+    if (!is_pinned(host_src)) return rtb_fail(RT_ERR_INVALID_ARG, "rt_upload: host_src is not pinned host memory");
     CUDA_TRY(cudaMemcpyAsync(dev_dst, host_src, bytes, cudaMemcpyHostToDevice, c->stream));
     return RT_OK;
 }
 
 rt_status rt_wait(rt_event* ev) {
-    if (!ev) return fail(RT_ERR_INVALID_ARG, "rt_wait: NULL event");
+    if (!ev) return rtb_fail(RT_ERR_INVALID_ARG, "rt_wait: NULL event");
     cudaError_t e = cudaEventSynchronize(ev->ev);
     cudaEventDestroy(ev->ev);
     delete ev;
-    if (e != cudaSuccess) return fail(RT_ERR_CUDA, "rt_wait: %s", cudaGetErrorString(e));
+    if (e != cudaSuccess) return rtb_fail(RT_ERR_CUDA, "rt_wait: %s", cudaGetErrorString(e));
     return RT_OK;
 }
 
 rt_status rt_query(rt_event* ev) {
-    if (!ev) return fail(RT_ERR_INVALID_ARG, "rt_query: NULL event");
+    if (!ev) return rtb_fail(RT_ERR_INVALID_ARG, "rt_query: NULL event");
     cudaError_t e = cudaEventQuery(ev->ev);
     if (e == cudaSuccess) return RT_OK;
     if (e == cudaErrorNotReady) {
         cudaGetLastError();
         return RT_ERR_NOT_READY;
     }
-    return fail(RT_ERR_CUDA, "rt_query: %s", cudaGetErrorString(e));
+    return rtb_fail(RT_ERR_CUDA, "rt_query: %s", cudaGetErrorString(e));
 }
 
 // ------------------------------------------------------------------------------ shards
 rt_status rt_shard_tiles(uint32_t W, uint32_t H, uint32_t rank, uint32_t world, uint32_t* n_tiles, uint32_t* ids) {
     if (!n_tiles || W == 0 || H == 0 || world == 0 || rank >= world || W > 16384 || H > 16384)
-        return fail(RT_ERR_INVALID_ARG, "rt_shard_tiles: bad arguments");
+        return rtb_fail(RT_ERR_INVALID_ARG, "rt_shard_tiles: bad arguments");
     const ShardGeom g = shard_geom(W, H, world);
     const uint32_t n = shard_count(g, rank, world);
     if (ids)
@@ -907,7 +806,7 @@ rt_status rt_shard_tiles(uint32_t W, uint32_t H, uint32_t rank, uint32_t world, 
 
 rt_status rt_shard_bytes(uint32_t W, uint32_t H, uint32_t world, uint32_t format, uint64_t* bytes) {
     if (!bytes || W == 0 || H == 0 || world == 0 || (format != RT_FORMAT_RGBA8 && format != RT_FORMAT_RGBA16F))
-        return fail(RT_ERR_INVALID_ARG, "rt_shard_bytes: bad arguments");
+        return rtb_fail(RT_ERR_INVALID_ARG, "rt_shard_bytes: bad arguments");
     const ShardGeom g = shard_geom(W, H, world);
     uint32_t mx = 0;
     for (uint32_t r = 0; r < world; ++r) mx = std::max(mx, shard_count(g, r, world));
@@ -920,9 +819,9 @@ rt_status rt_unpack_shards_host(const void* gathered, uint32_t W, uint32_t H, ui
     uint64_t per = 0;
     rt_status st = rt_shard_bytes(W, H, world, format, &per);
     if (st) return st;
-    if (!gathered) return fail(RT_ERR_INVALID_ARG, "rt_unpack_shards_host: NULL gathered");
+    if (!gathered) return rtb_fail(RT_ERR_INVALID_ARG, "rt_unpack_shards_host: NULL gathered");
     const uint32_t bpp = format == RT_FORMAT_RGBA8 ? 4 : 8;
-    if (pitch < (uint64_t)W * bpp) return fail(RT_ERR_SIZE, "rt_unpack_shards_host: pitch too small");
+    if (pitch < (uint64_t)W * bpp) return rtb_fail(RT_ERR_SIZE, "rt_unpack_shards_host: pitch too small");
     const ShardGeom g = shard_geom(W, H, world);
     const char* src = static_cast<const char*>(gathered);
     for (uint32_t r = 0; r < world; ++r) {
@@ -948,14 +847,21 @@ rt_status rt_unpack_shards_host(const void* gathered, uint32_t W, uint32_t H, ui
 rt_status rt_unpack_shards(rt_context* c, const void* gathered, uint32_t W, uint32_t H, uint32_t world, uint32_t format,
                            rt_fb left, rt_fb right) {
     NvtxRange nvtx_("rt_unpack_shards");
-    if (!c || !gathered) return fail(RT_ERR_INVALID_ARG, "rt_unpack_shards: NULL argument");
+    if (!c || !gathered) return rtb_fail(RT_ERR_INVALID_ARG, "rt_unpack_shards: NULL argument");
+    return rtb_unpack_on(c, gathered, W, H, world, format, left, right, c->stream);
+}
+
+}  // extern "C"
+
+rt_status rtb_unpack_on(rt_context* c, const void* gathered, uint32_t W, uint32_t H, uint32_t world, uint32_t format,
+                        rt_fb left, rt_fb right, cudaStream_t stream) {
     uint64_t per = 0;
     rt_status st = rt_shard_bytes(W, H, world, format, &per);
     if (st) return st;
     if ((left.dev_ptr && left.format != format) || (right.dev_ptr && right.format != format))
-        return fail(RT_ERR_INVALID_ARG, "rt_unpack_shards: framebuffer format differs from the shard format");
+        return rtb_fail(RT_ERR_INVALID_ARG, "rt_unpack_shards: framebuffer format differs from the shard format");
     if (left.dev_ptr && right.dev_ptr && left.pitch_bytes != right.pitch_bytes)
-        return fail(RT_ERR_INVALID_ARG, "rt_unpack_shards: left/right pitch differ");
+        return rtb_fail(RT_ERR_INVALID_ARG, "rt_unpack_shards: left/right pitch differ");
     if ((st = check_fb(left, W, "left")) || (st = check_fb(right, W, "right"))) return st;
     const ShardGeom g = shard_geom(W, H, world);
     UnpackParams U{};
@@ -971,34 +877,36 @@ rt_status rt_unpack_shards(rt_context* c, const void* gathered, uint32_t W, uint
     U.world = (int)world;
     U.shard_mode = g.mode;
     CUDA_TRY(cudaSetDevice(c->device));
-    CUDA_TRY(rtb_launch_unpack(gathered, U, c->stream));
+    CUDA_TRY(rtb_launch_unpack(gathered, U, stream));
     return RT_OK;
 }
 
+extern "C" {
+
 // ------------------------------------------------------------------------------ peer memory
 rt_status rt_ipc_get_handle(const void* dev_ptr, void* handle64, uint64_t* offset) {
-    if (!dev_ptr || !handle64 || !offset) return fail(RT_ERR_INVALID_ARG, "rt_ipc_get_handle: NULL argument");
+    if (!dev_ptr || !handle64 || !offset) return rtb_fail(RT_ERR_INVALID_ARG, "rt_ipc_get_handle: NULL argument");
     static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
     // driver entry point through the runtime (the library does not link libcuda directly)
     using GetRange = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
-        return fail(RT_ERR_PEER, "cuMemGetAddressRange entry point unavailable");
+        return rtb_fail(RT_ERR_PEER, "cuMemGetAddressRange entry point unavailable");
     CUdeviceptr base = 0;
     size_t size = 0;
     CUresult r = reinterpret_cast<GetRange>(fn)(&base, &size, (CUdeviceptr)dev_ptr);
-    if (r != CUDA_SUCCESS) return fail(RT_ERR_PEER, "cuMemGetAddressRange failed (%d)", (int)r);
+    if (r != CUDA_SUCCESS) return rtb_fail(RT_ERR_PEER, "cuMemGetAddressRange failed (%d)", (int)r);
     cudaIpcMemHandle_t h;
     cudaError_t e = cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base));
-    if (e != cudaSuccess) return fail(RT_ERR_PEER, "cudaIpcGetMemHandle: %s", cudaGetErrorString(e));
+    if (e != cudaSuccess) return rtb_fail(RT_ERR_PEER, "cudaIpcGetMemHandle: %s", cudaGetErrorString(e));
     memcpy(handle64, &h, 64);
     *offset = (uint64_t)((CUdeviceptr)dev_ptr - base);
     return RT_OK;
 }
 
 rt_status rt_ipc_open(rt_context* c, const void* handle64, void** dev_ptr) {
-    if (!c || !handle64 || !dev_ptr) return fail(RT_ERR_INVALID_ARG, "rt_ipc_open: NULL argument");
+    if (!c || !handle64 || !dev_ptr) return rtb_fail(RT_ERR_INVALID_ARG, "rt_ipc_open: NULL argument");
     CUDA_TRY(cudaSetDevice(c->device));
     // one mapping per exported allocation per process: several framebuffers can share one
     // caching-allocator block (one handle, different offsets), and CUDA maps a handle once
@@ -1012,13 +920,13 @@ rt_status rt_ipc_open(rt_context* c, const void* handle64, void** dev_ptr) {
     cudaIpcMemHandle_t h;
     memcpy(&h, handle64, 64);
     cudaError_t e = cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess);
-    if (e != cudaSuccess) return fail(RT_ERR_PEER, "cudaIpcOpenMemHandle: %s", cudaGetErrorString(e));
+    if (e != cudaSuccess) return rtb_fail(RT_ERR_PEER, "cudaIpcOpenMemHandle: %s", cudaGetErrorString(e));
     c->ipc_maps.push_back({key, *dev_ptr, 1});
     return RT_OK;
 }
 
 rt_status rt_ipc_close(rt_context* c, void* dev_ptr) {
-    if (!c || !dev_ptr) return fail(RT_ERR_INVALID_ARG, "rt_ipc_close: NULL argument");
+    if (!c || !dev_ptr) return rtb_fail(RT_ERR_INVALID_ARG, "rt_ipc_close: NULL argument");
     CUDA_TRY(cudaSetDevice(c->device));
     for (size_t i = 0; i < c->ipc_maps.size(); ++i)
         if (c->ipc_maps[i].ptr == dev_ptr) {
@@ -1027,19 +935,19 @@ rt_status rt_ipc_close(rt_context* c, void* dev_ptr) {
             break;
         }
     cudaError_t e = cudaIpcCloseMemHandle(dev_ptr);
-    if (e != cudaSuccess) return fail(RT_ERR_PEER, "cudaIpcCloseMemHandle: %s", cudaGetErrorString(e));
+    if (e != cudaSuccess) return rtb_fail(RT_ERR_PEER, "cudaIpcCloseMemHandle: %s", cudaGetErrorString(e));
     return RT_OK;
 }
 
 // ------------------------------------------------------------------------------ composition
 rt_status rt_compose(rt_context* c, rt_fb left, rt_fb right, uint32_t W, uint32_t H, uint32_t mode, rt_fb out) {
     NvtxRange nvtx_("rt_compose");
-    if (!c || !left.dev_ptr || !right.dev_ptr || !out.dev_ptr) return fail(RT_ERR_INVALID_ARG, "rt_compose: NULL argument");
+    if (!c || !left.dev_ptr || !right.dev_ptr || !out.dev_ptr) return rtb_fail(RT_ERR_INVALID_ARG, "rt_compose: NULL argument");
     if (left.format != RT_FORMAT_RGBA8 || right.format != RT_FORMAT_RGBA8 || out.format != RT_FORMAT_RGBA8)
-        return fail(RT_ERR_INVALID_ARG, "rt_compose: RGBA8 framebuffers only");
-    if (mode != RT_COMPOSE_ANAGLYPH && mode != RT_COMPOSE_SBS) return fail(RT_ERR_INVALID_ARG, "rt_compose: mode %u", mode);
-    if (W == 0 || H == 0 || W > 16384 || H > 16384) return fail(RT_ERR_SIZE, "rt_compose: size %ux%u", W, H);
-    if (mode == RT_COMPOSE_SBS && W < 2) return fail(RT_ERR_INVALID_ARG, "rt_compose: SBS needs width >= 2");
+        return rtb_fail(RT_ERR_INVALID_ARG, "rt_compose: RGBA8 framebuffers only");
+    if (mode != RT_COMPOSE_ANAGLYPH && mode != RT_COMPOSE_SBS) return rtb_fail(RT_ERR_INVALID_ARG, "rt_compose: mode %u", mode);
+    if (W == 0 || H == 0 || W > 16384 || H > 16384) return rtb_fail(RT_ERR_SIZE, "rt_compose: size %ux%u", W, H);
+    if (mode == RT_COMPOSE_SBS && W < 2) return rtb_fail(RT_ERR_INVALID_ARG, "rt_compose: SBS needs width >= 2");
     const uint64_t out_w = mode == RT_COMPOSE_ANAGLYPH ? W : 2 * (W / 2);
     rt_status st;
     if ((st = check_fb(left, W, "left")) || (st = check_fb(right, W, "right")) || (st = check_fb(out, (uint32_t)out_w, "out")))
@@ -1053,10 +961,10 @@ rt_status rt_compose(rt_context* c, rt_fb left, rt_fb right, uint32_t W, uint32_
 // ------------------------------------------------------------------------------ introspection
 rt_status rt_kdtree_build(rt_context* c, uint32_t max_leaf, uint32_t max_depth, uint64_t info[6]) {
     NvtxRange nvtx_("rt_kdtree_build");
-    if (!c) return fail(RT_ERR_INVALID_ARG, "rt_kdtree_build: NULL context");
-    if (max_leaf < 1 || max_leaf > 4096) return fail(RT_ERR_INVALID_ARG, "rt_kdtree_build: max_leaf %u", max_leaf);
-    if (max_depth > 60) return fail(RT_ERR_INVALID_ARG, "rt_kdtree_build: max_depth %u > 60", max_depth);
-    if (!c->has_scene) return fail(RT_ERR_NO_SCENE, "rt_kdtree_build: no scene");
+    if (!c) return rtb_fail(RT_ERR_INVALID_ARG, "rt_kdtree_build: NULL context");
+    if (max_leaf < 1 || max_leaf > 4096) return rtb_fail(RT_ERR_INVALID_ARG, "rt_kdtree_build: max_leaf %u", max_leaf);
+    if (max_depth > 60) return rtb_fail(RT_ERR_INVALID_ARG, "rt_kdtree_build: max_depth %u > 60", max_depth);
+    if (!c->has_scene) return rtb_fail(RT_ERR_NO_SCENE, "rt_kdtree_build: no scene");
     CUDA_TRY(cudaSetDevice(c->device));
     CUDA_TRY(wait_renders(c));                     // kd renders in flight read the buffers replaced below
     CUDA_TRY(cudaStreamSynchronize(c->stream));
@@ -1084,7 +992,7 @@ rt_status rt_kdtree_build(rt_context* c, uint32_t max_leaf, uint32_t max_depth, 
         if (e != cudaSuccess) {
             a.release();
             b.release();
-            return fail(RT_ERR_OOM, "rt_kdtree_build: cudaMalloc: %s", cudaGetErrorString(e));
+            return rtb_fail(RT_ERR_OOM, "rt_kdtree_build: cudaMalloc: %s", cudaGetErrorString(e));
         }
         c->kd_nodes_buf = a;
         c->kd_refs_buf = b;
@@ -1109,15 +1017,15 @@ rt_status rt_kdtree_build(rt_context* c, uint32_t max_leaf, uint32_t max_depth, 
 }
 
 rt_status rt_scene_info(rt_context* c, uint64_t info[8]) {
-    if (!c || !info) return fail(RT_ERR_INVALID_ARG, "rt_scene_info: NULL argument");
-    if (!c->has_scene) return fail(RT_ERR_NO_SCENE, "rt_scene_info: no scene");
+    if (!c || !info) return rtb_fail(RT_ERR_INVALID_ARG, "rt_scene_info: NULL argument");
+    if (!c->has_scene) return rtb_fail(RT_ERR_NO_SCENE, "rt_scene_info: no scene");
     memcpy(info, c->info, sizeof c->info);
     return RT_OK;
 }
 
 rt_status rt_bvh_export(rt_context* c, float* nodes, uint32_t* n_nodes, int32_t* prim_gid, uint32_t* n_prims) {
-    if (!c || !n_nodes || !n_prims) return fail(RT_ERR_INVALID_ARG, "rt_bvh_export: NULL argument");
-    if (!c->has_scene) return fail(RT_ERR_NO_SCENE, "rt_bvh_export: no scene");
+    if (!c || !n_nodes || !n_prims) return rtb_fail(RT_ERR_INVALID_ARG, "rt_bvh_export: NULL argument");
+    if (!c->has_scene) return rtb_fail(RT_ERR_NO_SCENE, "rt_bvh_export: no scene");
     const uint32_t nn = (uint32_t)c->info[4], np = (uint32_t)c->sc.n_bvh;
     CUDA_TRY(cudaSetDevice(c->device));
     CUDA_TRY(cudaStreamSynchronize(c->stream));
@@ -1150,7 +1058,7 @@ rt_status rt_bvh_export(rt_context* c, float* nodes, uint32_t* n_nodes, int32_t*
 }
 
 rt_status rt_bench_ffma(rt_context* c, uint32_t iters, double* tflops, double* ms) {
-    if (!c || !tflops || !ms || !iters) return fail(RT_ERR_INVALID_ARG, "rt_bench_ffma: bad argument");
+    if (!c || !tflops || !ms || !iters) return rtb_fail(RT_ERR_INVALID_ARG, "rt_bench_ffma: bad argument");
     CUDA_TRY(cudaSetDevice(c->device));
     const int grid = c->num_sms * 8;
     cudaEvent_t a, b;
@@ -1172,7 +1080,7 @@ rt_status rt_bench_ffma(rt_context* c, uint32_t iters, double* tflops, double* m
 }
 
 rt_status rt_bench_ceilings(rt_context* c, double out[RT_NUM_CEILINGS]) {
-    if (!c || !out) return fail(RT_ERR_INVALID_ARG, "rt_bench_ceilings: NULL argument");
+    if (!c || !out) return rtb_fail(RT_ERR_INVALID_ARG, "rt_bench_ceilings: NULL argument");
     CUDA_TRY(cudaSetDevice(c->device));
     for (int i = 0; i < RT_NUM_CEILINGS; ++i) out[i] = 0.0;
     CUDA_TRY(rtb_probe_ceilings(c->num_sms, c->stream, out));

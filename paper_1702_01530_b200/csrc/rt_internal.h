@@ -44,8 +44,6 @@ struct TraceParams {
     unsigned long long* counters;
     int stack_entries;      // BVH traversal stack depth (shared memory, [entry][thread])
     int n_tiles;            // 16x16 tiles in this shard (= n_work / 256)
-    const char* pf_base[2]; // L2 prefetch at kernel start: BVH nodes, primitive records (null = off)
-    unsigned long long pf_bytes[2];
     int peer_fence;         // framebuffers live in a peer's memory: fence system-wide at exit
 };
 

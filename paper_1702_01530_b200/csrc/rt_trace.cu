@@ -134,23 +134,6 @@ __global__ void __launch_bounds__(RT_BLOCK, RT_MINB) k_trace_stereo(const TraceP
     const int lane = threadIdx.x & 31;
     int lstack[STACK_CAP > RT_SMEM_STACK ? STACK_CAP - RT_SMEM_STACK : 1];
     TravStack stk{(uint32_t)__cvta_generic_to_shared(s_stack + threadIdx.x), lstack};
-    // Warm L2 with the scene before tracing: every frame starts with the scene + BVH cold in L2
-    // (the bench flushes it between frames, as a fresh frame after other work would find it),
-    // and demand misses then arrive one dependent traversal load at a time, latency-bound.
-    // Bulk L2 prefetches (TMA engine, asynchronous: issued and forgotten) stream it at HBM
-    // bandwidth instead -- 129 MB for C4, which fits the 126 MB L2 nearly whole.
-    if (P.pf_base[0]) {
-        constexpr unsigned long long CH = 16384;
-        const unsigned long long n0 = (P.pf_bytes[0] + CH - 1) / CH, n1 = (P.pf_bytes[1] + CH - 1) / CH;
-        for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < n0 + n1;
-             i += (unsigned long long)gridDim.x * blockDim.x) {
-            const int a = i < n0 ? 0 : 1;
-            const unsigned long long off = (i < n0 ? i : i - n0) * CH;
-            const unsigned long long rem = P.pf_bytes[a] - off;
-            const uint32_t sz = (uint32_t)((rem < CH ? rem : CH) & ~15ull);
-            if (sz) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(P.pf_base[a] + off), "r"(sz) : "memory");
-        }
-    }
     __shared__ int s_occ[RT_OCC_LIGHTS * RT_BLOCK];  // [light][thread] last-occluder hints
 #pragma unroll
     for (int j = 0; j < RT_OCC_LIGHTS; ++j) s_occ[j * RT_BLOCK + threadIdx.x] = -1;

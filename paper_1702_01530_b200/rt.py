@@ -22,6 +22,8 @@ RT_RENDER_COUNT, RT_RENDER_BRUTE_FORCE, RT_RENDER_PEER_STORE, RT_RENDER_KDTREE =
 RT_NUM_COUNTERS = 13
 RT_COMPOSE_ANAGLYPH, RT_COMPOSE_SBS = 0, 1
 RT_TILE = 16
+RT_DIST_ID_BYTES = 128
+RT_DIST_PEER, RT_DIST_NCCL = 0, 1
 COUNTER_NAMES = ["primary", "reflection", "refraction", "shadow", "node_visits", "tri_tests", "sphere_tests",
                  "plane_tests", "shade_hits", "light_evals", "misses", "pixels", "box_tests"]
 
@@ -31,7 +33,8 @@ EXPORTED = ["rt_create", "rt_destroy", "rt_synchronize", "rt_last_error", "rt_ve
             "rt_host_alloc", "rt_host_free", "rt_upload", "rt_shard_tiles", "rt_shard_bytes", "rt_unpack_shards_host",
             "rt_unpack_shards", "rt_ipc_get_handle", "rt_ipc_open", "rt_ipc_close", "rt_scene_info", "rt_bvh_export",
             "rt_bench_ffma", "rt_compose", "rt_scene_update_vertices", "rt_bvh_width", "rt_kdtree_build",
-            "rt_render_stereo_async", "rt_download_after", "rt_bench_ceilings"]
+            "rt_render_stereo_async", "rt_download_after", "rt_bench_ceilings", "rt_dist_unique_id", "rt_dist_init",
+            "rt_dist_finalize", "rt_dist_info", "rt_dist_host_selftest"]
 
 
 class RtError(RuntimeError):
@@ -111,6 +114,9 @@ def lib():
             "rt_scene_update_vertices": [vp, vp, u32],
             "rt_kdtree_build": [vp, u32, u32, vp],
             "rt_bench_ceilings": [vp, vp],
+            "rt_dist_unique_id": [vp], "rt_dist_init": [vp, C.c_int, C.c_int, vp, u32], "rt_dist_finalize": [vp],
+            "rt_dist_info": [vp, vp],
+            "rt_dist_host_selftest": [C.c_int, C.c_int, vp, u32, C.POINTER(u64)],
         }
         for name, args in sig.items():
             fn = getattr(L, name)
@@ -345,6 +351,37 @@ def rt_bench_ffma(ctx, iters=2048):
     tf, ms = C.c_double(), C.c_double()
     _check(lib().rt_bench_ffma(ctx, iters, C.byref(tf), C.byref(ms)))
     return tf.value, ms.value
+
+
+def rt_dist_unique_id():
+    """128-byte job id for rt_dist_init (rank 0 creates it, the caller broadcasts it)."""
+    b = (C.c_char * RT_DIST_ID_BYTES)()
+    _check(lib().rt_dist_unique_id(C.cast(b, C.c_void_p)))
+    return bytes(b)
+
+
+def rt_dist_init(ctx, rank, world, job_id, transport=RT_DIST_PEER):
+    b = (C.c_char * RT_DIST_ID_BYTES).from_buffer_copy(job_id)
+    _check(lib().rt_dist_init(ctx, int(rank), int(world), C.cast(b, C.c_void_p), int(transport)))
+
+
+def rt_dist_host_selftest(rank, world, job_id, frames):
+    """host half of the multi-GPU protocol, no device work (tests) -> checksum"""
+    b = (C.c_char * RT_DIST_ID_BYTES).from_buffer_copy(job_id)
+    h = C.c_uint64()
+    _check(lib().rt_dist_host_selftest(int(rank), int(world), C.cast(b, C.c_void_p), int(frames), C.byref(h)))
+    return h.value
+
+
+def rt_dist_finalize(ctx):
+    _check(lib().rt_dist_finalize(ctx))
+
+
+def rt_dist_info(ctx):
+    a = np.zeros(4, np.int32)
+    _check(lib().rt_dist_info(ctx, a.ctypes.data))
+    return {"rank": int(a[0]), "world": int(a[1]), "transport": {0: "peer", 1: "nccl"}.get(int(a[2]), "none"),
+            "frames": int(a[3])}
 
 
 CEILING_NAMES = ["ffma_flop_clk_sm", "ffma2_flop_clk_sm", "fmnmx_clk_sm", "fmnmx3_clk_sm", "l1_bytes_clk_sm",

@@ -1,6 +1,10 @@
-"""World-size-2 CPU tests (gloo) of the multi-GPU host logic: shard map -> per-rank packed
-shards -> bench.gather_to_root -> root unpack == the full image; max-over-ranks timing;
-and the reference arm under a 2-process launch (rank 1 exits without work)."""
+"""Multi-process CPU tests of the multi-GPU host logic:
+  - the library's own host protocol (rt_dist_host_selftest): shared-memory rendezvous, the
+    16-slot frame-descriptor ring with flow control over more frames than slots, and the leave,
+    in 2 and 3 processes -- the host half of rt_dist_init / frame renders / rt_dist_finalize;
+  - world-size-2 gloo: shard map -> per-rank packed shards -> gather -> root unpack == the full
+    image (the NCCL transport's data layout); max-over-ranks timing;
+  - the reference arm under a 2-process launch (rank 1 exits without work)."""
 import os
 import socket
 import subprocess
@@ -25,7 +29,6 @@ def _free_port():
 
 def _worker(rank, world, port, W, H, q):
     sys.path.insert(0, ROOT)
-    import bench  # noqa: F401  (gather_to_root re-export)
     from paper_1702_01530_b200 import rt
     from tests.test_abi import expected_image, synth_shards
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -34,7 +37,8 @@ def _worker(rank, world, port, W, H, q):
     mine = synth_shards(W, H, world)[rank].view(np.uint8)
     shard = torch.from_numpy(mine.copy())
     gathered = torch.zeros(world * per, dtype=torch.uint8) if rank == 0 else None
-    bench.gather_to_root(dist, shard, gathered, world, rank, per)
+    glist = [gathered[r * per:(r + 1) * per] for r in range(world)] if rank == 0 else None
+    dist.gather(shard, glist, dst=0)
     t = torch.tensor([1.0 + rank], dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ok = float(t[0]) == float(world)
@@ -60,6 +64,40 @@ def test_gloo_world2_gather_unpack(W, H):
         p.join(120)
         assert p.exitcode == 0
     assert q.get(timeout=10) is True
+
+
+def _selftest_worker(rank, world, job_id, frames, q):
+    sys.path.insert(0, ROOT)
+    from paper_1702_01530_b200 import rt
+    q.put((rank, rt.rt_dist_host_selftest(rank, world, job_id, frames)))
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_dist_host_protocol_multiprocess(world):
+    """rt_dist_init's rendezvous + the per-frame descriptor ring (40 frames through 16 slots:
+    rank 0 must wait for the slowest reader) + rt_dist_finalize's leave, in `world` processes
+    with no GPU: every rank sees every frame's descriptor, in order (equal checksums)."""
+    sys.path.insert(0, ROOT)
+    from paper_1702_01530_b200 import rt
+    job = rt.rt_dist_unique_id()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_selftest_worker, args=(r, world, job, 40, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    sums = dict(q.get(timeout=10) for _ in range(world))
+    assert len(set(sums.values())) == 1, sums
+    # a different job id is a different rendezvous: a lone rank of a 2-world times out cleanly
+    os.environ["RT_DIST_TIMEOUT_S"] = "1"
+    try:
+        with pytest.raises(rt.RtError) as e:
+            rt.rt_dist_host_selftest(1, 2, rt.rt_dist_unique_id(), 4)
+        assert e.value.status == rt.RT_ERR_PEER
+    finally:
+        del os.environ["RT_DIST_TIMEOUT_S"]
 
 
 def test_reference_arm_under_torchrun():

@@ -1,17 +1,20 @@
-"""Fused render -> gather on one GPU with two processes: rank 1 maps rank 0's framebuffers with
-CUDA IPC and its trace kernel stores its tiles into them (RT_RENDER_PEER_STORE); the assembled
-stereo frame must equal a single-process render bit-exactly (SURVEY §4 T3 invariant).
-Same-device IPC exercises exactly the code path NVLink peers use (mapped peer pointers)."""
+"""Multi-GPU frames through the C ABI (rt_dist_init) with 2 and 3 processes on
+one GPU: every rank renders its tiles of each frame and the library assembles the frame in rank
+0's framebuffers -- peer stores into rank 0's IPC-mapped framebuffers, ordered by device-side
+flags (same-device IPC exercises exactly the code path NVLink peers use).  Frames are kept in
+flight on 3 streams per rank, more frames than the 16-slot descriptor ring, each frame with its
+own camera; every assembled frame must equal the single-process render bit for bit.
+Python only broadcasts the job id; no torch.distributed data-path call is made."""
 import os
 import socket
 
-import numpy as np
 import pytest
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+N_FRAMES = 20
 
 
 def _port():
@@ -22,7 +25,7 @@ def _port():
     return p
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, transport, q):
     import sys
     sys.path.insert(0, ROOT)
     import torch.distributed as dist
@@ -31,46 +34,55 @@ def _worker(rank, world, port, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    s = scenes.scene_c2().with_view(width=93, height=61, max_depth=3)
+    s = scenes.scene_c3().with_view(width=93, height=61, max_depth=3)
     R = rt.StereoRenderer(0)
     R.upload(s)
-    R.set_camera(s.rig)
-    # three small framebuffer slots (frames in flight): they share caching-allocator blocks, so
-    # several mappings of one IPC handle at different offsets
-    fbs = [R.alloc_fb(s.width, s.height) for _ in range(3)]
-    for fb in fbs:
-        fb.zero_()
+    rigs = [scenes.c5_rig(10 * k) for k in range(5)]
+    info = multigpu.join_world(R, rank, world, dist, transport)
+    ok = info["world"] == world and info["rank"] == rank
+    streams = [torch.cuda.Stream() for _ in range(3)]
+    fbs = []
+    for k in range(N_FRAMES):
+        fb = R.alloc_fb(s.width, s.height) if rank == 0 else None
+        if fb is not None:
+            fb.zero_()
+            streams[k % 3].wait_stream(torch.cuda.current_stream())
+        fbs.append(fb)
+        R.set_camera(rigs[k % len(rigs)])
+        multigpu.Frame(R, fb, s.width, s.height).render(s.max_depth, streams[k % 3])
     torch.cuda.synchronize()
-    dist.barrier()
-    frames = [multigpu.PeerFrame(R, fb, rank, world, dist, s.width, s.height) for fb in fbs]
-    streams = [torch.cuda.Stream() for _ in fbs]
-    for f, st in zip(frames, streams):
-        f.render(s.max_depth, st)
-    torch.cuda.synchronize()
-    frames[0].assemble()
+    info = rt.rt_dist_info(R.ctx)
+    ok = ok and info["frames"] == N_FRAMES
+    rt.rt_dist_finalize(R.ctx)
     if rank == 0:
-        ref = R.render(s.width, s.height, s.max_depth)["fb"]
+        ref = []
+        for rg in rigs:
+            R.set_camera(rg)
+            ref.append(R.render(s.width, s.height, s.max_depth)["fb"])
         torch.cuda.synchronize()
-        q.put(all(bool(torch.equal(ref, fb)) for fb in fbs))
+        bad = [k for k in range(N_FRAMES) if not torch.equal(fbs[k], ref[k % len(rigs)])]
+        q.put((ok and not bad, info["transport"], bad))
     dist.barrier()
-    for f in frames:
-        f.close()
     R.close()
     dist.destroy_process_group()
 
 
 @pytest.mark.parametrize("world", [2, 3])
-def test_peer_store_frame_bit_exact(world):
+def test_dist_frames_bit_exact(world):
+    """world 2 = the eye split (rank 1 stores the whole right eye into rank 0's FB); world 3 =
+    tile pairs dealt round-robin."""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, "peer", q)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
-        p.join(300)
+        p.join(600)
         assert p.exitcode == 0
-    assert q.get(timeout=10) is True
+    ok, transport, bad = q.get(timeout=10)
+    assert transport == "peer"
+    assert ok, f"frames differing from the single-GPU render: {bad}"
