@@ -48,7 +48,11 @@ class OracleEps(C.Structure):
 
 CAND_K = 8          # near-tie candidate IDs kept per ID-fragile pixel
 
-DEFAULT_EPS = dict(eps_t=1e-4, eps_sphere=1e-4, eps_edge=1e-5, eps_abs=1e-5, perturb=1e-6, perturb_tol=1e-3)
+# eps_edge 1e-6: SURVEY §8(c) #22 sets the triangle-edge band to >= 4x the largest edge margin of
+# any GPU/oracle ID disagreement; the round-2 reports (profiles/r02_parity_report_eps1e-*.json:
+# 0.52 M C3 pixels, C4 and C5 samples) saw no disagreement at all, off or on the band, and the
+# FP32 edge-decision error is ~1e-7 angular (reading 22).
+DEFAULT_EPS = dict(eps_t=1e-4, eps_sphere=1e-4, eps_edge=1e-6, eps_abs=1e-5, perturb=1e-6, perturb_tol=1e-3)
 
 _lib = None
 

@@ -71,7 +71,7 @@ typedef struct {
 typedef struct {
     double eps_t;      /* relative t band for competing hits, grazing, gates   (1e-4) */
     double eps_sphere; /* angular band around sphere silhouettes               (1e-4) */
-    double eps_edge;   /* angular band around triangle edges                   (1e-5) */
+    double eps_edge;   /* angular band around triangle edges                   (1e-6) */
     double eps_abs;    /* absolute band (x (1+|o|)) around t_min               (1e-5) */
     double perturb;    /* F7: primary-ray perturbation angle (rad), 0 = off    (1e-6) */
     double perturb_tol;/* F7: radiance change that marks the pixel unstable    (1e-3) */

@@ -42,7 +42,11 @@ def compare(ref, ids, rgba8, radiance, label=""):
     max_err = float(err[ok].max()) if ok.any() else 0.0
     stats = dict(label=label, n=len(rid), id_excluded=float(1 - ok_id.mean()), id_mismatch=id_mism,
                  rgb_frac=frac, rad_excluded=float(1 - ok.mean()), max_err=max_err,
-                 all_id_mismatch=int((ids != rid).sum()), id_fragile=int(len(frag)),
+                 all_id_mismatch=int((ids != rid).sum()),
+                 # the oracle's primary boundary margin of every GPU/oracle ID disagreement: the
+                 # triangle-edge band eps_edge must stay >= 4x the largest
+                 mismatch_margins=sorted(float(x) for x in ref["margin"].reshape(-1)[ids != rid]),
+                 id_fragile=int(len(frag)),
                  id_fragile_checked=int(checkable.sum()), id_candidate_violations=cand_viol,
                  id_fragile_unchecked=int((~checkable).sum()))
     return stats

@@ -8,7 +8,7 @@ side of its band (closed form), so a dropped term, a wrong sign or a swapped ban
   F4 GRAZE    |n.d| = 5e-5 (flagged) / 2e-4 (not)
   F5 RANGE    a surface at t_min +- 5e-6 (flagged) / +- 5e-5 (not)
   F6 SHADE    n.l = +-5e-5 at the hit; the TIR discriminant k = +-5e-5
-  SHADOW      shadow segment 5e-6 t from an occluder edge / through its centre / far from it;
+  SHADOW      shadow segment 0.5 eps_edge t from an occluder edge / through its centre / far from it;
               an occluder at the segment's end
 The candidate sets are pinned by closed-form cases and, on real scenes, by brute force: the
 nearest hit of every ray turned by up to the band around an ID-fragile primary ray must be one of
@@ -18,13 +18,14 @@ import math
 
 import numpy as np
 
-from oracle.oracle import (FRAG_BOUNDARY, FRAG_COMPETE, FRAG_GRAZE, FRAG_RANGE, FRAG_SHADE, FRAG_SHADOW,
-                           ID_FRAGILE_MASK, Oracle)
+from oracle.oracle import (DEFAULT_EPS, FRAG_BOUNDARY, FRAG_COMPETE, FRAG_GRAZE, FRAG_RANGE, FRAG_SHADE,
+                           FRAG_SHADOW, ID_FRAGILE_MASK, Oracle)
 from paper_1702_01530_b200 import scenes
 from paper_1702_01530_b200.scenes import material
 from tests.test_oracle_pins import mk_scene
 
 EPS_T = 1e-4
+EPS_E = DEFAULT_EPS["eps_edge"]      # the triangle-edge band (angular)
 T_MIN = 1e-4
 BIG = 50.0
 
@@ -129,8 +130,9 @@ def test_shadow_flags():
         v, t = quad(5.0, x0=x0)
         return Oracle(mk_scene(verts=v, tris=t))
     t_edge = 5.0
-    for x0, want in ((0.5e-5 * t_edge, True),      # misses the occluder, 5e-6 t from its edge
-                     (-0.5e-5 * t_edge, True),     # blocked, but only 5e-6 t inside the edge
+    for x0, want in ((0.5 * EPS_E * t_edge, True),     # misses the occluder, 0.5 eps_edge t from its edge
+                     (-0.5 * EPS_E * t_edge, True),    # blocked, but only 0.5 eps_edge t inside the edge
+                     (3.0 * EPS_E * t_edge, False),    # misses it by 3 eps_edge t: robust
                      (-1.0, False),                # through the occluder's interior: robust
                      (2e-4 * t_edge, False)):      # misses by 2e-4 t: robustly unoccluded
         f, _ = occ(x0).ray_flags(O, DZ, kind="shadow", dist=10.0)
@@ -153,11 +155,11 @@ def test_candidates_closed_form():
     # hit robustly and FP32 Moller-Trumbore is not watertight across a shared edge
     assert o.ray_candidates(O, DZ)[0] == [-1, 0, 1]
     # 0.5 eps_edge * t off the diagonal (distance measured in the plane): still all; 3x: one
-    for off, want in ((0.5e-5 * 5, [-1, 0, 1]), (3e-5 * 5, [1])):
+    for off, want in ((0.5 * EPS_E * 5, [-1, 0, 1]), (3 * EPS_E * 5, [1])):
         p = np.array([1.0, 1.0, 0.0]) / math.sqrt(2) * off
         assert o.ray_candidates(p, DZ)[0] == want, off
     # the quad's outer edge at x = 1: inside by 0.5 band -> {tri, miss}; outside by 0.5 band too
-    for x, want in ((1 - 0.5e-5 * 5, [-1, 1]), (1 + 0.5e-5 * 5, [-1, 1]), (1 + 3e-5 * 5, [-1])):
+    for x, want in ((1 - 0.5 * EPS_E * 5, [-1, 1]), (1 + 0.5 * EPS_E * 5, [-1, 1]), (1 + 3 * EPS_E * 5, [-1])):
         assert o.ray_candidates([x, 0.5, 0], DZ)[0] == want, x
     # sphere silhouette (centre (1,0,10), r = 1, ray along x = 0): sphere or miss; with a plane
     # behind it: sphere or plane (a robust hit exists, so no miss)
@@ -232,7 +234,7 @@ def test_candidates_sound_under_perturbation():
         cand, n = o.ray_candidates(eye, d)
         assert n == len(cand) and n <= 8, (n, cand)
         assert o.nearest(eye, d)[1] in cand, cand
-        for dq in _perturbed(d, 0.9e-5, rng, 24):
+        for dq in _perturbed(d, 0.9 * EPS_E, rng, 24):
             assert o.nearest(eye, dq)[1] in cand, cand
         sizes.append(n)
     assert max(sizes) >= 2                                  # the cases are near ties indeed
