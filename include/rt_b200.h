@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define RT_ABI_VERSION 1
+#define RT_ABI_VERSION 2
 #define RT_MAX_DEPTH 16          /* max_depth limit (stack sizing)                 */
 #define RT_TILE 16               /* shard tile edge in pixels (16x16 tiles)        */
 #define RT_NUM_COUNTERS 13       /* see rt_counter                                  */
@@ -133,6 +133,10 @@ typedef struct rt_outputs {
     void* shard;                 /* packed tile-major shard (rt_shard_bytes) for the gather  */
     uint32_t shard_format;       /* rt_format of `shard`                                     */
     unsigned long long* counters;/* [RT_NUM_COUNTERS], accumulated when RT_RENDER_COUNT set  */
+    rt_fb composed;              /* stereo composition fused into the pack epilogue (NEXT-1,  */
+    uint32_t compose_mode;       /* PAPER.md:56): RGBA8 only, RT_COMPOSE_* as rt_compose; both */
+                                 /* eyes of a pixel must be traced in the same launch (a whole */
+                                 /* frame, or tile-pair shards; not the world-2 eye split)     */
 } rt_outputs;
 
 /* ------------------------------------------------------------------ context */

@@ -675,10 +675,27 @@ rt_status rtb_render_local(rt_context* c, const rt_render_params* p, const rt_ou
     if (P.stack_entries > rtb::STACK_CAP) return rtb_fail(RT_ERR_SIZE, "BVH too deep (%d levels)", (int)c->info[5]);
     P.n_tiles = (int)n_tiles;
     P.peer_fence = (p->flags & RT_RENDER_PEER_STORE) ? 1 : 0;
+    for (int e = 0; e < 2; ++e)
+        P.fb_vec[e] = P.fb[e] && ((uintptr_t)P.fb[e] % 16 == 0) && (P.fb_pitch[e] % 16 == 0);
+    if (out->composed.dev_ptr) {
+        if (out->composed.format != RT_FORMAT_RGBA8) return rtb_fail(RT_ERR_INVALID_ARG, "composed: RGBA8 only");
+        if (out->compose_mode != RT_COMPOSE_ANAGLYPH && out->compose_mode != RT_COMPOSE_SBS)
+            return rtb_fail(RT_ERR_INVALID_ARG, "composed: mode %u", out->compose_mode);
+        if (g.mode == 1) return rtb_fail(RT_ERR_INVALID_ARG, "composed: the world-2 eye split traces one eye per launch");
+        if (p->flags & (RT_RENDER_COUNT | RT_RENDER_BRUTE_FORCE | RT_RENDER_KDTREE))
+            return rtb_fail(RT_ERR_INVALID_ARG, "composed: product renders only (no COUNT / BRUTE_FORCE / KDTREE)");
+        if (out->compose_mode == RT_COMPOSE_SBS && W < 2) return rtb_fail(RT_ERR_INVALID_ARG, "composed: SBS needs width >= 2");
+        const uint32_t cw = out->compose_mode == RT_COMPOSE_ANAGLYPH ? W : 2 * (W / 2);
+        if ((st = check_fb(out->composed, cw, "composed"))) return st;
+        P.comp = out->composed.dev_ptr;
+        P.comp_pitch = (long long)out->composed.pitch_bytes;
+        P.comp_mode = (int)out->compose_mode;
+        P.comp_vec = ((uintptr_t)P.comp % 16 == 0) && (P.comp_pitch % 16 == 0);
+    }
     if (P.n_work == 0) return RT_OK;
     CUDA_TRY(cudaSetDevice(c->device));
     int occ = 0;
-    const unsigned kflags = p->flags & (RT_RENDER_COUNT | RT_RENDER_BRUTE_FORCE | RT_RENDER_KDTREE);
+    const unsigned kflags = P.comp ? RTB_TRACE_COMPOSE : (p->flags & (RT_RENDER_COUNT | RT_RENDER_BRUTE_FORCE | RT_RENDER_KDTREE));
     CUDA_TRY(rtb_trace_occupancy(kflags, P.stack_entries, &occ));
     if (occ < 1) occ = 1;
     const int block = rtb_trace_block();

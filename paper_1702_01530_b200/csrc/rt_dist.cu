@@ -382,7 +382,7 @@ rt_status rtb_dist_render(rt_context* c, const rt_render_params* p, const rt_out
     if ((st = check_err(D))) return st;
     if (p->flags & ~(RT_RENDER_COUNT | RT_RENDER_BRUTE_FORCE | RT_RENDER_KDTREE))
         return rtb_fail(RT_ERR_INVALID_ARG, "distributed frame: flags 0x%x", p->flags);
-    if (out->prim_id || out->radiance || out->shard)
+    if (out->prim_id || out->radiance || out->shard || out->composed.dev_ptr)
         return rtb_fail(RT_ERR_INVALID_ARG, "distributed frame: framebuffer outputs only (ID / radiance / shard "
                                             "planes need an explicit shard render)");
     if (!c->has_scene) return rtb_fail(RT_ERR_NO_SCENE, "render before rt_scene_upload");

@@ -45,6 +45,11 @@ struct TraceParams {
     int stack_entries;      // BVH traversal stack depth (shared memory, [entry][thread])
     int n_tiles;            // 16x16 tiles in this shard (= n_work / 256)
     int peer_fence;         // framebuffers live in a peer's memory: fence system-wide at exit
+    int fb_vec[2];          // rows 16-byte aligned (base and pitch): vectorised row stores
+    void* comp;             // fused stereo composition output (RGBA8), null = none
+    long long comp_pitch;
+    int comp_mode;          // RT_COMPOSE_ANAGLYPH / RT_COMPOSE_SBS
+    int comp_vec;           // composed rows 16-byte aligned
 };
 
 struct UnpackParams {
@@ -105,7 +110,9 @@ struct KdHost {
 void kd_build_host(const float4* prims, int n, int n_spheres, int max_leaf, int max_depth, KdHost& out);
 }  // namespace rtb
 
-// launchers (rt_trace.cu)
+// launchers (rt_trace.cu); flags = RT_RENDER_COUNT | _BRUTE_FORCE | _KDTREE, or RTB_TRACE_COMPOSE
+// alone (the product kernel with the fused stereo composition in its epilogue)
+constexpr unsigned RTB_TRACE_COMPOSE = 1u << 31;
 cudaError_t rtb_launch_trace(const TraceParams& P, unsigned flags, int grid, cudaStream_t st);
 cudaError_t rtb_trace_occupancy(unsigned flags, int stack_entries, int* blocks_per_sm);
 size_t rtb_trace_smem(int stack_entries);

@@ -124,9 +124,87 @@ __device__ __forceinline__ float3 trace_pixel(const TraceParams& P, float3 o, fl
     return col;
 }
 
+// Pack epilogue (run by the whole warp after its pixel trees): clamp + quantise,
+// then vectorised row stores -- every 4 consecutive lanes hold 4 consecutive pixels of one row
+// (px = 4k + (lane & 3)), which lane 4j gathers by shuffles and writes as one 16-byte (RGBA8) or,
+// per lane pair, 16-byte (RGBA16F) store; rows cut by the image edge fall back to per-pixel stores.
+// Optionally fused with the stereo composition (NEXT-1; "GPU post-processing ...
+// anaglyph/Anamorphic transformation"), which needs both eyes of a pixel (tile
+// pairs: lane l and lane l + 16 hold the same pixel of the left and right eye) or a pixel pair of
+// one eye (lanes l, l ^ 1): anaglyph (L.r, R.g, R.b, 255); side-by-side column-pair means,
+// (a + b + 1) >> 1 per channel, left image in the left half.
+#ifndef RT_PACK_VEC
+#define RT_PACK_VEC 1     // 0: one 4-byte store per lane (measurement variant)
+#endif
+template <bool COMP>
+__device__ __forceinline__ void pack_epilogue(const TraceParams& P, bool valid, int eye, int px, int py, uint32_t v,
+                                              uint2 h) {
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    if (P.fb_fmt[0] == RT_FORMAT_RGBA8 || P.fb_fmt[1] == RT_FORMAT_RGBA8 || COMP) {
+        const uint32_t v1 = __shfl_down_sync(FULL, v, 1, 4), v2 = __shfl_down_sync(FULL, v, 2, 4);
+        const uint32_t v3 = __shfl_down_sync(FULL, v, 3, 4);
+        if (valid && P.fb[eye] && P.fb_fmt[eye] == RT_FORMAT_RGBA8) {
+            char* row = static_cast<char*>(P.fb[eye]) + (long long)py * P.fb_pitch[eye];
+            const bool vec = RT_PACK_VEC && P.fb_vec[eye] && px + 3 < P.W;
+            if (vec) {
+                if ((lane & 3) == 0) reinterpret_cast<uint4*>(row)[px >> 2] = make_uint4(v, v1, v2, v3);
+            } else {
+                reinterpret_cast<uint32_t*>(row)[px] = v;
+            }
+        }
+        if (COMP) {
+            char* row = static_cast<char*>(P.comp) + (long long)py * P.comp_pitch;
+            if (P.comp_mode == RT_COMPOSE_ANAGLYPH) {
+                const uint32_t w = __shfl_xor_sync(FULL, v, 16);          // the other eye, same pixel
+                const uint32_t a = (v & 0xFFu) | (w & 0x00FFFF00u) | 0xFF000000u;
+                const uint32_t a1 = __shfl_down_sync(FULL, a, 1, 4), a2 = __shfl_down_sync(FULL, a, 2, 4);
+                const uint32_t a3 = __shfl_down_sync(FULL, a, 3, 4);
+                if (valid && eye == 0) {
+                    if (P.comp_vec && px + 3 < P.W) {
+                        if ((lane & 3) == 0) reinterpret_cast<uint4*>(row)[px >> 2] = make_uint4(a, a1, a2, a3);
+                    } else {
+                        reinterpret_cast<uint32_t*>(row)[px] = a;
+                    }
+                }
+            } else {
+                const uint32_t w = __shfl_xor_sync(FULL, v, 1);           // the pixel pair (px even, px + 1)
+                uint32_t m = 0xFF000000u;
+#pragma unroll
+                for (int ch = 0; ch < 3; ++ch) {
+                    const uint32_t x = (v >> (8 * ch)) & 0xFFu, y = (w >> (8 * ch)) & 0xFFu;
+                    m |= ((x + y + 1u) >> 1) << (8 * ch);
+                }
+                const uint32_t m2 = __shfl_down_sync(FULL, m, 2, 4);
+                if (valid && (px & 1) == 0 && px + 1 < P.W) {
+                    const int ox = (eye ? P.W / 2 : 0) + (px >> 1);
+                    if (P.comp_vec && px + 3 < P.W && (ox & 1) == 0) {
+                        if ((lane & 3) == 0) reinterpret_cast<uint2*>(row)[ox >> 1] = make_uint2(m, m2);
+                    } else {
+                        reinterpret_cast<uint32_t*>(row)[ox] = m;
+                    }
+                }
+            }
+        }
+    }
+    if (P.fb_fmt[0] == RT_FORMAT_RGBA16F || P.fb_fmt[1] == RT_FORMAT_RGBA16F) {
+        const uint2 h1 = make_uint2(__shfl_down_sync(FULL, h.x, 1, 2), __shfl_down_sync(FULL, h.y, 1, 2));
+        if (valid && P.fb[eye] && P.fb_fmt[eye] == RT_FORMAT_RGBA16F) {
+            char* row = static_cast<char*>(P.fb[eye]) + (long long)py * P.fb_pitch[eye];
+            if (P.fb_vec[eye] && px + 1 < P.W) {
+                if ((lane & 1) == 0) reinterpret_cast<uint4*>(row)[px >> 1] = make_uint4(h.x, h.y, h1.x, h1.y);
+            } else {
+                reinterpret_cast<uint2*>(row)[px] = h;
+            }
+        }
+    }
+}
+
 // Persistent warps: each warp takes 32 consecutive work items (one 8x4 pixel block) per
 // atomic and traces one pixel tree per lane; the BVH stack is in shared memory.
-template <bool COUNT, int ACC>
+// COMP: the pack epilogue also writes the fused stereo composition (a separate instantiation, so
+// the default kernel carries none of its registers)
+template <bool COUNT, int ACC, bool COMP = false>
 __global__ void __launch_bounds__(RT_BLOCK, RT_MINB) k_trace_stereo(const TraceParams P) {
     extern __shared__ int s_stack[];                 // [stack_entries][RT_BLOCK]
     Counters<COUNT> cnt;
@@ -144,7 +222,10 @@ __global__ void __launch_bounds__(RT_BLOCK, RT_MINB) k_trace_stereo(const TraceP
         if (base >= P.n_work) break;
         const int k = base + lane;
         int eye, px, py, lt;
-        if (map_work(P, k, eye, px, py, lt)) {
+        const bool valid = map_work(P, k, eye, px, py, lt);
+        uint32_t v8 = 0u;                            // the pixel packed (only the packed words stay live)
+        uint2 v16 = make_uint2(0u, 0u);
+        if (valid) {
             cnt.add(CNT_PIXELS);
             const float sx = fmaf(2.0f * (px + 0.5f), 1.0f / P.W, -1.0f) * P.cam.tha;
             const float sy = fmaf(-2.0f * (py + 0.5f), 1.0f / P.H, 1.0f) * P.cam.th;
@@ -152,7 +233,6 @@ __global__ void __launch_bounds__(RT_BLOCK, RT_MINB) k_trace_stereo(const TraceP
             int pid = -1;
             const float3 c = trace_pixel<COUNT, ACC>(P, P.cam.eye[eye], d, pid, stk, cnt, s_occ + threadIdx.x);
             const long long pix = ((long long)eye * P.H + py) * P.W + px;
-            if (P.fb[eye]) store_px(P.fb[eye], P.fb_fmt[eye], P.fb_pitch[eye], px, py, c);
             if (P.prim_id) P.prim_id[pix] = pid;
             if (P.radiance) P.radiance[pix] = make_float4(c.x, c.y, c.z, 0.0f);
             if (P.shard) {
@@ -160,7 +240,10 @@ __global__ void __launch_bounds__(RT_BLOCK, RT_MINB) k_trace_stereo(const TraceP
                 if (P.shard_fmt == RT_FORMAT_RGBA8) reinterpret_cast<uint32_t*>(P.shard)[s] = pack_rgba8(c);
                 else reinterpret_cast<uint2*>(P.shard)[s] = pack_rgba16f(c);
             }
+            if (P.fb_fmt[0] == RT_FORMAT_RGBA8 || P.fb_fmt[1] == RT_FORMAT_RGBA8 || COMP) v8 = pack_rgba8(c);
+            if (P.fb_fmt[0] == RT_FORMAT_RGBA16F || P.fb_fmt[1] == RT_FORMAT_RGBA16F) v16 = pack_rgba16f(c);
         }
+        pack_epilogue<COMP>(P, valid, eye, px, py, v8, v16);   // the whole warp: framebuffer rows (+ composition)
     }
     if (P.peer_fence) __threadfence_system();        // peer framebuffer stores visible system-wide
     if (COUNT) {
@@ -252,6 +335,7 @@ __global__ void __launch_bounds__(256) k_ffma_peak(float* out, int iters, float 
 using namespace rtb;
 
 static const void* trace_fn(unsigned flags) {
+    if (flags & RTB_TRACE_COMPOSE) return (const void*)k_trace_stereo<false, ACC_BVH, true>;
     const bool count = flags & RT_RENDER_COUNT;
     const int acc = (flags & RT_RENDER_BRUTE_FORCE) ? ACC_BRUTE : (flags & RT_RENDER_KDTREE) ? ACC_KD : ACC_BVH;
     if (count)

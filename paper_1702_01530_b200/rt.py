@@ -74,7 +74,8 @@ class rt_render_params(C.Structure):
 
 class rt_outputs(C.Structure):
     _fields_ = [("left", rt_fb), ("right", rt_fb), ("prim_id", C.c_void_p), ("radiance", C.c_void_p),
-                ("shard", C.c_void_p), ("shard_format", C.c_uint32), ("counters", C.c_void_p)]
+                ("shard", C.c_void_p), ("shard_format", C.c_uint32), ("counters", C.c_void_p),
+                ("composed", rt_fb), ("compose_mode", C.c_uint32)]
 
 
 _lib = None
@@ -438,7 +439,7 @@ class StereoRenderer:
 
     def render(self, width, height, max_depth, fmt=RT_FORMAT_RGBA8, fb=None, want_id=False, want_radiance=False,
                count=False, brute=False, shard=(0, 1), shard_buf=None, shard_fmt=RT_FORMAT_RGBA8, fb_ptrs=None,
-               peer=False, kdtree=False, stream=None):
+               peer=False, kdtree=False, stream=None, compose=None):
         """Enqueue one stereo render; returns dict of torch device tensors (not synchronised)."""
         t = self.torch
         out = {}
@@ -460,6 +461,11 @@ class StereoRenderer:
         if want_radiance:
             out["radiance"] = t.full((2, height, width, 4), float("nan"), dtype=t.float32, device=self.device)
             o.radiance = out["radiance"].data_ptr()
+        if compose is not None:                     # (mode, (H, W', 4) u8 tensor): fused composition
+            mode, comp = compose
+            o.composed = rt_fb(comp.data_ptr(), RT_FORMAT_RGBA8, comp.stride(0) * comp.element_size())
+            o.compose_mode = mode
+            out["composed"] = comp
         if shard_buf is not None:
             o.shard = shard_buf.data_ptr()
             o.shard_format = shard_fmt

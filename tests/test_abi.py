@@ -24,7 +24,7 @@ def test_library_exports_every_declared_symbol():
     L = rt.lib()
     for name in syms:
         assert getattr(L, name) is not None
-    assert rt.rt_version() == 1
+    assert rt.rt_version() == 2
 
 
 def test_library_is_sm100a_only():

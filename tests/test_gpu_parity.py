@@ -419,6 +419,37 @@ def test_compose_anaglyph_sbs(R, W, H):
         np.testing.assert_array_equal(out.cpu().numpy(), compose(g["fb"][0], g["fb"][1], name))
 
 
+@pytest.mark.parametrize("W,H", [(93, 61), (64, 40), (1920, 1080)])
+def test_fused_compose_in_pack_epilogue(R, W, H):
+    """NEXT-1 as specified (SURVEY §8(f): anaglyph / SBS "fused into the pack epilogue";
+    PAPER.md:56): the composition written by the trace kernel's epilogue equals the oracle's
+    composition of the same frame's bytes (SPEC S:442-460 integer formulas) and the separate
+    rt_compose pass, bit for bit, and leaves the framebuffers themselves unchanged.  Odd, 16-byte
+    aligned and 1080p widths (vectorised and per-pixel row stores)."""
+    from oracle.oracle import compose
+    s = scenes.scene_c2().with_view(width=W, height=H, max_depth=2)
+    plain = gpu_render(R, s)["fb"]
+    for mode, name in ((rt.RT_COMPOSE_ANAGLYPH, "anaglyph"), (rt.RT_COMPOSE_SBS, "sbs")):
+        ow = W if name == "anaglyph" else 2 * (W // 2)
+        comp = torch.zeros((H, ow, 4), dtype=torch.uint8, device="cuda")
+        g = gpu_render(R, s, compose=(mode, comp))
+        np.testing.assert_array_equal(g["fb"], plain)
+        np.testing.assert_array_equal(g["composed"], compose(plain[0], plain[1], name))
+        sep = torch.zeros_like(comp)
+        fb = torch.from_numpy(plain).cuda()
+        rt.rt_compose(R.ctx, rt.rt_fb(fb[0].data_ptr(), 0, W * 4), rt.rt_fb(fb[1].data_ptr(), 0, W * 4), W, H, mode,
+                      rt.rt_fb(sep.data_ptr(), 0, ow * 4))
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(g["composed"], sep.cpu().numpy())
+    # composition only (no framebuffers), and the eye-split shard cannot compose
+    comp = torch.zeros((H, W, 4), dtype=torch.uint8, device="cuda")
+    R.render(W, H, 2, fb=False, compose=(rt.RT_COMPOSE_ANAGLYPH, comp))
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(comp.cpu().numpy(), compose(plain[0], plain[1], "anaglyph"))
+    with pytest.raises(rt.RtError):
+        R.render(W, H, 2, fb=False, shard=(0, 2), compose=(rt.RT_COMPOSE_ANAGLYPH, comp))
+
+
 def test_refit_moving_mesh(R):
     """NEXT-3: rt_scene_update_vertices refits the device BVH for moved vertices.  The refit
     tree must give exactly the image of a fresh upload/rebuild of the moved scene (both equal
