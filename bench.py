@@ -577,7 +577,10 @@ def l1_roofline(prof, ceil, kernel_ms, sm_mhz):
     peak = 148 * ceil["l1_bytes_clk_sm"] * sm_mhz * 1e6 / 1e9
     ach = prof["l1tex_t_bytes"] / (kernel_ms * 1e-3) / 1e9
     return {"l1": {"achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-                   "bytes_per_launch": prof["l1tex_t_bytes"], "source": prof.get("source")}}
+                   "bytes_per_launch": prof["l1tex_t_bytes"],
+                   "data_pipe_wavefronts_pct_of_peak": prof.get("l1tex_data_pipe_lsu_wavefronts_pct_peak"),
+                   "note": "bytes = L1 tag lookups x 32 B; the L1 data pipe is the tighter L1 limit: incoherent "
+                           "128-bit loads cost one wavefront per distinct line", "source": prof.get("source")}}
 
 
 def load_traffic(name, world):
