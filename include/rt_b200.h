@@ -245,8 +245,12 @@ rt_status rt_upload(rt_context* ctx, const void* host_src, void* dev_dst, size_t
  * both eyes, to rank t mod world, so a rank's shard-local tile lt is G = 2 (rank + (lt div 2)
  * world) + (lt mod 2): the two eyes of a tile are traced together (one warp = the same 4x4
  * pixel block in both eyes).
- * rt_shard_tiles writes rank's global tile ids G (ascending) into tile_ids (may be NULL to
- * query the count) and their number into *n_tiles.  Pure host functions, no context. */
+ * Environment RT_SHARD_BLOCK=B > 1 (read once per process, the same on every rank) deals the tile
+ * pairs in B x B blocks of tiles instead (blocks in raster order, block b -> rank b mod world, tiles
+ * raster order inside a block): every rank's tiles are spatially compact.
+ * rt_shard_tiles writes rank's global tile ids G (ascending; block-major with RT_SHARD_BLOCK) into
+ * tile_ids (may be NULL to query the count) and their number into *n_tiles.  Pure host functions,
+ * no context. */
 rt_status rt_shard_tiles(uint32_t width, uint32_t height, uint32_t rank, uint32_t world,
                          uint32_t* n_tiles, uint32_t* tile_ids);
 /* Bytes of one rank's packed shard, padded to the largest rank (equal gather counts):

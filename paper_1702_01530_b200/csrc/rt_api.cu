@@ -157,6 +157,8 @@ rt_status rt_destroy(rt_context* c) {
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
     free_scene(c);
+    for (auto& e : c->tile_tables) e.buf.release();
+    c->tile_tables.clear();
     for (auto& m : c->ipc_maps) cudaIpcCloseMemHandle(m.ptr);
     c->ipc_maps.clear();
     if (c->work_counter) cudaFree(c->work_counter);
@@ -563,6 +565,7 @@ rt_status fill_camera(rt_context* c, uint32_t W, uint32_t H, rtb::DevCamera& cam
 
 struct ShardGeom {
     int tiles_x, tiles_y, tiles_per_eye, mode;
+    int block;              // mode 2: tile pairs dealt in B x B blocks of tiles (1 = single tiles)
 };
 
 ShardGeom shard_geom(uint32_t W, uint32_t H, uint32_t world) {
@@ -574,11 +577,29 @@ ShardGeom shard_geom(uint32_t W, uint32_t H, uint32_t world) {
     // rank and the root must see the same value) deals tile pairs at world 2 as well.
     static const bool pairs_at_2 = [] { const char* e = getenv("RT_SHARD_PAIRS"); return e && atoi(e) != 0; }();
     g.mode = world == 1 ? 0 : (world == 2 && !pairs_at_2 ? 1 : 2);
+    // RT_SHARD_BLOCK=B (read once per process; every rank must see the same value): tile pairs are
+    // dealt to ranks in B x B blocks of tiles (raster order of blocks, block b -> rank b mod world),
+    // so a rank's tiles are spatially compact; 1 (default) = single tiles round-robin
+    static const int block = [] { const char* e = getenv("RT_SHARD_BLOCK"); return e ? std::max(1, atoi(e)) : 1; }();
+    g.block = g.mode == 2 ? block : 1;
     return g;
+}
+
+// mode 2 with blocks: this rank's tile indices (raster order inside each of its blocks)
+std::vector<uint32_t> block_tiles(const ShardGeom& g, uint32_t rank, uint32_t world) {
+    std::vector<uint32_t> t;
+    const int B = g.block, nbx = (g.tiles_x + B - 1) / B, nby = (g.tiles_y + B - 1) / B;
+    for (int b = (int)rank; b < nbx * nby; b += (int)world) {
+        const int bx = b % nbx, by = b / nbx;
+        for (int y = by * B; y < std::min(g.tiles_y, by * B + B); ++y)
+            for (int x = bx * B; x < std::min(g.tiles_x, bx * B + B); ++x) t.push_back((uint32_t)(y * g.tiles_x + x));
+    }
+    return t;
 }
 
 uint32_t shard_count(const ShardGeom& g, uint32_t rank, uint32_t world) {
     if (g.mode == 1) return (uint32_t)g.tiles_per_eye;
+    if (g.block > 1) return 2u * (uint32_t)block_tiles(g, rank, world).size();
     const int pairs = (int)rank < g.tiles_per_eye ? (g.tiles_per_eye - (int)rank + (int)world - 1) / (int)world : 0;
     return 2u * (uint32_t)pairs;
 }
@@ -586,7 +607,34 @@ uint32_t shard_count(const ShardGeom& g, uint32_t rank, uint32_t world) {
 // global tile id G: eye = G & 1, tile = G >> 1 (eyes interleaved)
 uint32_t shard_tile(const ShardGeom& g, uint32_t rank, uint32_t world, uint32_t lt) {
     if (g.mode == 1) return 2u * lt + rank;
+    if (g.block > 1) return 2u * block_tiles(g, rank, world)[lt >> 1] + (lt & 1u);
     return 2u * (rank + (lt >> 1) * world) + (lt & 1u);
+}
+
+// device copy of a tile table (cached per layout): one rank's tiles (render) or every rank's,
+// padded with -1 to the largest rank (unpack)
+rt_status tile_table(rt_context* c, const ShardGeom& g, uint32_t W, uint32_t H, int rank, uint32_t world, uint32_t pad,
+                     const int** out) {
+    for (auto& e : c->tile_tables)
+        if (e.W == W && e.H == H && e.rank == rank && e.world == world && e.block == g.block) {
+            *out = static_cast<const int*>(e.buf.p);
+            return RT_OK;
+        }
+    std::vector<int> h;
+    for (uint32_t r = (rank < 0 ? 0u : (uint32_t)rank); r < (rank < 0 ? world : (uint32_t)rank + 1); ++r) {
+        const std::vector<uint32_t> t = block_tiles(g, r, world);
+        for (uint32_t x : t) h.push_back((int)x);
+        for (size_t k = t.size(); rank < 0 && k < pad; ++k) h.push_back(-1);
+    }
+    if (h.empty()) h.push_back(-1);
+    RtTileTable e;
+    e.W = W; e.H = H; e.rank = rank; e.world = world; e.block = g.block;
+    e.buf.bytes = h.size() * sizeof(int);
+    CUDA_TRY(cudaMalloc(&e.buf.p, e.buf.bytes));
+    CUDA_TRY(cudaMemcpy(e.buf.p, h.data(), e.buf.bytes, cudaMemcpyHostToDevice));   // once per layout
+    c->tile_tables.push_back(e);
+    *out = static_cast<const int*>(e.buf.p);
+    return RT_OK;
 }
 
 rt_status check_fb(const rt_fb& fb, uint32_t W, const char* name) {
@@ -660,6 +708,11 @@ rt_status rtb_render_local(rt_context* c, const rt_render_params* p, const rt_ou
     P.shard_mode = g.mode;
     P.shard_rank = (int)p->shard_rank;
     P.shard_world = (int)p->shard_world;
+    P.tile_list = nullptr;
+    if (g.mode == 2 && g.block > 1) {
+        CUDA_TRY(cudaSetDevice(c->device));
+        if ((st = tile_table(c, g, W, H, (int)p->shard_rank, p->shard_world, 0, &P.tile_list))) return st;
+    }
     P.fb[0] = out->left.dev_ptr;
     P.fb[1] = out->right.dev_ptr;
     P.fb_fmt[0] = (int)out->left.format;
@@ -893,7 +946,10 @@ rt_status rtb_unpack_on(rt_context* c, const void* gathered, uint32_t W, uint32_
     U.tiles_per_rank = (int)(per / (256u * (format == RT_FORMAT_RGBA8 ? 4u : 8u)));
     U.world = (int)world;
     U.shard_mode = g.mode;
+    U.gtile = nullptr;
     CUDA_TRY(cudaSetDevice(c->device));
+    if (g.mode == 2 && g.block > 1 && (st = tile_table(c, g, W, H, -1, world, (uint32_t)U.tiles_per_rank / 2, &U.gtile)))
+        return st;
     CUDA_TRY(rtb_launch_unpack(gathered, U, stream));
     return RT_OK;
 }

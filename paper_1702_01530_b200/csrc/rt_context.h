@@ -47,6 +47,13 @@ struct DevBuf {
 
 struct DistState;   // rt_dist.cu: multi-GPU frame assembly (rt_dist_init)
 
+// device tile table of a block shard layout (RT_SHARD_BLOCK > 1), cached per layout
+struct RtTileTable {
+    uint32_t W = 0, H = 0, world = 0;
+    int rank = 0, block = 1;    // rank -1: every rank's tiles (unpack)
+    DevBuf buf;
+};
+
 struct rt_event {
     cudaEvent_t ev = nullptr;
 };
@@ -103,6 +110,7 @@ struct rt_context {
     DevBuf kd_nodes_buf, kd_refs_buf;
     // multi-GPU frame assembly (rt_dist_init); null = single GPU
     DistState* dist = nullptr;
+    std::vector<RtTileTable> tile_tables;
 };
 
 // Enqueue one render of params/outputs exactly as given (one GPU, no frame assembly); rt_api.cu.

@@ -34,6 +34,7 @@ struct TraceParams {
     int tiles_x, tiles_per_eye;
     int shard_mode;         // 0 one rank, 1 eye split (world 2), 2 tile pairs round-robin (world >= 3)
     int shard_rank, shard_world;
+    const int* tile_list;   // mode 2 block layout: this rank's tile indices (null = round-robin tiles)
     void* fb[2];
     int fb_fmt[2];
     long long fb_pitch[2];
@@ -59,6 +60,7 @@ struct UnpackParams {
     int fmt;
     int W, H, tiles_x, tiles_per_eye, tiles_per_rank;
     int world, shard_mode;
+    const int* gtile;       // block layout: [world][tiles_per_rank / 2] tile indices, -1 pad (null = round-robin)
 };
 
 // BVH build scratch (device pointers), owned by the context.

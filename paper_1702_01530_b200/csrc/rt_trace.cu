@@ -270,8 +270,8 @@ __global__ void k_unpack_shards(const void* __restrict__ gathered, UnpackParams 
             if (lt >= U.tiles_per_eye) continue;
             g = 2 * lt + rank;
         } else {
-            const int t = rank + (lt >> 1) * U.world;
-            if (t >= U.tiles_per_eye) continue;
+            const int t = U.gtile ? U.gtile[rank * (U.tiles_per_rank >> 1) + (lt >> 1)] : rank + (lt >> 1) * U.world;
+            if (t < 0 || t >= U.tiles_per_eye) continue;
             g = 2 * t + (lt & 1);
         }
         const int eye = g & 1;

@@ -86,7 +86,7 @@ __device__ __forceinline__ bool map_work(const Params& P, int k, int& eye, int& 
         const int q = k >> 9, wp = (k >> 5) & 15;         // tile pair of this rank, warp of the pair
         eye = lane >> 4;
         lt = 2 * q + eye;
-        t = P.shard_rank + q * P.shard_world;
+        t = P.tile_list ? __ldg(&P.tile_list[q]) : P.shard_rank + q * P.shard_world;
         px = (t % P.tiles_x) * TILE + (wp & 3) * 4 + (lane & 3);
         py = (t / P.tiles_x) * TILE + (wp >> 2) * 4 + ((lane >> 2) & 3);
     }

@@ -144,6 +144,37 @@ def test_shard_pairs_knob_at_world_2():
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr
 
 
+@pytest.mark.parametrize("block", [2, 3, 8])
+def test_shard_block_layout(block):
+    """RT_SHARD_BLOCK=B: tile pairs dealt to ranks in B x B blocks of tiles -- exact
+    cover of both eyes, both eyes of a tile on one rank, every rank's tiles grouped by block, and
+    the host unpack reassembles the image for worlds 3, 4 and 8."""
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, sys; sys.path.insert(0, %r); sys.path.insert(0, %r)\n"
+        "from paper_1702_01530_b200 import rt\n"
+        "import test_abi as t\n"
+        "B = %d\n"
+        "for W, H in ((93, 61), (1920, 1080), (17, 40)):\n"
+        "    tx, ty = -(-W // 16), -(-H // 16); T = tx * ty\n"
+        "    for world in (3, 4, 8):\n"
+        "        ids = [rt.rt_shard_tiles(W, H, r, world).astype(int) for r in range(world)]\n"
+        "        allg = np.concatenate(ids)\n"
+        "        assert sorted(allg.tolist()) == list(range(2 * T)), (W, H, world)\n"
+        "        for r, a in enumerate(ids):\n"
+        "            assert all(((g >> 1) == (h >> 1)) and g %% 2 == 0 and h == g + 1 for g, h in zip(a[0::2], a[1::2]))\n"
+        "            blocks = [((g >> 1) %% tx // B) + (((g >> 1) // tx) // B) * (-(-tx // B)) for g in a[0::2]]\n"
+        "            assert all(b %% world == r for b in blocks) and blocks == sorted(blocks)\n"
+        "        g = t.synth_shards(W, H, world)\n"
+        "        L, R = rt.rt_unpack_shards_host(g.view(np.uint8).reshape(-1), W, H, world)\n"
+        "        np.testing.assert_array_equal(np.stack([L, R]).view(np.uint32)[..., 0], t.expected_image(W, H))\n"
+        "print('ok')\n") % (ROOT, os.path.join(ROOT, "tests"), block)
+    env = dict(os.environ, RT_SHARD_BLOCK=str(block))
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-3000:]
+
+
 def test_product_package_never_touches_the_oracle():
     """The product path must not import/link/execute oracle/ (it is test infrastructure)."""
     pkg = os.path.join(ROOT, "paper_1702_01530_b200")

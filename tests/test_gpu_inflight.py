@@ -142,3 +142,37 @@ def test_scene_change_waits_for_renders_in_flight(R):
     torch.cuda.synchronize()
     for k in range(8):
         assert torch.equal(fbs[k], ref_a), f"frame {k} saw the refit"
+
+
+_BLOCK_CODE = r"""
+import sys; sys.path.insert(0, %r)
+import numpy as np, torch
+from paper_1702_01530_b200 import rt, scenes
+R = rt.StereoRenderer(0)
+s = scenes.scene_c2().with_view(width=93, height=61, max_depth=3)
+R.upload(s); R.set_camera(s.rig)
+ref = R.render(s.width, s.height, s.max_depth)["fb"].clone()
+for world in (3, 4, 8):
+    fb = R.alloc_fb(s.width, s.height); fb.zero_()
+    per = rt.rt_shard_bytes(s.width, s.height, world)
+    gathered = torch.zeros(world * per, dtype=torch.uint8, device="cuda")
+    for r in range(world):
+        R.render(s.width, s.height, s.max_depth, fb=fb, shard=(r, world))
+        R.render(s.width, s.height, s.max_depth, fb=False, shard=(r, world), shard_buf=gathered[r * per:(r + 1) * per])
+    fb2 = torch.zeros_like(fb)
+    rt.rt_unpack_shards(R.ctx, gathered.data_ptr(), s.width, s.height, world, rt.RT_FORMAT_RGBA8,
+                        rt.rt_fb(fb2[0].data_ptr(), 0, s.width * 4), rt.rt_fb(fb2[1].data_ptr(), 0, s.width * 4))
+    torch.cuda.synchronize()
+    assert torch.equal(fb, ref), world
+    assert torch.equal(fb2, ref), world
+print("ok")
+"""
+
+
+def test_block_shard_layout_bit_exact():
+    """RT_SHARD_BLOCK=4 (tile pairs dealt in 4x4-tile blocks): every rank's shard
+    rendered into the frame, and packed + unpacked on the device, gives the single-launch image."""
+    import subprocess
+    env = dict(os.environ, RT_SHARD_BLOCK="4")
+    r = subprocess.run([sys.executable, "-c", _BLOCK_CODE % ROOT], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-3000:]
