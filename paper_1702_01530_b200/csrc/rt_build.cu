@@ -11,8 +11,8 @@
 //                    from common-prefix lengths (__clzll)
 //   k_refit          bottom-up AABB union with atomic arrival counters
 //   k_gather_prims   primitive records in leaf order
-//   k_sah_subtrees   maximal subtrees of <= 16384 primitives rebuilt by binned SAH, one CTA each
-//                    (k_sah_roots finds them)
+//   k_sah_level      maximal subtrees of <= 16384 primitives rebuilt by binned SAH, all at once,
+//                    level by level, one warp per node (k_sah_roots finds them, k_sah_init seeds)
 //   k_treelets       SAH treelet restructuring of the BVH2 (Karras & Aila 2013), optional passes
 //   k_wide           BVH2 -> 4-wide BVH collapse (level by level), small subtrees -> leaves
 // The result is a deterministic function of the input arrays.
@@ -528,16 +528,21 @@ __global__ void k_wide(BuildBuffers B, const int2* __restrict__ fin, int n_in, i
 }
 
 // ---------------------------------------------------------------- SAH subtrees
-// Every maximal LBVH subtree of at most SAH_T primitives (a contiguous Morton range [a, b] of
-// leaf slots) is rebuilt top-down by binned SAH (3 axes x SAH_BINS bins, centroid binning) by one
-// CTA (bins in shared memory, item order in global scratch); the subtree keeps its root id and
-// reuses its internal node ids, so the nodes above it are unchanged.  Partitions are stable and
-// the ids are taken in a fixed order: the result is deterministic.  Runs before the treelet
-// passes (parents are rewritten for them).  C4: node visits 16.2 -> 15.5 per ray, bench +4.3 %,
-// build 45 -> ~210 ms (DESIGN.md §5 v21).
+// Every maximal LBVH subtree of at most SAH_T primitives (a contiguous Morton range [a, a + m) of
+// leaf slots) is rebuilt top-down by binned SAH (3 axes x SAH_BINS bins, centroid binning).  The
+// rebuild is level-synchronous over ALL subtrees at once: one warp per task (a node and its item
+// range), bins in the warp's slice of shared memory, the split search as warp scans over the 32
+// bins, a stable ballot partition; the children become the next level's tasks.  Node ids need no
+// allocation: in a Karras LBVH the internal ids of a subtree over slots [a, a + m) are its root id
+// and exactly [a + 1, a + m - 2], and the rule "left child = split position, right child = split
+// position + 1" assigns that same set to ANY binary tree over the range (each internal node's id is
+// its first or last position; two nodes could only share one if one were a leaf), so the subtree
+// keeps its root and the nodes above it stay valid, and the result does not depend on the order
+// tasks run in: the build is deterministic.  Runs before the treelet passes.  C4: node visits 16.2
+// -> 15.5 per ray, bench +4.3 % (DESIGN.md §5 v21).
 constexpr int SAH_T = 16384;
 constexpr int SAH_BINS = 32;
-constexpr int SAH_THREADS = 256;
+constexpr int SAH_WARPS = 8;                 // warps (tasks) per CTA
 
 __global__ void k_sah_roots(BuildBuffers B, int n, int* roots, int* n_roots) {
     for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n - 1; v += gridDim.x * blockDim.x) {
@@ -557,232 +562,206 @@ __global__ void k_sah_roots(BuildBuffers B, int n, int* roots, int* n_roots) {
 // therefore the BVH4 and its traversal stack, STACK_CAP) stays within SAH_MAX_DEPTH levels.
 constexpr int SAH_MAX_DEPTH = 60;
 
-struct SahShared {
-    int4 stack[40];                     // (begin, end, node, depth); the smaller child is taken first
-    unsigned int bmin[3][SAH_BINS][3], bmax[3][SAH_BINS][3];
-    int bcnt[3][SAH_BINS];
-    float red[SAH_THREADS / 32][12];
-    float nb[12];
-    int sp, next_id, best_axis, best_bin, nl, warp_off[SAH_THREADS / 32 + 1];
-};
-
 __device__ __forceinline__ int ceil_log2(int n) { return n <= 1 ? 0 : 32 - __clz(n - 1); }
 
 __device__ __forceinline__ int sah_bin(float c, float lo, float k) {
     return min(SAH_BINS - 1, max(0, (int)((c - lo) * k)));
 }
 
-// Item arrays live in global scratch at the subtree's slot range [a, a + m): idx / tmp (item
-// order, permuted by the partitions), ids (the old subtree's internal ids, root first; also the
-// DFS stack that collects them); item boxes are read from the leaf boxes.
-__global__ void __launch_bounds__(SAH_THREADS) k_sah_subtrees(BuildBuffers B, const int* __restrict__ roots,
-                                                              int* gidx, int* gtmp, int* gids, int* gdfs) {
-    __shared__ SahShared S;
-    const int root = roots[blockIdx.x];
+// one warp per root: item slots [a, a + m) in order, the root's depth, the level-0 task
+__global__ void k_sah_init(BuildBuffers B, const int* __restrict__ roots, int n_roots, int* idx, int4* tasks) {
+    const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (w >= n_roots) return;
+    const int root = roots[w];
     const int2 rg = B.range[root];
-    const int a = rg.x, m = rg.y - rg.x + 1;
-    int* idx = gidx + a;
-    int* tmp = gtmp + a;
-    int* ids = gids + a;
-    const float4* llo = B.leaf_lo + a;
-    const float4* lhi = B.leaf_hi + a;
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    for (int k = tid; k < m; k += SAH_THREADS) idx[k] = k;
-    if (tid == 0) {                                      // the old subtree's internal ids, root first
-        int* dfs = gdfs + a;
-        int cnt = 0, sp = 0;
-        dfs[sp++] = root;
-        while (sp) {
-            const int v = dfs[--sp];
-            ids[cnt++] = v;
-            const int l = B.left[v], r = B.right[v];
-            if (l >= 0) dfs[sp++] = l;
-            if (r >= 0) dfs[sp++] = r;
-        }
-        int d0 = 0;                                      // depth of the subtree root in the BVH2
+    for (int k = rg.x + lane; k <= rg.y; k += 32) idx[k] = k;
+    if (lane == 0) {
+        int d0 = 0;
         for (int v = B.parent_int[root]; v >= 0; v = B.parent_int[v]) ++d0;
-        S.sp = 1;
-        S.stack[0] = make_int4(0, m, root, d0);
-        S.next_id = 1;
+        tasks[w] = make_int4(rg.x, rg.y + 1, root, d0);
     }
-    __syncthreads();
-    while (S.sp > 0) {
-        const int4 t = S.stack[S.sp - 1];
-        __syncthreads();
-        if (tid == 0) --S.sp;
-        const int begin = t.x, end = t.y, node = t.z, cnt = end - begin, depth = t.w;
-        // depth budget reached: median split (balanced below this node)
-        const bool median = depth + ceil_log2(cnt) >= SAH_MAX_DEPTH;
-        // node box and centroid bounds
-        float v[12];
+}
+
+struct SahWarpBins {
+    int cnt[3][SAH_BINS];
+    unsigned int lo[3][3][SAH_BINS], hi[3][3][SAH_BINS];    // [axis][component][bin], ordered floats
+};
+
+// One level: task (begin, end, node, depth) per warp over item slots idx[begin, end).
+__global__ void __launch_bounds__(32 * SAH_WARPS) k_sah_level(BuildBuffers B, const int4* __restrict__ tasks,
+                                                              int n_tasks, int4* next, int* n_next, int* idx, int* tmp) {
+    __shared__ SahWarpBins bins[SAH_WARPS];
+    const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+    const int w = blockIdx.x * SAH_WARPS + wl;
+    if (w >= n_tasks) return;
+    const unsigned FULL = 0xffffffffu;
+    const int4 t = tasks[w];
+    const int begin = t.x, end = t.y, node = t.z, depth = t.w, cnt = end - begin;
+    const bool median = depth + ceil_log2(cnt) >= SAH_MAX_DEPTH;   // depth budget: balanced below
+    // node box and centroid bounds
+    float v[12];
 #pragma unroll
-        for (int q = 0; q < 3; ++q) { v[q] = FLT_MAX; v[3 + q] = -FLT_MAX; v[6 + q] = FLT_MAX; v[9 + q] = -FLT_MAX; }
-        for (int i = begin + tid; i < end; i += SAH_THREADS) {
+    for (int q = 0; q < 3; ++q) { v[q] = FLT_MAX; v[3 + q] = -FLT_MAX; v[6 + q] = FLT_MAX; v[9 + q] = -FLT_MAX; }
+    for (int i = begin + lane; i < end; i += 32) {
+        const int k = idx[i];
+        const float4 l4 = B.leaf_lo[k], h4 = B.leaf_hi[k];
+        const float l[3] = {l4.x, l4.y, l4.z}, h[3] = {h4.x, h4.y, h4.z};
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            const float c = 0.5f * (l[q] + h[q]);
+            v[q] = fminf(v[q], l[q]); v[3 + q] = fmaxf(v[3 + q], h[q]);
+            v[6 + q] = fminf(v[6 + q], c); v[9 + q] = fmaxf(v[9 + q], c);
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < 12; ++q) {
+        const bool mx = (q >= 3 && q < 6) || q >= 9;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const float o = __shfl_xor_sync(FULL, v[q], off);
+            v[q] = mx ? fmaxf(v[q], o) : fminf(v[q], o);
+        }
+    }
+    if (lane == 0) {
+        B.node_lo[node] = make_float4(v[0], v[1], v[2], 0.f);
+        B.node_hi[node] = make_float4(v[3], v[4], v[5], 0.f);
+    }
+    float kq[3];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        const float ext = v[9 + q] - v[6 + q];
+        kq[q] = ext > 0.0f ? SAH_BINS * (1.0f - 1e-6f) / ext : 0.0f;
+    }
+    int ax = -1, nl = cnt / 2, bbin = 0;                 // no split found: halve the list
+    if (cnt > 2 && !median) {
+        SahWarpBins& S = bins[wl];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            S.cnt[q][lane] = 0;
+#pragma unroll
+            for (int e = 0; e < 3; ++e) { S.lo[q][e][lane] = 0xffffffffu; S.hi[q][e][lane] = 0u; }
+        }
+        __syncwarp();
+        for (int i = begin + lane; i < end; i += 32) {
             const int k = idx[i];
-            const float4 l4 = llo[k], h4 = lhi[k];
+            const float4 l4 = B.leaf_lo[k], h4 = B.leaf_hi[k];
             const float l[3] = {l4.x, l4.y, l4.z}, h[3] = {h4.x, h4.y, h4.z};
 #pragma unroll
             for (int q = 0; q < 3; ++q) {
-                const float c = 0.5f * (l[q] + h[q]);
-                v[q] = fminf(v[q], l[q]); v[3 + q] = fmaxf(v[3 + q], h[q]);
-                v[6 + q] = fminf(v[6 + q], c); v[9 + q] = fmaxf(v[9 + q], c);
+                if (kq[q] == 0.0f) continue;
+                const int b = sah_bin(0.5f * (l[q] + h[q]), v[6 + q], kq[q]);
+                atomicAdd(&S.cnt[q][b], 1);
+#pragma unroll
+                for (int e = 0; e < 3; ++e) {
+                    atomicMin(&S.lo[q][e][b], f2ord(l[e]));
+                    atomicMax(&S.hi[q][e][b], f2ord(h[e]));
+                }
             }
         }
-#pragma unroll
-        for (int q = 0; q < 12; ++q) {
-            const bool mx = (q >= 3 && q < 6) || q >= 9;
-            for (int off = 16; off > 0; off >>= 1) {
-                const float o = __shfl_xor_sync(0xffffffffu, v[q], off);
-                v[q] = mx ? fmaxf(v[q], o) : fminf(v[q], o);
-            }
-        }
-        if (lane == 0)
-            for (int q = 0; q < 12; ++q) S.red[wid][q] = v[q];
-        for (int q = tid; q < 3 * SAH_BINS * 3; q += SAH_THREADS) {
-            (&S.bmin[0][0][0])[q] = 0xffffffffu;
-            (&S.bmax[0][0][0])[q] = 0u;
-        }
-        for (int q = tid; q < 3 * SAH_BINS; q += SAH_THREADS) (&S.bcnt[0][0])[q] = 0;
-        __syncthreads();
-        if (tid < 12) {
-            const bool mx = (tid >= 3 && tid < 6) || tid >= 9;
-            float x = S.red[0][tid];
-            for (int w = 1; w < SAH_THREADS / 32; ++w) x = mx ? fmaxf(x, S.red[w][tid]) : fminf(x, S.red[w][tid]);
-            S.nb[tid] = x;
-        }
-        __syncthreads();
-        if (tid == 0) {
-            B.node_lo[node] = make_float4(S.nb[0], S.nb[1], S.nb[2], 0.f);
-            B.node_hi[node] = make_float4(S.nb[3], S.nb[4], S.nb[5], 0.f);
-        }
-        // bin centroids on every axis with extent
-        float kq[3];
-#pragma unroll
+        __syncwarp();
+        // split search: lane = bin; prefix (bins <= lane) and suffix (bins > lane) by warp scans
+        unsigned long long best = ~0ull;                 // (cost bits << 32) | (axis * 32 + bin)
+        int best_nl = 0;
         for (int q = 0; q < 3; ++q) {
-            const float ext = S.nb[9 + q] - S.nb[6 + q];
-            kq[q] = ext > 0.0f ? SAH_BINS * (1.0f - 1e-6f) / ext : 0.0f;
-        }
-        if (cnt > 2 && !median) {
-            for (int i = begin + tid; i < end; i += SAH_THREADS) {
-                const int k = idx[i];
-                const float4 l4 = llo[k], h4 = lhi[k];
-                const float l[3] = {l4.x, l4.y, l4.z}, h[3] = {h4.x, h4.y, h4.z};
+            if (kq[q] == 0.0f) continue;
+            const int c = S.cnt[q][lane];
+            float bl[3], bh[3];
 #pragma unroll
-                for (int q = 0; q < 3; ++q) {
-                    if (kq[q] == 0.0f) continue;
-                    const int b = sah_bin(0.5f * (l[q] + h[q]), S.nb[6 + q], kq[q]);
-                    atomicAdd(&S.bcnt[q][b], 1);
+            for (int e = 0; e < 3; ++e) {
+                bl[e] = c ? ord2f(S.lo[q][e][lane]) : FLT_MAX;
+                bh[e] = c ? ord2f(S.hi[q][e][lane]) : -FLT_MAX;
+            }
+            int pc = c, sc = c;
+            float pl[3], ph[3], sl[3], sh[3];
 #pragma unroll
-                    for (int e = 0; e < 3; ++e) {
-                        atomicMin(&S.bmin[q][b][e], f2ord(l[e]));
-                        atomicMax(&S.bmax[q][b][e], f2ord(h[e]));
-                    }
+            for (int e = 0; e < 3; ++e) { pl[e] = sl[e] = bl[e]; ph[e] = sh[e] = bh[e]; }
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const int uc = __shfl_up_sync(FULL, pc, off), dc = __shfl_down_sync(FULL, sc, off);
+                float ul[3], uh[3], dl[3], dh[3];
+#pragma unroll
+                for (int e = 0; e < 3; ++e) {
+                    ul[e] = __shfl_up_sync(FULL, pl[e], off); uh[e] = __shfl_up_sync(FULL, ph[e], off);
+                    dl[e] = __shfl_down_sync(FULL, sl[e], off); dh[e] = __shfl_down_sync(FULL, sh[e], off);
+                }
+                if (lane >= off) {
+                    pc += uc;
+#pragma unroll
+                    for (int e = 0; e < 3; ++e) { pl[e] = fminf(pl[e], ul[e]); ph[e] = fmaxf(ph[e], uh[e]); }
+                }
+                if (lane + off < 32) {
+                    sc += dc;
+#pragma unroll
+                    for (int e = 0; e < 3; ++e) { sl[e] = fminf(sl[e], dl[e]); sh[e] = fmaxf(sh[e], dh[e]); }
                 }
             }
+            // right side of a split after bin `lane` = suffix of bin lane + 1
+            const int rc = __shfl_down_sync(FULL, sc, 1);
+            float rl[3], rh[3];
+#pragma unroll
+            for (int e = 0; e < 3; ++e) { rl[e] = __shfl_down_sync(FULL, sl[e], 1); rh[e] = __shfl_down_sync(FULL, sh[e], 1); }
+            if (lane < SAH_BINS - 1 && pc > 0 && rc > 0) {
+                const float cost = area3(f3(pl[0], pl[1], pl[2]), f3(ph[0], ph[1], ph[2])) * pc +
+                                   area3(f3(rl[0], rl[1], rl[2]), f3(rh[0], rh[1], rh[2])) * rc;
+                const unsigned long long key = ((unsigned long long)__float_as_uint(cost) << 32) | (unsigned)(q * 32 + lane);
+                if (key < best) { best = key; best_nl = pc; }
+            }
         }
-        __syncthreads();
-        if (tid == 0) {
-            int ba = -1, bb = 0, bnl = 0;
-            float bc = FLT_MAX;
-            if (cnt > 2 && !median) {
-                for (int q = 0; q < 3; ++q) {
-                    if (kq[q] == 0.0f) continue;
-                    float ra[SAH_BINS];
-                    int rc[SAH_BINS];
-                    float l3[3] = {FLT_MAX, FLT_MAX, FLT_MAX}, h3[3] = {-FLT_MAX, -FLT_MAX, -FLT_MAX};
-                    int c = 0;
-                    for (int b = SAH_BINS - 1; b > 0; --b) {
-                        if (S.bcnt[q][b]) {
-                            for (int e = 0; e < 3; ++e) {
-                                l3[e] = fminf(l3[e], ord2f(S.bmin[q][b][e]));
-                                h3[e] = fmaxf(h3[e], ord2f(S.bmax[q][b][e]));
-                            }
-                        }
-                        c += S.bcnt[q][b];
-                        ra[b] = c ? area3(f3(l3[0], l3[1], l3[2]), f3(h3[0], h3[1], h3[2])) : 0.0f;
-                        rc[b] = c;
-                    }
-                    for (int e = 0; e < 3; ++e) { l3[e] = FLT_MAX; h3[e] = -FLT_MAX; }
-                    c = 0;
-                    for (int b = 0; b < SAH_BINS - 1; ++b) {
-                        if (S.bcnt[q][b]) {
-                            for (int e = 0; e < 3; ++e) {
-                                l3[e] = fminf(l3[e], ord2f(S.bmin[q][b][e]));
-                                h3[e] = fmaxf(h3[e], ord2f(S.bmax[q][b][e]));
-                            }
-                        }
-                        c += S.bcnt[q][b];
-                        if (c == 0 || rc[b + 1] == 0) continue;
-                        const float cost = area3(f3(l3[0], l3[1], l3[2]), f3(h3[0], h3[1], h3[2])) * c + ra[b + 1] * rc[b + 1];
-                        if (cost < bc) { bc = cost; ba = q; bb = b; bnl = c; }
-                    }
-                }
-            }
-            S.best_axis = ba;
-            S.best_bin = bb;
-            S.nl = ba >= 0 ? bnl : cnt / 2;                  // no split found: halve the list
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const unsigned long long o = __shfl_xor_sync(FULL, best, off);
+            const int onl = __shfl_xor_sync(FULL, best_nl, off);
+            if (o < best) { best = o; best_nl = onl; }
         }
-        __syncthreads();
-        const int ax = S.best_axis, bbin = S.best_bin, nl = S.nl;
-        // stable partition into tmp, then back
-        int lbase = 0, rbase = 0;
-        for (int c0 = begin; c0 < end; c0 += SAH_THREADS) {
-            const int i = c0 + tid;
-            bool left = false;
-            int k = 0;
-            if (i < end) {
-                k = idx[i];
-                if (ax >= 0) {
-                    const float4 l4 = llo[k], h4 = lhi[k];
-                    const float c = 0.5f * ((ax == 0 ? l4.x : ax == 1 ? l4.y : l4.z) + (ax == 0 ? h4.x : ax == 1 ? h4.y : h4.z));
-                    left = sah_bin(c, S.nb[6 + ax], kq[ax]) <= bbin;
-                } else {
-                    left = (i - begin) < nl;
-                }
-            }
-            const unsigned bal = __ballot_sync(0xffffffffu, left);
-            if (lane == 0) S.warp_off[wid] = __popc(bal);
-            __syncthreads();
-            if (tid == 0) {
-                int acc = 0;
-                for (int w = 0; w < SAH_THREADS / 32; ++w) { const int x = S.warp_off[w]; S.warp_off[w] = acc; acc += x; }
-                S.warp_off[SAH_THREADS / 32] = acc;
-            }
-            __syncthreads();
-            const int lrank = S.warp_off[wid] + __popc(bal & ((1u << lane) - 1u));
-            const int chunk_l = S.warp_off[SAH_THREADS / 32];
-            if (i < end) {
-                const int pos = left ? begin + lbase + lrank : begin + nl + rbase + (i - c0 - lrank);
-                tmp[pos] = k;
-            }
-            lbase += chunk_l;
-            rbase += min(SAH_THREADS, end - c0) - chunk_l;
-            __syncthreads();
+        if (best != ~0ull) {
+            const unsigned id = (unsigned)(best & 0xffffffffu);
+            ax = (int)(id >> 5);
+            bbin = (int)(id & 31u);
+            nl = best_nl;
         }
-        for (int i = begin + tid; i < end; i += SAH_THREADS) idx[i] = tmp[i];
-        __syncthreads();
-        if (tid == 0) {
-            const int mid = begin + nl;
-            int code[2];
-            const int rb[2] = {begin, mid}, re[2] = {mid, end};
-            for (int h = 0; h < 2; ++h) {
-                if (re[h] - rb[h] == 1) {
-                    code[h] = ~(a + idx[rb[h]]);
-                    B.parent_leaf[a + idx[rb[h]]] = node;
-                } else {
-                    code[h] = ids[S.next_id++];
-                    B.parent_int[code[h]] = node;
-                    B.range[code[h]] = make_int2(0, re[h] - rb[h] - 1);   // size only (leaf_max 1)
-                }
+    }
+    // stable partition into tmp, then back
+    int lbase = 0, rbase = 0;
+    for (int c0 = begin; c0 < end; c0 += 32) {
+        const int i = c0 + lane;
+        bool left = false;
+        int k = 0;
+        if (i < end) {
+            k = idx[i];
+            if (ax >= 0) {
+                const float4 l4 = B.leaf_lo[k], h4 = B.leaf_hi[k];
+                const float c = 0.5f * ((ax == 0 ? l4.x : ax == 1 ? l4.y : l4.z) + (ax == 0 ? h4.x : ax == 1 ? h4.y : h4.z));
+                left = sah_bin(c, v[6 + ax], kq[ax]) <= bbin;
+            } else {
+                left = (i - begin) < nl;
             }
-            // larger child pushed first, the smaller taken next: the stack stays O(log m) deep
-            const int big = (re[0] - rb[0]) >= (re[1] - rb[1]) ? 0 : 1;
-            for (int h : {big, 1 - big})
-                if (re[h] - rb[h] > 1) S.stack[S.sp++] = make_int4(rb[h], re[h], code[h], depth + 1);
-            B.left[node] = code[0];
-            B.right[node] = code[1];
         }
-        __syncthreads();
+        const unsigned bal = __ballot_sync(FULL, left);
+        const int lrank = __popc(bal & ((1u << lane) - 1u));
+        if (i < end) tmp[left ? begin + lbase + lrank : begin + nl + rbase + (lane - lrank)] = k;
+        lbase += __popc(bal);
+        rbase += min(32, end - c0) - __popc(bal);
+    }
+    __syncwarp();
+    for (int i = begin + lane; i < end; i += 32) idx[i] = tmp[i];
+    __syncwarp();
+    if (lane == 0) {
+        const int mid = begin + nl;
+        int code[2];
+        const int rb[2] = {begin, mid}, re[2] = {mid, end};
+        for (int h = 0; h < 2; ++h) {
+            if (re[h] - rb[h] == 1) {
+                code[h] = ~idx[rb[h]];
+                B.parent_leaf[idx[rb[h]]] = node;
+            } else {
+                code[h] = h == 0 ? mid - 1 : mid;        // Karras ids: split position / position + 1
+                B.parent_int[code[h]] = node;
+                B.range[code[h]] = make_int2(0, re[h] - rb[h] - 1);   // size only (leaf_max 1)
+                next[atomicAdd(n_next, 1)] = make_int4(rb[h], re[h], code[h], depth + 1);
+            }
+        }
+        B.left[node] = code[0];
+        B.right[node] = code[1];
     }
 }
 
@@ -929,13 +908,26 @@ cudaError_t rtb_build_bvh(const BuildBuffers& Bc, cudaStream_t st, int* root, in
         cudaMemcpyAsync(&h_roots, n_roots, sizeof(int), cudaMemcpyDeviceToHost, st);
         cudaError_t e = cudaStreamSynchronize(st);
         if (e != cudaSuccess) return e;
-        // scratch: the sort keys / values are free once the leaves are gathered and the
-        // hierarchy built; the DFS stack borrows frontier[1] (N int2, unused until k_wide)
-        if (h_roots > 0)
-            k_sah_subtrees<<<h_roots, SAH_THREADS, 0, st>>>(B, roots, reinterpret_cast<int*>(B.keys[0]),
-                                                           reinterpret_cast<int*>(B.keys[1]),
-                                                           reinterpret_cast<int*>(B.vals[0]),
-                                                           reinterpret_cast<int*>(B.frontier[1]));
+        // scratch: the sort keys are free once the leaves are gathered and the hierarchy built
+        // (item order idx / tmp); the level task lists borrow frontier[1] and the BVH4 staging
+        // (each >= N/2 int4, unused until k_wide)
+        if (h_roots > 0) {
+            int* idx = reinterpret_cast<int*>(B.keys[0]);
+            int* tmp = reinterpret_cast<int*>(B.keys[1]);
+            int4* tl[2] = {reinterpret_cast<int4*>(B.frontier[1]), reinterpret_cast<int4*>(B.nodes4)};
+            int* n_next = B.wide_counters + 1;
+            k_sah_init<<<(h_roots * 32 + 255) / 256, 256, 0, st>>>(B, roots, h_roots, idx, tl[0]);
+            int n_tasks = h_roots, cur_t = 0;
+            while (n_tasks > 0) {
+                cudaMemsetAsync(n_next, 0, sizeof(int), st);
+                k_sah_level<<<(n_tasks + SAH_WARPS - 1) / SAH_WARPS, 32 * SAH_WARPS, 0, st>>>(
+                    B, tl[cur_t], n_tasks, tl[cur_t ^ 1], n_next, idx, tmp);
+                cudaMemcpyAsync(&n_tasks, n_next, sizeof(int), cudaMemcpyDeviceToHost, st);
+                e = cudaStreamSynchronize(st);
+                if (e != cudaSuccess) return e;
+                cur_t ^= 1;
+            }
+        }
     }
     if (B.leaf_max == 1) {
         for (int pass = 0; pass < B.treelet_passes; ++pass) {
