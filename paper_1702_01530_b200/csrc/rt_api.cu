@@ -124,7 +124,7 @@ rt_status rt_create(int device, void* cuda_stream, rt_context** out) {
     c->device = device;
     if (const char* lm = getenv("RT_LEAF_MAX")) c->leaf_max = std::max(1, std::min(16, atoi(lm)));
     if (const char* tp = getenv("RT_TREELETS")) c->treelet_passes = std::max(0, std::min(8, atoi(tp)));
-    if (const char* ss = getenv("RT_SAH_SUBTREES")) c->sah_subtrees = atoi(ss) != 0;
+    if (const char* ss = getenv("RT_SAH_SUBTREES")) c->sah_subtrees = std::max(0, std::min(2, atoi(ss)));
     if (const char* gl = getenv("RT_GRID_LIMIT")) c->grid_limit = std::max(0, atoi(gl));
     cudaError_t e = cudaSetDevice(device);
     if (e == cudaSuccess && cuda_stream) {

@@ -586,10 +586,168 @@ struct SahWarpBins {
     int cnt[3][SAH_BINS];
     unsigned int lo[3][3][SAH_BINS], hi[3][3][SAH_BINS];    // [axis][component][bin], ordered floats
 };
+constexpr int SAH_BIG = 1 << 16;             // tasks above this many items: one 1024-thread CTA each
+constexpr int SAH_BIG_THREADS = 1024;
 
-// One level: task (begin, end, node, depth) per warp over item slots idx[begin, end).
+__device__ __forceinline__ void sah_bins_clear(SahWarpBins& S, int lane) {
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        S.cnt[q][lane] = 0;
+#pragma unroll
+        for (int e = 0; e < 3; ++e) { S.lo[q][e][lane] = 0xffffffffu; S.hi[q][e][lane] = 0u; }
+    }
+}
+
+// bin one item (its leaf box) on every axis with extent
+__device__ __forceinline__ void sah_bin_item(SahWarpBins& S, const BuildBuffers& B, int k, const float* v, const float* kq) {
+    const float4 l4 = B.leaf_lo[k], h4 = B.leaf_hi[k];
+    const float l[3] = {l4.x, l4.y, l4.z}, h[3] = {h4.x, h4.y, h4.z};
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        if (kq[q] == 0.0f) continue;
+        const int b = sah_bin(0.5f * (l[q] + h[q]), v[6 + q], kq[q]);
+        atomicAdd(&S.cnt[q][b], 1);
+#pragma unroll
+        for (int e = 0; e < 3; ++e) {
+            atomicMin(&S.lo[q][e][b], f2ord(l[e]));
+            atomicMax(&S.hi[q][e][b], f2ord(h[e]));
+        }
+    }
+}
+
+// Split search by one warp (lane = bin): SAH cost of splitting after every bin of every axis from
+// prefix (bins <= lane) and suffix (bins > lane) scans; the lowest (cost, axis, bin) wins.
+__device__ __forceinline__ void sah_split_search(const SahWarpBins& S, const float* kq, int lane, int& ax, int& bbin, int& nl) {
+    const unsigned FULL = 0xffffffffu;
+    unsigned long long best = ~0ull;                     // (cost bits << 32) | (axis * 32 + bin)
+    int best_nl = 0;
+    for (int q = 0; q < 3; ++q) {
+        if (kq[q] == 0.0f) continue;
+        const int c = S.cnt[q][lane];
+        float pl[3], ph[3], sl[3], sh[3];
+#pragma unroll
+        for (int e = 0; e < 3; ++e) {
+            pl[e] = sl[e] = c ? ord2f(S.lo[q][e][lane]) : FLT_MAX;
+            ph[e] = sh[e] = c ? ord2f(S.hi[q][e][lane]) : -FLT_MAX;
+        }
+        int pc = c, sc = c;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int uc = __shfl_up_sync(FULL, pc, off), dc = __shfl_down_sync(FULL, sc, off);
+            float ul[3], uh[3], dl[3], dh[3];
+#pragma unroll
+            for (int e = 0; e < 3; ++e) {
+                ul[e] = __shfl_up_sync(FULL, pl[e], off); uh[e] = __shfl_up_sync(FULL, ph[e], off);
+                dl[e] = __shfl_down_sync(FULL, sl[e], off); dh[e] = __shfl_down_sync(FULL, sh[e], off);
+            }
+            if (lane >= off) {
+                pc += uc;
+#pragma unroll
+                for (int e = 0; e < 3; ++e) { pl[e] = fminf(pl[e], ul[e]); ph[e] = fmaxf(ph[e], uh[e]); }
+            }
+            if (lane + off < 32) {
+                sc += dc;
+#pragma unroll
+                for (int e = 0; e < 3; ++e) { sl[e] = fminf(sl[e], dl[e]); sh[e] = fmaxf(sh[e], dh[e]); }
+            }
+        }
+        const int rc = __shfl_down_sync(FULL, sc, 1);   // right side of a split after bin `lane`
+        float rl[3], rh[3];
+#pragma unroll
+        for (int e = 0; e < 3; ++e) { rl[e] = __shfl_down_sync(FULL, sl[e], 1); rh[e] = __shfl_down_sync(FULL, sh[e], 1); }
+        if (lane < SAH_BINS - 1 && pc > 0 && rc > 0) {
+            const float cost = area3(f3(pl[0], pl[1], pl[2]), f3(ph[0], ph[1], ph[2])) * pc +
+                               area3(f3(rl[0], rl[1], rl[2]), f3(rh[0], rh[1], rh[2])) * rc;
+            const unsigned long long key = ((unsigned long long)__float_as_uint(cost) << 32) | (unsigned)(q * 32 + lane);
+            if (key < best) { best = key; best_nl = pc; }
+        }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        const unsigned long long o = __shfl_xor_sync(FULL, best, off);
+        const int onl = __shfl_xor_sync(FULL, best_nl, off);
+        if (o < best) { best = o; best_nl = onl; }
+    }
+    if (best != ~0ull) {
+        const unsigned id = (unsigned)(best & 0xffffffffu);
+        ax = (int)(id >> 5);
+        bbin = (int)(id & 31u);
+        nl = best_nl;
+    }
+}
+
+__device__ __forceinline__ bool sah_goes_left(const BuildBuffers& B, int k, int i, int begin, int ax, int bbin, int nl,
+                                              const float* v, const float* kq) {
+    if (ax < 0) return (i - begin) < nl;                 // median split in item order
+    const float4 l4 = B.leaf_lo[k], h4 = B.leaf_hi[k];
+    const float c = 0.5f * ((ax == 0 ? l4.x : ax == 1 ? l4.y : l4.z) + (ax == 0 ? h4.x : ax == 1 ? h4.y : h4.z));
+    return sah_bin(c, v[6 + ax], kq[ax]) <= bbin;
+}
+
+// children of a split node (one thread): leaves get their slot codes, internal children their
+// Karras ids and a task in the next level's list (large ones in the CTA list)
+__device__ __forceinline__ void sah_children(const BuildBuffers& B, const int* idx, int begin, int end, int nl, int node,
+                                             int depth, int4* next, int* n_next, int4* next_big, int* n_next_big) {
+    const int mid = begin + nl;
+    int code[2];
+    const int rb[2] = {begin, mid}, re[2] = {mid, end};
+    for (int h = 0; h < 2; ++h) {
+        if (re[h] - rb[h] == 1) {
+            code[h] = ~idx[rb[h]];
+            B.parent_leaf[idx[rb[h]]] = node;
+        } else {
+            code[h] = h == 0 ? mid - 1 : mid;            // Karras ids: split position / position + 1
+            B.parent_int[code[h]] = node;
+            B.range[code[h]] = make_int2(0, re[h] - rb[h] - 1);   // size only (leaf_max 1)
+            const int4 t = make_int4(rb[h], re[h], code[h], depth + 1);
+            if (re[h] - rb[h] > SAH_BIG) next_big[atomicAdd(n_next_big, 1)] = t;
+            else next[atomicAdd(n_next, 1)] = t;
+        }
+    }
+    B.left[node] = code[0];
+    B.right[node] = code[1];
+}
+
+__device__ __forceinline__ void sah_kq(const float* v, float* kq) {
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        const float ext = v[9 + q] - v[6 + q];
+        kq[q] = ext > 0.0f ? SAH_BINS * (1.0f - 1e-6f) / ext : 0.0f;
+    }
+}
+
+__device__ __forceinline__ void sah_bounds_item(const BuildBuffers& B, int k, float* v) {
+    const float4 l4 = B.leaf_lo[k], h4 = B.leaf_hi[k];
+    const float l[3] = {l4.x, l4.y, l4.z}, h[3] = {h4.x, h4.y, h4.z};
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        const float c = 0.5f * (l[q] + h[q]);
+        v[q] = fminf(v[q], l[q]); v[3 + q] = fmaxf(v[3 + q], h[q]);
+        v[6 + q] = fminf(v[6 + q], c); v[9 + q] = fmaxf(v[9 + q], c);
+    }
+}
+
+__device__ __forceinline__ void sah_bounds_init(float* v) {
+#pragma unroll
+    for (int q = 0; q < 3; ++q) { v[q] = FLT_MAX; v[3 + q] = -FLT_MAX; v[6 + q] = FLT_MAX; v[9 + q] = -FLT_MAX; }
+}
+
+__device__ __forceinline__ void sah_bounds_warp(float* v) {
+#pragma unroll
+    for (int q = 0; q < 12; ++q) {
+        const bool mx = (q >= 3 && q < 6) || q >= 9;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const float o = __shfl_xor_sync(0xffffffffu, v[q], off);
+            v[q] = mx ? fmaxf(v[q], o) : fminf(v[q], o);
+        }
+    }
+}
+
+// One level, tasks of <= SAH_BIG items: task (begin, end, node, depth) per warp over idx[begin, end).
 __global__ void __launch_bounds__(32 * SAH_WARPS) k_sah_level(BuildBuffers B, const int4* __restrict__ tasks,
-                                                              int n_tasks, int4* next, int* n_next, int* idx, int* tmp) {
+                                                              int n_tasks, int4* next, int* n_next, int4* next_big,
+                                                              int* n_next_big, int* idx, int* tmp) {
     __shared__ SahWarpBins bins[SAH_WARPS];
     const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
     const int w = blockIdx.x * SAH_WARPS + wl;
@@ -598,144 +756,30 @@ __global__ void __launch_bounds__(32 * SAH_WARPS) k_sah_level(BuildBuffers B, co
     const int4 t = tasks[w];
     const int begin = t.x, end = t.y, node = t.z, depth = t.w, cnt = end - begin;
     const bool median = depth + ceil_log2(cnt) >= SAH_MAX_DEPTH;   // depth budget: balanced below
-    // node box and centroid bounds
-    float v[12];
-#pragma unroll
-    for (int q = 0; q < 3; ++q) { v[q] = FLT_MAX; v[3 + q] = -FLT_MAX; v[6 + q] = FLT_MAX; v[9 + q] = -FLT_MAX; }
-    for (int i = begin + lane; i < end; i += 32) {
-        const int k = idx[i];
-        const float4 l4 = B.leaf_lo[k], h4 = B.leaf_hi[k];
-        const float l[3] = {l4.x, l4.y, l4.z}, h[3] = {h4.x, h4.y, h4.z};
-#pragma unroll
-        for (int q = 0; q < 3; ++q) {
-            const float c = 0.5f * (l[q] + h[q]);
-            v[q] = fminf(v[q], l[q]); v[3 + q] = fmaxf(v[3 + q], h[q]);
-            v[6 + q] = fminf(v[6 + q], c); v[9 + q] = fmaxf(v[9 + q], c);
-        }
-    }
-#pragma unroll
-    for (int q = 0; q < 12; ++q) {
-        const bool mx = (q >= 3 && q < 6) || q >= 9;
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-            const float o = __shfl_xor_sync(FULL, v[q], off);
-            v[q] = mx ? fmaxf(v[q], o) : fminf(v[q], o);
-        }
-    }
+    float v[12];                                         // node box and centroid bounds
+    sah_bounds_init(v);
+    for (int i = begin + lane; i < end; i += 32) sah_bounds_item(B, idx[i], v);
+    sah_bounds_warp(v);
     if (lane == 0) {
         B.node_lo[node] = make_float4(v[0], v[1], v[2], 0.f);
         B.node_hi[node] = make_float4(v[3], v[4], v[5], 0.f);
     }
     float kq[3];
-#pragma unroll
-    for (int q = 0; q < 3; ++q) {
-        const float ext = v[9 + q] - v[6 + q];
-        kq[q] = ext > 0.0f ? SAH_BINS * (1.0f - 1e-6f) / ext : 0.0f;
-    }
+    sah_kq(v, kq);
     int ax = -1, nl = cnt / 2, bbin = 0;                 // no split found: halve the list
     if (cnt > 2 && !median) {
         SahWarpBins& S = bins[wl];
-#pragma unroll
-        for (int q = 0; q < 3; ++q) {
-            S.cnt[q][lane] = 0;
-#pragma unroll
-            for (int e = 0; e < 3; ++e) { S.lo[q][e][lane] = 0xffffffffu; S.hi[q][e][lane] = 0u; }
-        }
+        sah_bins_clear(S, lane);
         __syncwarp();
-        for (int i = begin + lane; i < end; i += 32) {
-            const int k = idx[i];
-            const float4 l4 = B.leaf_lo[k], h4 = B.leaf_hi[k];
-            const float l[3] = {l4.x, l4.y, l4.z}, h[3] = {h4.x, h4.y, h4.z};
-#pragma unroll
-            for (int q = 0; q < 3; ++q) {
-                if (kq[q] == 0.0f) continue;
-                const int b = sah_bin(0.5f * (l[q] + h[q]), v[6 + q], kq[q]);
-                atomicAdd(&S.cnt[q][b], 1);
-#pragma unroll
-                for (int e = 0; e < 3; ++e) {
-                    atomicMin(&S.lo[q][e][b], f2ord(l[e]));
-                    atomicMax(&S.hi[q][e][b], f2ord(h[e]));
-                }
-            }
-        }
+        for (int i = begin + lane; i < end; i += 32) sah_bin_item(S, B, idx[i], v, kq);
         __syncwarp();
-        // split search: lane = bin; prefix (bins <= lane) and suffix (bins > lane) by warp scans
-        unsigned long long best = ~0ull;                 // (cost bits << 32) | (axis * 32 + bin)
-        int best_nl = 0;
-        for (int q = 0; q < 3; ++q) {
-            if (kq[q] == 0.0f) continue;
-            const int c = S.cnt[q][lane];
-            float bl[3], bh[3];
-#pragma unroll
-            for (int e = 0; e < 3; ++e) {
-                bl[e] = c ? ord2f(S.lo[q][e][lane]) : FLT_MAX;
-                bh[e] = c ? ord2f(S.hi[q][e][lane]) : -FLT_MAX;
-            }
-            int pc = c, sc = c;
-            float pl[3], ph[3], sl[3], sh[3];
-#pragma unroll
-            for (int e = 0; e < 3; ++e) { pl[e] = sl[e] = bl[e]; ph[e] = sh[e] = bh[e]; }
-#pragma unroll
-            for (int off = 1; off < 32; off <<= 1) {
-                const int uc = __shfl_up_sync(FULL, pc, off), dc = __shfl_down_sync(FULL, sc, off);
-                float ul[3], uh[3], dl[3], dh[3];
-#pragma unroll
-                for (int e = 0; e < 3; ++e) {
-                    ul[e] = __shfl_up_sync(FULL, pl[e], off); uh[e] = __shfl_up_sync(FULL, ph[e], off);
-                    dl[e] = __shfl_down_sync(FULL, sl[e], off); dh[e] = __shfl_down_sync(FULL, sh[e], off);
-                }
-                if (lane >= off) {
-                    pc += uc;
-#pragma unroll
-                    for (int e = 0; e < 3; ++e) { pl[e] = fminf(pl[e], ul[e]); ph[e] = fmaxf(ph[e], uh[e]); }
-                }
-                if (lane + off < 32) {
-                    sc += dc;
-#pragma unroll
-                    for (int e = 0; e < 3; ++e) { sl[e] = fminf(sl[e], dl[e]); sh[e] = fmaxf(sh[e], dh[e]); }
-                }
-            }
-            // right side of a split after bin `lane` = suffix of bin lane + 1
-            const int rc = __shfl_down_sync(FULL, sc, 1);
-            float rl[3], rh[3];
-#pragma unroll
-            for (int e = 0; e < 3; ++e) { rl[e] = __shfl_down_sync(FULL, sl[e], 1); rh[e] = __shfl_down_sync(FULL, sh[e], 1); }
-            if (lane < SAH_BINS - 1 && pc > 0 && rc > 0) {
-                const float cost = area3(f3(pl[0], pl[1], pl[2]), f3(ph[0], ph[1], ph[2])) * pc +
-                                   area3(f3(rl[0], rl[1], rl[2]), f3(rh[0], rh[1], rh[2])) * rc;
-                const unsigned long long key = ((unsigned long long)__float_as_uint(cost) << 32) | (unsigned)(q * 32 + lane);
-                if (key < best) { best = key; best_nl = pc; }
-            }
-        }
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-            const unsigned long long o = __shfl_xor_sync(FULL, best, off);
-            const int onl = __shfl_xor_sync(FULL, best_nl, off);
-            if (o < best) { best = o; best_nl = onl; }
-        }
-        if (best != ~0ull) {
-            const unsigned id = (unsigned)(best & 0xffffffffu);
-            ax = (int)(id >> 5);
-            bbin = (int)(id & 31u);
-            nl = best_nl;
-        }
+        sah_split_search(S, kq, lane, ax, bbin, nl);
     }
-    // stable partition into tmp, then back
-    int lbase = 0, rbase = 0;
+    int lbase = 0, rbase = 0;                            // stable partition into tmp, then back
     for (int c0 = begin; c0 < end; c0 += 32) {
         const int i = c0 + lane;
-        bool left = false;
-        int k = 0;
-        if (i < end) {
-            k = idx[i];
-            if (ax >= 0) {
-                const float4 l4 = B.leaf_lo[k], h4 = B.leaf_hi[k];
-                const float c = 0.5f * ((ax == 0 ? l4.x : ax == 1 ? l4.y : l4.z) + (ax == 0 ? h4.x : ax == 1 ? h4.y : h4.z));
-                left = sah_bin(c, v[6 + ax], kq[ax]) <= bbin;
-            } else {
-                left = (i - begin) < nl;
-            }
-        }
+        const int k = i < end ? idx[i] : 0;
+        const bool left = i < end && sah_goes_left(B, k, i, begin, ax, bbin, nl, v, kq);
         const unsigned bal = __ballot_sync(FULL, left);
         const int lrank = __popc(bal & ((1u << lane) - 1u));
         if (i < end) tmp[left ? begin + lbase + lrank : begin + nl + rbase + (lane - lrank)] = k;
@@ -745,24 +789,93 @@ __global__ void __launch_bounds__(32 * SAH_WARPS) k_sah_level(BuildBuffers B, co
     __syncwarp();
     for (int i = begin + lane; i < end; i += 32) idx[i] = tmp[i];
     __syncwarp();
-    if (lane == 0) {
-        const int mid = begin + nl;
-        int code[2];
-        const int rb[2] = {begin, mid}, re[2] = {mid, end};
-        for (int h = 0; h < 2; ++h) {
-            if (re[h] - rb[h] == 1) {
-                code[h] = ~idx[rb[h]];
-                B.parent_leaf[idx[rb[h]]] = node;
-            } else {
-                code[h] = h == 0 ? mid - 1 : mid;        // Karras ids: split position / position + 1
-                B.parent_int[code[h]] = node;
-                B.range[code[h]] = make_int2(0, re[h] - rb[h] - 1);   // size only (leaf_max 1)
-                next[atomicAdd(n_next, 1)] = make_int4(rb[h], re[h], code[h], depth + 1);
-            }
-        }
-        B.left[node] = code[0];
-        B.right[node] = code[1];
+    if (lane == 0) sah_children(B, idx, begin, end, nl, node, depth, next, n_next, next_big, n_next_big);
+}
+
+// One level, tasks of > SAH_BIG items (the top of a full SAH build): one 1024-thread CTA per task,
+// per-warp bins merged in shared memory, a CTA-wide stable partition.
+__global__ void __launch_bounds__(SAH_BIG_THREADS) k_sah_level_big(BuildBuffers B, const int4* __restrict__ tasks,
+                                                                   int4* next, int* n_next, int4* next_big,
+                                                                   int* n_next_big, int* idx, int* tmp) {
+    extern __shared__ SahWarpBins wb[];                  // [SAH_BIG_THREADS / 32] per-warp bins; [0] merged
+    __shared__ float red[SAH_BIG_THREADS / 32][12];
+    __shared__ int wcnt[SAH_BIG_THREADS / 32 + 1];
+    __shared__ int split[3];
+    const int tid = threadIdx.x, lane = tid & 31, wl = tid >> 5;
+    constexpr int NW = SAH_BIG_THREADS / 32;
+    const int4 t = tasks[blockIdx.x];
+    const int begin = t.x, end = t.y, node = t.z, depth = t.w, cnt = end - begin;
+    const bool median = depth + ceil_log2(cnt) >= SAH_MAX_DEPTH;
+    float v[12];
+    sah_bounds_init(v);
+    for (int i = begin + tid; i < end; i += SAH_BIG_THREADS) sah_bounds_item(B, idx[i], v);
+    sah_bounds_warp(v);
+    if (lane == 0)
+        for (int q = 0; q < 12; ++q) red[wl][q] = v[q];
+    sah_bins_clear(wb[wl], lane);
+    __syncthreads();
+    if (tid < 12) {
+        const bool mx = (tid >= 3 && tid < 6) || tid >= 9;
+        float x = red[0][tid];
+        for (int w = 1; w < NW; ++w) x = mx ? fmaxf(x, red[w][tid]) : fminf(x, red[w][tid]);
+        red[0][tid] = x;
     }
+    __syncthreads();
+    for (int q = 0; q < 12; ++q) v[q] = red[0][q];
+    if (tid == 0) {
+        B.node_lo[node] = make_float4(v[0], v[1], v[2], 0.f);
+        B.node_hi[node] = make_float4(v[3], v[4], v[5], 0.f);
+    }
+    float kq[3];
+    sah_kq(v, kq);
+    if (!median) {
+        for (int i = begin + tid; i < end; i += SAH_BIG_THREADS) sah_bin_item(wb[wl], B, idx[i], v, kq);
+    }
+    __syncthreads();
+    // merge the per-warp bins into wb[0] (one thread per bin entry)
+    constexpr int ENTRIES = sizeof(SahWarpBins) / 4;
+    for (int e = tid; e < ENTRIES; e += SAH_BIG_THREADS) {
+        unsigned* base = reinterpret_cast<unsigned*>(wb);
+        unsigned x = base[e];
+        const bool is_cnt = e < 3 * SAH_BINS, is_lo = !is_cnt && e < 3 * SAH_BINS + 9 * SAH_BINS;
+        for (int w = 1; w < NW; ++w) {
+            const unsigned y = base[w * ENTRIES + e];
+            x = is_cnt ? x + y : (is_lo ? min(x, y) : max(x, y));
+        }
+        base[e] = x;
+    }
+    __syncthreads();
+    if (wl == 0) {
+        int ax = -1, nl = cnt / 2, bbin = 0;
+        if (!median) sah_split_search(wb[0], kq, lane, ax, bbin, nl);
+        if (lane == 0) { split[0] = ax; split[1] = bbin; split[2] = nl; }
+    }
+    __syncthreads();
+    const int ax = split[0], bbin = split[1], nl = split[2];
+    int lbase = 0, rbase = 0;                            // CTA-wide stable partition, 1024 items a step
+    for (int c0 = begin; c0 < end; c0 += SAH_BIG_THREADS) {
+        const int i = c0 + tid;
+        const int k = i < end ? idx[i] : 0;
+        const bool left = i < end && sah_goes_left(B, k, i, begin, ax, bbin, nl, v, kq);
+        const unsigned bal = __ballot_sync(0xffffffffu, left);
+        if (lane == 0) wcnt[wl] = __popc(bal);
+        __syncthreads();
+        if (tid == 0) {
+            int acc = 0;
+            for (int w = 0; w < NW; ++w) { const int x = wcnt[w]; wcnt[w] = acc; acc += x; }
+            wcnt[NW] = acc;
+        }
+        __syncthreads();
+        const int lrank = wcnt[wl] + __popc(bal & ((1u << lane) - 1u));
+        const int chunk_l = wcnt[NW];
+        if (i < end) tmp[left ? begin + lbase + lrank : begin + nl + rbase + (i - c0 - lrank)] = k;
+        lbase += chunk_l;
+        rbase += min(SAH_BIG_THREADS, end - c0) - chunk_l;
+        __syncthreads();
+    }
+    for (int i = begin + tid; i < end; i += SAH_BIG_THREADS) idx[i] = tmp[i];
+    __syncthreads();
+    if (tid == 0) sah_children(B, idx, begin, end, nl, node, depth, next, n_next, next_big, n_next_big);
 }
 
 // leaf-order records and leaf AABBs (slot k = sorted position k)
@@ -902,10 +1015,15 @@ cudaError_t rtb_build_bvh(const BuildBuffers& Bc, cudaStream_t st, int* root, in
     if (B.leaf_max == 1 && n > 2 && B.sah_subtrees) {
         int* roots = B.frontier[0] ? reinterpret_cast<int*>(B.frontier[0]) : nullptr;   // scratch [N] int2
         int* n_roots = B.wide_counters;
-        cudaMemsetAsync(n_roots, 0, sizeof(int), st);
-        k_sah_roots<<<grid_for(n - 1), 256, 0, st>>>(B, n, roots, n_roots);
         int h_roots = 0;
-        cudaMemcpyAsync(&h_roots, n_roots, sizeof(int), cudaMemcpyDeviceToHost, st);
+        if (B.sah_subtrees == 2) {                       // full SAH: the whole tree is one subtree
+            cudaMemsetAsync(roots, 0, sizeof(int), st);  // Karras root 0, slots [0, n)
+            h_roots = 1;
+        } else {
+            cudaMemsetAsync(n_roots, 0, sizeof(int), st);
+            k_sah_roots<<<grid_for(n - 1), 256, 0, st>>>(B, n, roots, n_roots);
+            cudaMemcpyAsync(&h_roots, n_roots, sizeof(int), cudaMemcpyDeviceToHost, st);
+        }
         cudaError_t e = cudaStreamSynchronize(st);
         if (e != cudaSuccess) return e;
         // scratch: the sort keys are free once the leaves are gathered and the hierarchy built
@@ -914,17 +1032,37 @@ cudaError_t rtb_build_bvh(const BuildBuffers& Bc, cudaStream_t st, int* root, in
         if (h_roots > 0) {
             int* idx = reinterpret_cast<int*>(B.keys[0]);
             int* tmp = reinterpret_cast<int*>(B.keys[1]);
-            int4* tl[2] = {reinterpret_cast<int4*>(B.frontier[1]), reinterpret_cast<int4*>(B.nodes4)};
-            int* n_next = B.wide_counters + 1;
-            k_sah_init<<<(h_roots * 32 + 255) / 256, 256, 0, st>>>(B, roots, h_roots, idx, tl[0]);
-            int n_tasks = h_roots, cur_t = 0;
-            while (n_tasks > 0) {
-                cudaMemsetAsync(n_next, 0, sizeof(int), st);
-                k_sah_level<<<(n_tasks + SAH_WARPS - 1) / SAH_WARPS, 32 * SAH_WARPS, 0, st>>>(
-                    B, tl[cur_t], n_tasks, tl[cur_t ^ 1], n_next, idx, tmp);
-                cudaMemcpyAsync(&n_tasks, n_next, sizeof(int), cudaMemcpyDeviceToHost, st);
+            // task lists: small (warp) and big (CTA) tasks of the current and the next level; the
+            // big lists are short (< n / SAH_BIG entries) and live past the small ones
+            int4* base4 = reinterpret_cast<int4*>(B.nodes4);
+            int4* tl[2] = {reinterpret_cast<int4*>(B.frontier[1]), base4};
+            int4* tb[2] = {base4 + (n / 2 + 1), base4 + (n / 2 + 1) + (n / SAH_BIG + 2)};
+            int* cnts = B.wide_counters + 1;             // [0] next small, [1] next big
+            cudaFuncSetAttribute(k_sah_level_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(sizeof(SahWarpBins) * (SAH_BIG_THREADS / 32)));
+            int n_small = 0, n_big = 0;
+            if (B.sah_subtrees == 2 && n > SAH_BIG) {
+                k_sah_init<<<1, 32, 0, st>>>(B, roots, 1, idx, tb[0]);
+                n_big = 1;
+            } else {
+                k_sah_init<<<(h_roots * 32 + 255) / 256, 256, 0, st>>>(B, roots, h_roots, idx, tl[0]);
+                n_small = h_roots;
+            }
+            int cur_t = 0;
+            while (n_small + n_big > 0) {
+                cudaMemsetAsync(cnts, 0, 2 * sizeof(int), st);
+                if (n_big)
+                    k_sah_level_big<<<n_big, SAH_BIG_THREADS, sizeof(SahWarpBins) * (SAH_BIG_THREADS / 32), st>>>(
+                        B, tb[cur_t], tl[cur_t ^ 1], cnts, tb[cur_t ^ 1], cnts + 1, idx, tmp);
+                if (n_small)
+                    k_sah_level<<<(n_small + SAH_WARPS - 1) / SAH_WARPS, 32 * SAH_WARPS, 0, st>>>(
+                        B, tl[cur_t], n_small, tl[cur_t ^ 1], cnts, tb[cur_t ^ 1], cnts + 1, idx, tmp);
+                int h[2];
+                cudaMemcpyAsync(h, cnts, 2 * sizeof(int), cudaMemcpyDeviceToHost, st);
                 e = cudaStreamSynchronize(st);
                 if (e != cudaSuccess) return e;
+                n_small = h[0];
+                n_big = h[1];
                 cur_t ^= 1;
             }
         }

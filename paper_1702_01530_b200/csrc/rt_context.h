@@ -86,8 +86,10 @@ struct rt_context {
     double cam_eye[2][3], cam_f[3], cam_r[3], cam_u[3], cam_th, cam_sigma_unit;
     float vfov = 0;
     int leaf_max = 1;                // LBVH leaf collapse threshold (env RT_LEAF_MAX, <= 16)
-    int treelet_passes = 3;          // SAH treelet restructuring passes (env RT_TREELETS)
-    int sah_subtrees = 1;            // SAH rebuild of small LBVH subtrees (env RT_SAH_SUBTREES=0: off)
+    int treelet_passes = 0;          // SAH treelet restructuring passes (env RT_TREELETS; 0 after a full
+                                     // SAH build: measured neutral to slightly worse, DESIGN §5 r2)
+    int sah_subtrees = 2;            // binned-SAH rebuild: 1 LBVH subtrees <= 16K prims, 2 the whole tree,
+                                     // 0 off (env RT_SAH_SUBTREES)
     int grid_limit = 0;              // cap on trace CTAs (env RT_GRID_LIMIT; 0 = full machine)
     void* arena = nullptr;           // BVH build scratch (grow-only)
     size_t arena_bytes = 0;
