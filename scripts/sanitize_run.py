@@ -1,6 +1,7 @@
 """Small end-to-end workload for compute-sanitizer (memcheck / racecheck / synccheck / initcheck):
-upload + BVH build (spheres, planes, triangles), stereo renders with every output, shards +
-device unpack, refit, compose, download."""
+upload + BVH build (spheres, planes, triangles; a 90k-triangle mesh for the CTA-level SAH tasks),
+stereo renders with every output, the fused composition, shards + device unpack (round-robin and
+block layouts are separate processes: RT_SHARD_BLOCK), refit, compose, download, B0 probes."""
 import sys
 
 import numpy as np
@@ -11,7 +12,7 @@ from paper_1702_01530_b200 import rt, scenes  # noqa: E402
 
 R = rt.StereoRenderer(0)
 for s in (scenes.scene_c1(), scenes.scene_c2().with_view(width=40, height=30, max_depth=3),
-          scenes.scene_c3().with_view(width=48, height=27)):
+          scenes.scene_c3().with_view(width=48, height=27), scenes.scene_c4(nu=300, nv=150).with_view(width=40, height=24)):
     R.upload(s)
     R.set_camera(s.rig)
     out = R.render(s.width, s.height, s.max_depth, want_id=True, want_radiance=True, count=True)
@@ -29,6 +30,9 @@ for s in (scenes.scene_c1(), scenes.scene_c2().with_view(width=40, height=30, ma
     if s.n_tris:
         rt.rt_scene_update_vertices(R.ctx, s.vertices * 1.01)
         R.render(s.width, s.height, s.max_depth)
+    for mode in (rt.RT_COMPOSE_ANAGLYPH, rt.RT_COMPOSE_SBS):
+        c = torch.zeros((s.height, s.width if mode == 0 else 2 * (s.width // 2), 4), dtype=torch.uint8, device="cuda")
+        R.render(s.width, s.height, s.max_depth, compose=(mode, c))
     f = out["fb"]
     o = torch.zeros((s.height, s.width, 4), dtype=torch.uint8, device="cuda")
     rt.rt_compose(R.ctx, rt.rt_fb(f[0].data_ptr(), 0, s.width * 4), rt.rt_fb(f[1].data_ptr(), 0, s.width * 4),
@@ -36,6 +40,7 @@ for s in (scenes.scene_c1(), scenes.scene_c2().with_view(width=40, height=30, ma
     h = rt.rt_host_alloc(f.numel())
     rt.rt_wait(rt.rt_download(R.ctx, f.data_ptr(), h, f.numel()))
     rt.rt_host_free(h)
+rt.rt_bench_ceilings(R.ctx)
 torch.cuda.synchronize()
 R.close()
 print("sanitize workload done")
