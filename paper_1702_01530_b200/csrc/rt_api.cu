@@ -126,6 +126,8 @@ rt_status rt_create(int device, void* cuda_stream, rt_context** out) {
     if (const char* tp = getenv("RT_TREELETS")) c->treelet_passes = std::max(0, std::min(8, atoi(tp)));
     if (const char* ss = getenv("RT_SAH_SUBTREES")) c->sah_subtrees = std::max(0, std::min(2, atoi(ss)));
     if (const char* gl = getenv("RT_GRID_LIMIT")) c->grid_limit = std::max(0, atoi(gl));
+    if (const char* cd = getenv("RT_COLLAPSE_DP")) c->collapse_dp = atoi(cd) != 0;
+    if (const char* cp = getenv("RT_COLLAPSE_CPRIM")) c->collapse_cprim = (float)std::max(0.01, atof(cp));
     cudaError_t e = cudaSetDevice(device);
     if (e == cudaSuccess && cuda_stream) {
         c->stream = static_cast<cudaStream_t>(cuda_stream);
@@ -400,6 +402,8 @@ rt_status rt_scene_upload(rt_context* c, const rt_primitives* P, const rt_materi
         B.leaf_max = c->leaf_max;
         B.treelet_passes = c->treelet_passes;
         B.sah_subtrees = c->sah_subtrees;
+        B.collapse_dp = c->collapse_dp;
+        B.collapse_cprim = c->collapse_cprim;
         cudaError_t e = rtb_build_bvh(B, c->stream, &root, &n_nodes4, &depth4, level_start.data());
         if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
         if (e == cudaSuccess && n_nodes4 > 0) {        // compact the BVH4 into an exact-size buffer

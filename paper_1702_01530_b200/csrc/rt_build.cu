@@ -527,6 +527,119 @@ __global__ void k_wide(BuildBuffers B, const int2* __restrict__ fin, int n_in, i
     }
 }
 
+// ---------------------------------------------------------------- SAH-optimal 4-wide collapse
+// Instead of opening the largest-area child until a node has 4 (k_wide), choose every BVH4 node's
+// children by dynamic programming over the BVH2 (the wide-BVH collapse of Ylitie, Karras & Laine
+// 2017, for width 4): with A = box surface area (hit probability), c_node the cost of a BVH4 node
+// visit (4 box tests) and c_prim of a primitive test,
+//   D(x, j) = least cost of covering x's subtree with at most j child slots of one wide node,
+//   leaf:      D(x, j) = c_prim A(x)
+//   internal:  open(x, j) = min_k D(l, k) + D(r, j - k),   C(x) = c_node A(x) + open(x, 4),
+//              D(x, 1) = C(x),   D(x, j > 1) = min(C(x), open(x, j)),
+// computed bottom-up (arrival flags, as k_refit); a wide node at x then takes the slots of
+// open(x, 4) recursively (k_wide_dp).  choice[x]: best k of open(x, j) for j = 2, 3, 4 (2 bits
+// each) and, for j = 2, 3, 4, whether x is opened (bit 6 + j - 2).
+__device__ __forceinline__ void dp_child(int code, const BuildBuffers& B, const float* const* D, float c_prim, float d[4]) {
+    if (code < 0) {
+        const float c = c_prim * half_area(B.leaf_lo[~code], B.leaf_hi[~code]);
+        d[0] = d[1] = d[2] = d[3] = c;
+    } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) d[j] = __ldcg(&D[j][code]);
+    }
+}
+
+struct DpArrays {
+    float* D[4];
+    int* choice;
+};
+
+__global__ void k_collapse_dp(BuildBuffers B, int n, DpArrays X, float c_node, float c_prim) {
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+        int p = B.parent_leaf[k];
+        while (p >= 0) {
+            __threadfence();
+            if (atomicAdd(&B.flags[p], 1) == 0) break;    // first arrival: the sibling finishes p
+            __threadfence();
+            float dl[4], dr[4];
+            dp_child(B.left[p], B, X.D, c_prim, dl);
+            dp_child(B.right[p], B, X.D, c_prim, dr);
+            float o[5];
+            int kb[5];
+#pragma unroll
+            for (int j = 2; j <= 4; ++j) {
+                o[j] = FLT_MAX;
+                kb[j] = 1;
+#pragma unroll
+                for (int kk = 1; kk < j; ++kk) {
+                    const float c = dl[kk - 1] + dr[j - kk - 1];
+                    if (c < o[j]) { o[j] = c; kb[j] = kk; }
+                }
+            }
+            const float C = c_node * half_area(B.node_lo[p], B.node_hi[p]) + o[4];
+            int ch = kb[2] | (kb[3] << 2) | (kb[4] << 4);
+            float d[4];
+            d[0] = C;
+#pragma unroll
+            for (int j = 2; j <= 4; ++j) {
+                const bool opened = o[j] < C;
+                d[j - 1] = opened ? o[j] : C;
+                ch |= (opened ? 1 : 0) << (6 + j - 2);
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) __stcg(&X.D[j][p], d[j]);
+            __stcg(&X.choice[p], ch);
+            p = B.parent_int[p];
+        }
+    }
+}
+
+// BVH2 -> BVH4 by the DP choices: a wide node at BVH2 node src takes the slots of open(src, 4).
+__global__ void k_wide_dp(BuildBuffers B, const int* __restrict__ choice, const int2* __restrict__ fin, int n_in, int2* fout,
+                          int* counters) {
+    for (int it = blockIdx.x * blockDim.x + threadIdx.x; it < n_in; it += gridDim.x * blockDim.x) {
+        const int src = fin[it].x, dst = fin[it].y;
+        // expand (code, slots) pairs depth first; slots of a wide node: open(src, 4)
+        int st_code[8], st_j[8], sp = 0;
+        int codes[BVH_W], n = 0;
+        const int c0 = choice[src], k4 = (c0 >> 4) & 3;
+        st_code[sp] = B.right[src]; st_j[sp++] = 4 - k4;
+        st_code[sp] = B.left[src]; st_j[sp++] = k4;
+        while (sp > 0) {
+            --sp;
+            const int x = st_code[sp], j = st_j[sp];
+            const int cx = x >= 0 ? choice[x] : 0;
+            if (x < 0 || j == 1 || !((cx >> (6 + j - 2)) & 1)) {
+                codes[n++] = x;                          // one slot: a leaf or a wide child node
+            } else {
+                const int kx = (cx >> (2 * (j - 2))) & 3;
+                st_code[sp] = B.right[x]; st_j[sp++] = j - kx;
+                st_code[sp] = B.left[x]; st_j[sp++] = kx;
+            }
+        }
+        float3 lo[BVH_W], hi[BVH_W];
+        int oc[BVH_W];
+        for (int c = 0; c < BVH_W; ++c) {
+            if (c >= n) {
+                oc[c] = WIDE_EMPTY;
+                continue;
+            }
+            const WChild w = make_child(codes[c], B);
+            lo[c] = f3(w.lo.x, w.lo.y, w.lo.z);
+            hi[c] = f3(w.hi.x, w.hi.y, w.hi.z);
+            if (w.code < 0) {
+                oc[c] = w.code;                                     // BVH2 leaf: ~slot (count 1)
+            } else {
+                const int slot = atomicAdd(&counters[1], 1);
+                const int q = atomicAdd(&counters[0], 1);
+                fout[q] = make_int2(w.code, slot);
+                oc[c] = slot;
+            }
+        }
+        node_write(B.nodes4 + NODE_F4 * (size_t)dst, lo, hi, oc);
+    }
+}
+
 // ---------------------------------------------------------------- SAH subtrees
 // Every maximal LBVH subtree of at most SAH_T primitives (a contiguous Morton range [a, a + m) of
 // leaf slots) is rebuilt top-down by binned SAH (3 axes x SAH_BINS bins, centroid binning).  The
@@ -1080,6 +1193,18 @@ cudaError_t rtb_build_bvh(const BuildBuffers& Bc, cudaStream_t st, int* root, in
         *depth4 = 0;
         return cudaGetLastError();
     }
+    // SAH-optimal collapse (leaf_max 1): DP tables in the sort scratch (free after the SAH build)
+    const bool dp = B.leaf_max == 1 && B.collapse_dp;
+    DpArrays dpx{};
+    if (dp) {
+        dpx.D[0] = reinterpret_cast<float*>(B.keys[0]);
+        dpx.D[1] = reinterpret_cast<float*>(B.keys[1]);
+        dpx.D[2] = reinterpret_cast<float*>(B.vals[0]);
+        dpx.D[3] = reinterpret_cast<float*>(B.vals[1]);
+        dpx.choice = B.count;
+        cudaMemsetAsync(B.flags, 0, sizeof(int) * (n - 1), st);
+        k_collapse_dp<<<grid_for(n), 256, 0, st>>>(B, n, dpx, 1.0f, B.collapse_cprim);
+    }
     int2 first = make_int2(0, 0);
     int h_counters[2] = {0, 1};
     if (level_start) { level_start[0] = 0; level_start[1] = 1; }
@@ -1089,7 +1214,11 @@ cudaError_t rtb_build_bvh(const BuildBuffers& Bc, cudaStream_t st, int* root, in
         h_counters[0] = 0;
         cudaMemcpyAsync(B.wide_counters, h_counters, sizeof(int), cudaMemcpyHostToDevice, st);
         if (levels == 0) cudaMemcpyAsync(B.wide_counters + 1, h_counters + 1, sizeof(int), cudaMemcpyHostToDevice, st);
-        k_wide<<<grid_for(n_in), 256, 0, st>>>(B, B.frontier[cur_f], n_in, B.frontier[cur_f ^ 1], B.wide_counters);
+        if (dp)
+            k_wide_dp<<<grid_for(n_in), 256, 0, st>>>(B, dpx.choice, B.frontier[cur_f], n_in, B.frontier[cur_f ^ 1],
+                                                      B.wide_counters);
+        else
+            k_wide<<<grid_for(n_in), 256, 0, st>>>(B, B.frontier[cur_f], n_in, B.frontier[cur_f ^ 1], B.wide_counters);
         cudaError_t e = cudaMemcpyAsync(h_counters, B.wide_counters, 2 * sizeof(int), cudaMemcpyDeviceToHost, st);
         if (e == cudaSuccess) e = cudaStreamSynchronize(st);
         if (e != cudaSuccess) return e;

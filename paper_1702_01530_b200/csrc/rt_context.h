@@ -90,6 +90,8 @@ struct rt_context {
                                      // SAH build: measured neutral to slightly worse, DESIGN §5 r2)
     int sah_subtrees = 2;            // binned-SAH rebuild: 1 LBVH subtrees <= 16K prims, 2 the whole tree,
                                      // 0 off (env RT_SAH_SUBTREES)
+    int collapse_dp = 1;             // SAH-optimal BVH4 collapse (env RT_COLLAPSE_DP=0: largest-area opening)
+    float collapse_cprim = 0.4f;     // its primitive-test cost relative to a node visit (env RT_COLLAPSE_CPRIM)
     int grid_limit = 0;              // cap on trace CTAs (env RT_GRID_LIMIT; 0 = full machine)
     void* arena = nullptr;           // BVH build scratch (grow-only)
     size_t arena_bytes = 0;

@@ -10,11 +10,13 @@ import torch
 sys.path.insert(0, ".")
 from paper_1702_01530_b200 import rt, scenes  # noqa: E402
 
-VARIANTS = [("subtrees16K+0treelets", {"RT_SAH_SUBTREES": "1", "RT_TREELETS": "0"}),
-            ("subtrees16K+3treelets", {"RT_SAH_SUBTREES": "1", "RT_TREELETS": "3"}),
-            ("fullSAH+3treelets", {"RT_SAH_SUBTREES": "2", "RT_TREELETS": "3"}),
-            ("fullSAH+0treelets", {"RT_SAH_SUBTREES": "2", "RT_TREELETS": "0"}),
-            ("fullSAH+1treelet", {"RT_SAH_SUBTREES": "2", "RT_TREELETS": "1"})]
+BASE = {"RT_SAH_SUBTREES": "2", "RT_TREELETS": "0"}
+VARIANTS = [("fullSAH greedy collapse", {**BASE, "RT_COLLAPSE_DP": "0"})] + [
+    (f"fullSAH DP collapse cprim={c}", {**BASE, "RT_COLLAPSE_DP": "1", "RT_COLLAPSE_CPRIM": c})
+    for c in ("0.25", "0.4", "0.6", "1.0")]
+if os.environ.get("RT_BVH_VARIANTS_OLD"):
+    VARIANTS = [("subtrees16K+3treelets", {"RT_SAH_SUBTREES": "1", "RT_TREELETS": "3"}),
+                ("fullSAH+0treelets", BASE)]
 
 
 def time_frames(R, s, fb, flush, inflight=4, k=24):
