@@ -193,6 +193,11 @@ struct DistState {
     int* d_err = nullptr;
     uint64_t seq = 0;
     double timeout = 60.0;
+    // completion of the last frame that used each ring slot on this rank: a frame reusing the slot
+    // waits for it on the device, so a slot's flag words only ever move frame by frame, in order,
+    // even with frames in flight on streams that complete out of order
+    cudaEvent_t slot_ev[DIST_SLOTS] = {};
+    bool slot_used[DIST_SLOTS] = {};
     struct Map {
         std::string key;
         void* ptr;
@@ -229,6 +234,8 @@ void free_state(DistState* D, bool unlink_shm) {
         if (D->gathered[i]) cudaFree(D->gathered[i]);
         if (D->ring_ev[i]) cudaEventDestroy(D->ring_ev[i]);
     }
+    for (auto& ev : D->slot_ev)
+        if (ev) cudaEventDestroy(ev);
     if (D->h_err) cudaFreeHost(D->h_err);
     if (D->shm) munmap(D->shm, sizeof(ShmBlock));
     if (unlink_shm && !D->shm_name.empty()) shm_unlink(D->shm_name.c_str());
@@ -374,6 +381,9 @@ bool shm_leave(DistState* D) {
 }  // namespace
 
 // ------------------------------------------------------------------------------ frames
+static rt_status dist_frame(rt_context* c, DistState* D, const rt_render_params* p, const rt_outputs* out,
+                            cudaStream_t stream, uint64_t k, int slot);
+
 rt_status rtb_dist_render(rt_context* c, const rt_render_params* p, const rt_outputs* out, cudaStream_t stream) {
     DistState* D = c->dist;
     // an explicit tile subset (shard_world > 1) is a local render of those tiles, not a frame
@@ -390,6 +400,18 @@ rt_status rtb_dist_render(rt_context* c, const rt_render_params* p, const rt_out
     CUDA_TRY(cudaSetDevice(c->device));
     const uint64_t k = ++D->seq;
     const int slot = (int)(k % DIST_SLOTS);
+    if (D->slot_used[slot]) CUDA_TRY(cudaStreamWaitEvent(stream, D->slot_ev[slot], 0));
+    st = dist_frame(c, D, p, out, stream, k, slot);
+    if (st) return st;
+    CUDA_TRY(cudaEventRecord(D->slot_ev[slot], stream));
+    D->slot_used[slot] = true;
+    return RT_OK;
+}
+
+// frame k of a distributed context in ring slot `slot` (peer or NCCL transport)
+static rt_status dist_frame(rt_context* c, DistState* D, const rt_render_params* p, const rt_outputs* out,
+                            cudaStream_t stream, uint64_t k, int slot) {
+    rt_status st;
     rt_render_params q = *p;
     q.shard_rank = (uint32_t)D->rank;
     q.shard_world = (uint32_t)D->world;
@@ -579,6 +601,9 @@ rt_status rt_dist_init(rt_context* c, int rank, int world, const void* id, uint3
         }
     }
     if ((st = shm_join(D, ipc_ok))) return bail(st);
+    for (int i = 0; i < DIST_SLOTS; ++i)
+        if ((e = cudaEventCreateWithFlags(&D->slot_ev[i], cudaEventDisableTiming)) != cudaSuccess)
+            return bail(rtb_fail(RT_ERR_CUDA, "rt_dist_init: %s", cudaGetErrorString(e)));
     bool all_ipc = true;
     for (int r = 0; r < world; ++r) all_ipc = all_ipc && S->joined[r] == 2;
     D->transport = (S->transport == RT_DIST_PEER && all_ipc) ? RT_DIST_PEER : RT_DIST_NCCL;
