@@ -62,6 +62,17 @@ def test_null_arguments_are_rejected_without_a_device():
     assert L.rt_ipc_open(None, None, None) == rt.RT_ERR_INVALID_ARG
     assert L.rt_ipc_close(None, None) == rt.RT_ERR_INVALID_ARG
     assert L.rt_scene_info(None, None) == rt.RT_ERR_INVALID_ARG
+    assert L.rt_bench_ceilings(None, None) == rt.RT_ERR_INVALID_ARG
+    assert L.rt_dist_unique_id(None) == rt.RT_ERR_INVALID_ARG
+    assert L.rt_dist_init(None, 0, 1, None, 0) == rt.RT_ERR_INVALID_ARG
+    assert L.rt_dist_finalize(None) == rt.RT_ERR_INVALID_ARG
+    assert L.rt_dist_info(None, None) == rt.RT_ERR_INVALID_ARG
+    job = rt.rt_dist_unique_id()
+    assert len(job) == rt.RT_DIST_ID_BYTES and any(job) and job != rt.rt_dist_unique_id()
+    import ctypes as C2
+    h = C2.c_uint64()
+    b = (C2.c_char * 128).from_buffer_copy(job)
+    assert L.rt_dist_host_selftest(2, 2, C2.cast(b, C2.c_void_p), 1, C2.byref(h)) == rt.RT_ERR_INVALID_ARG   # rank >= world
     assert "NULL" in rt.rt_last_error() or rt.rt_last_error() != ""
 
 

@@ -227,12 +227,17 @@ def test_determinism_and_counters(R):
     np.testing.assert_array_equal(b["fb"], b2["fb"])                       # same kernel: bit-exact
     np.testing.assert_array_equal(b["radiance"].view(np.uint32), b2["radiance"].view(np.uint32))
     np.testing.assert_array_equal(b["id"], b2["id"])
-    # the instrumented variant is a separate compilation (FMA contraction may differ in the last
-    # bit); it must agree to rounding and trace exactly the same rays
+    # the instrumented variant is a separate compilation: ptxas may contract the shading arithmetic
+    # differently (last-bit differences), and reflections off curved mirrors amplify those at every
+    # bounce.  It must trace exactly the same rays, agree within 1e-6 on pixels whose whole ray
+    # tree is well conditioned (no exclusion flag, DESIGN reading 22), and within 1e-5 anywhere.
     np.testing.assert_array_equal(a["id"], b["id"])
-    assert np.abs(a["radiance"] - b["radiance"]).max() <= 1e-5
+    ref = Oracle(s).render()
+    diff = np.abs(a["radiance"] - b["radiance"])[..., :3].max(-1)
+    stable = ref["tflags"] == 0
+    print("instrumented vs product radiance: max", diff.max(), "on unflagged pixels", diff[stable].max())
+    assert diff[stable].max() <= 1e-6 and diff.max() <= 1e-5
     c = R.counters_dict(torch.from_numpy(a["counters"]))
-    ref = Oracle(s).render(flags=False)
     oc = dict(zip(["primary", "reflection", "refraction", "shadow"], ref["counts"]))
     assert c["primary"] == oc["primary"] == 2 * 64 * 48
     assert c["pixels"] == 2 * 64 * 48
