@@ -24,7 +24,7 @@ constexpr int RT_MINB = 1024 / RT_BLOCK;   // 64 registers: 1024 threads per SM
 // Radiance accumulates as sum over tree nodes of path_weight * local_term, which equals the
 // recursive definition c = local + kt*T(refr) + kr_eff*T(refl) (reading 17).
 template <bool COUNT, int ACC>
-__device__ __forceinline__ float3 trace_pixel(const TraceParams& P, float3 o, float3 d, int& prim_id, TravStack& stk,
+__device__ __forceinline__ float3 trace_pixel(const TraceParams& P, float3 o, float3 d, int& prim_id, const TravStack& stk,
                                               Counters<COUNT>& cnt, int* occ_hint) {
     constexpr bool BRUTE = ACC == ACC_BRUTE;
     const DevScene& S = P.sc;
@@ -206,12 +206,12 @@ __device__ __forceinline__ void pack_epilogue(const TraceParams& P, bool valid, 
 // the default kernel carries none of its registers)
 template <bool COUNT, int ACC, bool COMP = false>
 __global__ void __launch_bounds__(RT_BLOCK, RT_MINB) k_trace_stereo(const TraceParams P) {
-    extern __shared__ int s_stack[];                 // [stack_entries][RT_BLOCK]
+    __shared__ int s_stack[RT_SMEM_STACK * RT_BLOCK];   // [entry][thread]
     Counters<COUNT> cnt;
     cnt.zero();
     const int lane = threadIdx.x & 31;
     int lstack[STACK_CAP > RT_SMEM_STACK ? STACK_CAP - RT_SMEM_STACK : 1];
-    TravStack stk{(uint32_t)__cvta_generic_to_shared(s_stack + threadIdx.x), lstack};
+    const TravStack stk{TravStack::pin((uint32_t)__cvta_generic_to_shared(s_stack)), lstack};
     __shared__ int s_occ[RT_OCC_LIGHTS * RT_BLOCK];  // [light][thread] last-occluder hints
 #pragma unroll
     for (int j = 0; j < RT_OCC_LIGHTS; ++j) s_occ[j * RT_BLOCK + threadIdx.x] = -1;
@@ -349,9 +349,7 @@ static const void* trace_fn(unsigned flags) {
 
 int rtb_trace_block() { return RT_BLOCK; }
 
-size_t rtb_trace_smem(int stack_entries) {
-    return (size_t)(stack_entries < RT_SMEM_STACK ? stack_entries : RT_SMEM_STACK) * RT_BLOCK * sizeof(int);
-}
+size_t rtb_trace_smem(int) { return 0; }   // the stack's shared part is a static array
 
 
 cudaError_t rtb_launch_trace(const TraceParams& P, unsigned flags, int grid, cudaStream_t st) {

@@ -14,28 +14,45 @@ constexpr int RT_OCC_LIGHTS = 4;  // lights with a last-occluder hint slot (ligh
 // Per-thread traversal stack: the first RT_SMEM_STACK entries live in shared memory laid out
 // [entry][thread] (conflict-free), deeper entries in thread-local memory (L1-cached).  Keeping the
 // shared part short leaves most of the 228 KB L1/shared array to cache BVH nodes.
+//
+// The stack pointer is the byte offset of the next memory entry in the CTA's stack array:
+// sp = i * E + 4 * tid for logical memory depth i (E = RT_BLOCK * 4 bytes per entry row; 4 * tid
+// < E, so i = sp / E).  One loop-carried register is depth, emptiness test (sp < E, an immediate
+// compare) and STS/LDS offset; the array's shared-window address `base` is the same for every
+// thread and sits in a uniform register (STS [R + UR]).  It is pinned there through a volatile
+// move: plain __cvta_generic_to_shared values are rematerialised by ptxas at every use from
+// S2R SR_CgaCtaId (+ SR_TID.X for a per-thread base, as in round 1), which put S2R latencies in
+// front of every push and refill load.
+constexpr uint32_t STK_E = RT_BLOCK * 4u;   // bytes per stack entry row
 struct TravStack {
-    // 32-bit shared-window address of this thread's entry 0: STS/LDS take it directly instead of
-    // rebuilding the generic->shared conversion (S2R CgaCtaId + LEA) at every push and pop
-    uint32_t sa;
-    int* l;   // local:  l[i - RT_SMEM_STACK]
-    __device__ __forceinline__ void set(int i, int v) {
-        if (i < RT_SMEM_STACK) asm volatile("st.shared.b32 [%0], %1;" ::"r"(sa + (uint32_t)i * (RT_BLOCK * 4u)), "r"(v));
+    uint32_t base;   // shared-window byte address of the CTA's stack array (uniform)
+    int* l;          // local part: logical entry i >= RT_SMEM_STACK at l[i - RT_SMEM_STACK]
+    __device__ __forceinline__ static uint32_t pin(uint32_t a) {
+        uint32_t r;
+        asm volatile("mov.u32 %0, %1;" : "=r"(r) : "r"(a));
+        return r;
+    }
+    __device__ __forceinline__ static uint32_t empty() { return 4u * threadIdx.x; }
+    __device__ __forceinline__ static bool nonempty(uint32_t a) { return a >= STK_E; }
+    // true when entries a and a + E both lie in the shared part
+    __device__ __forceinline__ static bool two_fit(uint32_t a) { return a < (RT_SMEM_STACK - 1) * STK_E; }
+    __device__ __forceinline__ void st_if(bool p, uint32_t a, int v) const {
+        asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.shared.b32 [%0], %1;\n\t}" ::"r"(base + a),
+                     "r"(v), "r"((uint32_t)p));
+    }
+    __device__ __forceinline__ int ld(uint32_t a) const {
+        int v;
+        asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(base + a));
+        return v;
+    }
+    __device__ __forceinline__ void set(uint32_t a, int v) const {
+        const int i = (int)(a / STK_E);
+        if (i < RT_SMEM_STACK) st_if(true, a, v);
         else l[i - RT_SMEM_STACK] = v;
     }
-    __device__ __forceinline__ int get(int i) const {
-        if (i < RT_SMEM_STACK) {
-            int v;
-            asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(sa + (uint32_t)i * (RT_BLOCK * 4u)));
-            return v;
-        }
-        return l[i - RT_SMEM_STACK];
-    }
-    // shared address of entry i (valid for i < RT_SMEM_STACK); entry i + k is at + k * RT_BLOCK * 4
-    __device__ __forceinline__ uint32_t addr(int i) const { return sa + (uint32_t)i * (RT_BLOCK * 4u); }
-    __device__ __forceinline__ static void st_if(bool p, uint32_t a, int v) {
-        asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.shared.b32 [%0], %1;\n\t}" ::"r"(a), "r"(v),
-                     "r"((uint32_t)p));
+    __device__ __forceinline__ int get(uint32_t a) const {
+        const int i = (int)(a / STK_E);
+        return i < RT_SMEM_STACK ? ld(a) : l[i - RT_SMEM_STACK];
     }
 };
 
@@ -185,8 +202,8 @@ __device__ __forceinline__ int pick4(const int4& c, uint32_t i) {
 // patterns order like unsigned ints; the 2 low bits carry the child slot and a 5-exchange network
 // sorts them.  The nearest continues, the second nearest becomes the cached top, the others are
 // pushed far-to-near with predicated stores (no branches).
-__device__ __forceinline__ bool order_push_top(unsigned m, const float tn[4], const int4& ch, TravStack& stk, int& sp,
-                                               int& top, int& node) {
+__device__ __forceinline__ bool order_push_top(unsigned m, const float tn[4], const int4& ch, const TravStack& stk,
+                                               uint32_t& sp, int& top, int& node) {
     if (!m) return false;
     uint32_t k0 = (m & 1) ? ((__float_as_uint(tn[0]) & ~3u) | 0u) : 0xffffffffu;
     uint32_t k1 = (m & 2) ? ((__float_as_uint(tn[1]) & ~3u) | 1u) : 0xffffffffu;
@@ -196,19 +213,18 @@ __device__ __forceinline__ bool order_push_top(unsigned m, const float tn[4], co
     const int nh = __popc(m);
     if (nh > 1) {
         // old top -> memory entry sp-1; k3, k2 -> entries sp.. (far first); k1 -> top
-        if (sp + 2 <= RT_SMEM_STACK) {
-            const uint32_t a = stk.addr(sp);
-            constexpr uint32_t E = RT_BLOCK * 4u;
-            TravStack::st_if(sp > 0, a - E, top);
-            TravStack::st_if(nh > 3, a, pick4(ch, k3 & 3u));
-            TravStack::st_if(nh > 2, a + (uint32_t)(nh - 3) * E, pick4(ch, k2 & 3u));
+        const bool has = stk.nonempty(sp);               // logical depth > 0: the old top is real
+        if (stk.two_fit(sp)) {
+            stk.st_if(has, sp - STK_E, top);
+            stk.st_if(nh > 3, sp, pick4(ch, k3 & 3u));
+            stk.st_if(nh > 2, sp + (uint32_t)(nh - 3) * STK_E, pick4(ch, k2 & 3u));
         } else {
-            if (sp > 0) stk.set(sp - 1, top);
+            if (has) stk.set(sp - STK_E, top);
             if (nh > 3) stk.set(sp, pick4(ch, k3 & 3u));
-            if (nh > 2) stk.set(sp + nh - 3, pick4(ch, k2 & 3u));
+            if (nh > 2) stk.set(sp + (uint32_t)(nh - 3) * STK_E, pick4(ch, k2 & 3u));
         }
         top = pick4(ch, k1 & 3u);
-        sp += nh - 1;
+        sp += (uint32_t)(nh - 1) * STK_E;
     }
     node = pick4(ch, k0 & 3u);
     return true;
@@ -216,34 +232,35 @@ __device__ __forceinline__ bool order_push_top(unsigned m, const float tn[4], co
 
 // Any-hit (shadow) rays: continue with the lowest hit slot, push the others in slot order (no
 // distance sort: measured 7 % faster, and fewer triangle tests).
-__device__ __forceinline__ bool plain_push_top(unsigned m, const int4& ch, TravStack& stk, int& sp, int& top, int& node) {
+__device__ __forceinline__ bool plain_push_top(unsigned m, const int4& ch, const TravStack& stk, uint32_t& sp, int& top,
+                                               int& node) {
     if (!m) return false;
     const unsigned r = m & (m - 1u);                       // pushed slots (all hits but the lowest)
     if (r) {
         const int hi = 31 - __clz(r);                      // highest pushed slot -> top
         const unsigned rr = r & ~(1u << hi);               // the others -> memory, slot order
-        if (sp + 2 <= RT_SMEM_STACK) {
-            const uint32_t a = stk.addr(sp);
-            constexpr uint32_t E = RT_BLOCK * 4u;
-            TravStack::st_if(sp > 0, a - E, top);
-            TravStack::st_if(rr & 2u, a, ch.y);
-            TravStack::st_if(rr & 4u, a + ((rr >> 1) & 1u) * E, ch.z);
+        const bool has = stk.nonempty(sp);
+        if (stk.two_fit(sp)) {
+            stk.st_if(has, sp - STK_E, top);
+            stk.st_if(rr & 2u, sp, ch.y);
+            stk.st_if(rr & 4u, sp + ((rr >> 1) & 1u) * STK_E, ch.z);
         } else {
-            if (sp > 0) stk.set(sp - 1, top);
+            if (has) stk.set(sp - STK_E, top);
             if (rr & 2u) stk.set(sp, ch.y);
-            if (rr & 4u) stk.set(sp + (int)((rr >> 1) & 1u), ch.z);
+            if (rr & 4u) stk.set(sp + ((rr >> 1) & 1u) * STK_E, ch.z);
         }
         top = pick4(ch, (uint32_t)hi);
-        sp += __popc(r);
+        sp += (uint32_t)__popc(r) * STK_E;
     }
     node = pick4(ch, __ffs(m) - 1);
     return true;
 }
 
-__device__ __forceinline__ bool pop_top(TravStack& stk, int& sp, int& top, int& node) {
-    if (sp == 0) return false;
+__device__ __forceinline__ bool pop_top(const TravStack& stk, uint32_t& sp, int& top, int& node) {
+    if (!stk.nonempty(sp)) return false;
     node = top;
-    if (--sp > 0) top = stk.get(sp - 1);
+    sp -= STK_E;
+    if (stk.nonempty(sp)) top = stk.get(sp - STK_E);
     return true;
 }
 
@@ -354,7 +371,7 @@ __device__ __forceinline__ bool kd_trace(const DevScene& S, float3 o, float3 d, 
 // the planes.  Acceptance: t > t_min and (t, gid) lexicographically smallest (
 // reading 9).  Children are visited near-to-far (order_push_top).
 template <bool COUNT, int ACC>
-__device__ __forceinline__ Hit closest_hit(const DevScene& S, float3 o, float3 d, TravStack& stk, Counters<COUNT>& cnt) {
+__device__ __forceinline__ Hit closest_hit(const DevScene& S, float3 o, float3 d, const TravStack& stk, Counters<COUNT>& cnt) {
     constexpr bool BRUTE = ACC == ACC_BRUTE;
     Hit h;
     h.t = __int_as_float(0x7f800000);
@@ -387,7 +404,7 @@ __device__ __forceinline__ Hit closest_hit(const DevScene& S, float3 o, float3 d
         return h;
     }
     const RayBox rb = make_raybox(o, d, S.bound);
-    int sp = 0;
+    uint32_t sp = stk.empty();
     int node = S.root;
     int top = 0;          // cached top stack entry
     while (true) {
@@ -412,7 +429,7 @@ __device__ __forceinline__ Hit closest_hit(const DevScene& S, float3 o, float3 d
 // and, if it blocks the segment, the answer is already exact (visibility is a boolean, so which
 // occluder proves it does not matter); otherwise the traversal runs and records its occluder.
 template <bool COUNT, int ACC>
-__device__ __forceinline__ bool occluded(const DevScene& S, float3 o, float3 d, float dist, TravStack& stk, Counters<COUNT>& cnt,
+__device__ __forceinline__ bool occluded(const DevScene& S, float3 o, float3 d, float dist, const TravStack& stk, Counters<COUNT>& cnt,
                                          int* hint = nullptr) {
     constexpr bool BRUTE = ACC == ACC_BRUTE;
     for (int i = 0; i < S.n_planes; ++i) {
@@ -446,7 +463,7 @@ __device__ __forceinline__ bool occluded(const DevScene& S, float3 o, float3 d, 
     };
     if (BRUTE) return leaf_test(0, S.n_bvh - 1);
     const RayBox rb = make_raybox(o, d, S.bound);
-    int sp = 0;
+    uint32_t sp = stk.empty();
     int node = S.root;
     int top = 0;          // cached top stack entry
     while (true) {

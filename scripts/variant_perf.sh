@@ -8,7 +8,7 @@ for round in 1 2; do
   for lib in paper_1702_01530_b200/lib/librt_b200.so paper_1702_01530_b200/lib/variants/*.so; do
     n=$(basename $lib .so)
     for c in $CFGS; do
-      RT_LIB_PATH=$PWD/$lib timeout 300 python scripts/quick_perf.py $c 2>&1 | grep -E "median" | sed "s/^/$n r$round /" >> $OUT/variants.log
+      RT_LIB_PATH=$PWD/$lib timeout 300 python scripts/quick_perf.py $c 2>&1 | grep -E "median|inflight" | sed "s/^/$n r$round /" >> $OUT/variants.log
     done
   done
 done
