@@ -17,7 +17,11 @@
 
 namespace rtb {
 
+#ifndef RT_MINB_X
 constexpr int RT_MINB = 1024 / RT_BLOCK;   // 64 registers: 1024 threads per SM
+#else
+constexpr int RT_MINB = RT_MINB_X;
+#endif
 
 // Trace the whole ray tree of one pixel.  Iterative: the reflection child continues in
 // registers, the refraction child is pushed on a per-thread stack (<= max_depth entries).

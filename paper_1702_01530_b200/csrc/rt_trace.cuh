@@ -8,7 +8,11 @@ namespace rtb {
 
 constexpr int RT_BLOCK = 64;      // threads per trace CTA (stack stride); small CTAs free their slots as soon as
                                   // their 2 warps finish, so a next frame in flight fills the SM sooner
+#ifndef RT_SMEM_STACK_X
 constexpr int RT_SMEM_STACK = 16; // traversal-stack entries kept in shared memory; deeper ones in local
+#else
+constexpr int RT_SMEM_STACK = RT_SMEM_STACK_X;
+#endif
 constexpr int RT_OCC_LIGHTS = 4;  // lights with a last-occluder hint slot (light j uses slot j; others none)
 
 // Per-thread traversal stack: the first RT_SMEM_STACK entries live in shared memory laid out
@@ -195,15 +199,14 @@ __device__ __forceinline__ int pick4(const int4& c, uint32_t i) {
     return (i & 2u) ? hi : lo;
 }
 
-// Traversal stack with its top entry cached in a register: logical entries [0, sp) are memory entries
-// [0, sp-1) plus `top`.  A pop is a register move; the LDS/LDL that refills `top` is issued
-// right away but its latency overlaps the popped node's visit instead of preceding it.
 // Nearest-hit rays: visit order of the hit children.  Entry distances are >= 0, so their bit
 // patterns order like unsigned ints; the 2 low bits carry the child slot and a 5-exchange network
-// sorts them.  The nearest continues, the second nearest becomes the cached top, the others are
-// pushed far-to-near with predicated stores (no branches).
-__device__ __forceinline__ bool order_push_top(unsigned m, const float tn[4], const int4& ch, const TravStack& stk,
-                                               uint32_t& sp, int& top, int& node) {
+// sorts them.  The nearest continues, the others are pushed far-to-near with predicated stores
+// (no branches).  No cached top entry: with the stack pointer a plain shared offset the pop's LDS
+// costs less than the top register's bookkeeping (C4 -0.6 %, C3 -0.6 %; round 1's v16 kept one
+// when every push and pop also rebuilt the stack address).
+__device__ __forceinline__ bool order_push(unsigned m, const float tn[4], const int4& ch, const TravStack& stk,
+                                           uint32_t& sp, int& node) {
     if (!m) return false;
     uint32_t k0 = (m & 1) ? ((__float_as_uint(tn[0]) & ~3u) | 0u) : 0xffffffffu;
     uint32_t k1 = (m & 2) ? ((__float_as_uint(tn[1]) & ~3u) | 1u) : 0xffffffffu;
@@ -212,57 +215,52 @@ __device__ __forceinline__ bool order_push_top(unsigned m, const float tn[4], co
     cswap(k0, k1); cswap(k2, k3); cswap(k0, k2); cswap(k1, k3); cswap(k1, k2);
     const int nh = __popc(m);
     if (nh > 1) {
-        // old top -> memory entry sp-1; k3, k2 -> entries sp.. (far first); k1 -> top
-        const bool has = stk.nonempty(sp);               // logical depth > 0: the old top is real
-        if (stk.two_fit(sp)) {
-            stk.st_if(has, sp - STK_E, top);
+        // k3, k2, k1 -> entries sp, sp+1, sp+2 (far first; only the hit ones)
+        const uint32_t a = sp + (uint32_t)(nh - 2) * STK_E;   // entry of k1
+        if (stk.two_fit(sp + STK_E)) {
             stk.st_if(nh > 3, sp, pick4(ch, k3 & 3u));
-            stk.st_if(nh > 2, sp + (uint32_t)(nh - 3) * STK_E, pick4(ch, k2 & 3u));
+            stk.st_if(nh > 2, a - STK_E, pick4(ch, k2 & 3u));
+            stk.st_if(true, a, pick4(ch, k1 & 3u));
         } else {
-            if (has) stk.set(sp - STK_E, top);
             if (nh > 3) stk.set(sp, pick4(ch, k3 & 3u));
-            if (nh > 2) stk.set(sp + (uint32_t)(nh - 3) * STK_E, pick4(ch, k2 & 3u));
+            if (nh > 2) stk.set(a - STK_E, pick4(ch, k2 & 3u));
+            stk.set(a, pick4(ch, k1 & 3u));
         }
-        top = pick4(ch, k1 & 3u);
-        sp += (uint32_t)(nh - 1) * STK_E;
+        sp = a + STK_E;
     }
     node = pick4(ch, k0 & 3u);
     return true;
 }
 
-// Any-hit (shadow) rays: continue with the lowest hit slot, push the others in slot order (no
-// distance sort: measured 7 % faster, and fewer triangle tests).
-__device__ __forceinline__ bool plain_push_top(unsigned m, const int4& ch, const TravStack& stk, uint32_t& sp, int& top,
-                                               int& node) {
+// Any-hit (shadow) rays: continue with the lowest hit slot, the others (slots 1-3 only: slot 0 is
+// always the lowest when hit) go to memory in slot order -- no distance sort (measured 7 % faster,
+// and fewer triangle tests) and no cached top entry (the pop's LDS latency costs less than the
+// top register's bookkeeping: C4 -1.3 %, C3 -1 %).
+__device__ __forceinline__ bool plain_push(unsigned m, const int4& ch, const TravStack& stk, uint32_t& sp, int& node) {
     if (!m) return false;
-    const unsigned r = m & (m - 1u);                       // pushed slots (all hits but the lowest)
+    const unsigned r = m & (m - 1u);
     if (r) {
-        const int hi = 31 - __clz(r);                      // highest pushed slot -> top
-        const unsigned rr = r & ~(1u << hi);               // the others -> memory, slot order
-        const bool has = stk.nonempty(sp);
-        if (stk.two_fit(sp)) {
-            stk.st_if(has, sp - STK_E, top);
-            stk.st_if(rr & 2u, sp, ch.y);
-            stk.st_if(rr & 4u, sp + ((rr >> 1) & 1u) * STK_E, ch.z);
+        if (stk.two_fit(sp + STK_E)) {
+            stk.st_if(r & 2u, sp, ch.y);
+            stk.st_if(r & 4u, sp + ((r >> 1) & 1u) * STK_E, ch.z);
+            stk.st_if(r & 8u, sp + (uint32_t)__popc(r & 6u) * STK_E, ch.w);
         } else {
-            if (has) stk.set(sp - STK_E, top);
-            if (rr & 2u) stk.set(sp, ch.y);
-            if (rr & 4u) stk.set(sp + ((rr >> 1) & 1u) * STK_E, ch.z);
+            if (r & 2u) stk.set(sp, ch.y);
+            if (r & 4u) stk.set(sp + ((r >> 1) & 1u) * STK_E, ch.z);
+            if (r & 8u) stk.set(sp + (uint32_t)__popc(r & 6u) * STK_E, ch.w);
         }
-        top = pick4(ch, (uint32_t)hi);
         sp += (uint32_t)__popc(r) * STK_E;
     }
     node = pick4(ch, __ffs(m) - 1);
     return true;
 }
-
-__device__ __forceinline__ bool pop_top(const TravStack& stk, uint32_t& sp, int& top, int& node) {
+__device__ __forceinline__ bool pop_mem(const TravStack& stk, uint32_t& sp, int& node) {
     if (!stk.nonempty(sp)) return false;
-    node = top;
     sp -= STK_E;
-    if (stk.nonempty(sp)) top = stk.get(sp - STK_E);
+    node = stk.get(sp);
     return true;
 }
+
 
 // ---------------------------------------------------------------- NEXT-4: kd-tree ablation
 // Stack traversal of the host-built kd-tree (rt_kdtree.cu): front-to-back cells, each split
@@ -369,7 +367,7 @@ __device__ __forceinline__ bool kd_trace(const DevScene& S, float3 o, float3 d, 
 
 // Nearest hit over the 4-wide BVH (or every BVH primitive when BRUTE, the kd-tree when KD) and
 // the planes.  Acceptance: t > t_min and (t, gid) lexicographically smallest (
-// reading 9).  Children are visited near-to-far (order_push_top).
+// reading 9).  Children are visited near-to-far (order_push).
 template <bool COUNT, int ACC>
 __device__ __forceinline__ Hit closest_hit(const DevScene& S, float3 o, float3 d, const TravStack& stk, Counters<COUNT>& cnt) {
     constexpr bool BRUTE = ACC == ACC_BRUTE;
@@ -406,7 +404,6 @@ __device__ __forceinline__ Hit closest_hit(const DevScene& S, float3 o, float3 d
     const RayBox rb = make_raybox(o, d, S.bound);
     uint32_t sp = stk.empty();
     int node = S.root;
-    int top = 0;          // cached top stack entry
     while (true) {
         if (node >= 0) {
             cnt.add(CNT_NODE_VISITS);
@@ -414,13 +411,13 @@ __device__ __forceinline__ Hit closest_hit(const DevScene& S, float3 o, float3 d
             int4 ch;
             const unsigned m = node4_hits(S.nodes, node, rb, h.t, tn, ch);
             count_boxes(cnt, ch);
-            if (order_push_top(m, tn, ch, stk, sp, top, node)) continue;
+            if (order_push(m, tn, ch, stk, sp, node)) continue;
         } else {
             const int enc = ~node;
             const int first = enc & ((1 << LEAF_SHIFT) - 1);
             leaf_test(first, first + (enc >> LEAF_SHIFT));
         }
-        if (!pop_top(stk, sp, top, node)) return h;
+        if (!pop_mem(stk, sp, node)) return h;
     }
 }
 
@@ -465,7 +462,6 @@ __device__ __forceinline__ bool occluded(const DevScene& S, float3 o, float3 d, 
     const RayBox rb = make_raybox(o, d, S.bound);
     uint32_t sp = stk.empty();
     int node = S.root;
-    int top = 0;          // cached top stack entry
     while (true) {
         if (node >= 0) {
             cnt.add(CNT_NODE_VISITS);
@@ -473,13 +469,13 @@ __device__ __forceinline__ bool occluded(const DevScene& S, float3 o, float3 d, 
             int4 ch;
             const unsigned m = node4_hits(S.nodes, node, rb, dist, tn, ch);
             count_boxes(cnt, ch);
-            if (plain_push_top(m, ch, stk, sp, top, node)) continue;
+            if (plain_push(m, ch, stk, sp, node)) continue;
         } else {
             const int enc = ~node;
             const int first = enc & ((1 << LEAF_SHIFT) - 1);
             if (leaf_test(first, first + (enc >> LEAF_SHIFT))) return true;
         }
-        if (!pop_top(stk, sp, top, node)) return false;
+        if (!pop_mem(stk, sp, node)) return false;
     }
 }
 
