@@ -617,6 +617,15 @@ __global__ void k_wide_dp(BuildBuffers B, const int* __restrict__ choice, const 
                 st_code[sp] = B.left[x]; st_j[sp++] = kx;
             }
         }
+        // the node's internal children get consecutive slots (one allocation), so siblings share
+        // the cache lines at their boundaries
+        int n_int = 0;
+        for (int c = 0; c < n; ++c) n_int += codes[c] >= 0;
+        int slot = 0, q = 0;
+        if (n_int) {
+            slot = atomicAdd(&counters[1], n_int);
+            q = atomicAdd(&counters[0], n_int);
+        }
         float3 lo[BVH_W], hi[BVH_W];
         int oc[BVH_W];
         for (int c = 0; c < BVH_W; ++c) {
@@ -630,10 +639,8 @@ __global__ void k_wide_dp(BuildBuffers B, const int* __restrict__ choice, const 
             if (w.code < 0) {
                 oc[c] = w.code;                                     // BVH2 leaf: ~slot (count 1)
             } else {
-                const int slot = atomicAdd(&counters[1], 1);
-                const int q = atomicAdd(&counters[0], 1);
-                fout[q] = make_int2(w.code, slot);
-                oc[c] = slot;
+                fout[q++] = make_int2(w.code, slot);
+                oc[c] = slot++;
             }
         }
         node_write(B.nodes4 + NODE_F4 * (size_t)dst, lo, hi, oc);
