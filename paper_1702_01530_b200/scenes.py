@@ -443,6 +443,40 @@ def paper_scene(n_objects):
     return s.finalize()
 
 
+def scene_urchin(n=30000, seed=7):
+    """Stress scene for the traversal stack (not a BASELINE config): n triangles radiating from
+    the origin in seeded random directions (one vertex within 0.05 of the origin, the other two
+    ~2-3 units out and 0.5-1 apart, aspect ratio <= ~6), so every BVH box contains the centre and
+    a ray through the centre hits all four children at every level of its first descent: stack
+    depth ~3 per BVH4 level, beyond the 16 shared-memory entries.  Mirror-ish material, one light,
+    depth 1.  (Slivers 0.01-0.03 wide were tried first: Moller-Trumbore's FP32 edge decision
+    degrades with the aspect ratio -- det ~ area, so the barycentric error grows ~aspect x ulp --
+    and one shadow ray 2e-4 relative from a sliver's tip edge flipped, outside every band of
+    reading 22; the north star's tolerances presume well-shaped triangles like C3/C4's.)"""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    u = rng.normal(size=(n, 3))
+    u /= np.linalg.norm(u, axis=1, keepdims=True)
+    w = rng.normal(size=(n, 3))
+    w -= (w * u).sum(1, keepdims=True) * u                 # a direction perpendicular to u
+    w /= np.linalg.norm(w, axis=1, keepdims=True)
+    r = rng.uniform(2.0, 3.0, size=(n, 1))
+    half = rng.uniform(0.25, 0.5, size=(n, 1))
+    a = rng.uniform(-0.05, 0.05, size=(n, 3))
+    b = r * u + half * w
+    c = r * u - half * w
+    s = Scene("urchin")
+    s.vertices = np.stack([a, b, c], 1).reshape(-1, 3)
+    s.tris = np.arange(3 * n, dtype=np.uint32).reshape(n, 3)
+    s.tri_mat = np.zeros(n, np.uint32)
+    s.materials = np.stack([material((0.7, 0.5, 0.3), 0.4, 24.0, kr=0.3)])
+    s.lights = np.array([[4.0, 6.0, 8.0, 1.0, 1.0, 1.0]])
+    s.ambient = np.full(3, 0.1)
+    s.background = np.array(SKY)
+    s.rig = _rig((0.0, 0.0, 8.0), (0.0, 0.0, 0.0), 40.0)
+    s.width, s.height, s.max_depth = 40, 30, 1
+    return s.finalize()
+
+
 CONFIGS = {
     "C1": scene_c1,
     "C2": scene_c2,

@@ -145,6 +145,48 @@ def test_bvh_equals_bruteforce(R):
         np.testing.assert_array_equal(a["fb"], b["fb"])
 
 
+def _first_descent_stack_depth(nodes, o, d):
+    """Host emulation (float64 slab tests) of the nearest-hit traversal's first descent from the
+    root: hit children sorted near-first, the nearest continues, the others are pushed; returns the
+    stack depth when the descent reaches its first leaf (no t_best pruning has happened yet)."""
+    W = rt.rt_bvh_width()
+    child = nodes[:, 6 * W:7 * W].view(np.int32)
+    inv = 1.0 / np.where(d == 0, 1e-300, d)
+    node, depth = 0, 0
+    while node >= 0:
+        lo = np.stack([nodes[node, 0 * W:1 * W], nodes[node, 2 * W:3 * W], nodes[node, 4 * W:5 * W]], 1).astype(np.float64)
+        hi = np.stack([nodes[node, 1 * W:2 * W], nodes[node, 3 * W:4 * W], nodes[node, 5 * W:6 * W]], 1).astype(np.float64)
+        t0, t1 = (lo - o) * inv, (hi - o) * inv
+        tn = np.maximum(np.minimum(t0, t1).max(1), 0.0)
+        tf = np.maximum(t0, t1).min(1)
+        hit = [(tn[c], c) for c in range(W) if child[node, c] != 0x7FFFFFFF and tn[c] <= tf[c]]
+        if not hit:
+            break
+        hit.sort()
+        depth += len(hit) - 1
+        node = int(child[node, hit[0][1]])
+    return depth
+
+
+def test_deep_traversal_stack(R):
+    """Traversal stacks deeper than the 16 shared-memory entries take the thread-local part
+    (TravStack::set/get): a scene where every BVH box contains the centre (scenes.scene_urchin:
+    30 000 slivers radiating from the origin) must still give BVH == brute force bit for bit, and
+    oracle parity.  The host emulation shows the centre ray's first descent alone stacks > 16."""
+    s = scenes.scene_urchin()
+    R.upload(s)
+    nodes, _ = rt.rt_bvh_export(R.ctx)
+    depth = _first_descent_stack_depth(nodes, np.array([0.0, 0.0, 8.0]), np.array([0.0, 0.0, -1.0]))
+    print("urchin: centre-ray stack depth at the first leaf", depth)
+    assert depth > 16
+    a = gpu_render(R, s)
+    b = gpu_render(R, s, brute=True)
+    np.testing.assert_array_equal(a["id"], b["id"])
+    np.testing.assert_array_equal(a["radiance"].view(np.uint32), b["radiance"].view(np.uint32))
+    np.testing.assert_array_equal(a["fb"], b["fb"])
+    full_parity(R, s, "urchin (deep stacks)")
+
+
 def test_sah_subtrees_do_not_change_the_image(R, monkeypatch):
     """The SAH rebuild of small LBVH subtrees (k_sah_subtrees, DESIGN §5 v21) changes the tree, not
     the result: hits are chosen by (t, ID) over exactly computed t, so the image, IDs and radiance
