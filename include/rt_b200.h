@@ -287,7 +287,10 @@ rt_status rt_unpack_shards(rt_context* ctx, const void* gathered, uint32_t width
  * radiance / shard planes are rejected (render an explicit shard, shard_world > 1, which stays a
  * local render of those tiles).  Rank 0's framebuffers must stay allocated until the frame's work
  * on rank 0's stream completes.  Device-side waits are bounded (env RT_DIST_TIMEOUT_S, default
- * 60 s): a rank that never posts makes later calls fail with RT_ERR_PEER, not a hung GPU. */
+ * 60 s): a rank that never posts makes later calls fail with RT_ERR_PEER, not a hung GPU.
+ * A one-rank world renders locally, except with flags RT_DIST_NCCL: then every frame runs the
+ * NCCL transport's whole data path (pack, a one-rank ncclGather, unpack) -- a check of that
+ * transport on one GPU, since NCCL refuses two ranks on one device. */
 #define RT_DIST_ID_BYTES 128
 #define RT_DIST_PEER 0u          /* fused peer-store assembly (default)                     */
 #define RT_DIST_NCCL 1u          /* NCCL gather of packed shards + root unpack              */

@@ -387,7 +387,10 @@ static rt_status dist_frame(rt_context* c, DistState* D, const rt_render_params*
 rt_status rtb_dist_render(rt_context* c, const rt_render_params* p, const rt_outputs* out, cudaStream_t stream) {
     DistState* D = c->dist;
     // an explicit tile subset (shard_world > 1) is a local render of those tiles, not a frame
-    if (p->shard_world != 1 || D->world == 1) return rtb_render_local(c, p, out, stream);
+    // (a one-rank world renders locally, except under an explicit RT_DIST_NCCL: then the frame goes
+    // through the NCCL transport -- pack, a one-rank ncclGather, unpack -- the whole data path of a
+    // multi-GPU frame, exercisable on one GPU)
+    if (p->shard_world != 1 || (D->world == 1 && !D->comm)) return rtb_render_local(c, p, out, stream);
     rt_status st;
     if ((st = check_err(D))) return st;
     if (p->flags & ~(RT_RENDER_COUNT | RT_RENDER_BRUTE_FORCE | RT_RENDER_KDTREE))
@@ -607,7 +610,7 @@ rt_status rt_dist_init(rt_context* c, int rank, int world, const void* id, uint3
     bool all_ipc = true;
     for (int r = 0; r < world; ++r) all_ipc = all_ipc && S->joined[r] == 2;
     D->transport = (S->transport == RT_DIST_PEER && all_ipc) ? RT_DIST_PEER : RT_DIST_NCCL;
-    if (D->transport == RT_DIST_NCCL && world > 1) {
+    if (D->transport == RT_DIST_NCCL && (world > 1 || flags == RT_DIST_NCCL)) {
         if (!nccl().ok) return bail(rtb_fail(RT_ERR_PEER, "rt_dist_init: peer mappings failed and libnccl.so.2 is unavailable"));
         ncclUniqueId u;
         memcpy(&u, id, RT_DIST_ID_BYTES);
