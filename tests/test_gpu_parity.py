@@ -156,7 +156,8 @@ def _first_descent_stack_depth(nodes, o, d):
     while node >= 0:
         lo = np.stack([nodes[node, 0 * W:1 * W], nodes[node, 2 * W:3 * W], nodes[node, 4 * W:5 * W]], 1).astype(np.float64)
         hi = np.stack([nodes[node, 1 * W:2 * W], nodes[node, 3 * W:4 * W], nodes[node, 5 * W:6 * W]], 1).astype(np.float64)
-        t0, t1 = (lo - o) * inv, (hi - o) * inv
+        with np.errstate(over="ignore", invalid="ignore"):     # axis-parallel ray x inverted empty boxes
+            t0, t1 = (lo - o) * inv, (hi - o) * inv
         tn = np.maximum(np.minimum(t0, t1).max(1), 0.0)
         tf = np.maximum(t0, t1).min(1)
         hit = [(tn[c], c) for c in range(W) if child[node, c] != 0x7FFFFFFF and tn[c] <= tf[c]]
