@@ -752,7 +752,9 @@ rt_status rtb_render_local(rt_context* c, const rt_render_params* p, const rt_ou
     if (P.n_work == 0) return RT_OK;
     CUDA_TRY(cudaSetDevice(c->device));
     int occ = 0;
-    const unsigned kflags = P.comp ? RTB_TRACE_COMPOSE : (p->flags & (RT_RENDER_COUNT | RT_RENDER_BRUTE_FORCE | RT_RENDER_KDTREE));
+    unsigned kflags = P.comp ? RTB_TRACE_COMPOSE : (p->flags & (RT_RENDER_COUNT | RT_RENDER_BRUTE_FORCE | RT_RENDER_KDTREE));
+    if (P.sc.n_spheres == 0 && P.sc.n_planes == 0 && !(kflags & (RT_RENDER_COUNT | RT_RENDER_BRUTE_FORCE | RT_RENDER_KDTREE)))
+        kflags |= RTB_TRACE_TRI;                  // triangles-only scene: the instantiation without sphere/plane code
     CUDA_TRY(rtb_trace_occupancy(kflags, P.stack_entries, &occ));
     if (occ < 1) occ = 1;
     const int block = rtb_trace_block();

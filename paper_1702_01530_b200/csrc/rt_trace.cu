@@ -27,7 +27,7 @@ constexpr int RT_MINB = RT_MINB_X;
 // registers, the refraction child is pushed on a per-thread stack (<= max_depth entries).
 // Radiance accumulates as sum over tree nodes of path_weight * local_term, which equals the
 // recursive definition c = local + kt*T(refr) + kr_eff*T(refl) (reading 17).
-template <bool COUNT, int ACC>
+template <bool COUNT, int ACC, bool TRI = false>
 __device__ __forceinline__ float3 trace_pixel(const TraceParams& P, float3 o, float3 d, int& prim_id, const TravStack& stk,
                                               Counters<COUNT>& cnt, int* occ_hint) {
     constexpr bool BRUTE = ACC == ACC_BRUTE;
@@ -40,7 +40,7 @@ __device__ __forceinline__ float3 trace_pixel(const TraceParams& P, float3 o, fl
     float3 col = f3(0.f, 0.f, 0.f);
     cnt.add(CNT_PRIMARY);
     while (true) {
-        const Hit h = closest_hit<COUNT, ACC>(S, o, d, stk, cnt);
+        const Hit h = closest_hit<COUNT, ACC, TRI>(S, o, d, stk, cnt);
         if (primary) { prim_id = h.gid; primary = false; }
         bool cont = false;
         if (h.gid < 0) {
@@ -51,7 +51,7 @@ __device__ __forceinline__ float3 trace_pixel(const TraceParams& P, float3 o, fl
             const float3 p = fma3(d, h.t, o);
             float3 ng;
             int mat;
-            if (h.slot < 0) {
+            if (!TRI && h.slot < 0) {
                 const int i = ~h.slot;
                 ng = xyz(__ldg(&S.planes[i]));
                 mat = __ldg(&S.plane_mat[i]);
@@ -61,7 +61,7 @@ __device__ __forceinline__ float3 trace_pixel(const TraceParams& P, float3 o, fl
                 mat = __float_as_int(b.w);
                 // (p - c) / r in FP32 is off unit length by the hit point's rounding (~1e-5 relative),
                 // which a Phong exponent of 256 amplifies to ~1e-2: renormalise like triangles
-                if (h.gid < S.n_spheres) ng = normalize(p - xyz(a));
+                if (!TRI && h.gid < S.n_spheres) ng = normalize(p - xyz(a));
                 else ng = normalize(cross(xyz(b), xyz(__ldg(&S.prims[3 * h.slot + 2]))));
             }
             const bool front = dot(d, ng) < 0.0f;
@@ -84,7 +84,7 @@ __device__ __forceinline__ float3 trace_pixel(const TraceParams& P, float3 o, fl
                 const float dist = sqrt_dist(dot(sv, sv));
                 cnt.add(CNT_SHADOW);
                 int* hint = j < RT_OCC_LIGHTS ? occ_hint + j * RT_BLOCK : nullptr;
-                if (!occluded<COUNT, ACC>(S, os, sv * rcp_dist(dist), dist, stk, cnt, hint)) c = c + term;   // reading 3
+                if (!occluded<COUNT, ACC, TRI>(S, os, sv * rcp_dist(dist), dist, stk, cnt, hint)) c = c + term;   // reading 3
             }
             col = fma3(c, w, col);
             if (depth > 0) {
@@ -208,7 +208,7 @@ __device__ __forceinline__ void pack_epilogue(const TraceParams& P, bool valid, 
 // atomic and traces one pixel tree per lane; the BVH stack is in shared memory.
 // COMP: the pack epilogue also writes the fused stereo composition (a separate instantiation, so
 // the default kernel carries none of its registers)
-template <bool COUNT, int ACC, bool COMP = false>
+template <bool COUNT, int ACC, bool COMP = false, bool TRI = false>
 __global__ void __launch_bounds__(RT_BLOCK, RT_MINB) k_trace_stereo(const TraceParams P) {
     __shared__ int s_stack[RT_SMEM_STACK * RT_BLOCK];   // [entry][thread]
     Counters<COUNT> cnt;
@@ -235,7 +235,7 @@ __global__ void __launch_bounds__(RT_BLOCK, RT_MINB) k_trace_stereo(const TraceP
             const float sy = fmaf(-2.0f * (py + 0.5f), 1.0f / P.H, 1.0f) * P.cam.th;
             const float3 d = normalize(P.cam.f + P.cam.r * (sx + P.cam.sigma[eye]) + P.cam.u * sy);
             int pid = -1;
-            const float3 c = trace_pixel<COUNT, ACC>(P, P.cam.eye[eye], d, pid, stk, cnt, s_occ + threadIdx.x);
+            const float3 c = trace_pixel<COUNT, ACC, TRI>(P, P.cam.eye[eye], d, pid, stk, cnt, s_occ + threadIdx.x);
             const long long pix = ((long long)eye * P.H + py) * P.W + px;
             if (P.prim_id) P.prim_id[pix] = pid;
             if (P.radiance) P.radiance[pix] = make_float4(c.x, c.y, c.z, 0.0f);
@@ -339,7 +339,9 @@ __global__ void __launch_bounds__(256) k_ffma_peak(float* out, int iters, float 
 using namespace rtb;
 
 static const void* trace_fn(unsigned flags) {
-    if (flags & RTB_TRACE_COMPOSE) return (const void*)k_trace_stereo<false, ACC_BVH, true>;
+    const bool tri = flags & RTB_TRACE_TRI;
+    if (flags & RTB_TRACE_COMPOSE)
+        return tri ? (const void*)k_trace_stereo<false, ACC_BVH, true, true> : (const void*)k_trace_stereo<false, ACC_BVH, true>;
     const bool count = flags & RT_RENDER_COUNT;
     const int acc = (flags & RT_RENDER_BRUTE_FORCE) ? ACC_BRUTE : (flags & RT_RENDER_KDTREE) ? ACC_KD : ACC_BVH;
     if (count)
@@ -348,6 +350,7 @@ static const void* trace_fn(unsigned flags) {
                                 : (const void*)k_trace_stereo<true, ACC_BVH>;
     return acc == ACC_BRUTE ? (const void*)k_trace_stereo<false, ACC_BRUTE>
          : acc == ACC_KD    ? (const void*)k_trace_stereo<false, ACC_KD>
+         : tri              ? (const void*)k_trace_stereo<false, ACC_BVH, false, true>
                             : (const void*)k_trace_stereo<false, ACC_BVH>;
 }
 

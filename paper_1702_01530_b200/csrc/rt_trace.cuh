@@ -136,7 +136,9 @@ __device__ __forceinline__ void store_px(void* base, int fmt, long long pitch, i
 }
 
 // Primitive test shared by the BVH leaves and the brute-force path (bit-identical results).
-template <bool COUNT>
+// TRI: the scene holds triangles only (no spheres, no planes): the launch picks this
+// instantiation so the sphere and plane code, never taken there, costs no registers (C4 -2.6 %).
+template <bool COUNT, bool TRI = false>
 __device__ __forceinline__ bool prim_t(const DevScene& S, int k, float3 o, float3 d, float& t, int& gid,
                                        Counters<COUNT>& cnt) {
     // all three 16-byte records up front, before the type test: both kinds read records 0 and 2
@@ -146,7 +148,7 @@ __device__ __forceinline__ bool prim_t(const DevScene& S, int k, float3 o, float
     const float4 b = __ldg(&S.prims[3 * k + 1]);
     const float4 c = __ldg(&S.prims[3 * k + 2]);
     gid = __float_as_int(a.w);
-    if (gid < S.n_spheres) {
+    if (!TRI && gid < S.n_spheres) {
         cnt.add(CNT_SPHERE_TESTS);
         return sphere_intersect(o, d, a, c.x, T_MIN, t);
     }
@@ -372,14 +374,14 @@ __device__ __forceinline__ bool kd_trace(const DevScene& S, float3 o, float3 d, 
 // Nearest hit over the 4-wide BVH (or every BVH primitive when BRUTE, the kd-tree when KD) and
 // the planes.  Acceptance: t > t_min and (t, gid) lexicographically smallest (
 // reading 9).  Children are visited near-to-far (order_push).
-template <bool COUNT, int ACC>
+template <bool COUNT, int ACC, bool TRI = false>
 __device__ __forceinline__ Hit closest_hit(const DevScene& S, float3 o, float3 d, const TravStack& stk, Counters<COUNT>& cnt) {
     constexpr bool BRUTE = ACC == ACC_BRUTE;
     Hit h;
     h.t = __int_as_float(0x7f800000);
     h.gid = -1;
     h.slot = 0;
-    for (int i = 0; i < S.n_planes; ++i) {
+    for (int i = 0; i < (TRI ? 0 : S.n_planes); ++i) {
         cnt.add(CNT_PLANE_TESTS);
         float t;
         if (plane_intersect(o, d, __ldg(&S.planes[i]), t) && t > T_MIN) {
@@ -396,7 +398,7 @@ __device__ __forceinline__ Hit closest_hit(const DevScene& S, float3 o, float3 d
         for (int k = first; k <= last; ++k) {
             float t;
             int gid;
-            if (prim_t<COUNT>(S, k, o, d, t, gid, cnt) && (t < h.t || (t == h.t && gid < h.gid))) {
+            if (prim_t<COUNT, TRI>(S, k, o, d, t, gid, cnt) && (t < h.t || (t == h.t && gid < h.gid))) {
                 h.t = t; h.gid = gid; h.slot = k;
             }
         }
@@ -432,11 +434,11 @@ __device__ __forceinline__ Hit closest_hit(const DevScene& S, float3 o, float3 d
 // that is a sphere.  A sphere covers many neighbouring pixels' shadow rays (C3: 1.1 M of the
 // frame's shadow rays end at the hint), a triangle of a fine mesh almost none (C4: 329 of 0.79 M
 // occluded rays), so triangle hints only cost a primitive test per shadow ray (C4 -0.5 %).
-template <bool COUNT, int ACC>
+template <bool COUNT, int ACC, bool TRI = false>
 __device__ __forceinline__ bool occluded(const DevScene& S, float3 o, float3 d, float dist, const TravStack& stk, Counters<COUNT>& cnt,
                                          int* hint = nullptr) {
     constexpr bool BRUTE = ACC == ACC_BRUTE;
-    for (int i = 0; i < S.n_planes; ++i) {
+    for (int i = 0; i < (TRI ? 0 : S.n_planes); ++i) {
         cnt.add(CNT_PLANE_TESTS);
         float t;
         if (plane_intersect(o, d, __ldg(&S.planes[i]), t) && t > T_MIN && t < dist) return true;
@@ -447,7 +449,7 @@ __device__ __forceinline__ bool occluded(const DevScene& S, float3 o, float3 d, 
         const int k = *hint;
         float t;
         int gid;
-        if (k >= 0 && prim_t<COUNT>(S, k, o, d, t, gid, cnt) && t < dist) return true;
+        if (k >= 0 && prim_t<COUNT, TRI>(S, k, o, d, t, gid, cnt) && t < dist) return true;
     }
     if constexpr (ACC == ACC_KD) {
         Hit h;
@@ -458,7 +460,7 @@ __device__ __forceinline__ bool occluded(const DevScene& S, float3 o, float3 d, 
         for (int k = first; k <= last; ++k) {
             float t;
             int gid;
-            if (prim_t<COUNT>(S, k, o, d, t, gid, cnt) && t < dist) {
+            if (prim_t<COUNT, TRI>(S, k, o, d, t, gid, cnt) && t < dist) {
                 if (hint && gid < S.n_spheres) *hint = k;   // spheres only (see occluded)
                 return true;
             }
