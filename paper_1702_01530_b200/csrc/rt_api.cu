@@ -128,6 +128,7 @@ rt_status rt_create(int device, void* cuda_stream, rt_context** out) {
     if (const char* gl = getenv("RT_GRID_LIMIT")) c->grid_limit = std::max(0, atoi(gl));
     if (const char* cd = getenv("RT_COLLAPSE_DP")) c->collapse_dp = atoi(cd) != 0;
     if (const char* cp = getenv("RT_COLLAPSE_CPRIM")) c->collapse_cprim = (float)std::max(0.01, atof(cp));
+    if (const char* sm = getenv("RT_SPEC_MASK")) c->spec_mask = atoi(sm) & 3;
     cudaError_t e = cudaSetDevice(device);
     if (e == cudaSuccess && cuda_stream) {
         c->stream = static_cast<cudaStream_t>(cuda_stream);
@@ -437,6 +438,8 @@ rt_status rt_scene_upload(rt_context* c, const rt_primitives* P, const rt_materi
     D.n_spheres = (int)S;
     D.n_planes = (int)PL;
     D.n_lights = (int)n_lights;
+    D.refractive = 0;
+    for (uint32_t i = 0; i < n_mats; ++i) D.refractive |= mats[i].kt > 0.0f;
     D.bound = (float)(bound * (1.0 + 1e-6));
     D.ambient = make_float3(env->ambient[0], env->ambient[1], env->ambient[2]);
     D.background = make_float3(env->background[0], env->background[1], env->background[2]);
@@ -753,8 +756,11 @@ rt_status rtb_render_local(rt_context* c, const rt_render_params* p, const rt_ou
     CUDA_TRY(cudaSetDevice(c->device));
     int occ = 0;
     unsigned kflags = P.comp ? RTB_TRACE_COMPOSE : (p->flags & (RT_RENDER_COUNT | RT_RENDER_BRUTE_FORCE | RT_RENDER_KDTREE));
-    if (P.sc.n_spheres == 0 && P.sc.n_planes == 0 && !(kflags & (RT_RENDER_COUNT | RT_RENDER_BRUTE_FORCE | RT_RENDER_KDTREE)))
-        kflags |= RTB_TRACE_TRI;                  // triangles-only scene: the instantiation without sphere/plane code
+    if (!(kflags & (RT_RENDER_COUNT | RT_RENDER_BRUTE_FORCE | RT_RENDER_KDTREE))) {
+        // product launches: the instantiation without the code this scene can never take
+        if ((c->spec_mask & 1) && P.sc.n_spheres == 0 && P.sc.n_planes == 0) kflags |= RTB_TRACE_TRI;
+        if ((c->spec_mask & 2) && !P.sc.refractive) kflags |= RTB_TRACE_OPAQUE;
+    }
     CUDA_TRY(rtb_trace_occupancy(kflags, P.stack_entries, &occ));
     if (occ < 1) occ = 1;
     const int block = rtb_trace_block();

@@ -87,6 +87,7 @@ struct DevScene {
     int n_spheres;
     int n_planes;
     int n_lights;
+    int refractive;     // some material has kt > 0 (else the launch may pick the opaque instantiation)
     float bound;        // max |x|+|y|+|z| over the BVH bounds (box-test margin scale)
     float3 ambient;
     float3 background;

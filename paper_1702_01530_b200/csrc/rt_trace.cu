@@ -27,12 +27,17 @@ constexpr int RT_MINB = RT_MINB_X;
 // registers, the refraction child is pushed on a per-thread stack (<= max_depth entries).
 // Radiance accumulates as sum over tree nodes of path_weight * local_term, which equals the
 // recursive definition c = local + kt*T(refr) + kr_eff*T(refl) (reading 17).
-template <bool COUNT, int ACC, bool TRI = false>
+// SPEC (product launches, chosen from the uploaded scene): SPEC_TRI = triangles only (no sphere,
+// plane or occluder-hint code), SPEC_OPAQUE = no material refracts (no refraction branch and no
+// per-thread refraction stack).  Each removes code the scene can never take, and with it registers.
+enum { SPEC_TRI = 1, SPEC_OPAQUE = 2 };
+template <bool COUNT, int ACC, int SPEC = 0>
 __device__ __forceinline__ float3 trace_pixel(const TraceParams& P, float3 o, float3 d, int& prim_id, const TravStack& stk,
                                               Counters<COUNT>& cnt, int* occ_hint) {
     constexpr bool BRUTE = ACC == ACC_BRUTE;
+    constexpr bool TRI = SPEC & SPEC_TRI, OPQ = SPEC & SPEC_OPAQUE;
     const DevScene& S = P.sc;
-    float4 st_a[MAX_DEPTH], st_b[MAX_DEPTH];   // refraction children: (o, w) (d, depth)
+    float4 st_a[OPQ ? 1 : MAX_DEPTH], st_b[OPQ ? 1 : MAX_DEPTH];   // refraction children: (o, w) (d, depth)
     int sp = 0;
     float w = 1.0f;
     int depth = P.max_depth;
@@ -83,7 +88,7 @@ __device__ __forceinline__ float3 trace_pixel(const TraceParams& P, float3 o, fl
                 const float3 sv = Lp - os;
                 const float dist = sqrt_dist(dot(sv, sv));
                 cnt.add(CNT_SHADOW);
-                int* hint = j < RT_OCC_LIGHTS ? occ_hint + j * RT_BLOCK : nullptr;
+                int* hint = (!TRI && j < RT_OCC_LIGHTS) ? occ_hint + j * RT_BLOCK : nullptr;   // hints hold spheres
                 if (!occluded<COUNT, ACC, TRI>(S, os, sv * rcp_dist(dist), dist, stk, cnt, hint)) c = c + term;   // reading 3
             }
             col = fma3(c, w, col);
@@ -91,7 +96,7 @@ __device__ __forceinline__ float3 trace_pixel(const TraceParams& P, float3 o, fl
                 const float4 m2 = __ldg(&S.mats[3 * mat + 2]);
                 float kr_eff = __ldg(&S.mats[3 * mat + 1]).w;
                 const float kt = m2.x;
-                if (kt > 0.0f) {
+                if (!OPQ && kt > 0.0f) {
                     const float eta = front ? rcp_dist(m2.y) : m2.y;
                     const float cosi = -dot(d, nf);
                     const float kk = 1.0f - eta * eta * (1.0f - cosi * cosi);
@@ -117,7 +122,7 @@ __device__ __forceinline__ float3 trace_pixel(const TraceParams& P, float3 o, fl
             }
         }
         if (cont) continue;
-        if (sp == 0) break;
+        if (OPQ || sp == 0) break;
         --sp;
         const float4 a = st_a[sp], b = st_b[sp];
         o = xyz(a);
@@ -208,7 +213,7 @@ __device__ __forceinline__ void pack_epilogue(const TraceParams& P, bool valid, 
 // atomic and traces one pixel tree per lane; the BVH stack is in shared memory.
 // COMP: the pack epilogue also writes the fused stereo composition (a separate instantiation, so
 // the default kernel carries none of its registers)
-template <bool COUNT, int ACC, bool COMP = false, bool TRI = false>
+template <bool COUNT, int ACC, bool COMP = false, int SPEC = 0>
 __global__ void __launch_bounds__(RT_BLOCK, RT_MINB) k_trace_stereo(const TraceParams P) {
     __shared__ int s_stack[RT_SMEM_STACK * RT_BLOCK];   // [entry][thread]
     Counters<COUNT> cnt;
@@ -235,7 +240,7 @@ __global__ void __launch_bounds__(RT_BLOCK, RT_MINB) k_trace_stereo(const TraceP
             const float sy = fmaf(-2.0f * (py + 0.5f), 1.0f / P.H, 1.0f) * P.cam.th;
             const float3 d = normalize(P.cam.f + P.cam.r * (sx + P.cam.sigma[eye]) + P.cam.u * sy);
             int pid = -1;
-            const float3 c = trace_pixel<COUNT, ACC, TRI>(P, P.cam.eye[eye], d, pid, stk, cnt, s_occ + threadIdx.x);
+            const float3 c = trace_pixel<COUNT, ACC, SPEC>(P, P.cam.eye[eye], d, pid, stk, cnt, s_occ + threadIdx.x);
             const long long pix = ((long long)eye * P.H + py) * P.W + px;
             if (P.prim_id) P.prim_id[pix] = pid;
             if (P.radiance) P.radiance[pix] = make_float4(c.x, c.y, c.z, 0.0f);
@@ -338,10 +343,19 @@ __global__ void __launch_bounds__(256) k_ffma_peak(float* out, int iters, float 
 // ------------------------------------------------------------------ launchers
 using namespace rtb;
 
+template <bool COMP>
+static const void* product_fn(int spec) {
+    switch (spec) {
+        case SPEC_TRI: return (const void*)k_trace_stereo<false, ACC_BVH, COMP, SPEC_TRI>;
+        case SPEC_OPAQUE: return (const void*)k_trace_stereo<false, ACC_BVH, COMP, SPEC_OPAQUE>;
+        case SPEC_TRI | SPEC_OPAQUE: return (const void*)k_trace_stereo<false, ACC_BVH, COMP, SPEC_TRI | SPEC_OPAQUE>;
+        default: return (const void*)k_trace_stereo<false, ACC_BVH, COMP>;
+    }
+}
+
 static const void* trace_fn(unsigned flags) {
-    const bool tri = flags & RTB_TRACE_TRI;
-    if (flags & RTB_TRACE_COMPOSE)
-        return tri ? (const void*)k_trace_stereo<false, ACC_BVH, true, true> : (const void*)k_trace_stereo<false, ACC_BVH, true>;
+    const int spec = ((flags & RTB_TRACE_TRI) ? SPEC_TRI : 0) | ((flags & RTB_TRACE_OPAQUE) ? SPEC_OPAQUE : 0);
+    if (flags & RTB_TRACE_COMPOSE) return product_fn<true>(spec);
     const bool count = flags & RT_RENDER_COUNT;
     const int acc = (flags & RT_RENDER_BRUTE_FORCE) ? ACC_BRUTE : (flags & RT_RENDER_KDTREE) ? ACC_KD : ACC_BVH;
     if (count)
@@ -350,8 +364,7 @@ static const void* trace_fn(unsigned flags) {
                                 : (const void*)k_trace_stereo<true, ACC_BVH>;
     return acc == ACC_BRUTE ? (const void*)k_trace_stereo<false, ACC_BRUTE>
          : acc == ACC_KD    ? (const void*)k_trace_stereo<false, ACC_KD>
-         : tri              ? (const void*)k_trace_stereo<false, ACC_BVH, false, true>
-                            : (const void*)k_trace_stereo<false, ACC_BVH>;
+                            : product_fn<false>(spec);
 }
 
 int rtb_trace_block() { return RT_BLOCK; }
