@@ -128,7 +128,7 @@ rt_status rt_create(int device, void* cuda_stream, rt_context** out) {
     if (const char* gl = getenv("RT_GRID_LIMIT")) c->grid_limit = std::max(0, atoi(gl));
     if (const char* cd = getenv("RT_COLLAPSE_DP")) c->collapse_dp = atoi(cd) != 0;
     if (const char* cp = getenv("RT_COLLAPSE_CPRIM")) c->collapse_cprim = (float)std::max(0.01, atof(cp));
-    if (const char* sm = getenv("RT_SPEC_MASK")) c->spec_mask = atoi(sm) & 3;
+    if (const char* sm = getenv("RT_SPEC_MASK")) c->spec_mask = atoi(sm) & 7;
     cudaError_t e = cudaSetDevice(device);
     if (e == cudaSuccess && cuda_stream) {
         c->stream = static_cast<cudaStream_t>(cuda_stream);
@@ -455,6 +455,7 @@ rt_status rt_scene_upload(rt_context* c, const rt_primitives* P, const rt_materi
     c->info[7] = (uint64_t)std::chrono::duration_cast<std::chrono::microseconds>(t1 - t0).count();
     // kept for rt_scene_update_vertices (NEXT-3 refit)
     c->d_prim_orig = d_prim_orig;
+    c->scene_leaf_max = c->leaf_max;                 // the leaf bound this scene's BVH was built with
     c->d_vertices = d_vertices;
     c->d_tri = d_tri;
     c->d_spheres = d_spheres;
@@ -760,6 +761,7 @@ rt_status rtb_render_local(rt_context* c, const rt_render_params* p, const rt_ou
         // product launches: the instantiation without the code this scene can never take
         if ((c->spec_mask & 1) && P.sc.n_spheres == 0 && P.sc.n_planes == 0) kflags |= RTB_TRACE_TRI;
         if ((c->spec_mask & 2) && !P.sc.refractive) kflags |= RTB_TRACE_OPAQUE;
+        if ((c->spec_mask & 4) && c->scene_leaf_max == 1) kflags |= RTB_TRACE_LEAF1;
     }
     CUDA_TRY(rtb_trace_occupancy(kflags, P.stack_entries, &occ));
     if (occ < 1) occ = 1;

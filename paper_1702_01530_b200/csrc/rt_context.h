@@ -85,7 +85,8 @@ struct rt_context {
     bool has_camera = false;
     double cam_eye[2][3], cam_f[3], cam_r[3], cam_u[3], cam_th, cam_sigma_unit;
     float vfov = 0;
-    int spec_mask = 3;               // scene-specialised trace instantiations allowed (bit 0 TRI, 1 OPAQUE; env RT_SPEC_MASK, A/B only)
+    int spec_mask = 7;               // scene-specialised trace instantiations allowed (bit 0 TRI, 1 OPAQUE, 2 LEAF1; env RT_SPEC_MASK, A/B only)
+    int scene_leaf_max = 1;          // leaf_max of the uploaded scene's BVH (LEAF1 needs 1)
     int leaf_max = 1;                // LBVH leaf collapse threshold (env RT_LEAF_MAX, <= 16)
     int treelet_passes = 0;          // SAH treelet restructuring passes (env RT_TREELETS; 0 after a full
                                      // SAH build: measured neutral to slightly worse, DESIGN §5 r2)

@@ -119,6 +119,7 @@ void kd_build_host(const float4* prims, int n, int n_spheres, int max_leaf, int 
 constexpr unsigned RTB_TRACE_COMPOSE = 1u << 31;
 constexpr unsigned RTB_TRACE_TRI = 1u << 30;       // the scene holds triangles only (product instantiation)
 constexpr unsigned RTB_TRACE_OPAQUE = 1u << 29;    // no material refracts (product instantiation)
+constexpr unsigned RTB_TRACE_LEAF1 = 1u << 28;     // every BVH leaf holds one primitive (product instantiation)
 cudaError_t rtb_launch_trace(const TraceParams& P, unsigned flags, int grid, cudaStream_t st);
 cudaError_t rtb_trace_occupancy(unsigned flags, int stack_entries, int* blocks_per_sm);
 size_t rtb_trace_smem(int stack_entries);

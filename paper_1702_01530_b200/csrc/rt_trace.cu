@@ -30,12 +30,12 @@ constexpr int RT_MINB = RT_MINB_X;
 // SPEC (product launches, chosen from the uploaded scene): SPEC_TRI = triangles only (no sphere,
 // plane or occluder-hint code), SPEC_OPAQUE = no material refracts (no refraction branch and no
 // per-thread refraction stack).  Each removes code the scene can never take, and with it registers.
-enum { SPEC_TRI = 1, SPEC_OPAQUE = 2 };
+enum { SPEC_TRI = 1, SPEC_OPAQUE = 2, SPEC_LEAF1 = 4 };
 template <bool COUNT, int ACC, int SPEC = 0>
 __device__ __forceinline__ float3 trace_pixel(const TraceParams& P, float3 o, float3 d, int& prim_id, const TravStack& stk,
                                               Counters<COUNT>& cnt, int* occ_hint) {
     constexpr bool BRUTE = ACC == ACC_BRUTE;
-    constexpr bool TRI = SPEC & SPEC_TRI, OPQ = SPEC & SPEC_OPAQUE;
+    constexpr bool TRI = SPEC & SPEC_TRI, OPQ = SPEC & SPEC_OPAQUE, L1 = SPEC & SPEC_LEAF1;
     const DevScene& S = P.sc;
     float4 st_a[OPQ ? 1 : MAX_DEPTH], st_b[OPQ ? 1 : MAX_DEPTH];   // refraction children: (o, w) (d, depth)
     int sp = 0;
@@ -45,7 +45,7 @@ __device__ __forceinline__ float3 trace_pixel(const TraceParams& P, float3 o, fl
     float3 col = f3(0.f, 0.f, 0.f);
     cnt.add(CNT_PRIMARY);
     while (true) {
-        const Hit h = closest_hit<COUNT, ACC, TRI>(S, o, d, stk, cnt);
+        const Hit h = closest_hit<COUNT, ACC, TRI, L1>(S, o, d, stk, cnt);
         if (primary) { prim_id = h.gid; primary = false; }
         bool cont = false;
         if (h.gid < 0) {
@@ -89,7 +89,7 @@ __device__ __forceinline__ float3 trace_pixel(const TraceParams& P, float3 o, fl
                 const float dist = sqrt_dist(dot(sv, sv));
                 cnt.add(CNT_SHADOW);
                 int* hint = (!TRI && j < RT_OCC_LIGHTS) ? occ_hint + j * RT_BLOCK : nullptr;   // hints hold spheres
-                if (!occluded<COUNT, ACC, TRI>(S, os, sv * rcp_dist(dist), dist, stk, cnt, hint)) c = c + term;   // reading 3
+                if (!occluded<COUNT, ACC, TRI, L1>(S, os, sv * rcp_dist(dist), dist, stk, cnt, hint)) c = c + term;   // reading 3
             }
             col = fma3(c, w, col);
             if (depth > 0) {
@@ -343,18 +343,19 @@ __global__ void __launch_bounds__(256) k_ffma_peak(float* out, int iters, float 
 // ------------------------------------------------------------------ launchers
 using namespace rtb;
 
+template <bool COMP, int SPEC>
+static const void* spec_fn() { return (const void*)k_trace_stereo<false, ACC_BVH, COMP, SPEC>; }
+
 template <bool COMP>
 static const void* product_fn(int spec) {
-    switch (spec) {
-        case SPEC_TRI: return (const void*)k_trace_stereo<false, ACC_BVH, COMP, SPEC_TRI>;
-        case SPEC_OPAQUE: return (const void*)k_trace_stereo<false, ACC_BVH, COMP, SPEC_OPAQUE>;
-        case SPEC_TRI | SPEC_OPAQUE: return (const void*)k_trace_stereo<false, ACC_BVH, COMP, SPEC_TRI | SPEC_OPAQUE>;
-        default: return (const void*)k_trace_stereo<false, ACC_BVH, COMP>;
-    }
+    static const void* const table[8] = {spec_fn<COMP, 0>(), spec_fn<COMP, 1>(), spec_fn<COMP, 2>(), spec_fn<COMP, 3>(),
+                                         spec_fn<COMP, 4>(), spec_fn<COMP, 5>(), spec_fn<COMP, 6>(), spec_fn<COMP, 7>()};
+    return table[spec & 7];
 }
 
 static const void* trace_fn(unsigned flags) {
-    const int spec = ((flags & RTB_TRACE_TRI) ? SPEC_TRI : 0) | ((flags & RTB_TRACE_OPAQUE) ? SPEC_OPAQUE : 0);
+    const int spec = ((flags & RTB_TRACE_TRI) ? SPEC_TRI : 0) | ((flags & RTB_TRACE_OPAQUE) ? SPEC_OPAQUE : 0) |
+                     ((flags & RTB_TRACE_LEAF1) ? SPEC_LEAF1 : 0);
     if (flags & RTB_TRACE_COMPOSE) return product_fn<true>(spec);
     const bool count = flags & RT_RENDER_COUNT;
     const int acc = (flags & RT_RENDER_BRUTE_FORCE) ? ACC_BRUTE : (flags & RT_RENDER_KDTREE) ? ACC_KD : ACC_BVH;

@@ -374,7 +374,7 @@ __device__ __forceinline__ bool kd_trace(const DevScene& S, float3 o, float3 d, 
 // Nearest hit over the 4-wide BVH (or every BVH primitive when BRUTE, the kd-tree when KD) and
 // the planes.  Acceptance: t > t_min and (t, gid) lexicographically smallest (
 // reading 9).  Children are visited near-to-far (order_push).
-template <bool COUNT, int ACC, bool TRI = false>
+template <bool COUNT, int ACC, bool TRI = false, bool L1 = false>
 __device__ __forceinline__ Hit closest_hit(const DevScene& S, float3 o, float3 d, const TravStack& stk, Counters<COUNT>& cnt) {
     constexpr bool BRUTE = ACC == ACC_BRUTE;
     Hit h;
@@ -418,6 +418,8 @@ __device__ __forceinline__ Hit closest_hit(const DevScene& S, float3 o, float3 d
             const unsigned m = node4_hits(S.nodes, node, rb, h.t, tn, ch);
             count_boxes(cnt, ch);
             if (order_push(m, tn, ch, stk, sp, node)) continue;
+        } else if (L1) {
+            leaf_test(~node, ~node);                 // single-primitive leaves: the code is ~slot
         } else {
             const int enc = ~node;
             const int first = enc & ((1 << LEAF_SHIFT) - 1);
@@ -434,7 +436,7 @@ __device__ __forceinline__ Hit closest_hit(const DevScene& S, float3 o, float3 d
 // that is a sphere.  A sphere covers many neighbouring pixels' shadow rays (C3: 1.1 M of the
 // frame's shadow rays end at the hint), a triangle of a fine mesh almost none (C4: 329 of 0.79 M
 // occluded rays), so triangle hints only cost a primitive test per shadow ray (C4 -0.5 %).
-template <bool COUNT, int ACC, bool TRI = false>
+template <bool COUNT, int ACC, bool TRI = false, bool L1 = false>
 __device__ __forceinline__ bool occluded(const DevScene& S, float3 o, float3 d, float dist, const TravStack& stk, Counters<COUNT>& cnt,
                                          int* hint = nullptr) {
     constexpr bool BRUTE = ACC == ACC_BRUTE;
@@ -479,6 +481,8 @@ __device__ __forceinline__ bool occluded(const DevScene& S, float3 o, float3 d, 
             const unsigned m = node4_hits(S.nodes, node, rb, dist, tn, ch);
             count_boxes(cnt, ch);
             if (plain_push(m, ch, stk, sp, node)) continue;
+        } else if (L1) {
+            if (leaf_test(~node, ~node)) return true;   // single-primitive leaves: the code is ~slot
         } else {
             const int enc = ~node;
             const int first = enc & ((1 << LEAF_SHIFT) - 1);
