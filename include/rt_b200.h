@@ -347,6 +347,26 @@ rt_status rt_ipc_close(rt_context* ctx, void* dev_ptr);
 rt_status rt_compose(rt_context* ctx, rt_fb left, rt_fb right, uint32_t width, uint32_t height, uint32_t mode,
                      rt_fb out);
 
+/* ------------------------------------------------------------------ ray queries */
+/* The method's intersection step (§2 "intersection of the ray with the objects";
+ * SURVEY §8(a) a4; SPEC.md:180-188 nearest hit, :292-300 BVH traversal) on caller-given rays,
+ * with the same device code the renderer runs: for ray i (origin o[3i..3i+2], direction
+ * d[3i..3i+2], any length != 0 -- normalised on the device as the renderer's rays are):
+ *   RT_QUERY_NEAREST: out_t[i] = the smallest t > t_min (1e-4) over every primitive, ties to the
+ *     smallest global ID; out_id[i] = that ID, or -1 and +inf on a miss (tmax ignored);
+ *   RT_QUERY_ANY: out_id[i] = 1 if some primitive has t_min < t < tmax[i] (a shadow query), else
+ *     0; out_t[i] is left unwritten.
+ * | RT_QUERY_BRUTE_FORCE tests every primitive instead of traversing the BVH (the reference the
+ * BVH must equal bit for bit).  o, d, tmax (ANY only), out_t (NEAREST only), out_id: DEVICE
+ * arrays (float32 / int32); enqueued on `stream` (cudaStream_t, NULL = the context's stream),
+ * asynchronous.  Errors: RT_ERR_INVALID_ARG (NULL arrays, unknown flags), RT_ERR_NO_SCENE,
+ * RT_ERR_CUDA. */
+#define RT_QUERY_NEAREST 0u
+#define RT_QUERY_ANY 1u
+#define RT_QUERY_BRUTE_FORCE 2u
+rt_status rt_intersect(rt_context* ctx, const float* o, const float* d, const float* tmax, uint32_t n, uint32_t flags,
+                       float* out_t, int32_t* out_id, void* stream);
+
 /* ------------------------------------------------------------------ introspection */
 /* Scene statistics after upload: [0] n_spheres [1] n_planes [2] n_triangles [3] bvh prims
  * [4] BVH4 nodes [5] BVH4 depth (levels) [6] device bytes of scene+BVH [7] build time us. */

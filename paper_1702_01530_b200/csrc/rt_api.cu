@@ -1110,6 +1110,32 @@ rt_status rt_scene_info(rt_context* c, uint64_t info[8]) {
     return RT_OK;
 }
 
+rt_status rt_intersect(rt_context* c, const float* o, const float* d, const float* tmax, uint32_t n, uint32_t flags,
+                       float* out_t, int32_t* out_id, void* stream) {
+    if (!c) return rtb_fail(RT_ERR_INVALID_ARG, "rt_intersect: NULL context");
+    if (flags & ~(RT_QUERY_ANY | RT_QUERY_BRUTE_FORCE)) return rtb_fail(RT_ERR_INVALID_ARG, "rt_intersect: flags 0x%x", flags);
+    const bool any = flags & RT_QUERY_ANY;
+    if (n && (!o || !d || !out_id || (any && !tmax) || (!any && !out_t)))
+        return rtb_fail(RT_ERR_INVALID_ARG, "rt_intersect: NULL array");
+    if (!c->has_scene) return rtb_fail(RT_ERR_NO_SCENE, "rt_intersect: no scene");
+    if (n == 0) return RT_OK;
+    CUDA_TRY(cudaSetDevice(c->device));
+    QueryParams Q;
+    Q.sc = c->sc;
+    Q.o = o;
+    Q.d = d;
+    Q.tmax = tmax;
+    Q.out_t = out_t;
+    Q.out_id = out_id;
+    Q.n = n;
+    Q.any = any;
+    Q.brute = (flags & RT_QUERY_BRUTE_FORCE) != 0;
+    const int block = rtb_trace_block();
+    const int grid = (int)std::min<long long>((long long)c->num_sms * 16, ((long long)n + block - 1) / block);
+    CUDA_TRY(rtb_launch_query(Q, grid, stream ? static_cast<cudaStream_t>(stream) : c->stream));
+    return RT_OK;
+}
+
 rt_status rt_bvh_export(rt_context* c, float* nodes, uint32_t* n_nodes, int32_t* prim_gid, uint32_t* n_prims) {
     if (!c || !n_nodes || !n_prims) return rtb_fail(RT_ERR_INVALID_ARG, "rt_bvh_export: NULL argument");
     if (!c->has_scene) return rtb_fail(RT_ERR_NO_SCENE, "rt_bvh_export: no scene");

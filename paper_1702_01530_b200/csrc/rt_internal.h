@@ -124,6 +124,17 @@ cudaError_t rtb_launch_trace(const TraceParams& P, unsigned flags, int grid, cud
 cudaError_t rtb_trace_occupancy(unsigned flags, int stack_entries, int* blocks_per_sm);
 size_t rtb_trace_smem(int stack_entries);
 int rtb_trace_block();      // threads per trace CTA (RT_BLOCK)
+struct QueryParams {
+    rtb::DevScene sc;
+    const float* o;
+    const float* d;
+    const float* tmax;
+    float* out_t;
+    int* out_id;
+    unsigned n;
+    int any, brute;
+};
+cudaError_t rtb_launch_query(const QueryParams& Q, int grid, cudaStream_t st);
 cudaError_t rtb_launch_unpack(const void* gathered, const UnpackParams& U, cudaStream_t st);
 cudaError_t rtb_launch_ffma(float* out, int iters, int grid, cudaStream_t st);
 // B0 ceilings (rt_probe.cu)

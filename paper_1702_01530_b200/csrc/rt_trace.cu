@@ -266,6 +266,27 @@ __global__ void __launch_bounds__(RT_BLOCK, RT_MINB) k_trace_stereo(const TraceP
     }
 }
 
+// rt_intersect: the renderer's nearest-hit / any-hit queries (BVH or brute force) on caller rays,
+// one ray per thread (grid-stride), the same traversal stack layout as k_trace_stereo.
+template <int ACC>
+__global__ void __launch_bounds__(RT_BLOCK) k_query(const QueryParams Q) {
+    __shared__ int s_stack[RT_SMEM_STACK * RT_BLOCK];
+    int lstack[STACK_CAP > RT_SMEM_STACK ? STACK_CAP - RT_SMEM_STACK : 1];
+    const TravStack stk{TravStack::pin((uint32_t)__cvta_generic_to_shared(s_stack)), lstack};
+    Counters<false> cnt;
+    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < Q.n; i += gridDim.x * blockDim.x) {
+        const float3 o = f3(Q.o[3 * i], Q.o[3 * i + 1], Q.o[3 * i + 2]);
+        const float3 d = normalize(f3(Q.d[3 * i], Q.d[3 * i + 1], Q.d[3 * i + 2]));
+        if (Q.any) {
+            Q.out_id[i] = occluded<false, ACC>(Q.sc, o, d, Q.tmax[i], stk, cnt) ? 1 : 0;
+        } else {
+            const Hit h = closest_hit<false, ACC>(Q.sc, o, d, stk, cnt);
+            Q.out_t[i] = h.t;
+            Q.out_id[i] = h.gid;
+        }
+    }
+}
+
 // Root-side tile unpack for the gather path: shards (rank-major) -> row-major FBs.
 __global__ void k_unpack_shards(const void* __restrict__ gathered, UnpackParams U) {
     const long long n = (long long)U.world * U.tiles_per_rank * 256;
@@ -388,6 +409,12 @@ cudaError_t rtb_trace_occupancy(unsigned flags, int stack_entries, int* blocks_p
     cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, f, RT_BLOCK, smem);
+}
+
+cudaError_t rtb_launch_query(const QueryParams& Q, int grid, cudaStream_t st) {
+    if (Q.brute) k_query<ACC_BRUTE><<<grid, RT_BLOCK, 0, st>>>(Q);
+    else k_query<ACC_BVH><<<grid, RT_BLOCK, 0, st>>>(Q);
+    return cudaGetLastError();
 }
 
 cudaError_t rtb_launch_unpack(const void* gathered, const UnpackParams& U, cudaStream_t st) {

@@ -34,7 +34,7 @@ EXPORTED = ["rt_create", "rt_destroy", "rt_synchronize", "rt_last_error", "rt_ve
             "rt_unpack_shards", "rt_ipc_get_handle", "rt_ipc_open", "rt_ipc_close", "rt_scene_info", "rt_bvh_export",
             "rt_bench_ffma", "rt_compose", "rt_scene_update_vertices", "rt_bvh_width", "rt_kdtree_build",
             "rt_render_stereo_async", "rt_download_after", "rt_bench_ceilings", "rt_dist_unique_id", "rt_dist_init",
-            "rt_dist_finalize", "rt_dist_info", "rt_dist_host_selftest"]
+            "rt_dist_finalize", "rt_dist_info", "rt_dist_host_selftest", "rt_intersect"]
 
 
 class RtError(RuntimeError):
@@ -110,6 +110,7 @@ def lib():
             "rt_ipc_get_handle": [vp, vp, C.POINTER(u64)], "rt_ipc_open": [vp, vp, C.POINTER(vp)], "rt_ipc_close": [vp, vp],
             "rt_scene_info": [vp, vp],
             "rt_bvh_export": [vp, vp, C.POINTER(u32), vp, C.POINTER(u32)],
+            "rt_intersect": [vp, vp, vp, vp, u32, u32, vp, vp, vp],
             "rt_bench_ffma": [vp, u32, C.POINTER(C.c_double), C.POINTER(C.c_double)],
             "rt_compose": [vp, rt_fb, rt_fb, u32, u32, u32, rt_fb],
             "rt_scene_update_vertices": [vp, vp, u32],
@@ -334,6 +335,24 @@ def rt_bvh_export(ctx):
     gids = np.zeros(max(npr.value, 1), np.int32)
     _check(lib().rt_bvh_export(ctx, nodes.ctypes.data, C.byref(nn), gids.ctypes.data, C.byref(npr)))
     return nodes[:nn.value], gids[:npr.value]
+
+
+RT_QUERY_NEAREST, RT_QUERY_ANY, RT_QUERY_BRUTE_FORCE = 0, 1, 2
+
+
+def rt_intersect(ctx, o, d, tmax=None, any_hit=False, brute=False, stream=None):
+    """Ray queries through the renderer's traversal (rt_b200.h rt_intersect).  o, d: contiguous
+    float32 CUDA tensors (n, 3); tmax: (n,) float32 for any-hit queries.  Returns (t, id) CUDA
+    tensors for nearest-hit queries, the int32 occlusion flags for any-hit ones (not synchronised)."""
+    import torch
+    n = o.shape[0]
+    ids = torch.empty(n, dtype=torch.int32, device=o.device)
+    t = None if any_hit else torch.empty(n, dtype=torch.float32, device=o.device)
+    flags = (RT_QUERY_ANY if any_hit else RT_QUERY_NEAREST) | (RT_QUERY_BRUTE_FORCE if brute else 0)
+    st = (stream or torch.cuda.current_stream()).cuda_stream
+    _check(lib().rt_intersect(ctx, o.data_ptr(), d.data_ptr(), tmax.data_ptr() if tmax is not None else None, n, flags,
+                              t.data_ptr() if t is not None else None, ids.data_ptr(), st))
+    return ids if any_hit else (t, ids)
 
 
 def rt_kdtree_build(ctx, max_leaf=1, max_depth=0):
