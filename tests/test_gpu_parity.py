@@ -599,3 +599,40 @@ def test_download_many_outstanding(R):
     finally:
         for h in hosts:
             rt.rt_host_free(h)
+
+
+def _glass_polyhedra():
+    """paper_scene(6) with glass materials: a triangles-only scene that refracts."""
+    s = scenes.paper_scene(6).with_view(width=72, height=54, max_depth=4)
+    s.materials = s.materials.copy()
+    s.materials[:, 8] = 0.6          # kt
+    s.materials[:, 9] = 1.45         # ior
+    s.materials[:, 7] = 0.2          # kr
+    return s.finalize()
+
+
+def test_glass_triangle_mesh_parity(R):
+    """A refracting triangles-only scene (the SPEC_TRI instantiation with its refraction code)."""
+    full_parity(R, _glass_polyhedra(), "glass polyhedra")
+
+
+@pytest.mark.parametrize("leaf_max", ["1", "2"])
+def test_specialised_instantiations_match_general_kernel(R, monkeypatch, leaf_max):
+    """Product renders launch a scene-specialised k_trace_stereo (triangles only / opaque /
+    one-primitive leaves, DESIGN §5 r2f-r2g); each must render exactly what the general kernel
+    (RT_SPEC_MASK=0) renders: four scenes x two leaf bounds cover all eight instantiations."""
+    monkeypatch.setenv("RT_LEAF_MAX", leaf_max)
+    sc = [scenes.scene_c4().with_view(width=64, height=40), _glass_polyhedra(), scenes.scene_c1(),
+          scenes.scene_c3().with_view(width=64, height=40)]
+    Rs = rt.StereoRenderer(0)
+    monkeypatch.setenv("RT_SPEC_MASK", "0")
+    Rg = rt.StereoRenderer(0)
+    try:
+        for s in sc:
+            a, b = gpu_render(Rs, s), gpu_render(Rg, s)
+            np.testing.assert_array_equal(a["id"], b["id"])
+            np.testing.assert_array_equal(a["radiance"].view(np.uint32), b["radiance"].view(np.uint32))
+            np.testing.assert_array_equal(a["fb"], b["fb"])
+    finally:
+        Rs.close()
+        Rg.close()
