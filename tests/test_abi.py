@@ -63,6 +63,7 @@ def test_null_arguments_are_rejected_without_a_device():
     assert L.rt_ipc_close(None, None) == rt.RT_ERR_INVALID_ARG
     assert L.rt_scene_info(None, None) == rt.RT_ERR_INVALID_ARG
     assert L.rt_bench_ceilings(None, None) == rt.RT_ERR_INVALID_ARG
+    assert L.rt_intersect(None, None, None, None, 1, 0, None, None, None) == rt.RT_ERR_INVALID_ARG
     assert L.rt_dist_unique_id(None) == rt.RT_ERR_INVALID_ARG
     assert L.rt_dist_init(None, 0, 1, None, 0) == rt.RT_ERR_INVALID_ARG
     assert L.rt_dist_finalize(None) == rt.RT_ERR_INVALID_ARG
