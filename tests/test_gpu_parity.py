@@ -121,14 +121,15 @@ def test_c3_full_sampled(R):
 @pytest.mark.slow
 def test_c4_full_sampled(R):
     """The headline config (configs[3]: 1080p stereo, 1M triangles, depth 4) in bench's launch
-    configuration: 2048 seeded pixels per eye."""
-    sampled_parity(R, scenes.scene_c4(), 2048, 12, "C4 1080p sampled")
+    configuration: 4096 seeded pixels per eye."""
+    sampled_parity(R, scenes.scene_c4(), 4096, 12, "C4 1080p sampled")
 
 
 @pytest.mark.slow
 def test_c5_frames_sampled(R):
     """configs[4] (4K stereo, 1M triangles, depth 6, camera orbit): the first, middle and last
-    orbit frames, 512 seeded pixels per eye each."""
+    orbit frames, 512 seeded pixels per eye each (1 024 per eye in the committed r02 run,
+    `profiles/r02_parity_c4_4096_c5_1024.log`)."""
     for f in (0, 30, 59):
         sampled_parity(R, scenes.scene_c5(frame=f), 512, 13 + f, f"C5 4K frame {f} sampled")
 
