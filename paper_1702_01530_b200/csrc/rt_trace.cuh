@@ -214,6 +214,18 @@ __device__ __forceinline__ bool order_push(unsigned m, const float tn[4], const 
         node = pick4(ch, __ffs(m) - 1);
         return true;
     }
+    if (__popc(m) == 2) {                                   // two hits: one compare, no network
+        const int i0 = __ffs(m) - 1, i1 = 31 - __clz(m);
+        const float t0 = i0 == 0 ? tn[0] : (i0 == 1 ? tn[1] : tn[2]);
+        const float t1 = i1 == 3 ? tn[3] : (i1 == 2 ? tn[2] : tn[1]);
+        const bool sw = t1 < t0;                            // ties keep slot order (as the keyed network)
+        const int near = pick4(ch, (uint32_t)(sw ? i1 : i0)), far = pick4(ch, (uint32_t)(sw ? i0 : i1));
+        if (stk.two_fit(sp)) stk.st_if(true, sp, far);
+        else stk.set(sp, far);
+        sp += STK_E;
+        node = near;
+        return true;
+    }
     uint32_t k0 = (m & 1) ? ((__float_as_uint(tn[0]) & ~3u) | 0u) : 0xffffffffu;
     uint32_t k1 = (m & 2) ? ((__float_as_uint(tn[1]) & ~3u) | 1u) : 0xffffffffu;
     uint32_t k2 = (m & 4) ? ((__float_as_uint(tn[2]) & ~3u) | 2u) : 0xffffffffu;
