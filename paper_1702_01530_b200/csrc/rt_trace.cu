@@ -244,7 +244,7 @@ __global__ void __launch_bounds__(RT_BLOCK, RT_MINB) k_trace_stereo(const TraceP
             // only the work item k stays live across the pixel's ray tree; its pixel coordinates are
             // recomputed for the epilogue (pinned: ptxas would otherwise keep eye/px/py/lt live,
             // 4 registers the traversal loops spill around -- C4 -0.5 %, C3 -0.8 %)
-            k = TravStack::pin(k);
+            k = (int)pin_reg((uint32_t)k);
             const float3 c = trace_pixel<COUNT, ACC, SPEC>(P, o, d, pid, stk, cnt, s_occ + threadIdx.x);
             valid = map_work(P, k, eye, px, py, lt);
             const long long pix = ((long long)eye * P.H + py) * P.W + px;

@@ -28,14 +28,19 @@ constexpr int RT_OCC_LIGHTS = 4;  // lights with a last-occluder hint slot (ligh
 // S2R SR_CgaCtaId (+ SR_TID.X for a per-thread base, as in round 1), which put S2R latencies in
 // front of every push and refill load.
 constexpr uint32_t STK_E = RT_BLOCK * 4u;   // bytes per stack entry row
+
+// A value ptxas must keep (or spill) rather than rematerialise at every use: the result of a
+// volatile move cannot be recomputed.
+__device__ __forceinline__ uint32_t pin_reg(uint32_t a) {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %1;" : "=r"(r) : "r"(a));
+    return r;
+}
+
 struct TravStack {
     uint32_t base;   // shared-window byte address of the CTA's stack array (uniform)
     int* l;          // local part: logical entry i >= RT_SMEM_STACK at l[i - RT_SMEM_STACK]
-    __device__ __forceinline__ static uint32_t pin(uint32_t a) {
-        uint32_t r;
-        asm volatile("mov.u32 %0, %1;" : "=r"(r) : "r"(a));
-        return r;
-    }
+    __device__ __forceinline__ static uint32_t pin(uint32_t a) { return pin_reg(a); }
     __device__ __forceinline__ static uint32_t empty() { return 4u * threadIdx.x; }
     __device__ __forceinline__ static bool nonempty(uint32_t a) { return a >= STK_E; }
     // true when entries a and a + E both lie in the shared part
