@@ -26,7 +26,11 @@ K_FRAMES = int(os.environ.get("RT_K", "24"))        # frames per pipelined measu
 def main():
     names = sys.argv[1:] or ["C4"]
     R = rt.StereoRenderer(0)
-    flush = torch.empty(int(os.environ.get("RT_FLUSH_MIB", "256")) * 2**20 // 4, dtype=torch.float32, device="cuda")
+    # the bench's flush (bench.l2_flush_bytes: 1.25x L2, at least 160 MiB) unless RT_FLUSH_MIB overrides it
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from bench import l2_flush_bytes
+    fb_bytes = int(os.environ["RT_FLUSH_MIB"]) << 20 if "RT_FLUSH_MIB" in os.environ else l2_flush_bytes(torch.device("cuda", 0))
+    flush = torch.empty(fb_bytes // 4, dtype=torch.float32, device="cuda")
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     res = {}
     for name in names:
