@@ -639,7 +639,14 @@ rt_status tile_table(rt_context* c, const ShardGeom& g, uint32_t W, uint32_t H, 
     e.W = W; e.H = H; e.rank = rank; e.world = world; e.block = g.block;
     e.buf.bytes = h.size() * sizeof(int);
     CUDA_TRY(cudaMalloc(&e.buf.p, e.buf.bytes));
-    CUDA_TRY(cudaMemcpy(e.buf.p, h.data(), e.buf.bytes, cudaMemcpyHostToDevice));   // once per layout
+    // once per layout; a pageable cudaMemcpy may return before its DMA lands and is not ordered
+    // with the (non-blocking) render streams, so copy on the context stream and wait for it
+    cudaError_t ce = cudaMemcpyAsync(e.buf.p, h.data(), e.buf.bytes, cudaMemcpyHostToDevice, c->stream);
+    if (ce == cudaSuccess) ce = cudaStreamSynchronize(c->stream);
+    if (ce != cudaSuccess) {
+        cudaFree(e.buf.p);
+        return rtb_fail(RT_ERR_CUDA, "tile table upload: %s", cudaGetErrorString(ce));
+    }
     c->tile_tables.push_back(e);
     *out = static_cast<const int*>(e.buf.p);
     return RT_OK;

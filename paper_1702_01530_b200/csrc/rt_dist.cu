@@ -272,6 +272,10 @@ rt_status map_handle(DistState* D, const unsigned char* handle, void** ptr) {
             return RT_OK;
         }
     if (D->maps.size() >= 64) {                     // bounded cache: drop the oldest mapping
+        // frames in flight may still store through it: drain this rank's device work first
+        // (rare: only a caller cycling through more than 64 distinct framebuffer allocations)
+        const cudaError_t se = cudaDeviceSynchronize();
+        if (se != cudaSuccess) return rtb_fail(RT_ERR_CUDA, "draining before unmapping a framebuffer: %s", cudaGetErrorString(se));
         cudaIpcCloseMemHandle(D->maps.front().ptr);
         D->maps.erase(D->maps.begin());
     }
@@ -302,7 +306,16 @@ rt_status shm_attach(DistState* D, uint32_t transport, const unsigned char* flag
             fd = -1;
         }
     } else {
-        host_wait([&] { return (fd = shm_open(D->shm_name.c_str(), O_RDWR, 0600)) >= 0; }, D->timeout);
+        // open only once rank 0 has sized the block: between its shm_open and ftruncate the object
+        // is 0 bytes, and touching a mapping past the end of the object raises SIGBUS
+        host_wait([&] {
+            if ((fd = shm_open(D->shm_name.c_str(), O_RDWR, 0600)) < 0) return false;
+            struct stat sb;
+            if (fstat(fd, &sb) == 0 && sb.st_size >= (off_t)sizeof(ShmBlock)) return true;
+            close(fd);
+            fd = -1;
+            return false;
+        }, D->timeout);
     }
     if (fd < 0) return rtb_fail(RT_ERR_PEER, "rt_dist_init: shared memory %s unavailable", D->shm_name.c_str());
     void* m = mmap(nullptr, sizeof(ShmBlock), PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
