@@ -66,10 +66,20 @@ def test_gloo_world2_gather_unpack(W, H):
     assert q.get(timeout=10) is True
 
 
-def _selftest_worker(rank, world, job_id, frames, q):
+def _selftest_worker(rank, world, job_id, frames, q, delay=0.0):
+    import time
     sys.path.insert(0, ROOT)
     from paper_1702_01530_b200 import rt
+    time.sleep(delay)
     q.put((rank, rt.rt_dist_host_selftest(rank, world, job_id, frames)))
+
+
+def _shm_path(job_id):
+    """/dev/shm file of the job's rendezvous block: FNV-1a of the 128-byte id (rt_dist.cu)."""
+    h = 1469598103934665603
+    for b in bytes(job_id):
+        h = ((h ^ b) * 1099511628211) & 0xFFFFFFFFFFFFFFFF
+    return "/dev/shm/rtb200_%016x" % h
 
 
 @pytest.mark.parametrize("world", [2, 3])
@@ -98,6 +108,32 @@ def test_dist_host_protocol_multiprocess(world):
         assert e.value.status == rt.RT_ERR_PEER
     finally:
         del os.environ["RT_DIST_TIMEOUT_S"]
+
+
+@pytest.mark.skipif(not os.path.isdir("/dev/shm"), reason="needs POSIX shared memory in /dev/shm")
+def test_dist_peers_first_over_a_stale_empty_block():
+    """Peers that start before rank 0 find a 0-byte object under the job's name (a block rank 0
+    has created but not yet sized, here a stale one): they must wait until rank 0 has (re)created
+    and sized it instead of mapping it (a read past the end of the object is a SIGBUS)."""
+    sys.path.insert(0, ROOT)
+    from paper_1702_01530_b200 import rt
+    job = rt.rt_dist_unique_id()
+    path = _shm_path(job)
+    open(path, "wb").close()                        # 0 bytes, the state between shm_open and ftruncate
+    try:
+        ctx = mp.get_context("spawn")
+        q = ctx.Queue()
+        procs = [ctx.Process(target=_selftest_worker, args=(r, 3, job, 20, q, 0.0 if r else 2.0)) for r in range(3)]
+        for p in procs:
+            p.start()
+        for p in procs:
+            p.join(120)
+            assert p.exitcode == 0                  # -7 (SIGBUS) before the size check
+        sums = dict(q.get(timeout=10) for _ in range(3))
+        assert len(set(sums.values())) == 1, sums
+    finally:
+        if os.path.exists(path):
+            os.unlink(path)
 
 
 def test_reference_arm_under_torchrun():
