@@ -257,7 +257,6 @@ rt_status rt_scene_upload(rt_context* c, const rt_primitives* P, const rt_materi
                 hi[k] = std::max(a, std::max(b, cc));
                 e1[k] = b - a;
                 e2[k] = cc - a;
-                bound = std::max(bound, 0.0);
             }
             const double cx = e1[1] * e2[2] - e1[2] * e2[1], cy = e1[2] * e2[0] - e1[0] * e2[2],
                          cz = e1[0] * e2[1] - e1[1] * e2[0];
@@ -351,7 +350,6 @@ rt_status rt_scene_upload(rt_context* c, const rt_primitives* P, const rt_materi
         if (!measuring) *p = static_cast<char*>(c->arena) + off;
         return RT_OK;
     };
-    auto free_scratch = [&]() {};
     float4* d_prims = nullptr;
     float4* d_nodes = nullptr;
     const size_t Nn = N > 1 ? N - 1 : 0;
@@ -409,7 +407,6 @@ rt_status rt_scene_upload(rt_context* c, const rt_primitives* P, const rt_materi
         if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
         if (e == cudaSuccess && n_nodes4 > 0) {        // compact the BVH4 into an exact-size buffer
             if ((st = dalloc(c, rtb::NODE_F4 * (size_t)n_nodes4, &d_nodes))) {
-                free_scratch();
                 free_scene(c);
                 return st;
             }
@@ -417,7 +414,6 @@ rt_status rt_scene_upload(rt_context* c, const rt_primitives* P, const rt_materi
                                 c->stream);
         }
         if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);   // staging and build scratch free again
-        free_scratch();
         if (e != cudaSuccess) {
             free_scene(c);
             return rtb_fail(RT_ERR_CUDA, "LBVH build: %s", cudaGetErrorString(e));
