@@ -125,6 +125,7 @@ rt_status rt_create(int device, void* cuda_stream, rt_context** out) {
     if (const char* lm = getenv("RT_LEAF_MAX")) c->leaf_max = std::max(1, std::min(16, atoi(lm)));
     if (const char* tp = getenv("RT_TREELETS")) c->treelet_passes = std::max(0, std::min(8, atoi(tp)));
     if (const char* ss = getenv("RT_SAH_SUBTREES")) c->sah_subtrees = std::max(0, std::min(2, atoi(ss)));
+    if (const char* sb = getenv("RT_SAH_BIG")) c->sah_big = (int)std::max(2048L, std::min(2147483647L, atol(sb)));
     if (const char* gl = getenv("RT_GRID_LIMIT")) c->grid_limit = std::max(0, atoi(gl));
     if (const char* cd = getenv("RT_COLLAPSE_DP")) c->collapse_dp = atoi(cd) != 0;
     if (const char* cp = getenv("RT_COLLAPSE_CPRIM")) c->collapse_cprim = (float)std::max(0.01, atof(cp));
@@ -401,6 +402,7 @@ rt_status rt_scene_upload(rt_context* c, const rt_primitives* P, const rt_materi
         B.leaf_max = c->leaf_max;
         B.treelet_passes = c->treelet_passes;
         B.sah_subtrees = c->sah_subtrees;
+        B.sah_big = c->sah_big;
         B.collapse_dp = c->collapse_dp;
         B.collapse_cprim = c->collapse_cprim;
         cudaError_t e = rtb_build_bvh(B, c->stream, &root, &n_nodes4, &depth4, level_start.data());

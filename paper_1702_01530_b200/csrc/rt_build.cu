@@ -147,17 +147,28 @@ __global__ void __launch_bounds__(SORT_THREADS) k_radix_hist(const uint32_t* __r
     hist[threadIdx.x * nblocks + blockIdx.x] = h[threadIdx.x];
 }
 
-// Exclusive scan of `n` entries with one block of 1024 threads (n is ~256 * N/2048).
+// Exclusive scan of `n` entries with one block of 1024 threads (n is ~256 * N/2048), 8 consecutive
+// entries per thread a step (round 1: one entry per thread, 113 us for C4's 125 K entries).
 __global__ void __launch_bounds__(1024) k_scan_single(uint32_t* a, int n) {
+    constexpr int IPT = 8;                               // the vector path below assumes 8
     __shared__ uint32_t warp_sums[32];
     __shared__ uint32_t carry;
     if (threadIdx.x == 0) carry = 0;
     __syncthreads();
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    for (int base = 0; base < n; base += 1024) {
-        const int i = base + threadIdx.x;
-        const uint32_t v = i < n ? a[i] : 0u;
-        uint32_t x = v;
+    for (int base = 0; base < n; base += 1024 * IPT) {
+        const int i0 = base + threadIdx.x * IPT;
+        uint32_t v[IPT], t = 0;
+        if (i0 + IPT <= n && (reinterpret_cast<uintptr_t>(a) & 15u) == 0) {   // two 16-byte loads
+            const uint4 x0 = reinterpret_cast<const uint4*>(a + i0)[0], x1 = reinterpret_cast<const uint4*>(a + i0)[1];
+            v[0] = x0.x; v[1] = x0.y; v[2] = x0.z; v[3] = x0.w; v[4] = x1.x; v[5] = x1.y; v[6] = x1.z; v[7] = x1.w;
+        } else {
+#pragma unroll
+            for (int k = 0; k < IPT; ++k) v[k] = i0 + k < n ? a[i0 + k] : 0u;
+        }
+#pragma unroll
+        for (int k = 0; k < IPT; ++k) t += v[k];
+        uint32_t x = t;
 #pragma unroll
         for (int off = 1; off < 32; off <<= 1) {
             const uint32_t y = __shfl_up_sync(0xffffffffu, x, off);
@@ -175,10 +186,23 @@ __global__ void __launch_bounds__(1024) k_scan_single(uint32_t* a, int n) {
             warp_sums[lane] = s;
         }
         __syncthreads();
-        const uint32_t excl = x - v + (wid ? warp_sums[wid - 1] : 0u) + carry;
-        if (i < n) a[i] = excl;
+        uint32_t run = x - t + (wid ? warp_sums[wid - 1] : 0u) + carry;
+        uint32_t o[IPT];
+#pragma unroll
+        for (int k = 0; k < IPT; ++k) {
+            o[k] = run;
+            run += v[k];
+        }
+        if (i0 + IPT <= n && (reinterpret_cast<uintptr_t>(a) & 15u) == 0) {
+            reinterpret_cast<uint4*>(a + i0)[0] = make_uint4(o[0], o[1], o[2], o[3]);
+            reinterpret_cast<uint4*>(a + i0)[1] = make_uint4(o[4], o[5], o[6], o[7]);
+        } else {
+#pragma unroll
+            for (int k = 0; k < IPT; ++k)
+                if (i0 + k < n) a[i0 + k] = o[k];
+        }
         __syncthreads();
-        if (threadIdx.x == 1023) carry = excl + v;
+        if (threadIdx.x == 1023) carry = run;
         __syncthreads();
     }
 }
@@ -706,8 +730,29 @@ struct SahWarpBins {
     int cnt[3][SAH_BINS];
     unsigned int lo[3][3][SAH_BINS], hi[3][3][SAH_BINS];    // [axis][component][bin], ordered floats
 };
-constexpr int SAH_BIG = 1 << 16;             // tasks above this many items: one 1024-thread CTA each
-constexpr int SAH_BIG_THREADS = 1024;
+// Tasks of more than B.sah_big items (the top levels of a full SAH build) are split over many
+// CTAs: every task's item range is cut into SAH_CHUNK-item chunks, one CTA per chunk, and the
+// bounds, bins and left counts of a task are merged from its chunks with global atomics (min/max
+// on ordered floats and integer adds: exact and order independent, so the tree is the one a single
+// warp or CTA would build; tests/test_gpu_build.py).  Round 1 ran such a task on one 1024-thread
+// CTA: 11 ms for the C4 root alone.
+constexpr int SAH_CHUNK = 4096;              // items per CTA of a chunked task
+constexpr int SAH_CTHR = 512;                  // threads per chunk CTA
+constexpr int SAH_BIG_DEFAULT = 4096;        // tasks above this many items are chunked (env RT_SAH_BIG)
+
+struct SahTaskAcc {                          // one chunked task's merged state (global memory)
+    unsigned int v[12];                      // ordered floats: box lo/hi, centroid lo/hi
+    SahWarpBins bins;
+    int ax, bbin, nl, pad;
+};
+
+// per-level bookkeeping of the chunked tasks: task i's chunks are [cbase[i], cbase[i + 1]) in
+// allocation order (a packed 64-bit counter hands out the task slot and its chunk range together)
+struct SahChunked {
+    int4* tasks;                             // (begin, end, node, depth)
+    int* cbase;                              // first chunk of each task
+    int* ctask;                              // chunk -> task
+};
 
 __device__ __forceinline__ void sah_bins_clear(SahWarpBins& S, int lane) {
 #pragma unroll
@@ -805,9 +850,10 @@ __device__ __forceinline__ bool sah_goes_left(const BuildBuffers& B, int k, int 
 }
 
 // children of a split node (one thread): leaves get their slot codes, internal children their
-// Karras ids and a task in the next level's list (large ones in the CTA list)
+// Karras ids and a task in the next level's list (chunked ones with their chunk range)
 __device__ __forceinline__ void sah_children(const BuildBuffers& B, const int* idx, int begin, int end, int nl, int node,
-                                             int depth, int4* next, int* n_next, int4* next_big, int* n_next_big) {
+                                             int depth, int4* next, int* n_next, SahChunked nb,
+                                             unsigned long long* nb_ctr) {
     const int mid = begin + nl;
     int code[2];
     const int rb[2] = {begin, mid}, re[2] = {mid, end};
@@ -820,8 +866,16 @@ __device__ __forceinline__ void sah_children(const BuildBuffers& B, const int* i
             B.parent_int[code[h]] = node;
             B.range[code[h]] = make_int2(0, re[h] - rb[h] - 1);   // size only (leaf_max 1)
             const int4 t = make_int4(rb[h], re[h], code[h], depth + 1);
-            if (re[h] - rb[h] > SAH_BIG) next_big[atomicAdd(n_next_big, 1)] = t;
-            else next[atomicAdd(n_next, 1)] = t;
+            if (re[h] - rb[h] > B.sah_big) {
+                const int nch = (re[h] - rb[h] + SAH_CHUNK - 1) / SAH_CHUNK;
+                const unsigned long long r = atomicAdd(nb_ctr, (1ull << 32) | (unsigned long long)nch);
+                const int ti = (int)(r >> 32), c0 = (int)(r & 0xffffffffu);
+                nb.tasks[ti] = t;
+                nb.cbase[ti] = c0;
+                for (int j = 0; j < nch; ++j) nb.ctask[c0 + j] = ti;
+            } else {
+                next[atomicAdd(n_next, 1)] = t;
+            }
         }
     }
     B.left[node] = code[0];
@@ -864,10 +918,10 @@ __device__ __forceinline__ void sah_bounds_warp(float* v) {
     }
 }
 
-// One level, tasks of <= SAH_BIG items: task (begin, end, node, depth) per warp over idx[begin, end).
+// One level, tasks of <= B.sah_big items: task (begin, end, node, depth) per warp over idx[begin, end).
 __global__ void __launch_bounds__(32 * SAH_WARPS) k_sah_level(BuildBuffers B, const int4* __restrict__ tasks,
-                                                              int n_tasks, int4* next, int* n_next, int4* next_big,
-                                                              int* n_next_big, int* idx, int* tmp) {
+                                                              int n_tasks, int4* next, int* n_next, SahChunked nb,
+                                                              unsigned long long* nb_ctr, int* idx, int* tmp) {
     __shared__ SahWarpBins bins[SAH_WARPS];
     const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
     const int w = blockIdx.x * SAH_WARPS + wl;
@@ -909,93 +963,214 @@ __global__ void __launch_bounds__(32 * SAH_WARPS) k_sah_level(BuildBuffers B, co
     __syncwarp();
     for (int i = begin + lane; i < end; i += 32) idx[i] = tmp[i];
     __syncwarp();
-    if (lane == 0) sah_children(B, idx, begin, end, nl, node, depth, next, n_next, next_big, n_next_big);
+    if (lane == 0) sah_children(B, idx, begin, end, nl, node, depth, next, n_next, nb, nb_ctr);
 }
 
-// One level, tasks of > SAH_BIG items (the top of a full SAH build): one 1024-thread CTA per task,
-// per-warp bins merged in shared memory, a CTA-wide stable partition.
-__global__ void __launch_bounds__(SAH_BIG_THREADS) k_sah_level_big(BuildBuffers B, const int4* __restrict__ tasks,
-                                                                   int4* next, int* n_next, int4* next_big,
-                                                                   int* n_next_big, int* idx, int* tmp) {
-    extern __shared__ SahWarpBins wb[];                  // [SAH_BIG_THREADS / 32] per-warp bins; [0] merged
-    __shared__ float red[SAH_BIG_THREADS / 32][12];
-    __shared__ int wcnt[SAH_BIG_THREADS / 32 + 1];
-    __shared__ int split[3];
-    const int tid = threadIdx.x, lane = tid & 31, wl = tid >> 5;
-    constexpr int NW = SAH_BIG_THREADS / 32;
-    const int4 t = tasks[blockIdx.x];
-    const int begin = t.x, end = t.y, node = t.z, depth = t.w, cnt = end - begin;
-    const bool median = depth + ceil_log2(cnt) >= SAH_MAX_DEPTH;
+// ---- chunked tasks (> B.sah_big items): one level = init, bounds, bins, split, count, scatter,
+// copy back + children; every kernel but init / split runs one CTA per chunk
+__device__ __forceinline__ void chunk_range(const SahChunked& T, int chunk, int& task, int4& t, int& lo, int& hi) {
+    task = T.ctask[chunk];
+    t = T.tasks[task];
+    lo = t.x + (chunk - T.cbase[task]) * SAH_CHUNK;
+    hi = min(t.y, lo + SAH_CHUNK);
+}
+
+__device__ __forceinline__ bool chunk_median(const int4& t) { return t.w + ceil_log2(t.y - t.x) >= SAH_MAX_DEPTH; }
+
+__global__ void k_sah_chunk_init(SahTaskAcc* acc, int n_tasks) {
+    constexpr int WORDS = sizeof(SahTaskAcc) / 4;
+    unsigned int* a = reinterpret_cast<unsigned int*>(acc + blockIdx.x);
+    if (blockIdx.x >= n_tasks) return;
+    for (int e = threadIdx.x; e < WORDS; e += blockDim.x) {
+        unsigned int x = 0u;                                     // counts, maxima, split fields
+        if (e < 12) x = (e < 3 || (e >= 6 && e < 9)) ? 0xffffffffu : 0u;
+        else if (e >= 12 + 3 * SAH_BINS && e < 12 + 12 * SAH_BINS) x = 0xffffffffu;   // bin minima
+        a[e] = x;
+    }
+}
+
+// CTA-wide reduction of v[12] (min for box/centroid lo, max for hi) into acc[task].v
+__global__ void __launch_bounds__(SAH_CTHR) k_sah_chunk_bounds(BuildBuffers B, SahChunked T, SahTaskAcc* acc,
+                                                              const int* __restrict__ idx) {
+    __shared__ float red[SAH_CTHR / 32][12];
+    int task, lo, hi;
+    int4 t;
+    chunk_range(T, blockIdx.x, task, t, lo, hi);
     float v[12];
     sah_bounds_init(v);
-    for (int i = begin + tid; i < end; i += SAH_BIG_THREADS) sah_bounds_item(B, idx[i], v);
+    for (int i = lo + threadIdx.x; i < hi; i += SAH_CTHR) sah_bounds_item(B, idx[i], v);
     sah_bounds_warp(v);
+    const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
     if (lane == 0)
         for (int q = 0; q < 12; ++q) red[wl][q] = v[q];
-    sah_bins_clear(wb[wl], lane);
     __syncthreads();
-    if (tid < 12) {
-        const bool mx = (tid >= 3 && tid < 6) || tid >= 9;
-        float x = red[0][tid];
-        for (int w = 1; w < NW; ++w) x = mx ? fmaxf(x, red[w][tid]) : fminf(x, red[w][tid]);
-        red[0][tid] = x;
+    if (threadIdx.x < 12) {
+        const int q = threadIdx.x;
+        const bool mx = (q >= 3 && q < 6) || q >= 9;
+        float x = red[0][q];
+        for (int w = 1; w < SAH_CTHR / 32; ++w) x = mx ? fmaxf(x, red[w][q]) : fminf(x, red[w][q]);
+        if (mx) atomicMax(&acc[task].v[q], f2ord(x));
+        else atomicMin(&acc[task].v[q], f2ord(x));
     }
-    __syncthreads();
-    for (int q = 0; q < 12; ++q) v[q] = red[0][q];
-    if (tid == 0) {
-        B.node_lo[node] = make_float4(v[0], v[1], v[2], 0.f);
-        B.node_hi[node] = make_float4(v[3], v[4], v[5], 0.f);
-    }
-    float kq[3];
+}
+
+__device__ __forceinline__ void acc_bounds(const SahTaskAcc& A, float* v) {
+#pragma unroll
+    for (int q = 0; q < 12; ++q) v[q] = ord2f(A.v[q]);
+}
+
+// per-warp shared bins, merged per CTA, then into acc[task].bins with global atomics
+__global__ void __launch_bounds__(SAH_CTHR) k_sah_chunk_bin(BuildBuffers B, SahChunked T, SahTaskAcc* acc,
+                                                           const int* __restrict__ idx) {
+    extern __shared__ SahWarpBins cb[];                  // [SAH_CTHR / 32]
+    int task, lo, hi;
+    int4 t;
+    chunk_range(T, blockIdx.x, task, t, lo, hi);
+    if (t.y - t.x <= 2 || chunk_median(t)) return;
+    const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+    float v[12], kq[3];
+    acc_bounds(acc[task], v);
     sah_kq(v, kq);
-    if (!median) {
-        for (int i = begin + tid; i < end; i += SAH_BIG_THREADS) sah_bin_item(wb[wl], B, idx[i], v, kq);
-    }
+    sah_bins_clear(cb[wl], lane);
     __syncthreads();
-    // merge the per-warp bins into wb[0] (one thread per bin entry)
+    for (int i = lo + threadIdx.x; i < hi; i += SAH_CTHR) sah_bin_item(cb[wl], B, idx[i], v, kq);
+    __syncthreads();
     constexpr int ENTRIES = sizeof(SahWarpBins) / 4;
-    for (int e = tid; e < ENTRIES; e += SAH_BIG_THREADS) {
-        unsigned* base = reinterpret_cast<unsigned*>(wb);
-        unsigned x = base[e];
+    const unsigned* base = reinterpret_cast<const unsigned*>(cb);
+    unsigned* dst = reinterpret_cast<unsigned*>(&acc[task].bins);
+    for (int e = threadIdx.x; e < ENTRIES; e += SAH_CTHR) {
         const bool is_cnt = e < 3 * SAH_BINS, is_lo = !is_cnt && e < 3 * SAH_BINS + 9 * SAH_BINS;
-        for (int w = 1; w < NW; ++w) {
+        unsigned x = base[e];
+        for (int w = 1; w < SAH_CTHR / 32; ++w) {
             const unsigned y = base[w * ENTRIES + e];
             x = is_cnt ? x + y : (is_lo ? min(x, y) : max(x, y));
         }
-        base[e] = x;
+        if (is_cnt) { if (x) atomicAdd(&dst[e], x); }
+        else if (is_lo) { if (x != 0xffffffffu) atomicMin(&dst[e], x); }
+        else if (x) atomicMax(&dst[e], x);
     }
-    __syncthreads();
-    if (wl == 0) {
-        int ax = -1, nl = cnt / 2, bbin = 0;
-        if (!median) sah_split_search(wb[0], kq, lane, ax, bbin, nl);
-        if (lane == 0) { split[0] = ax; split[1] = bbin; split[2] = nl; }
+}
+
+// one warp per task: node box, then the split (the same search as a warp task)
+__global__ void k_sah_chunk_split(BuildBuffers B, SahChunked T, SahTaskAcc* acc, int n_tasks) {
+    __shared__ SahWarpBins S;
+    const int task = blockIdx.x, lane = threadIdx.x;
+    if (task >= n_tasks) return;
+    const int4 t = T.tasks[task];
+    const int cnt = t.y - t.x;
+    float v[12], kq[3];
+    acc_bounds(acc[task], v);
+    if (lane == 0) {
+        B.node_lo[t.z] = make_float4(v[0], v[1], v[2], 0.f);
+        B.node_hi[t.z] = make_float4(v[3], v[4], v[5], 0.f);
     }
+    sah_kq(v, kq);
+    int ax = -1, nl = cnt / 2, bbin = 0;
+    if (cnt > 2 && !chunk_median(t)) {
+        const unsigned* src = reinterpret_cast<const unsigned*>(&acc[task].bins);
+        unsigned* dst = reinterpret_cast<unsigned*>(&S);
+        for (int e = lane; e < (int)(sizeof(SahWarpBins) / 4); e += 32) dst[e] = src[e];
+        __syncwarp();
+        sah_split_search(S, kq, lane, ax, bbin, nl);
+    }
+    if (lane == 0) { acc[task].ax = ax; acc[task].bbin = bbin; acc[task].nl = nl; }
+}
+
+// left items of every chunk
+__global__ void __launch_bounds__(SAH_CTHR) k_sah_chunk_count(BuildBuffers B, SahChunked T, const SahTaskAcc* acc,
+                                                             const int* __restrict__ idx, int* cleft) {
+    __shared__ int wsum[SAH_CTHR / 32];
+    int task, lo, hi;
+    int4 t;
+    chunk_range(T, blockIdx.x, task, t, lo, hi);
+    const SahTaskAcc& A = acc[task];
+    float v[12], kq[3];
+    acc_bounds(A, v);
+    sah_kq(v, kq);
+    int c = 0;
+    for (int i = lo + threadIdx.x; i < hi; i += SAH_CTHR) c += sah_goes_left(B, idx[i], i, t.x, A.ax, A.bbin, A.nl, v, kq);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) c += __shfl_xor_sync(0xffffffffu, c, off);
+    if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = c;
     __syncthreads();
-    const int ax = split[0], bbin = split[1], nl = split[2];
-    int lbase = 0, rbase = 0;                            // CTA-wide stable partition, 1024 items a step
-    for (int c0 = begin; c0 < end; c0 += SAH_BIG_THREADS) {
-        const int i = c0 + tid;
-        const int k = i < end ? idx[i] : 0;
-        const bool left = i < end && sah_goes_left(B, k, i, begin, ax, bbin, nl, v, kq);
+    if (threadIdx.x == 0) {
+        int s2 = 0;
+        for (int w = 0; w < SAH_CTHR / 32; ++w) s2 += wsum[w];
+        cleft[blockIdx.x] = s2;
+    }
+}
+
+// stable partition of the chunk into tmp: left items after the left items of the task's earlier
+// chunks, right items after theirs
+__global__ void __launch_bounds__(SAH_CTHR) k_sah_chunk_scatter(BuildBuffers B, SahChunked T, const SahTaskAcc* acc,
+                                                               const int* __restrict__ idx, const int* __restrict__ cleft,
+                                                               int* tmp) {
+    __shared__ int wcnt[SAH_CTHR / 32 + 1];
+    __shared__ int lbase_s;
+    int task, lo, hi;
+    int4 t;
+    chunk_range(T, blockIdx.x, task, t, lo, hi);
+    const SahTaskAcc& A = acc[task];
+    const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+    if (wl == 0) {                                        // left items in this task's earlier chunks
+        int s2 = 0;
+        for (int c = T.cbase[task] + lane; c < (int)blockIdx.x; c += 32) s2 += cleft[c];
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, off);
+        if (lane == 0) lbase_s = s2;
+    }
+    float v[12], kq[3];
+    acc_bounds(A, v);
+    sah_kq(v, kq);
+    __syncthreads();
+    int lbase = lbase_s, rbase = (lo - t.x) - lbase_s;
+    for (int c0 = lo; c0 < hi; c0 += SAH_CTHR) {
+        const int i = c0 + threadIdx.x;
+        const int k = i < hi ? idx[i] : 0;
+        const bool left = i < hi && sah_goes_left(B, k, i, t.x, A.ax, A.bbin, A.nl, v, kq);
         const unsigned bal = __ballot_sync(0xffffffffu, left);
         if (lane == 0) wcnt[wl] = __popc(bal);
         __syncthreads();
-        if (tid == 0) {
-            int acc = 0;
-            for (int w = 0; w < NW; ++w) { const int x = wcnt[w]; wcnt[w] = acc; acc += x; }
-            wcnt[NW] = acc;
+        if (threadIdx.x == 0) {
+            int acc2 = 0;
+            for (int w = 0; w < SAH_CTHR / 32; ++w) { const int x = wcnt[w]; wcnt[w] = acc2; acc2 += x; }
+            wcnt[SAH_CTHR / 32] = acc2;
         }
         __syncthreads();
         const int lrank = wcnt[wl] + __popc(bal & ((1u << lane) - 1u));
-        const int chunk_l = wcnt[NW];
-        if (i < end) tmp[left ? begin + lbase + lrank : begin + nl + rbase + (i - c0 - lrank)] = k;
+        const int chunk_l = wcnt[SAH_CTHR / 32];
+        if (i < hi) tmp[left ? t.x + lbase + lrank : t.x + A.nl + rbase + (i - c0 - lrank)] = k;
         lbase += chunk_l;
-        rbase += min(SAH_BIG_THREADS, end - c0) - chunk_l;
+        rbase += min(SAH_CTHR, hi - c0) - chunk_l;
         __syncthreads();
     }
-    for (int i = begin + tid; i < end; i += SAH_BIG_THREADS) idx[i] = tmp[i];
-    __syncthreads();
-    if (tid == 0) sah_children(B, idx, begin, end, nl, node, depth, next, n_next, next_big, n_next_big);
+}
+
+// partitioned order back into idx; the task's first chunk emits its children (reading tmp, which
+// holds the same order)
+__global__ void __launch_bounds__(SAH_CTHR) k_sah_chunk_finish(BuildBuffers B, SahChunked T, const SahTaskAcc* acc,
+                                                              int* idx, const int* __restrict__ tmp, int4* next,
+                                                              int* n_next, SahChunked nb, unsigned long long* nb_ctr) {
+    int task, lo, hi;
+    int4 t;
+    chunk_range(T, blockIdx.x, task, t, lo, hi);
+    for (int i = lo + threadIdx.x; i < hi; i += SAH_CTHR) idx[i] = tmp[i];
+    if (threadIdx.x == 0 && (int)blockIdx.x == T.cbase[task])
+        sah_children(B, tmp, t.x, t.y, acc[task].nl, t.z, t.w, next, n_next, nb, nb_ctr);
+}
+
+// the whole tree (Karras root 0, slots [0, n)) as one chunked task: identity item order, every
+// chunk mapped to task 0 (full SAH build of n > B.sah_big items)
+__global__ void k_sah_chunk_seed(SahChunked T, int* idx, int n, int depth0) {
+    const int nch = (n + SAH_CHUNK - 1) / SAH_CHUNK;
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+        idx[j] = j;
+        if (j < nch) T.ctask[j] = 0;
+        if (j == 0) {
+            T.tasks[0] = make_int4(0, n, 0, depth0);
+            T.cbase[0] = 0;
+        }
+    }
 }
 
 // leaf-order records and leaf AABBs (slot k = sorted position k)
@@ -1152,38 +1327,69 @@ cudaError_t rtb_build_bvh(const BuildBuffers& Bc, cudaStream_t st, int* root, in
         if (h_roots > 0) {
             int* idx = reinterpret_cast<int*>(B.keys[0]);
             int* tmp = reinterpret_cast<int*>(B.keys[1]);
-            // task lists: small (warp) and big (CTA) tasks of the current and the next level; the
-            // big lists are short (< n / SAH_BIG entries) and live past the small ones
+            // task lists: warp tasks of the current and the next level in frontier[1] / the BVH4
+            // staging (each >= N/2 int4, unused until k_wide); behind the latter the chunked
+            // tasks' lists, chunk maps and merged state (sized for n / sah_big tasks a level)
             int4* base4 = reinterpret_cast<int4*>(B.nodes4);
             int4* tl[2] = {reinterpret_cast<int4*>(B.frontier[1]), base4};
-            int4* tb[2] = {base4 + (n / 2 + 1), base4 + (n / 2 + 1) + (n / SAH_BIG + 2)};
-            int* cnts = B.wide_counters + 1;             // [0] next small, [1] next big
-            cudaFuncSetAttribute(k_sah_level_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)(sizeof(SahWarpBins) * (SAH_BIG_THREADS / 32)));
-            int n_small = 0, n_big = 0;
-            if (B.sah_subtrees == 2 && n > SAH_BIG) {
-                k_sah_init<<<1, 32, 0, st>>>(B, roots, 1, idx, tb[0]);
+            int* n_next = B.wide_counters + 1;
+            unsigned long long* nb_ctr = reinterpret_cast<unsigned long long*>(B.wide_counters + 2);
+            SahChunked tc[2] = {};
+            SahTaskAcc* acc = nullptr;
+            int* cleft = nullptr;
+            if (n > B.sah_big) {
+                const size_t max_t = (size_t)n / B.sah_big + 2, max_c = (size_t)n / SAH_CHUNK + max_t + 1;
+                char* p = reinterpret_cast<char*>(base4 + (n / 2 + 1));
+                auto carve = [&](size_t bytes) { char* q = p; p += (bytes + 255) & ~size_t(255); return q; };
+                for (int k = 0; k < 2; ++k) {
+                    tc[k].tasks = reinterpret_cast<int4*>(carve(max_t * sizeof(int4)));
+                    tc[k].cbase = reinterpret_cast<int*>(carve(max_t * sizeof(int)));
+                    tc[k].ctask = reinterpret_cast<int*>(carve(max_c * sizeof(int)));
+                }
+                cleft = reinterpret_cast<int*>(carve(max_c * sizeof(int)));
+                acc = reinterpret_cast<SahTaskAcc*>(carve(max_t * sizeof(SahTaskAcc)));
+            }
+            static const bool attr = [] {
+                return cudaFuncSetAttribute(k_sah_chunk_bin, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)(sizeof(SahWarpBins) * (SAH_CTHR / 32))) == cudaSuccess;
+            }();
+            if (!attr) return cudaErrorInvalidValue;
+            int n_small = 0, n_big = 0, n_chunks = 0;
+            if (B.sah_subtrees == 2 && n > B.sah_big) {
+                k_sah_chunk_seed<<<grid_for(n), 256, 0, st>>>(tc[0], idx, n, 0);
                 n_big = 1;
+                n_chunks = (n + SAH_CHUNK - 1) / SAH_CHUNK;
             } else {
                 k_sah_init<<<(h_roots * 32 + 255) / 256, 256, 0, st>>>(B, roots, h_roots, idx, tl[0]);
                 n_small = h_roots;
             }
-            int cur_t = 0;
+            int cur = 0;
             while (n_small + n_big > 0) {
-                cudaMemsetAsync(cnts, 0, 2 * sizeof(int), st);
-                if (n_big)
-                    k_sah_level_big<<<n_big, SAH_BIG_THREADS, sizeof(SahWarpBins) * (SAH_BIG_THREADS / 32), st>>>(
-                        B, tb[cur_t], tl[cur_t ^ 1], cnts, tb[cur_t ^ 1], cnts + 1, idx, tmp);
+                cudaMemsetAsync(B.wide_counters + 1, 0, 3 * sizeof(int), st);   // n_next + nb_ctr
+                const SahChunked& T = tc[cur];
+                const SahChunked& N2 = tc[cur ^ 1];
+                if (n_big) {
+                    k_sah_chunk_init<<<n_big, 256, 0, st>>>(acc, n_big);
+                    k_sah_chunk_bounds<<<n_chunks, SAH_CTHR, 0, st>>>(B, T, acc, idx);
+                    k_sah_chunk_bin<<<n_chunks, SAH_CTHR, sizeof(SahWarpBins) * (SAH_CTHR / 32), st>>>(B, T, acc, idx);
+                    k_sah_chunk_split<<<n_big, 32, 0, st>>>(B, T, acc, n_big);
+                    k_sah_chunk_count<<<n_chunks, SAH_CTHR, 0, st>>>(B, T, acc, idx, cleft);
+                    k_sah_chunk_scatter<<<n_chunks, SAH_CTHR, 0, st>>>(B, T, acc, idx, cleft, tmp);
+                    k_sah_chunk_finish<<<n_chunks, SAH_CTHR, 0, st>>>(B, T, acc, idx, tmp, tl[cur ^ 1], n_next, N2, nb_ctr);
+                }
                 if (n_small)
                     k_sah_level<<<(n_small + SAH_WARPS - 1) / SAH_WARPS, 32 * SAH_WARPS, 0, st>>>(
-                        B, tl[cur_t], n_small, tl[cur_t ^ 1], cnts, tb[cur_t ^ 1], cnts + 1, idx, tmp);
-                int h[2];
-                cudaMemcpyAsync(h, cnts, 2 * sizeof(int), cudaMemcpyDeviceToHost, st);
+                        B, tl[cur], n_small, tl[cur ^ 1], n_next, N2, nb_ctr, idx, tmp);
+                int h[3];
+                cudaMemcpyAsync(h, B.wide_counters + 1, 3 * sizeof(int), cudaMemcpyDeviceToHost, st);
                 e = cudaStreamSynchronize(st);
                 if (e != cudaSuccess) return e;
+                unsigned long long ctr;
+                memcpy(&ctr, h + 1, sizeof ctr);
                 n_small = h[0];
-                n_big = h[1];
-                cur_t ^= 1;
+                n_big = (int)(ctr >> 32);
+                n_chunks = (int)(ctr & 0xffffffffu);
+                cur ^= 1;
             }
         }
     }

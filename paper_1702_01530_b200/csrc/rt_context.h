@@ -90,6 +90,7 @@ struct rt_context {
     int leaf_max = 1;                // LBVH leaf collapse threshold (env RT_LEAF_MAX, <= 16)
     int treelet_passes = 0;          // SAH treelet restructuring passes (env RT_TREELETS; 0 after a full
                                      // SAH build: measured neutral to slightly worse, DESIGN §5 r2)
+    int sah_big = 4096;              // SAH tasks above this many items are split over many CTAs (env RT_SAH_BIG >= 2048)
     int sah_subtrees = 2;            // binned-SAH rebuild: 1 LBVH subtrees <= 16K prims, 2 the whole tree,
                                      // 0 off (env RT_SAH_SUBTREES)
     int collapse_dp = 1;             // SAH-optimal BVH4 collapse (env RT_COLLAPSE_DP=0: largest-area opening)

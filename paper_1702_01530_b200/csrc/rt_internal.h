@@ -99,6 +99,7 @@ struct BuildBuffers {
     int* count;                 // [N-1] primitives below each internal node (treelets)
     int treelet_passes;         // 0 = plain LBVH
     int sah_subtrees;           // binned SAH: 1 LBVH subtrees of <= 16384 primitives, 2 the whole tree
+    int sah_big;                // SAH tasks above this many items run on many CTAs (chunked), others on a warp
     int collapse_dp;            // BVH2 -> BVH4 by the SAH-optimal DP (else largest-area-first opening)
     float collapse_cprim;       // DP cost of a primitive test relative to a BVH4 node visit
 };

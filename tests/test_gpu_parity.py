@@ -210,6 +210,57 @@ def test_sah_subtrees_do_not_change_the_image(R, monkeypatch):
     assert ca["primary"] == cb["primary"] and ca["shadow"] == cb["shadow"]
 
 
+def _canonical_bvh4(nodes):
+    """The BVH4 as a depth-first serialisation from the root in child-slot order: every node's box
+    planes (bits, -0 as +0) and its child codes (internal children as a marker, then their own
+    nodes), so two trees compare equal iff they have the same structure, boxes and leaves whatever
+    order the collapse allocated node slots in (it hands them out with atomics)."""
+    u = nodes.view(np.uint32).copy()
+    u[(u & 0x7FFFFFFF) == 0] = 0
+    codes = nodes.view(np.int32)[:, 24:28]                # export order: lo/hi x, y, z, then codes
+    box = u[:, :24]
+    out, stack = [], [0]
+    while stack:
+        i = stack.pop()
+        out.append(box[i])
+        ch = codes[i]
+        out.append(np.where((ch >= 0) & (ch != 0x7FFFFFFF), -2, ch).astype(np.int64).astype(np.uint32))
+        stack.extend(int(c) for c in ch[::-1] if 0 <= c != 0x7FFFFFFF)
+    return np.concatenate(out)
+
+
+@pytest.mark.parametrize("name", ["C3", "C4_200k"])
+def test_chunked_sah_builds_the_same_tree(R, monkeypatch, name):
+    """The top SAH levels run as chunked multi-CTA tasks (tasks above RT_SAH_BIG items, default
+    4096: bounds, bins and left counts merged from 4096-item chunks with exact atomics).  The tree
+    must be the one the one-warp-per-task path builds from the same item lists: the same primitive
+    order and the same BVH4 (structure, boxes bit for bit up to -0 / +0, leaves; node slots are
+    allocated with atomics, so the comparison walks both trees from the root), for two chunking
+    thresholds against none (RT_SAH_BIG = 2^31 - 1)."""
+    s = scenes.scene_c3() if name == "C3" else scenes.scene_c4(nu=400, nv=250)
+    trees = {}
+    for big in ("2147483647", "2048", None):
+        if big is None:
+            monkeypatch.delenv("RT_SAH_BIG", raising=False)
+        else:
+            monkeypatch.setenv("RT_SAH_BIG", big)
+        Rb = rt.StereoRenderer(0)
+        try:
+            Rb.upload(s)
+            trees[big] = rt.rt_bvh_export(Rb.ctx)
+            info = rt.rt_scene_info(Rb.ctx)
+        finally:
+            Rb.close()
+        print(name, "RT_SAH_BIG", big, "build_us", info["build_us"], "nodes", info["bvh_nodes"])
+    ref_nodes, ref_gids = trees["2147483647"]
+    ref = _canonical_bvh4(ref_nodes)
+    for big in ("2048", None):
+        nodes, gids = trees[big]
+        np.testing.assert_array_equal(gids, ref_gids)
+        assert nodes.shape == ref_nodes.shape
+        np.testing.assert_array_equal(_canonical_bvh4(nodes), ref)
+
+
 def _kd_render(R, s, max_leaf=1, max_depth=0):
     R.upload(s)
     info = rt.rt_kdtree_build(R.ctx, max_leaf, max_depth)
