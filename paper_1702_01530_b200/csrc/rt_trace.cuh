@@ -190,7 +190,17 @@ __device__ __forceinline__ unsigned node4_hits(const float4* __restrict__ nodes,
     tn[1] = tn1;
     tn[2] = tn2;
     tn[3] = tn3;
+#if defined(RT_MASK_SIGN) && RT_MASK_SIGN
+    // hit iff tf - tn >= +0: the sign bits of two packed differences (a box whose exit is exactly
+    // t = -0 is culled; it holds no hit beyond t_min)
+    const float2 dA = __fadd2_rn(make_float2(tf0, tf1), make_float2(-tn0, -tn1));
+    const float2 dB = __fadd2_rn(make_float2(tf2, tf3), make_float2(-tn2, -tn3));
+    const uint32_t sg = (__float_as_uint(dA.x) >> 31) | ((__float_as_uint(dA.y) >> 31) << 1) |
+                        ((__float_as_uint(dB.x) >> 31) << 2) | ((__float_as_uint(dB.y) >> 31) << 3);
+    return sg ^ 15u;
+#else
     return (tn0 <= tf0 ? 1u : 0u) | (tn1 <= tf1 ? 2u : 0u) | (tn2 <= tf2 ? 4u : 0u) | (tn3 <= tf3 ? 8u : 0u);
+#endif
 }
 
 __device__ __forceinline__ void cswap(uint32_t& a, uint32_t& b) {
@@ -206,6 +216,15 @@ __device__ __forceinline__ int pick4(const int4& c, uint32_t i) {
     return (i & 2u) ? hi : lo;
 }
 
+#ifndef RT_PICK_CHAIN
+#define RT_PICK_CHAIN 0
+#endif
+// child code of the lowest set bit of m (m != 0)
+__device__ __forceinline__ int pick_lowest(const int4& c, unsigned m) {
+    if (RT_PICK_CHAIN) return (m & 1u) ? c.x : (m & 2u) ? c.y : (m & 4u) ? c.z : c.w;   // predicate chain
+    return pick4(c, __ffs(m) - 1);
+}
+
 // Nearest-hit rays: visit order of the hit children.  Entry distances are >= 0, so their bit
 // patterns order like unsigned ints; the 2 low bits carry the child slot and a 5-exchange network
 // sorts them.  The nearest continues, the others are pushed far-to-near with predicated stores
@@ -216,7 +235,7 @@ __device__ __forceinline__ bool order_push(unsigned m, const float tn[4], const 
                                            uint32_t& sp, int& node) {
     if (!m) return false;
     if (!(m & (m - 1u))) {                                  // one hit (~40 % of visits): nothing to order
-        node = pick4(ch, __ffs(m) - 1);
+        node = pick_lowest(ch, m);
         return true;
     }
     if (__popc(m) == 2) {                                   // two hits: one compare, no network
@@ -274,7 +293,7 @@ __device__ __forceinline__ bool plain_push(unsigned m, const int4& ch, const Tra
         }
         sp += (uint32_t)__popc(r) * STK_E;
     }
-    node = pick4(ch, __ffs(m) - 1);
+    node = pick_lowest(ch, m);
     return true;
 }
 __device__ __forceinline__ bool pop_mem(const TravStack& stk, uint32_t& sp, int& node) {
