@@ -1349,11 +1349,7 @@ cudaError_t rtb_build_bvh(const BuildBuffers& Bc, cudaStream_t st, int* root, in
                 cleft = reinterpret_cast<int*>(carve(max_c * sizeof(int)));
                 acc = reinterpret_cast<SahTaskAcc*>(carve(max_t * sizeof(SahTaskAcc)));
             }
-            static const bool attr = [] {
-                return cudaFuncSetAttribute(k_sah_chunk_bin, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            (int)(sizeof(SahWarpBins) * (SAH_CTHR / 32))) == cudaSuccess;
-            }();
-            if (!attr) return cudaErrorInvalidValue;
+            static_assert(sizeof(SahWarpBins) * (SAH_CTHR / 32) <= 48 * 1024, "chunk bins fit the default dynamic smem");
             int n_small = 0, n_big = 0, n_chunks = 0;
             if (B.sah_subtrees == 2 && n > B.sah_big) {
                 k_sah_chunk_seed<<<grid_for(n), 256, 0, st>>>(tc[0], idx, n, 0);
