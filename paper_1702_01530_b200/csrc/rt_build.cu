@@ -1223,7 +1223,7 @@ __device__ __forceinline__ void prim_box(int k, const int* __restrict__ prim_ori
 }
 
 // Bottom-up refit of one BVH4 level (nodes [begin, end)); deeper levels are already refit, and
-// empty slots keep their inverted boxes, which are neutral under min/max.
+// empty slots are skipped and rewritten as empty.
 __global__ void k_refit4(float4* nodes, int begin, int end, const int* __restrict__ prim_orig, int n_spheres,
                          const float4* __restrict__ spheres, const uint32_t* __restrict__ tri_idx,
                          const float* __restrict__ vtx) {
@@ -1248,6 +1248,7 @@ __global__ void k_refit4(float4* nodes, int begin, int end, const int* __restric
             } else {
                 const float4* r = nodes + NODE_F4 * (size_t)code;
                 for (int k = 0; k < BVH_W; ++k) {
+                    if (node_code(r, k) == WIDE_EMPTY) continue;
                     float3 bl, bh;
                     node_child_box(r, k, bl, bh);
                     l = f3(fminf(l.x, bl.x), fminf(l.y, bl.y), fminf(l.z, bl.z));
