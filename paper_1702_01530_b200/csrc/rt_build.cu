@@ -1349,6 +1349,9 @@ cudaError_t rtb_build_bvh(const BuildBuffers& Bc, cudaStream_t st, int* root, in
                 }
                 cleft = reinterpret_cast<int*>(carve(max_c * sizeof(int)));
                 acc = reinterpret_cast<SahTaskAcc*>(carve(max_t * sizeof(SahTaskAcc)));
+                // the whole carve must stay inside the BVH4 staging (16 * NODE_F4 * (n - 1) bytes)
+                if (p > reinterpret_cast<char*>(B.nodes4) + 16 * (size_t)NODE_F4 * (size_t)(n - 1))
+                    return cudaErrorInvalidValue;
             }
             static_assert(sizeof(SahWarpBins) * (SAH_CTHR / 32) <= 48 * 1024, "chunk bins fit the default dynamic smem");
             int n_small = 0, n_big = 0, n_chunks = 0;

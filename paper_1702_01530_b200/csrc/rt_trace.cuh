@@ -242,21 +242,19 @@ __device__ __forceinline__ bool order_push(unsigned m, const float tn[4], const 
     uint32_t k2 = (m & 4) ? ((__float_as_uint(tn[2]) & ~3u) | 2u) : 0xffffffffu;
     uint32_t k3 = (m & 8) ? ((__float_as_uint(tn[3]) & ~3u) | 3u) : 0xffffffffu;
     cswap(k0, k1); cswap(k2, k3); cswap(k0, k2); cswap(k1, k3); cswap(k1, k2);
-    const int nh = __popc(m);
-    if (nh > 1) {
-        // k3, k2, k1 -> entries sp, sp+1, sp+2 (far first; only the hit ones)
-        const uint32_t a = sp + (uint32_t)(nh - 2) * STK_E;   // entry of k1
-        if (stk.two_fit(sp + STK_E)) {
-            stk.st_if(nh > 3, sp, pick4(ch, k3 & 3u));
-            stk.st_if(nh > 2, a - STK_E, pick4(ch, k2 & 3u));
-            stk.st_if(true, a, pick4(ch, k1 & 3u));
-        } else {
-            if (nh > 3) stk.set(sp, pick4(ch, k3 & 3u));
-            if (nh > 2) stk.set(a - STK_E, pick4(ch, k2 & 3u));
-            stk.set(a, pick4(ch, k1 & 3u));
-        }
-        sp = a + STK_E;
+    // three or four hits: k3 (four only), k2, k1 -> entries sp, ..., far first
+    const bool four = m == 15u;
+    const uint32_t a = sp + (four ? 2u : 1u) * STK_E;     // entry of k1
+    if (stk.two_fit(sp + STK_E)) {
+        stk.st_if(four, sp, pick4(ch, k3 & 3u));
+        stk.st_if(true, a - STK_E, pick4(ch, k2 & 3u));
+        stk.st_if(true, a, pick4(ch, k1 & 3u));
+    } else {
+        if (four) stk.set(sp, pick4(ch, k3 & 3u));
+        stk.set(a - STK_E, pick4(ch, k2 & 3u));
+        stk.set(a, pick4(ch, k1 & 3u));
     }
+    sp = a + STK_E;
     node = pick4(ch, k0 & 3u);
     return true;
 }
