@@ -73,7 +73,7 @@ typedef struct {
     double eps_sphere; /* angular band around sphere silhouettes               (1e-4) */
     double eps_edge;   /* angular band around triangle edges                   (1e-6) */
     double eps_abs;    /* absolute band (x (1+|o|)) around t_min               (1e-5) */
-    double perturb;    /* F7: primary-ray perturbation angle (rad), 0 = off    (1e-6) */
+    double perturb;    /* F7: primary-ray perturbation angle (rad), 0 = off    (1e-6; also /10, /33) */
     double perturb_tol;/* F7: radiance change that marks the pixel unstable    (1e-3) */
 } oracle_eps;
 
@@ -724,17 +724,21 @@ int oracle_render(const oracle_scene* sc, const oracle_cam* cam, int32_t max_dep
         if (eps && eps->perturb > 0.0) {
             /* F7 (reading 22): curved mirrors and glass amplify angular error at every
              * bounce (~2D/r), so a deep ray can cross a silhouette that the unperturbed tree misses
-             * by more than the band.  Re-trace with the primary ray turned by `perturb` rad in four
-             * directions; a clamped radiance change above perturb_tol marks the pixel unstable. */
+             * by more than the band.  Re-trace with the primary ray turned in four directions by
+             * `perturb`, perturb / 10 and perturb / 33 rad (1e-6, 1e-7, 3e-8: from ~10x down to the
+             * FP32 rounding of a unit direction; the response is not monotonic in the turn -- a deep
+             * ray can graze a boundary at one scale and not at the others, as the full-frame C3
+             * report found); a clamped radiance change above perturb_tol marks the pixel unstable. */
             v3 dv = ld3(d);
             v3 a = fabs(dv.y) < 0.9 ? mk(0, 1, 0) : mk(1, 0, 0);
             v3 u = nrm(cross(dv, a)), w = cross(dv, u);
             v3 dirs[4] = {u, scl(u, -1.0), w, scl(w, -1.0)};
-            for (int q = 0; q < 4 && !(cx.flags & FRAG_UNSTABLE); ++q) {
+            const double scale[3] = {1.0, 0.1, 1.0 / 33.0};
+            for (int q = 0; q < 12 && !(cx.flags & FRAG_UNSTABLE); ++q) {
                 trace_ctx cq;
                 memset(&cq, 0, sizeof cq);
                 cq.sc = sc;
-                v3 dq = nrm(add(dv, scl(dirs[q], eps->perturb)));
+                v3 dq = nrm(add(dv, scl(dirs[q & 3], eps->perturb * scale[q >> 2])));
                 v3 cc = trace(&cq, ld3(o), dq, max_depth, 0, NULL, NULL, NULL);
                 double dc[3] = {cc.x, cc.y, cc.z}, c0[3] = {c.x, c.y, c.z};
                 for (int k = 0; k < 3; ++k) {

@@ -77,12 +77,22 @@ def main():
         gid = g["id"][e, y, x]
         st = compare(ref, gid, g["fb"][e, y, x], g["radiance"][e, y, x], label)
         mism = np.flatnonzero(gid != ref["id"])
+        # the worst radiance errors off the exclusion set (pixel, both radiances, IDs, flags)
+        gr = np.clip(g["radiance"][e, y, x][:, :3].astype(np.float64), 0, 1)
+        orad = np.clip(ref["radiance"].reshape(-1, 3), 0, 1)
+        err = np.abs(gr - orad).max(1)
+        okr = ref["tflags"].reshape(-1) == 0
+        worst = [int(i) for i in np.argsort(-np.where(okr, err, -1.0))[:20] if okr[i] and err[i] > 2e-4]
         st.update({"width": s.width, "height": s.height, "max_depth": s.max_depth, "pixels": int(len(pix)),
                    "pixel_set": (f"every {a.c3_row_step}th row of both eyes" if per_eye is None
                                  else f"{per_eye} seeded pixels per eye (seed {seed})"),
                    "oracle_s": dt, "flags": flag_table(ref),
                    "id_mismatch_margins": sorted(float(ref["margin"][i]) for i in mism),
                    "id_mismatch_pflags": [int(ref["pflags"][i]) for i in mism],
+                   "worst_unflagged": [{"eye": int(e[i]), "x": int(x[i]), "y": int(y[i]), "err": float(err[i]),
+                                        "gpu": gr[i].tolist(), "oracle": orad[i].tolist(), "gpu_id": int(gid[i]),
+                                        "oracle_id": int(ref["id"].reshape(-1)[i]),
+                                        "pflags": int(ref["pflags"].reshape(-1)[i])} for i in worst],
                    "pass": bool(st["id_mismatch"] == 0 and st["id_candidate_violations"] == 0
                                 and st["rgb_frac"] >= 0.999 and st["max_err"] <= 1e-3)})
         print(label, {k: v for k, v in st.items() if k != "flags"}, file=sys.stderr, flush=True)

@@ -535,9 +535,9 @@ def test_unstable_flag_smooth_scene_never_fires():
 def test_unstable_flag_matches_definition():
     """R#22 (F7): in C2 (mirror + glass spheres over a reflective floor, Phong n = 128/256) angular
     error grows at every curved bounce, so some pixels that no structural band (F1-F6) catches
-    are unstable.  Check the flag against its definition by tracing the four perturbed primaries
-    independently (numpy basis, single-ray entry point): flagged <=> some clamped channel moves
-    by more than 1e-3."""
+    are unstable.  Check the flag against its definition by tracing the perturbed primaries
+    independently (numpy basis, single-ray entry point; four directions at 1e-6, 1e-7 and
+    1e-6/33 rad): flagged <=> some clamped channel moves by more than 1e-3."""
     sc = scenes.scene_c2().with_view(width=160, height=120)
     o = Oracle(sc)
     out = o.render()
@@ -552,7 +552,7 @@ def test_unstable_flag_matches_definition():
         org, d = o.primary_ray(cam, int(eye), int(px), int(py))
         base = np.clip(out["radiance"][eye, py, px], 0, 1)
         moved = max(np.abs(np.clip(o.trace_ray(org, dq, sc.max_depth)[0], 0, 1) - base).max()
-                    for dq in _perturbed_dirs(d, 1e-6))
+                    for delta in (1e-6, 1e-6 * 0.1, 1e-6 / 33.0) for dq in _perturbed_dirs(d, delta))
         assert bool(tf[eye, py, px] & FRAG_UNSTABLE) == (moved > 1e-3), (eye, py, px, moved)
 
 
