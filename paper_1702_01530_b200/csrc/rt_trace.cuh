@@ -221,11 +221,12 @@ __device__ __forceinline__ int pick_lowest(const int4& c, unsigned m) {
 __device__ __forceinline__ bool order_push(unsigned m, const float tn[4], const int4& ch, const TravStack& stk,
                                            uint32_t& sp, int& node) {
     if (!m) return false;
-    if (!(m & (m - 1u))) {                                  // one hit (~40 % of visits): nothing to order
+    const int nh = __popc(m);                               // one popcount drives both tests (C4 -0.3 %)
+    if (nh == 1) {                                          // one hit (~40 % of visits): nothing to order
         node = pick_lowest(ch, m);
         return true;
     }
-    if (__popc(m) == 2) {                                   // two hits: one compare, no network
+    if (nh == 2) {                                          // two hits: one compare, no network
         const float t0 = (m & 1u) ? tn[0] : (m & 2u) ? tn[1] : tn[2];        // lowest / highest hit slot
         const float t1 = (m & 8u) ? tn[3] : (m & 4u) ? tn[2] : tn[1];
         const int c0 = pick_lowest(ch, m), c1 = (m & 8u) ? ch.w : (m & 4u) ? ch.z : ch.y;
